@@ -1,0 +1,245 @@
+/*
+ * dynsparse_b200.h -- C ABI of the B200-native dynsparse hot path.
+ *
+ * One shared library (libdynsparse_b200.so, sm_100a) exports these symbols.
+ * Every entry point takes plain device pointers + sizes and a CUDA stream
+ * (cudaStream_t passed as void*; NULL = legacy default stream), enqueues
+ * stream-ordered work and returns an int status (DS_OK = 0).  No torch types
+ * cross the boundary.  Buffers are owned by the caller; the library borrows
+ * them for the duration of the stream-ordered call.  Internal temporaries use
+ * the stream-ordered allocator (cudaMallocAsync) and are released on the same
+ * stream.
+ *
+ * Index arrays are int32 on the device (the reference stores int64,
+ * formats.py:82-83; the host layer narrows on upload after checking every
+ * dimension is < 2^31 and widens on download).  Values are IEEE float64.
+ *
+ * Each block cites the reference interface it replaces (file:line relative
+ * to the reference's pkg/src/dynsparse/).  Status codes map 1:1 onto the
+ * reference's exception classes (errors.py).
+ */
+#ifndef DYNSPARSE_B200_H
+#define DYNSPARSE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DS_ABI_VERSION 1
+
+/* ---- status codes (errors.py) ------------------------------------------ */
+enum {
+  DS_OK = 0,
+  DS_ERR_INVALID_ARGUMENT = 1,          /* ValueError / DimensionMismatch (host-checked) */
+  DS_ERR_CUDA = 2,                      /* DeviceError (new): a CUDA runtime failure     */
+  DS_ERR_DIA_FILL_OVERFLOW = 3,         /* DiaFillOverflow        errors.py:52-53        */
+  DS_ERR_STRUCTURALLY_ABSENT_DIAG = 4,  /* StructurallyAbsentDiagonal errors.py:73-78    */
+  DS_ERR_BREAKDOWN = 5,                 /* BreakdownZeroCurvature errors.py:81-82        */
+  DS_ERR_NOT_SUPPORTED = 6              /* dims >= 2^31 or a layout the kernels refuse   */
+};
+
+/* Message of the last failing call on this host thread ("" if none). */
+const char* ds_last_error(void);
+int ds_abi_version(void);
+/* SM count of the current device (grid sizing is a multiple of it). */
+int ds_device_sm_count(int* out);
+
+/* ---- SpMV: replaces kernels._SPMV_KERNELS (kernels.py:166-170) behind
+ *      spmv (kernels.py:173-186, accumulate=0: y = A x) and
+ *      spmv_add (kernels.py:189-198, accumulate=1: y = y + (A x)).
+ * Rounding contract (bitwise equal to the reference on the same inputs):
+ *   CSR: y[i] = p[first] + pairwise8(p[first+1:end])   (np.add.reduceat)
+ *   DIA: y[i] = ((0 + p_0) + p_1) + ...  over in-range diagonals ascending
+ *   COO (rows nondecreasing): sequential per row in stored order from 0.0 (np.bincount)
+ *   COO (unsorted): atomics, within 1e-13 relative (as the reference's threaded COO)
+ * with every product rounded before the add (no FMA).                       */
+
+/* Rows longer than 129 entries need the pairwise recursion; ds_csr_analyze
+ * lists them so ds_spmv_csr can hand them to a CTA-per-row kernel.
+ * long_rows must hold nrows int32; *n_long is written (host, synchronises). */
+int ds_csr_analyze(int64_t nrows, const int32_t* row_offsets, int32_t* long_rows,
+                   int64_t* n_long, int32_t* max_row_len, void* stream);
+
+/* long_rows may be NULL (then every row is handled in-line, correct but slow
+ * for rows > 129).  n_long is the count from ds_csr_analyze.                */
+int ds_spmv_csr(int64_t nrows, int64_t ncols, int64_t nnz, const int32_t* row_offsets,
+                const int32_t* col_indices, const double* values,
+                const int32_t* long_rows, int64_t n_long,
+                const double* x, double* y, int accumulate, void* stream);
+
+/* values: row-major (nrows, ndiags), entry (i, i+offsets[j]) at values[i*ndiags+j]
+ * (formats.py:217-258); offsets strictly increasing, on the device.         */
+int ds_spmv_dia(int64_t nrows, int64_t ncols, int32_t ndiags, const int32_t* offsets,
+                const double* values, const double* x, double* y, int accumulate,
+                void* stream);
+
+/* rows_sorted != 0 promises row indices are nondecreasing (canonical COO). */
+int ds_spmv_coo(int64_t nrows, int64_t ncols, int64_t nnz, const int32_t* row_indices,
+                const int32_t* col_indices, const double* values, int rows_sorted,
+                const double* x, double* y, int accumulate, void* stream);
+
+/* flags bit0: rows nondecreasing; bit1: (row, col) strictly increasing
+ * (already canonical).  Written to host memory (synchronises).              */
+int ds_coo_order_flags(int64_t nnz, const int32_t* row_indices, const int32_t* col_indices,
+                       int32_t* flags, void* stream);
+
+/* ---- dense-vector kernels (kernels.py:205-235) -------------------------- */
+/* Deterministic two-level tree reduction (fixed for a given n); result to
+ * device memory.  workspace: ds_dot_workspace_bytes() bytes of device memory
+ * (zeroed once before first use; the kernel leaves it re-usable).           */
+int64_t ds_dot_workspace_bytes(void);
+int ds_dot(int64_t n, const double* x, const double* y, double* result_dev,
+           void* workspace, void* stream);
+/* w = alpha*x + beta*y, products rounded separately (no FMA); w may alias x or y. */
+int ds_waxpby(int64_t n, double alpha, const double* x, double beta, const double* y,
+              double* w, void* stream);
+/* Exact sequential prefix sums (np.cumsum order); out may be NULL for reduce. */
+int ds_scan(int64_t n, const double* x, double* out, double* total_dev, void* stream);
+
+/* ---- diagonal extract / update (kernels.py:242-337) --------------------- */
+/* out[i] = A(i,i) for i < min(nrows,ncols); absent -> 0.0.  COO duplicates are
+ * summed in stored order (np.bincount).                                      */
+int ds_extract_diag_csr(int64_t nrows, int64_t ncols, const int32_t* row_offsets,
+                        const int32_t* col_indices, const double* values, double* out,
+                        void* stream);
+int ds_extract_diag_coo(int64_t nrows, int64_t ncols, int64_t nnz, const int32_t* rows,
+                        const int32_t* cols, const double* values, double* out, void* stream);
+/* Overwrite A(i,i) = d[i].  Returns DS_ERR_STRUCTURALLY_ABSENT_DIAG with
+ * *first_missing set when some (i,i) is not stored (checked before writing).
+ * COO duplicates: first stored occurrence takes d[i], later ones 0.0.        */
+int ds_update_diag_csr(int64_t nrows, int64_t ncols, const int32_t* row_offsets,
+                       const int32_t* col_indices, double* values, const double* d,
+                       int64_t* first_missing, void* stream);
+int ds_update_diag_coo(int64_t nrows, int64_t ncols, int64_t nnz, const int32_t* rows,
+                       const int32_t* cols, double* values, const double* d,
+                       int64_t* first_missing, void* stream);
+/* DIA nnz = nonzero in-range slots (formats.py:239-255); written to host.    */
+int ds_dia_count_nonzero(int64_t nrows, int64_t ncols, int32_t ndiags, const int32_t* offsets,
+                         const double* values, int64_t* count, void* stream);
+
+/* ---- conversion via the canonical COO proxy (datamove.py:208-295) -------
+ * Two phases so the caller allocates outputs:  begin_* builds the canonical
+ * COO (stable (row,col) sort + duplicate sums in reduceat order) on the
+ * device, sizes the target and -- for DIA -- applies the fill-limit test
+ * BEFORE any target allocation (datamove.py:246-252): it returns
+ * DS_ERR_DIA_FILL_OVERFLOW with *out_ndiags set.  finish_* writes the target
+ * arrays and frees the job; abort frees it without writing.                */
+typedef struct ds_convert_job ds_convert_job;
+enum { DS_FMT_COO = 0, DS_FMT_CSR = 1, DS_FMT_DIA = 2 };   /* FormatId, formats.py:33-42 */
+
+int ds_convert_begin_coo(int64_t nrows, int64_t ncols, int64_t nnz, const int32_t* rows,
+                         const int32_t* cols, const double* values, int target,
+                         int64_t fill_limit, void* stream, ds_convert_job** job,
+                         int64_t* out_nnz, int64_t* out_ndiags);
+int ds_convert_begin_csr(int64_t nrows, int64_t ncols, int64_t nnz, const int32_t* row_offsets,
+                         const int32_t* cols, const double* values, int target,
+                         int64_t fill_limit, void* stream, ds_convert_job** job,
+                         int64_t* out_nnz, int64_t* out_ndiags);
+int ds_convert_begin_dia(int64_t nrows, int64_t ncols, int32_t ndiags, const int32_t* offsets,
+                         const double* values, int target, int64_t fill_limit, void* stream,
+                         ds_convert_job** job, int64_t* out_nnz, int64_t* out_ndiags);
+int ds_convert_finish_coo(ds_convert_job* job, int32_t* rows, int32_t* cols, double* values);
+int ds_convert_finish_csr(ds_convert_job* job, int32_t* row_offsets, int32_t* cols,
+                          double* values);
+int ds_convert_finish_dia(ds_convert_job* job, int32_t* offsets, double* values);
+void ds_convert_abort(ds_convert_job* job);
+
+/* ---- halo exchange pieces (stencil.py:280-319) ---------------------------
+ * dst[k] = src[idx[k]]: packs a neighbour's send list, or -- single process,
+ * all partitions visible (peer access enabled) -- writes the ghost slice
+ * x_k[n+start : n+start+count] straight from x_q (stencil.py:293-295).      */
+int ds_gather(int64_t count, const int32_t* idx, const double* src, double* dst, void* stream);
+
+/* ---- format-dispatched entry (kernels.py:166-198) -----------------------
+ * One descriptor for whichever format is active, so a DynamicMatrix costs
+ * one switch in C like the reference's one dict lookup (kernels.py:186).  */
+typedef struct ds_matrix {
+  int32_t format;            /* DS_FMT_COO / DS_FMT_CSR / DS_FMT_DIA            */
+  int32_t ndiags;            /* DIA                                             */
+  int64_t nrows, ncols, nnz; /* nnz: stored entries (COO/CSR)                   */
+  const int32_t* idx0;       /* COO row_indices | CSR row_offsets | DIA offsets */
+  const int32_t* idx1;       /* COO/CSR col_indices                             */
+  const double* values;      /* COO/CSR values | DIA (nrows, ndiags) row-major  */
+  const int32_t* long_rows;  /* CSR: rows > 129 entries (ds_csr_analyze), or NULL */
+  int64_t n_long;
+  int32_t rows_sorted;       /* COO: row indices nondecreasing                  */
+  int32_t pad;
+} ds_matrix;
+
+int ds_spmv(const ds_matrix* a, const double* x, double* y, int accumulate, void* stream);
+
+/* ---- conjugate gradient building blocks (solver.py:56-189) --------------
+ * The CG scalars live on the device in a ds_cg_scalars block.  Every kernel
+ * below first tests s->done and returns when set, so a chunk of iterations
+ * (or a captured CUDA graph of them) can be enqueued without host round
+ * trips and the iteration count / residual history stay exact.
+ *
+ * Global dots: each partition writes its local dot to parts[k]; the global
+ * value is the rank-ordered sum parts[0] + parts[1] + ... (the reference's
+ * Python sum, solver.py:140-141).  With nparts_final > 0 the kernel that
+ * completes parts[k] also runs the CG stage on parts[0..nparts_final) (the
+ * single-partition fast path); otherwise the caller gathers every
+ * partition's part (same device, or NCCL all-gather across ranks) and calls
+ * ds_cg_finalize.                                                           */
+typedef struct ds_cg_scalars {
+  double rr;        /* r.r of the current residual                          */
+  double pap;       /* p.Ap of the current iteration                        */
+  double alpha, beta;
+  double scale;     /* ||b||, or 1.0 when ||b|| == 0   (solver.py:98-99)    */
+  double tol;
+  double bb;
+  double rr_new;
+  int32_t iter;     /* iterations completed                                 */
+  int32_t max_iters;
+  int32_t done;     /* 0 running, 1 converged, 2 breakdown (p.Ap <= 0), 3 max_iters */
+  int32_t pad;
+} ds_cg_scalars;
+
+enum { DS_CG_STAGE_NONE = 0, DS_CG_STAGE_PAP = 1, DS_CG_STAGE_RR = 2, DS_CG_STAGE_SETUP = 3 };
+
+/* Device workspace for one stream: fused-reduction partials and tickets.
+ * Must be zero-filled once before first use.                               */
+int64_t ds_cg_workspace_bytes(void);
+
+/* y = A x (accumulate: y += A x); if dot_with != NULL also
+ * *dot_out = dot_with[0:nrows] . y  (fused into the SpMV epilogue when the
+ * kernel supports it), then the CG stage when nparts_final > 0.  s may be
+ * NULL (no guard).                                                          */
+int ds_cg_spmv_dot(const ds_matrix* a, const double* x, double* y, int accumulate,
+                   const double* dot_with, double* dot_out, int stage, ds_cg_scalars* s,
+                   double* history, const double* parts, int nparts_final, void* workspace,
+                   void* stream);
+/* r = 1*b + (-1)*ap; p = 1*r + 0*r (solver.py:89,101 / 155-167);
+ * bb_out = b.b, rr_out = r.r (partition-local).                            */
+int ds_cg_setup_residual(int64_t n, const double* b, const double* ap, double* r, double* p,
+                         double* bb_out, double* rr_out, void* workspace, void* stream);
+/* s <- tol/max_iters, scale from sum(bb_parts), rr from sum(rr_parts),
+ * history[0], done (0 or 1 converged at x0, 3 when max_iters <= 0).        */
+int ds_cg_setup_finalize(ds_cg_scalars* s, const double* bb_parts, const double* rr_parts,
+                         int nparts, double tol, int32_t max_iters, double* history,
+                         void* stream);
+/* x = 1*x + alpha*p; r = 1*r + (-alpha)*ap; *rr_out = r.r, then stage RR
+ * when nparts_final > 0 (solver.py:177-184).                               */
+int ds_cg_update(int64_t n, double* x, double* r, const double* p, const double* ap,
+                 ds_cg_scalars* s, double* rr_out, double* history, const double* parts,
+                 int nparts_final, void* workspace, void* stream);
+/* p = 1*r + beta*p  (solver.py:185-188) */
+int ds_cg_direction(int64_t n, const double* r, double* p, const ds_cg_scalars* s, void* stream);
+/* Stage PAP or RR over parts[0..nparts) (after an all-gather).             */
+int ds_cg_finalize(int stage, ds_cg_scalars* s, double* history, const double* parts,
+                   int nparts, void* stream);
+/* halo gather guarded by s->done (dst[k] = src[idx[k]])                    */
+int ds_cg_gather(int64_t count, const int32_t* idx, const double* src, double* dst,
+                 const ds_cg_scalars* s, void* stream);
+
+/* ---- DIA diagonal column helpers (kernels.py:258-262, 325-330) --------- */
+/* direction 0: out[i] = values[i*ndiags + j0] (i < n); 1: values[...] = d[i] */
+int ds_dia_diag_column(int64_t n, int32_t ndiags, int32_t j0, double* values, double* vec,
+                       int direction, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DYNSPARSE_B200_H */

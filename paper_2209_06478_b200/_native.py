@@ -1,0 +1,157 @@
+"""ctypes binding of the C ABI in include/dynsparse_b200.h.
+
+The shared library is built in-tree by ``__graft_entry__.build()`` (or
+``make -C paper_2209_06478_b200/csrc``) into ``paper_2209_06478_b200/_lib``.
+There is deliberately no fallback: every compute entry point raises
+``DeviceError`` when the library or a CUDA device is missing.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from .errors import (
+    BreakdownZeroCurvature,
+    DeviceError,
+    DiaFillOverflow,
+    StructurallyAbsentDiagonal,
+)
+
+LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib")
+LIB_PATH = os.path.join(LIB_DIR, "libdynsparse_b200.so")
+
+DS_OK = 0
+DS_ERR_INVALID_ARGUMENT = 1
+DS_ERR_CUDA = 2
+DS_ERR_DIA_FILL_OVERFLOW = 3
+DS_ERR_STRUCTURALLY_ABSENT_DIAG = 4
+DS_ERR_BREAKDOWN = 5
+DS_ERR_NOT_SUPPORTED = 6
+
+DS_CG_STAGE_NONE, DS_CG_STAGE_PAP, DS_CG_STAGE_RR, DS_CG_STAGE_SETUP = 0, 1, 2, 3
+
+c_i32, c_i64, c_dbl, c_vp, c_int = (ctypes.c_int32, ctypes.c_int64, ctypes.c_double,
+                                    ctypes.c_void_p, ctypes.c_int)
+P_i64 = ctypes.POINTER(ctypes.c_int64)
+P_i32 = ctypes.POINTER(ctypes.c_int32)
+
+
+class DsMatrix(ctypes.Structure):
+    """Mirror of ``ds_matrix``."""
+
+    _fields_ = [
+        ("format", c_i32), ("ndiags", c_i32),
+        ("nrows", c_i64), ("ncols", c_i64), ("nnz", c_i64),
+        ("idx0", c_vp), ("idx1", c_vp), ("values", c_vp), ("long_rows", c_vp),
+        ("n_long", c_i64), ("rows_sorted", c_i32), ("pad", c_i32),
+    ]
+
+
+class DsCgScalars(ctypes.Structure):
+    """Mirror of ``ds_cg_scalars`` (lives on the device; 80 bytes)."""
+
+    _fields_ = [
+        ("rr", c_dbl), ("pap", c_dbl), ("alpha", c_dbl), ("beta", c_dbl),
+        ("scale", c_dbl), ("tol", c_dbl), ("bb", c_dbl), ("rr_new", c_dbl),
+        ("iter", c_i32), ("max_iters", c_i32), ("done", c_i32), ("pad", c_i32),
+    ]
+
+
+CG_SCALARS_BYTES = ctypes.sizeof(DsCgScalars)
+P_mat = ctypes.POINTER(DsMatrix)
+
+# name -> (restype, argtypes)
+_SIGNATURES = {
+    "ds_last_error": (ctypes.c_char_p, []),
+    "ds_abi_version": (c_int, []),
+    "ds_device_sm_count": (c_int, [P_i32]),
+    "ds_csr_analyze": (c_int, [c_i64, c_vp, c_vp, P_i64, P_i32, c_vp]),
+    "ds_spmv_csr": (c_int, [c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp,
+                            c_int, c_vp]),
+    "ds_spmv_dia": (c_int, [c_i64, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_int, c_vp]),
+    "ds_spmv_coo": (c_int, [c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_int, c_vp, c_vp, c_int,
+                            c_vp]),
+    "ds_coo_order_flags": (c_int, [c_i64, c_vp, c_vp, P_i32, c_vp]),
+    "ds_dot_workspace_bytes": (c_i64, []),
+    "ds_dot": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "ds_waxpby": (c_int, [c_i64, c_dbl, c_vp, c_dbl, c_vp, c_vp, c_vp]),
+    "ds_scan": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "ds_extract_diag_csr": (c_int, [c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "ds_extract_diag_coo": (c_int, [c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "ds_update_diag_csr": (c_int, [c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, P_i64, c_vp]),
+    "ds_update_diag_coo": (c_int, [c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, P_i64, c_vp]),
+    "ds_dia_count_nonzero": (c_int, [c_i64, c_i64, c_i32, c_vp, c_vp, P_i64, c_vp]),
+    "ds_dia_diag_column": (c_int, [c_i64, c_i32, c_i32, c_vp, c_vp, c_int, c_vp]),
+    "ds_convert_begin_coo": (c_int, [c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_int, c_i64, c_vp,
+                                     ctypes.POINTER(c_vp), P_i64, P_i64]),
+    "ds_convert_begin_csr": (c_int, [c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_int, c_i64, c_vp,
+                                     ctypes.POINTER(c_vp), P_i64, P_i64]),
+    "ds_convert_begin_dia": (c_int, [c_i64, c_i64, c_i32, c_vp, c_vp, c_int, c_i64, c_vp,
+                                     ctypes.POINTER(c_vp), P_i64, P_i64]),
+    "ds_convert_finish_coo": (c_int, [c_vp, c_vp, c_vp, c_vp]),
+    "ds_convert_finish_csr": (c_int, [c_vp, c_vp, c_vp, c_vp]),
+    "ds_convert_finish_dia": (c_int, [c_vp, c_vp, c_vp]),
+    "ds_convert_abort": (None, [c_vp]),
+    "ds_gather": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "ds_spmv": (c_int, [P_mat, c_vp, c_vp, c_int, c_vp]),
+    "ds_cg_workspace_bytes": (c_i64, []),
+    "ds_cg_spmv_dot": (c_int, [P_mat, c_vp, c_vp, c_int, c_vp, c_vp, c_int, c_vp, c_vp, c_vp,
+                               c_int, c_vp, c_vp]),
+    "ds_cg_setup_residual": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "ds_cg_setup_finalize": (c_int, [c_vp, c_vp, c_vp, c_int, c_dbl, c_i32, c_vp, c_vp]),
+    "ds_cg_update": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_vp,
+                             c_vp]),
+    "ds_cg_direction": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "ds_cg_finalize": (c_int, [c_int, c_vp, c_vp, c_vp, c_int, c_vp]),
+    "ds_cg_gather": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
+}
+
+EXPORTED_SYMBOLS = tuple(_SIGNATURES)
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load():
+    """Load (once) and return the ctypes handle; raise DeviceError if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise DeviceError(
+                    f"native extension missing at {LIB_PATH}; build it with "
+                    "`python -c 'import __graft_entry__ as g; g.build()'`")
+            lib = ctypes.CDLL(LIB_PATH)
+            for name, (res, args) in _SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    return _lib
+
+
+def last_error() -> str:
+    msg = load().ds_last_error()
+    return msg.decode(errors="replace") if msg else ""
+
+
+def check(status: int, *, index: int | None = None) -> None:
+    """Map a C status code onto the reference's exception classes."""
+    if status == DS_OK:
+        return
+    msg = last_error()
+    if status == DS_ERR_DIA_FILL_OVERFLOW:
+        raise DiaFillOverflow(msg)
+    if status == DS_ERR_STRUCTURALLY_ABSENT_DIAG:
+        raise StructurallyAbsentDiagonal(int(index if index is not None else 0))
+    if status == DS_ERR_BREAKDOWN:
+        raise BreakdownZeroCurvature(msg)
+    raise DeviceError(f"dynsparse native error {status}: {msg}")
+
+
+def call(name: str, *args, **kw) -> None:
+    check(getattr(load(), name)(*args), **kw)

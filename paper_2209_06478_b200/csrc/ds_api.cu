@@ -1,0 +1,46 @@
+// ds_api.cu -- error state and device queries of the C ABI.
+#include <stdarg.h>
+#include <string.h>
+
+#include <mutex>
+
+#include "ds_common.cuh"
+
+namespace ds {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  set_error("CUDA error %d (%s) in %s", (int)e, cudaGetErrorString(e), what);
+  return DS_ERR_CUDA;
+}
+
+int sm_count() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (dev < 0 || dev >= 64) return 148;
+  if (cache[dev] == 0) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
+      v = 148;
+    cache[dev] = v;
+  }
+  return cache[dev];
+}
+
+}  // namespace ds
+
+extern "C" const char* ds_last_error(void) { return ds::g_err; }
+extern "C" int ds_abi_version(void) { return DS_ABI_VERSION; }
+extern "C" int ds_device_sm_count(int* out) {
+  *out = ds::sm_count();
+  return DS_OK;
+}

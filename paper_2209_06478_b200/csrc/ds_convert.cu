@@ -1,0 +1,565 @@
+// ds_convert.cu -- on-device format conversion through the canonical COO
+// proxy (datamove.py:208-295, formats.py:439-479).  Bit-exact with the
+// reference:
+//   entries:    CSR rows = repeat(arange(n), diff(offsets)); DIA = in-range
+//               NONZERO slots (explicit 0.0 / -0.0 dropped, formats.py:463-465)
+//   canonical:  stable lexsort((cols, rows)) then duplicate runs summed as
+//               np.add.reduceat: first + pairwise(rest) (datamove.py:208-220)
+//   COO->CSR:   histogram + scan of row ids (datamove.py:238-243)
+//   COO->DIA:   distinct (col - row) ascending; DiaFillOverflow iff
+//               ndiags * nrows > fill_limit, tested BEFORE the target is
+//               allocated (datamove.py:246-258); scatter.
+// Shortcuts that keep the bits: a COO/CSR source that is already strictly
+// (row, col)-increasing skips the sort (a stable sort of sorted unique keys is
+// the identity); a DIA source yields canonical order directly (row-major walk
+// of the slab, columns ascending because offsets ascend).
+//
+// Integer scans and histograms are hand-written (3-phase block scan).  The
+// general-case stable sort uses CUB's LSD radix sort (DeviceRadixSort::
+// SortPairs on (row*ncols+col, index) keys limited to the needed bits) -- a
+// documented stop-gap until a hand-written onesweep lands.
+#include <cub/device/device_radix_sort.cuh>
+
+#include "ds_common.cuh"
+#include "ds_kernels.cuh"
+
+struct ds_convert_job {
+  cudaStream_t st = nullptr;
+  int target = 0;
+  int64_t nrows = 0, ncols = 0;
+  int64_t nnz = 0;             // canonical entries
+  int* r = nullptr;            // canonical COO (device)
+  int* c = nullptr;
+  double* v = nullptr;
+  bool own_r = false, own_c = false, own_v = false;
+  int64_t ndiags = 0;          // DIA target
+  int* diag_map = nullptr;     // exclusive scan of diagonal presence (nrows+ncols-1)
+  int* dia_off = nullptr;      // (ndiags)
+};
+
+namespace ds {
+
+constexpr int kScanBlock = 256;
+constexpr int kScanPer = 8;
+constexpr int kScanTile = kScanBlock * kScanPer;
+
+// ---------------------------------------------------------------- scans ----
+// Exclusive scan of f(k), k in [0, n), into out[0..n) (out may be null) and
+// *total.  f returns small non-negative ints; the sum must fit in int32.
+template <class F>
+__global__ void __launch_bounds__(kScanBlock) scan_reduce_tiles(int64_t n, F f, int* tile_sums) {
+  __shared__ int sh[kScanBlock / 32];
+  const int64_t base = (int64_t)blockIdx.x * kScanTile;
+  int s = 0;
+#pragma unroll
+  for (int q = 0; q < kScanPer; ++q) {
+    const int64_t k = base + (int64_t)q * kScanBlock + threadIdx.x;
+    if (k < n) s += f(k);
+  }
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int w = 0; w < kScanBlock / 32; ++w) t += sh[w];
+    tile_sums[blockIdx.x] = t;
+  }
+}
+
+// single block: exclusive scan of tile sums in place, total to *total
+__global__ void __launch_bounds__(1024) scan_tile_sums(int64_t ntiles, int* sums, int* total) {
+  __shared__ int sh[32];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t b0 = 0; b0 < ntiles; b0 += 1024) {
+    const int64_t k = b0 + threadIdx.x;
+    const int v = (k < ntiles) ? sums[k] : 0;
+    int incl = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if ((threadIdx.x & 31) >= o) incl += t;
+    }
+    if ((threadIdx.x & 31) == 31) sh[threadIdx.x >> 5] = incl;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      int w = sh[threadIdx.x];
+      int wi = w;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, wi, o);
+        if (threadIdx.x >= o) wi += t;
+      }
+      sh[threadIdx.x] = wi - w;  // exclusive warp prefix
+    }
+    __syncthreads();
+    const int excl = carry + sh[threadIdx.x >> 5] + incl - v;
+    if (k < ntiles) sums[k] = excl;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = excl + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *total = carry;
+}
+
+template <class F>
+__global__ void __launch_bounds__(kScanBlock)
+    scan_downsweep(int64_t n, F f, const int* tile_offsets, int* out) {
+  __shared__ int sh[kScanBlock / 32];
+  const int64_t base = (int64_t)blockIdx.x * kScanTile;
+  // each thread owns kScanPer consecutive elements for the in-tile order
+  const int64_t k0 = base + (int64_t)threadIdx.x * kScanPer;
+  int v[kScanPer];
+  int s = 0;
+#pragma unroll
+  for (int q = 0; q < kScanPer; ++q) {
+    v[q] = (k0 + q < n) ? f(k0 + q) : 0;
+    s += v[q];
+  }
+  int incl = s;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if ((threadIdx.x & 31) >= o) incl += t;
+  }
+  if ((threadIdx.x & 31) == 31) sh[threadIdx.x >> 5] = incl;
+  __syncthreads();
+  int wpre = 0;
+  for (int w = 0; w < (int)(threadIdx.x >> 5); ++w) wpre += sh[w];
+  int run = tile_offsets[blockIdx.x] + wpre + incl - s;
+#pragma unroll
+  for (int q = 0; q < kScanPer; ++q) {
+    if (k0 + q < n) out[k0 + q] = run;
+    run += v[q];
+  }
+}
+
+// Returns total on the host (synchronises).  out may be null.
+template <class F>
+static int exclusive_scan(int64_t n, F f, int* out, int64_t* total_host, cudaStream_t st) {
+  const int64_t ntiles = n > 0 ? ceil_div(n, kScanTile) : 0;
+  int* sums = nullptr;
+  DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&sums), (ntiles + 1) * sizeof(int), st));
+  int* dtotal = sums + ntiles;
+  if (ntiles > 0) {
+    scan_reduce_tiles<<<(unsigned)ntiles, kScanBlock, 0, st>>>(n, f, sums);
+    scan_tile_sums<<<1, 1024, 0, st>>>(ntiles, sums, dtotal);
+    if (out) scan_downsweep<<<(unsigned)ntiles, kScanBlock, 0, st>>>(n, f, sums, out);
+    DS_LAUNCH_CHECK("exclusive_scan");
+  } else {
+    DS_CUDA(cudaMemsetAsync(dtotal, 0, sizeof(int), st));
+  }
+  int h = 0;
+  DS_CUDA(cudaMemcpyAsync(&h, dtotal, sizeof(int), cudaMemcpyDeviceToHost, st));
+  DS_CUDA(cudaFreeAsync(sums, st));
+  DS_CUDA(cudaStreamSynchronize(st));
+  *total_host = h;
+  return DS_OK;
+}
+
+// --------------------------------------------------------- entry arrays ----
+__global__ void csr_expand_rows(int nrows, const int* __restrict__ off, int* rows) {
+  // 8 lanes per row write its row id over its slice
+  const int lane8 = threadIdx.x & 7;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 3; r < nrows;
+       r += (gridDim.x * blockDim.x) >> 3)
+    for (int k = off[r] + lane8; k < off[r + 1]; k += 8) rows[k] = r;
+}
+
+struct OrderBad {  // 1 where (row, col) is not strictly greater than its predecessor
+  const int* r;
+  const int* c;
+  __device__ int operator()(int64_t k) const {
+    if (k == 0) return 0;
+    return (r[k] < r[k - 1] || (r[k] == r[k - 1] && c[k] <= c[k - 1])) ? 1 : 0;
+  }
+};
+
+__global__ void make_keys(int64_t nnz, int64_t ncols, const int* __restrict__ r,
+                          const int* __restrict__ c, unsigned long long* keys, int* idx) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    keys[k] = (unsigned long long)r[k] * (unsigned long long)ncols + (unsigned long long)c[k];
+    idx[k] = (int)k;
+  }
+}
+
+struct RunHead {  // 1 at the first entry of each run of equal sorted keys
+  const unsigned long long* keys;
+  __device__ int operator()(int64_t k) const { return (k == 0 || keys[k] != keys[k - 1]) ? 1 : 0; }
+};
+
+// one thread per run head: canonical (row, col, value) with
+// value = first + pairwise(rest) in stable (input) order
+__global__ void reduce_runs(int64_t nnz, int64_t ncols, const unsigned long long* __restrict__ keys,
+                            const int* __restrict__ perm, const int* __restrict__ pos,
+                            const double* __restrict__ vals, int* r_out, int* c_out,
+                            double* v_out) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long key = keys[k];
+    if (k > 0 && keys[k - 1] == key) continue;
+    int64_t e = k + 1;
+    while (e < nnz && keys[e] == key) ++e;
+    const double first = vals[perm[k]];
+    double v = first;
+    if (e - k > 1) {
+      const int* p = perm + k + 1;
+      v = add(first, pairwise_serial(e - k - 1, [&](int64_t i) { return vals[p[i]]; }));
+    }
+    const int o = pos[k];
+    r_out[o] = (int)(key / (unsigned long long)ncols);
+    c_out[o] = (int)(key % (unsigned long long)ncols);
+    v_out[o] = v;
+  }
+}
+
+// DIA source: per-row count of nonzero in-range slots
+struct DiaRowCount {
+  int nrows, ncols, nd;
+  const int* off;
+  const double* vals;
+  __device__ int operator()(int64_t i) const {
+    int cnt = 0;
+    for (int j = 0; j < nd; ++j) {
+      const int64_t col = i + off[j];
+      if (col >= 0 && col < ncols && vals[i * nd + j] != 0.0) ++cnt;
+    }
+    return cnt;
+  }
+};
+__global__ void dia_emit(int nrows, int ncols, int nd, const int* __restrict__ off,
+                         const double* __restrict__ vals, const int* __restrict__ start,
+                         int* r, int* c, double* v) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nrows; i += gridDim.x * blockDim.x) {
+    int o = start[i];
+    for (int j = 0; j < nd; ++j) {
+      const int64_t col = (int64_t)i + off[j];
+      const double x = vals[(int64_t)i * nd + j];
+      if (col >= 0 && col < ncols && x != 0.0) {
+        r[o] = i;
+        c[o] = (int)col;
+        v[o] = x;
+        ++o;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------- targets -----
+// offsets[i] = first canonical entry with row >= i  (rows sorted)
+__global__ void rows_to_offsets(int64_t nnz, int nrows, const int* __restrict__ r, int* off) {
+  if (nnz == 0) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= nrows; i += gridDim.x * blockDim.x)
+      off[i] = 0;
+    return;
+  }
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k <= nnz;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int lo = (k == 0) ? -1 : r[k - 1];
+    const int hi = (k == nnz) ? nrows : r[k];
+    for (int i = lo + 1; i <= hi; ++i) off[i] = (int)k;
+  }
+}
+
+__global__ void mark_diags(int64_t nnz, int nrows, const int* __restrict__ r,
+                           const int* __restrict__ c, unsigned char* flags) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz;
+       k += (int64_t)gridDim.x * blockDim.x)
+    flags[(int64_t)c[k] - r[k] + nrows - 1] = 1;
+}
+struct FlagAt {
+  const unsigned char* f;
+  __device__ int operator()(int64_t k) const { return f[k]; }
+};
+__global__ void diag_offsets_kernel(int64_t D, int nrows, const unsigned char* __restrict__ flags,
+                                    const int* __restrict__ map, int* offsets) {
+  for (int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; d < D;
+       d += (int64_t)gridDim.x * blockDim.x)
+    if (flags[d]) offsets[map[d]] = (int)(d - (nrows - 1));
+}
+__global__ void zero_f64(int64_t n, double* p) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = 0.0;
+}
+__global__ void dia_scatter(int64_t nnz, int nrows, int64_t nd, const int* __restrict__ r,
+                            const int* __restrict__ c, const double* __restrict__ v,
+                            const int* __restrict__ map, double* vals) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int j = map[(int64_t)c[k] - r[k] + nrows - 1];
+    vals[(int64_t)r[k] * nd + j] = v[k];
+  }
+}
+
+static unsigned grid1d(int64_t n) {
+  int64_t g = ceil_div(n, 256);
+  const int64_t cap = (int64_t)sm_count() * 16;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (unsigned)g;
+}
+
+static int bits_for(unsigned long long maxkey) {
+  int b = 0;
+  while (b < 64 && (maxkey >> b) != 0ull) ++b;
+  return b < 1 ? 1 : b;
+}
+
+// canonicalise raw (rows, cols, vals) into job->{r,c,v}
+static int canonicalize(ds_convert_job* job, int64_t nnz, const int* rows, const int* cols,
+                        const double* vals, bool rows_owned) {
+  cudaStream_t st = job->st;
+  if (nnz == 0) {
+    job->nnz = 0;
+    if (rows_owned) DS_CUDA(cudaFreeAsync(const_cast<int*>(rows), st));
+    return DS_OK;
+  }
+  int64_t bad = 0;
+  int rc = exclusive_scan(nnz, OrderBad{rows, cols}, nullptr, &bad, st);
+  if (rc) return rc;
+  if (bad == 0) {  // already canonical: borrow (copied into the target at finish)
+    job->nnz = nnz;
+    job->r = const_cast<int*>(rows);
+    job->own_r = rows_owned;
+    job->c = const_cast<int*>(cols);
+    job->v = const_cast<double*>(vals);
+    return DS_OK;
+  }
+  // stable radix sort of (row*ncols + col) keys with the entry index
+  unsigned long long *keys = nullptr, *keys_s = nullptr;
+  int *idx = nullptr, *perm = nullptr, *pos = nullptr;
+  DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&keys), nnz * 8, st));
+  DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&keys_s), nnz * 8, st));
+  DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&idx), nnz * 4, st));
+  DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&perm), nnz * 4, st));
+  make_keys<<<grid1d(nnz), 256, 0, st>>>(nnz, job->ncols, rows, cols, keys, idx);
+  DS_LAUNCH_CHECK("make_keys");
+  const unsigned long long maxkey =
+      (unsigned long long)(job->nrows > 0 ? job->nrows : 1) * (unsigned long long)(job->ncols > 0 ? job->ncols : 1);
+  const int end_bit = bits_for(maxkey - 1);
+  size_t tmp_bytes = 0;
+  DS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys_s, idx, perm, (int)nnz, 0,
+                                          end_bit, st));
+  void* tmp = nullptr;
+  DS_CUDA(cudaMallocAsync(&tmp, tmp_bytes, st));
+  DS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys_s, idx, perm, (int)nnz, 0,
+                                          end_bit, st));
+  DS_CUDA(cudaFreeAsync(tmp, st));
+  DS_CUDA(cudaFreeAsync(keys, st));
+  DS_CUDA(cudaFreeAsync(idx, st));
+  if (rows_owned) DS_CUDA(cudaFreeAsync(const_cast<int*>(rows), st));
+  DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&pos), nnz * 4, st));
+  int64_t nc = 0;
+  rc = exclusive_scan(nnz, RunHead{keys_s}, pos, &nc, st);
+  if (rc) return rc;
+  job->nnz = nc;
+  DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&job->r), nc * 4, st));
+  DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&job->c), nc * 4, st));
+  DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&job->v), nc * 8, st));
+  job->own_r = job->own_c = job->own_v = true;
+  reduce_runs<<<grid1d(nnz), 256, 0, st>>>(nnz, job->ncols, keys_s, perm, pos, vals, job->r,
+                                           job->c, job->v);
+  DS_LAUNCH_CHECK("reduce_runs");
+  DS_CUDA(cudaFreeAsync(keys_s, st));
+  DS_CUDA(cudaFreeAsync(perm, st));
+  DS_CUDA(cudaFreeAsync(pos, st));
+  return DS_OK;
+}
+
+static void free_job(ds_convert_job* job) {
+  if (!job) return;
+  cudaStream_t st = job->st;
+  if (job->own_r && job->r) cudaFreeAsync(job->r, st);
+  if (job->own_c && job->c) cudaFreeAsync(job->c, st);
+  if (job->own_v && job->v) cudaFreeAsync(job->v, st);
+  if (job->diag_map) cudaFreeAsync(job->diag_map, st);
+  if (job->dia_off) cudaFreeAsync(job->dia_off, st);
+  delete job;
+}
+
+// size the target; DIA: presence flags -> ndiags -> fill check before alloc
+static int size_target(ds_convert_job* job, int64_t fill_limit, int64_t* out_nnz,
+                       int64_t* out_ndiags) {
+  cudaStream_t st = job->st;
+  *out_nnz = job->nnz;
+  *out_ndiags = 0;
+  if (job->target != DS_FMT_DIA) return DS_OK;
+  const int64_t D = job->nrows + job->ncols - 1;
+  int64_t nd = 0;
+  if (D > 0 && job->nnz > 0) {
+    unsigned char* flags = nullptr;
+    DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&flags), D, st));
+    DS_CUDA(cudaMemsetAsync(flags, 0, D, st));
+    mark_diags<<<grid1d(job->nnz), 256, 0, st>>>(job->nnz, (int)job->nrows, job->r, job->c,
+                                                 flags);
+    DS_LAUNCH_CHECK("mark_diags");
+    DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&job->diag_map), D * sizeof(int), st));
+    int rc = exclusive_scan(D, FlagAt{flags}, job->diag_map, &nd, st);
+    if (rc) return rc;
+    if (nd > 0) {
+      DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&job->dia_off), nd * sizeof(int), st));
+      diag_offsets_kernel<<<grid1d(D), 256, 0, st>>>(D, (int)job->nrows, flags, job->diag_map,
+                                                      job->dia_off);
+      DS_LAUNCH_CHECK("diag_offsets_kernel");
+    }
+    DS_CUDA(cudaFreeAsync(flags, st));
+  }
+  job->ndiags = nd;
+  *out_ndiags = nd;
+  const __int128 slots = (__int128)nd * (__int128)job->nrows;
+  if (slots > (__int128)fill_limit) {
+    set_error("%lld diagonals x %lld rows = %lld value slots exceed the fill limit of %lld",
+              (long long)nd, (long long)job->nrows, (long long)(nd * job->nrows),
+              (long long)fill_limit);
+    return DS_ERR_DIA_FILL_OVERFLOW;
+  }
+  return DS_OK;
+}
+
+static int begin_common(ds_convert_job* job, int64_t fill_limit, ds_convert_job** out,
+                        int64_t* out_nnz, int64_t* out_ndiags) {
+  int rc = size_target(job, fill_limit, out_nnz, out_ndiags);
+  if (rc) {
+    free_job(job);
+    *out = nullptr;
+    return rc;
+  }
+  *out = job;
+  return DS_OK;
+}
+
+}  // namespace ds
+
+using namespace ds;
+
+static ds_convert_job* new_job(int64_t nrows, int64_t ncols, int target, void* stream) {
+  ds_convert_job* job = new ds_convert_job;
+  job->st = as_stream(stream);
+  job->nrows = nrows;
+  job->ncols = ncols;
+  job->target = target;
+  return job;
+}
+
+static bool dims_ok(int64_t nrows, int64_t ncols, int64_t nnz) {
+  if (nrows < 0 || ncols < 0 || nrows >= (1ll << 31) || ncols >= (1ll << 31) ||
+      nnz >= (1ll << 31)) {
+    set_error("dimensions must be < 2^31");
+    return false;
+  }
+  return true;
+}
+
+extern "C" int ds_convert_begin_coo(int64_t nrows, int64_t ncols, int64_t nnz, const int32_t* rows,
+                                    const int32_t* cols, const double* values, int target,
+                                    int64_t fill_limit, void* stream, ds_convert_job** job,
+                                    int64_t* out_nnz, int64_t* out_ndiags) {
+  *job = nullptr;
+  if (!dims_ok(nrows, ncols, nnz)) return DS_ERR_NOT_SUPPORTED;
+  ds_convert_job* j = new_job(nrows, ncols, target, stream);
+  int rc = canonicalize(j, nnz, rows, cols, values, false);
+  if (rc) {
+    free_job(j);
+    return rc;
+  }
+  return begin_common(j, fill_limit, job, out_nnz, out_ndiags);
+}
+
+extern "C" int ds_convert_begin_csr(int64_t nrows, int64_t ncols, int64_t nnz,
+                                    const int32_t* row_offsets, const int32_t* cols,
+                                    const double* values, int target, int64_t fill_limit,
+                                    void* stream, ds_convert_job** job, int64_t* out_nnz,
+                                    int64_t* out_ndiags) {
+  *job = nullptr;
+  if (!dims_ok(nrows, ncols, nnz)) return DS_ERR_NOT_SUPPORTED;
+  ds_convert_job* j = new_job(nrows, ncols, target, stream);
+  int* rows = nullptr;
+  if (nnz > 0) {
+    DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&rows), nnz * 4, j->st));
+    csr_expand_rows<<<grid1d(nrows * 8), 256, 0, j->st>>>((int)nrows, row_offsets, rows);
+    DS_LAUNCH_CHECK("csr_expand_rows");
+  }
+  int rc = canonicalize(j, nnz, rows, cols, values, true);
+  if (rc) {
+    free_job(j);
+    return rc;
+  }
+  return begin_common(j, fill_limit, job, out_nnz, out_ndiags);
+}
+
+extern "C" int ds_convert_begin_dia(int64_t nrows, int64_t ncols, int32_t ndiags,
+                                    const int32_t* offsets, const double* values, int target,
+                                    int64_t fill_limit, void* stream, ds_convert_job** job,
+                                    int64_t* out_nnz, int64_t* out_ndiags) {
+  *job = nullptr;
+  if (!dims_ok(nrows, ncols, 0)) return DS_ERR_NOT_SUPPORTED;
+  ds_convert_job* j = new_job(nrows, ncols, target, stream);
+  cudaStream_t st = j->st;
+  int64_t nc = 0;
+  if (nrows > 0 && ndiags > 0) {
+    int* start = nullptr;
+    DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&start), nrows * sizeof(int), st));
+    int rc = exclusive_scan(nrows, DiaRowCount{(int)nrows, (int)ncols, ndiags, offsets, values},
+                            start, &nc, st);
+    if (rc) {
+      free_job(j);
+      return rc;
+    }
+    if (nc > 0) {
+      DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&j->r), nc * 4, st));
+      DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&j->c), nc * 4, st));
+      DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&j->v), nc * 8, st));
+      j->own_r = j->own_c = j->own_v = true;
+      dia_emit<<<grid1d(nrows), 256, 0, st>>>((int)nrows, (int)ncols, ndiags, offsets, values,
+                                              start, j->r, j->c, j->v);
+      DS_LAUNCH_CHECK("dia_emit");
+    }
+    DS_CUDA(cudaFreeAsync(start, st));
+  }
+  j->nnz = nc;
+  return begin_common(j, fill_limit, job, out_nnz, out_ndiags);
+}
+
+extern "C" int ds_convert_finish_coo(ds_convert_job* job, int32_t* rows, int32_t* cols,
+                                     double* values) {
+  cudaStream_t st = job->st;
+  if (job->nnz > 0) {
+    DS_CUDA(cudaMemcpyAsync(rows, job->r, job->nnz * 4, cudaMemcpyDeviceToDevice, st));
+    DS_CUDA(cudaMemcpyAsync(cols, job->c, job->nnz * 4, cudaMemcpyDeviceToDevice, st));
+    DS_CUDA(cudaMemcpyAsync(values, job->v, job->nnz * 8, cudaMemcpyDeviceToDevice, st));
+  }
+  free_job(job);
+  return DS_OK;
+}
+
+extern "C" int ds_convert_finish_csr(ds_convert_job* job, int32_t* row_offsets, int32_t* cols,
+                                     double* values) {
+  cudaStream_t st = job->st;
+  rows_to_offsets<<<grid1d(job->nnz + 1 > job->nrows + 1 ? job->nnz + 1 : job->nrows + 1), 256, 0,
+                    st>>>(job->nnz, (int)job->nrows, job->r, row_offsets);
+  DS_LAUNCH_CHECK("rows_to_offsets");
+  if (job->nnz > 0) {
+    DS_CUDA(cudaMemcpyAsync(cols, job->c, job->nnz * 4, cudaMemcpyDeviceToDevice, st));
+    DS_CUDA(cudaMemcpyAsync(values, job->v, job->nnz * 8, cudaMemcpyDeviceToDevice, st));
+  }
+  free_job(job);
+  return DS_OK;
+}
+
+extern "C" int ds_convert_finish_dia(ds_convert_job* job, int32_t* offsets, double* values) {
+  cudaStream_t st = job->st;
+  const int64_t nd = job->ndiags;
+  if (nd > 0) {
+    DS_CUDA(cudaMemcpyAsync(offsets, job->dia_off, nd * sizeof(int), cudaMemcpyDeviceToDevice,
+                            st));
+    const int64_t slots = nd * job->nrows;
+    zero_f64<<<grid1d(slots), 256, 0, st>>>(slots, values);
+    dia_scatter<<<grid1d(job->nnz), 256, 0, st>>>(job->nnz, (int)job->nrows, nd, job->r, job->c,
+                                                  job->v, job->diag_map, values);
+    DS_LAUNCH_CHECK("dia_scatter");
+  }
+  free_job(job);
+  return DS_OK;
+}
+
+extern "C" void ds_convert_abort(ds_convert_job* job) { free_job(job); }

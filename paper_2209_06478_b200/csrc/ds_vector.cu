@@ -1,0 +1,621 @@
+// ds_vector.cu -- dense-vector kernels, diagonal helpers, halo gather and the
+// CG building blocks (kernels.py:205-337, stencil.py:280-295, solver.py:56-189).
+#include "ds_common.cuh"
+#include "ds_kernels.cuh"
+
+namespace ds {
+
+constexpr int kVecBlock = 256;
+
+static unsigned grid_for(int64_t n, int per_thread = 4) {
+  int64_t g = ceil_div(n, (int64_t)kVecBlock * per_thread);
+  const int64_t cap = (int64_t)sm_count() * 16;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (unsigned)g;
+}
+
+// ------------------------------------------------------------------ dot ----
+// Fixed-order reduction: thread t of block b sums i = b*B + t (+ grid stride)
+// sequentially, blocks reduce with a fixed tree, the last block sums the
+// block partials in a fixed tree.  Same n -> same bits, every run.
+__global__ void __launch_bounds__(kVecBlock)
+    dot_kernel(int64_t n, const double* __restrict__ a, const double* __restrict__ b, DotOut d) {
+  if (d.skip()) return;
+  double v = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * kVecBlock + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * kVecBlock)
+    v = add(v, mul(a[i], b[i]));
+  d.finish_block<kVecBlock>(v);
+}
+
+int launch_dot(int64_t n, const double* a, const double* b, const DotOut& d, cudaStream_t st) {
+  int64_t g = ceil_div(n, (int64_t)kVecBlock * 8);
+  if (g < 1) g = 1;
+  if (g > 1024) g = 1024;  // a function of n only: reproducible across devices
+  g = d.clamp_grid(g);
+  dot_kernel<<<(unsigned)g, kVecBlock, 0, st>>>(n, a, b, d);
+  DS_LAUNCH_CHECK("dot_kernel");
+  return DS_OK;
+}
+
+// workspace layout: [ticket (16 B)] [partials kMaxPartials doubles]
+struct Workspace {
+  unsigned* ticket;
+  double* partials;
+  explicit Workspace(void* w)
+      : ticket(reinterpret_cast<unsigned*>(w)),
+        partials(reinterpret_cast<double*>(reinterpret_cast<char*>(w) + 16)) {}
+};
+constexpr int64_t kWorkspaceBytes = 16 + (int64_t)kMaxPartials * 8;
+
+// --------------------------------------------------------------- waxpby ----
+// w = alpha*x + beta*y with both products rounded (numpy evaluates
+// alpha * x and beta * y into temporaries, kernels.py:219).  w may alias.
+__global__ void __launch_bounds__(kVecBlock)
+    waxpby_kernel(int64_t n, double alpha, const double* x, double beta, const double* y,
+                  double* w, const int* guard) {
+  if (guard && *guard) return;
+  for (int64_t i = (int64_t)blockIdx.x * kVecBlock + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * kVecBlock)
+    w[i] = add(mul(alpha, x[i]), mul(beta, y[i]));
+}
+
+// ----------------------------------------------------------------- scan ----
+// np.cumsum is strictly sequential; reproduce it exactly: one thread carries
+// the running sum while the block stages tiles through shared memory.
+constexpr int kScanTile = 4096;
+__global__ void __launch_bounds__(kVecBlock)
+    scan_seq_kernel(int64_t n, const double* __restrict__ x, double* out, double* total) {
+  __shared__ double buf[kScanTile];
+  double acc = 0.0;
+  for (int64_t t0 = 0; t0 < n; t0 += kScanTile) {
+    const int cnt = (int)min64(kScanTile, n - t0);
+    for (int k = threadIdx.x; k < cnt; k += kVecBlock) buf[k] = x[t0 + k];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int k = 0;
+      if (t0 == 0) {
+        acc = buf[0];  // out[0] = x[0]
+        k = 1;
+      }
+      for (; k < cnt; ++k) {
+        acc = add(acc, buf[k]);
+        buf[k] = acc;
+      }
+    }
+    __syncthreads();
+    if (out)
+      for (int k = threadIdx.x; k < cnt; k += kVecBlock) out[t0 + k] = buf[k];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && total) *total = (n > 0) ? acc : 0.0;
+}
+
+// --------------------------------------------------------------- gather ----
+__global__ void gather_kernel(int64_t count, const int* __restrict__ idx,
+                              const double* __restrict__ src, double* __restrict__ dst,
+                              const int* guard) {
+  if (guard && *guard) return;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < count;
+       k += (int64_t)gridDim.x * blockDim.x)
+    dst[k] = src[idx[k]];
+}
+
+// ------------------------------------------------------------- diagonal ----
+__global__ void extract_diag_csr_kernel(int n, const int* __restrict__ off,
+                                        const int* __restrict__ col,
+                                        const double* __restrict__ val, double* out) {
+  // out[rows[hit]] = values[hit]: with repeated (i,i) the last stored wins
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double v = 0.0;
+    for (int k = off[i]; k < off[i + 1]; ++k)
+      if (col[k] == i) v = val[k];
+    out[i] = v;
+  }
+}
+
+__global__ void csr_diag_presence(int n, const int* __restrict__ off, const int* __restrict__ col,
+                                  long long* first_missing) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    bool hit = false;
+    for (int k = off[i]; k < off[i + 1] && !hit; ++k) hit = (col[k] == i);
+    if (!hit) atomicMin(first_missing, (long long)i);
+  }
+}
+
+__global__ void update_diag_csr_kernel(int nrows, int n, const int* __restrict__ off,
+                                       const int* __restrict__ col, double* val,
+                                       const double* __restrict__ d) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nrows && i < n;
+       i += gridDim.x * blockDim.x)
+    for (int k = off[i]; k < off[i + 1]; ++k)
+      if (col[k] == i) val[k] = d[i];
+}
+
+// COO: per-row count of diagonal entries and first occurrence index
+__global__ void coo_diag_scan(int64_t nnz, int n, const int* __restrict__ rows,
+                              const int* __restrict__ cols, int* count, int* first) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int r = rows[k];
+    if (r == cols[k] && r < n) {
+      atomicAdd(count + r, 1);
+      atomicMin(first + r, (int)k);
+    }
+  }
+}
+__global__ void coo_diag_missing(int n, const int* __restrict__ count, long long* first_missing,
+                                 int* maxcount) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int c = count[i];
+    if (c == 0) atomicMin(first_missing, (long long)i);
+    atomicMax(maxcount, c);
+  }
+}
+// extract with <= 2 duplicates per row: 0 + a + b is order independent
+__global__ void coo_extract_atomic(int64_t nnz, int n, const int* __restrict__ rows,
+                                   const int* __restrict__ cols, const double* __restrict__ val,
+                                   double* out) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int r = rows[k];
+    if (r == cols[k] && r < n) atomicAdd(out + r, val[k]);
+  }
+}
+// general case: sequential in stored order (np.bincount)
+__global__ void coo_extract_serial(int64_t nnz, int n, const int* __restrict__ rows,
+                                   const int* __restrict__ cols, const double* __restrict__ val,
+                                   double* out) {
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    for (int64_t k = 0; k < nnz; ++k) {
+      const int r = rows[k];
+      if (r == cols[k] && r < n) out[r] = add(out[r], val[k]);
+    }
+}
+__global__ void coo_update_kernel(int64_t nnz, int n, const int* __restrict__ rows,
+                                  const int* __restrict__ cols, double* val,
+                                  const int* __restrict__ first, const double* __restrict__ d) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int r = rows[k];
+    if (r == cols[k] && r < n) val[k] = (first[r] == (int)k) ? d[r] : 0.0;
+  }
+}
+__global__ void fill_i32(int64_t n, int* p, int v) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+__global__ void fill_f64_plain(int64_t n, double* p, double v) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+__global__ void dia_diag_column_kernel(int64_t n, int nd, int j0, double* vals, double* vec,
+                                       int dir) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (dir == 0) vec[i] = vals[i * nd + j0];
+    else vals[i * nd + j0] = vec[i];
+  }
+}
+
+__global__ void dia_nonzero_kernel(int nrows, int ncols, int nd, const int* __restrict__ off,
+                                   const double* __restrict__ vals, unsigned long long* count) {
+  unsigned long long c = 0;
+  const int64_t total = (int64_t)nrows * nd;
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < total;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(s / nd), j = (int)(s % nd);
+    const int64_t c0 = (int64_t)i + off[j];
+    if (c0 >= 0 && c0 < ncols && vals[s] != 0.0) ++c;
+  }
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
+}
+
+// ------------------------------------------------------------------- CG ----
+// setup: r = 1*b + (-1)*ap ; p = 1*r + 0*r ; partial b.b and r.r
+__global__ void __launch_bounds__(kVecBlock)
+    cg_setup_kernel(int64_t n, const double* __restrict__ b, const double* __restrict__ ap,
+                    double* r, double* p, DotOut dbb, DotOut drr) {
+  double vb = 0.0, vr = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * kVecBlock + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * kVecBlock) {
+    const double bi = b[i];
+    const double ri = add(mul(1.0, bi), mul(-1.0, ap[i]));
+    r[i] = ri;
+    p[i] = add(mul(1.0, ri), mul(0.0, ri));
+    vb = add(vb, mul(bi, bi));
+    vr = add(vr, mul(ri, ri));
+  }
+  // two reductions share one launch: separate tickets/partials
+  dbb.finish_block<kVecBlock>(vb);
+  drr.finish_block<kVecBlock>(vr);
+}
+
+__global__ void cg_setup_finalize_kernel(ds_cg_scalars* s, const double* bb_parts,
+                                         const double* rr_parts, int nparts, double tol,
+                                         int max_iters, double* history) {
+  s->tol = tol;
+  s->max_iters = max_iters;
+  s->bb = ordered_sum(bb_parts, nparts);
+  s->alpha = s->beta = s->pap = s->rr_new = 0.0;
+  cg_finalize(kStageSetup, s, history, rr_parts, nparts);
+}
+
+// x = 1*x + alpha*p ; r = 1*r + (-alpha)*ap ; partial r.r   (solver.py:177-180)
+__global__ void __launch_bounds__(kVecBlock)
+    cg_update_kernel(int64_t n, double* x, double* r, const double* __restrict__ p,
+                     const double* __restrict__ ap, const ds_cg_scalars* s, DotOut d) {
+  if (d.skip()) return;
+  const double alpha = s->alpha;
+  const double nalpha = -alpha;
+  double v = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * kVecBlock + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * kVecBlock) {
+    x[i] = add(mul(1.0, x[i]), mul(alpha, p[i]));
+    const double ri = add(mul(1.0, r[i]), mul(nalpha, ap[i]));
+    r[i] = ri;
+    v = add(v, mul(ri, ri));
+  }
+  d.finish_block<kVecBlock>(v);
+}
+
+// p = 1*r + beta*p  (solver.py:185-188)
+__global__ void __launch_bounds__(kVecBlock)
+    cg_direction_kernel(int64_t n, const double* __restrict__ r, double* p,
+                        const ds_cg_scalars* s) {
+  if (s->done) return;
+  const double beta = s->beta;
+  for (int64_t i = (int64_t)blockIdx.x * kVecBlock + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * kVecBlock)
+    p[i] = add(mul(1.0, r[i]), mul(beta, p[i]));
+}
+
+__global__ void cg_finalize_kernel(int stage, ds_cg_scalars* s, double* history,
+                                   const double* parts, int nparts) {
+  cg_finalize(stage, s, history, parts, nparts);
+}
+
+}  // namespace ds
+
+// ============================================================== C ABI ======
+using namespace ds;
+
+static DotOut make_dot(void* workspace, int slot, const double* other, double* result) {
+  // workspace holds two independent reduction slots (tickets + partials)
+  char* base = reinterpret_cast<char*>(workspace) + (int64_t)slot * kWorkspaceBytes;
+  Workspace w(base);
+  DotOut d;
+  d.other = other;
+  d.partials = w.partials;
+  d.ticket = w.ticket;
+  d.result = result;
+  d.max_blocks = kMaxPartials;
+  return d;
+}
+
+extern "C" int64_t ds_dot_workspace_bytes(void) { return 2 * kWorkspaceBytes; }
+extern "C" int64_t ds_cg_workspace_bytes(void) { return 2 * kWorkspaceBytes; }
+
+extern "C" int ds_dot(int64_t n, const double* x, const double* y, double* result_dev,
+                      void* workspace, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  if (n <= 0) {
+    DS_CUDA(cudaMemsetAsync(result_dev, 0, sizeof(double), st));
+    return DS_OK;
+  }
+  DotOut d = make_dot(workspace, 0, nullptr, result_dev);
+  return launch_dot(n, x, y, d, st);
+}
+
+extern "C" int ds_waxpby(int64_t n, double alpha, const double* x, double beta, const double* y,
+                         double* w, void* stream) {
+  if (n <= 0) return DS_OK;
+  waxpby_kernel<<<grid_for(n), kVecBlock, 0, as_stream(stream)>>>(n, alpha, x, beta, y, w,
+                                                                  nullptr);
+  DS_LAUNCH_CHECK("waxpby_kernel");
+  return DS_OK;
+}
+
+extern "C" int ds_scan(int64_t n, const double* x, double* out, double* total_dev,
+                       void* stream) {
+  scan_seq_kernel<<<1, kVecBlock, 0, as_stream(stream)>>>(n, x, out, total_dev);
+  DS_LAUNCH_CHECK("scan_seq_kernel");
+  return DS_OK;
+}
+
+extern "C" int ds_gather(int64_t count, const int32_t* idx, const double* src, double* dst,
+                         void* stream) {
+  if (count <= 0) return DS_OK;
+  gather_kernel<<<grid_for(count, 2), kVecBlock, 0, as_stream(stream)>>>(count, idx, src, dst,
+                                                                         nullptr);
+  DS_LAUNCH_CHECK("gather_kernel");
+  return DS_OK;
+}
+
+extern "C" int ds_cg_gather(int64_t count, const int32_t* idx, const double* src, double* dst,
+                            const ds_cg_scalars* s, void* stream) {
+  if (count <= 0) return DS_OK;
+  gather_kernel<<<grid_for(count, 2), kVecBlock, 0, as_stream(stream)>>>(
+      count, idx, src, dst, s ? &s->done : nullptr);
+  DS_LAUNCH_CHECK("gather_kernel");
+  return DS_OK;
+}
+
+extern "C" int ds_extract_diag_csr(int64_t nrows, int64_t ncols, const int32_t* row_offsets,
+                                   const int32_t* col_indices, const double* values, double* out,
+                                   void* stream) {
+  const int64_t n = nrows < ncols ? nrows : ncols;
+  if (n <= 0) return DS_OK;
+  extract_diag_csr_kernel<<<grid_for(n, 1), kVecBlock, 0, as_stream(stream)>>>(
+      (int)n, row_offsets, col_indices, values, out);
+  DS_LAUNCH_CHECK("extract_diag_csr_kernel");
+  return DS_OK;
+}
+
+extern "C" int ds_update_diag_csr(int64_t nrows, int64_t ncols, const int32_t* row_offsets,
+                                  const int32_t* col_indices, double* values, const double* d,
+                                  int64_t* first_missing, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  const int64_t n = nrows < ncols ? nrows : ncols;
+  *first_missing = -1;
+  if (n <= 0) return DS_OK;
+  long long* dm = nullptr;
+  DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dm), sizeof(long long), st));
+  const long long big = 0x7fffffffffffffffll;
+  DS_CUDA(cudaMemcpyAsync(dm, &big, sizeof(big), cudaMemcpyHostToDevice, st));
+  csr_diag_presence<<<grid_for(n, 1), kVecBlock, 0, st>>>((int)n, row_offsets, col_indices, dm);
+  long long h = big;
+  DS_CUDA(cudaMemcpyAsync(&h, dm, sizeof(h), cudaMemcpyDeviceToHost, st));
+  DS_CUDA(cudaFreeAsync(dm, st));
+  DS_CUDA(cudaStreamSynchronize(st));
+  if (h != big) {
+    *first_missing = h;
+    set_error("diagonal entry (%lld, %lld) is not structurally present", h, h);
+    return DS_ERR_STRUCTURALLY_ABSENT_DIAG;
+  }
+  update_diag_csr_kernel<<<grid_for(n, 1), kVecBlock, 0, st>>>((int)nrows, (int)n, row_offsets,
+                                                               col_indices, values, d);
+  DS_LAUNCH_CHECK("update_diag_csr_kernel");
+  return DS_OK;
+}
+
+// shared COO diagonal analysis: count/first per row, first missing, max count
+static int coo_diag_analysis(int64_t n, int64_t nnz, const int32_t* rows, const int32_t* cols,
+                             cudaStream_t st, int** count, int** first, long long* missing,
+                             int* maxcount) {
+  DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(count), n * sizeof(int), st));
+  DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(first), n * sizeof(int), st));
+  long long* dm = nullptr;
+  DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dm), 2 * sizeof(long long), st));
+  fill_i32<<<grid_for(n), kVecBlock, 0, st>>>(n, *count, 0);
+  fill_i32<<<grid_for(n), kVecBlock, 0, st>>>(n, *first, 0x7fffffff);
+  const long long init[2] = {0x7fffffffffffffffll, 0};
+  DS_CUDA(cudaMemcpyAsync(dm, init, sizeof(init), cudaMemcpyHostToDevice, st));
+  if (nnz > 0)
+    coo_diag_scan<<<grid_for(nnz), kVecBlock, 0, st>>>(nnz, (int)n, rows, cols, *count, *first);
+  coo_diag_missing<<<grid_for(n), kVecBlock, 0, st>>>((int)n, *count, dm,
+                                                      reinterpret_cast<int*>(dm + 1));
+  DS_LAUNCH_CHECK("coo_diag_analysis");
+  long long h[2];
+  DS_CUDA(cudaMemcpyAsync(h, dm, sizeof(h), cudaMemcpyDeviceToHost, st));
+  DS_CUDA(cudaFreeAsync(dm, st));
+  DS_CUDA(cudaStreamSynchronize(st));
+  *missing = h[0];
+  *maxcount = static_cast<int>(h[1] & 0xffffffff);
+  return DS_OK;
+}
+
+extern "C" int ds_extract_diag_coo(int64_t nrows, int64_t ncols, int64_t nnz, const int32_t* rows,
+                                   const int32_t* cols, const double* values, double* out,
+                                   void* stream) {
+  cudaStream_t st = as_stream(stream);
+  const int64_t n = nrows < ncols ? nrows : ncols;
+  if (n <= 0) return DS_OK;
+  int *count = nullptr, *first = nullptr;
+  long long missing;
+  int maxcount;
+  int rc = coo_diag_analysis(n, nnz, rows, cols, st, &count, &first, &missing, &maxcount);
+  if (rc) return rc;
+  fill_f64_plain<<<grid_for(n), kVecBlock, 0, st>>>(n, out, 0.0);
+  if (nnz > 0) {
+    if (maxcount <= 2)
+      coo_extract_atomic<<<grid_for(nnz), kVecBlock, 0, st>>>(nnz, (int)n, rows, cols, values,
+                                                              out);
+    else
+      coo_extract_serial<<<1, 1, 0, st>>>(nnz, (int)n, rows, cols, values, out);
+  }
+  DS_LAUNCH_CHECK("coo_extract");
+  DS_CUDA(cudaFreeAsync(count, st));
+  DS_CUDA(cudaFreeAsync(first, st));
+  return DS_OK;
+}
+
+extern "C" int ds_update_diag_coo(int64_t nrows, int64_t ncols, int64_t nnz, const int32_t* rows,
+                                  const int32_t* cols, double* values, const double* d,
+                                  int64_t* first_missing, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  const int64_t n = nrows < ncols ? nrows : ncols;
+  *first_missing = -1;
+  if (n <= 0) return DS_OK;
+  int *count = nullptr, *first = nullptr;
+  long long missing;
+  int maxcount;
+  int rc = coo_diag_analysis(n, nnz, rows, cols, st, &count, &first, &missing, &maxcount);
+  if (rc) return rc;
+  if (missing != 0x7fffffffffffffffll) {
+    DS_CUDA(cudaFreeAsync(count, st));
+    DS_CUDA(cudaFreeAsync(first, st));
+    *first_missing = missing;
+    set_error("diagonal entry (%lld, %lld) is not structurally present", missing, missing);
+    return DS_ERR_STRUCTURALLY_ABSENT_DIAG;
+  }
+  coo_update_kernel<<<grid_for(nnz), kVecBlock, 0, st>>>(nnz, (int)n, rows, cols, values, first,
+                                                         d);
+  DS_LAUNCH_CHECK("coo_update_kernel");
+  DS_CUDA(cudaFreeAsync(count, st));
+  DS_CUDA(cudaFreeAsync(first, st));
+  return DS_OK;
+}
+
+extern "C" int ds_dia_diag_column(int64_t n, int32_t ndiags, int32_t j0, double* values,
+                                  double* vec, int direction, void* stream) {
+  if (n <= 0) return DS_OK;
+  dia_diag_column_kernel<<<grid_for(n), kVecBlock, 0, as_stream(stream)>>>(n, ndiags, j0, values,
+                                                                           vec, direction);
+  DS_LAUNCH_CHECK("dia_diag_column_kernel");
+  return DS_OK;
+}
+
+extern "C" int ds_dia_count_nonzero(int64_t nrows, int64_t ncols, int32_t ndiags,
+                                    const int32_t* offsets, const double* values, int64_t* count,
+                                    void* stream) {
+  cudaStream_t st = as_stream(stream);
+  *count = 0;
+  if (nrows <= 0 || ndiags <= 0) return DS_OK;
+  unsigned long long* dc = nullptr;
+  DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dc), sizeof(*dc), st));
+  DS_CUDA(cudaMemsetAsync(dc, 0, sizeof(*dc), st));
+  dia_nonzero_kernel<<<grid_for(nrows * ndiags), kVecBlock, 0, st>>>((int)nrows, (int)ncols,
+                                                                      ndiags, offsets, values, dc);
+  DS_LAUNCH_CHECK("dia_nonzero_kernel");
+  unsigned long long h = 0;
+  DS_CUDA(cudaMemcpyAsync(&h, dc, sizeof(h), cudaMemcpyDeviceToHost, st));
+  DS_CUDA(cudaFreeAsync(dc, st));
+  DS_CUDA(cudaStreamSynchronize(st));
+  *count = (int64_t)h;
+  return DS_OK;
+}
+
+// ------------------------------------------------------------------ CG -----
+extern "C" int ds_spmv(const ds_matrix* a, const double* x, double* y, int accumulate,
+                       void* stream) {
+  return ds_cg_spmv_dot(a, x, y, accumulate, nullptr, nullptr, 0, nullptr, nullptr, nullptr, 0,
+                        nullptr, stream);
+}
+
+extern "C" int ds_cg_spmv_dot(const ds_matrix* a, const double* x, double* y, int accumulate,
+                              const double* dot_with, double* dot_out, int stage,
+                              ds_cg_scalars* s, double* history, const double* parts,
+                              int nparts_final, void* workspace, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  if (a->nrows < 0 || a->nrows >= (1ll << 31) || a->ncols >= (1ll << 31)) {
+    set_error("dims out of range");
+    return DS_ERR_NOT_SUPPORTED;
+  }
+  DotOut d;
+  d.guard = s ? &s->done : nullptr;
+  const bool want_dot = dot_with != nullptr;
+  DotOut fused;
+  if (want_dot) {
+    fused = make_dot(workspace, 0, dot_with, dot_out);
+    fused.guard = d.guard;
+    fused.stage = stage;
+    fused.s = s;
+    fused.history = history;
+    fused.parts = parts;
+    fused.nparts_final = nparts_final;
+  }
+  const bool acc = accumulate != 0;
+  int rc = DS_OK;
+  bool done_dot = false;
+  switch (a->format) {
+    case DS_FMT_CSR: {
+      const bool can_fuse = want_dot && (a->long_rows == nullptr || a->n_long == 0);
+      rc = launch_csr(a->nrows, a->idx0, a->idx1, a->values, a->long_rows, a->n_long, x, y, acc,
+                      can_fuse ? &fused : &d, st);
+      done_dot = can_fuse;
+      break;
+    }
+    case DS_FMT_DIA: {
+      const bool can_fuse =
+          want_dot && ceil_div(a->nrows, 256) <= (int64_t)kMaxPartials;
+      rc = launch_dia(a->nrows, a->ncols, a->ndiags, a->idx0, a->values, x, y, acc,
+                      can_fuse ? &fused : &d, st);
+      done_dot = can_fuse;
+      break;
+    }
+    case DS_FMT_COO:
+      rc = launch_coo(a->nrows, a->nnz, a->idx0, a->idx1, a->values, a->rows_sorted != 0, x, y,
+                      acc, d.guard, st);
+      break;
+    default:
+      set_error("unknown format %d", a->format);
+      return DS_ERR_INVALID_ARGUMENT;
+  }
+  if (rc) return rc;
+  if (want_dot && !done_dot) {
+    if (a->nrows == 0) {
+      set_error("empty operator in CG");
+      return DS_ERR_INVALID_ARGUMENT;
+    }
+    rc = launch_dot(a->nrows, dot_with, y, fused, st);
+  }
+  return rc;
+}
+
+extern "C" int ds_cg_setup_residual(int64_t n, const double* b, const double* ap, double* r,
+                                    double* p, double* bb_out, double* rr_out, void* workspace,
+                                    void* stream) {
+  cudaStream_t st = as_stream(stream);
+  if (n <= 0) {
+    DS_CUDA(cudaMemsetAsync(bb_out, 0, sizeof(double), st));
+    DS_CUDA(cudaMemsetAsync(rr_out, 0, sizeof(double), st));
+    return DS_OK;
+  }
+  DotOut dbb = make_dot(workspace, 0, nullptr, bb_out);
+  DotOut drr = make_dot(workspace, 1, nullptr, rr_out);
+  int64_t g = ceil_div(n, (int64_t)kVecBlock * 8);
+  if (g > 1024) g = 1024;
+  cg_setup_kernel<<<(unsigned)g, kVecBlock, 0, st>>>(n, b, ap, r, p, dbb, drr);
+  DS_LAUNCH_CHECK("cg_setup_kernel");
+  return DS_OK;
+}
+
+extern "C" int ds_cg_setup_finalize(ds_cg_scalars* s, const double* bb_parts,
+                                    const double* rr_parts, int nparts, double tol,
+                                    int32_t max_iters, double* history, void* stream) {
+  cg_setup_finalize_kernel<<<1, 1, 0, as_stream(stream)>>>(s, bb_parts, rr_parts, nparts, tol,
+                                                           max_iters, history);
+  DS_LAUNCH_CHECK("cg_setup_finalize_kernel");
+  return DS_OK;
+}
+
+extern "C" int ds_cg_update(int64_t n, double* x, double* r, const double* p, const double* ap,
+                            ds_cg_scalars* s, double* rr_out, double* history,
+                            const double* parts, int nparts_final, void* workspace,
+                            void* stream) {
+  cudaStream_t st = as_stream(stream);
+  DotOut d = make_dot(workspace, 0, nullptr, rr_out);
+  d.guard = &s->done;
+  d.stage = kStageRr;
+  d.s = s;
+  d.history = history;
+  d.parts = parts;
+  d.nparts_final = nparts_final;
+  int64_t g = ceil_div(n, (int64_t)kVecBlock * 8);
+  if (g < 1) g = 1;
+  if (g > 1024) g = 1024;
+  cg_update_kernel<<<(unsigned)g, kVecBlock, 0, st>>>(n, x, r, p, ap, s, d);
+  DS_LAUNCH_CHECK("cg_update_kernel");
+  return DS_OK;
+}
+
+extern "C" int ds_cg_direction(int64_t n, const double* r, double* p, const ds_cg_scalars* s,
+                               void* stream) {
+  if (n <= 0) return DS_OK;
+  cg_direction_kernel<<<grid_for(n), kVecBlock, 0, as_stream(stream)>>>(n, r, p, s);
+  DS_LAUNCH_CHECK("cg_direction_kernel");
+  return DS_OK;
+}
+
+extern "C" int ds_cg_finalize(int stage, ds_cg_scalars* s, double* history, const double* parts,
+                              int nparts, void* stream) {
+  cg_finalize_kernel<<<1, 1, 0, as_stream(stream)>>>(stage, s, history, parts, nparts);
+  DS_LAUNCH_CHECK("cg_finalize_kernel");
+  return DS_OK;
+}

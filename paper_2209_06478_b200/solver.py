@@ -1,0 +1,353 @@
+"""Unpreconditioned CG on the device (solver.py:1-234 of the reference).
+
+The recurrence is the reference's, operation for operation (solver.py:73-189):
+
+    r = 1*b + (-1)*(A x0);  ||b||;  rr = r.r;  history[0] = sqrt(rr)/scale
+    p = 1*r + 0*r
+    repeat:  Ap = A p;  pAp = p.Ap  (breakdown iff pAp <= 0);  alpha = rr/pAp
+             x = 1*x + alpha*p;  r = 1*r + (-alpha)*Ap;  rr' = r.r
+             history += sqrt(rr')/scale;  stop iff <= tol
+             p = 1*r + (rr'/rr)*p
+
+but every scalar lives on the device (ds_cg_scalars): the fused kernels
+compute p.Ap inside the SpMV epilogue and r.r inside the x/r update, and the
+block that completes a reduction also derives alpha / beta / history /
+convergence.  Once ``done`` is set every later kernel is a no-op, so the
+host enqueues whole chunks of iterations (optionally as one CUDA graph) and
+reads 80 bytes back per chunk; iteration counts and histories stay exact.
+
+Distributed problems (DistributedOperator) run all partitions from this one
+controller like the reference (partition dots summed in rank order by the
+finalize kernel); dist.py runs one partition per process over NCCL.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .errors import BreakdownZeroCurvature, DimensionMismatch, ValidationFailed
+from .formats import DenseVector, DynamicMatrix, MemorySpace
+from .kernels import ExecBackend, descriptor, extract_diagonal, update_diagonal
+from .stencil import PartitionedProblem, SplitMatrix, device_halo, distributed_spmv
+
+PAP, RR = _native.DS_CG_STAGE_PAP, _native.DS_CG_STAGE_RR
+
+
+@dataclass
+class CgResult:
+    """x, iterations, relative residual history (iterations + 1 entries),
+    converged (solver.py:23-34)."""
+
+    x: DenseVector | list[DenseVector]
+    iterations: int
+    residual_history: np.ndarray
+    converged: bool
+
+
+@dataclass
+class DistributedOperator:
+    problem: PartitionedProblem
+    splits: list[SplitMatrix]
+
+
+@dataclass
+class ValidationReport:
+    passed: bool
+    converged: bool
+    iterations: int
+    iteration_bound: int
+    final_residual: float
+
+
+# ---------------------------------------------------------------------------
+# device CG engine
+# ---------------------------------------------------------------------------
+
+class _Part:
+    """One partition's device state."""
+
+    def __init__(self, local, remote, n, ghosts, device):
+        import torch
+        self.local, self.remote, self.n = local, remote, n
+        self.d_local = descriptor(local)
+        self.d_remote = descriptor(remote) if remote is not None else None
+        f64 = dict(dtype=torch.float64, device=device)
+        self.p_full = torch.zeros(n + ghosts, **f64)
+        self.p = self.p_full[:n]
+        self.x = torch.zeros(n, **f64)
+        self.r = torch.empty(n, **f64)
+        self.ap = torch.empty(n, **f64)
+        self.b = None
+        self.halo = []   # (src partition, count, idx tensor, dst offset in p_full)
+
+
+class CgEngine:
+    """Device-resident CG over one or more partitions on one device."""
+
+    def __init__(self, parts: list[_Part], device, tol: float, max_iters: int):
+        import torch
+        from . import _device
+        self.parts, self.dev = parts, device
+        self.tol, self.max_iters = float(tol), int(max_iters)
+        self.P = len(parts)
+        f64 = dict(dtype=torch.float64, device=device)
+        self.scal = torch.zeros(_native.CG_SCALARS_BYTES // 8, **f64)
+        self.hist = torch.zeros(max(self.max_iters, 0) + 1, **f64)
+        # [bb(P) | rr0(P) | pap(P) | rr(P)] partition partial dots
+        self.dots = torch.zeros(4 * self.P, **f64)
+        self.lib = _native.load()
+        self.ws = _device.workspace(device)
+        self.graph = None
+
+    # pointers ---------------------------------------------------------------
+    def _p(self, t):
+        return t.data_ptr()
+
+    def _dot(self, which: int, k: int) -> int:
+        return self.dots.data_ptr() + 8 * (which * self.P + k)
+
+    def _ck(self, rc):
+        _native.check(rc)
+
+    # setup (solver.py:88-101 / 147-167) --------------------------------------
+    def setup(self, stream) -> None:
+        lib, s = self.lib, self._p(self.scal)
+        self._exchange(stream, guard=None)
+        for k, pt in enumerate(self.parts):
+            self._ck(lib.ds_cg_spmv_dot(ctypes.byref(pt.d_local), self._p(pt.p_full),
+                                        self._p(pt.ap), 0, None, None, 0, None, None, None, 0,
+                                        self._p(self.ws), stream))
+            if pt.d_remote is not None:
+                self._ck(lib.ds_cg_spmv_dot(ctypes.byref(pt.d_remote),
+                                            self._p(pt.p_full) + 8 * pt.n, self._p(pt.ap), 1,
+                                            None, None, 0, None, None, None, 0,
+                                            self._p(self.ws), stream))
+            self._ck(lib.ds_cg_setup_residual(pt.n, self._p(pt.b), self._p(pt.ap),
+                                              self._p(pt.r), self._p(pt.p), self._dot(0, k),
+                                              self._dot(1, k), self._p(self.ws), stream))
+        self._ck(lib.ds_cg_setup_finalize(s, self._dot(0, 0), self._dot(1, 0), self.P, self.tol,
+                                          self.max_iters, self._p(self.hist), stream))
+
+    def _exchange(self, stream, guard) -> None:
+        for pt in self.parts:
+            for q, cnt, idx, off in pt.halo:
+                self._ck(self.lib.ds_cg_gather(cnt, self._p(idx), self._p(self.parts[q].p_full),
+                                               self._p(pt.p_full) + 8 * off, guard, stream))
+
+    # one iteration (solver.py:102-116 / 170-188) ------------------------------
+    def step(self, stream) -> None:
+        lib, s, hist = self.lib, self._p(self.scal), self._p(self.hist)
+        P, ws = self.P, self._p(self.ws)
+        fin = 1 if P == 1 else 0
+        self._exchange(stream, guard=s)
+        for k, pt in enumerate(self.parts):
+            if pt.d_remote is None:
+                self._ck(lib.ds_cg_spmv_dot(ctypes.byref(pt.d_local), self._p(pt.p_full),
+                                            self._p(pt.ap), 0, self._p(pt.p), self._dot(2, k),
+                                            PAP, s, hist, self._dot(2, 0), fin, ws, stream))
+            else:
+                self._ck(lib.ds_cg_spmv_dot(ctypes.byref(pt.d_local), self._p(pt.p_full),
+                                            self._p(pt.ap), 0, None, None, 0, s, None, None, 0,
+                                            ws, stream))
+                self._ck(lib.ds_cg_spmv_dot(ctypes.byref(pt.d_remote),
+                                            self._p(pt.p_full) + 8 * pt.n, self._p(pt.ap), 1,
+                                            self._p(pt.p), self._dot(2, k), PAP, s, hist,
+                                            self._dot(2, 0), fin, ws, stream))
+        if not fin:
+            self._ck(lib.ds_cg_finalize(PAP, s, hist, self._dot(2, 0), P, stream))
+        for k, pt in enumerate(self.parts):
+            self._ck(lib.ds_cg_update(pt.n, self._p(pt.x), self._p(pt.r), self._p(pt.p),
+                                      self._p(pt.ap), s, self._dot(3, k), hist,
+                                      self._dot(3, 0), fin, ws, stream))
+        if not fin:
+            self._ck(lib.ds_cg_finalize(RR, s, hist, self._dot(3, 0), P, stream))
+        for pt in self.parts:
+            self._ck(lib.ds_cg_direction(pt.n, self._p(pt.r), self._p(pt.p), s, stream))
+
+    def scalars(self) -> _native.DsCgScalars:
+        raw = self.scal.cpu().numpy().tobytes()
+        return _native.DsCgScalars.from_buffer_copy(raw)
+
+    def run(self, chunk: int | None = None, use_graph: bool | None = None) -> _native.DsCgScalars:
+        """Enqueue iterations in chunks until ``done`` (one 80-byte readback per chunk)."""
+        import torch
+        from . import _device
+        dev = self.dev
+        with torch.cuda.device(dev):
+            st = _device.stream(dev)
+            self.setup(st)
+            sc = self.scalars()
+            if sc.done:
+                return sc
+            if use_graph is None:
+                use_graph = self.max_iters >= 16
+            c = chunk or (8 if use_graph else 4)
+            if use_graph:
+                self._capture(c)
+            while True:
+                if use_graph:
+                    self.graph.replay()
+                else:
+                    for _ in range(c):
+                        self.step(st)
+                sc = self.scalars()
+                if sc.done:
+                    return sc
+
+    def _capture(self, c: int) -> None:
+        import torch
+        from . import _device
+        cap = torch.cuda.Stream(self.dev)
+        cap.wait_stream(torch.cuda.current_stream(self.dev))
+        with torch.cuda.stream(cap):
+            ws = _device.workspace(self.dev)  # workspace bound to the capture stream
+        torch.cuda.synchronize(self.dev)
+        saved, self.ws = self.ws, ws
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=cap):
+            st = cap.cuda_stream
+            for _ in range(c):
+                self.step(st)
+        self.ws = saved
+        self.graph = g
+
+
+def _finish(engine: CgEngine, sc) -> tuple[int, np.ndarray, bool]:
+    it = int(sc.iter)
+    if sc.done == 2:
+        raise BreakdownZeroCurvature(f"p'Ap = {sc.pap} at iteration {it + 1}")
+    hist = engine.hist[:it + 1].cpu().numpy().copy()
+    return it, hist, sc.done == 1
+
+
+# ---------------------------------------------------------------------------
+# public API
+# ---------------------------------------------------------------------------
+
+def cg(backend: ExecBackend, a, b, x0=None, tol: float = 1e-9, max_iters: int = 500,
+       use_graph: bool | None = None) -> CgResult:
+    """CG for SPD systems (solver.py:56-70): ``a`` is a container, a
+    DynamicMatrix or a DistributedOperator (then b / x0 are per-partition
+    owned vectors).  Stops when ||r||/||b|| <= tol or after max_iters; raises
+    BreakdownZeroCurvature when p'Ap <= 0."""
+    if tol <= 0:
+        raise ValueError(f"tol must be positive, got {tol}")
+    if isinstance(a, DistributedOperator):
+        return _cg_distributed(a, b, x0, tol, max_iters, use_graph)
+    return _cg_single(a, b, x0, tol, max_iters, use_graph)
+
+
+def _cg_single(a, b, x0, tol, max_iters, use_graph):
+    import torch
+    from .datamove import to_device
+    from .kernels import _exec_device
+    mat = a.payload if isinstance(a, DynamicMatrix) else a
+    if mat.nrows != mat.ncols:
+        raise DimensionMismatch(f"cg needs a square matrix, got {mat.nrows}x{mat.ncols}")
+    n = mat.nrows
+    if b.length != n:
+        raise DimensionMismatch(f"b length {b.length} != {n}")
+    if x0 is not None and x0.length != n:
+        raise DimensionMismatch(f"x0 length {x0.length} != {n}")
+    dev = _exec_device(mat, b, x0)
+    A = to_device(mat, dev)
+    with torch.cuda.device(dev):
+        pt = _Part(A, None, n, 0, dev)
+        pt.b = to_device(b, dev).data
+        if x0 is not None:
+            pt.p_full.copy_(to_device(x0, dev).data)   # setup computes A x0 from p_full
+            pt.x.copy_(pt.p_full)
+        eng = CgEngine([pt], dev, tol, max_iters)
+        sc = eng.run(use_graph=use_graph)
+        it, hist, conv = _finish(eng, sc)
+        x = DenseVector(pt.x)
+    if b.space == MemorySpace.HOST:
+        x = DenseVector(pt.x.cpu().numpy())
+    return CgResult(x, it, hist, conv)
+
+
+def build_engine(op: DistributedOperator, bs, x0s, tol, max_iters) -> tuple[CgEngine, list]:
+    """Device engine for a single-controller DistributedOperator."""
+    import torch
+    from .datamove import to_device
+    from .kernels import _exec_device
+    problem, splits = op.problem, op.splits
+    P = problem.npartitions
+    n = problem.spec.local_points
+    if len(bs) != P:
+        raise DimensionMismatch(f"expected {P} right-hand sides, got {len(bs)}")
+    for v in bs:
+        if v.length != n:
+            raise DimensionMismatch(f"b length {v.length} != local size {n}")
+    if x0s is not None:
+        if len(x0s) != P:
+            raise DimensionMismatch(f"expected {P} initial guesses, got {len(x0s)}")
+        for v in x0s:
+            if v.length != n:
+                raise DimensionMismatch(f"x0 length {v.length} != local size {n}")
+    dev = _exec_device(splits[0].local.payload, *bs)
+    parts = []
+    with torch.cuda.device(dev):
+        for k, (part, split) in enumerate(zip(problem.partitions, splits)):
+            loc = to_device(split.local.payload, dev)
+            rem = to_device(split.remote.payload, dev)
+            pt = _Part(loc, rem, n, part.halo.ghost_count, dev)
+            pt.b = to_device(bs[k], dev).data
+            if x0s is not None:
+                pt.x.copy_(to_device(x0s[k], dev).data)
+                pt.p.copy_(pt.x)
+            pt.halo = [(q, cnt, idx, n + start)
+                       for q, cnt, idx, start in device_halo(part, dev) if cnt]
+            parts.append(pt)
+    return CgEngine(parts, dev, tol, max_iters), parts
+
+
+def _cg_distributed(op, bs, x0s, tol, max_iters, use_graph):
+    import torch
+    eng, parts = build_engine(op, bs, x0s, tol, max_iters)
+    with torch.cuda.device(eng.dev):
+        sc = eng.run(use_graph=use_graph)
+        it, hist, conv = _finish(eng, sc)
+    host = bs[0].space == MemorySpace.HOST
+    xs = [DenseVector(pt.x.cpu().numpy()) if host else DenseVector(pt.x) for pt in parts]
+    return CgResult(xs, it, hist, conv)
+
+
+def validate_solver(backend: ExecBackend, problem: PartitionedProblem,
+                    splits: list[SplitMatrix], diag_value: float = 1.0e6, tol: float = 1e-12,
+                    max_iters: int = 50, iteration_bound: int = 12) -> ValidationReport:
+    """Diagonal-modification check (solver.py:192-234): diagonal := diag_value,
+    b := A 1, CG must reach tol within iteration_bound; diagonals restored
+    exactly in every case; ValidationFailed carries the report."""
+    n = problem.spec.local_points
+    saved = [extract_diagonal(sp.local) for sp in splits]
+    space = splits[0].local.space
+    dev = splits[0].local.device
+    new_diag = DenseVector(np.full(n, diag_value)) if space == MemorySpace.HOST else \
+        DenseVector.ones(n, MemorySpace.DEVICE, dev)
+    if space == MemorySpace.DEVICE:
+        new_diag.data.fill_(diag_value)
+    try:
+        for sp in splits:
+            update_diagonal(sp.local, new_diag)
+        ones = [DenseVector.ones(n + p.halo.ghost_count, space, dev) for p in problem.partitions]
+        bs = [DenseVector.zeros(n, space, dev) for _ in problem.partitions]
+        distributed_spmv(backend, problem, splits, ones, bs)
+        res = cg(backend, DistributedOperator(problem, splits), bs, tol=tol, max_iters=max_iters)
+    finally:
+        for sp, d in zip(splits, saved):
+            update_diagonal(sp.local, d)
+    passed = res.converged and res.iterations <= iteration_bound
+    report = ValidationReport(passed=passed, converged=res.converged, iterations=res.iterations,
+                              iteration_bound=iteration_bound,
+                              final_residual=float(res.residual_history[-1]))
+    if not passed:
+        raise ValidationFailed(
+            f"validation cg took {res.iterations} iterations (bound {iteration_bound}), "
+            f"converged={res.converged}", report=report)
+    return report
+
