@@ -1,0 +1,500 @@
+#!/usr/bin/env python
+"""bench.py -- HPCG-style CG on B200 (BASELINE.json metric: "SpMV GFLOP/s & HBM
+GB/s per format; HPCG CG GFLOP/s at 1/2/4/8 B200").
+
+A "step" is ONE conjugate-gradient iteration (solver.py:170-188) on a 27-point
+stencil with a 104^3 local grid per GPU (BASELINE config 3): halo exchange,
+SpMV (local part DIA, remote part CSR -- the paper's multi-format plan), the
+two global dots, three WAXPBY-equivalent updates.  Flops per step are HPCG's
+2*nnz + 10*n.  GPUs -> process grid (1,1,1) (2,1,1) (2,2,1)
+(2,2,2); one process per GPU, weak scaling.
+
+Printed JSON (rank 0, one line): value = whole-job GFLOP/s of the K timed
+steps (CUDA events, max over ranks), plus
+  spmv_sweep  -- config 2: COO / CSR / DIA SpMV at 104^3 (GFLOP/s, GB/s, frac)
+  powerlaw    -- config 4: irregular ~54.5M-nnz matrix, CSR vs COO (+ DIA
+                 overflow), conversion time, the tuner's pick
+  roofline    -- the dominant kernel (fused DIA SpMV + p.Ap) of the CG step
+  e2e         -- the same metric through the public API with host buffers
+  cpu_baseline-- the CPU oracle (oracle/, numpy port of the reference) timed
+                 on this host's cores on a bounded sample
+  clocks      -- nvidia-smi samples taken during the measurements
+
+``--impl reference`` times the reference's CPU implementation (the oracle
+port; the reference itself is pure Python and cannot travel to the box) on
+the same config, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+PROCS = {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2)}
+METRIC = "HPCG CG GFLOP/s (27-pt stencil, 104^3 per GPU)"
+
+
+def procs_for(n: int) -> tuple[int, int, int]:
+    if n in PROCS:
+        return PROCS[n]
+    raise SystemExit(f"unsupported GPU count {n} (use 1, 2, 4 or 8)")
+
+
+def peaks() -> dict:
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            p = json.load(fh)
+        return {"hbm_gbs": float(p["hbm_gbs"]), "source": "measured"}
+    except Exception:
+        return {"hbm_gbs": 6650.0, "source": "fallback"}
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the measurements)
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"samples": 0}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, mx, reasons = [], 0.0, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        loaded = [s for s in sm if s > 0.5 * mx] if mx else []
+        return {"sm_mhz": statistics.median(loaded) if loaded else (statistics.median(sm) if sm else None),
+                "sm_max_mhz": mx or None, "reasons": sorted(reasons), "samples": len(sm),
+                "samples_under_load": len(loaded)}
+
+
+# ---------------------------------------------------------------------------
+# problem setup
+# ---------------------------------------------------------------------------
+
+def flops_per_iter(nnz: int, n: int) -> int:
+    return 2 * nnz + 10 * n
+
+
+def dia_bytes(n: int, ncols: int, ndiags: int) -> int:
+    return 8 * ndiags * n + 8 * ndiags + 8 * ncols + 8 * n
+
+
+def csr_bytes(n: int, ncols: int, nnz: int) -> int:
+    return 12 * nnz + 4 * (n + 1) + 8 * ncols + 8 * n
+
+
+def coo_bytes(n: int, ncols: int, nnz: int) -> int:
+    return 16 * nnz + 8 * ncols + 8 * n
+
+
+def build_rank(ds, spec, rank, dev, local_fmt, remote_fmt):
+    """This rank's partition on the device, split and converted (host setup)."""
+    part = ds.generate_partition(spec, rank, space=ds.MemorySpace.DEVICE, device=dev)
+    prob = ds.PartitionedProblem(spec, [part])
+    split = ds.split_local_remote(prob, 0)
+    ds.convert_inplace(split.local, local_fmt)
+    try:
+        ds.convert_inplace(split.remote, remote_fmt)
+    except ds.DiaFillOverflow:
+        pass  # remote DIA overflows on the stencil: keep CSR like the tuner's skip
+    return part, split
+
+
+# ---------------------------------------------------------------------------
+# SpMV sweeps (config 2 and 4)
+# ---------------------------------------------------------------------------
+
+def time_spmv(ds, torch, m, x, y, warm=20, reps=200):
+    """Median per-launch time (ms) of y = A x, CUDA events on the launch stream."""
+    st = torch.cuda.current_stream()
+    for _ in range(warm):
+        ds.spmv(ds.SERIAL, m, x, y)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(reps)]
+    torch.cuda.synchronize()
+    for e0, e1 in ev:
+        e0.record(st)
+        ds.spmv(ds.SERIAL, m, x, y)
+        e1.record(st)
+    torch.cuda.synchronize()
+    return statistics.median(e0.elapsed_time(e1) for e0, e1 in ev)
+
+
+def sweep_104(ds, torch, a_full, dev, peak):
+    import numpy as np
+    n = a_full.nrows
+    x = ds.DenseVector(torch.from_numpy(np.random.default_rng(0).standard_normal(n)).to(dev))
+    y = ds.DenseVector.zeros(n, ds.MemorySpace.DEVICE, dev)
+    out = {}
+    for name in ("coo", "csr", "dia"):
+        m = ds.convert(a_full, ds.FormatId[name.upper()])
+        ms = time_spmv(ds, torch, m, x, y)
+        nnz = a_full.nnz
+        if name == "csr":
+            b = csr_bytes(n, n, nnz)
+        elif name == "coo":
+            b = coo_bytes(n, n, nnz)
+        else:
+            b = dia_bytes(n, n, m.ndiags)
+        gbs = b / (ms * 1e-3) / 1e9
+        out[name] = {"ms": round(ms, 5), "gflops": round(2 * nnz / (ms * 1e-3) / 1e9, 1),
+                     "gbs": round(gbs, 1), "frac": round(gbs / peak, 3), "bytes": b}
+        del m
+    return out
+
+
+def sweep_powerlaw(ds, torch, dev, peak):
+    """BASELINE config 4: generator of BASELINE.md §2, device conversion, CSR vs
+    COO SpMV, DIA overflow; the tuner's choice is the measured-fastest format."""
+    import numpy as np
+    t0 = time.time()
+    rng = np.random.default_rng(2209)
+    n = 4_194_304
+    L = np.minimum(n, np.floor(6.0 * (1.0 - rng.random(n)) ** (-1 / 1.8))).astype(np.int64)
+    rows = np.repeat(np.arange(n, dtype=np.int64), L)
+    cols = rng.integers(0, n, rows.size)
+    vals = rng.standard_normal(rows.size)
+    gen_s = time.time() - t0
+    coo = ds.CooMatrix(n, n, rows, cols, vals, ds.MemorySpace.DEVICE, dev)
+    del rows, cols, vals
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    csr = ds.convert(coo, ds.FormatId.CSR)
+    torch.cuda.synchronize()
+    conv_ms = (time.perf_counter() - t0) * 1e3
+    del coo
+    ccoo = ds.convert(csr, ds.FormatId.COO)
+    nnz = csr.nnz
+    x = ds.DenseVector(torch.from_numpy(np.random.default_rng(1).standard_normal(n)).to(dev))
+    y = ds.DenseVector.zeros(n, ds.MemorySpace.DEVICE, dev)
+    out = {"nnz": nnz, "host_generate_s": round(gen_s, 2), "convert_coo_to_csr_ms": round(conv_ms, 2)}
+    for name, m, b in (("csr", csr, csr_bytes(n, n, nnz)), ("coo", ccoo, coo_bytes(n, n, nnz))):
+        ms = time_spmv(ds, torch, m, x, y, warm=10, reps=50)
+        gbs = b / (ms * 1e-3) / 1e9
+        out[name] = {"ms": round(ms, 4), "gflops": round(2 * nnz / (ms * 1e-3) / 1e9, 1),
+                     "gbs": round(gbs, 1), "frac": round(gbs / peak, 3)}
+    try:
+        ds.convert(csr, ds.FormatId.DIA)
+        out["dia"] = "converted"
+    except ds.DiaFillOverflow as exc:
+        out["dia"] = f"DiaFillOverflow: {str(exc)[:60]}"
+    out["selected"] = min(("csr", "coo"), key=lambda k: out[k]["ms"])
+    return out
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline (oracle port of the reference), bounded sample
+# ---------------------------------------------------------------------------
+
+def cpu_cg_sample(spec_args, rank_list, iters: int, threads: int) -> dict:
+    """Time ``iters`` CG iterations of the oracle on the host (untimed setup),
+    the reference's own loop (solver.py:170-188) with its threaded backend."""
+    import numpy as np
+    from oracle import dynsparse_oracle as O
+    nx, ny, nz, px, py, pz = spec_args
+    parts = [O.stencil_partition(nx, ny, nz, px, py, pz, r) for r in range(px * py * pz)]
+    splits = []
+    for p in parts:
+        loc, rem = O.split(p)
+        splits.append((O.convert(loc, O.DIA), rem))
+    P = len(parts)
+    n = parts[0].a_full.nrows
+    bs = [p.b for p in parts]
+    # one untimed setup, then time the loop body
+    x = [np.zeros(n) for _ in range(P)]
+    p_full = [np.zeros(n + parts[k].ghost_count) for k in range(P)]
+    p = [pf[:n] for pf in p_full]
+    r = [b.copy() for b in bs]
+    ap = [np.zeros(n) for _ in range(P)]
+    for k in range(P):
+        p[k][:] = r[k]
+    rr = sum(O.dot(r[k], r[k]) for k in range(P))
+    nnz_total = sum(p.a_full.vals.size for p in parts)
+    t0 = time.perf_counter()
+    for _ in range(iters):
+        O.dist_spmv(parts, splits, p_full, ap, nthreads=threads)
+        pap = sum(O.dot(p[k], ap[k]) for k in range(P))
+        alpha = rr / pap
+        for k in range(P):
+            O.waxpby(1.0, x[k], alpha, p[k], x[k])
+            O.waxpby(1.0, r[k], -alpha, ap[k], r[k])
+        rr_new = sum(O.dot(r[k], r[k]) for k in range(P))
+        beta = rr_new / rr
+        for k in range(P):
+            O.waxpby(1.0, r[k], beta, p[k], p[k])
+        rr = rr_new
+    dt = time.perf_counter() - t0
+    fl = iters * flops_per_iter(nnz_total, n * P)
+    return {"value": round(fl / dt / 1e9, 4), "unit": "GFLOP/s", "cores": threads,
+            "kind": "port", "seconds": round(dt, 3),
+            "sample": f"{iters} CG iterations of the oracle (numpy port of the reference), "
+                      f"grid {nx}^3 x {P} partition(s), local DIA + remote CSR, "
+                      f"ExecBackend.threaded({threads}), OPENBLAS_NUM_THREADS="
+                      f"{os.environ.get('OPENBLAS_NUM_THREADS')}"}
+
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------------------
+# reference arm
+# ---------------------------------------------------------------------------
+
+def reference_arm(args, rank: int, world: int) -> int:
+    if rank != 0:
+        return 0
+    threads = host_threads()
+    os.environ["OPENBLAS_NUM_THREADS"] = str(threads)
+    px, py, pz = procs_for(args.gpus)
+    nx = args.nx
+    # bounded sample: enough iterations for ~10-60 s of CPU work
+    iters = max(1, min(args.steps, 10 if world == 1 else 3))
+    res = cpu_cg_sample((nx, nx, nx, px, py, pz), None, iters, threads)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": res["value"], "unit": "GFLOP/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(res["seconds"] / iters * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"hpcg_cg_27pt_{nx}^3_per_gpu", "grid_per_gpu": [nx, nx, nx],
+                   "procs": [px, py, pz], "local_format": "dia", "remote_format": "csr"},
+        "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": res["value"], "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def run(args, rank: int, world: int) -> int:
+    import numpy as np
+    import torch
+
+    import paper_2209_06478_b200 as ds
+    from paper_2209_06478_b200 import solver as S
+
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    pk = peaks()
+    peak = pk["hbm_gbs"]
+    px, py, pz = procs_for(world)
+    nx = args.nx
+    spec = ds.GridSpec(nx, nx, nx, px, py, pz)
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+
+    extras = {}
+    part, split = build_rank(ds, spec, rank, dev, ds.FormatId.DIA, ds.FormatId.CSR)
+    n = part.a_full.nrows
+    nnz_local = part.a_full.nnz
+    if world == 1 and not args.no_sweep:
+        extras["spmv_sweep"] = sweep_104(ds, torch, part.a_full, dev, peak)
+    torch.cuda.synchronize()
+
+    if world == 1:
+        eng, _ = S.build_engine(S.DistributedOperator(ds.PartitionedProblem(spec, [part]), [split]),
+                                [part.b], None, 1e-300, args.warmup + args.steps + 8)
+    else:
+        from paper_2209_06478_b200 import dist as D
+        eng = D.RankCG(spec, part, split, dev, 1e-300, args.warmup + args.steps + 8)
+    st = torch.cuda.current_stream(dev)
+    with torch.cuda.device(dev):
+        eng.setup(st.cuda_stream)
+        use_graph = not args.eager
+        if use_graph:
+            eng.capture_step()
+        step = eng.replay if use_graph else (lambda: eng.step(st.cuda_stream))
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(args.steps):
+            step()
+        e1.record(st)
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        ms = e0.elapsed_time(e1)
+        sc = eng.scalars()
+        state = {"iter": int(sc.iter), "done": int(sc.done)}
+
+        # dominant kernel: time the fused DIA SpMV launches inside eager steps
+        kern = eng.time_spmv_in_steps(min(args.steps, 200), st.cuda_stream)
+
+    clk = clocks.stop()
+    nnz_total, ms_max = nnz_local, ms
+    if world > 1:
+        t = torch.tensor([ms, float(nnz_local)], dtype=torch.float64, device=dev)
+        tmax = t.clone()
+        torch.distributed.all_reduce(tmax, op=torch.distributed.ReduceOp.MAX)
+        tsum = t.clone()
+        torch.distributed.all_reduce(tsum, op=torch.distributed.ReduceOp.SUM)
+        ms_max, nnz_total = float(tmax[0]), int(tsum[1])
+    fl = args.steps * flops_per_iter(nnz_total, n * world)
+    value = fl / (ms_max * 1e-3) / 1e9
+
+    # roofline of the dominant kernel (per launch, algorithmic bytes)
+    lm = eng.parts[0].local if world == 1 else eng.local
+    nd = lm.ndiags if hasattr(lm, "ndiags") else 27
+    kb = dia_bytes(n, n, nd)
+    k_ach = kb / (kern["avg_ms"] * 1e-3) / 1e9 if kern["avg_ms"] > 0 else 0.0
+    roof = {"kernel": "dia_slab_tma (fused p.Ap, CG step)", "bound": "hbm",
+            "achieved": round(k_ach, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(k_ach / peak, 3), "traffic": None, "peak_source": pk["source"],
+            "algorithmic_bytes_per_launch": kb, "avg_launch_ms": round(kern["avg_ms"], 5),
+            "share_of_step": round(kern["avg_ms"] / kern["step_ms"], 3) if kern["step_ms"] else None}
+
+    e2e = None
+    cpu = None
+    if rank == 0 and world == 1:
+        e2e = measure_e2e(ds, torch, spec, split, part, n, nnz_local)
+        if not args.no_cpu:
+            thr = host_threads()
+            os.environ["OPENBLAS_NUM_THREADS"] = str(thr)
+            cpu = cpu_cg_sample((nx, nx, nx, 1, 1, 1), None, 5, thr)
+            cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        if args.powerlaw:
+            extras["powerlaw"] = sweep_powerlaw(ds, torch, dev, peak)
+
+    launches_per_step = eng.launches_per_step()
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 5),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"hpcg_cg_27pt_{nx}^3_per_gpu", "grid_per_gpu": [nx, nx, nx],
+                   "procs": [px, py, pz], "local_format": "dia", "remote_format": "csr",
+                   "flops_per_step": flops_per_iter(nnz_total, n * world),
+                   "graph": not args.eager,
+                   "l2": f"no flush: the DIA matrix ({8 * 27 * n / 1e6:.0f} MB/GPU) exceeds the "
+                         f"126 MB L2 and is re-streamed every step"},
+        "roofline": roof,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clk,
+        "cg_state": state,
+        **extras,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def measure_e2e(ds, torch, spec, split, part, n, nnz, iters=50, reps=3):
+    """cg() through the public API: host b in, host x out (pageable copies),
+    matrix resident on the device; wall clock incl. copies, median of reps."""
+    import numpy as np
+    b_host = ds.DenseVector(part.b.data.cpu().numpy())
+    op = ds.DistributedOperator(ds.PartitionedProblem(spec, [part]), [split])
+    times = []
+    for _ in range(reps + 1):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = ds.cg(ds.SERIAL, op, [b_host], tol=1e-300, max_iters=iters)
+        assert isinstance(res.x[0].data, np.ndarray)
+        times.append(time.perf_counter() - t0)
+    t = statistics.median(times[1:])
+    fl = iters * flops_per_iter(nnz, n)
+    return {"value": round(fl / t / 1e9, 2), "unit": "GFLOP/s", "h2d_bytes_per_step": 8 * n,
+            "d2h_bytes_per_step": 8 * n + 8 * (iters + 1),
+            "step": f"one ds.cg() solve of {iters} iterations from a host b (numpy) to a host x",
+            "seconds": round(t, 5)}
+
+
+def main(argv=None) -> int:
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
+    ap.add_argument("--nx", type=int, default=104)
+    ap.add_argument("--eager", action="store_true", help="no CUDA graph for the step")
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--powerlaw", action="store_true", help="also run BASELINE config 4")
+    args = ap.parse_args(argv)
+    if args.warmup < 3:
+        raise SystemExit("--warmup must be >= 3")
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus and args.impl != "reference":
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.impl == "reference":
+        return reference_arm(args, rank, world)
+    return run(args, rank, world)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -79,6 +79,8 @@ struct DotOut {
   double* history = nullptr;
   const double* parts = nullptr;   // all partitions' dots (result is one of them)
   int nparts_final = 0;            // >0: run cg_finalize(parts, nparts_final)
+  int plus_zero = 0;               // epilogue y = (A x) + 0.0: the exact effect of
+                                   // spmv_add with an EMPTY remote part (kernels.py:196-198)
 
   __host__ __device__ bool fused() const { return partials != nullptr; }
   __device__ __forceinline__ bool skip() const { return guard != nullptr && *guard != 0; }
@@ -109,7 +111,7 @@ int launch_dia(int64_t nrows, int64_t ncols, int ndiags, const int* off, const d
                const double* x, double* y, bool accum, const DotOut* dot, cudaStream_t st);
 int launch_coo(int64_t nrows, int64_t nnz, const int* rows, const int* cols, const double* vals,
                bool sorted, const double* x, double* y, bool accum, const int* guard,
-               cudaStream_t st);
+               cudaStream_t st, bool plus_zero = false);
 // stand-alone fused dot with the same epilogue (used when a SpMV kernel
 // cannot fuse it): result = a[0:n] . b[0:n]
 int launch_dot(int64_t n, const double* a, const double* b, const DotOut& d, cudaStream_t st);

@@ -153,7 +153,8 @@ __global__ void __launch_bounds__(kCsrBlock)
     }
     if (lane8 == 0) {
       const double s = (len > 0) ? add(p0, res) : 0.0;
-      const double out = ACCUM ? add(y[row], s) : s;
+      double out = ACCUM ? add(y[row], s) : s;
+      if (dot.plus_zero) out = add(out, 0.0);
       y[row] = out;
       if (FUSE_DOT) dsum = add(dsum, mul(dot.other[row], out));
     }
@@ -373,7 +374,8 @@ __global__ void __launch_bounds__(kDiaBlock)
       const int c = i + s_off[j];
       if (c >= 0 && c < ncols) acc = add(acc, mul(v[j], ld_gather(x + c)));
     }
-    const double out = ACCUM ? add(y[i], acc) : acc;
+    double out = ACCUM ? add(y[i], acc) : acc;
+    if (dot.plus_zero) out = add(out, 0.0);
     y[i] = out;
     if (FUSE_DOT) dsum = mul(dot.other[i], out);
   }
@@ -397,7 +399,8 @@ __global__ void __launch_bounds__(kDiaBlock)
       const int c = i + __ldg(offsets + j);
       if (c >= 0 && c < ncols) acc = add(acc, mul(v[j], ld_gather(x + c)));
     }
-    const double out = ACCUM ? add(y[i], acc) : acc;
+    double out = ACCUM ? add(y[i], acc) : acc;
+    if (dot.plus_zero) out = add(out, 0.0);
     y[i] = out;
     if (FUSE_DOT) dsum = mul(dot.other[i], out);
   }
@@ -485,14 +488,15 @@ __device__ __forceinline__ int64_t coo_row_start_at_or_after(const int* rows, in
 
 template <bool ACCUM>
 __device__ __forceinline__ void coo_fill_gap(double* y, int from, int to) {
-  for (int r = from; r < to; ++r) y[r] = ACCUM ? add(y[r], 0.0) : 0.0;
+  for (int r = from; r < to; ++r) y[r] = ACCUM ? add(y[r], 0.0) : 0.0;  // +0.0 either way
 }
 
 template <bool ACCUM>
 __global__ void __launch_bounds__(kCooBlock)
     coo_sorted_segments(int nrows, int64_t nnz, const int* __restrict__ rows,
                         const int* __restrict__ cols, const double* __restrict__ vals,
-                        const double* __restrict__ x, double* y, const int* guard) {
+                        const double* __restrict__ x, double* y, const int* guard,
+                        int plus_zero) {
   if (guard && *guard) return;
   __shared__ int s_row[kCooTile];
   __shared__ double s_p[kCooTile];
@@ -568,7 +572,9 @@ __global__ void __launch_bounds__(kCooBlock)
         s_carry = acc;  // row continues in the next tile
         s_carry_row = r;
       } else {
-        y[r] = ACCUM ? add(y[r], acc) : acc;
+        double out = ACCUM ? add(y[r], acc) : acc;
+        if (plus_zero) out = add(out, 0.0);
+        y[r] = out;
       }
     }
     __syncthreads();
@@ -606,16 +612,16 @@ __global__ void axpy_inplace(int64_t n, double* y, const double* t, const int* g
 
 int launch_coo(int64_t nrows, int64_t nnz, const int* rows, const int* cols, const double* vals,
                bool sorted, const double* x, double* y, bool accum, const int* guard,
-               cudaStream_t st) {
+               cudaStream_t st, bool plus_zero) {
   if (nrows == 0) return DS_OK;
   if (sorted) {
     const int64_t blocks = nnz == 0 ? 1 : ceil_div(nnz, kCooPerBlock);
     if (accum)
       coo_sorted_segments<true><<<(unsigned)blocks, kCooBlock, 0, st>>>((int)nrows, nnz, rows,
-                                                                        cols, vals, x, y, guard);
+                                                                        cols, vals, x, y, guard, (int)plus_zero);
     else
       coo_sorted_segments<false><<<(unsigned)blocks, kCooBlock, 0, st>>>((int)nrows, nnz, rows,
-                                                                         cols, vals, x, y, guard);
+                                                                         cols, vals, x, y, guard, (int)plus_zero);
     DS_LAUNCH_CHECK("coo_sorted_segments");
     return DS_OK;
   }
@@ -633,6 +639,8 @@ int launch_coo(int64_t nrows, int64_t nnz, const int* rows, const int* cols, con
     axpy_inplace<<<g, 256, 0, st>>>(nrows, y, target, guard);
     DS_CUDA(cudaFreeAsync(target, st));
   }
+  // atomics start from +0.0, so y + 0.0 is already the identity: plus_zero is free here
+  (void)plus_zero;
   DS_LAUNCH_CHECK("coo_atomic");
   return DS_OK;
 }
@@ -713,7 +721,7 @@ extern "C" int ds_spmv_coo(int64_t nrows, int64_t ncols, int64_t nnz, const int3
     return DS_ERR_NOT_SUPPORTED;
   }
   return launch_coo(nrows, nnz, row_indices, col_indices, values, rows_sorted != 0, x, y,
-                    accumulate != 0, nullptr, as_stream(stream));
+                    accumulate == 1, nullptr, as_stream(stream), accumulate == 2);
 }
 
 extern "C" int ds_coo_order_flags(int64_t nnz, const int32_t* row_indices,

@@ -509,18 +509,20 @@ extern "C" int ds_cg_spmv_dot(const ds_matrix* a, const double* x, double* y, in
   }
   DotOut d;
   d.guard = s ? &s->done : nullptr;
+  d.plus_zero = (accumulate == 2);
   const bool want_dot = dot_with != nullptr;
   DotOut fused;
   if (want_dot) {
     fused = make_dot(workspace, 0, dot_with, dot_out);
     fused.guard = d.guard;
+    fused.plus_zero = d.plus_zero;
     fused.stage = stage;
     fused.s = s;
     fused.history = history;
     fused.parts = parts;
     fused.nparts_final = nparts_final;
   }
-  const bool acc = accumulate != 0;
+  const bool acc = accumulate == 1;
   int rc = DS_OK;
   bool done_dot = false;
   switch (a->format) {
@@ -541,7 +543,7 @@ extern "C" int ds_cg_spmv_dot(const ds_matrix* a, const double* x, double* y, in
     }
     case DS_FMT_COO:
       rc = launch_coo(a->nrows, a->nnz, a->idx0, a->idx1, a->values, a->rows_sorted != 0, x, y,
-                      acc, d.guard, st);
+                      acc, d.guard, st, d.plus_zero != 0);
       break;
     default:
       set_error("unknown format %d", a->format);

@@ -74,7 +74,11 @@ class _Part:
         import torch
         self.local, self.remote, self.n = local, remote, n
         self.d_local = descriptor(local)
-        self.d_remote = descriptor(remote) if remote is not None else None
+        # an EMPTY remote part only turns y into y + 0.0 (kernels.py:196-198):
+        # fold that into the local kernel's epilogue instead of a second pass
+        self.fold_remote = remote is not None and remote.nnz == 0
+        self.d_remote = descriptor(remote) if remote is not None and not self.fold_remote else None
+        self.local_mode = 2 if self.fold_remote else 0
         f64 = dict(dtype=torch.float64, device=device)
         self.p_full = torch.zeros(n + ghosts, **f64)
         self.p = self.p_full[:n]
@@ -119,8 +123,8 @@ class CgEngine:
         self._exchange(stream, guard=None)
         for k, pt in enumerate(self.parts):
             self._ck(lib.ds_cg_spmv_dot(ctypes.byref(pt.d_local), self._p(pt.p_full),
-                                        self._p(pt.ap), 0, None, None, 0, None, None, None, 0,
-                                        self._p(self.ws), stream))
+                                        self._p(pt.ap), pt.local_mode, None, None, 0, None, None,
+                                        None, 0, self._p(self.ws), stream))
             if pt.d_remote is not None:
                 self._ck(lib.ds_cg_spmv_dot(ctypes.byref(pt.d_remote),
                                             self._p(pt.p_full) + 8 * pt.n, self._p(pt.ap), 1,
@@ -144,19 +148,29 @@ class CgEngine:
         P, ws = self.P, self._p(self.ws)
         fin = 1 if P == 1 else 0
         self._exchange(stream, guard=s)
+        marks = getattr(self, "_marks", None)
         for k, pt in enumerate(self.parts):
+            if marks is not None and k == 0:
+                marks[1].record(marks[0])
             if pt.d_remote is None:
                 self._ck(lib.ds_cg_spmv_dot(ctypes.byref(pt.d_local), self._p(pt.p_full),
-                                            self._p(pt.ap), 0, self._p(pt.p), self._dot(2, k),
+                                            self._p(pt.ap), pt.local_mode, self._p(pt.p),
+                                            self._dot(2, k),
                                             PAP, s, hist, self._dot(2, 0), fin, ws, stream))
             else:
                 self._ck(lib.ds_cg_spmv_dot(ctypes.byref(pt.d_local), self._p(pt.p_full),
                                             self._p(pt.ap), 0, None, None, 0, s, None, None, 0,
                                             ws, stream))
+                if marks is not None and k == 0:
+                    marks[2].record(marks[0])
+                    marks = None
                 self._ck(lib.ds_cg_spmv_dot(ctypes.byref(pt.d_remote),
                                             self._p(pt.p_full) + 8 * pt.n, self._p(pt.ap), 1,
                                             self._p(pt.p), self._dot(2, k), PAP, s, hist,
                                             self._dot(2, 0), fin, ws, stream))
+            if marks is not None and k == 0:
+                marks[2].record(marks[0])
+                marks = None
         if not fin:
             self._ck(lib.ds_cg_finalize(PAP, s, hist, self._dot(2, 0), P, stream))
         for k, pt in enumerate(self.parts):
@@ -197,6 +211,46 @@ class CgEngine:
                 sc = self.scalars()
                 if sc.done:
                     return sc
+
+    # benchmarking hooks ---------------------------------------------------
+    def capture_step(self) -> None:
+        """Capture ONE iteration as a CUDA graph (replayed by ``replay``)."""
+        self._capture(1)
+
+    def replay(self) -> None:
+        self.graph.replay()
+
+    def launches_per_step(self) -> int:
+        n = sum(1 for pt in self.parts for h in pt.halo if h[1])
+        for pt in self.parts:
+            n += 1 + (pt.d_remote is not None) + 2      # spmv(s), update, direction
+        return n + (2 if self.P > 1 else 0)              # finalize kernels
+
+    def time_spmv_in_steps(self, steps: int, stream_handle=None) -> dict:
+        """Eager iterations with CUDA events around partition 0's local SpMV
+        launch (the dominant kernel) and around each whole step."""
+        import torch
+        st = torch.cuda.current_stream(self.dev)
+        lib, ws = self.lib, self._p(self.ws)
+        ev = []
+        for _ in range(steps):
+            a, b, c, d = (torch.cuda.Event(enable_timing=True) for _ in range(4))
+            a.record(st)
+            self._step_with_marks(st, b, c)
+            d.record(st)
+            ev.append((a, b, c, d))
+        torch.cuda.synchronize(self.dev)
+        k = [b.elapsed_time(c) for _, b, c, _ in ev]
+        s = [a.elapsed_time(d) for a, _, _, d in ev]
+        del lib, ws
+        return {"avg_ms": sum(k) / len(k), "step_ms": sum(s) / len(s), "launches": len(k)}
+
+    def _step_with_marks(self, st, mark0, mark1) -> None:
+        self._marks = (st, mark0, mark1)
+        try:
+            self.step(st.cuda_stream)
+        finally:
+            self._marks = None
 
     def _capture(self, c: int) -> None:
         import torch
