@@ -356,12 +356,14 @@ def run(args, rank: int, world: int) -> int:
         extras["spmv_sweep"] = sweep_104(ds, torch, part.a_full, dev, peak)
     torch.cuda.synchronize()
 
+    kern_steps = min(args.steps, 200)
+    budget = args.warmup + args.steps + kern_steps + 8   # no step may hit max_iters
     if world == 1:
         eng, _ = S.build_engine(S.DistributedOperator(ds.PartitionedProblem(spec, [part]), [split]),
-                                [part.b], None, 1e-300, args.warmup + args.steps + 8)
+                                [part.b], None, 1e-300, budget)
     else:
         from paper_2209_06478_b200 import dist as D
-        eng = D.RankCG(spec, part, split, dev, 1e-300, args.warmup + args.steps + 8)
+        eng = D.RankCG(spec, part, split, dev, 1e-300, budget)
     st = torch.cuda.current_stream(dev)
     with torch.cuda.device(dev):
         eng.setup(st.cuda_stream)
@@ -388,7 +390,9 @@ def run(args, rank: int, world: int) -> int:
         state = {"iter": int(sc.iter), "done": int(sc.done)}
 
         # dominant kernel: time the fused DIA SpMV launches inside eager steps
-        kern = eng.time_spmv_in_steps(min(args.steps, 200), st.cuda_stream)
+        kern = eng.time_spmv_in_steps(kern_steps, st.cuda_stream)
+        if int(eng.scalars().done) != 0:
+            raise RuntimeError("CG stopped inside the measured steps; timings would be no-ops")
 
     clk = clocks.stop()
     nnz_total, ms_max = nnz_local, ms

@@ -250,10 +250,14 @@ def test_stencil_distributed_spmv_bitwise(K):
 
 
 def _check_history(got, want, it_got, it_want):
+    """Iterations +-1 (test_solver.py:121); history within 1e-8 relative, with
+    an absolute floor of 64 eps: once ||r||/||b|| reaches the rounding floor
+    (~1e-17) both sides hold rounding noise and no relative bar applies."""
     assert abs(it_got - it_want) <= 1
     k = min(len(got), len(want))
     g, w = np.asarray(got[:k]), np.asarray(want[:k])
-    assert np.allclose(g, w, rtol=1e-8, atol=0.0), np.max(np.abs(g - w) / np.maximum(w, 1e-300))
+    tol = 1e-8 * w + 64 * np.finfo(np.float64).eps
+    assert np.all(np.abs(g - w) <= tol), np.max(np.abs(g - w) / np.maximum(w, 1e-300))
 
 
 @pytest.mark.parametrize("use_graph", [False, True])
