@@ -36,6 +36,33 @@ int sm_count() {
   return cache[dev];
 }
 
+int max_dynamic_smem() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 227 * 1024;
+  if (cache[dev] == 0) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess ||
+        v <= 0)
+      v = 227 * 1024;
+    cache[dev] = v;
+  }
+  return cache[dev];
+}
+
+int allow_dynamic_smem(const void* kernel, size_t bytes) {
+  cudaFuncAttributes fa;
+  DS_CUDA(cudaFuncGetAttributes(&fa, kernel));
+  if (fa.maxDynamicSharedSizeBytes >= (int)bytes) return DS_OK;
+  const int room = max_dynamic_smem() - (int)fa.sharedSizeBytes;
+  if ((int)bytes > room) {
+    set_error("kernel needs %zu B of dynamic shared memory, %d available", bytes, room);
+    return DS_ERR_NOT_SUPPORTED;
+  }
+  DS_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, room));
+  return DS_OK;
+}
+
 }  // namespace ds
 
 extern "C" const char* ds_last_error(void) { return ds::g_err; }

@@ -43,6 +43,9 @@ int cuda_fail(cudaError_t e, const char* what);
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 int sm_count();           // cached per device
+int max_dynamic_smem();   // opt-in shared memory per block (bytes), cached per device
+// raise a kernel's dynamic shared-memory limit to `bytes` (minus its static use)
+int allow_dynamic_smem(const void* kernel, size_t bytes);
 constexpr int kWarp = 32;
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }

@@ -2,7 +2,7 @@
 //
 // Replaces the reference's format-dispatched kernels (kernels.py:102-198):
 //   _csr_spmv  kernels.py:102-119   -> csr_rows_g8 (+ csr_long_rows)
-//   _dia_spmv  kernels.py:122-140   -> dia_slab_tma (+ dia_rows_direct)
+//   _dia_spmv  kernels.py:122-140   -> dia_pipe (+ dia_rows_direct)
 //   _coo_spmv  kernels.py:143-163   -> coo_sorted_segments / coo_atomic
 // Results are bitwise equal to the reference (see include/dynsparse_b200.h)
 // except for unsorted COO (atomics; within 1e-13 like the reference's
@@ -13,13 +13,15 @@
 //   CSR: 8 lanes per row (the exact numpy pairwise structure), all loads of a
 //        row issued before the dependent add chain; matrix arrays streamed
 //        with L1::no_allocate, x gathered through L1/L2 (x stays L2-resident).
-//   DIA: the (nrows, ndiags) row-major value slab of a block is moved into
-//        shared memory by ONE 1-D TMA bulk copy (cp.async.bulk + mbarrier,
-//        L2 evict_first); each thread then walks its row from shared memory
-//        (odd row stride in 8-B words -> conflict-free) and gathers x.
+//   DIA: persistent CTAs stream (T rows x ndiags) value slabs into a ring of
+//        shared-memory stages with 1-D TMA bulk copies (cp.async.bulk +
+//        mbarrier, L2 evict_first); each thread walks its row from shared
+//        memory (odd row stride in 8-B words -> conflict-free) and gathers x.
 //   COO: blocks own row-aligned entry ranges; entries are staged to shared
 //        memory with their products, then one thread per row segment sums
 //        sequentially (np.bincount order), carrying across tiles.
+#include <stdlib.h>
+
 #include "ds_common.cuh"
 #include "ds_kernels.cuh"
 
@@ -54,19 +56,16 @@ __device__ __forceinline__ double csr_leaf_g8(const int* __restrict__ col,
   for (int k0 = 0; k0 < rounds; k0 += 4) {
     int c[4];
     double v[4], a[4];
+    // unpredicated loads of a clamped index (m >= 1 here): every lane keeps
+    // 4 col->x chains in flight; products of clamped slots are never used
 #pragma unroll
     for (int kk = 0; kk < 4; ++kk) {
-      const int i = lane8 + 8 * (k0 + kk);
-      const bool ok = (k0 + kk < rounds) && (i < m);
-      c[kk] = ok ? ld_stream(col + base + i) : 0;
-      v[kk] = ok ? ld_stream(val + base + i) : 0.0;
+      const int i = min(lane8 + 8 * (k0 + kk), m - 1);
+      c[kk] = ld_stream(col + base + i);
+      v[kk] = ld_stream(val + base + i);
     }
 #pragma unroll
-    for (int kk = 0; kk < 4; ++kk) {
-      const int i = lane8 + 8 * (k0 + kk);
-      const bool ok = (k0 + kk < rounds) && (i < m);
-      a[kk] = ok ? mul(v[kk], ld_gather(x + c[kk])) : 0.0;
-    }
+    for (int kk = 0; kk < 4; ++kk) a[kk] = mul(v[kk], ld_gather(x + c[kk]));
 #pragma unroll
     for (int kk = 0; kk < 4; ++kk) {
       const int k = k0 + kk;
@@ -333,53 +332,118 @@ int launch_csr(int64_t nrows, const int* off, const int* col, const double* val,
 
 constexpr int kDiaBlock = 256;
 
-// Block = kDiaBlock rows.  The slab values[r0:r0+rows, :] is contiguous
-// (row-major) and lands in shared memory via one TMA bulk copy.
+// Persistent variant: grid = a few CTAs per SM, tile t = blockIdx.x + k*G
+// (static, deterministic schedule).  Each CTA keeps S tiles of T rows in
+// flight: thread 0 issues one 1-D TMA bulk copy per tile into a ring of S
+// shared-memory stages (mbarrier transaction counts signal arrival) and
+// refills a stage as soon as the CTA has finished reading it, so HBM
+// streaming never waits on the x gathers / add chains of the consumers.
+// The fused dot needs only G block partials.
+struct DiaPipeCfg {
+  int T;        // rows per tile (== blockDim.x, even)
+  int S;        // stages
+  int stage_bytes;
+};
+
+__device__ __forceinline__ void dia_issue_tile(const double* __restrict__ vals, int64_t nrows,
+                                               int nd, int T, int64_t t, double* stage,
+                                               uint64_t* bar, uint64_t pol) {
+  const int64_t r0 = t * T;
+  const int rows = (int)min64(T, nrows - r0);
+  const uint32_t bytes = (uint32_t)rows * (uint32_t)nd * 8u;
+  const uint32_t bulk = bytes & ~15u;
+  if (bulk != bytes) stage[bulk / 8] = vals[r0 * nd + bulk / 8];  // before the arrive (release)
+  fence_proxy_async();
+  mbar_arrive_expect_tx(bar, bulk);
+  if (bulk) bulk_g2s(stage, vals + r0 * nd, bulk, bar, pol);
+}
+
 template <bool ACCUM, bool FUSE_DOT, int ND>
-__global__ void __launch_bounds__(kDiaBlock)
-    dia_slab_tma(int nrows, int ncols, int ndiags_rt, const int* __restrict__ offsets,
-                 const double* __restrict__ vals, const double* __restrict__ x, double* y,
-                 DotOut dot) {
+__global__ void __launch_bounds__(256, 1)   // 1 CTA/SM: registers for all 27 gathers in flight
+    dia_pipe(int nrows, int ncols, int ndiags_rt, const int* __restrict__ offsets,
+             const double* __restrict__ vals, const double* __restrict__ x, double* y,
+             DiaPipeCfg cfg, DotOut dot) {
   if (dot.skip()) return;
   extern __shared__ __align__(128) unsigned char smem[];
-  const int ndiags = ND > 0 ? ND : ndiags_rt;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
-  int* s_off = reinterpret_cast<int*>(smem + 16);
-  double* s_val = reinterpret_cast<double*>(smem + 16 + ((ndiags * 4 + 15) & ~15));
+  const int nd = ND > 0 ? ND : ndiags_rt;
+  const int T = cfg.T, S = cfg.S;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);               // <= 8 barriers
+  int* s_off = reinterpret_cast<int*>(smem + 64);
+  unsigned char* stage0 = smem + 64 + ((nd * 4 + 127) & ~127);
   const int tid = threadIdx.x;
-  const int64_t r0 = (int64_t)blockIdx.x * kDiaBlock;
-  const int rows = (int)min64(kDiaBlock, nrows - r0);
-  const uint32_t bytes = (uint32_t)rows * (uint32_t)ndiags * 8u;
-  const uint32_t bulk = bytes & ~15u;
+  const int64_t ntiles = (nrows + T - 1) / T;
+  const int64_t G = gridDim.x;
+  uint64_t pol = 0;
   if (tid == 0) {
-    mbar_init(bar, 1);
+    for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
     fence_barrier_init();
+    pol = policy_evict_first();
   }
+  for (int j = tid; j < nd; j += blockDim.x) s_off[j] = offsets[j];
   __syncthreads();
-  if (tid == 0) {
-    mbar_arrive_expect_tx(bar, bulk);
-    if (bulk) bulk_g2s(s_val, vals + r0 * ndiags, bulk, bar, policy_evict_first());
-    if (bulk != bytes) s_val[bulk / 8] = vals[r0 * ndiags + bulk / 8];
-  }
-  for (int j = tid; j < ndiags; j += kDiaBlock) s_off[j] = offsets[j];
-  __syncthreads();
-  mbar_wait(bar, 0);
-  double dsum = 0.0;
-  if (tid < rows) {
-    const int i = (int)r0 + tid;
-    const double* v = s_val + (size_t)tid * ndiags;
-    double acc = 0.0;
-#pragma unroll(ND > 0 ? ND : 9)
-    for (int j = 0; j < ndiags; ++j) {
-      const int c = i + s_off[j];
-      if (c >= 0 && c < ncols) acc = add(acc, mul(v[j], ld_gather(x + c)));
+  if (tid == 0)
+    for (int s = 0; s < S; ++s) {
+      const int64_t t = blockIdx.x + s * G;
+      if (t < ntiles)
+        dia_issue_tile(vals, nrows, nd, T, t,
+                       reinterpret_cast<double*>(stage0 + (size_t)s * cfg.stage_bytes), &full[s],
+                       pol);
     }
-    double out = ACCUM ? add(y[i], acc) : acc;
-    if (dot.plus_zero) out = add(out, 0.0);
-    y[i] = out;
-    if (FUSE_DOT) dsum = mul(dot.other[i], out);
+  double dsum = 0.0;
+  int s = 0;
+  uint32_t ph = 0;
+  for (int64_t t = blockIdx.x; t < ntiles; t += G) {
+    const double* v_stage = reinterpret_cast<const double*>(stage0 + (size_t)s * cfg.stage_bytes);
+    mbar_wait(&full[s], ph);
+    const int64_t r0 = t * T;
+    const int rows = (int)min64(T, nrows - r0);
+    if (tid < rows) {
+      const int i = (int)r0 + tid;
+      const double* v = v_stage + (size_t)tid * nd;
+      // Unpredicated gathers (clamped index) so all nd loads are in flight at
+      // once; out-of-range slots contribute a selected +0.0.  acc starts at
+      // +0.0 and can never become -0.0 (x + (-x) rounds to +0.0), so adding
+      // +0.0 is the identity: bitwise equal to skipping the slot
+      // (kernels.py:133-138).
+      double xv[ND > 0 ? ND : 1];
+      double acc = 0.0;
+      if (ND > 0) {
+#pragma unroll
+        for (int j = 0; j < ND; ++j) {
+          const int c = i + s_off[j];
+          xv[j] = ld_gather(x + min(max(c, 0), ncols - 1));
+        }
+#pragma unroll
+        for (int j = 0; j < ND; ++j) {
+          const int c = i + s_off[j];
+          const double pr = mul(v[j], xv[j]);
+          acc = add(acc, (c >= 0 && c < ncols) ? pr : 0.0);
+        }
+      } else {
+        for (int j = 0; j < nd; ++j) {
+          const int c = i + s_off[j];
+          if (c >= 0 && c < ncols) acc = add(acc, mul(v[j], ld_gather(x + c)));
+        }
+      }
+      double out = ACCUM ? add(y[i], acc) : acc;
+      if (dot.plus_zero) out = add(out, 0.0);
+      y[i] = out;
+      if (FUSE_DOT) dsum = add(dsum, mul(dot.other[i], out));
+    }
+    __syncthreads();  // stage s fully consumed
+    if (tid == 0) {
+      const int64_t tn = t + (int64_t)S * G;
+      if (tn < ntiles)
+        dia_issue_tile(vals, nrows, nd, T, tn,
+                       reinterpret_cast<double*>(stage0 + (size_t)s * cfg.stage_bytes), &full[s],
+                       pol);
+    }
+    if (++s == S) {
+      s = 0;
+      ph ^= 1u;
+    }
   }
-  if (FUSE_DOT) dot.finish_block<kDiaBlock>(dsum);
+  if (FUSE_DOT) dot.finish_block<256>(dsum);
 }
 
 // Fallback when the slab cannot be staged (huge ndiags or misaligned base):
@@ -408,22 +472,36 @@ __global__ void __launch_bounds__(kDiaBlock)
 }
 
 template <bool A, bool F, int ND>
-static int dia_tma_launch(int64_t nrows, int64_t ncols, int ndiags, const int* off,
-                          const double* val, const double* x, double* y, DotOut d,
-                          size_t smem, cudaStream_t st) {
-  auto k = dia_slab_tma<A, F, ND>;
-  static bool attr_set[64] = {};  // per device
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (!attr_set[dev & 63]) {
-    DS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr_set[dev & 63] = true;
-  }
-  const int64_t blocks = ceil_div(nrows, kDiaBlock);
-  k<<<(unsigned)blocks, kDiaBlock, smem, st>>>((int)nrows, (int)ncols, ndiags, off, val, x, y,
-                                               d);
-  DS_LAUNCH_CHECK("dia_slab_tma");
+static int dia_pipe_launch(int64_t nrows, int64_t ncols, int ndiags, const int* off,
+                           const double* val, const double* x, double* y, DotOut d,
+                           DiaPipeCfg cfg, size_t smem, int64_t grid, cudaStream_t st) {
+  auto k = dia_pipe<A, F, ND>;
+  int rc = allow_dynamic_smem(reinterpret_cast<const void*>(k), smem);
+  if (rc) return rc;
+  k<<<(unsigned)grid, cfg.T, smem, st>>>((int)nrows, (int)ncols, ndiags, off, val, x, y, cfg, d);
+  DS_LAUNCH_CHECK("dia_pipe");
   return DS_OK;
+}
+
+// tile shape: env DS_DIA_T / DS_DIA_S / DS_DIA_CTAS override (tuning only)
+static void dia_shape(int ndiags, int* T, int* S, int* ctas) {
+  static int eT = -2, eS = -2, eC = -2;
+  if (eT == -2) {
+    const char* a = getenv("DS_DIA_T");
+    const char* b = getenv("DS_DIA_S");
+    const char* c = getenv("DS_DIA_CTAS");
+    eT = a ? atoi(a) : -1;
+    eS = b ? atoi(b) : -1;
+    eC = c ? atoi(c) : -1;
+  }
+  *T = 256;
+  *S = 3;
+  *ctas = 1;
+  // keep each stage <= ~64 KB
+  while (*T > 32 && (int64_t)(*T) * ndiags * 8 > 64 * 1024) *T /= 2;
+  if (eT > 0) *T = eT;
+  if (eS > 0) *S = eS;
+  if (eC > 0) *ctas = eC;
 }
 
 int launch_dia(int64_t nrows, int64_t ncols, int ndiags, const int* off, const double* val,
@@ -431,25 +509,34 @@ int launch_dia(int64_t nrows, int64_t ncols, int ndiags, const int* off, const d
   if (nrows == 0) return DS_OK;
   DotOut d = dot ? *dot : DotOut{};
   const bool fuse = d.fused();
-  const size_t smem = 16 + ((ndiags * 4 + 15) & ~15) + (size_t)kDiaBlock * ndiags * 8;
   const bool aligned = (reinterpret_cast<uintptr_t>(val) & 15) == 0;
+  int T, S, ctas;
+  dia_shape(ndiags, &T, &S, &ctas);
+  const int stage_bytes = (int)((((int64_t)T * ndiags * 8) + 127) & ~127ll);
+  const size_t smem = 64 + ((ndiags * 4 + 127) & ~127) + (size_t)S * stage_bytes;
+  if (aligned && ndiags > 0 && S <= 8 && T >= 32 && smem <= (size_t)max_dynamic_smem() - 1024) {
+    const int64_t ntiles = ceil_div(nrows, T);
+    int64_t grid = (int64_t)sm_count() * ctas;
+    if (grid > ntiles) grid = ntiles;
+    if (fuse) grid = d.clamp_grid(grid);
+    DiaPipeCfg cfg{T, S, stage_bytes};
+#define DS_DIAP(A, F)                                                                           \
+  return (ndiags == 27)                                                                         \
+             ? dia_pipe_launch<A, F, 27>(nrows, ncols, ndiags, off, val, x, y, d, cfg, smem,    \
+                                         grid, st)                                              \
+             : dia_pipe_launch<A, F, 0>(nrows, ncols, ndiags, off, val, x, y, d, cfg, smem,     \
+                                        grid, st)
+    if (accum) {
+      if (fuse) DS_DIAP(true, true); else DS_DIAP(true, false);
+    } else {
+      if (fuse) DS_DIAP(false, true); else DS_DIAP(false, false);
+    }
+#undef DS_DIAP
+  }
   const int64_t blocks = ceil_div(nrows, kDiaBlock);
   if (fuse && d.clamp_grid(blocks) != blocks) {
     set_error("fused dot grid too large");
     return DS_ERR_NOT_SUPPORTED;
-  }
-  if (aligned && ndiags > 0 && smem <= 200 * 1024) {
-#define DS_DIA(A, F)                                                                       \
-  return (ndiags == 27) ? dia_tma_launch<A, F, 27>(nrows, ncols, ndiags, off, val, x, y, d, \
-                                                  smem, st)                                 \
-                        : dia_tma_launch<A, F, 0>(nrows, ncols, ndiags, off, val, x, y, d,  \
-                                                 smem, st)
-    if (accum) {
-      if (fuse) DS_DIA(true, true); else DS_DIA(true, false);
-    } else {
-      if (fuse) DS_DIA(false, true); else DS_DIA(false, false);
-    }
-#undef DS_DIA
   }
 #define DS_DIAD(A, F)                                                                   \
   dia_rows_direct<A, F><<<(unsigned)blocks, kDiaBlock, 0, st>>>((int)nrows, (int)ncols, \

@@ -247,6 +247,9 @@ __global__ void cg_setup_finalize_kernel(ds_cg_scalars* s, const double* bb_part
 }
 
 // x = 1*x + alpha*p ; r = 1*r + (-alpha)*ap ; partial r.r   (solver.py:177-180)
+// VEC: 16-B aligned operands, element pairs per thread (LDG.128); the odd
+// tail element is folded in by the first thread after its pairs.
+template <bool VEC>
 __global__ void __launch_bounds__(kVecBlock)
     cg_update_kernel(int64_t n, double* x, double* r, const double* __restrict__ p,
                      const double* __restrict__ ap, const ds_cg_scalars* s, DotOut d) {
@@ -254,25 +257,84 @@ __global__ void __launch_bounds__(kVecBlock)
   const double alpha = s->alpha;
   const double nalpha = -alpha;
   double v = 0.0;
-  for (int64_t i = (int64_t)blockIdx.x * kVecBlock + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * kVecBlock) {
-    x[i] = add(mul(1.0, x[i]), mul(alpha, p[i]));
-    const double ri = add(mul(1.0, r[i]), mul(nalpha, ap[i]));
-    r[i] = ri;
-    v = add(v, mul(ri, ri));
+  const int64_t gtid = (int64_t)blockIdx.x * kVecBlock + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * kVecBlock;
+  if (VEC) {
+    const int64_t n2 = n >> 1;
+    double2* x2 = reinterpret_cast<double2*>(x);
+    double2* r2 = reinterpret_cast<double2*>(r);
+    const double2* p2 = reinterpret_cast<const double2*>(p);
+    const double2* a2 = reinterpret_cast<const double2*>(ap);
+    for (int64_t i = gtid; i < n2; i += stride) {
+      const double2 xv = x2[i], rv = r2[i], pv = p2[i], av = a2[i];
+      double2 xo, ro;
+      xo.x = add(mul(1.0, xv.x), mul(alpha, pv.x));
+      xo.y = add(mul(1.0, xv.y), mul(alpha, pv.y));
+      ro.x = add(mul(1.0, rv.x), mul(nalpha, av.x));
+      ro.y = add(mul(1.0, rv.y), mul(nalpha, av.y));
+      x2[i] = xo;
+      r2[i] = ro;
+      v = add(v, mul(ro.x, ro.x));
+      v = add(v, mul(ro.y, ro.y));
+    }
+    if ((n & 1) && gtid == 0) {
+      const int64_t i = n - 1;
+      x[i] = add(mul(1.0, x[i]), mul(alpha, p[i]));
+      const double ri = add(mul(1.0, r[i]), mul(nalpha, ap[i]));
+      r[i] = ri;
+      v = add(v, mul(ri, ri));
+    }
+  } else {
+    for (int64_t i = gtid; i < n; i += stride) {
+      x[i] = add(mul(1.0, x[i]), mul(alpha, p[i]));
+      const double ri = add(mul(1.0, r[i]), mul(nalpha, ap[i]));
+      r[i] = ri;
+      v = add(v, mul(ri, ri));
+    }
   }
   d.finish_block<kVecBlock>(v);
 }
 
 // p = 1*r + beta*p  (solver.py:185-188)
+template <bool VEC>
 __global__ void __launch_bounds__(kVecBlock)
     cg_direction_kernel(int64_t n, const double* __restrict__ r, double* p,
                         const ds_cg_scalars* s) {
   if (s->done) return;
   const double beta = s->beta;
-  for (int64_t i = (int64_t)blockIdx.x * kVecBlock + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * kVecBlock)
-    p[i] = add(mul(1.0, r[i]), mul(beta, p[i]));
+  const int64_t gtid = (int64_t)blockIdx.x * kVecBlock + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * kVecBlock;
+  if (VEC) {
+    const int64_t n2 = n >> 1;
+    const double2* r2 = reinterpret_cast<const double2*>(r);
+    double2* p2 = reinterpret_cast<double2*>(p);
+    for (int64_t i = gtid; i < n2; i += stride) {
+      const double2 rv = r2[i], pv = p2[i];
+      double2 o;
+      o.x = add(mul(1.0, rv.x), mul(beta, pv.x));
+      o.y = add(mul(1.0, rv.y), mul(beta, pv.y));
+      p2[i] = o;
+    }
+    if ((n & 1) && gtid == 0) p[n - 1] = add(mul(1.0, r[n - 1]), mul(beta, p[n - 1]));
+  } else {
+    for (int64_t i = gtid; i < n; i += stride) p[i] = add(mul(1.0, r[i]), mul(beta, p[i]));
+  }
+}
+
+static bool aligned16(const void* a, const void* b = nullptr, const void* c = nullptr,
+                      const void* d = nullptr) {
+  auto ok = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  return ok(a) && ok(b) && ok(c) && ok(d);
+}
+
+// grid of the streaming vector kernels: enough CTAs for ~4 pairs per thread,
+// at most 8 per SM (G partials for the fused reductions)
+static unsigned vec_grid(int64_t n) {
+  int64_t g = ceil_div(n, (int64_t)kVecBlock * 8);
+  const int64_t cap = (int64_t)sm_count() * 8;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (unsigned)g;
 }
 
 __global__ void cg_finalize_kernel(int stage, ds_cg_scalars* s, double* history,
@@ -599,10 +661,11 @@ extern "C" int ds_cg_update(int64_t n, double* x, double* r, const double* p, co
   d.history = history;
   d.parts = parts;
   d.nparts_final = nparts_final;
-  int64_t g = ceil_div(n, (int64_t)kVecBlock * 8);
-  if (g < 1) g = 1;
-  if (g > 1024) g = 1024;
-  cg_update_kernel<<<(unsigned)g, kVecBlock, 0, st>>>(n, x, r, p, ap, s, d);
+  const unsigned g = vec_grid(n);
+  if (aligned16(x, r, p, ap))
+    cg_update_kernel<true><<<g, kVecBlock, 0, st>>>(n, x, r, p, ap, s, d);
+  else
+    cg_update_kernel<false><<<g, kVecBlock, 0, st>>>(n, x, r, p, ap, s, d);
   DS_LAUNCH_CHECK("cg_update_kernel");
   return DS_OK;
 }
@@ -610,7 +673,11 @@ extern "C" int ds_cg_update(int64_t n, double* x, double* r, const double* p, co
 extern "C" int ds_cg_direction(int64_t n, const double* r, double* p, const ds_cg_scalars* s,
                                void* stream) {
   if (n <= 0) return DS_OK;
-  cg_direction_kernel<<<grid_for(n), kVecBlock, 0, as_stream(stream)>>>(n, r, p, s);
+  const unsigned g = vec_grid(n);
+  if (aligned16(r, p))
+    cg_direction_kernel<true><<<g, kVecBlock, 0, as_stream(stream)>>>(n, r, p, s);
+  else
+    cg_direction_kernel<false><<<g, kVecBlock, 0, as_stream(stream)>>>(n, r, p, s);
   DS_LAUNCH_CHECK("cg_direction_kernel");
   return DS_OK;
 }

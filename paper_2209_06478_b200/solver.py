@@ -24,6 +24,7 @@ finalize kernel); dist.py runs one partition per process over NCCL.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -76,7 +77,8 @@ class _Part:
         self.d_local = descriptor(local)
         # an EMPTY remote part only turns y into y + 0.0 (kernels.py:196-198):
         # fold that into the local kernel's epilogue instead of a second pass
-        self.fold_remote = remote is not None and remote.nnz == 0
+        self.fold_remote = (remote is not None and remote.nnz == 0
+                            and not os.environ.get("DS_NO_FOLD"))
         self.d_remote = descriptor(remote) if remote is not None and not self.fold_remote else None
         self.local_mode = 2 if self.fold_remote else 0
         f64 = dict(dtype=torch.float64, device=device)
@@ -354,7 +356,8 @@ def build_engine(op: DistributedOperator, bs, x0s, tol, max_iters) -> tuple[CgEn
             if x0s is not None:
                 pt.x.copy_(to_device(x0s[k], dev).data)
                 pt.p.copy_(pt.x)
-            pt.halo = [(q, cnt, idx, n + start)
+            # recv starts are absolute slots (n + ghost index) into p_full
+            pt.halo = [(q, cnt, idx, start)
                        for q, cnt, idx, start in device_halo(part, dev) if cnt]
             parts.append(pt)
     return CgEngine(parts, dev, tol, max_iters), parts

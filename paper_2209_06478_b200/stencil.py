@@ -231,7 +231,8 @@ def split_local_remote(problem: PartitionedProblem, partition: int) -> SplitMatr
 # ---------------------------------------------------------------------------
 
 def device_halo(part: PartitionData, device):
-    """[(neighbor, count, send_idx int32 tensor, recv_start)] on ``device``.
+    """[(neighbor, count, send_idx int32 tensor, recv_start)] on ``device``;
+    recv_start is the ABSOLUTE slot (>= n) of the neighbour's first ghost.
     Recv slots are one contiguous slice per neighbour (ghosts are numbered by
     owner), so the gather writes straight into x[n + start : ...]."""
     import torch
