@@ -358,11 +358,15 @@ def run(args, rank: int, world: int) -> int:
 
     kern_steps = min(args.steps, 200)
     budget = args.warmup + args.steps + kern_steps + 8   # no step may hit max_iters
-    if world == 1:
+    if world == 1 and not args.rank_engine:
         eng, _ = S.build_engine(S.DistributedOperator(ds.PartitionedProblem(spec, [part]), [split]),
                                 [part.b], None, 1e-300, budget)
     else:
         from paper_2209_06478_b200 import dist as D
+        if world == 1 and not torch.distributed.is_initialized():
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            torch.distributed.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
         eng = D.RankCG(spec, part, split, dev, 1e-300, budget)
     st = torch.cuda.current_stream(dev)
     with torch.cuda.device(dev):
@@ -407,7 +411,7 @@ def run(args, rank: int, world: int) -> int:
     value = fl / (ms_max * 1e-3) / 1e9
 
     # roofline of the dominant kernel (per launch, algorithmic bytes)
-    lm = eng.parts[0].local if world == 1 else eng.local
+    lm = eng.local if hasattr(eng, "local") else eng.parts[0].local
     nd = lm.ndiags if hasattr(lm, "ndiags") else 27
     kb = dia_bytes(n, n, nd)
     k_ach = kb / (kern["avg_ms"] * 1e-3) / 1e9 if kern["avg_ms"] > 0 else 0.0
@@ -447,11 +451,12 @@ def run(args, rank: int, world: int) -> int:
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk,
         "cg_state": state,
+        "engine": type(eng).__name__ + ("+graph" if getattr(eng, "graph", None) is not None else ""),
         **extras,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if torch.distributed.is_initialized():
         torch.distributed.destroy_process_group()
     return 0
 
@@ -488,6 +493,8 @@ def main(argv=None) -> int:
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--powerlaw", action="store_true", help="also run BASELINE config 4")
+    ap.add_argument("--rank-engine", action="store_true",
+                    help="at N=1 use the NCCL one-partition-per-process engine (dist.RankCG)")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")

@@ -234,6 +234,24 @@ int ds_cg_finalize(int stage, ds_cg_scalars* s, double* history, const double* p
 int ds_cg_gather(int64_t count, const int32_t* idx, const double* src, double* dst,
                  const ds_cg_scalars* s, void* stream);
 
+/* ---- one partition per process: NCCL halo exchange + global dots --------
+ * (stencil.py:280-295 / solver.py:140-141 across processes).  NCCL is
+ * resolved at run time from the libnccl.so.2 already loaded in the process.
+ * The unique id is created on rank 0 and broadcast by the caller.          */
+int ds_nccl_unique_id_bytes(void);
+int ds_nccl_unique_id(char* out, int nbytes);
+int ds_nccl_comm_init(const char* id_bytes, int nranks, int rank, void** comm);
+int ds_nccl_comm_destroy(void* comm);
+/* For each neighbour q (ascending rank): gather x_full[send_idx[q][k]] into
+ * send_bufs[q] (skipped when *guard != 0), then in one NCCL group send it to
+ * peers[q] and receive recv_counts[q] doubles into x_full + recv_starts[q]. */
+int ds_halo_exchange(int nnbr, const int32_t* peers, const int64_t* send_counts,
+                     const int32_t* const* send_idx, double* const* send_bufs,
+                     const int64_t* recv_counts, const int64_t* recv_starts, double* x_full,
+                     const int32_t* guard, void* comm, void* stream);
+/* recv[r*count : (r+1)*count] = rank r's send (ncclAllGather, float64).   */
+int ds_allgather_f64(const double* send, double* recv, int64_t count, void* comm, void* stream);
+
 /* ---- DIA diagonal column helpers (kernels.py:258-262, 325-330) --------- */
 /* direction 0: out[i] = values[i*ndiags + j0] (i < n); 1: values[...] = d[i] */
 int ds_dia_diag_column(int64_t n, int32_t ndiags, int32_t j0, double* values, double* vec,

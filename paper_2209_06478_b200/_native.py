@@ -106,6 +106,13 @@ _SIGNATURES = {
     "ds_cg_direction": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp]),
     "ds_cg_finalize": (c_int, [c_int, c_vp, c_vp, c_vp, c_int, c_vp]),
     "ds_cg_gather": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "ds_nccl_unique_id_bytes": (c_int, []),
+    "ds_nccl_unique_id": (c_int, [ctypes.c_char_p, c_int]),
+    "ds_nccl_comm_init": (c_int, [ctypes.c_char_p, c_int, c_int, ctypes.POINTER(c_vp)]),
+    "ds_nccl_comm_destroy": (c_int, [c_vp]),
+    "ds_halo_exchange": (c_int, [c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                 c_vp]),
+    "ds_allgather_f64": (c_int, [c_vp, c_vp, c_i64, c_vp, c_vp]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)

@@ -173,6 +173,35 @@ def _partition(spec: GridSpec, rank: int) -> PartitionData:
         local_to_global=gx + gnx * (gy + gny * gz), ghost_to_global=g2g)
 
 
+def halo_send_lists(spec: GridSpec, rank: int) -> dict[int, np.ndarray]:
+    """What this rank must SEND each neighbour: q's ghosts owned by ``rank``.
+
+    The stencil is symmetric, so my point i is a ghost of q iff one of i's
+    27 neighbours is owned by q; q numbers its ghosts by (owner, owner-local)
+    ascending (stencil.py:198-209), so the list is my local indices in
+    ascending order -- exactly q's HaloExchange.send_local_indices for me
+    (stencil.py:221-230), computed without generating q's partition."""
+    nx, ny, nz, px, py, pz = spec.nx, spec.ny, spec.nz, spec.px, spec.py, spec.pz
+    gnx, gny, gnz = spec.global_dims
+    n = spec.local_points
+    cx, cy, cz = rank % px, (rank // px) % py, rank // (px * py)
+    ids = np.arange(n, dtype=np.int64)
+    gx = ids % nx + cx * nx
+    gy = (ids // nx) % ny + cy * ny
+    gz = ids // (nx * ny) + cz * nz
+    per_owner: dict[int, list[np.ndarray]] = {}
+    for dx, dy, dz in _STEPS:
+        tx, ty, tz = gx + dx, gy + dy, gz + dz
+        ok = (tx >= 0) & (tx < gnx) & (ty >= 0) & (ty < gny) & (tz >= 0) & (tz < gnz)
+        owner = (tx // nx) + px * ((ty // ny) + py * (tz // nz))
+        far = ok & (owner != rank)
+        if not far.any():
+            continue
+        for q in np.unique(owner[far]).tolist():
+            per_owner.setdefault(int(q), []).append(ids[far & (owner == q)])
+    return {q: np.unique(np.concatenate(v)) for q, v in sorted(per_owner.items())}
+
+
 def _to_space(part: PartitionData, space, device) -> PartitionData:
     if space is None or MemorySpace(space) == MemorySpace.HOST:
         return part
