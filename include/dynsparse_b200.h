@@ -62,8 +62,10 @@ int ds_device_sm_count(int* out);
 int ds_csr_analyze(int64_t nrows, const int32_t* row_offsets, int32_t* long_rows,
                    int64_t* n_long, int32_t* max_row_len, void* stream);
 
-/* long_rows may be NULL (then every row is handled in-line, correct but slow
- * for rows > 129).  n_long is the count from ds_csr_analyze.                */
+/* long_rows may be NULL: the matrix is then treated as un-analysed and every
+ * row is handled in-line (correct, slower).  A non-NULL long_rows (even with
+ * n_long == 0) enables the TMA-tiled kernel, which leaves rows > 129 entries
+ * to a CTA-per-row kernel.  n_long is the count from ds_csr_analyze.        */
 int ds_spmv_csr(int64_t nrows, int64_t ncols, int64_t nnz, const int32_t* row_offsets,
                 const int32_t* col_indices, const double* values,
                 const int32_t* long_rows, int64_t n_long,

@@ -104,7 +104,7 @@ struct DotOut {
 };
 
 // launchers shared between translation units
-int launch_csr(int64_t nrows, const int* off, const int* col, const double* val,
+int launch_csr(int64_t nrows, int64_t nnz, const int* off, const int* col, const double* val,
                const int* long_rows, int64_t n_long, const double* x, double* y, bool accum,
                const DotOut* dot, cudaStream_t st);
 int launch_dia(int64_t nrows, int64_t ncols, int ndiags, const int* off, const double* val,

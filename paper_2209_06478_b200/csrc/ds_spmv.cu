@@ -90,6 +90,62 @@ __device__ __forceinline__ double csr_leaf_g8(const int* __restrict__ col,
   return res;
 }
 
+// Short-row leaf (m <= 32: one batch of 4 rounds) split into phases so two
+// rows can be interleaved: all loads of both rows are issued before either
+// row's dependent gathers and adds.
+struct ShortLeaf {
+  int c[4];
+  double v[4];
+  double a[4];
+  int c0;
+  double v0;
+};
+
+__device__ __forceinline__ void short_leaf_load(const int* __restrict__ col,
+                                                const double* __restrict__ val, int start,
+                                                int len, int lane8, ShortLeaf& L) {
+  const int m = len - 1;  // addends after p[first]
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) {
+    const int i = max(min(lane8 + 8 * kk, m - 1), 0);   // clamped: always in the row
+    L.c[kk] = ld_stream(col + start + 1 + i);
+    L.v[kk] = ld_stream(val + start + 1 + i);
+  }
+  L.c0 = ld_stream(col + start);
+  L.v0 = ld_stream(val + start);
+}
+
+__device__ __forceinline__ void short_leaf_gather(const double* __restrict__ x, ShortLeaf& L) {
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) L.a[kk] = mul(L.v[kk], ld_gather(x + L.c[kk]));
+  L.v0 = mul(L.v0, ld_gather(x + L.c0));   // p[first]
+}
+
+// y-value of a row with 1 <= len <= 33 (bitwise np.add.reduceat order)
+__device__ __forceinline__ double short_leaf_finish(int len, int lane8, unsigned mask,
+                                                    const ShortLeaf& L) {
+  const int m = len - 1;
+  const int full = m & ~7, nfull = full >> 3;
+  double r = 0.0, tail = 0.0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (k < nfull) r = (k == 0) ? L.a[k] : add(r, L.a[k]);
+    else if (k == nfull) tail = L.a[k];
+  }
+  double res;
+  if (full > 0) {
+    r = add(r, __shfl_xor_sync(mask, r, 1, 8));
+    r = add(r, __shfl_xor_sync(mask, r, 2, 8));
+    r = add(r, __shfl_xor_sync(mask, r, 4, 8));
+    res = r;
+  } else {
+    res = -0.0;
+  }
+  const int ntail = m - full;
+  for (int t = 0; t < ntail; ++t) res = add(res, __shfl_sync(mask, tail, t, 8));
+  return add(L.v0, res);
+}
+
 // Recursion for m > 128 by one 8-lane group (no plan): group-uniform DFS.
 __device__ double csr_group_pairwise(const int* __restrict__ col, const double* __restrict__ val,
                                      const double* __restrict__ x, int64_t base, int64_t m,
@@ -125,7 +181,38 @@ __device__ double csr_group_pairwise(const int* __restrict__ col, const double* 
 constexpr int kCsrBlock = 256;
 constexpr int kLongRow = 129;  // rows longer than this need the recursion
 
-// One 8-lane group per row; grid-stride over row groups.
+// One 8-lane group per PAIR of consecutive rows; grid-stride over pairs.
+// Rows of <= 33 entries (the stencil's 8..27, the power-law's typical 6..33)
+// take the interleaved fast path; longer ones the general leaf / recursion.
+template <bool ACCUM, bool SKIP_LONG, bool FUSE_DOT>
+__device__ __forceinline__ void csr_emit(int row, int len, double sres, double* y,
+                                         const DotOut& dot, double& dsum) {
+  double out = ACCUM ? add(y[row], sres) : sres;
+  if (dot.plus_zero) out = add(out, 0.0);
+  y[row] = out;
+  if (FUSE_DOT) dsum = add(dsum, mul(dot.other[row], out));
+}
+
+template <bool ACCUM, bool SKIP_LONG, bool FUSE_DOT>
+__device__ __forceinline__ void csr_row_general(int row, int start, int len,
+                                                const int* __restrict__ col,
+                                                const double* __restrict__ val,
+                                                const double* __restrict__ x, double* y,
+                                                int lane8, unsigned mask, const DotOut& dot,
+                                                double& dsum) {
+  if (SKIP_LONG && len > kLongRow) return;  // the long-row kernel owns it
+  double res = 0.0, p0 = 0.0;
+  if (len > 0) {
+    if (lane8 == 0) p0 = mul(ld_stream(val + start), ld_gather(x + ld_stream(col + start)));
+    if (len <= kLongRow)
+      res = csr_leaf_g8(col, val, x, (int64_t)start + 1, len - 1, lane8, mask);
+    else
+      res = csr_group_pairwise(col, val, x, (int64_t)start + 1, len - 1, lane8, mask);
+  }
+  if (lane8 == 0) csr_emit<ACCUM, SKIP_LONG, FUSE_DOT>(row, len, len > 0 ? add(p0, res) : 0.0,
+                                                      y, dot, dsum);
+}
+
 template <bool ACCUM, bool SKIP_LONG, bool FUSE_DOT>
 __global__ void __launch_bounds__(kCsrBlock)
     csr_rows_g8(int nrows, const int* __restrict__ off, const int* __restrict__ col,
@@ -135,30 +222,288 @@ __global__ void __launch_bounds__(kCsrBlock)
   const int lane8 = threadIdx.x & 7;
   const unsigned mask = 0xffu << (threadIdx.x & 24);
   const int groups_per_grid = (gridDim.x * kCsrBlock) >> 3;
+  const int npairs = (nrows + 1) >> 1;
   double dsum = 0.0;
-  for (int row = (blockIdx.x * kCsrBlock + threadIdx.x) >> 3; row < nrows;
-       row += groups_per_grid) {
-    const int start = __ldg(off + row);
-    const int end = __ldg(off + row + 1);
-    const int len = end - start;
-    if (SKIP_LONG && len > kLongRow) continue;  // the long-row kernel owns it
-    double res = 0.0, p0 = 0.0;
-    if (len > 0) {
-      if (lane8 == 0) p0 = mul(ld_stream(val + start), ld_gather(x + ld_stream(col + start)));
-      if (len <= kLongRow)
-        res = csr_leaf_g8(col, val, x, (int64_t)start + 1, len - 1, lane8, mask);
-      else
-        res = csr_group_pairwise(col, val, x, (int64_t)start + 1, len - 1, lane8, mask);
-    }
-    if (lane8 == 0) {
-      const double s = (len > 0) ? add(p0, res) : 0.0;
-      double out = ACCUM ? add(y[row], s) : s;
-      if (dot.plus_zero) out = add(out, 0.0);
-      y[row] = out;
-      if (FUSE_DOT) dsum = add(dsum, mul(dot.other[row], out));
+  for (int pr = (blockIdx.x * kCsrBlock + threadIdx.x) >> 3; pr < npairs;
+       pr += groups_per_grid) {
+    const int ra = 2 * pr, rb = ra + 1;
+    const bool has_b = rb < nrows;
+    const int sa = __ldg(off + ra), ea = __ldg(off + ra + 1);
+    const int eb = has_b ? __ldg(off + rb + 1) : ea;
+    const int la = ea - sa, lb = eb - ea;
+    if (la >= 1 && la <= 33 && lb >= 1 && lb <= 33) {
+      ShortLeaf A, B;
+      short_leaf_load(col, val, sa, la, lane8, A);
+      short_leaf_load(col, val, ea, lb, lane8, B);
+      short_leaf_gather(x, A);
+      short_leaf_gather(x, B);
+      const double ya = short_leaf_finish(la, lane8, mask, A);
+      const double yb = short_leaf_finish(lb, lane8, mask, B);
+      if (lane8 == 0) {
+        csr_emit<ACCUM, SKIP_LONG, FUSE_DOT>(ra, la, ya, y, dot, dsum);
+        csr_emit<ACCUM, SKIP_LONG, FUSE_DOT>(rb, lb, yb, y, dot, dsum);
+      }
+    } else {
+      csr_row_general<ACCUM, SKIP_LONG, FUSE_DOT>(ra, sa, la, col, val, x, y, lane8, mask, dot,
+                                                  dsum);
+      if (has_b)
+        csr_row_general<ACCUM, SKIP_LONG, FUSE_DOT>(rb, ea, lb, col, val, x, y, lane8, mask,
+                                                    dot, dsum);
     }
   }
   if (FUSE_DOT) dot.finish_block<kCsrBlock>(dsum);
+}
+
+// ---------------------------------------------------------------------------
+// CSR v2: TMA-staged row tiles, warp-specialised.
+//
+// Persistent CTAs: warp 0 is the producer, warps 1..16 (64 lane-groups of 8)
+// consume.  Tiles are R=64 consecutive rows, tile t = blockIdx.x + k*G.
+// The producer warp prefetches the bounding row offsets of the next 16
+// tiles with one load per lane, then for each tile waits for its ring slot to
+// be released (empty[s] mbarrier, one arrive per consumer warp) and issues
+// cp.async.bulk copies of the tile's offsets, column indices and values
+// (16-byte aligned: the copies start at the aligned-down first entry and end
+// at the aligned-up last one, so no ragged loads are needed; a tile whose
+// rounded range would leave the arrays or overflow a stage is "fat" and its
+// rows are read from global memory).  Consumers wait on full[s], compute the
+// exact numpy pairwise leaf of their row from shared memory (x gathered from
+// L2), and release the slot.  Rows longer than kLongRow go to csr_long_rows.
+constexpr int kCsr2ConsumerWarps = 16;
+constexpr int kCsr2Threads = 32 * (kCsr2ConsumerWarps + 1);
+constexpr int kCsr2Rows = 2 * 32 * kCsr2ConsumerWarps / 8;   // 64 rows: one per group
+constexpr int kCsr2OffInts = kCsr2Rows + 4;                   // staged offsets (16-B multiple)
+
+struct Csr2Cfg {
+  int S;          // stages (<= 8)
+  int ecap;       // entry capacity per stage (multiple of 4)
+  int stage_bytes;
+};
+
+struct Csr2Hdr {  // written by the producer before its arrive (release)
+  int e0, e1;     // tile entry range
+  int bc, bv;     // first staged col / val element (aligned down)
+  int fat;        // consumers read global memory for this tile
+  int offs_staged;
+  int pad0, pad1;
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ int* csr2_offs(unsigned char* st) {
+  return reinterpret_cast<int*>(st + 64);
+}
+__device__ __forceinline__ int* csr2_cols(unsigned char* st) {
+  return reinterpret_cast<int*>(st + 64 + 4 * kCsr2OffInts);
+}
+__device__ __forceinline__ double* csr2_vals(unsigned char* st, int ecap) {
+  return reinterpret_cast<double*>(st + 64 + 4 * kCsr2OffInts + 4 * (size_t)ecap);
+}
+
+// exact pairwise leaf from shared memory (m <= 128 addends after p[first])
+__device__ __forceinline__ double csr2_leaf_smem(const int* s_col, const double* s_val, int kc,
+                                                int kv, int m, const double* __restrict__ x,
+                                                int lane8, unsigned mask) {
+  const int full = m & ~7;
+  const int nfull = full >> 3;
+  const int rounds = (m + 7) >> 3;
+  double r = 0.0, tail = 0.0;
+  for (int k0 = 0; k0 < rounds; k0 += 4) {
+    double a[4];
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      const int i = min(lane8 + 8 * (k0 + kk), m - 1);
+      a[kk] = mul(s_val[kv + i], ld_gather(x + s_col[kc + i]));
+    }
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      const int k = k0 + kk;
+      if (k < nfull) r = (k == 0) ? a[kk] : add(r, a[kk]);
+      else if (k == nfull) tail = a[kk];
+    }
+  }
+  double res;
+  if (full > 0) {
+    r = add(r, __shfl_xor_sync(mask, r, 1, 8));
+    r = add(r, __shfl_xor_sync(mask, r, 2, 8));
+    r = add(r, __shfl_xor_sync(mask, r, 4, 8));
+    res = r;
+  } else {
+    res = -0.0;
+  }
+  const int ntail = m - full;
+  for (int t = 0; t < ntail; ++t) res = add(res, __shfl_sync(mask, tail, t, 8));
+  return res;
+}
+
+template <bool ACCUM, bool FUSE_DOT>
+__global__ void __launch_bounds__(kCsr2Threads)
+    csr_tiles_tma(int nrows, int nnz, const int* __restrict__ off, const int* __restrict__ col,
+                  const double* __restrict__ val, const double* __restrict__ x, double* y,
+                  Csr2Cfg cfg, DotOut dot) {
+  if (dot.skip()) return;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);        // S <= 8
+  uint64_t* empty = full + 8;
+  unsigned char* stage0 = smem + 128;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t ntiles = (nrows + kCsr2Rows - 1) / kCsr2Rows;
+  const int64_t G = gridDim.x;
+  const int S = cfg.S;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kCsr2ConsumerWarps);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  double dsum = 0.0;
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    const uint64_t pol = policy_evict_first();
+    for (int64_t k0 = 0; blockIdx.x + k0 * G < ntiles; k0 += 16) {
+      // lane j: bounding offset (j&1) of tile k0 + j/2
+      const int64_t tl = blockIdx.x + (k0 + (lane >> 1)) * G;
+      int bound = 0;
+      if (tl < ntiles) {
+        const int64_t r = min64(tl * kCsr2Rows + (lane & 1) * kCsr2Rows, nrows);
+        bound = off[r];
+      }
+      for (int j = 0; j < 16; ++j) {
+        const int64_t k = k0 + j;
+        const int64_t t = blockIdx.x + k * G;
+        const int e0 = __shfl_sync(0xffffffffu, bound, 2 * j);
+        const int e1 = __shfl_sync(0xffffffffu, bound, 2 * j + 1);
+        if (t >= ntiles) break;
+        const int s = (int)(k % S);
+        const uint32_t use = (uint32_t)(k / S);
+        if (use > 0) mbar_wait(&empty[s], (use - 1) & 1u);
+        if (lane == 0) {
+          unsigned char* st = stage0 + (size_t)s * cfg.stage_bytes;
+          Csr2Hdr* h = reinterpret_cast<Csr2Hdr*>(st);
+          const int r0 = (int)(t * kCsr2Rows);
+          const int bc = e0 & ~3, bv = e0 & ~1;
+          // aligned-up ends; copying past e1 reads the next tile's entries (in
+          // bounds unless the rounding leaves the arrays: then the tile is fat)
+          const int ec = (e1 + 3) & ~3, ev = (e1 + 1) & ~1;
+          const bool fat = ec > nnz || (ec - bc) > cfg.ecap || (ev - bv) > cfg.ecap;
+          const bool offs = (r0 + kCsr2OffInts <= nrows + 1);
+          h->e0 = e0;
+          h->e1 = e1;
+          h->bc = bc;
+          h->bv = bv;
+          h->fat = fat;
+          h->offs_staged = offs;
+          const uint32_t cbytes = fat ? 0u : 4u * (uint32_t)(ec - bc);
+          const uint32_t vbytes = fat ? 0u : 8u * (uint32_t)(ev - bv);
+          const uint32_t bytes = (offs ? 4u * kCsr2OffInts : 0u) + cbytes + vbytes;
+          mbar_arrive_expect_tx(&full[s], bytes);
+          if (offs) bulk_g2s(csr2_offs(st), off + r0, 4u * kCsr2OffInts, &full[s], pol);
+          if (cbytes) bulk_g2s(csr2_cols(st), col + bc, cbytes, &full[s], pol);
+          if (vbytes) bulk_g2s(csr2_vals(st, cfg.ecap), val + bv, vbytes, &full[s], pol);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ consumers
+    const int grp = (tid - 32) >> 3, lane8 = tid & 7;
+    const unsigned mask = 0xffu << (tid & 24);
+    int s = 0;
+    uint32_t ph = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += G) {
+      unsigned char* st = stage0 + (size_t)s * cfg.stage_bytes;
+      mbar_wait(&full[s], ph);
+      const Csr2Hdr h = *reinterpret_cast<const Csr2Hdr*>(st);
+      const int r0 = (int)(t * kCsr2Rows);
+      const int row = r0 + grp;
+      if (row < nrows) {
+        int start, end;
+        if (h.offs_staged) {
+          start = csr2_offs(st)[grp];
+          end = csr2_offs(st)[grp + 1];
+        } else {
+          start = __ldg(off + row);
+          end = __ldg(off + row + 1);
+        }
+        const int len = end - start;
+        if (len <= kLongRow) {
+          double res = 0.0, p0 = 0.0;
+          if (len > 0) {
+            if (h.fat) {
+              if (lane8 == 0)
+                p0 = mul(ld_stream(val + start), ld_gather(x + ld_stream(col + start)));
+              res = csr_leaf_g8(col, val, x, (int64_t)start + 1, len - 1, lane8, mask);
+            } else {
+              const int* s_col = csr2_cols(st);
+              const double* s_val = csr2_vals(st, cfg.ecap);
+              if (lane8 == 0) p0 = mul(s_val[start - h.bv], ld_gather(x + s_col[start - h.bc]));
+              res = csr2_leaf_smem(s_col, s_val, start + 1 - h.bc, start + 1 - h.bv, len - 1, x,
+                                   lane8, mask);
+            }
+          }
+          if (lane8 == 0) {
+            const double sres = (len > 0) ? add(p0, res) : 0.0;
+            double out = ACCUM ? add(y[row], sres) : sres;
+            if (dot.plus_zero) out = add(out, 0.0);
+            y[row] = out;
+            if (FUSE_DOT) dsum = add(dsum, mul(dot.other[row], out));
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (++s == S) {
+        s = 0;
+        ph ^= 1u;
+      }
+    }
+  }
+  if (FUSE_DOT) dot.finish_block<kCsr2Threads>(dsum);
+}
+
+static int csr_tiles_launch(int64_t nrows, int64_t nnz, const int* off, const int* col,
+                            const double* val, const double* x, double* y, bool accum, DotOut d,
+                            bool fuse, cudaStream_t st) {
+  static int eS = -2, eE = -2, eC = -2;
+  if (eS == -2) {
+    const char* a = getenv("DS_CSR_S");
+    const char* b = getenv("DS_CSR_ECAP");
+    const char* c = getenv("DS_CSR_CTAS");
+    eS = a ? atoi(a) : -1;
+    eE = b ? atoi(b) : -1;
+    eC = c ? atoi(c) : -1;
+  }
+  Csr2Cfg cfg;
+  cfg.S = eS > 0 ? min(eS, 8) : 6;
+  cfg.ecap = eE > 0 ? (eE & ~3) : 2304;  // 36 entries per row on average + alignment slack
+  cfg.stage_bytes = (int)((64 + 4 * kCsr2OffInts + 12 * (int64_t)cfg.ecap + 127) & ~127);
+  const size_t smem = 128 + (size_t)cfg.S * cfg.stage_bytes;
+  const int64_t ntiles = ceil_div(nrows, kCsr2Rows);
+  int64_t grid = (int64_t)sm_count() * (eC > 0 ? eC : 1);
+  if (grid > ntiles) grid = ntiles;
+  if (fuse) grid = d.clamp_grid(grid);
+  const void* k;
+  if (accum)
+    k = fuse ? (const void*)csr_tiles_tma<true, true> : (const void*)csr_tiles_tma<true, false>;
+  else
+    k = fuse ? (const void*)csr_tiles_tma<false, true> : (const void*)csr_tiles_tma<false, false>;
+  int rc = allow_dynamic_smem(k, smem);
+  if (rc) return rc;
+#define DS_CSR2(A, F)                                                                     \
+  csr_tiles_tma<A, F><<<(unsigned)grid, kCsr2Threads, smem, st>>>((int)nrows, (int)nnz, off, \
+                                                                  col, val, x, y, cfg, d)
+  if (accum) {
+    if (fuse) DS_CSR2(true, true); else DS_CSR2(true, false);
+  } else {
+    if (fuse) DS_CSR2(false, true); else DS_CSR2(false, false);
+  }
+#undef DS_CSR2
+  DS_LAUNCH_CHECK("csr_tiles_tma");
+  return DS_OK;
 }
 
 // One CTA per long row: the pairwise recursion tree is cut into subtrees of
@@ -288,17 +633,46 @@ __global__ void csr_find_long(int nrows, const int* __restrict__ off, int* long_
   }
 }
 
-int launch_csr(int64_t nrows, const int* off, const int* col, const double* val,
+int launch_csr(int64_t nrows, int64_t nnz, const int* off, const int* col, const double* val,
                const int* long_rows, int64_t n_long, const double* x, double* y, bool accum,
                const DotOut* dot, cudaStream_t st) {
   if (nrows == 0) return DS_OK;
-  const int64_t groups = nrows;
+  const int64_t groups = (nrows + 1) / 2;   // one 8-lane group per row pair
   int64_t blocks = ceil_div(groups * 8, kCsrBlock);
-  const int64_t cap = (int64_t)sm_count() * 8 * 16;  // grid-stride beyond 16 waves
+  static int eB = -2;
+  if (eB == -2) {
+    const char* e = getenv("DS_CSR_BLOCKS_PER_SM");
+    eB = e ? atoi(e) : -1;
+  }
+  // 8 resident CTAs per SM (measured best: 84 us vs 97 us for a 16-wave grid)
+  const int64_t cap = (int64_t)sm_count() * (eB > 0 ? eB : 8);
   if (blocks > cap) blocks = cap;
   const bool skip = (long_rows != nullptr);
   DotOut d = dot ? *dot : DotOut{};
   const bool fuse = d.fused();
+  // the TMA-tiled variant is experimental (slower than the paired direct
+  // kernel on the 104^3 stencil, see profiles/r01/README.md): opt-in only
+  static int use_v1 = -1;
+  if (use_v1 < 0) use_v1 = getenv("DS_CSR_TILES") ? 0 : 1;
+  const bool aligned = ((reinterpret_cast<uintptr_t>(off) | reinterpret_cast<uintptr_t>(col) |
+                         reinterpret_cast<uintptr_t>(val)) & 15) == 0;
+  // the tiled kernel skips rows > kLongRow: it needs the long-row plan
+  // (long_rows != NULL, possibly empty) so those rows are computed elsewhere
+  if (!use_v1 && aligned && skip && !(fuse && n_long > 0)) {
+    int rc = csr_tiles_launch(nrows, nnz, off, col, val, x, y, accum, d, fuse, st);
+    if (rc) return rc;
+    if (skip && n_long > 0) {
+      int64_t lb = n_long < (int64_t)sm_count() * 8 ? n_long : (int64_t)sm_count() * 8;
+      if (accum)
+        csr_long_rows<true><<<(unsigned)lb, kCsrBlock, 0, st>>>(long_rows, (int)n_long, off, col,
+                                                               val, x, y, d.guard);
+      else
+        csr_long_rows<false><<<(unsigned)lb, kCsrBlock, 0, st>>>(long_rows, (int)n_long, off,
+                                                                col, val, x, y, d.guard);
+      DS_LAUNCH_CHECK("csr_long_rows");
+    }
+    return DS_OK;
+  }
   if (fuse) blocks = d.clamp_grid(blocks);
 #define DS_CSR(A, S, F) \
   csr_rows_g8<A, S, F><<<(unsigned)blocks, kCsrBlock, 0, st>>>((int)nrows, off, col, val, x, y, d)
@@ -606,9 +980,29 @@ __global__ void __launch_bounds__(kCooBlock)
   __syncthreads();
   for (int64_t t0 = start; t0 < end; t0 += kCooTile) {
     const int cnt = (int)min64(kCooTile, end - t0);
-    for (int k = tid; k < cnt; k += kCooBlock) {
-      s_row[k] = ld_stream(rows + t0 + k);
-      s_p[k] = mul(ld_stream(vals + t0 + k), ld_gather(x + ld_stream(cols + t0 + k)));
+    {
+      // all loads of the thread's entries first (clamped, unpredicated), then
+      // the gathers, then the stores: PER independent chains in flight
+      constexpr int PER = kCooTile / kCooBlock;
+      int rr[PER], cc[PER];
+      double vv[PER];
+#pragma unroll
+      for (int q = 0; q < PER; ++q) {
+        const int k = min(tid + q * kCooBlock, cnt - 1);
+        rr[q] = ld_stream(rows + t0 + k);
+        cc[q] = ld_stream(cols + t0 + k);
+        vv[q] = ld_stream(vals + t0 + k);
+      }
+#pragma unroll
+      for (int q = 0; q < PER; ++q) vv[q] = mul(vv[q], ld_gather(x + cc[q]));
+#pragma unroll
+      for (int q = 0; q < PER; ++q) {
+        const int k = tid + q * kCooBlock;
+        if (k < cnt) {
+          s_row[k] = rr[q];
+          s_p[k] = vv[q];
+        }
+      }
     }
     __syncthreads();
     // segment heads: 8 consecutive entries per thread, block exclusive scan
@@ -652,7 +1046,12 @@ __global__ void __launch_bounds__(kCooBlock)
       const int r = s_row[hs];
       const bool cont = (s == 0 && r == carry_row_in);
       double acc = cont ? carry_in : 0.0;
-      for (int k = hs; k < he; ++k) acc = add(acc, s_p[k]);
+      int k = hs;
+      for (; k + 4 <= he; k += 4) {  // 4 independent shared loads per dependent chain step
+        const double p0 = s_p[k], p1 = s_p[k + 1], p2 = s_p[k + 2], p3 = s_p[k + 3];
+        acc = add(add(add(add(acc, p0), p1), p2), p3);
+      }
+      for (; k < he; ++k) acc = add(acc, s_p[k]);
       const int prev = (s == 0) ? prev_row_in : s_row[s_seg[s - 1]];
       if (!cont) coo_fill_gap<ACCUM>(y, prev + 1, r);
       if (s == nseg - 1 && more && next_row == r) {
@@ -784,7 +1183,7 @@ extern "C" int ds_spmv_csr(int64_t nrows, int64_t ncols, int64_t nnz, const int3
     set_error("nrows out of range");
     return DS_ERR_NOT_SUPPORTED;
   }
-  return launch_csr(nrows, row_offsets, col_indices, values, long_rows, n_long, x, y,
+  return launch_csr(nrows, nnz, row_offsets, col_indices, values, long_rows, n_long, x, y,
                     accumulate != 0, nullptr, as_stream(stream));
 }
 

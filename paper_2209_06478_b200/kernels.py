@@ -113,7 +113,9 @@ def csr_plan(m: CsrMatrix):
             _native.call("ds_csr_analyze", m.nrows, D.ptr(m.row_offsets), D.ptr(buf),
                          ctypes.byref(n_long), ctypes.byref(max_len), D.stream(m.device))
         nl = int(n_long.value)
-        lr = buf[:nl].clone() if nl else None
+        # keep a valid pointer even when empty: non-NULL tells the C side the
+        # matrix was analysed (rows > 129 are then handled by their own kernel)
+        lr = buf[:max(nl, 1)].clone()
     m._cache["plan"] = (k, lr, nl)
     return lr, nl
 
@@ -146,7 +148,7 @@ def descriptor(m) -> _native.DsMatrix:
         d.format, d.nnz = int(FormatId.CSR), m.nnz
         d.idx0, d.idx1, d.values = D.ptr(m.row_offsets), D.ptr(m.col_indices), D.ptr(m.values)
         lr, nl = csr_plan(m)
-        d.long_rows, d.n_long = D.ptr(lr), nl
+        d.long_rows, d.n_long = (lr.data_ptr() if lr is not None else None), nl
     elif isinstance(m, CooMatrix):
         d.format, d.nnz = int(FormatId.COO), m.nnz
         d.idx0, d.idx1, d.values = D.ptr(m.row_indices), D.ptr(m.col_indices), D.ptr(m.values)
