@@ -932,19 +932,21 @@ constexpr int kCooTile = 2048;            // entries staged per tile
 constexpr int kCooPerBlock = 4 * kCooTile; // nominal entries per block
 
 // First entry index >= k that starts a row (rows sorted); k in [0, nnz].
-__device__ __forceinline__ int64_t coo_row_start_at_or_after(const int* rows, int64_t nnz,
-                                                             int64_t k) {
+// Called by one full warp: 32 row ids per step, ballot for the first change,
+// so a boundary inside a row costs ceil(row_len / 32) coalesced loads.
+__device__ __forceinline__ int64_t coo_row_start_at_or_after_warp(const int* rows, int64_t nnz,
+                                                                  int64_t k) {
   if (k <= 0) return 0;
   if (k >= nnz) return nnz;
+  const int lane = threadIdx.x & 31;
   const int prev = rows[k - 1];
-  if (rows[k] != prev) return k;
-  // upper_bound of prev in [k, nnz)
-  int64_t lo = k, hi = nnz;
-  while (lo < hi) {
-    const int64_t mid = (lo + hi) >> 1;
-    if (rows[mid] <= prev) lo = mid + 1; else hi = mid;
+  for (int64_t b = k; b < nnz; b += 32) {
+    const int64_t i = b + lane;
+    const bool diff = (i < nnz) && (rows[i] != prev);
+    const unsigned m = __ballot_sync(0xffffffffu, diff);
+    if (m) return b + (__ffs(m) - 1);
   }
-  return lo;
+  return nnz;
 }
 
 template <bool ACCUM>
@@ -966,18 +968,27 @@ __global__ void __launch_bounds__(kCooBlock)
   __shared__ int s_nseg;
   __shared__ double s_carry;
   __shared__ int s_carry_row, s_prev_row;
+  __shared__ int64_t s_start, s_end;
+  __shared__ int s_R0, s_R1;
   const int tid = threadIdx.x;
-  const int64_t start = coo_row_start_at_or_after(rows, nnz, (int64_t)blockIdx.x * kCooPerBlock);
-  const int64_t end =
-      coo_row_start_at_or_after(rows, nnz, (int64_t)(blockIdx.x + 1) * kCooPerBlock);
-  const int R0 = (start == 0) ? 0 : (start < nnz ? rows[start] : nrows);
-  const int R1 = (end < nnz) ? rows[end] : nrows;
-  if (tid == 0) {
-    s_carry_row = -1;
-    s_carry = 0.0;
-    s_prev_row = R0 - 1;
+  if (tid < 32) {  // warp 0: row-aligned bounds of this block's entry range
+    const int64_t st = coo_row_start_at_or_after_warp(rows, nnz,
+                                                      (int64_t)blockIdx.x * kCooPerBlock);
+    const int64_t en = coo_row_start_at_or_after_warp(rows, nnz,
+                                                      (int64_t)(blockIdx.x + 1) * kCooPerBlock);
+    if (tid == 0) {
+      s_start = st;
+      s_end = en;
+      s_R0 = (st == 0) ? 0 : (st < nnz ? rows[st] : nrows);
+      s_R1 = (en < nnz) ? rows[en] : nrows;
+      s_carry_row = -1;
+      s_carry = 0.0;
+      s_prev_row = s_R0 - 1;
+    }
   }
   __syncthreads();
+  const int64_t start = s_start, end = s_end;
+  const int R1 = s_R1;
   for (int64_t t0 = start; t0 < end; t0 += kCooTile) {
     const int cnt = (int)min64(kCooTile, end - t0);
     {
@@ -1074,6 +1085,150 @@ __global__ void __launch_bounds__(kCooBlock)
   if (tid == 0) coo_fill_gap<ACCUM>(y, s_prev_row + 1, R1);
 }
 
+// ---------------------------------------------------------------------------
+// COO v2: warp-centric segments.  Each warp owns row-aligned chunks of
+// kCooWarpChunk entries (chunk c = global warp + k * warps, bounds moved
+// forward to the next row start with a ballot scan) and walks them in tiles
+// of 256 entries: coalesced strided loads (lane + 32 i) of rows / cols /
+// vals, the x gathers, products to warp-private shared memory; the NEXT
+// tile's loads are issued before the current tile's segments are summed.
+// Row segments come from a warp scan of head flags; one lane per segment
+// sums sequentially from +0.0 in stored order (np.bincount), a row that
+// continues into the next tile is carried.  No block-wide barriers.
+constexpr int kCooWarps = 8;
+constexpr int kCooWTile = 256;
+constexpr int kCooWarpChunk = 4096;
+
+struct CooTileRegs {
+  int r[8], c[8];
+  double v[8];
+};
+
+__device__ __forceinline__ void coo_tile_load(const int* __restrict__ rows,
+                                              const int* __restrict__ cols,
+                                              const double* __restrict__ vals, int64_t t0,
+                                              int cnt, int lane, CooTileRegs& T) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int k = min(lane + 32 * i, cnt - 1);
+    T.r[i] = ld_stream(rows + t0 + k);
+    T.c[i] = ld_stream(cols + t0 + k);
+    T.v[i] = ld_stream(vals + t0 + k);
+  }
+}
+
+template <bool ACCUM>
+__global__ void __launch_bounds__(32 * kCooWarps)
+    coo_warp_segments(int nrows, int64_t nnz, const int* __restrict__ rows,
+                      const int* __restrict__ cols, const double* __restrict__ vals,
+                      const double* __restrict__ x, double* y, const int* guard, int plus_zero) {
+  if (guard && *guard) return;
+  __shared__ double s_p[kCooWarps][kCooWTile];
+  __shared__ int s_r[kCooWarps][kCooWTile];
+  __shared__ int s_seg[kCooWarps][kCooWTile + 1];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double* sp = s_p[w];
+  int* sr = s_r[w];
+  int* sg = s_seg[w];
+  const int64_t nchunks = (nnz + kCooWarpChunk - 1) / kCooWarpChunk;
+  const int64_t nw = (int64_t)gridDim.x * kCooWarps;
+  const int64_t gw = (int64_t)blockIdx.x * kCooWarps + w;
+  // empty matrix: warp 0 of block 0 zero-fills (the loop below has no chunks)
+  if (nnz == 0) {
+    if (gw == 0)
+      for (int r = lane; r < nrows; r += 32) {
+        double o = ACCUM ? add(y[r], 0.0) : 0.0;
+        y[r] = o;
+      }
+    return;
+  }
+  for (int64_t c = gw; c < nchunks; c += nw) {
+    const int64_t start = coo_row_start_at_or_after_warp(rows, nnz, c * kCooWarpChunk);
+    const int64_t end = coo_row_start_at_or_after_warp(rows, nnz, (c + 1) * kCooWarpChunk);
+    const int R0 = (start == 0) ? 0 : (start < nnz ? rows[start] : nrows);
+    const int R1 = (end < nnz) ? rows[end] : nrows;
+    int prev_row = R0 - 1, carry_row = -1;
+    double carry = 0.0;
+    CooTileRegs T;
+    if (start < end) coo_tile_load(rows, cols, vals, start, (int)min64(kCooWTile, end - start), lane, T);
+    for (int64_t t0 = start; t0 < end; t0 += kCooWTile) {
+      const int cnt = (int)min64(kCooWTile, end - t0);
+      // products of this tile -> warp-private shared memory
+#pragma unroll
+      for (int i = 0; i < 8; ++i) T.v[i] = mul(T.v[i], ld_gather(x + T.c[i]));
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int k = lane + 32 * i;
+        if (k < cnt) {
+          sr[k] = T.r[i];
+          sp[k] = T.v[i];
+        }
+      }
+      // segment heads from registers: position k = lane + 32 i, its
+      // predecessor is lane-1 of round i (lane 31 of round i-1 for lane 0);
+      // one ballot per round gives every head its segment index in order
+      int nseg = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        int prev_r = __shfl_up_sync(0xffffffffu, T.r[i], 1);
+        const int wrap = __shfl_sync(0xffffffffu, T.r[i > 0 ? i - 1 : 0], 31);
+        if (lane == 0) prev_r = wrap;
+        const int k = lane + 32 * i;
+        const bool head = (k < cnt) && (k == 0 || T.r[i] != prev_r);
+        const unsigned m = __ballot_sync(0xffffffffu, head);
+        if (head) sg[nseg + __popc(m & ((1u << lane) - 1u))] = k;
+        nseg += __popc(m);
+      }
+      if (lane == 0) sg[nseg] = cnt;
+      __syncwarp();
+      // prefetch the next tile while this one is reduced
+      const int64_t tn = t0 + kCooWTile;
+      if (tn < end) coo_tile_load(rows, cols, vals, tn, (int)min64(kCooWTile, end - tn), lane, T);
+      const bool more = tn < end;
+      const int next_row = more ? rows[tn] : -1;
+      int last_row = 0;
+      double last_acc = 0.0;
+      for (int sgi = lane; sgi < nseg; sgi += 32) {
+        const int hs = sg[sgi], he = sg[sgi + 1];
+        const int row = sr[hs];
+        const bool cont = (sgi == 0 && row == carry_row);
+        double acc = cont ? carry : 0.0;
+        int k = hs;
+        for (; k + 4 <= he; k += 4) {
+          const double p0 = sp[k], p1 = sp[k + 1], p2 = sp[k + 2], p3 = sp[k + 3];
+          acc = add(add(add(add(acc, p0), p1), p2), p3);
+        }
+        for (; k < he; ++k) acc = add(acc, sp[k]);
+        const int prev = (sgi == 0) ? prev_row : sr[sg[sgi - 1]];
+        if (!cont) coo_fill_gap<ACCUM>(y, prev + 1, row);
+        if (sgi == nseg - 1) {
+          last_row = row;
+          last_acc = acc;
+        }
+        if (!(sgi == nseg - 1 && more && next_row == row)) {
+          double out = ACCUM ? add(y[row], acc) : acc;
+          if (plus_zero) out = add(out, 0.0);
+          y[row] = out;
+        }
+      }
+      const int owner = (nseg - 1) & 31;
+      last_row = __shfl_sync(0xffffffffu, last_row, owner);
+      last_acc = __shfl_sync(0xffffffffu, last_acc, owner);
+      prev_row = last_row;
+      if (more && next_row == last_row) {
+        carry_row = last_row;
+        carry = last_acc;
+      } else {
+        carry_row = -1;
+      }
+      __syncwarp();
+    }
+    // rows after the chunk's last entry up to the next chunk's first row
+    for (int r = prev_row + 1 + lane; r < R1; r += 32) y[r] = ACCUM ? add(y[r], 0.0) : 0.0;
+    __syncwarp();
+  }
+}
+
 __global__ void coo_atomic(int64_t nnz, const int* __restrict__ rows, const int* __restrict__ cols,
                            const double* __restrict__ vals, const double* __restrict__ x,
                            double* y, const int* guard) {
@@ -1100,6 +1255,22 @@ int launch_coo(int64_t nrows, int64_t nnz, const int* rows, const int* cols, con
                bool sorted, const double* x, double* y, bool accum, const int* guard,
                cudaStream_t st, bool plus_zero) {
   if (nrows == 0) return DS_OK;
+  static int coo_v1 = -1;
+  if (coo_v1 < 0) coo_v1 = getenv("DS_COO_V1") ? 1 : 0;
+  if (sorted && !coo_v1) {
+    int64_t blocks = ceil_div(ceil_div(nnz, kCooWarpChunk), kCooWarps);
+    const int64_t cap = (int64_t)sm_count() * 8;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    if (accum)
+      coo_warp_segments<true><<<(unsigned)blocks, 32 * kCooWarps, 0, st>>>(
+          (int)nrows, nnz, rows, cols, vals, x, y, guard, (int)plus_zero);
+    else
+      coo_warp_segments<false><<<(unsigned)blocks, 32 * kCooWarps, 0, st>>>(
+          (int)nrows, nnz, rows, cols, vals, x, y, guard, (int)plus_zero);
+    DS_LAUNCH_CHECK("coo_warp_segments");
+    return DS_OK;
+  }
   if (sorted) {
     const int64_t blocks = nnz == 0 ? 1 : ceil_div(nnz, kCooPerBlock);
     if (accum)
