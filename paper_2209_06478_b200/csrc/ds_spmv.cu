@@ -105,11 +105,13 @@ __device__ __forceinline__ void short_leaf_load(const int* __restrict__ col,
                                                 const double* __restrict__ val, int start,
                                                 int len, int lane8, ShortLeaf& L) {
   const int m = len - 1;  // addends after p[first]
+  // clamped indices keep every load unpredicated; L1-allocating loads make
+  // the clamped duplicates (rows shorter than 33) hit L1 instead of L2
 #pragma unroll
   for (int kk = 0; kk < 4; ++kk) {
     const int i = max(min(lane8 + 8 * kk, m - 1), 0);   // clamped: always in the row
-    L.c[kk] = ld_stream(col + start + 1 + i);
-    L.v[kk] = ld_stream(val + start + 1 + i);
+    L.c[kk] = __ldg(col + start + 1 + i);
+    L.v[kk] = __ldg(val + start + 1 + i);
   }
   L.c0 = ld_stream(col + start);
   L.v0 = ld_stream(val + start);

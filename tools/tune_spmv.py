@@ -14,7 +14,20 @@ import paper_2209_06478_b200 as ds  # noqa: E402
 fmt = os.environ.get("FMT", "dia")
 nx = int(os.environ.get("NX", "104"))
 dev = torch.device("cuda", 0)
-part = ds.generate_partition(ds.GridSpec(nx, nx, nx), 0, space=ds.MemorySpace.DEVICE, device=dev)
+if os.environ.get("POWERLAW"):
+    rng = np.random.default_rng(2209)
+    n = 4_194_304
+    L = np.minimum(n, np.floor(6.0 * (1.0 - rng.random(n)) ** (-1 / 1.8))).astype(np.int64)
+    rows = np.repeat(np.arange(n, dtype=np.int64), L)
+    a_csr = ds.convert(ds.CooMatrix(n, n, rows, rng.integers(0, n, rows.size),
+                                    rng.standard_normal(rows.size), ds.MemorySpace.DEVICE, dev),
+                       ds.FormatId.CSR)
+
+    class _P:  # stand-in for a partition
+        a_full = a_csr
+    part = _P()
+else:
+    part = ds.generate_partition(ds.GridSpec(nx, nx, nx), 0, space=ds.MemorySpace.DEVICE, device=dev)
 n = part.a_full.nrows
 x = ds.DenseVector(torch.from_numpy(np.random.default_rng(0).standard_normal(n)).to(dev))
 y = ds.DenseVector.zeros(n, ds.MemorySpace.DEVICE, dev)
@@ -32,7 +45,7 @@ for a, b in ev:
 torch.cuda.synchronize()
 ms = statistics.median(a.elapsed_time(b) for a, b in ev)
 nnz = part.a_full.nnz
-byts = {"dia": 8 * 27 * n + 8 * 27 + 16 * n, "csr": 12 * nnz + 4 * (n + 1) + 16 * n,
+byts = {"dia": 8 * getattr(m, "ndiags", 27) * n + 16 * n, "csr": 12 * nnz + 4 * (n + 1) + 16 * n,
         "coo": 16 * nnz + 16 * n}[fmt]
 err = float(torch.linalg.norm(y.data - ref.data) / torch.linalg.norm(ref.data))
 print(json.dumps({"fmt": fmt, "env": {k: v for k, v in os.environ.items() if k.startswith("DS_")},
