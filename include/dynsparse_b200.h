@@ -197,6 +197,9 @@ typedef struct ds_cg_scalars {
   int32_t max_iters;
   int32_t done;     /* 0 running, 1 converged, 2 breakdown (p.Ap <= 0), 3 max_iters */
   int32_t pad;
+  double rr_used;   /* deferred path: the rr that produced alpha (read by the p update) */
+  int32_t iter_next;/* deferred path: iteration being completed                */
+  int32_t pad2;
 } ds_cg_scalars;
 
 enum { DS_CG_STAGE_NONE = 0, DS_CG_STAGE_PAP = 1, DS_CG_STAGE_RR = 2, DS_CG_STAGE_SETUP = 3 };
@@ -232,6 +235,17 @@ int ds_cg_direction(int64_t n, const double* r, double* p, const ds_cg_scalars* 
 /* Stage PAP or RR over parts[0..nparts) (after an all-gather).             */
 int ds_cg_finalize(int stage, ds_cg_scalars* s, double* history, const double* parts,
                    int nparts, void* stream);
+/* Deferred-reduction iteration for ONE partition (no all-gather needed):
+ * the SpMV (stage DS_CG_STAGE_DEFERRED in ds_cg_spmv_dot) and the update
+ * only write fixed-order block partials; the NEXT kernel reduces them in its
+ * prologue (every block identically) and derives alpha / breakdown, resp.
+ * history / convergence / beta.  No completion tickets, no tail block: each
+ * scalar is written by one kernel and read only by later ones.            */
+enum { DS_CG_STAGE_DEFERRED = 4 };
+int ds_cg_update_deferred(int64_t n, double* x, double* r, const double* p, const double* ap,
+                          ds_cg_scalars* s, void* workspace, void* stream);
+int ds_cg_direction_deferred(int64_t n, const double* r, double* p, ds_cg_scalars* s,
+                             double* history, void* workspace, void* stream);
 /* halo gather guarded by s->done (dst[k] = src[idx[k]])                    */
 int ds_cg_gather(int64_t count, const int32_t* idx, const double* src, double* dst,
                  const ds_cg_scalars* s, void* stream);

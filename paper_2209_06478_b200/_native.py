@@ -31,6 +31,7 @@ DS_ERR_BREAKDOWN = 5
 DS_ERR_NOT_SUPPORTED = 6
 
 DS_CG_STAGE_NONE, DS_CG_STAGE_PAP, DS_CG_STAGE_RR, DS_CG_STAGE_SETUP = 0, 1, 2, 3
+DS_CG_STAGE_DEFERRED = 4
 
 c_i32, c_i64, c_dbl, c_vp, c_int = (ctypes.c_int32, ctypes.c_int64, ctypes.c_double,
                                     ctypes.c_void_p, ctypes.c_int)
@@ -50,12 +51,13 @@ class DsMatrix(ctypes.Structure):
 
 
 class DsCgScalars(ctypes.Structure):
-    """Mirror of ``ds_cg_scalars`` (lives on the device; 80 bytes)."""
+    """Mirror of ``ds_cg_scalars`` (lives on the device; 96 bytes)."""
 
     _fields_ = [
         ("rr", c_dbl), ("pap", c_dbl), ("alpha", c_dbl), ("beta", c_dbl),
         ("scale", c_dbl), ("tol", c_dbl), ("bb", c_dbl), ("rr_new", c_dbl),
         ("iter", c_i32), ("max_iters", c_i32), ("done", c_i32), ("pad", c_i32),
+        ("rr_used", c_dbl), ("iter_next", c_i32), ("pad2", c_i32),
     ]
 
 
@@ -106,6 +108,8 @@ _SIGNATURES = {
     "ds_cg_direction": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp]),
     "ds_cg_finalize": (c_int, [c_int, c_vp, c_vp, c_vp, c_int, c_vp]),
     "ds_cg_gather": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "ds_cg_update_deferred": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "ds_cg_direction_deferred": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "ds_nccl_unique_id_bytes": (c_int, []),
     "ds_nccl_unique_id": (c_int, [ctypes.c_char_p, c_int]),
     "ds_nccl_comm_init": (c_int, [ctypes.c_char_p, c_int, c_int, ctypes.POINTER(c_vp)]),

@@ -79,6 +79,8 @@ struct DotOut {
   double* history = nullptr;
   const double* parts = nullptr;   // all partitions' dots (result is one of them)
   int nparts_final = 0;            // >0: run cg_finalize(parts, nparts_final)
+  int partials_only = 0;           // deferred mode: write partials[blockIdx] and the
+                                   // grid size (at ticket[2]); the consumer reduces them
   int plus_zero = 0;               // epilogue y = (A x) + 0.0: the exact effect of
                                    // spmv_add with an EMPTY remote part (kernels.py:196-198)
 
@@ -90,6 +92,13 @@ struct DotOut {
   __device__ void finish_block(double v) const {
     __shared__ double sh[32];
     double bsum = block_sum<BLOCK>(v, sh);
+    if (partials_only) {
+      if (threadIdx.x == 0) {
+        partials[blockIdx.x] = bsum;
+        if (blockIdx.x == 0) ticket[2] = gridDim.x;   // count word; ticket[0] stays 0
+      }
+      return;
+    }
     double total;
     if (grid_sum_last_block<BLOCK>(bsum, partials, ticket, &total, sh)) {
       if (threadIdx.x == 0) {
@@ -102,6 +111,21 @@ struct DotOut {
     }
   }
 };
+
+// Deferred reduction: every block sums the producer's G block partials in
+// the same fixed order (thread t: t, t+BLOCK, ... sequentially; then the
+// block tree), so all blocks obtain bitwise the same total.
+template <int BLOCK>
+__device__ double reduce_partials(const double* partials, const unsigned* count, double* sh) {
+  const int G = (int)*count;
+  double v = 0.0;
+  for (int i = threadIdx.x; i < G; i += BLOCK) v = add(v, partials[i]);
+  v = block_sum<BLOCK>(v, sh);
+  __shared__ double s_tot;
+  if (threadIdx.x == 0) s_tot = v;
+  __syncthreads();
+  return s_tot;
+}
 
 // launchers shared between translation units
 int launch_csr(int64_t nrows, int64_t nnz, const int* off, const int* col, const double* val,

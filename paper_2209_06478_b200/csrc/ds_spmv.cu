@@ -757,6 +757,8 @@ __global__ void __launch_bounds__(256, 1)   // 1 CTA/SM: registers for all 27 ga
   }
   for (int j = tid; j < nd; j += blockDim.x) s_off[j] = offsets[j];
   __syncthreads();
+  bool has_main = false;
+  for (int j = 0; j < nd; ++j) has_main |= (s_off[j] == 0);
   if (tid == 0)
     for (int s = 0; s < S; ++s) {
       const int64_t t = blockIdx.x + s * G;
@@ -783,11 +785,13 @@ __global__ void __launch_bounds__(256, 1)   // 1 CTA/SM: registers for all 27 ga
       // (kernels.py:133-138).
       double xv[ND > 0 ? ND : 1];
       double acc = 0.0;
+      double xdiag = 0.0;   // x[i] when offset 0 is a diagonal (the fused dot reuses it)
       if (ND > 0) {
 #pragma unroll
         for (int j = 0; j < ND; ++j) {
           const int c = i + s_off[j];
           xv[j] = ld_gather(x + min(max(c, 0), ncols - 1));
+          if (s_off[j] == 0) xdiag = xv[j];
         }
 #pragma unroll
         for (int j = 0; j < ND; ++j) {
@@ -804,7 +808,12 @@ __global__ void __launch_bounds__(256, 1)   // 1 CTA/SM: registers for all 27 ga
       double out = ACCUM ? add(y[i], acc) : acc;
       if (dot.plus_zero) out = add(out, 0.0);
       y[i] = out;
-      if (FUSE_DOT) dsum = add(dsum, mul(dot.other[i], out));
+      if (FUSE_DOT) {
+        // p.Ap with p == x (the CG case): x[i] was already gathered for the
+        // main diagonal; otherwise load it
+        const double pi = (ND > 0 && has_main && dot.other == x) ? xdiag : dot.other[i];
+        dsum = add(dsum, mul(pi, out));
+      }
     }
     __syncthreads();  // stage s fully consumed
     if (tid == 0) {

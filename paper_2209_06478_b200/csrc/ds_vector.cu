@@ -247,8 +247,12 @@ __global__ void cg_setup_finalize_kernel(ds_cg_scalars* s, const double* bb_part
 }
 
 // x = 1*x + alpha*p ; r = 1*r + (-alpha)*ap ; partial r.r   (solver.py:177-180)
-// VEC: 16-B aligned operands, element pairs per thread (LDG.128); the odd
-// tail element is folded in by the first thread after its pairs.
+// VEC: 16-B aligned operands, element pairs (LDG.128), U pairs per thread and
+// iteration with every load issued before any use; the odd tail element is
+// folded in by the first thread after its pairs.  Grid = 4 CTAs per SM: few
+// partials for the fused reduction, all loads of a sweep in flight.
+constexpr int kVecUnroll = 4;
+
 template <bool VEC>
 __global__ void __launch_bounds__(kVecBlock)
     cg_update_kernel(int64_t n, double* x, double* r, const double* __restrict__ p,
@@ -265,17 +269,31 @@ __global__ void __launch_bounds__(kVecBlock)
     double2* r2 = reinterpret_cast<double2*>(r);
     const double2* p2 = reinterpret_cast<const double2*>(p);
     const double2* a2 = reinterpret_cast<const double2*>(ap);
-    for (int64_t i = gtid; i < n2; i += stride) {
-      const double2 xv = x2[i], rv = r2[i], pv = p2[i], av = a2[i];
-      double2 xo, ro;
-      xo.x = add(mul(1.0, xv.x), mul(alpha, pv.x));
-      xo.y = add(mul(1.0, xv.y), mul(alpha, pv.y));
-      ro.x = add(mul(1.0, rv.x), mul(nalpha, av.x));
-      ro.y = add(mul(1.0, rv.y), mul(nalpha, av.y));
-      x2[i] = xo;
-      r2[i] = ro;
-      v = add(v, mul(ro.x, ro.x));
-      v = add(v, mul(ro.y, ro.y));
+    for (int64_t i0 = gtid; i0 < n2; i0 += stride * kVecUnroll) {
+      double2 xv[kVecUnroll], rv[kVecUnroll], pv[kVecUnroll], av[kVecUnroll];
+#pragma unroll
+      for (int u = 0; u < kVecUnroll; ++u) {
+        const int64_t i = min64(i0 + u * stride, n2 - 1);
+        xv[u] = x2[i];
+        rv[u] = r2[i];
+        pv[u] = p2[i];
+        av[u] = a2[i];
+      }
+#pragma unroll
+      for (int u = 0; u < kVecUnroll; ++u) {
+        const int64_t i = i0 + u * stride;
+        if (i < n2) {
+          double2 xo, ro;
+          xo.x = add(mul(1.0, xv[u].x), mul(alpha, pv[u].x));
+          xo.y = add(mul(1.0, xv[u].y), mul(alpha, pv[u].y));
+          ro.x = add(mul(1.0, rv[u].x), mul(nalpha, av[u].x));
+          ro.y = add(mul(1.0, rv[u].y), mul(nalpha, av[u].y));
+          x2[i] = xo;
+          r2[i] = ro;
+          v = add(v, mul(ro.x, ro.x));
+          v = add(v, mul(ro.y, ro.y));
+        }
+      }
     }
     if ((n & 1) && gtid == 0) {
       const int64_t i = n - 1;
@@ -308,12 +326,24 @@ __global__ void __launch_bounds__(kVecBlock)
     const int64_t n2 = n >> 1;
     const double2* r2 = reinterpret_cast<const double2*>(r);
     double2* p2 = reinterpret_cast<double2*>(p);
-    for (int64_t i = gtid; i < n2; i += stride) {
-      const double2 rv = r2[i], pv = p2[i];
-      double2 o;
-      o.x = add(mul(1.0, rv.x), mul(beta, pv.x));
-      o.y = add(mul(1.0, rv.y), mul(beta, pv.y));
-      p2[i] = o;
+    for (int64_t i0 = gtid; i0 < n2; i0 += stride * kVecUnroll) {
+      double2 rv[kVecUnroll], pv[kVecUnroll];
+#pragma unroll
+      for (int u = 0; u < kVecUnroll; ++u) {
+        const int64_t i = min64(i0 + u * stride, n2 - 1);
+        rv[u] = r2[i];
+        pv[u] = p2[i];
+      }
+#pragma unroll
+      for (int u = 0; u < kVecUnroll; ++u) {
+        const int64_t i = i0 + u * stride;
+        if (i < n2) {
+          double2 o;
+          o.x = add(mul(1.0, rv[u].x), mul(beta, pv[u].x));
+          o.y = add(mul(1.0, rv[u].y), mul(beta, pv[u].y));
+          p2[i] = o;
+        }
+      }
     }
     if ((n & 1) && gtid == 0) p[n - 1] = add(mul(1.0, r[n - 1]), mul(beta, p[n - 1]));
   } else {
@@ -327,14 +357,160 @@ static bool aligned16(const void* a, const void* b = nullptr, const void* c = nu
   return ok(a) && ok(b) && ok(c) && ok(d);
 }
 
-// grid of the streaming vector kernels: enough CTAs for ~4 pairs per thread,
-// at most 8 per SM (G partials for the fused reductions)
+// grid of the streaming vector kernels: 4 resident CTAs per SM (592
+// partials for the fused reductions -- thousands of CTAs made the
+// same-address completion tickets the bottleneck), kVecUnroll pairs per
+// thread in flight
 static unsigned vec_grid(int64_t n) {
-  int64_t g = ceil_div(n, (int64_t)kVecBlock * 8);
-  const int64_t cap = (int64_t)sm_count() * 8;
+  int64_t g = ceil_div(n, (int64_t)kVecBlock * 2 * kVecUnroll);
+  const int64_t cap = (int64_t)sm_count() * 4;
   if (g > cap) g = cap;
   if (g < 1) g = 1;
   return (unsigned)g;
+}
+
+// ---- deferred-reduction single-partition iteration -------------------------
+// update: prologue reduces the SpMV's p.Ap partials -> alpha (or breakdown);
+// body = cg_update (x, r, partial r.r written without a ticket)
+template <bool VEC>
+__global__ void __launch_bounds__(kVecBlock)
+    cg_update_deferred_kernel(int64_t n, double* x, double* r, const double* __restrict__ p,
+                              const double* __restrict__ ap, ds_cg_scalars* s,
+                              const double* pap_parts, const unsigned* pap_count,
+                              double* rr_parts, unsigned* rr_count) {
+  __shared__ double sh[32];
+  if (s->done) return;
+  const double pap = reduce_partials<kVecBlock>(pap_parts, pap_count, sh);
+  if (pap <= 0.0) {  // breakdown: every block sees the same pap
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      s->pap = pap;
+      s->done = 2;
+    }
+    return;
+  }
+  const double rr = s->rr;
+  const double alpha = rr / pap;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    s->pap = pap;
+    s->alpha = alpha;
+    s->rr_used = rr;
+    s->iter_next = s->iter + 1;
+  }
+  const double nalpha = -alpha;
+  double v = 0.0;
+  const int64_t gtid = (int64_t)blockIdx.x * kVecBlock + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * kVecBlock;
+  if (VEC) {
+    const int64_t n2 = n >> 1;
+    double2* x2 = reinterpret_cast<double2*>(x);
+    double2* r2 = reinterpret_cast<double2*>(r);
+    const double2* p2 = reinterpret_cast<const double2*>(p);
+    const double2* a2 = reinterpret_cast<const double2*>(ap);
+    for (int64_t i0 = gtid; i0 < n2; i0 += stride * kVecUnroll) {
+      double2 xv[kVecUnroll], rv[kVecUnroll], pv[kVecUnroll], av[kVecUnroll];
+#pragma unroll
+      for (int u = 0; u < kVecUnroll; ++u) {
+        const int64_t i = min64(i0 + u * stride, n2 - 1);
+        xv[u] = x2[i];
+        rv[u] = r2[i];
+        pv[u] = p2[i];
+        av[u] = a2[i];
+      }
+#pragma unroll
+      for (int u = 0; u < kVecUnroll; ++u) {
+        const int64_t i = i0 + u * stride;
+        if (i < n2) {
+          double2 xo, ro;
+          xo.x = add(mul(1.0, xv[u].x), mul(alpha, pv[u].x));
+          xo.y = add(mul(1.0, xv[u].y), mul(alpha, pv[u].y));
+          ro.x = add(mul(1.0, rv[u].x), mul(nalpha, av[u].x));
+          ro.y = add(mul(1.0, rv[u].y), mul(nalpha, av[u].y));
+          x2[i] = xo;
+          r2[i] = ro;
+          v = add(v, mul(ro.x, ro.x));
+          v = add(v, mul(ro.y, ro.y));
+        }
+      }
+    }
+    if ((n & 1) && gtid == 0) {
+      const int64_t i = n - 1;
+      x[i] = add(mul(1.0, x[i]), mul(alpha, p[i]));
+      const double ri = add(mul(1.0, r[i]), mul(nalpha, ap[i]));
+      r[i] = ri;
+      v = add(v, mul(ri, ri));
+    }
+  } else {
+    for (int64_t i = gtid; i < n; i += stride) {
+      x[i] = add(mul(1.0, x[i]), mul(alpha, p[i]));
+      const double ri = add(mul(1.0, r[i]), mul(nalpha, ap[i]));
+      r[i] = ri;
+      v = add(v, mul(ri, ri));
+    }
+  }
+  v = block_sum<kVecBlock>(v, sh);
+  if (threadIdx.x == 0) {
+    rr_parts[blockIdx.x] = v;
+    if (blockIdx.x == 0) *rr_count = gridDim.x;
+  }
+}
+
+// direction: prologue reduces the r.r partials -> history, convergence, beta;
+// body p = 1*r + beta*p (skipped when converged / at max_iters, like the
+// reference's break before the p update, solver.py:182-188)
+template <bool VEC>
+__global__ void __launch_bounds__(kVecBlock)
+    cg_direction_deferred_kernel(int64_t n, const double* __restrict__ r, double* p,
+                                 ds_cg_scalars* s, double* history, const double* rr_parts,
+                                 const unsigned* rr_count) {
+  __shared__ double sh[32];
+  if (s->done) return;
+  const double rr_new = reduce_partials<kVecBlock>(rr_parts, rr_count, sh);
+  const int it = s->iter_next;
+  const double h = sqrt(rr_new) / s->scale;
+  const bool converged = h <= s->tol;
+  const bool last = it >= s->max_iters;
+  const double beta = rr_new / s->rr_used;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    history[it] = h;
+    s->iter = it;
+    s->rr_new = rr_new;
+    if (converged) s->done = 1;
+    else if (last) s->done = 3;
+    else {
+      s->beta = beta;
+      s->rr = rr_new;
+    }
+  }
+  if (converged || last) return;
+  const int64_t gtid = (int64_t)blockIdx.x * kVecBlock + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * kVecBlock;
+  if (VEC) {
+    const int64_t n2 = n >> 1;
+    const double2* r2 = reinterpret_cast<const double2*>(r);
+    double2* p2 = reinterpret_cast<double2*>(p);
+    for (int64_t i0 = gtid; i0 < n2; i0 += stride * kVecUnroll) {
+      double2 rv[kVecUnroll], pv[kVecUnroll];
+#pragma unroll
+      for (int u = 0; u < kVecUnroll; ++u) {
+        const int64_t i = min64(i0 + u * stride, n2 - 1);
+        rv[u] = r2[i];
+        pv[u] = p2[i];
+      }
+#pragma unroll
+      for (int u = 0; u < kVecUnroll; ++u) {
+        const int64_t i = i0 + u * stride;
+        if (i < n2) {
+          double2 o;
+          o.x = add(mul(1.0, rv[u].x), mul(beta, pv[u].x));
+          o.y = add(mul(1.0, rv[u].y), mul(beta, pv[u].y));
+          p2[i] = o;
+        }
+      }
+    }
+    if ((n & 1) && gtid == 0) p[n - 1] = add(mul(1.0, r[n - 1]), mul(beta, p[n - 1]));
+  } else {
+    for (int64_t i = gtid; i < n; i += stride) p[i] = add(mul(1.0, r[i]), mul(beta, p[i]));
+  }
 }
 
 __global__ void cg_finalize_kernel(int stage, ds_cg_scalars* s, double* history,
@@ -578,6 +754,7 @@ extern "C" int ds_cg_spmv_dot(const ds_matrix* a, const double* x, double* y, in
     fused = make_dot(workspace, 0, dot_with, dot_out);
     fused.guard = d.guard;
     fused.plus_zero = d.plus_zero;
+    fused.partials_only = (stage == DS_CG_STAGE_DEFERRED);
     fused.stage = stage;
     fused.s = s;
     fused.history = history;
@@ -679,6 +856,38 @@ extern "C" int ds_cg_direction(int64_t n, const double* r, double* p, const ds_c
   else
     cg_direction_kernel<false><<<g, kVecBlock, 0, as_stream(stream)>>>(n, r, p, s);
   DS_LAUNCH_CHECK("cg_direction_kernel");
+  return DS_OK;
+}
+
+extern "C" int ds_cg_update_deferred(int64_t n, double* x, double* r, const double* p,
+                                     const double* ap, ds_cg_scalars* s, void* workspace,
+                                     void* stream) {
+  Workspace w0(reinterpret_cast<char*>(workspace));
+  Workspace w1(reinterpret_cast<char*>(workspace) + kWorkspaceBytes);
+  const unsigned g = vec_grid(n);
+  cudaStream_t st = as_stream(stream);
+  if (aligned16(x, r, p, ap))
+    cg_update_deferred_kernel<true><<<g, kVecBlock, 0, st>>>(
+        n, x, r, p, ap, s, w0.partials, w0.ticket + 2, w1.partials, w1.ticket + 2);
+  else
+    cg_update_deferred_kernel<false><<<g, kVecBlock, 0, st>>>(
+        n, x, r, p, ap, s, w0.partials, w0.ticket + 2, w1.partials, w1.ticket + 2);
+  DS_LAUNCH_CHECK("cg_update_deferred_kernel");
+  return DS_OK;
+}
+
+extern "C" int ds_cg_direction_deferred(int64_t n, const double* r, double* p, ds_cg_scalars* s,
+                                        double* history, void* workspace, void* stream) {
+  Workspace w1(reinterpret_cast<char*>(workspace) + kWorkspaceBytes);
+  const unsigned g = vec_grid(n);
+  cudaStream_t st = as_stream(stream);
+  if (aligned16(r, p))
+    cg_direction_deferred_kernel<true><<<g, kVecBlock, 0, st>>>(n, r, p, s, history,
+                                                                w1.partials, w1.ticket + 2);
+  else
+    cg_direction_deferred_kernel<false><<<g, kVecBlock, 0, st>>>(n, r, p, s, history,
+                                                                 w1.partials, w1.ticket + 2);
+  DS_LAUNCH_CHECK("cg_direction_deferred_kernel");
   return DS_OK;
 }
 

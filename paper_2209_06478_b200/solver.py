@@ -36,6 +36,7 @@ from .kernels import ExecBackend, descriptor, extract_diagonal, update_diagonal
 from .stencil import PartitionedProblem, SplitMatrix, device_halo, distributed_spmv
 
 PAP, RR = _native.DS_CG_STAGE_PAP, _native.DS_CG_STAGE_RR
+DEFERRED = _native.DS_CG_STAGE_DEFERRED
 
 
 @dataclass
@@ -148,6 +149,8 @@ class CgEngine:
     def step(self, stream) -> None:
         lib, s, hist = self.lib, self._p(self.scal), self._p(self.hist)
         P, ws = self.P, self._p(self.ws)
+        if P == 1 and self.parts[0].d_remote is None and not os.environ.get("DS_CG_TICKETS"):
+            return self._step_deferred(stream)
         fin = 1 if P == 1 else 0
         self._exchange(stream, guard=s)
         marks = getattr(self, "_marks", None)
@@ -183,6 +186,25 @@ class CgEngine:
             self._ck(lib.ds_cg_finalize(RR, s, hist, self._dot(3, 0), P, stream))
         for pt in self.parts:
             self._ck(lib.ds_cg_direction(pt.n, self._p(pt.r), self._p(pt.p), s, stream))
+
+    def _step_deferred(self, stream) -> None:
+        """Single partition: 3 kernels, no reduction tails -- the SpMV and the
+        update leave fixed-order block partials that the next kernel reduces
+        (DS_CG_STAGE_DEFERRED)."""
+        lib, s, hist, ws = self.lib, self._p(self.scal), self._p(self.hist), self._p(self.ws)
+        pt = self.parts[0]
+        marks = getattr(self, "_marks", None)
+        if marks is not None:
+            marks[1].record(marks[0])
+        self._ck(lib.ds_cg_spmv_dot(ctypes.byref(pt.d_local), self._p(pt.p_full),
+                                    self._p(pt.ap), pt.local_mode, self._p(pt.p), self._dot(2, 0),
+                                    DEFERRED, s, hist, None, 0, ws, stream))
+        if marks is not None:
+            marks[2].record(marks[0])
+        self._ck(lib.ds_cg_update_deferred(pt.n, self._p(pt.x), self._p(pt.r), self._p(pt.p),
+                                           self._p(pt.ap), s, ws, stream))
+        self._ck(lib.ds_cg_direction_deferred(pt.n, self._p(pt.r), self._p(pt.p), s, hist, ws,
+                                              stream))
 
     def scalars(self) -> _native.DsCgScalars:
         raw = self.scal.cpu().numpy().tobytes()
