@@ -246,6 +246,16 @@ int ds_cg_update_deferred(int64_t n, double* x, double* r, const double* p, cons
                           ds_cg_scalars* s, void* workspace, void* stream);
 int ds_cg_direction_deferred(int64_t n, const double* r, double* p, ds_cg_scalars* s,
                              double* history, void* workspace, void* stream);
+/* The same two kernels for one partition per process: the prologue sums the
+ * all-gathered partition dots pap_all[0..nparts) / rr_all[0..nparts)
+ * sequentially in rank order (solver.py:140-141); the update's partition
+ * r.r goes to *rr_mine (completion ticket) for the next all-gather.        */
+int ds_cg_update_gathered(int64_t n, double* x, double* r, const double* p, const double* ap,
+                          ds_cg_scalars* s, const double* pap_all, int nparts, double* rr_mine,
+                          void* workspace, void* stream);
+int ds_cg_direction_gathered(int64_t n, const double* r, double* p, ds_cg_scalars* s,
+                             double* history, const double* rr_all, int nparts, void* workspace,
+                             void* stream);
 /* halo gather guarded by s->done (dst[k] = src[idx[k]])                    */
 int ds_cg_gather(int64_t count, const int32_t* idx, const double* src, double* dst,
                  const ds_cg_scalars* s, void* stream);

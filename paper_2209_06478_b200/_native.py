@@ -110,6 +110,9 @@ _SIGNATURES = {
     "ds_cg_gather": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "ds_cg_update_deferred": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "ds_cg_direction_deferred": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "ds_cg_update_gathered": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_vp,
+                                      c_vp, c_vp]),
+    "ds_cg_direction_gathered": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_vp, c_vp]),
     "ds_nccl_unique_id_bytes": (c_int, []),
     "ds_nccl_unique_id": (c_int, [ctypes.c_char_p, c_int]),
     "ds_nccl_comm_init": (c_int, [ctypes.c_char_p, c_int, c_int, ctypes.POINTER(c_vp)]),

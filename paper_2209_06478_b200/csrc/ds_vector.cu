@@ -372,15 +372,26 @@ static unsigned vec_grid(int64_t n) {
 // ---- deferred-reduction single-partition iteration -------------------------
 // update: prologue reduces the SpMV's p.Ap partials -> alpha (or breakdown);
 // body = cg_update (x, r, partial r.r written without a ticket)
+// gathered mode (nparts > 0): the inputs are the P all-gathered partition
+// dots, summed sequentially in rank order (solver.py:140-141); the output
+// partial goes through the completion-ticket DotOut (one partition total).
+__device__ __forceinline__ double gathered_sum(const double* parts, int nparts) {
+  __shared__ double s_g;
+  if (threadIdx.x == 0) s_g = ordered_sum(parts, nparts);
+  __syncthreads();
+  return s_g;
+}
+
 template <bool VEC>
 __global__ void __launch_bounds__(kVecBlock)
     cg_update_deferred_kernel(int64_t n, double* x, double* r, const double* __restrict__ p,
                               const double* __restrict__ ap, ds_cg_scalars* s,
                               const double* pap_parts, const unsigned* pap_count,
-                              double* rr_parts, unsigned* rr_count) {
+                              double* rr_parts, unsigned* rr_count, int nparts, DotOut rr_out) {
   __shared__ double sh[32];
   if (s->done) return;
-  const double pap = reduce_partials<kVecBlock>(pap_parts, pap_count, sh);
+  const double pap = nparts > 0 ? gathered_sum(pap_parts, nparts)
+                                : reduce_partials<kVecBlock>(pap_parts, pap_count, sh);
   if (pap <= 0.0) {  // breakdown: every block sees the same pap
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       s->pap = pap;
@@ -447,6 +458,10 @@ __global__ void __launch_bounds__(kVecBlock)
       v = add(v, mul(ri, ri));
     }
   }
+  if (nparts > 0) {
+    rr_out.finish_block<kVecBlock>(v);   // this partition's r.r -> all-gather
+    return;
+  }
   v = block_sum<kVecBlock>(v, sh);
   if (threadIdx.x == 0) {
     rr_parts[blockIdx.x] = v;
@@ -461,10 +476,11 @@ template <bool VEC>
 __global__ void __launch_bounds__(kVecBlock)
     cg_direction_deferred_kernel(int64_t n, const double* __restrict__ r, double* p,
                                  ds_cg_scalars* s, double* history, const double* rr_parts,
-                                 const unsigned* rr_count) {
+                                 const unsigned* rr_count, int nparts) {
   __shared__ double sh[32];
   if (s->done) return;
-  const double rr_new = reduce_partials<kVecBlock>(rr_parts, rr_count, sh);
+  const double rr_new = nparts > 0 ? gathered_sum(rr_parts, nparts)
+                                   : reduce_partials<kVecBlock>(rr_parts, rr_count, sh);
   const int it = s->iter_next;
   const double h = sqrt(rr_new) / s->scale;
   const bool converged = h <= s->tol;
@@ -862,31 +878,47 @@ extern "C" int ds_cg_direction(int64_t n, const double* r, double* p, const ds_c
 extern "C" int ds_cg_update_deferred(int64_t n, double* x, double* r, const double* p,
                                      const double* ap, ds_cg_scalars* s, void* workspace,
                                      void* stream) {
+  return ds_cg_update_gathered(n, x, r, p, ap, s, nullptr, 0, nullptr, workspace, stream);
+}
+
+extern "C" int ds_cg_update_gathered(int64_t n, double* x, double* r, const double* p,
+                                     const double* ap, ds_cg_scalars* s, const double* pap_all,
+                                     int nparts, double* rr_mine, void* workspace,
+                                     void* stream) {
   Workspace w0(reinterpret_cast<char*>(workspace));
   Workspace w1(reinterpret_cast<char*>(workspace) + kWorkspaceBytes);
+  DotOut d = make_dot(workspace, 1, nullptr, rr_mine);
   const unsigned g = vec_grid(n);
   cudaStream_t st = as_stream(stream);
+  const double* in = nparts > 0 ? pap_all : w0.partials;
   if (aligned16(x, r, p, ap))
     cg_update_deferred_kernel<true><<<g, kVecBlock, 0, st>>>(
-        n, x, r, p, ap, s, w0.partials, w0.ticket + 2, w1.partials, w1.ticket + 2);
+        n, x, r, p, ap, s, in, w0.ticket + 2, w1.partials, w1.ticket + 2, nparts, d);
   else
     cg_update_deferred_kernel<false><<<g, kVecBlock, 0, st>>>(
-        n, x, r, p, ap, s, w0.partials, w0.ticket + 2, w1.partials, w1.ticket + 2);
+        n, x, r, p, ap, s, in, w0.ticket + 2, w1.partials, w1.ticket + 2, nparts, d);
   DS_LAUNCH_CHECK("cg_update_deferred_kernel");
   return DS_OK;
 }
 
 extern "C" int ds_cg_direction_deferred(int64_t n, const double* r, double* p, ds_cg_scalars* s,
                                         double* history, void* workspace, void* stream) {
+  return ds_cg_direction_gathered(n, r, p, s, history, nullptr, 0, workspace, stream);
+}
+
+extern "C" int ds_cg_direction_gathered(int64_t n, const double* r, double* p, ds_cg_scalars* s,
+                                        double* history, const double* rr_all, int nparts,
+                                        void* workspace, void* stream) {
   Workspace w1(reinterpret_cast<char*>(workspace) + kWorkspaceBytes);
   const unsigned g = vec_grid(n);
   cudaStream_t st = as_stream(stream);
+  const double* in = nparts > 0 ? rr_all : w1.partials;
   if (aligned16(r, p))
-    cg_direction_deferred_kernel<true><<<g, kVecBlock, 0, st>>>(n, r, p, s, history,
-                                                                w1.partials, w1.ticket + 2);
+    cg_direction_deferred_kernel<true><<<g, kVecBlock, 0, st>>>(n, r, p, s, history, in,
+                                                                w1.ticket + 2, nparts);
   else
-    cg_direction_deferred_kernel<false><<<g, kVecBlock, 0, st>>>(n, r, p, s, history,
-                                                                 w1.partials, w1.ticket + 2);
+    cg_direction_deferred_kernel<false><<<g, kVecBlock, 0, st>>>(n, r, p, s, history, in,
+                                                                 w1.ticket + 2, nparts);
   DS_LAUNCH_CHECK("cg_direction_deferred_kernel");
   return DS_OK;
 }

@@ -98,7 +98,10 @@ class RankCG:
         self.local = to_device(split.local.payload, device)
         self.remote = to_device(split.remote.payload, device)
         self.d_local = descriptor(self.local)
-        self.d_remote = descriptor(self.remote)
+        # an empty remote part (world size 1) only adds +0.0: fold it into the
+        # local kernel's epilogue (mode 2) instead of a pass over every row
+        self.fold = self.remote.nnz == 0
+        self.d_remote = None if self.fold else descriptor(self.remote)
         f64 = dict(dtype=torch.float64, device=device)
         g = part.halo.ghost_count
         self.p_full = torch.zeros(n + g, **f64)
@@ -160,11 +163,12 @@ class RankCG:
         lib, ws = self.lib, self.ws.data_ptr()
         self._exchange(stream, None)
         self._ck(lib.ds_cg_spmv_dot(ctypes.byref(self.d_local), self.p_full.data_ptr(),
-                                    self.ap.data_ptr(), 0, None, None, 0, None, None, None, 0,
-                                    ws, stream))
-        self._ck(lib.ds_cg_spmv_dot(ctypes.byref(self.d_remote), self.p_full.data_ptr() + 8 * self.n,
-                                    self.ap.data_ptr(), 1, None, None, 0, None, None, None, 0,
-                                    ws, stream))
+                                    self.ap.data_ptr(), 2 if self.fold else 0, None, None, 0,
+                                    None, None, None, 0, ws, stream))
+        if not self.fold:
+            self._ck(lib.ds_cg_spmv_dot(ctypes.byref(self.d_remote),
+                                        self.p_full.data_ptr() + 8 * self.n, self.ap.data_ptr(),
+                                        1, None, None, 0, None, None, None, 0, ws, stream))
         self._ck(lib.ds_cg_setup_residual(self.n, self.b.data_ptr(), self.ap.data_ptr(),
                                           self.r.data_ptr(), self.p.data_ptr(), self._mine(2),
                                           self._mine(3), ws, stream))
@@ -185,22 +189,33 @@ class RankCG:
         self._exchange(self.side.cuda_stream, s)
         if self._marks is not None:
             self._marks[1].record(main)
-        self._ck(lib.ds_cg_spmv_dot(ctypes.byref(self.d_local), self.p_full.data_ptr(),
-                                    self.ap.data_ptr(), 0, None, None, 0, s, None, None, 0, ws,
-                                    stream))
-        if self._marks is not None:
-            self._marks[2].record(main)
-        main.wait_stream(self.side)
-        self._ck(lib.ds_cg_spmv_dot(ctypes.byref(self.d_remote), self.p_full.data_ptr() + 8 * self.n,
-                                    self.ap.data_ptr(), 1, self.p.data_ptr(), self._mine(0), PAP,
-                                    s, hist, None, 0, ws, stream))
+        if self.fold:   # world size 1: local SpMV + fused partition p.Ap
+            self._ck(lib.ds_cg_spmv_dot(ctypes.byref(self.d_local), self.p_full.data_ptr(),
+                                        self.ap.data_ptr(), 2, self.p.data_ptr(), self._mine(0),
+                                        PAP, s, hist, None, 0, ws, stream))
+            if self._marks is not None:
+                self._marks[2].record(main)
+            main.wait_stream(self.side)
+        else:
+            self._ck(lib.ds_cg_spmv_dot(ctypes.byref(self.d_local), self.p_full.data_ptr(),
+                                        self.ap.data_ptr(), 0, None, None, 0, s, None, None, 0,
+                                        ws, stream))
+            if self._marks is not None:
+                self._marks[2].record(main)
+            main.wait_stream(self.side)
+            self._ck(lib.ds_cg_spmv_dot(ctypes.byref(self.d_remote),
+                                        self.p_full.data_ptr() + 8 * self.n, self.ap.data_ptr(), 1,
+                                        self.p.data_ptr(), self._mine(0), PAP, s, hist, None, 0,
+                                        ws, stream))
         self._gather(0, stream)
-        self._ck(lib.ds_cg_finalize(PAP, s, hist, self._allp(0), self.P, stream))
-        self._ck(lib.ds_cg_update(self.n, self.x.data_ptr(), self.r.data_ptr(), self.p.data_ptr(),
-                                  self.ap.data_ptr(), s, self._mine(1), hist, None, 0, ws, stream))
+        # alpha from the rank-ordered sum of the gathered p.Ap, x/r update,
+        # this partition's r.r -> all-gather -> history / beta / p update
+        self._ck(lib.ds_cg_update_gathered(self.n, self.x.data_ptr(), self.r.data_ptr(),
+                                           self.p.data_ptr(), self.ap.data_ptr(), s,
+                                           self._allp(0), self.P, self._mine(1), ws, stream))
         self._gather(1, stream)
-        self._ck(lib.ds_cg_finalize(RR, s, hist, self._allp(1), self.P, stream))
-        self._ck(lib.ds_cg_direction(self.n, self.r.data_ptr(), self.p.data_ptr(), s, stream))
+        self._ck(lib.ds_cg_direction_gathered(self.n, self.r.data_ptr(), self.p.data_ptr(), s,
+                                              hist, self._allp(1), self.P, ws, stream))
 
     def scalars(self) -> _native.DsCgScalars:
         return _native.DsCgScalars.from_buffer_copy(self.scal.cpu().numpy().tobytes())
@@ -234,7 +249,7 @@ class RankCG:
 
     def launches_per_step(self) -> int:
         packs = sum(1 for s in self.sched.send_idx if s.size)
-        return packs + 2 + 1 + 1 + 1 + 1   # packs, 2 SpMV, 2 finalize, update, direction
+        return packs + (1 if self.fold else 2) + 2    # packs, SpMV(s), update, direction
 
     def time_spmv_in_steps(self, steps: int, stream_handle=None) -> dict:
         import torch
