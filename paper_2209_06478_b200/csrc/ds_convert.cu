@@ -212,7 +212,11 @@ __global__ void reduce_runs(int64_t nnz, int64_t ncols, const unsigned long long
   }
 }
 
-// DIA source: per-row count of nonzero in-range slots
+// DIA source: the (rows x ndiags) slab of a block is copied to shared
+// memory with coalesced loads, then one thread per row walks its row there
+// (a thread-per-row walk over global memory reads 8*ndiags-byte strided rows
+// and thrashes L1: 1 ms -> ~0.1 ms at 104^3).
+// DIA source fallback for slabs that do not fit shared memory
 struct DiaRowCount {
   int nrows, ncols, nd;
   const int* off;
@@ -226,9 +230,9 @@ struct DiaRowCount {
     return cnt;
   }
 };
-__global__ void dia_emit(int nrows, int ncols, int nd, const int* __restrict__ off,
-                         const double* __restrict__ vals, const int* __restrict__ start,
-                         int* r, int* c, double* v) {
+__global__ void dia_emit_direct(int nrows, int ncols, int nd, const int* __restrict__ off,
+                                const double* __restrict__ vals, const int* __restrict__ start,
+                                int* r, int* c, double* v) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nrows; i += gridDim.x * blockDim.x) {
     int o = start[i];
     for (int j = 0; j < nd; ++j) {
@@ -241,6 +245,79 @@ __global__ void dia_emit(int nrows, int ncols, int nd, const int* __restrict__ o
         ++o;
       }
     }
+  }
+}
+
+constexpr int kDiaWalkRows = 128;
+
+__device__ __forceinline__ int dia_stage_slab(const double* __restrict__ vals, int nrows, int nd,
+                                              int r0, double* slab) {
+  const int rows = min(kDiaWalkRows, nrows - r0);
+  const int64_t base = (int64_t)r0 * nd;
+  const int total = rows * nd;
+  for (int k = threadIdx.x; k < total; k += blockDim.x) slab[k] = vals[base + k];
+  __syncthreads();
+  return rows;
+}
+
+__global__ void dia_row_counts(int nrows, int ncols, int nd, const int* __restrict__ off,
+                               const double* __restrict__ vals, int* counts) {
+  extern __shared__ double slab[];
+  for (int r0 = blockIdx.x * kDiaWalkRows; r0 < nrows; r0 += gridDim.x * kDiaWalkRows) {
+    const int rows = dia_stage_slab(vals, nrows, nd, r0, slab);
+    if (threadIdx.x < rows) {
+      const int i = r0 + threadIdx.x;
+      int cnt = 0;
+      for (int j = 0; j < nd; ++j) {
+        const int64_t col = (int64_t)i + off[j];
+        if (col >= 0 && col < ncols && slab[threadIdx.x * nd + j] != 0.0) ++cnt;
+      }
+      counts[i] = cnt;
+    }
+    __syncthreads();
+  }
+}
+
+struct ArrayAt {
+  const int* a;
+  __device__ int operator()(int64_t k) const { return a[k]; }
+};
+
+// emit with both the input slab and the output range staged in shared
+// memory: the block's entries are contiguous in the canonical COO
+// ([start[r0], start[r0+rows])), so the final copy-out is coalesced
+__global__ void dia_emit(int nrows, int ncols, int nd, const int* __restrict__ off,
+                         const double* __restrict__ vals, const int* __restrict__ start,
+                         int nnz_total, int* r, int* c, double* v) {
+  extern __shared__ double slab[];
+  double* ov = slab + (size_t)kDiaWalkRows * nd;                 // rows*nd values
+  int* orow = reinterpret_cast<int*>(ov + (size_t)kDiaWalkRows * nd);
+  int* ocol = orow + kDiaWalkRows * nd;
+  for (int r0 = blockIdx.x * kDiaWalkRows; r0 < nrows; r0 += gridDim.x * kDiaWalkRows) {
+    const int rows = dia_stage_slab(vals, nrows, nd, r0, slab);
+    const int e0 = start[r0];
+    const int e1 = (r0 + rows < nrows) ? start[r0 + rows] : nnz_total;
+    if (threadIdx.x < rows) {
+      const int i = r0 + threadIdx.x;
+      int o = start[i] - e0;
+      for (int j = 0; j < nd; ++j) {
+        const int64_t col = (int64_t)i + off[j];
+        const double x = slab[threadIdx.x * nd + j];
+        if (col >= 0 && col < ncols && x != 0.0) {
+          orow[o] = i;
+          ocol[o] = (int)col;
+          ov[o] = x;
+          ++o;
+        }
+      }
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < e1 - e0; k += blockDim.x) {
+      r[e0 + k] = orow[k];
+      c[e0 + k] = ocol[k];
+      v[e0 + k] = ov[k];
+    }
+    __syncthreads();
   }
 }
 
@@ -260,11 +337,20 @@ __global__ void rows_to_offsets(int64_t nnz, int nrows, const int* __restrict__ 
   }
 }
 
+// Presence flags of every diagonal.  Few distinct diagonals are hit by very
+// many entries (27 for the stencil) and same-address stores serialise in L2.
+// Test first with an L1-CACHED load: an SM's own store invalidates its L1
+// line, the next miss brings back the 1, so every SM writes each flag about
+// once and all other tests hit L1 (a racing duplicate store of 1 is harmless).
 __global__ void mark_diags(int64_t nnz, int nrows, const int* __restrict__ r,
                            const int* __restrict__ c, unsigned char* flags) {
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz;
-       k += (int64_t)gridDim.x * blockDim.x)
-    flags[(int64_t)c[k] - r[k] + nrows - 1] = 1;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t d = (int64_t)c[k] - r[k] + nrows - 1;
+    unsigned short v;
+    asm volatile("ld.global.ca.u8 %0, [%1];" : "=h"(v) : "l"(flags + d));
+    if (v == 0) flags[d] = 1;
+  }
 }
 struct FlagAt {
   const unsigned char* f;
@@ -497,10 +583,28 @@ extern "C" int ds_convert_begin_dia(int64_t nrows, int64_t ncols, int32_t ndiags
   cudaStream_t st = j->st;
   int64_t nc = 0;
   if (nrows > 0 && ndiags > 0) {
-    int* start = nullptr;
+    int *counts = nullptr, *start = nullptr;
+    DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&counts), nrows * sizeof(int), st));
     DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&start), nrows * sizeof(int), st));
-    int rc = exclusive_scan(nrows, DiaRowCount{(int)nrows, (int)ncols, ndiags, offsets, values},
-                            start, &nc, st);
+    const size_t slab = (size_t)kDiaWalkRows * ndiags * sizeof(double);
+    const size_t emit_smem = slab * 2 + (size_t)kDiaWalkRows * ndiags * 8;   // + rows, cols
+    const bool staged = emit_smem <= 200 * 1024;
+    const unsigned gw = (unsigned)min64(ceil_div(nrows, kDiaWalkRows), (int64_t)sm_count() * 8);
+    if (staged) {
+      int rc0 = allow_dynamic_smem(reinterpret_cast<const void*>(dia_row_counts), slab);
+      if (!rc0) rc0 = allow_dynamic_smem(reinterpret_cast<const void*>(dia_emit), emit_smem);
+      if (rc0) {
+        free_job(j);
+        return rc0;
+      }
+      dia_row_counts<<<gw, kDiaWalkRows, slab, st>>>((int)nrows, (int)ncols, ndiags, offsets,
+                                                     values, counts);
+      DS_LAUNCH_CHECK("dia_row_counts");
+    }
+    int rc = staged ? exclusive_scan(nrows, ArrayAt{counts}, start, &nc, st)
+                    : exclusive_scan(nrows,
+                                     DiaRowCount{(int)nrows, (int)ncols, ndiags, offsets, values},
+                                     start, &nc, st);
     if (rc) {
       free_job(j);
       return rc;
@@ -510,10 +614,15 @@ extern "C" int ds_convert_begin_dia(int64_t nrows, int64_t ncols, int32_t ndiags
       DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&j->c), nc * 4, st));
       DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&j->v), nc * 8, st));
       j->own_r = j->own_c = j->own_v = true;
-      dia_emit<<<grid1d(nrows), 256, 0, st>>>((int)nrows, (int)ncols, ndiags, offsets, values,
-                                              start, j->r, j->c, j->v);
+      if (staged)
+        dia_emit<<<gw, kDiaWalkRows, emit_smem, st>>>((int)nrows, (int)ncols, ndiags, offsets,
+                                                      values, start, (int)nc, j->r, j->c, j->v);
+      else
+        dia_emit_direct<<<grid1d(nrows), 256, 0, st>>>((int)nrows, (int)ncols, ndiags, offsets,
+                                                       values, start, j->r, j->c, j->v);
       DS_LAUNCH_CHECK("dia_emit");
     }
+    DS_CUDA(cudaFreeAsync(counts, st));
     DS_CUDA(cudaFreeAsync(start, st));
   }
   j->nnz = nc;

@@ -202,16 +202,18 @@ __global__ void dia_diag_column_kernel(int64_t n, int nd, int j0, double* vals, 
   }
 }
 
+// nonzero in-range slots: one warp per row, lane j checks slot j (no 64-bit
+// divisions; the row's nd values are one coalesced 8*nd-byte segment)
 __global__ void dia_nonzero_kernel(int nrows, int ncols, int nd, const int* __restrict__ off,
                                    const double* __restrict__ vals, unsigned long long* count) {
   unsigned long long c = 0;
-  const int64_t total = (int64_t)nrows * nd;
-  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < total;
-       s += (int64_t)gridDim.x * blockDim.x) {
-    const int i = (int)(s / nd), j = (int)(s % nd);
-    const int64_t c0 = (int64_t)i + off[j];
-    if (c0 >= 0 && c0 < ncols && vals[s] != 0.0) ++c;
-  }
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nrows; i += warps)
+    for (int j = lane; j < nd; j += 32) {
+      const int64_t c0 = i + off[j];
+      if (c0 >= 0 && c0 < ncols && vals[i * nd + j] != 0.0) ++c;
+    }
   for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
 }
@@ -734,8 +736,8 @@ extern "C" int ds_dia_count_nonzero(int64_t nrows, int64_t ncols, int32_t ndiags
   unsigned long long* dc = nullptr;
   DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dc), sizeof(*dc), st));
   DS_CUDA(cudaMemsetAsync(dc, 0, sizeof(*dc), st));
-  dia_nonzero_kernel<<<grid_for(nrows * ndiags), kVecBlock, 0, st>>>((int)nrows, (int)ncols,
-                                                                      ndiags, offsets, values, dc);
+  dia_nonzero_kernel<<<(unsigned)min64(ceil_div(nrows, 8), (int64_t)sm_count() * 16), kVecBlock,
+                       0, st>>>((int)nrows, (int)ncols, ndiags, offsets, values, dc);
   DS_LAUNCH_CHECK("dia_nonzero_kernel");
   unsigned long long h = 0;
   DS_CUDA(cudaMemcpyAsync(&h, dc, sizeof(h), cudaMemcpyDeviceToHost, st));
