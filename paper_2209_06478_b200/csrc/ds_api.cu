@@ -1,5 +1,6 @@
 // ds_api.cu -- error state and device queries of the C ABI.
 #include <stdarg.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <mutex>
@@ -74,6 +75,35 @@ int allow_dynamic_smem(const void* kernel, size_t bytes) {
   }
   DS_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, room));
   return DS_OK;
+}
+
+bool x_window_begin(cudaStream_t st, const void* base, size_t bytes) {
+  static int max_persist[64] = {0}, max_window[64] = {0}, done[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return false;
+  if (!getenv("DS_L2_WINDOW")) return false;   // measured slower (profiles/r01/README.md): opt-in
+  if (!done[dev]) {
+    cudaDeviceGetAttribute(&max_persist[dev], cudaDevAttrMaxPersistingL2CacheSize, dev);
+    cudaDeviceGetAttribute(&max_window[dev], cudaDevAttrMaxAccessPolicyWindowSize, dev);
+    if (max_persist[dev] > 0) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, max_persist[dev]);
+    done[dev] = 1;
+  }
+  if (max_persist[dev] <= 0 || max_window[dev] <= 0) return false;
+  cudaStreamAttrValue a = {};
+  a.accessPolicyWindow.base_ptr = const_cast<void*>(base);
+  a.accessPolicyWindow.num_bytes = bytes < (size_t)max_window[dev] ? bytes : (size_t)max_window[dev];
+  const double fit = (double)max_persist[dev] / (double)a.accessPolicyWindow.num_bytes;
+  a.accessPolicyWindow.hitRatio = (float)(fit < 1.0 ? fit : 1.0);
+  a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  return cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &a) == cudaSuccess;
+}
+
+void x_window_end(cudaStream_t st) {
+  cudaStreamAttrValue a = {};
+  a.accessPolicyWindow.num_bytes = 0;
+  cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &a);
+  cudaCtxResetPersistingL2Cache();
 }
 
 }  // namespace ds

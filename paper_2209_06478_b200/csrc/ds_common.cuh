@@ -43,6 +43,11 @@ int cuda_fail(cudaError_t e, const char* what);
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 int sm_count();           // cached per device
+// Pin [base, base+bytes) in L2 (persisting access-policy window on the
+// stream) for the gathered vector of irregular SpMV; returns false if the
+// device offers no persisting L2.  x_window_end() resets the stream.
+bool x_window_begin(cudaStream_t st, const void* base, size_t bytes);
+void x_window_end(cudaStream_t st);
 int max_dynamic_smem();   // opt-in shared memory per block (bytes), cached per device
 // raise a kernel's dynamic shared-memory limit to `bytes` (minus its static use)
 int allow_dynamic_smem(const void* kernel, size_t bytes);
@@ -69,6 +74,32 @@ __device__ __forceinline__ int ld_stream(const int* p) {
 }
 // gathered vector entries: keep in L1/L2
 __device__ __forceinline__ double ld_gather(const double* p) { return __ldg(p); }
+
+// L2 eviction-priority policies: the matrix arrays are streamed once
+// (evict_first) so that the gathered vector -- up to tens of MB, e.g. the
+// 33.5 MB x of the 4.2M-row power-law matrix -- stays L2-resident
+// (evict_last) instead of being re-fetched from HBM one 32-B sector per
+// 8-B gather.
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t policy_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ int ld_hint(const int* p, uint64_t pol) {
+  int v;
+  asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ld_hint(const double* p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
 
 // ------------------------------------------------------- mbarrier + TMA -----
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

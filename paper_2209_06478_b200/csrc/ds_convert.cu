@@ -518,6 +518,52 @@ static int begin_common(ds_convert_job* job, int64_t fill_limit, ds_convert_job*
 
 using namespace ds;
 
+// ---------------------------------------------------------------- CSR bins --
+__device__ __forceinline__ int csr_bin_of(int len) {
+  if (len == 0) return 0;
+  if (len <= 9) return 1;
+  if (len <= 17) return 2;
+  if (len <= 25) return 3;
+  if (len <= 33) return 4;
+  if (len <= 129) return 5;
+  return 6;
+}
+struct IsBin {
+  const int* off;
+  int b;
+  __device__ int operator()(int64_t r) const { return csr_bin_of(off[r + 1] - off[r]) == b; }
+};
+__global__ void bin_scatter(int nrows, const int* __restrict__ off, int b, const int* __restrict__ pos,
+                            int64_t base, int* perm) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += gridDim.x * blockDim.x)
+    if (csr_bin_of(off[r + 1] - off[r]) == b) perm[base + pos[r]] = r;
+}
+
+extern "C" int ds_csr_bins(int64_t nrows, const int32_t* row_offsets, int32_t* perm, int64_t* bins,
+                           void* stream) {
+  cudaStream_t st = as_stream(stream);
+  for (int b = 0; b < 8; ++b) bins[b] = 0;
+  if (nrows <= 0) return DS_OK;
+  int* pos = nullptr;
+  DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&pos), nrows * sizeof(int), st));
+  int64_t base = 0;
+  for (int b = 0; b < 7; ++b) {   // stable: rows ascending inside every bin
+    int64_t cnt = 0;
+    int rc = exclusive_scan(nrows, IsBin{row_offsets, b}, pos, &cnt, st);
+    if (rc) return rc;
+    bins[b] = base;
+    if (cnt) {
+      bin_scatter<<<grid1d(nrows), 256, 0, st>>>((int)nrows, row_offsets, b, pos, base, perm);
+      DS_LAUNCH_CHECK("bin_scatter");
+    }
+    base += cnt;
+  }
+  bins[7] = base;
+  DS_CUDA(cudaFreeAsync(pos, st));
+  DS_CUDA(cudaStreamSynchronize(st));
+  return DS_OK;
+}
+
 static ds_convert_job* new_job(int64_t nrows, int64_t ncols, int target, void* stream) {
   ds_convert_job* job = new ds_convert_job;
   job->st = as_stream(stream);

@@ -182,6 +182,8 @@ __device__ double csr_group_pairwise(const int* __restrict__ col, const double* 
 
 constexpr int kCsrBlock = 256;
 constexpr int kLongRow = 129;  // rows longer than this need the recursion
+constexpr int kSub = 8192;     // <= 128 leaves per subtree / warp-kernel row limit
+constexpr int kMaxLeaves = 160;
 
 // One 8-lane group per PAIR of consecutive rows; grid-stride over pairs.
 // Rows of <= 33 entries (the stencil's 8..27, the power-law's typical 6..33)
@@ -251,6 +253,136 @@ __global__ void __launch_bounds__(kCsrBlock)
       if (has_b)
         csr_row_general<ACCUM, SKIP_LONG, FUSE_DOT>(rb, ea, lb, col, val, x, y, lane8, mask,
                                                     dot, dsum);
+    }
+  }
+  if (FUSE_DOT) dot.finish_block<kCsrBlock>(dsum);
+}
+
+// ---------------------------------------------------------------------------
+// Binned CSR (irregular matrices).  Rows are grouped by length bin
+// (ds_csr_bins): each bin runs with its exact number of load rounds R
+// (bin b in 1..4: rows of <= 8b+1 entries -> R = b), so there is neither
+// round padding nor per-lane predication; two rows per 8-lane group keep
+// 2R load chains in flight.  Work item = a pair of consecutive rows of the
+// permuted list; items of all bins are enumerated in one grid-stride loop.
+struct CsrBins {
+  int64_t start[8];     // bin b rows = perm[start[b] .. start[b+1])
+  int64_t pair_off[8];  // cumulative work items (kBinRows[b] rows each) before bin b
+};
+// rows per work item (8-lane group) per bin: empty, R=1, R=2, R=3, R=4, general
+__constant__ int kBinRows[7] = {4, 4, 4, 2, 2, 2, 1};
+static const int kBinRowsHost[7] = {4, 4, 4, 2, 2, 2, 1};
+
+template <int R>
+__device__ __forceinline__ void binned_load(const int* __restrict__ col,
+                                            const double* __restrict__ val, int start, int len,
+                                            int lane8, int (&c)[R], double (&v)[R], int& c0,
+                                            double& v0, uint64_t pol) {
+  const int m = len - 1;
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const int i = max(min(lane8 + 8 * k, m - 1), -1);   // -1 -> p[first]: in bounds
+    c[k] = ld_hint(col + start + 1 + i, pol);
+    v[k] = ld_hint(val + start + 1 + i, pol);
+  }
+  c0 = ld_hint(col + start, pol);
+  v0 = ld_hint(val + start, pol);
+}
+
+template <int R>
+__device__ __forceinline__ double binned_finish(int len, int lane8, unsigned mask,
+                                                const double (&a)[R], double p0) {
+  const int m = len - 1;
+  const int full = m & ~7, nfull = full >> 3;
+  double r = 0.0, tail = 0.0;
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    if (k < nfull) r = (k == 0) ? a[k] : add(r, a[k]);
+    else if (k == nfull) tail = a[k];
+  }
+  double res;
+  if (full > 0) {
+    r = add(r, __shfl_xor_sync(mask, r, 1, 8));
+    r = add(r, __shfl_xor_sync(mask, r, 2, 8));
+    r = add(r, __shfl_xor_sync(mask, r, 4, 8));
+    res = r;
+  } else {
+    res = -0.0;
+  }
+  const int ntail = m - full;
+  for (int t = 0; t < ntail; ++t) res = add(res, __shfl_sync(mask, tail, t, 8));
+  return add(p0, res);
+}
+
+// U rows per 8-lane group, all U*R loads and gathers issued before any
+// reduction (short rows have little work each: more rows = more MLP)
+template <int R, int U, bool ACCUM, bool FUSE_DOT>
+__device__ __forceinline__ void binned_rows(const int* rws, int nr, const int* __restrict__ off,
+                                            const int* __restrict__ col,
+                                            const double* __restrict__ val,
+                                            const double* __restrict__ x, double* y, int lane8,
+                                            unsigned mask, const DotOut& dot, double& dsum,
+                                            uint64_t pf, uint64_t pl) {
+  int st[U], ln[U], c[U][R], c0[U];
+  double v[U][R], v0[U], a[U][R], p0[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int row = rws[min(u, nr - 1)];
+    st[u] = __ldg(off + row);
+    ln[u] = __ldg(off + row + 1) - st[u];
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+    binned_load<R>(col, val, st[u], ln[u], lane8, c[u], v[u], c0[u], v0[u], pf);
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+#pragma unroll
+    for (int k = 0; k < R; ++k) a[u][k] = mul(v[u][k], ld_hint(x + c[u][k], pl));
+    p0[u] = mul(v0[u], ld_hint(x + c0[u], pl));
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const double yv = binned_finish<R>(ln[u], lane8, mask, a[u], p0[u]);
+    if (lane8 == 0 && u < nr) csr_emit<ACCUM, false, FUSE_DOT>(rws[u], ln[u], yv, y, dot, dsum);
+  }
+}
+
+template <bool ACCUM, bool FUSE_DOT>
+__global__ void __launch_bounds__(kCsrBlock)
+    csr_binned(const int* __restrict__ off, const int* __restrict__ col,
+               const double* __restrict__ val, const double* __restrict__ x, double* y,
+               const int* __restrict__ perm, CsrBins bi, DotOut dot) {
+  if (dot.skip()) return;
+  const int lane8 = threadIdx.x & 7;
+  const unsigned mask = 0xffu << (threadIdx.x & 24);
+  const int64_t groups = ((int64_t)gridDim.x * kCsrBlock) >> 3;
+  const int64_t W = bi.pair_off[6];
+  const uint64_t pf = policy_first(), pl = policy_evict_last();
+  double dsum = 0.0;
+  for (int64_t w = ((int64_t)blockIdx.x * kCsrBlock + threadIdx.x) >> 3; w < W; w += groups) {
+    int b = 0;
+#pragma unroll
+    for (int k = 1; k < 6; ++k) b += (w >= bi.pair_off[k]);
+    const int U = kBinRows[b];
+    const int64_t q = bi.start[b] + (int64_t)U * (w - bi.pair_off[b]);
+    const int nr = (int)min64(U, bi.start[b + 1] - q);
+    const int* rws = perm + q;
+    switch (b) {
+      case 0:
+        if (lane8 == 0)
+          for (int u = 0; u < nr; ++u) csr_emit<ACCUM, false, FUSE_DOT>(rws[u], 0, 0.0, y, dot, dsum);
+        break;
+      case 1: binned_rows<1, 4, ACCUM, FUSE_DOT>(rws, nr, off, col, val, x, y, lane8, mask, dot, dsum, pf, pl); break;
+      case 2: binned_rows<2, 4, ACCUM, FUSE_DOT>(rws, nr, off, col, val, x, y, lane8, mask, dot, dsum, pf, pl); break;
+      case 3: binned_rows<3, 2, ACCUM, FUSE_DOT>(rws, nr, off, col, val, x, y, lane8, mask, dot, dsum, pf, pl); break;
+      case 4: binned_rows<4, 2, ACCUM, FUSE_DOT>(rws, nr, off, col, val, x, y, lane8, mask, dot, dsum, pf, pl); break;
+      default:
+        for (int u = 0; u < nr; ++u) {
+          const int row = rws[u];
+          const int sr = __ldg(off + row);
+          csr_row_general<ACCUM, true, FUSE_DOT>(row, sr, __ldg(off + row + 1) - sr, col, val, x,
+                                                 y, lane8, mask, dot, dsum);
+        }
     }
   }
   if (FUSE_DOT) dot.finish_block<kCsrBlock>(dsum);
@@ -512,8 +644,88 @@ static int csr_tiles_launch(int64_t nrows, int64_t nnz, const int* off, const in
 // at most kSub addends; each subtree's leaves (64..128 addends each) are
 // summed by the CTA's 32 lane-groups in parallel, then thread 0 replays the
 // recursion to combine them in numpy's order.
-constexpr int kSub = 8192;           // <= 128 leaves per subtree
-constexpr int kMaxLeaves = 160;
+
+// Warp per long row (kLongRow < len <= kSub): lane 0 enumerates the pairwise
+// recursion's leaves (64..128 addends each) into warp-private shared memory,
+// the warp's four 8-lane groups sum leaves in parallel, lane 0 replays the
+// recursion to combine them.  No block-wide barriers, 8 rows per CTA.
+constexpr int kWarpLeaves = 128;
+
+template <bool ACCUM>
+__global__ void __launch_bounds__(kCsrBlock)
+    csr_long_rows_warp(const int* __restrict__ rows, int n, const int* __restrict__ off,
+                       const int* __restrict__ col, const double* __restrict__ val,
+                       const double* __restrict__ x, double* y, const int* guard) {
+  if (guard && *guard) return;
+  __shared__ int s_lo[kCsrBlock / 32][kWarpLeaves];
+  __shared__ short s_n[kCsrBlock / 32][kWarpLeaves];
+  __shared__ double s_v[kCsrBlock / 32][kWarpLeaves];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, lane8 = lane & 7, grp = lane >> 3;
+  const unsigned mask = 0xffu << (lane & 24);
+  struct Frame {
+    int lo, n, expanded;
+  };
+  const int nw = gridDim.x * (kCsrBlock / 32);
+  for (int li = blockIdx.x * (kCsrBlock / 32) + w; li < n; li += nw) {
+    const int row = rows[li];
+    const int start = off[row];
+    const int m = off[row + 1] - start - 1;
+    if (m + 1 > kSub) continue;          // the CTA kernel owns it
+    int nl = 0;
+    if (lane == 0) {                      // leaves left to right
+      Frame st[32];
+      int ft = 0;
+      st[ft++] = {0, m, 0};
+      while (ft > 0) {
+        Frame f = st[--ft];
+        if (f.n <= 128) {
+          s_lo[w][nl] = f.lo;
+          s_n[w][nl] = (short)f.n;
+          ++nl;
+        } else {
+          int n2 = f.n / 2;
+          n2 -= n2 % 8;
+          st[ft++] = {f.lo + n2, f.n - n2, 0};
+          st[ft++] = {f.lo, n2, 0};
+        }
+      }
+    }
+    nl = __shfl_sync(0xffffffffu, nl, 0);
+    __syncwarp();
+    for (int l = grp; l < nl; l += 4) {
+      const double v = csr_leaf_g8(col, val, x, (int64_t)start + 1 + s_lo[w][l], s_n[w][l],
+                                   lane8, mask);
+      if (lane8 == 0) s_v[w][l] = v;
+    }
+    __syncwarp();
+    if (lane == 0) {                      // combine in recursion order
+      Frame st[32];
+      double vs[32];
+      int ft = 0, vt = 0, next = 0;
+      st[ft++] = {0, m, 0};
+      while (ft > 0) {
+        Frame f = st[--ft];
+        if (f.n <= 128) {
+          vs[vt++] = s_v[w][next++];
+        } else if (!f.expanded) {
+          int n2 = f.n / 2;
+          n2 -= n2 % 8;
+          st[ft++] = {f.lo, f.n, 1};
+          st[ft++] = {f.lo + n2, f.n - n2, 0};
+          st[ft++] = {f.lo, n2, 0};
+        } else {
+          const double b = vs[--vt];
+          const double a = vs[--vt];
+          vs[vt++] = add(a, b);
+        }
+      }
+      const double p0 = mul(val[start], __ldg(x + col[start]));
+      const double sres = add(p0, vs[0]);
+      y[row] = ACCUM ? add(y[row], sres) : sres;
+    }
+    __syncwarp();
+  }
+}
 
 template <bool ACCUM>
 __global__ void __launch_bounds__(kCsrBlock)
@@ -536,6 +748,7 @@ __global__ void __launch_bounds__(kCsrBlock)
     const int row = long_rows[li];
     const int64_t start = off[row];
     const int64_t m = (int64_t)off[row + 1] - start - 1;
+    if (m + 1 <= kSub) continue;   // csr_long_rows_warp owns it
     const int64_t base = start + 1;
     // thread-0 top-level DFS state
     Frame st[48];
@@ -635,6 +848,64 @@ __global__ void csr_find_long(int nrows, const int* __restrict__ off, int* long_
   }
 }
 
+int launch_csr_binned(int64_t nrows, int64_t ncols, const int* off, const int* col,
+                      const double* val, const int* perm, const int64_t* bins, const double* x,
+                      double* y, bool accum, const DotOut* dot, cudaStream_t st) {
+  if (nrows == 0) return DS_OK;
+  DotOut d = dot ? *dot : DotOut{};
+  const bool fuse = d.fused();
+  const int64_t n_long = bins[7] - bins[6];
+  if (fuse && n_long > 0) {
+    set_error("fused dot with long rows is not supported");
+    return DS_ERR_NOT_SUPPORTED;
+  }
+  CsrBins bi;
+  int64_t acc = 0;
+  for (int b = 0; b < 8; ++b) bi.start[b] = bins[b];
+  for (int b = 0; b < 6; ++b) {
+    bi.pair_off[b] = acc;
+    acc += ceil_div(bins[b + 1] - bins[b], kBinRowsHost[b]);
+  }
+  bi.pair_off[6] = acc;
+  bi.pair_off[7] = acc;
+  int64_t blocks = ceil_div(acc * 8, kCsrBlock);
+  const int64_t cap = (int64_t)sm_count() * 8;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  if (fuse) blocks = d.clamp_grid(blocks);
+  // the binned path serves irregular matrices whose x is gathered at random:
+  // keep x persisting in L2 while the row stream passes through
+  const bool win = x_window_begin(st, x, (size_t)ncols * 8);
+#define DS_CSRB(A, F) \
+  csr_binned<A, F><<<(unsigned)blocks, kCsrBlock, 0, st>>>(off, col, val, x, y, perm, bi, d)
+  if (accum) {
+    if (fuse) DS_CSRB(true, true); else DS_CSRB(true, false);
+  } else {
+    if (fuse) DS_CSRB(false, true); else DS_CSRB(false, false);
+  }
+#undef DS_CSRB
+  DS_LAUNCH_CHECK("csr_binned");
+  if (n_long > 0) {
+    const int* long_rows = perm + bins[6];
+    int64_t lb = n_long < (int64_t)sm_count() * 8 ? n_long : (int64_t)sm_count() * 8;
+    const int64_t lw = min64(ceil_div(n_long, kCsrBlock / 32), (int64_t)sm_count() * 8);
+    if (accum) {
+      csr_long_rows_warp<true><<<(unsigned)lw, kCsrBlock, 0, st>>>(long_rows, (int)n_long, off,
+                                                                  col, val, x, y, d.guard);
+      csr_long_rows<true><<<(unsigned)lb, kCsrBlock, 0, st>>>(long_rows, (int)n_long, off, col,
+                                                             val, x, y, d.guard);
+    } else {
+      csr_long_rows_warp<false><<<(unsigned)lw, kCsrBlock, 0, st>>>(long_rows, (int)n_long, off,
+                                                                   col, val, x, y, d.guard);
+      csr_long_rows<false><<<(unsigned)lb, kCsrBlock, 0, st>>>(long_rows, (int)n_long, off, col,
+                                                              val, x, y, d.guard);
+    }
+    DS_LAUNCH_CHECK("csr_long_rows");
+  }
+  if (win) x_window_end(st);
+  return DS_OK;
+}
+
 int launch_csr(int64_t nrows, int64_t nnz, const int* off, const int* col, const double* val,
                const int* long_rows, int64_t n_long, const double* x, double* y, bool accum,
                const DotOut* dot, cudaStream_t st) {
@@ -665,12 +936,18 @@ int launch_csr(int64_t nrows, int64_t nnz, const int* off, const int* col, const
     if (rc) return rc;
     if (skip && n_long > 0) {
       int64_t lb = n_long < (int64_t)sm_count() * 8 ? n_long : (int64_t)sm_count() * 8;
-      if (accum)
+      const int64_t lw = min64(ceil_div(n_long, kCsrBlock / 32), (int64_t)sm_count() * 8);
+      if (accum) {
+        csr_long_rows_warp<true><<<(unsigned)lw, kCsrBlock, 0, st>>>(long_rows, (int)n_long,
+                                                                    off, col, val, x, y, d.guard);
         csr_long_rows<true><<<(unsigned)lb, kCsrBlock, 0, st>>>(long_rows, (int)n_long, off, col,
                                                                val, x, y, d.guard);
-      else
+      } else {
+        csr_long_rows_warp<false><<<(unsigned)lw, kCsrBlock, 0, st>>>(long_rows, (int)n_long,
+                                                                     off, col, val, x, y, d.guard);
         csr_long_rows<false><<<(unsigned)lb, kCsrBlock, 0, st>>>(long_rows, (int)n_long, off,
                                                                 col, val, x, y, d.guard);
+      }
       DS_LAUNCH_CHECK("csr_long_rows");
     }
     return DS_OK;
@@ -693,12 +970,18 @@ int launch_csr(int64_t nrows, int64_t nnz, const int* off, const int* col, const
   DS_LAUNCH_CHECK("csr_rows_g8");
   if (skip && n_long > 0) {
     int64_t lb = n_long < (int64_t)sm_count() * 8 ? n_long : (int64_t)sm_count() * 8;
-    if (accum)
+    const int64_t lw = min64(ceil_div(n_long, kCsrBlock / 32), (int64_t)sm_count() * 8);
+    if (accum) {
+      csr_long_rows_warp<true><<<(unsigned)lw, kCsrBlock, 0, st>>>(long_rows, (int)n_long, off,
+                                                                  col, val, x, y, d.guard);
       csr_long_rows<true><<<(unsigned)lb, kCsrBlock, 0, st>>>(long_rows, (int)n_long, off, col,
                                                              val, x, y, d.guard);
-    else
+    } else {
+      csr_long_rows_warp<false><<<(unsigned)lw, kCsrBlock, 0, st>>>(long_rows, (int)n_long, off,
+                                                                   col, val, x, y, d.guard);
       csr_long_rows<false><<<(unsigned)lb, kCsrBlock, 0, st>>>(long_rows, (int)n_long, off, col,
                                                               val, x, y, d.guard);
+    }
     DS_LAUNCH_CHECK("csr_long_rows");
   }
   return DS_OK;

@@ -784,6 +784,13 @@ extern "C" int ds_cg_spmv_dot(const ds_matrix* a, const double* x, double* y, in
   bool done_dot = false;
   switch (a->format) {
     case DS_FMT_CSR: {
+      if (a->row_perm) {  // irregular matrix: length-binned kernels
+        const bool can_fuse = want_dot && a->bins[7] == a->bins[6];
+        rc = launch_csr_binned(a->nrows, a->ncols, a->idx0, a->idx1, a->values, a->row_perm,
+                               a->bins, x, y, acc, can_fuse ? &fused : &d, st);
+        done_dot = can_fuse;
+        break;
+      }
       const bool can_fuse = want_dot && (a->long_rows == nullptr || a->n_long == 0);
       rc = launch_csr(a->nrows, a->nnz, a->idx0, a->idx1, a->values, a->long_rows, a->n_long, x, y, acc,
                       can_fuse ? &fused : &d, st);

@@ -116,8 +116,27 @@ def csr_plan(m: CsrMatrix):
         # keep a valid pointer even when empty: non-NULL tells the C side the
         # matrix was analysed (rows > 129 are then handled by their own kernel)
         lr = buf[:max(nl, 1)].clone()
+        # irregular rows (longer than the 33-entry paired fast path): bin rows
+        # by length once, each bin then runs with its exact load rounds
+        if int(max_len.value) > 33:
+            perm = torch.empty(m.nrows, dtype=torch.int32, device=m.device)
+            bins = (ctypes.c_int64 * 8)()
+            with torch.cuda.device(m.device):
+                _native.call("ds_csr_bins", m.nrows, D.ptr(m.row_offsets), D.ptr(perm), bins,
+                             D.stream(m.device))
+            m._cache["bins"] = (k, perm, list(bins))
     m._cache["plan"] = (k, lr, nl)
     return lr, nl
+
+
+def csr_bins(m: CsrMatrix):
+    """(perm tensor, bins[8]) when the matrix was binned, else None."""
+    csr_plan(m)
+    hit = m._cache.get("bins")
+    k = ("plan",) + _key(m.row_offsets)
+    if hit is not None and hit[0] == k:
+        return hit[1], hit[2]
+    return None
 
 
 def coo_flags(m: CooMatrix) -> int:
@@ -149,6 +168,11 @@ def descriptor(m) -> _native.DsMatrix:
         d.idx0, d.idx1, d.values = D.ptr(m.row_offsets), D.ptr(m.col_indices), D.ptr(m.values)
         lr, nl = csr_plan(m)
         d.long_rows, d.n_long = (lr.data_ptr() if lr is not None else None), nl
+        b = csr_bins(m)
+        if b is not None:
+            d.row_perm = b[0].data_ptr()
+            for i in range(8):
+                d.bins[i] = b[1][i]
     elif isinstance(m, CooMatrix):
         d.format, d.nnz = int(FormatId.COO), m.nnz
         d.idx0, d.idx1, d.values = D.ptr(m.row_indices), D.ptr(m.col_indices), D.ptr(m.values)
