@@ -148,6 +148,27 @@ int ds_convert_finish_csr(ds_convert_job* job, int32_t* row_offsets, int32_t* co
 int ds_convert_finish_dia(ds_convert_job* job, int32_t* offsets, double* values);
 void ds_convert_abort(ds_convert_job* job);
 
+/* ---- on-device generate_problem for one partition (stencil.py:143-253) --
+ * begin sizes the partition (nnz, ghost count); the caller allocates
+ * row_offsets (n+1 int32), cols (nnz int32), vals (nnz f64), b (n f64) and
+ * ghost_keys (nghosts int64: owner*n + owner_local, ascending -- the ghost
+ * numbering, from which the halo plan follows); finish fills them.        */
+typedef struct ds_stencil_job ds_stencil_job;
+int ds_stencil_begin(int nx, int ny, int nz, int px, int py, int pz, int rank, void* stream,
+                     ds_stencil_job** job, int64_t* nnz, int64_t* nghosts);
+int ds_stencil_finish(ds_stencil_job* job, int32_t* row_offsets, int32_t* cols, double* vals,
+                      double* b, int64_t* ghost_keys);
+
+/* ---- split_local_remote on the device (stencil.py:256-277) ------------
+ * count: loc_off (nrows+1) and the local nnz; fill: both CSR parts (remote
+ * columns re-based by -n_owned; rem_off has nrows+1 entries).             */
+int ds_csr_split_count(int64_t nrows, int64_t n_owned, const int32_t* row_offsets,
+                       const int32_t* cols, int32_t* loc_off, int64_t* nnz_local, void* stream);
+int ds_csr_split_fill(int64_t nrows, int64_t n_owned, int64_t nnz, const int32_t* row_offsets,
+                      const int32_t* cols, const double* vals, const int32_t* loc_off,
+                      int64_t nnz_local, int32_t* loc_cols, double* loc_vals, int32_t* rem_off,
+                      int32_t* rem_cols, double* rem_vals, void* stream);
+
 /* ---- halo exchange pieces (stencil.py:280-319) ---------------------------
  * dst[k] = src[idx[k]]: packs a neighbour's send list, or -- single process,
  * all partitions visible (peer access enabled) -- writes the ghost slice

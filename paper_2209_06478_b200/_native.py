@@ -99,6 +99,12 @@ _SIGNATURES = {
     "ds_convert_finish_dia": (c_int, [c_vp, c_vp, c_vp]),
     "ds_convert_abort": (None, [c_vp]),
     "ds_gather": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "ds_stencil_begin": (c_int, [c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_vp,
+                                 ctypes.POINTER(c_vp), P_i64, P_i64]),
+    "ds_stencil_finish": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "ds_csr_split_count": (c_int, [c_i64, c_i64, c_vp, c_vp, c_vp, P_i64, c_vp]),
+    "ds_csr_split_fill": (c_int, [c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp,
+                                  c_vp, c_vp, c_vp, c_vp]),
     "ds_spmv": (c_int, [P_mat, c_vp, c_vp, c_int, c_vp]),
     "ds_cg_workspace_bytes": (c_i64, []),
     "ds_cg_spmv_dot": (c_int, [P_mat, c_vp, c_vp, c_int, c_vp, c_vp, c_int, c_vp, c_vp, c_vp,

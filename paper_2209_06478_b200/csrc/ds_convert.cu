@@ -564,6 +564,244 @@ extern "C" int ds_csr_bins(int64_t nrows, const int32_t* row_offsets, int32_t* p
   return DS_OK;
 }
 
+// ------------------------------------------------------- stencil generator --
+// On-device generate_problem for one partition (stencil.py:143-253): 27-point
+// couplings, x-fastest local numbering, rank = cx + px*(cy + py*cz), ghosts
+// numbered by sorted (owner*n + owner_local) keys, columns ascending per row,
+// values 26 / -1, b = 27 - row_len (exact row sums).  Integer-exact, so the
+// arrays are bitwise those of the host generator (tested).
+struct StencilGrid {
+  int nx, ny, nz, px, py, pz, rank;
+};
+
+__device__ __forceinline__ bool stencil_nbr(const StencilGrid& g, int64_t i, int t, int64_t n,
+                                            int& owner, int& oloc) {
+  const int dz = t / 9 - 1, dy = (t / 3) % 3 - 1, dx = t % 3 - 1;
+  const int cx = g.rank % g.px, cy = (g.rank / g.px) % g.py, cz = g.rank / (g.px * g.py);
+  const int lx = (int)(i % g.nx), ly = (int)((i / g.nx) % g.ny), lz = (int)(i / ((int64_t)g.nx * g.ny));
+  const int tx = lx + cx * g.nx + dx, ty = ly + cy * g.ny + dy, tz = lz + cz * g.nz + dz;
+  if (tx < 0 || ty < 0 || tz < 0 || tx >= g.nx * g.px || ty >= g.ny * g.py || tz >= g.nz * g.pz)
+    return false;
+  const int ox = tx / g.nx, oy = ty / g.ny, oz = tz / g.nz;
+  owner = ox + g.px * (oy + g.py * oz);
+  oloc = (tx - ox * g.nx) + g.nx * ((ty - oy * g.ny) + g.ny * (tz - oz * g.nz));
+  (void)n;
+  return true;
+}
+
+struct StencilCount {
+  StencilGrid g;
+  int64_t n;
+  int ghosts_only;
+  __device__ int operator()(int64_t i) const {
+    int c = 0, ow, ol;
+    for (int t = 0; t < 27; ++t)
+      if (stencil_nbr(g, i, t, n, ow, ol) && (!ghosts_only || ow != g.rank)) ++c;
+    return c;
+  }
+};
+
+__global__ void stencil_ghost_keys(StencilGrid g, int64_t n, const int* __restrict__ gpos,
+                                   unsigned long long* keys) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int o = gpos[i], ow, ol;
+    for (int t = 0; t < 27; ++t)
+      if (stencil_nbr(g, i, t, n, ow, ol) && ow != g.rank)
+        keys[o++] = (unsigned long long)ow * (unsigned long long)n + (unsigned long long)ol;
+  }
+}
+
+struct KeyHead {
+  const unsigned long long* k;
+  __device__ int operator()(int64_t i) const { return (i == 0 || k[i] != k[i - 1]) ? 1 : 0; }
+};
+__global__ void compact_keys(int64_t m, const unsigned long long* __restrict__ k,
+                             const int* __restrict__ pos, unsigned long long* out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (i == 0 || k[i] != k[i - 1]) out[pos[i]] = k[i];
+}
+
+__global__ void stencil_fill(StencilGrid g, int64_t n, const int* __restrict__ off,
+                             const unsigned long long* __restrict__ ukeys, int64_t G, int* cols,
+                             double* vals, double* b) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t c[27];
+    int cnt = 0, ow, ol;
+    for (int t = 0; t < 27; ++t) {
+      if (!stencil_nbr(g, i, t, n, ow, ol)) continue;
+      int64_t col;
+      if (ow == g.rank) {
+        col = ol;
+      } else {  // n + rank of the key among the sorted unique ghost keys
+        const unsigned long long key = (unsigned long long)ow * (unsigned long long)n + ol;
+        int64_t lo = 0, hi = G;
+        while (lo < hi) {
+          const int64_t mid = (lo + hi) >> 1;
+          if (ukeys[mid] < key) lo = mid + 1; else hi = mid;
+        }
+        col = n + lo;
+      }
+      int j = cnt++;  // insertion sort (<= 27 entries)
+      while (j > 0 && c[j - 1] > col) {
+        c[j] = c[j - 1];
+        --j;
+      }
+      c[j] = col;
+    }
+    const int o = off[i];
+    for (int j = 0; j < cnt; ++j) {
+      cols[o + j] = (int)c[j];
+      vals[o + j] = (c[j] == i) ? 26.0 : -1.0;
+    }
+    b[i] = (double)(27 - cnt);
+  }
+}
+
+struct ds_stencil_job {
+  cudaStream_t st;
+  StencilGrid g;
+  int64_t n, nnz, G;
+  int* offsets;                 // n+1 (owned by the job until finish)
+  unsigned long long* ukeys;    // G
+};
+
+extern "C" int ds_stencil_begin(int nx, int ny, int nz, int px, int py, int pz, int rank,
+                                void* stream, ds_stencil_job** job, int64_t* nnz,
+                                int64_t* nghosts) {
+  *job = nullptr;
+  cudaStream_t st = as_stream(stream);
+  const int64_t n = (int64_t)nx * ny * nz;
+  if (n <= 0 || n * 27 >= (1ll << 31) || (int64_t)px * py * pz * n >= (1ll << 62)) {
+    set_error("grid too large for int32 device indices");
+    return DS_ERR_NOT_SUPPORTED;
+  }
+  StencilGrid g{nx, ny, nz, px, py, pz, rank};
+  ds_stencil_job* j = new ds_stencil_job{st, g, n, 0, 0, nullptr, nullptr};
+  int* gpos = nullptr;
+  DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&j->offsets), (n + 1) * sizeof(int), st));
+  DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&gpos), n * sizeof(int), st));
+  int64_t total = 0, gtotal = 0;
+  int rc = exclusive_scan(n, StencilCount{g, n, 0}, j->offsets, &total, st);
+  if (!rc) rc = exclusive_scan(n, StencilCount{g, n, 1}, gpos, &gtotal, st);
+  if (rc) return rc;
+  const int tot32 = (int)total;
+  DS_CUDA(cudaMemcpyAsync(j->offsets + n, &tot32, sizeof(int), cudaMemcpyHostToDevice, st));
+  int64_t G = 0;
+  if (gtotal > 0) {
+    unsigned long long *keys = nullptr, *sorted = nullptr;
+    int* pos = nullptr;
+    DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&keys), gtotal * 8, st));
+    DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&sorted), gtotal * 8, st));
+    DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&pos), gtotal * 4, st));
+    stencil_ghost_keys<<<grid1d(n), 256, 0, st>>>(g, n, gpos, keys);
+    DS_LAUNCH_CHECK("stencil_ghost_keys");
+    size_t tmp_bytes = 0;
+    DS_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, keys, sorted, (int)gtotal, 0, 64, st));
+    void* tmp = nullptr;
+    DS_CUDA(cudaMallocAsync(&tmp, tmp_bytes, st));
+    DS_CUDA(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, keys, sorted, (int)gtotal, 0, 64, st));
+    DS_CUDA(cudaFreeAsync(tmp, st));
+    rc = exclusive_scan(gtotal, KeyHead{sorted}, pos, &G, st);
+    if (rc) return rc;
+    DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&j->ukeys), (G > 0 ? G : 1) * 8, st));
+    compact_keys<<<grid1d(gtotal), 256, 0, st>>>(gtotal, sorted, pos, j->ukeys);
+    DS_LAUNCH_CHECK("compact_keys");
+    DS_CUDA(cudaFreeAsync(keys, st));
+    DS_CUDA(cudaFreeAsync(sorted, st));
+    DS_CUDA(cudaFreeAsync(pos, st));
+  }
+  DS_CUDA(cudaFreeAsync(gpos, st));
+  j->nnz = total;
+  j->G = G;
+  *nnz = total;
+  *nghosts = G;
+  *job = j;
+  return DS_OK;
+}
+
+extern "C" int ds_stencil_finish(ds_stencil_job* j, int32_t* row_offsets, int32_t* cols,
+                                 double* vals, double* b, int64_t* ghost_keys) {
+  cudaStream_t st = j->st;
+  stencil_fill<<<grid1d(j->n), 256, 0, st>>>(j->g, j->n, j->offsets, j->ukeys, j->G, cols, vals,
+                                              b);
+  DS_LAUNCH_CHECK("stencil_fill");
+  DS_CUDA(cudaMemcpyAsync(row_offsets, j->offsets, (j->n + 1) * sizeof(int),
+                          cudaMemcpyDeviceToDevice, st));
+  if (j->G > 0 && ghost_keys)
+    DS_CUDA(cudaMemcpyAsync(ghost_keys, j->ukeys, j->G * 8, cudaMemcpyDeviceToDevice, st));
+  DS_CUDA(cudaFreeAsync(j->offsets, st));
+  if (j->ukeys) DS_CUDA(cudaFreeAsync(j->ukeys, st));
+  delete j;
+  return DS_OK;
+}
+
+// -------------------------------------------------------- local/remote split --
+// split_local_remote (stencil.py:256-277): columns < n_owned form the local
+// (square) part, the rest the remote part re-based by -n_owned.  Columns are
+// sorted per row, so each row's local entries are a prefix.
+struct LocalCount {
+  const int* off;
+  const int* cols;
+  int n_owned;
+  __device__ int operator()(int64_t i) const {
+    int c = 0;
+    for (int k = off[i]; k < off[i + 1] && cols[k] < n_owned; ++k) ++c;
+    return c;
+  }
+};
+
+__global__ void split_fill(int nrows, int n_owned, const int* __restrict__ off,
+                           const int* __restrict__ cols, const double* __restrict__ vals,
+                           const int* __restrict__ loc_off, int* loc_cols, double* loc_vals,
+                           int* rem_off, int* rem_cols, double* rem_vals, int nnz_loc,
+                           int nnz_total) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= nrows; i += gridDim.x * blockDim.x) {
+    const int lo = (i < nrows) ? loc_off[i] : nnz_loc;
+    const int ro = ((i < nrows) ? off[i] : nnz_total) - lo;
+    rem_off[i] = ro;
+    if (i == nrows) break;
+    int k = off[i], o = lo;
+    const int e = off[i + 1];
+    for (; k < e && cols[k] < n_owned; ++k, ++o) {
+      loc_cols[o] = cols[k];
+      loc_vals[o] = vals[k];
+    }
+    for (int r = ro; k < e; ++k, ++r) {
+      rem_cols[r] = cols[k] - n_owned;
+      rem_vals[r] = vals[k];
+    }
+  }
+}
+
+extern "C" int ds_csr_split_count(int64_t nrows, int64_t n_owned, const int32_t* row_offsets,
+                                  const int32_t* cols, int32_t* loc_off, int64_t* nnz_local,
+                                  void* stream) {
+  cudaStream_t st = as_stream(stream);
+  int64_t tot = 0;
+  int rc = exclusive_scan(nrows, LocalCount{row_offsets, cols, (int)n_owned}, loc_off, &tot, st);
+  if (rc) return rc;
+  const int t32 = (int)tot;
+  DS_CUDA(cudaMemcpyAsync(loc_off + nrows, &t32, sizeof(int), cudaMemcpyHostToDevice, st));
+  *nnz_local = tot;
+  return DS_OK;
+}
+
+extern "C" int ds_csr_split_fill(int64_t nrows, int64_t n_owned, int64_t nnz,
+                                 const int32_t* row_offsets, const int32_t* cols,
+                                 const double* vals, const int32_t* loc_off, int64_t nnz_local,
+                                 int32_t* loc_cols, double* loc_vals, int32_t* rem_off,
+                                 int32_t* rem_cols, double* rem_vals, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  split_fill<<<grid1d(nrows + 1), 256, 0, st>>>((int)nrows, (int)n_owned, row_offsets, cols, vals,
+                                                loc_off, loc_cols, loc_vals, rem_off, rem_cols,
+                                                rem_vals, (int)nnz_local, (int)nnz);
+  DS_LAUNCH_CHECK("split_fill");
+  return DS_OK;
+}
+
 static ds_convert_job* new_job(int64_t nrows, int64_t ncols, int target, void* stream) {
   ds_convert_job* job = new ds_convert_job;
   job->st = as_stream(stream);

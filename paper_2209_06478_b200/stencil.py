@@ -4,8 +4,9 @@
 * ``generate_problem`` builds every partition's system exactly as the
   reference (diagonal 26, off-diagonals -1, x-fastest local numbering,
   rank = cx + px*(cy + py*cz), ghosts numbered by (owner, owner-local),
-  columns sorted per row, b = row sums).  It is host setup (integer-exact);
-  ``space=MemorySpace.DEVICE`` uploads the result.
+  columns sorted per row, b = row sums).  Integer-exact: HOST space runs
+  numpy, ``space=MemorySpace.DEVICE`` runs the generator kernels on the GPU
+  (ds_stencil_*) -- bitwise the same arrays.
 * ``exchange_halo`` is a set of device gathers: each neighbour's send list
   is gathered straight into the receiver's contiguous ghost slice
   (ds_gather); across processes the same plan drives NCCL (dist.py).
@@ -202,6 +203,58 @@ def halo_send_lists(spec: GridSpec, rank: int) -> dict[int, np.ndarray]:
     return {q: np.unique(np.concatenate(v)) for q, v in sorted(per_owner.items())}
 
 
+def _partition_device(spec: GridSpec, rank: int, device) -> PartitionData:
+    """Device-side generation (ds_stencil_begin / ds_stencil_finish): the
+    matrix, b and the sorted ghost keys are produced by kernels; the halo
+    plan and the two index maps follow on the host from the ghost keys
+    (O(ghosts) + O(n) integer arithmetic)."""
+    import ctypes
+
+    import torch
+    from . import _device
+    dev = _device.require_cuda(device)
+    n = spec.local_points
+    lib = _native.load()
+    job = ctypes.c_void_p()
+    nnz, ng = ctypes.c_int64(), ctypes.c_int64()
+    with torch.cuda.device(dev):
+        st = _device.stream(dev)
+        _native.check(lib.ds_stencil_begin(spec.nx, spec.ny, spec.nz, spec.px, spec.py, spec.pz,
+                                           rank, st, ctypes.byref(job), ctypes.byref(nnz),
+                                           ctypes.byref(ng)))
+        i32 = dict(dtype=torch.int32, device=dev)
+        f64 = dict(dtype=torch.float64, device=dev)
+        off = torch.empty(n + 1, **i32)
+        cols = torch.empty(int(nnz.value), **i32)
+        vals = torch.empty(int(nnz.value), **f64)
+        b = torch.empty(n, **f64)
+        keys = torch.empty(max(int(ng.value), 1), dtype=torch.int64, device=dev)
+        _native.check(lib.ds_stencil_finish(job, off.data_ptr(), cols.data_ptr(),
+                                            vals.data_ptr(), b.data_ptr(), keys.data_ptr()))
+        ghost_keys = keys[:int(ng.value)].cpu().numpy()
+    nx, ny, nz, px, py, pz = spec.nx, spec.ny, spec.nz, spec.px, spec.py, spec.pz
+    gnx, gny, gnz = spec.global_dims
+    cx, cy, cz = rank % px, (rank // px) % py, rank // (px * py)
+    g_owner, g_local = ghost_keys // n, ghost_keys % n
+    exchanges = []
+    for q in np.unique(g_owner).tolist():
+        sel = np.flatnonzero(g_owner == q)
+        exchanges.append(HaloExchange(int(q), g_local[sel].copy(), n + sel))
+    ids = np.arange(n, dtype=np.int64)
+    gx = ids % nx + cx * nx
+    gy = (ids // nx) % ny + cy * ny
+    gz = ids // (nx * ny) + cz * nz
+    qx, qy, qz = g_owner % px, (g_owner // px) % py, g_owner // (px * py)
+    g2g = ((g_local % nx + qx * nx)
+           + gnx * (((g_local // nx) % ny + qy * ny) + gny * (g_local // (nx * ny) + qz * nz)))
+    return PartitionData(
+        rank=rank, coords=(cx, cy, cz),
+        a_full=CsrMatrix(n, n + int(ghost_keys.size), off, cols, vals, MemorySpace.DEVICE),
+        b=DenseVector(b), xexact=DenseVector.ones(n, MemorySpace.DEVICE, dev),
+        halo=HaloPlan(int(ghost_keys.size), exchanges),
+        local_to_global=gx + gnx * (gy + gny * gz), ghost_to_global=g2g)
+
+
 def _to_space(part: PartitionData, space, device) -> PartitionData:
     if space is None or MemorySpace(space) == MemorySpace.HOST:
         return part
@@ -218,12 +271,18 @@ def generate_problem(spec: GridSpec, space: MemorySpace | None = None, device=No
     restricts generation to a subset (one rank per process); ``space``
     places matrices/vectors on the device."""
     which = range(spec.npartitions) if ranks is None else list(ranks)
-    parts = [_to_space(_partition(spec, r), space, device) for r in which]
+    parts = [generate_partition(spec, r, space, device) for r in which]
     return PartitionedProblem(spec=spec, partitions=parts)
 
 
 def generate_partition(spec: GridSpec, rank: int, space: MemorySpace | None = None,
                        device=None) -> PartitionData:
+    """One partition.  DEVICE space: generated by kernels on the device
+    (set DS_HOST_GENERATOR=1 to build on the host and upload instead)."""
+    import os
+    if space is not None and MemorySpace(space) == MemorySpace.DEVICE and \
+            not os.environ.get("DS_HOST_GENERATOR"):
+        return _partition_device(spec, rank, device)
     return _to_space(_partition(spec, rank), space, device)
 
 
@@ -249,10 +308,38 @@ def split_local_remote(problem: PartitionedProblem, partition: int) -> SplitMatr
     if a.space == MemorySpace.HOST:
         loc, rem = _split_host(a, part.halo.ghost_count)
     else:
-        from .datamove import to_device, to_host
-        loc, rem = _split_host(to_host(a), part.halo.ghost_count)
-        loc, rem = to_device(loc, a.device), to_device(rem, a.device)
+        loc, rem = _split_device(a, part.halo.ghost_count)
     return SplitMatrix(local=DynamicMatrix(loc), remote=DynamicMatrix(rem))
+
+
+def _split_device(a: CsrMatrix, ghost_count: int):
+    """ds_csr_split_count / ds_csr_split_fill on a DEVICE CSR."""
+    import ctypes
+
+    import torch
+    from . import _device
+    n, dev = a.nrows, a.device
+    lib = _native.load()
+    i32 = dict(dtype=torch.int32, device=dev)
+    f64 = dict(dtype=torch.float64, device=dev)
+    with torch.cuda.device(dev):
+        st = _device.stream(dev)
+        loc_off = torch.empty(n + 1, **i32)
+        nl = ctypes.c_int64()
+        _native.check(lib.ds_csr_split_count(n, n, a.row_offsets.data_ptr(),
+                                             _device.ptr(a.col_indices), loc_off.data_ptr(),
+                                             ctypes.byref(nl), st))
+        nl = int(nl.value)
+        nr = a.nnz - nl
+        lc, lv = torch.empty(nl, **i32), torch.empty(nl, **f64)
+        ro, rc, rv = torch.empty(n + 1, **i32), torch.empty(nr, **i32), torch.empty(nr, **f64)
+        _native.check(lib.ds_csr_split_fill(n, n, a.nnz, a.row_offsets.data_ptr(),
+                                            _device.ptr(a.col_indices), _device.ptr(a.values),
+                                            loc_off.data_ptr(), nl, _device.ptr(lc),
+                                            _device.ptr(lv), ro.data_ptr(), _device.ptr(rc),
+                                            _device.ptr(rv), st))
+    return (CsrMatrix(n, n, loc_off, lc, lv, MemorySpace.DEVICE),
+            CsrMatrix(n, ghost_count, ro, rc, rv, MemorySpace.DEVICE))
 
 
 # ---------------------------------------------------------------------------

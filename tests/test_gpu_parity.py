@@ -370,3 +370,45 @@ def test_powerlaw_golden_hashes():
     assert digest(host(y.data)) == H["pl/spmv_coo"]
     with pytest.raises(ds.DiaFillOverflow):
         ds.convert(csr, F.DIA)
+
+
+def test_device_generator_bitwise_equals_host():
+    """On-device generate_problem (ds_stencil_*) == host generator == reference
+    structure, for every partition of several decompositions."""
+    for sp in [(1, 1, 1, 1, 1, 1), (3, 3, 3, 1, 1, 1), (4, 3, 2, 2, 1, 1), (4, 4, 4, 2, 2, 2),
+               (5, 4, 3, 1, 3, 2), (7, 5, 6, 3, 2, 2), (16, 16, 16, 1, 1, 1)]:
+        spec = ds.GridSpec(*sp)
+        for r in range(spec.npartitions):
+            h = ds.generate_partition(spec, r)
+            d = ds.generate_partition(spec, r, space=ds.MemorySpace.DEVICE, device=DEV)
+            assert d.a_full.space == ds.MemorySpace.DEVICE
+            assert np.array_equal(host(d.a_full.row_offsets), h.a_full.row_offsets)
+            assert np.array_equal(host(d.a_full.col_indices), h.a_full.col_indices)
+            assert host(d.a_full.values).tobytes() == h.a_full.values.tobytes()
+            assert host(d.b.data).tobytes() == h.b.data.tobytes()
+            assert d.a_full.ncols == h.a_full.ncols
+            assert d.halo.ghost_count == h.halo.ghost_count
+            for e1, e2 in zip(d.halo.exchanges, h.halo.exchanges):
+                assert e1.neighbor == e2.neighbor
+                assert np.array_equal(e1.send_local_indices, e2.send_local_indices)
+                assert np.array_equal(e1.recv_ghost_slots, e2.recv_ghost_slots)
+            assert np.array_equal(d.local_to_global, h.local_to_global)
+            assert np.array_equal(d.ghost_to_global, h.ghost_to_global)
+
+
+def test_device_split_bitwise_equals_reference(K):
+    for si in range(int(K["nspecs"][0])):
+        key = f"st{si}"
+        spec = ds.GridSpec(*K[f"{key}/spec"].tolist())
+        prob = ds.generate_problem(spec, space=ds.MemorySpace.DEVICE, device=DEV)
+        for k in range(prob.npartitions):
+            sp = ds.split_local_remote(prob, k)
+            loc, rem = sp.local.payload, sp.remote.payload
+            pk = f"{key}/p{k}"
+            assert np.array_equal(host(loc.row_offsets), K[f"{pk}/loc_offsets"])
+            assert np.array_equal(host(loc.col_indices), K[f"{pk}/loc_cols"])
+            assert host(loc.values).tobytes() == K[f"{pk}/loc_vals"].tobytes()
+            assert np.array_equal(host(rem.row_offsets), K[f"{pk}/rem_offsets"])
+            assert np.array_equal(host(rem.col_indices), K[f"{pk}/rem_cols"])
+            assert host(rem.values).tobytes() == K[f"{pk}/rem_vals"].tobytes()
+            assert rem.ncols == prob.partitions[k].halo.ghost_count
