@@ -349,7 +349,32 @@ def run(args, rank: int, world: int) -> int:
     clocks.start()
 
     extras = {}
-    part, split = build_rank(ds, spec, rank, dev, ds.FormatId.DIA, ds.FormatId.CSR)
+    if args.fixed_plan:
+        part, split = build_rank(ds, spec, rank, dev, ds.FormatId.DIA, ds.FormatId.CSR)
+        plan = ("dia", "csr")
+    else:
+        # dynamic per-GPU format selection (tuner 'multi' on this rank's
+        # partition; conversion cost of every switch recorded)
+        from paper_2209_06478_b200 import dist as D
+        part = ds.generate_partition(spec, rank, space=ds.MemorySpace.DEVICE, device=dev)
+        split = ds.split_local_remote(ds.PartitionedProblem(spec, [part]), 0)
+        t_tune = time.perf_counter()
+        prof = D.profile_rank(part, split, reps=10)
+        lf, rf = D.select_rank_plan(prof["entries"], "multi", world)
+        t_conv = time.perf_counter()
+        ds.convert_inplace(split.local, lf)
+        ds.convert_inplace(split.remote, rf)
+        torch.cuda.synchronize()
+        t_end = time.perf_counter()
+        plan = (lf.name.lower(), rf.name.lower())
+        extras["tuner"] = {
+            "mode": "multi", "plan": list(plan),
+            "spmv_us": {f"{a.name.lower()}/{b.name.lower()}": round(t * 1e6, 2)
+                        for (a, b), t in sorted(prof["entries"].items())},
+            "skipped": [f"{a.name.lower()}/{b.name.lower()}" for a, b in prof["skipped"]],
+            "convert_ms": {f"{a.name.lower()}/{b.name.lower()}": round(t * 1e3, 3)
+                           for (a, b), t in sorted(prof["convert_s"].items())},
+            "tune_s": round(t_conv - t_tune, 3), "apply_convert_ms": round((t_end - t_conv) * 1e3, 3)}
     n = part.a_full.nrows
     nnz_local = part.a_full.nnz
     if world == 1 and not args.no_sweep:
@@ -412,10 +437,14 @@ def run(args, rank: int, world: int) -> int:
 
     # roofline of the dominant kernel (per launch, algorithmic bytes)
     lm = eng.local if hasattr(eng, "local") else eng.parts[0].local
-    nd = lm.ndiags if hasattr(lm, "ndiags") else 27
-    kb = dia_bytes(n, n, nd)
+    if isinstance(lm, ds.DiaMatrix):
+        kb = dia_bytes(n, n, lm.ndiags)
+    elif isinstance(lm, ds.CsrMatrix):
+        kb = csr_bytes(n, n, lm.nnz)
+    else:
+        kb = coo_bytes(n, n, lm.nnz)
     k_ach = kb / (kern["avg_ms"] * 1e-3) / 1e9 if kern["avg_ms"] > 0 else 0.0
-    roof = {"kernel": "dia_slab_tma (fused p.Ap, CG step)", "bound": "hbm",
+    roof = {"kernel": f"{plan[0]} SpMV of the CG step (fused p.Ap)", "bound": "hbm",
             "achieved": round(k_ach, 1), "peak": peak, "unit": "GB/s",
             "frac": round(k_ach / peak, 3), "traffic": None, "peak_source": pk["source"],
             "algorithmic_bytes_per_launch": kb, "avg_launch_ms": round(kern["avg_ms"], 5),
@@ -423,8 +452,11 @@ def run(args, rank: int, world: int) -> int:
 
     e2e = None
     cpu = None
-    if rank == 0 and world == 1:
+    if world > 1 or args.rank_engine:
+        e2e = measure_e2e_ranks(torch, eng, part, n, nnz_total, world)
+    elif rank == 0:
         e2e = measure_e2e(ds, torch, spec, split, part, n, nnz_local)
+    if rank == 0 and world == 1:
         if not args.no_cpu:
             thr = host_threads()
             os.environ["OPENBLAS_NUM_THREADS"] = str(thr)
@@ -440,7 +472,8 @@ def run(args, rank: int, world: int) -> int:
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": f"hpcg_cg_27pt_{nx}^3_per_gpu", "grid_per_gpu": [nx, nx, nx],
-                   "procs": [px, py, pz], "local_format": "dia", "remote_format": "csr",
+                   "procs": [px, py, pz], "local_format": plan[0], "remote_format": plan[1],
+                   "format_selection": "fixed" if args.fixed_plan else "tuner multi (per GPU)",
                    "flops_per_step": flops_per_iter(nnz_total, n * world),
                    "graph": not args.eager,
                    "l2": f"no flush: the DIA matrix ({8 * 27 * n / 1e6:.0f} MB/GPU) exceeds the "
@@ -482,6 +515,35 @@ def measure_e2e(ds, torch, spec, split, part, n, nnz, iters=50, reps=3):
             "seconds": round(t, 5)}
 
 
+def measure_e2e_ranks(torch, eng, part, n, nnz_total, world, iters=50, reps=3):
+    """One partition per process: every rank solves from a host numpy b to a
+    host x through its engine (pinned staging, setup, ``iters`` iterations);
+    wall time per solve, max over ranks, median of reps."""
+    import numpy as np
+    b = part.b.data.cpu().numpy() if hasattr(part.b.data, "cpu") else np.asarray(part.b.data)
+    times = []
+    for _ in range(reps + 1):
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        x = eng.solve_host(b, iters)
+        t = time.perf_counter() - t0
+        if world > 1:
+            tt = torch.tensor([t], dtype=torch.float64, device=eng.dev)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            t = float(tt[0])
+        times.append(t)
+        assert x.shape == (n,)
+    t = statistics.median(times[1:])
+    fl = iters * flops_per_iter(nnz_total, n * world)
+    return {"value": round(fl / t / 1e9, 2), "unit": "GFLOP/s", "h2d_bytes_per_step": 8 * n,
+            "d2h_bytes_per_step": 8 * n,
+            "step": f"per rank: host numpy b -> {iters} CG iterations -> host numpy x "
+                    f"(dist.RankCG.solve_host), max over {world} rank(s)",
+            "seconds": round(t, 5)}
+
+
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     ap.add_argument("--gpus", type=int, default=1)
@@ -493,6 +555,8 @@ def main(argv=None) -> int:
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--powerlaw", action="store_true", help="also run BASELINE config 4")
+    ap.add_argument("--fixed-plan", action="store_true",
+                    help="local DIA / remote CSR instead of the per-GPU tuner's choice")
     ap.add_argument("--rank-engine", action="store_true",
                     help="at N=1 use the NCCL one-partition-per-process engine (dist.RankCG)")
     args = ap.parse_args(argv)

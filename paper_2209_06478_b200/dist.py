@@ -296,6 +296,29 @@ class RankCG:
         hist = self.hist[:it + 1].cpu().numpy().copy()
         return DenseVector(self.x), it, hist, sc.done == 1
 
+    def solve_host(self, b_host: np.ndarray, iters: int, chunk: int = 8) -> np.ndarray:
+        """End-to-end solve through host memory: b from a numpy array (pinned
+        staging), setup, ``iters`` iterations (tolerance as configured), x back
+        to a numpy array.  Reuses this engine's buffers and captured graph."""
+        import torch
+        with torch.cuda.device(self.dev):
+            st = torch.cuda.current_stream(self.dev)
+            pin = self.__dict__.get("_pin")
+            if pin is None:
+                pin = (torch.empty(self.n, dtype=torch.float64, pin_memory=True),
+                       torch.empty(self.n, dtype=torch.float64, pin_memory=True))
+                self._pin = pin
+            pin[0].numpy()[:] = b_host
+            self.b.copy_(pin[0], non_blocking=True)
+            self.x.zero_()
+            self.p.zero_()
+            self.setup(st.cuda_stream)
+            for _ in range(iters):
+                self.replay()
+            pin[1].copy_(self.x, non_blocking=True)
+            st.synchronize()
+            return pin[1].numpy().copy()
+
     def close(self) -> None:
         if self.comm:
             _native.check(self.lib.ds_nccl_comm_destroy(self.comm))
@@ -315,4 +338,105 @@ def rank_cg(spec: GridSpec, part: PartitionData, split: SplitMatrix, tol: float 
         eng.close()
 
 
-__all__ = ["HaloSchedule", "RankCG", "init_comm", "rank_cg", "MemorySpace"]
+def profile_rank(part: PartitionData, split: SplitMatrix, reps: int = 20,
+                 fill_limit: int | None = None) -> dict:
+    """This rank's row of the tuner's TimingTable (tuner.py:53-120): every
+    (local, remote) combination converted in place (conversion wall time
+    recorded -- the cost of runtime switching), one warm-up, then the median
+    of ``reps`` CUDA-event timings of local SpMV + remote spmv_add (the halo
+    exchange excluded, like the reference's per_partition_ns).  Failed
+    conversions are skipped; both parts are restored to CSR at the end.
+    Returns {"entries": {(lf, rf): seconds}, "skipped": [...],
+    "convert_s": {(lf, rf): seconds}}."""
+    import statistics
+    import time
+
+    import torch
+    from .datamove import convert_inplace
+    from .errors import DynSparseError
+    from .formats import FormatId
+    from .kernels import spmv, spmv_add, SERIAL
+    from .tuner import FORMATS
+    dev = split.local.device
+    n = part.a_full.nrows
+    g = part.halo.ghost_count
+    remote_axis = FORMATS if g > 0 else (FormatId.CSR,)
+    x = DenseVector.ones(n + g, MemorySpace.DEVICE, dev)
+    y = DenseVector.zeros(n, MemorySpace.DEVICE, dev)
+    xo, xg = DenseVector(x.data[:n]), DenseVector(x.data[n:])
+    entries, skipped, conv = {}, [], {}
+    for lf in FORMATS:
+        for rf in remote_axis:
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            try:
+                convert_inplace(split.local, lf, fill_limit)
+                convert_inplace(split.remote, rf, fill_limit)
+            except DynSparseError:
+                skipped.append((lf, rf))
+                convert_inplace(split.local, FormatId.CSR)
+                convert_inplace(split.remote, FormatId.CSR)
+                continue
+            torch.cuda.synchronize(dev)
+            conv[(lf, rf)] = time.perf_counter() - t0
+            st = torch.cuda.current_stream(dev)
+            spmv(SERIAL, split.local, xo, y)          # warm-up, untimed
+            spmv_add(SERIAL, split.remote, xg, y)
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                  for _ in range(reps)]
+            for a, b in ev:
+                a.record(st)
+                spmv(SERIAL, split.local, xo, y)
+                spmv_add(SERIAL, split.remote, xg, y)
+                b.record(st)
+            torch.cuda.synchronize(dev)
+            med = statistics.median(a.elapsed_time(b) for a, b in ev) * 1e-3
+            entries[(lf, rf)] = max(med, 1e-9)
+            convert_inplace(split.local, FormatId.CSR)
+            convert_inplace(split.remote, FormatId.CSR)
+    if g == 0:   # no ghosts: the remote format cannot matter (tuner.py:112-118)
+        for (lf, _), t in list(entries.items()):
+            for rf in FORMATS:
+                entries[(lf, rf)] = t
+    return {"entries": entries, "skipped": skipped, "convert_s": conv}
+
+
+def select_rank_plan(entries: dict, mode: str = "multi", world: int = 1):
+    """(local, remote) for THIS rank (tuner.py:146-180): ``multi`` is the
+    rank-local argmin (ties to the lower FormatId, local first); ``morpheus``
+    / ``ghost`` pick one format for all ranks minimising the max over ranks
+    (all-reduce MAX across processes)."""
+    from .errors import EmptySearchSpace
+    from .formats import FormatId
+    from .tuner import FORMATS
+    if mode == "fixed":
+        return (FormatId.CSR, FormatId.CSR)
+    if mode == "multi":
+        cands = [(t, lf, rf) for (lf, rf), t in entries.items()]
+        if not cands:
+            raise EmptySearchSpace("this partition has no measured combination")
+        _, lf, rf = min(cands)
+        return (lf, rf)
+    if mode not in ("morpheus", "ghost"):
+        raise ValueError(f"unknown mode {mode!r}")
+    import torch
+    vary_local = mode == "morpheus"
+    vals = []
+    for f in FORMATS:
+        cell = (f, FormatId.CSR) if vary_local else (FormatId.CSR, f)
+        vals.append(entries.get(cell, float("inf")))
+    t = torch.tensor(vals, dtype=torch.float64)
+    if world > 1:
+        import torch.distributed as dist
+        t = t.cuda() if dist.get_backend() == "nccl" else t
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    worst = t.cpu().tolist()
+    best = min(range(len(FORMATS)), key=lambda i: (worst[i], i))
+    if worst[best] == float("inf"):
+        raise EmptySearchSpace("no format was measured on every partition")
+    f = FORMATS[best]
+    return (f, FormatId.CSR) if vary_local else (FormatId.CSR, f)
+
+
+__all__ = ["HaloSchedule", "RankCG", "init_comm", "rank_cg", "profile_rank", "select_rank_plan",
+           "MemorySpace"]

@@ -224,17 +224,23 @@ class CgEngine:
             if use_graph is None:
                 use_graph = self.max_iters >= 16
             c = chunk or (8 if use_graph else 4)
-            if use_graph:
+            if use_graph and self.graph is None:
                 self._capture(c)
+            rounds = 1
             while True:
-                if use_graph:
-                    self.graph.replay()
-                else:
-                    for _ in range(c):
-                        self.step(st)
+                # replays between readbacks grow geometrically (1, 1, 2, 4, ...
+                # graphs of c steps): after convergence every kernel is a
+                # no-op, so overshooting costs only launch latency
+                for _ in range(rounds):
+                    if use_graph:
+                        self.graph.replay()
+                    else:
+                        for _ in range(c):
+                            self.step(st)
                 sc = self.scalars()
                 if sc.done:
                     return sc
+                rounds = min(rounds * 2, 16)
 
     # benchmarking hooks ---------------------------------------------------
     def capture_step(self) -> None:
@@ -385,14 +391,72 @@ def build_engine(op: DistributedOperator, bs, x0s, tol, max_iters) -> tuple[CgEn
     return CgEngine(parts, dev, tol, max_iters), parts
 
 
+def _pinned(eng, name: str, n: int):
+    """Pinned host staging buffer cached on the engine (allocated once)."""
+    import torch
+    buf = eng.__dict__.setdefault("_pins", {}).get((name, n))
+    if buf is None:
+        buf = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        eng._pins[(name, n)] = buf
+    return buf
+
+
+def _pinned_copy(eng, name: str, dst, src_np) -> None:
+    """Host numpy -> device tensor through a cached pinned staging buffer."""
+    import torch
+    buf = _pinned(eng, name, dst.numel())
+    torch.cuda.current_stream(dst.device).synchronize()   # buffer free for reuse
+    buf.numpy()[:] = src_np
+    dst.copy_(buf, non_blocking=True)
+
+
+def _reload(eng: CgEngine, bs, x0s) -> None:
+    """Refill a cached engine's right-hand sides / initial guesses in place
+    (its captured graph keeps pointing at the same buffers)."""
+    for k, pt in enumerate(eng.parts):
+        src = bs[k]
+        if src.space == MemorySpace.HOST:
+            _pinned_copy(eng, f"b{k}", pt.b, src.data)
+        else:
+            pt.b.copy_(src.data)
+        if x0s is None:
+            pt.x.zero_()
+        elif x0s[k].space == MemorySpace.HOST:
+            _pinned_copy(eng, f"x0{k}", pt.x, x0s[k].data)
+        else:
+            pt.x.copy_(x0s[k].data)
+        pt.p.copy_(pt.x)
+        pt.p_full[pt.n:].zero_()
+
+
 def _cg_distributed(op, bs, x0s, tol, max_iters, use_graph):
     import torch
-    eng, parts = build_engine(op, bs, x0s, tol, max_iters)
+    # Reuse the engine (device buffers + captured CUDA graph) across calls on
+    # the same operator with the same controls -- the analysis-reuse pattern
+    # of sparse solvers; a changed matrix format/storage rebuilds it.
+    key = (float(tol), int(max_iters), use_graph,
+           tuple((sp.local.active, id(sp.local.payload), sp.remote.active, id(sp.remote.payload))
+                 for sp in op.splits))
+    cached = op.__dict__.get("_cg_engine")
+    if cached is not None and cached[0] == key and len(bs) == cached[1].P:
+        eng = cached[1]
+        _reload(eng, bs, x0s)
+    else:
+        eng, _ = build_engine(op, bs, x0s, tol, max_iters)
+        op.__dict__["_cg_engine"] = (key, eng)
+    parts = eng.parts
     with torch.cuda.device(eng.dev):
         sc = eng.run(use_graph=use_graph)
         it, hist, conv = _finish(eng, sc)
     host = bs[0].space == MemorySpace.HOST
-    xs = [DenseVector(pt.x.cpu().numpy()) if host else DenseVector(pt.x) for pt in parts]
+    if host:
+        outs = [_pinned(eng, f"x{k}", pt.n) for k, pt in enumerate(parts)]
+        for o, pt in zip(outs, parts):
+            o.copy_(pt.x, non_blocking=True)
+        torch.cuda.synchronize(eng.dev)
+        xs = [DenseVector(o.numpy().copy()) for o in outs]
+    else:
+        xs = [DenseVector(pt.x.clone()) for pt in parts]
     return CgResult(xs, it, hist, conv)
 
 
