@@ -308,6 +308,21 @@ int ds_halo_exchange(int nnbr, const int32_t* peers, const int64_t* send_counts,
 /* recv[r*count : (r+1)*count] = rank r's send (ncclAllGather, float64).   */
 int ds_allgather_f64(const double* send, double* recv, int64_t count, void* comm, void* stream);
 
+/* ---- HPCG smoother and multigrid transfers (NOT in the
+ * reference -- parity pinned to the oracle's restatement of HPCG's
+ * ComputeSYMGS_ref / ComputeMG_ref with the 8-colour stencil ordering) -----
+ * ds_symgs: one symmetric sweep in place, colours 0..n-1 then n-1..0; rows of
+ * colour c are color_rows[color_start[c] .. color_start[c+1]).  Per row:
+ * s = r[i]; s -= a_ij*x[j] (j != i, stored order, no FMA); x[i] = s / a_ii. */
+int ds_symgs(int64_t nrows, const int32_t* row_offsets, const int32_t* cols,
+             const double* values, const int32_t* color_rows, const int64_t* color_start,
+             int ncolors, const double* r, double* x, void* stream);
+/* rc[i] = r[f2c[i]] - axf[f2c[i]]  /  x[f2c[i]] += xc[i]                   */
+int ds_mg_restrict(int64_t ncoarse, const int32_t* f2c, const double* r, const double* axf,
+                   double* rc, void* stream);
+int ds_mg_prolong(int64_t ncoarse, const int32_t* f2c, const double* xc, double* x,
+                  void* stream);
+
 /* ---- DIA diagonal column helpers (kernels.py:258-262, 325-330) --------- */
 /* direction 0: out[i] = values[i*ndiags + j0] (i < n); 1: values[...] = d[i] */
 int ds_dia_diag_column(int64_t n, int32_t ndiags, int32_t j0, double* values, double* vec,

@@ -663,3 +663,116 @@ def host_threads() -> int:
         return len(os.sched_getaffinity(0))
     except AttributeError:  # pragma: no cover
         return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------------------
+# HPCG SymGS / MG -- NOT in the reference (SPEC.md:16,
+# PAPER.md:166): PARITY UNPINNED against the reference.  This restates the
+# HPCG benchmark's ComputeSYMGS_ref / ComputeMG_ref with the 8-colour
+# ordering of the 27-point stencil (colour = x%2 + 2(y%2) + 4(z%2), local
+# coordinates), under which rows of one colour are independent.  The device
+# kernels are held to bitwise parity with these functions.
+# ---------------------------------------------------------------------------
+
+def stencil_colors(nx, ny, nz) -> np.ndarray:
+    i = np.arange(nx * ny * nz, dtype=I64)
+    return (i % nx) % 2 + 2 * (((i // nx) % ny) % 2) + 4 * ((i // (nx * ny)) % 2)
+
+
+def symgs_colored(m: OCsr, r: np.ndarray, x: np.ndarray, colors: np.ndarray) -> None:
+    """One symmetric Gauss-Seidel sweep in place: colours 0..7 forward, then
+    7..0 backward.  Per row i: s = r[i]; s = s - a_ij * x[j] for every j != i
+    in stored (ascending) column order; x[i] = s / a_ii (ComputeSYMGS_ref)."""
+    off, cols, vals = m.offsets, m.cols, m.vals
+    n = m.nrows
+    order = [np.flatnonzero(colors == c) for c in range(8)]
+
+    def relax(rows):
+        for i in rows.tolist():
+            s = r[i]
+            d = 0.0
+            for k in range(int(off[i]), int(off[i + 1])):
+                j = int(cols[k])
+                if j == i:
+                    d = vals[k]
+                else:
+                    s = s - vals[k] * x[j]
+            x[i] = s / d
+    for c in range(8):
+        relax(order[c])
+    for c in range(7, -1, -1):
+        relax(order[c])
+    assert x.size == n
+
+
+def mg_levels(nx, ny, nz, levels=4):
+    """[(matrix, colors, f2c)] finest first; coarse grids halve every
+    dimension while it stays even (GenerateCoarseProblem)."""
+    out = []
+    for lev in range(levels):
+        part = stencil_partition(nx, ny, nz)
+        f2c = None
+        if lev + 1 < levels and nx % 2 == 0 and ny % 2 == 0 and nz % 2 == 0:
+            cx, cy, cz = nx // 2, ny // 2, nz // 2
+            ic = np.arange(cx * cy * cz, dtype=I64)
+            xc, yc, zc = ic % cx, (ic // cx) % cy, ic // (cx * cy)
+            f2c = 2 * xc + nx * (2 * yc + ny * 2 * zc)
+        out.append((part.a_full, stencil_colors(nx, ny, nz), f2c))
+        if f2c is None:
+            break
+        nx, ny, nz = nx // 2, ny // 2, nz // 2
+    return out
+
+
+def mg_vcycle(levels, lev: int, r: np.ndarray, x: np.ndarray) -> None:
+    """ComputeMG_ref: x = 0; pre-smooth; Axf = A x; rc = r[f2c] - Axf[f2c];
+    recurse; x[f2c] += xc; post-smooth (coarsest: one smooth)."""
+    a, colors, f2c = levels[lev]
+    x[:] = 0.0
+    symgs_colored(a, r, x, colors)
+    if f2c is None or lev + 1 >= len(levels):
+        return
+    axf = np.zeros(a.nrows)
+    spmv(a, x, axf)
+    rc = r[f2c] - axf[f2c]
+    xc = np.zeros(f2c.size)
+    mg_vcycle(levels, lev + 1, rc, xc)
+    x[f2c] += xc
+    symgs_colored(a, r, x, colors)
+
+
+def pcg_mg(levels, b: np.ndarray, tol=1e-9, max_iters=50) -> OCgResult:
+    """HPCG's preconditioned CG (ComputeCG_ref) with the MG preconditioner;
+    history = ||r|| / ||b|| like the unpreconditioned solver."""
+    a = levels[0][0]
+    n = a.nrows
+    x, r, z, p, ap = (np.zeros(n) for _ in range(5))
+    spmv(a, x, ap)
+    waxpby(1.0, b, -1.0, ap, r)
+    nb = math.sqrt(dot(b, b))
+    scale = nb if nb > 0.0 else 1.0
+    hist = [math.sqrt(dot(r, r)) / scale]
+    if hist[0] <= tol:
+        return OCgResult(x, 0, np.asarray(hist), True)
+    mg_vcycle(levels, 0, r, z)
+    waxpby(1.0, z, 0.0, z, p)
+    rtz = dot(r, z)
+    it, done = 0, False
+    for k in range(1, max_iters + 1):
+        it = k
+        spmv(a, p, ap)
+        pap = dot(p, ap)
+        if pap <= 0.0:
+            raise OracleBreakdown(f"p'Ap = {pap} at iteration {k}")
+        alpha = rtz / pap
+        waxpby(1.0, x, alpha, p, x)
+        waxpby(1.0, r, -alpha, ap, r)
+        hist.append(math.sqrt(dot(r, r)) / scale)
+        if hist[-1] <= tol:
+            done = True
+            break
+        mg_vcycle(levels, 0, r, z)
+        rtz_new = dot(r, z)
+        waxpby(1.0, z, rtz_new / rtz, p, p)
+        rtz = rtz_new
+    return OCgResult(x, it, np.asarray(hist), done)

@@ -99,6 +99,9 @@ _SIGNATURES = {
     "ds_convert_finish_dia": (c_int, [c_vp, c_vp, c_vp]),
     "ds_convert_abort": (None, [c_vp]),
     "ds_gather": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "ds_symgs": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, P_i64, c_int, c_vp, c_vp, c_vp]),
+    "ds_mg_restrict": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "ds_mg_prolong": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp]),
     "ds_stencil_begin": (c_int, [c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_vp,
                                  ctypes.POINTER(c_vp), P_i64, P_i64]),
     "ds_stencil_finish": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
