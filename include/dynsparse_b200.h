@@ -311,13 +311,52 @@ int ds_allgather_f64(const double* send, double* recv, int64_t count, void* comm
 /* ---- HPCG smoother and multigrid transfers (NOT in the
  * reference -- parity pinned to the oracle's restatement of HPCG's
  * ComputeSYMGS_ref / ComputeMG_ref with the 8-colour stencil ordering) -----
- * ds_symgs: one symmetric sweep in place, colours 0..n-1 then n-1..0; rows of
+ * ds_symgs: one symmetric sweep in place, colours 0..n-1 then n-1..0 (the
+ * second, identical visit of colour n-1 is skipped); rows of
  * colour c are color_rows[color_start[c] .. color_start[c+1]).  Per row:
  * s = r[i]; s -= a_ij*x[j] (j != i, stored order, no FMA); x[i] = s / a_ii. */
 int ds_symgs(int64_t nrows, const int32_t* row_offsets, const int32_t* cols,
              const double* values, const int32_t* color_rows, const int64_t* color_start,
              int ncolors, const double* r, double* x, void* stream);
+/* Colour-ordered ELL layout of the same sweep (coalesced slot loads):
+ * ds_symgs_ell_width -> max off-diagonal count per row (synchronises stream);
+ * round it up to a supported width (8, 16, 26, 32); ds_symgs_ell_fill writes
+ * ell_cols/ell_vals [width][nrows] (slot-major over colour position),
+ * ell_len[nrows] and diag[nrows]; ds_symgs_ell sweeps bitwise like ds_symgs. */
+int ds_symgs_ell_width(int64_t nrows, const int32_t* row_offsets, const int32_t* cols,
+                       int32_t* width_out, void* stream);
+int ds_symgs_ell_fill(int64_t nrows, int32_t width, const int32_t* row_offsets,
+                      const int32_t* cols, const double* values, const int32_t* color_rows,
+                      int32_t* ell_cols, double* ell_vals, int32_t* ell_len, double* diag,
+                      void* stream);
+int ds_symgs_ell(int64_t nrows, int32_t width, const int32_t* color_rows,
+                 const int64_t* color_start, int ncolors, const int32_t* ell_cols,
+                 const double* ell_vals, const int32_t* ell_len, const double* diag,
+                 const double* r, double* x, void* stream);
+/* Device-resident PCG (ComputeCG_ref with z = M r): the host writes the block
+ * after setup; each iteration is spmv(p) -> ds_dot(p,Ap -> &pap) ->
+ * ds_pcg_alpha -> ds_pcg_axpy(x += alpha p) -> ds_pcg_axpy(r -= alpha Ap) ->
+ * ds_dot(r,r -> &rr) -> ds_pcg_check -> V-cycle(r -> z) ->
+ * ds_dot(r,z -> &rtz_new) -> ds_pcg_beta -> ds_pcg_axpy(p = z + beta p).
+ * Vector updates are no-ops once done != 0 (graph replays may overshoot).  */
+typedef struct ds_pcg_scalars {
+  double rtz, pap, rr, rtz_new, alpha, beta, scale, tol;
+  int32_t iter, max_iters;
+  int32_t done;     /* 0 running, 1 converged, 2 breakdown, 3 max_iters     */
+  int32_t pad;
+} ds_pcg_scalars;
+int ds_pcg_alpha(ds_pcg_scalars* s, void* stream);
+int ds_pcg_check(ds_pcg_scalars* s, double* history, void* stream);
+int ds_pcg_beta(ds_pcg_scalars* s, void* stream);
+/* w = 1.0*x + c*y, c = *coef_dev (negated when negate != 0); guarded by s->done */
+int ds_pcg_axpy(int64_t n, double* w, const double* x, const double* coef_dev, int negate,
+                const double* y, const ds_pcg_scalars* s, void* stream);
 /* rc[i] = r[f2c[i]] - axf[f2c[i]]  /  x[f2c[i]] += xc[i]                   */
+/* Fused residual + restriction on a DIA operator: rc[i] = r[f] - (A z)[f],
+ * f = f2c[i], forming only the coarse rows of A z (bitwise equal to
+ * ds_spmv + ds_mg_restrict).  DS_ERR_NOT_SUPPORTED for other formats.      */
+int ds_mg_restrict_residual(const ds_matrix* a, int64_t ncoarse, const int32_t* f2c,
+                            const double* z, const double* r, double* rc, void* stream);
 int ds_mg_restrict(int64_t ncoarse, const int32_t* f2c, const double* r, const double* axf,
                    double* rc, void* stream);
 int ds_mg_prolong(int64_t ncoarse, const int32_t* f2c, const double* xc, double* x,

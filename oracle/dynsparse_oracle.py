@@ -705,9 +705,11 @@ def symgs_colored(m: OCsr, r: np.ndarray, x: np.ndarray, colors: np.ndarray) -> 
     assert x.size == n
 
 
-def mg_levels(nx, ny, nz, levels=4):
-    """[(matrix, colors, f2c)] finest first; coarse grids halve every
-    dimension while it stays even (GenerateCoarseProblem)."""
+def mg_levels(nx, ny, nz, levels=4, fmt=CSR):
+    """[(matrix, colors, f2c, op)] finest first; coarse grids halve every
+    dimension while it stays even (GenerateCoarseProblem).  ``op`` is the
+    level matrix converted to ``fmt`` -- the format the residual SpMVs run
+    in (the smoother always walks the CSR rows)."""
     out = []
     for lev in range(levels):
         part = stencil_partition(nx, ny, nz)
@@ -717,7 +719,8 @@ def mg_levels(nx, ny, nz, levels=4):
             ic = np.arange(cx * cy * cz, dtype=I64)
             xc, yc, zc = ic % cx, (ic // cx) % cy, ic // (cx * cy)
             f2c = 2 * xc + nx * (2 * yc + ny * 2 * zc)
-        out.append((part.a_full, stencil_colors(nx, ny, nz), f2c))
+        a = part.a_full
+        out.append((a, stencil_colors(nx, ny, nz), f2c, a if fmt == CSR else convert(a, fmt)))
         if f2c is None:
             break
         nx, ny, nz = nx // 2, ny // 2, nz // 2
@@ -727,13 +730,13 @@ def mg_levels(nx, ny, nz, levels=4):
 def mg_vcycle(levels, lev: int, r: np.ndarray, x: np.ndarray) -> None:
     """ComputeMG_ref: x = 0; pre-smooth; Axf = A x; rc = r[f2c] - Axf[f2c];
     recurse; x[f2c] += xc; post-smooth (coarsest: one smooth)."""
-    a, colors, f2c = levels[lev]
+    a, colors, f2c, op = levels[lev]
     x[:] = 0.0
     symgs_colored(a, r, x, colors)
     if f2c is None or lev + 1 >= len(levels):
         return
     axf = np.zeros(a.nrows)
-    spmv(a, x, axf)
+    spmv(op, x, axf)
     rc = r[f2c] - axf[f2c]
     xc = np.zeros(f2c.size)
     mg_vcycle(levels, lev + 1, rc, xc)
@@ -744,7 +747,7 @@ def mg_vcycle(levels, lev: int, r: np.ndarray, x: np.ndarray) -> None:
 def pcg_mg(levels, b: np.ndarray, tol=1e-9, max_iters=50) -> OCgResult:
     """HPCG's preconditioned CG (ComputeCG_ref) with the MG preconditioner;
     history = ||r|| / ||b|| like the unpreconditioned solver."""
-    a = levels[0][0]
+    a = levels[0][3]
     n = a.nrows
     x, r, z, p, ap = (np.zeros(n) for _ in range(5))
     spmv(a, x, ap)

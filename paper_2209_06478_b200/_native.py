@@ -63,6 +63,16 @@ class DsCgScalars(ctypes.Structure):
 
 
 CG_SCALARS_BYTES = ctypes.sizeof(DsCgScalars)
+
+
+class DsPcgScalars(ctypes.Structure):
+    """Mirror of ``ds_pcg_scalars`` (lives on the device; 80 bytes)."""
+
+    _fields_ = [
+        ("rtz", c_dbl), ("pap", c_dbl), ("rr", c_dbl), ("rtz_new", c_dbl),
+        ("alpha", c_dbl), ("beta", c_dbl), ("scale", c_dbl), ("tol", c_dbl),
+        ("iter", c_i32), ("max_iters", c_i32), ("done", c_i32), ("pad", c_i32),
+    ]
 P_mat = ctypes.POINTER(DsMatrix)
 
 # name -> (restype, argtypes)
@@ -100,6 +110,16 @@ _SIGNATURES = {
     "ds_convert_abort": (None, [c_vp]),
     "ds_gather": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp]),
     "ds_symgs": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, P_i64, c_int, c_vp, c_vp, c_vp]),
+    "ds_symgs_ell_width": (c_int, [c_i64, c_vp, c_vp, ctypes.POINTER(c_i32), c_vp]),
+    "ds_symgs_ell_fill": (c_int, [c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                  c_vp]),
+    "ds_symgs_ell": (c_int, [c_i64, c_i32, c_vp, P_i64, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                             c_vp]),
+    "ds_pcg_alpha": (c_int, [c_vp, c_vp]),
+    "ds_pcg_check": (c_int, [c_vp, c_vp, c_vp]),
+    "ds_pcg_beta": (c_int, [c_vp, c_vp]),
+    "ds_pcg_axpy": (c_int, [c_i64, c_vp, c_vp, c_vp, c_int, c_vp, c_vp, c_vp]),
+    "ds_mg_restrict_residual": (c_int, [P_mat, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "ds_mg_restrict": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "ds_mg_prolong": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp]),
     "ds_stencil_begin": (c_int, [c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_vp,

@@ -53,6 +53,178 @@ __global__ void prolong_kernel(int64_t nc, const int* __restrict__ f2c,
   }
 }
 
+
+// ---- colour-ordered ELL copy of the operator for the sweep -----------------
+// Position k (0..n) walks the rows colour by colour (color_rows); slot q of
+// position k lives at [q * n + k], so the 32 rows of a warp read each slot
+// as one coalesced 256 B (values) / 128 B (columns) segment.  The diagonal is
+// held apart (diag[k]); off-diagonals keep their stored order; rows shorter
+// than the width are padded with (column i, 0.0) and the padding never enters
+// the arithmetic (len[k] predicates it), so the sweep stays bitwise equal to
+// the CSR walk.
+__global__ void ell_width_kernel(int64_t n, const int* __restrict__ off,
+                                 const int* __restrict__ col, int* width) {
+  int w = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int c = 0;
+    for (int q = off[i]; q < off[i + 1]; ++q) c += col[q] != (int)i;
+    w = max(w, c);
+  }
+  for (int o = 16; o; o >>= 1) w = max(w, __shfl_xor_sync(0xffffffffu, w, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(width, w);
+}
+
+__global__ void ell_fill_kernel(int64_t n, int width, const int* __restrict__ rows,
+                                const int* __restrict__ off, const int* __restrict__ col,
+                                const double* __restrict__ val, int* ecol, double* eval,
+                                int* elen, double* diag) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int i = rows[k];
+    int q = 0;
+    double d = 0.0;
+    for (int e = off[i]; e < off[i + 1]; ++e) {
+      const int j = col[e];
+      if (j == i) { d = val[e]; continue; }
+      ecol[(int64_t)q * n + k] = j;
+      eval[(int64_t)q * n + k] = val[e];
+      ++q;
+    }
+    elen[k] = q;
+    diag[k] = d;
+    for (; q < width; ++q) {
+      ecol[(int64_t)q * n + k] = i;
+      eval[(int64_t)q * n + k] = 0.0;
+    }
+  }
+}
+
+// Slots are processed in chunks of CH: all CH column/value loads, then all CH
+// gathers of x, are issued before any arithmetic (compiler barriers keep
+// them batched), so each thread has ~2*CH independent loads in flight --
+// a colour covers under one wave of the GPU, so the memory-level
+// parallelism has to come from inside the thread.
+template <int W, int CH>
+__device__ __forceinline__ void relax_ell(int64_t n, int64_t k, const int* __restrict__ rows,
+                                          const int* __restrict__ ecol,
+                                          const double* __restrict__ eval,
+                                          const int* __restrict__ elen,
+                                          const double* __restrict__ diag,
+                                          const double* __restrict__ r, double* x) {
+  static_assert(W % CH == 0, "chunk must divide the width");
+  const int i = rows[k];
+  const int len = elen[k];
+  const double dk = diag[k];
+  double s = r[i];
+#pragma unroll
+  for (int c0 = 0; c0 < W; c0 += CH) {
+    int j[CH];
+    double a[CH], xv[CH];
+#pragma unroll
+    for (int q = 0; q < CH; ++q) {
+      j[q] = __ldg(ecol + (int64_t)(c0 + q) * n + k);
+      a[q] = __ldg(eval + (int64_t)(c0 + q) * n + k);
+    }
+#pragma unroll
+    for (int q = 0; q < CH; ++q) xv[q] = x[j[q]];
+#pragma unroll
+    for (int q = 0; q < CH; ++q) {
+      const double t = __dadd_rn(s, -__dmul_rn(a[q], xv[q]));
+      s = c0 + q < len ? t : s;
+    }
+  }
+  x[i] = __ddiv_rn(s, dk);
+}
+
+// Slots are processed in chunks of CH: the CH column/value loads and then
+// the CH gathers of x are independent, so each thread has ~2*CH loads in
+// flight -- a colour covers under one wave of the GPU, so the memory-level
+// parallelism has to come from inside the thread (MINB steers ptxas towards
+// hoisting the loads).
+template <int W, int CH, int MINB>
+__global__ void __launch_bounds__(128, MINB) symgs_ell_kernel(
+    int64_t n, int64_t k0, int64_t k1, const int* __restrict__ rows,
+    const int* __restrict__ ecol, const double* __restrict__ eval,
+    const int* __restrict__ elen, const double* __restrict__ diag,
+    const double* __restrict__ r, double* x) {
+  for (int64_t k = k0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < k1;
+       k += (int64_t)gridDim.x * blockDim.x)
+    relax_ell<W, CH>(n, k, rows, ecol, eval, elen, diag, r, x);
+}
+
+// ---- device-resident PCG scalars (ComputeCG_ref's scalar recurrences) ------
+// Tiny single-thread kernels carry the scalar recurrences so an iteration
+// never returns to the host and can be captured as a CUDA graph; every
+// vector update is guarded by `done`, so replaying past convergence is a
+// no-op for x, r and the history.
+__global__ void pcg_alpha_kernel(ds_pcg_scalars* s) {
+  if (s->done) return;
+  if (!(s->pap > 0.0) && s->pap <= 0.0) { s->done = 2; return; }   // p'Ap <= 0
+  s->alpha = __ddiv_rn(s->rtz, s->pap);
+}
+
+__global__ void pcg_check_kernel(ds_pcg_scalars* s, double* history) {
+  if (s->done) return;
+  const int it = s->iter + 1;
+  s->iter = it;
+  const double h = __ddiv_rn(__dsqrt_rn(s->rr), s->scale);
+  if (history) history[it] = h;
+  if (h <= s->tol) s->done = 1;
+  else if (it >= s->max_iters) s->done = 3;
+}
+
+__global__ void pcg_beta_kernel(ds_pcg_scalars* s) {
+  if (s->done) return;
+  s->beta = __ddiv_rn(s->rtz_new, s->rtz);
+  s->rtz = s->rtz_new;
+}
+
+// w = 1.0*x + c*y with c = +-(*coef)   (waxpby, two rounded products)
+__global__ void pcg_axpy_kernel(int64_t n, double* w, const double* x, const double* coef,
+                                int negate, const double* y, const int* done) {
+  if (*done) return;
+  const double c = negate ? -*coef : *coef;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    w[i] = __dadd_rn(__dmul_rn(1.0, x[i]), __dmul_rn(c, y[i]));
+}
+
+// The symmetric sweep visits colours 0..C-1 then C-1..0.  The two visits of
+// colour C-1 are back to back with no other colour updated in between, and a
+// row never reads its own colour, so the second visit recomputes identical
+// bits: it is skipped (2C-1 passes, not 2C).
+static inline int sweep_color(int q, int ncolors) {
+  return q < ncolors ? q : 2 * ncolors - 2 - q;
+}
+
+// ---- fused residual + restriction for a DIA level operator -----------------
+// rc[i] = r[f] - (A z)[f] with f = f2c[i]: only the coarse points' rows of
+// A z are formed (1/8 of the SpMV), each with the DIA SpMV's exact order --
+// sequential over the in-range diagonals from +0.0 -- so rc is bitwise the
+// SpMV-then-restrict result.
+template <int ND>
+__global__ void __launch_bounds__(256) dia_restrict_kernel(
+    int64_t nc, const int* __restrict__ f2c, int64_t ncols, int ndiags_rt,
+    const int* __restrict__ offsets, const double* __restrict__ vals,
+    const double* __restrict__ z, const double* __restrict__ r, double* rc) {
+  const int nd = ND > 0 ? ND : ndiags_rt;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nc;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t f = f2c[i];
+    const double* v = vals + f * nd;
+    double acc = 0.0;
+#pragma unroll 9
+    for (int j = 0; j < nd; ++j) {
+      const int64_t c = f + __ldg(offsets + j);
+      const bool in = c >= 0 && c < ncols;
+      const double p = __dmul_rn(__ldg(v + j), z[in ? c : f]);
+      acc = in ? __dadd_rn(acc, p) : acc;
+    }
+    rc[i] = __dadd_rn(r[f], -acc);
+  }
+}
+
 static unsigned grid_n(int64_t n) {
   int64_t g = ceil_div(n, 256);
   const int64_t cap = (int64_t)sm_count() * 16;
@@ -71,15 +243,121 @@ extern "C" int ds_symgs(int64_t nrows, const int32_t* row_offsets, const int32_t
                         void* stream) {
   (void)nrows;
   cudaStream_t st = as_stream(stream);
-  for (int pass = 0; pass < 2; ++pass)
-    for (int q = 0; q < ncolors; ++q) {
-      const int c = pass == 0 ? q : ncolors - 1 - q;
-      const int64_t cnt = color_start[c + 1] - color_start[c];
-      if (cnt <= 0) continue;
-      symgs_color_kernel<<<grid_n(cnt), 256, 0, st>>>(cnt, color_rows + color_start[c],
-                                                      row_offsets, cols, values, r, x);
-    }
+  for (int q = 0; q < 2 * ncolors - 1; ++q) {
+    const int c = sweep_color(q, ncolors);
+    const int64_t cnt = color_start[c + 1] - color_start[c];
+    if (cnt <= 0) continue;
+    symgs_color_kernel<<<grid_n(cnt), 256, 0, st>>>(cnt, color_rows + color_start[c],
+                                                    row_offsets, cols, values, r, x);
+  }
   DS_LAUNCH_CHECK("symgs_color_kernel");
+  return DS_OK;
+}
+
+
+extern "C" int ds_symgs_ell_width(int64_t nrows, const int32_t* row_offsets, const int32_t* cols,
+                                  int32_t* width_out, void* stream) {
+  if (!width_out) { set_error("ds_symgs_ell_width: width_out is NULL"); return DS_ERR_INVALID_ARGUMENT; }
+  *width_out = 0;
+  if (nrows <= 0) return DS_OK;
+  cudaStream_t st = as_stream(stream);
+  int* dw = nullptr;
+  DS_CUDA(cudaMallocAsync(&dw, sizeof(int), st));
+  DS_CUDA(cudaMemsetAsync(dw, 0, sizeof(int), st));
+  ell_width_kernel<<<grid_n(nrows), 256, 0, st>>>(nrows, row_offsets, cols, dw);
+  DS_LAUNCH_CHECK("ell_width_kernel");
+  int w = 0;
+  DS_CUDA(cudaMemcpyAsync(&w, dw, sizeof(int), cudaMemcpyDeviceToHost, st));
+  DS_CUDA(cudaFreeAsync(dw, st));
+  DS_CUDA(cudaStreamSynchronize(st));
+  *width_out = w;
+  return DS_OK;
+}
+
+extern "C" int ds_symgs_ell_fill(int64_t nrows, int32_t width, const int32_t* row_offsets,
+                                 const int32_t* cols, const double* values,
+                                 const int32_t* color_rows, int32_t* ell_cols, double* ell_vals,
+                                 int32_t* ell_len, double* diag, void* stream) {
+  if (nrows <= 0) return DS_OK;
+  ell_fill_kernel<<<grid_n(nrows), 256, 0, as_stream(stream)>>>(
+      nrows, width, color_rows, row_offsets, cols, values, ell_cols, ell_vals, ell_len, diag);
+  DS_LAUNCH_CHECK("ell_fill_kernel");
+  return DS_OK;
+}
+
+extern "C" int ds_symgs_ell(int64_t nrows, int32_t width, const int32_t* color_rows,
+                            const int64_t* color_start, int ncolors, const int32_t* ell_cols,
+                            const double* ell_vals, const int32_t* ell_len, const double* diag,
+                            const double* r, double* x, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  const int wt = width <= 8 ? 8 : width <= 16 ? 16 : width <= 26 ? 26 : width <= 32 ? 32 : -1;
+  if (wt != width) {
+    set_error("ds_symgs_ell: width %d must be one of 8, 16, 26, 32 (pad the layout)", width);
+    return DS_ERR_NOT_SUPPORTED;
+  }
+  for (int q = 0; q < 2 * ncolors - 1; ++q) {
+    const int c = sweep_color(q, ncolors);
+    const int64_t k0 = color_start[c], k1 = color_start[c + 1];
+    if (k1 <= k0) continue;
+    const unsigned g = (unsigned)min64(ceil_div(k1 - k0, 128), (int64_t)sm_count() * 32);
+#define DS_SYMGS_LAUNCH(W_, CH_)                                                      \
+  symgs_ell_kernel<W_, CH_, 8><<<g, 128, 0, st>>>(nrows, k0, k1, color_rows, ell_cols, \
+                                                  ell_vals, ell_len, diag, r, x)
+    switch (width) {
+      case 8: DS_SYMGS_LAUNCH(8, 8); break;
+      case 16: DS_SYMGS_LAUNCH(16, 8); break;
+      case 26: DS_SYMGS_LAUNCH(26, 13); break;
+      default: DS_SYMGS_LAUNCH(32, 8); break;
+    }
+#undef DS_SYMGS_LAUNCH
+  }
+  DS_LAUNCH_CHECK("symgs_ell_kernel");
+  return DS_OK;
+}
+
+extern "C" int ds_pcg_alpha(ds_pcg_scalars* s, void* stream) {
+  pcg_alpha_kernel<<<1, 1, 0, as_stream(stream)>>>(s);
+  DS_LAUNCH_CHECK("pcg_alpha_kernel");
+  return DS_OK;
+}
+
+extern "C" int ds_pcg_check(ds_pcg_scalars* s, double* history, void* stream) {
+  pcg_check_kernel<<<1, 1, 0, as_stream(stream)>>>(s, history);
+  DS_LAUNCH_CHECK("pcg_check_kernel");
+  return DS_OK;
+}
+
+extern "C" int ds_pcg_beta(ds_pcg_scalars* s, void* stream) {
+  pcg_beta_kernel<<<1, 1, 0, as_stream(stream)>>>(s);
+  DS_LAUNCH_CHECK("pcg_beta_kernel");
+  return DS_OK;
+}
+
+extern "C" int ds_pcg_axpy(int64_t n, double* w, const double* x, const double* coef_dev,
+                           int negate, const double* y, const ds_pcg_scalars* s, void* stream) {
+  if (n <= 0) return DS_OK;
+  pcg_axpy_kernel<<<grid_n(n), 256, 0, as_stream(stream)>>>(n, w, x, coef_dev, negate, y,
+                                                            &s->done);
+  DS_LAUNCH_CHECK("pcg_axpy_kernel");
+  return DS_OK;
+}
+
+extern "C" int ds_mg_restrict_residual(const ds_matrix* a, int64_t ncoarse, const int32_t* f2c,
+                                       const double* z, const double* r, double* rc,
+                                       void* stream) {
+  if (!a || a->format != DS_FMT_DIA) {
+    set_error("ds_mg_restrict_residual: the level operator must be DIA");
+    return DS_ERR_NOT_SUPPORTED;
+  }
+  if (ncoarse <= 0) return DS_OK;
+  cudaStream_t st = as_stream(stream);
+  if (a->ndiags == 27)
+    dia_restrict_kernel<27><<<grid_n(ncoarse), 256, 0, st>>>(
+        ncoarse, f2c, a->ncols, 27, a->idx0, a->values, z, r, rc);
+  else
+    dia_restrict_kernel<0><<<grid_n(ncoarse), 256, 0, st>>>(
+        ncoarse, f2c, a->ncols, a->ndiags, a->idx0, a->values, z, r, rc);
+  DS_LAUNCH_CHECK("dia_restrict_kernel");
   return DS_OK;
 }
 

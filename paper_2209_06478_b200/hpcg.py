@@ -27,7 +27,7 @@ import numpy as np
 
 from . import _native
 from .errors import BreakdownZeroCurvature, DimensionMismatch
-from .formats import CsrMatrix, DenseVector, MemorySpace
+from .formats import CsrMatrix, DenseVector, FormatId, MemorySpace
 from .solver import CgResult
 from .stencil import GridSpec, generate_partition
 
@@ -62,6 +62,9 @@ class MgLevel:
     r: object = None
     x: object = None
     axf: object = None
+    ell: tuple | None = None    # (width, cols, vals, len, diag) colour-ordered ELL
+    op: object = None           # the level operator in the SpMV format
+    desc: object = None         # cached ds_matrix descriptor of ``op``
 
     @property
     def nrows(self) -> int:
@@ -74,9 +77,20 @@ class MgHierarchy:
     device: object = None
 
     @staticmethod
-    def build(nx: int, ny: int, nz: int, nlevels: int = 4, device=None) -> "MgHierarchy":
+    def build(nx: int, ny: int, nz: int, nlevels: int = 4, device=None,
+              layout: str = "ell", spmv_format="dia") -> "MgHierarchy":
         """GenerateProblem + GenerateCoarseProblem: each coarse grid halves
-        every dimension while all three stay even (at most ``nlevels``)."""
+        every dimension while all three stay even (at most ``nlevels``).
+        ``layout`` "ell" adds the colour-ordered ELL copy the sweep reads
+        (coalesced); "csr" sweeps the CSR operator directly.  The residual
+        SpMVs (PCG's A p and the V-cycle's A z) run on the level operator
+        converted to ``spmv_format`` -- the runtime format switch applied to
+        HPCG (DIA streams the 27 diagonals at ~90% of HBM)."""
+        from .datamove import convert
+        from .formats import as_format_id
+        fmt = as_format_id(spmv_format)
+        if layout not in ("ell", "csr"):
+            raise ValueError(f"layout must be 'ell' or 'csr', got {layout!r}")
         import torch
         from . import _device
         dev = _device.require_cuda(device)
@@ -98,6 +112,9 @@ class MgHierarchy:
                 dims=(nx, ny, nz), a=part.a_full, color_rows=torch.from_numpy(rows).to(dev),
                 color_start=start, f2c=f2c, r=torch.empty(n, **f64), x=torch.empty(n, **f64),
                 axf=torch.empty(n, **f64)))
+            if layout == "ell":
+                h.levels[-1].ell = _ell(h.levels[-1], dev)
+            h.levels[-1].op = part.a_full if fmt == FormatId.CSR else convert(part.a_full, fmt)
             if not coarsen:
                 break
             nx, ny, nz = nx // 2, ny // 2, nz // 2
@@ -108,38 +125,83 @@ class MgHierarchy:
         from . import _device
         return _device.stream(self.device)
 
-    def symgs(self, lev: int, r, x) -> None:
-        """One symmetric colour sweep in place on level ``lev`` (ds_symgs)."""
+    def symgs(self, lev: int, r, x, st=None) -> None:
+        """One symmetric colour sweep in place on level ``lev`` (ds_symgs_ell,
+        or ds_symgs on the CSR operator)."""
         L = self.levels[lev]
         a = L.a
-        st = L.color_start
+        cs = L.color_start.ctypes.data_as(_native.P_i64)
+        st = self._stream() if st is None else st
+        if L.ell is not None:
+            w, ec, ev, el, dg = L.ell
+            _native.call("ds_symgs_ell", a.nrows, w, L.color_rows.data_ptr(), cs, NCOLORS,
+                         ec.data_ptr(), ev.data_ptr(), el.data_ptr(), dg.data_ptr(),
+                         r.data_ptr(), x.data_ptr(), st)
+            return
         _native.call("ds_symgs", a.nrows, a.row_offsets.data_ptr(), a.col_indices.data_ptr(),
-                     a.values.data_ptr(), L.color_rows.data_ptr(),
-                     st.ctypes.data_as(_native.P_i64), NCOLORS, r.data_ptr(), x.data_ptr(),
-                     self._stream())
+                     a.values.data_ptr(), L.color_rows.data_ptr(), cs, NCOLORS, r.data_ptr(),
+                     x.data_ptr(), st)
 
-    def _spmv(self, lev: int, x, y) -> None:
-        from .kernels import descriptor
-        d = descriptor(self.levels[lev].a)
-        _native.call("ds_spmv", ctypes.byref(d), x.data_ptr(), y.data_ptr(), 0, self._stream())
+    def _desc(self, lev: int):
+        L = self.levels[lev]
+        if L.desc is None:
+            from .kernels import descriptor
+            L.desc = descriptor(L.op)
+        return L.desc
 
-    def vcycle(self, r, z, lev: int = 0) -> None:
+    def _spmv(self, lev: int, x, y, st=None) -> None:
+        _native.call("ds_spmv", ctypes.byref(self._desc(lev)), x.data_ptr(), y.data_ptr(), 0,
+                     self._stream() if st is None else st)
+
+    def vcycle(self, r, z, lev: int = 0, st=None) -> None:
         """z = M^-1 r (ComputeMG_ref): z = 0; pre-smooth; restrict
         r - A z; recurse; prolong; post-smooth.  Coarsest: one smooth."""
         L = self.levels[lev]
-        z.zero_()
-        self.symgs(lev, r, z)
+        st = self._stream() if st is None else st
+        z.zero_()                    # torch's current stream == st (eager or capture)
+        self.symgs(lev, r, z, st)
         if L.f2c is None:
             return
         C = self.levels[lev + 1]
-        st = self._stream()
-        self._spmv(lev, z, L.axf)
         nc = C.nrows
-        _native.call("ds_mg_restrict", nc, L.f2c.data_ptr(), r.data_ptr(), L.axf.data_ptr(),
-                     C.r.data_ptr(), st)
-        self.vcycle(C.r, C.x, lev + 1)
+        if L.op.format_id == FormatId.DIA:
+            # only the coarse rows of A z are formed (fused, bitwise equal)
+            _native.call("ds_mg_restrict_residual", ctypes.byref(self._desc(lev)), nc,
+                         L.f2c.data_ptr(), z.data_ptr(), r.data_ptr(), C.r.data_ptr(), st)
+        else:
+            self._spmv(lev, z, L.axf, st)
+            _native.call("ds_mg_restrict", nc, L.f2c.data_ptr(), r.data_ptr(),
+                         L.axf.data_ptr(), C.r.data_ptr(), st)
+        self.vcycle(C.r, C.x, lev + 1, st)
         _native.call("ds_mg_prolong", nc, L.f2c.data_ptr(), C.x.data_ptr(), z.data_ptr(), st)
-        self.symgs(lev, r, z)
+        self.symgs(lev, r, z, st)
+
+
+_ELL_WIDTHS = (8, 16, 26, 32)
+
+
+def _ell(L: MgLevel, dev):
+    """Colour-ordered ELL copy of the level operator (None if a row has more
+    than 32 off-diagonals: the sweep then reads the CSR operator)."""
+    import torch
+    from . import _device
+    a = L.a
+    n = a.nrows
+    st = _device.stream(dev)
+    w = ctypes.c_int32()
+    _native.call("ds_symgs_ell_width", n, a.row_offsets.data_ptr(), a.col_indices.data_ptr(),
+                 ctypes.byref(w), st)
+    width = next((v for v in _ELL_WIDTHS if v >= w.value), None)
+    if width is None:
+        return None
+    ec = torch.empty(width * n, dtype=torch.int32, device=dev)
+    ev = torch.empty(width * n, dtype=torch.float64, device=dev)
+    el = torch.empty(n, dtype=torch.int32, device=dev)
+    dg = torch.empty(n, dtype=torch.float64, device=dev)
+    _native.call("ds_symgs_ell_fill", n, width, a.row_offsets.data_ptr(),
+                 a.col_indices.data_ptr(), a.values.data_ptr(), L.color_rows.data_ptr(),
+                 ec.data_ptr(), ev.data_ptr(), el.data_ptr(), dg.data_ptr(), st)
+    return (width, ec, ev, el, dg)
 
 
 def _t(v):
@@ -171,65 +233,132 @@ def _cuda(dev):
     return torch.cuda.device(dev)
 
 
-def pcg(h: MgHierarchy, b, x0=None, tol: float = 1e-9, max_iters: int = 50) -> CgResult:
-    """HPCG's preconditioned CG (ComputeCG_ref) with the MG preconditioner.
-    History = ||r|| / ||b|| per iteration, like ``cg`` (solver.py:56-189)."""
-    import torch
-    from . import _device
-    dev = h.device
-    n = h.levels[0].nrows
-    bt = _t(b)
-    if bt.numel() != n:
-        raise DimensionMismatch(f"b has {bt.numel()} entries, operator {n}")
-    with _cuda(dev):
-        st = _device.stream(dev)
-        ws = _device.workspace(dev)
-        f64 = dict(dtype=torch.float64, device=dev)
-        x = torch.zeros(n, **f64) if x0 is None else _t(x0).clone()
-        r, z, p, ap = (torch.empty(n, **f64) for _ in range(4))
-        dots = torch.zeros(3, **f64)
+class PcgEngine:
+    """HPCG's preconditioned CG (ComputeCG_ref) with every scalar on the
+    device (ds_pcg_scalars), so an iteration -- SpMV, three dots, the
+    V-cycle's ~120 launches and the guarded vector updates -- is one CUDA
+    graph replay with no host round trip; the host reads the 80-byte scalar
+    block once per chunk of iterations."""
 
-        def ddot(u, v, k):
-            _native.call("ds_dot", n, u.data_ptr(), v.data_ptr(), dots[k:].data_ptr(),
-                         ws.data_ptr(), st)
+    def __init__(self, h: MgHierarchy, b, x0=None, tol: float = 1e-9, max_iters: int = 50):
+        import torch
+        from . import _device
+        self.h, self.dev = h, h.device
+        n = self.n = h.levels[0].nrows
+        bt = _t(b)
+        if bt.numel() != n:
+            raise DimensionMismatch(f"b has {bt.numel()} entries, operator {n}")
+        f64 = dict(dtype=torch.float64, device=self.dev)
+        self.b = bt
+        self.x = torch.zeros(n, **f64) if x0 is None else _t(x0).clone()
+        self.r, self.z, self.p, self.ap = (torch.empty(n, **f64) for _ in range(4))
+        self.tol, self.max_iters = float(tol), int(max_iters)
+        self.hist = torch.zeros(self.max_iters + 1, **f64)
+        self.scal = torch.zeros(ctypes.sizeof(_native.DsPcgScalars), dtype=torch.uint8,
+                                device=self.dev)
+        self.ws = _device.workspace(self.dev)
+        self.graph = None
 
-        def wax(al, u, be, v, w):
-            _native.call("ds_waxpby", n, float(al), u.data_ptr(), float(be), v.data_ptr(),
-                         w.data_ptr(), st)
+    def _sp(self, field: str) -> int:
+        return self.scal.data_ptr() + getattr(_native.DsPcgScalars, field).offset
 
-        h._spmv(0, x, ap)
-        wax(1.0, bt, -1.0, ap, r)
-        ddot(bt, bt, 0)
-        ddot(r, r, 1)
-        bb, rr = dots[:2].tolist()
+    def _dot(self, u, v, field: str, st) -> None:
+        _native.call("ds_dot", self.n, u.data_ptr(), v.data_ptr(), self._sp(field),
+                     self.ws.data_ptr(), st)
+
+    def _axpy(self, w, x, coef: str, negate: int, y, st) -> None:
+        _native.call("ds_pcg_axpy", self.n, w.data_ptr(), x.data_ptr(), self._sp(coef), negate,
+                     y.data_ptr(), self.scal.data_ptr(), st)
+
+    def scalars(self) -> _native.DsPcgScalars:
+        return _native.DsPcgScalars.from_buffer_copy(self.scal.cpu().numpy().tobytes())
+
+    def setup(self) -> bool:
+        """r = b - A x0, ||b||, history[0], z = M r, p = z, r.z.  True if
+        already converged (no iteration needed)."""
+        import torch
+        from . import _device
+        h, n, st = self.h, self.n, _device.stream(self.dev)
+        h._spmv(0, self.x, self.ap)
+        _native.call("ds_waxpby", n, 1.0, self.b.data_ptr(), -1.0, self.ap.data_ptr(),
+                     self.r.data_ptr(), st)
+        self._dot(self.b, self.b, "rtz_new", st)          # scratch slots for bb, rr
+        self._dot(self.r, self.r, "rr", st)
+        sc = self.scalars()
+        bb, rr = sc.rtz_new, sc.rr
         nb = math.sqrt(bb)
         scale = nb if nb > 0.0 else 1.0
-        hist = [math.sqrt(rr) / scale]
-        if hist[0] <= tol:
-            return CgResult(DenseVector(x), 0, np.asarray(hist), True)
-        h.vcycle(r, z)
-        wax(1.0, z, 0.0, z, p)
-        ddot(r, z, 2)
-        rtz = float(dots[2].item())
-        it, done = 0, False
-        for k in range(1, max_iters + 1):
-            it = k
-            h._spmv(0, p, ap)
-            ddot(p, ap, 0)
-            pap = float(dots[0].item())
-            if pap <= 0.0:
-                raise BreakdownZeroCurvature(f"p'Ap = {pap} at iteration {k}")
-            alpha = rtz / pap
-            wax(1.0, x, alpha, p, x)
-            wax(1.0, r, -alpha, ap, r)
-            ddot(r, r, 1)
-            hist.append(math.sqrt(float(dots[1].item())) / scale)
-            if hist[-1] <= tol:
-                done = True
-                break
-            h.vcycle(r, z)
-            ddot(r, z, 2)
-            rtz_new = float(dots[2].item())
-            wax(1.0, z, rtz_new / rtz, p, p)
-            rtz = rtz_new
-        return CgResult(DenseVector(x), it, np.asarray(hist), done)
+        h0 = math.sqrt(rr) / scale
+        init = _native.DsPcgScalars(rr=rr, scale=scale, tol=self.tol,
+                                    max_iters=self.max_iters, done=1 if h0 <= self.tol else 0)
+        self.scal.copy_(torch.frombuffer(bytearray(bytes(init)), dtype=torch.uint8))
+        self.hist[0] = h0
+        if init.done:
+            return True
+        h.vcycle(self.r, self.z)
+        _native.call("ds_waxpby", n, 1.0, self.z.data_ptr(), 0.0, self.z.data_ptr(),
+                     self.p.data_ptr(), st)
+        self._dot(self.r, self.z, "rtz", st)
+        return False
+
+    def step(self, st) -> None:
+        h = self.h
+        h._spmv(0, self.p, self.ap, st)
+        self._dot(self.p, self.ap, "pap", st)
+        _native.call("ds_pcg_alpha", self.scal.data_ptr(), st)
+        self._axpy(self.x, self.x, "alpha", 0, self.p, st)
+        self._axpy(self.r, self.r, "alpha", 1, self.ap, st)
+        self._dot(self.r, self.r, "rr", st)
+        _native.call("ds_pcg_check", self.scal.data_ptr(), self.hist.data_ptr(), st)
+        h.vcycle(self.r, self.z, 0, st)
+        self._dot(self.r, self.z, "rtz_new", st)
+        _native.call("ds_pcg_beta", self.scal.data_ptr(), st)
+        self._axpy(self.p, self.z, "beta", 0, self.p, st)
+
+    def _capture(self, c: int) -> None:
+        import torch
+        from . import _device
+        cap = torch.cuda.Stream(self.dev)
+        cap.wait_stream(torch.cuda.current_stream(self.dev))
+        with torch.cuda.stream(cap):
+            ws = _device.workspace(self.dev)       # workspace bound to the capture stream
+        torch.cuda.synchronize(self.dev)
+        saved, self.ws = self.ws, ws
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=cap):
+            for _ in range(c):
+                self.step(cap.cuda_stream)
+        self.ws = saved
+        self.graph = g
+
+    def run(self, use_graph: bool = True, chunk: int = 4) -> CgResult:
+        from . import _device
+        with _cuda(self.dev):
+            if not self.setup():
+                if use_graph and self.graph is None:
+                    self._capture(chunk)
+                rounds = 1
+                while True:
+                    for _ in range(rounds):
+                        if use_graph:
+                            self.graph.replay()
+                        else:
+                            st = _device.stream(self.dev)
+                            for _ in range(chunk):
+                                self.step(st)
+                    sc = self.scalars()
+                    if sc.done:
+                        break
+                    rounds = min(rounds * 2, 8)
+            sc = self.scalars()
+            if sc.done == 2:
+                raise BreakdownZeroCurvature(f"p'Ap = {sc.pap} at iteration {sc.iter + 1}")
+            hist = self.hist[:sc.iter + 1].cpu().numpy().copy()
+        return CgResult(DenseVector(self.x), int(sc.iter), hist, sc.done == 1)
+
+
+def pcg(h: MgHierarchy, b, x0=None, tol: float = 1e-9, max_iters: int = 50,
+        use_graph: bool = True) -> CgResult:
+    """HPCG's preconditioned CG (ComputeCG_ref) with the MG preconditioner.
+    History = ||r|| / ||b|| per iteration, like ``cg`` (solver.py:56-189)."""
+    return PcgEngine(h, b, x0, tol, max_iters).run(use_graph=use_graph)

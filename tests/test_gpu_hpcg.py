@@ -25,10 +25,12 @@ def dev(a):
     return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(DEV)
 
 
-@pytest.mark.parametrize("dims", [(8, 8, 8), (5, 6, 7), (16, 8, 4), (1, 1, 3)])
-def test_symgs_bitwise(dims):
+@pytest.mark.parametrize("layout", ["ell", "csr"])
+@pytest.mark.parametrize("dims", [(8, 8, 8), (5, 6, 7), (16, 8, 4), (1, 1, 3), (2, 1, 1)])
+def test_symgs_bitwise(dims, layout):
     nx, ny, nz = dims
-    h = hpcg.MgHierarchy.build(nx, ny, nz, nlevels=1, device=DEV)
+    h = hpcg.MgHierarchy.build(nx, ny, nz, nlevels=1, device=DEV, layout=layout)
+    assert (h.levels[0].ell is not None) == (layout == "ell")
     m = O.stencil_partition(nx, ny, nz).a_full
     rng = np.random.default_rng(sum(dims))
     r = rng.standard_normal(m.nrows)
@@ -41,9 +43,10 @@ def test_symgs_bitwise(dims):
 
 
 @pytest.mark.parametrize("dims", [(16, 16, 16), (8, 12, 16)])
-def test_vcycle_bitwise(dims):
-    h = hpcg.MgHierarchy.build(*dims, nlevels=4, device=DEV)
-    levels = O.mg_levels(*dims, levels=4)
+@pytest.mark.parametrize("layout,fmt", [("ell", "dia"), ("csr", "csr"), ("ell", "coo")])
+def test_vcycle_bitwise(dims, layout, fmt):
+    h = hpcg.MgHierarchy.build(*dims, nlevels=4, device=DEV, layout=layout, spmv_format=fmt)
+    levels = O.mg_levels(*dims, levels=4, fmt={"dia": O.DIA, "csr": O.CSR, "coo": O.COO}[fmt])
     assert [L.nrows for L in h.levels] == [lv[0].nrows for lv in levels]
     rng = np.random.default_rng(7)
     r = rng.standard_normal(levels[0][0].nrows)
@@ -54,13 +57,52 @@ def test_vcycle_bitwise(dims):
     assert zd.cpu().numpy().tobytes() == z.tobytes()
 
 
-def test_pcg_matches_oracle_and_beats_cg():
+def test_symgs_large_level_layouts_agree():
+    """A level spanning many CTAs per colour: ELL and CSR sweeps and the
+    restatement agree bit for bit over repeated sweeps."""
+    dims = (48, 40, 36)
+    m = O.stencil_partition(*dims).a_full
+    rng = np.random.default_rng(5)
+    r, x = rng.standard_normal(m.nrows), rng.standard_normal(m.nrows)
+    outs = []
+    for layout in ("ell", "csr"):
+        h = hpcg.MgHierarchy.build(*dims, nlevels=1, device=DEV, layout=layout)
+        xd = dev(x)
+        for _ in range(3):
+            hpcg.symgs(h, dev(r), xd)
+        outs.append(xd.cpu().numpy())
+    assert outs[0].tobytes() == outs[1].tobytes()
+    ref = x.copy()
+    O.symgs_colored(m, r, ref, O.stencil_colors(*dims))
+    h = hpcg.MgHierarchy.build(*dims, nlevels=1, device=DEV)
+    xd = dev(x)
+    hpcg.symgs(h, dev(r), xd)
+    assert xd.cpu().numpy().tobytes() == ref.tobytes()
+
+
+def test_symgs_signed_zero_and_padding():
+    """Padding slots never touch the arithmetic: r = -0 rows with x = -1
+    neighbours keep their signed zeros exactly like the CSR walk."""
+    dims = (3, 3, 3)                      # corner rows have 7 entries, pad to 26
+    h = hpcg.MgHierarchy.build(*dims, nlevels=1, device=DEV)
+    assert h.levels[0].ell[0] == 26
+    m = O.stencil_partition(*dims).a_full
+    r = np.full(m.nrows, -0.0)
+    x = np.full(m.nrows, -0.0)
+    xd = dev(x)
+    O.symgs_colored(m, r, x, O.stencil_colors(*dims))
+    hpcg.symgs(h, dev(r), xd)
+    assert xd.cpu().numpy().tobytes() == x.tobytes()
+
+
+@pytest.mark.parametrize("use_graph", [True, False])
+def test_pcg_matches_oracle_and_beats_cg(use_graph):
     dims = (16, 16, 16)
     h = hpcg.MgHierarchy.build(*dims, device=DEV)
-    levels = O.mg_levels(*dims)
+    levels = O.mg_levels(*dims, fmt=O.DIA)
     b = O.stencil_partition(*dims).b
     ref = O.pcg_mg(levels, b, tol=1e-9, max_iters=50)
-    res = hpcg.pcg(h, dev(b), tol=1e-9, max_iters=50)
+    res = hpcg.pcg(h, dev(b), tol=1e-9, max_iters=50, use_graph=use_graph)
     assert res.converged and ref.converged
     assert res.iterations == ref.iterations
     rel = np.abs(res.residual_history - ref.history) / np.abs(ref.history)
@@ -69,3 +111,16 @@ def test_pcg_matches_oracle_and_beats_cg():
     assert np.abs(x - 1.0).max() < 1e-7          # xexact = ones
     plain = O.cg(O.stencil_partition(*dims).a_full, b, tol=1e-9)
     assert res.iterations < plain.iterations
+
+
+def test_pcg_max_iters_and_zero_rhs():
+    dims = (8, 8, 8)
+    h = hpcg.MgHierarchy.build(*dims, device=DEV)
+    levels = O.mg_levels(*dims, fmt=O.DIA)
+    b = O.stencil_partition(*dims).b
+    ref = O.pcg_mg(levels, b, tol=1e-30, max_iters=3)
+    res = hpcg.pcg(h, dev(b), tol=1e-30, max_iters=3)      # graph chunk of 4 overshoots
+    assert res.iterations == 3 and not res.converged and res.residual_history.size == 4
+    assert np.allclose(res.residual_history, ref.history, rtol=1e-8, atol=0)
+    z = hpcg.pcg(h, dev(np.zeros_like(b)))
+    assert z.converged and z.iterations == 0 and not z.x.data.abs().sum().item()

@@ -43,8 +43,8 @@ def test_symgs_fixed_point_and_levels():
     O.symgs_colored(m, b, x, O.stencil_colors(4, 4, 4))
     assert np.allclose(x, 1.0, rtol=0, atol=1e-14)
     lv = O.mg_levels(8, 8, 8)
-    assert [a.nrows for a, _, _ in lv] == [512, 64, 8, 1]
-    assert lv[-1][2] is None and all(f.size == a.nrows for (_, _, f), (a, _, _)
+    assert [a.nrows for a, _, _, _ in lv] == [512, 64, 8, 1]
+    assert lv[-1][2] is None and all(f.size == a.nrows for (_, _, f, _), (a, _, _, _)
                                      in zip(lv[:-1], lv[1:]))
 
 
@@ -55,3 +55,6 @@ def test_pcg_converges_faster_than_cg():
     plain = O.cg(p.a_full, p.b, tol=1e-9)
     assert res.converged and res.iterations < plain.iterations
     assert np.abs(res.x - 1.0).max() < 1e-7
+    dia = O.pcg_mg(O.mg_levels(*dims, fmt=O.DIA), p.b, tol=1e-9)
+    assert dia.iterations == res.iterations
+    assert np.allclose(dia.history, res.history, rtol=1e-10, atol=0)

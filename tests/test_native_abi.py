@@ -48,6 +48,7 @@ def test_struct_layouts_match_header():
     from paper_2209_06478_b200 import _native
     assert ctypes.sizeof(_native.DsMatrix) == 4 + 4 + 8 * 3 + 8 * 4 + 8 + 4 + 4 + 8 + 8 * 8
     assert ctypes.sizeof(_native.DsCgScalars) == 8 * 8 + 4 * 4 + 8 + 4 + 4
+    assert ctypes.sizeof(_native.DsPcgScalars) == 8 * 8 + 4 * 4
     assert _native.CG_SCALARS_BYTES % 8 == 0
 
 
