@@ -188,7 +188,7 @@ typedef struct ds_matrix {
   const int32_t* long_rows;  /* CSR: rows > 129 entries (ds_csr_analyze), or NULL */
   int64_t n_long;
   int32_t rows_sorted;       /* COO: row indices nondecreasing                  */
-  int32_t pad;
+  int32_t max_row_len;       /* CSR: longest row if known (ds_csr_analyze), else 0 */
   const int32_t* row_perm;   /* CSR: rows grouped by length bin (ds_csr_bins), or NULL */
   int64_t bins[8];           /* CSR: bin b = row_perm[bins[b] .. bins[b+1])     */
 } ds_matrix;

@@ -242,7 +242,9 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   if (l == 0) sh[w] = v;
   __syncthreads();
-  constexpr int NW = BLOCK / 32;
+  // warps actually present (kernels whose tile size sets blockDim may run
+  // with fewer than BLOCK threads); same tree when blockDim.x == BLOCK
+  const int NW = min(BLOCK, (int)blockDim.x) / 32;
   if (w == 0) {
     double t = (l < NW) ? sh[l] : 0.0;
     for (int o = 16; o > 0; o >>= 1) t = add(t, __shfl_xor_sync(0xffffffffu, t, o));

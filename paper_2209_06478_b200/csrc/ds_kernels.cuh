@@ -129,7 +129,8 @@ __device__ double reduce_partials(const double* partials, const unsigned* count,
 
 // launchers shared between translation units
 int launch_csr(int64_t nrows, int64_t nnz, const int* off, const int* col, const double* val,
-               const int* long_rows, int64_t n_long, const double* x, double* y, bool accum,
+               const int* long_rows, int64_t n_long, int max_len, const double* x, double* y,
+               bool accum,
                const DotOut* dot, cudaStream_t st);
 int launch_csr_binned(int64_t nrows, int64_t ncols, const int* off, const int* col,
                       const double* val, const int* perm, const int64_t* bins, const double* x,

@@ -389,257 +389,276 @@ __global__ void __launch_bounds__(kCsrBlock)
 }
 
 // ---------------------------------------------------------------------------
-// CSR v2: TMA-staged row tiles, warp-specialised.
+// CSR v3: persistent TMA pipeline, one thread per row (the DIA design).
 //
-// Persistent CTAs: warp 0 is the producer, warps 1..16 (64 lane-groups of 8)
-// consume.  Tiles are R=64 consecutive rows, tile t = blockIdx.x + k*G.
-// The producer warp prefetches the bounding row offsets of the next 16
-// tiles with one load per lane, then for each tile waits for its ring slot to
-// be released (empty[s] mbarrier, one arrive per consumer warp) and issues
-// cp.async.bulk copies of the tile's offsets, column indices and values
-// (16-byte aligned: the copies start at the aligned-down first entry and end
-// at the aligned-up last one, so no ragged loads are needed; a tile whose
-// rounded range would leave the arrays or overflow a stage is "fat" and its
-// rows are read from global memory).  Consumers wait on full[s], compute the
-// exact numpy pairwise leaf of their row from shared memory (x gathered from
-// L2), and release the slot.  Rows longer than kLongRow go to csr_long_rows.
-constexpr int kCsr2ConsumerWarps = 16;
-constexpr int kCsr2Threads = 32 * (kCsr2ConsumerWarps + 1);
-constexpr int kCsr2Rows = 2 * 32 * kCsr2ConsumerWarps / 8;   // 64 rows: one per group
-constexpr int kCsr2OffInts = kCsr2Rows + 4;                   // staged offsets (16-B multiple)
-
-struct Csr2Cfg {
-  int S;          // stages (<= 8)
-  int ecap;       // entry capacity per stage (multiple of 4)
-  int stage_bytes;
+// Regular matrices (every row <= 33 entries: the stencil) are HBM-bound only
+// if each SM keeps enough gathers in flight; the 8-lane-group kernels above
+// hold ~1.7K per SM.  Here the matrix stream is decoupled from the gathers:
+// thread 0 copies each tile's entry range [off[r0], off[r0+T]) -- column
+// indices and values, contiguous in CSR -- into a ring of S shared-memory
+// stages with two 1-D TMA bulk copies (mbarrier transaction counts, L2
+// evict_first so x stays L2-resident), and refills a stage as soon as the
+// CTA has consumed it.  Each thread then reads its row from shared memory
+// (a row stride of 27 words / doubles is bank-conflict free) and issues all
+// LMAX gathers unpredicated (clamped to the row's last entry) before any add,
+// so 256 x LMAX gathers per SM are in flight.
+//
+// Sum order (np.add.reduceat, kernels.py:117): y = p[0] + pw(p[1..m]), m =
+// len-1, pw(n < 8) = sequential from -0.0, pw(8 <= n <= 128) = 8 strided
+// accumulators combined ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) then the n%8
+// tail.  With every index static (register arrays) this is: r[j] = p[1+j]
+// (+ p[1+j+8q] while 8q < full), res = full ? combine(r) : -0.0, then
+// res += p[k] for full < k <= m ascending -- exactly the tail of either case.
+// Rows longer than LMAX (<= kLongRow) take the serial emulation; a tile whose
+// entries do not fit a stage ("fat") is read straight from global memory.
+struct CsrPipeCfg {
+  int T;            // rows per tile == blockDim.x
+  int S;            // stages (<= 8)
+  int cap;          // entries per stage (multiple of 4)
+  int stage_bytes;  // 4*cap (cols) + 8*cap (vals), 128-B multiple
 };
 
-struct Csr2Hdr {  // written by the producer before its arrive (release)
-  int e0, e1;     // tile entry range
-  int bc, bv;     // first staged col / val element (aligned down)
-  int fat;        // consumers read global memory for this tile
-  int offs_staged;
-  int pad0, pad1;
+struct CsrPipeHdr {  // per stage, written by thread 0 before its arrive (release)
+  int bc, bv;        // first staged col / val entry (aligned down to 16 B)
+  int fat;
+  int pad;
 };
 
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-__device__ __forceinline__ int* csr2_offs(unsigned char* st) {
-  return reinterpret_cast<int*>(st + 64);
-}
-__device__ __forceinline__ int* csr2_cols(unsigned char* st) {
-  return reinterpret_cast<int*>(st + 64 + 4 * kCsr2OffInts);
-}
-__device__ __forceinline__ double* csr2_vals(unsigned char* st, int ecap) {
-  return reinterpret_cast<double*>(st + 64 + 4 * kCsr2OffInts + 4 * (size_t)ecap);
-}
-
-// exact pairwise leaf from shared memory (m <= 128 addends after p[first])
-__device__ __forceinline__ double csr2_leaf_smem(const int* s_col, const double* s_val, int kc,
-                                                int kv, int m, const double* __restrict__ x,
-                                                int lane8, unsigned mask) {
-  const int full = m & ~7;
-  const int nfull = full >> 3;
-  const int rounds = (m + 7) >> 3;
-  double r = 0.0, tail = 0.0;
-  for (int k0 = 0; k0 < rounds; k0 += 4) {
-    double a[4];
-#pragma unroll
-    for (int kk = 0; kk < 4; ++kk) {
-      const int i = min(lane8 + 8 * (k0 + kk), m - 1);
-      a[kk] = mul(s_val[kv + i], ld_gather(x + s_col[kc + i]));
-    }
-#pragma unroll
-    for (int kk = 0; kk < 4; ++kk) {
-      const int k = k0 + kk;
-      if (k < nfull) r = (k == 0) ? a[kk] : add(r, a[kk]);
-      else if (k == nfull) tail = a[kk];
-    }
+__device__ __forceinline__ void csr_pipe_issue(const int* __restrict__ col,
+                                               const double* __restrict__ val, int nnz, int e0,
+                                               int e1, const CsrPipeCfg& cfg, unsigned char* st,
+                                               CsrPipeHdr* h, uint64_t* bar, uint64_t pol) {
+  const int bc = e0 & ~3, bv = e0 & ~1;
+  // copy up to the 16-B aligned end: the few entries past e1 belong to the
+  // next tile (never read here).  Only where that would leave the arrays
+  // (the last tile) is the sub-16-byte tail copied by hand -- a dependent
+  // global load on thread 0, so it is kept off every other tile.
+  const int cu = (e1 + 3) & ~3, vu = (e1 + 1) & ~1;
+  const bool fat = (cu - bc) > cfg.cap;
+  h->bc = bc;
+  h->bv = bv;
+  h->fat = fat;
+  uint32_t bytes = 0;
+  int* s_col = reinterpret_cast<int*>(st);
+  double* s_val = reinterpret_cast<double*>(st + 4 * (size_t)cfg.cap);
+  int cb = 0, vb = 0;
+  if (!fat) {
+    cb = cu <= nnz ? cu : (e1 & ~3);
+    vb = vu <= nnz ? vu : (e1 & ~1);
+    for (int e = cb; e < e1; ++e) s_col[e - bc] = col[e];
+    if (vb < e1) s_val[vb - bv] = val[vb];
+    bytes = 4u * (uint32_t)(cb - bc) + 8u * (uint32_t)(vb - bv);
   }
-  double res;
-  if (full > 0) {
-    r = add(r, __shfl_xor_sync(mask, r, 1, 8));
-    r = add(r, __shfl_xor_sync(mask, r, 2, 8));
-    r = add(r, __shfl_xor_sync(mask, r, 4, 8));
-    res = r;
-  } else {
-    res = -0.0;
+  fence_proxy_async();
+  mbar_arrive_expect_tx(bar, bytes);
+  if (!fat) {
+    if (cb > bc) bulk_g2s(s_col, col + bc, 4u * (uint32_t)(cb - bc), bar, pol);
+    if (vb > bv) bulk_g2s(s_val, val + bv, 8u * (uint32_t)(vb - bv), bar, pol);
   }
-  const int ntail = m - full;
-  for (int t = 0; t < ntail; ++t) res = add(res, __shfl_sync(mask, tail, t, 8));
-  return res;
 }
 
-template <bool ACCUM, bool FUSE_DOT>
-__global__ void __launch_bounds__(kCsr2Threads)
-    csr_tiles_tma(int nrows, int nnz, const int* __restrict__ off, const int* __restrict__ col,
-                  const double* __restrict__ val, const double* __restrict__ x, double* y,
-                  Csr2Cfg cfg, DotOut dot) {
+// One row with 1 <= len <= LMAX in two phases around the stage release:
+// load() copies the row's columns and values into registers and issues all
+// LMAX gathers (unpredicated, clamped to the row's last entry); finish()
+// forms the products and the exact np.add.reduceat sum.
+template <int LMAX>
+struct CsrRowRegs {
+  double v[LMAX];
+  double p[LMAX];
+
+  template <class IP, class VP>
+  __device__ __forceinline__ void load(IP cp, VP vp, int len, const double* __restrict__ x) {
+    const int last = len - 1;
+    int c[LMAX];
+#pragma unroll
+    for (int k = 0; k < LMAX; ++k) c[k] = cp[min(k, last)];
+#pragma unroll
+    for (int k = 0; k < LMAX; ++k) p[k] = ld_gather(x + c[k]);
+#pragma unroll
+    for (int k = 0; k < LMAX; ++k) v[k] = vp[min(k, last)];
+  }
+
+  __device__ __forceinline__ double finish(int len) {
+#pragma unroll
+    for (int k = 0; k < LMAX; ++k) p[k] = mul(v[k], p[k]);
+    const int m = len - 1, full = m & ~7;
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = (1 + j < LMAX) ? p[(1 + j) % LMAX] : 0.0;
+#pragma unroll
+    for (int q = 1; 1 + 8 * q < LMAX; ++q)
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (1 + j + 8 * q < LMAX && 8 * q < full) r[j] = add(r[j], p[(1 + j + 8 * q) % LMAX]);
+    double res = -0.0;
+    if (full > 0)
+      res = add(add(add(r[0], r[1]), add(r[2], r[3])), add(add(r[4], r[5]), add(r[6], r[7])));
+#pragma unroll
+    for (int k = 1; k < LMAX; ++k)
+      if (k > full && k <= m) res = add(res, p[k]);
+    return add(p[0], res);
+  }
+};
+
+template <class IP, class VP>
+__device__ __noinline__ double csr_row_serial(IP cp, VP vp, int len,
+                                              const double* __restrict__ x) {
+  const double p0 = mul(vp[0], ld_gather(x + cp[0]));
+  const double rest =
+      pairwise_serial(len - 1, [&](int64_t i) { return mul(vp[1 + i], ld_gather(x + cp[1 + i])); });
+  return add(p0, rest);
+}
+
+template <int LMAX, bool ACCUM, bool SKIP_LONG, bool FUSE_DOT>
+__global__ void __launch_bounds__(256, 1)
+    csr_pipe(int nrows, int nnz, const int* __restrict__ off, const int* __restrict__ col,
+             const double* __restrict__ val, const double* __restrict__ x, double* y,
+             CsrPipeCfg cfg, DotOut dot) {
   if (dot.skip()) return;
   extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem);        // S <= 8
-  uint64_t* empty = full + 8;
-  unsigned char* stage0 = smem + 128;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t ntiles = (nrows + kCsr2Rows - 1) / kCsr2Rows;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);                   // <= 8 barriers
+  CsrPipeHdr* hdr = reinterpret_cast<CsrPipeHdr*>(smem + 64);            // <= 8 headers
+  unsigned char* stage0 = smem + 256;
+  const int tid = threadIdx.x;
+  const int T = cfg.T, S = cfg.S;
+  const int64_t ntiles = (nrows + T - 1) / T;
   const int64_t G = gridDim.x;
-  const int S = cfg.S;
+  uint64_t pol = 0;
   if (tid == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kCsr2ConsumerWarps);
-    }
+    for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
     fence_barrier_init();
+    pol = policy_evict_first();
   }
   __syncthreads();
-  double dsum = 0.0;
-  if (warp == 0) {
-    // ------------------------------------------------------------ producer
-    const uint64_t pol = policy_evict_first();
-    for (int64_t k0 = 0; blockIdx.x + k0 * G < ntiles; k0 += 16) {
-      // lane j: bounding offset (j&1) of tile k0 + j/2
-      const int64_t tl = blockIdx.x + (k0 + (lane >> 1)) * G;
-      int bound = 0;
-      if (tl < ntiles) {
-        const int64_t r = min64(tl * kCsr2Rows + (lane & 1) * kCsr2Rows, nrows);
-        bound = off[r];
-      }
-      for (int j = 0; j < 16; ++j) {
-        const int64_t k = k0 + j;
-        const int64_t t = blockIdx.x + k * G;
-        const int e0 = __shfl_sync(0xffffffffu, bound, 2 * j);
-        const int e1 = __shfl_sync(0xffffffffu, bound, 2 * j + 1);
-        if (t >= ntiles) break;
-        const int s = (int)(k % S);
-        const uint32_t use = (uint32_t)(k / S);
-        if (use > 0) mbar_wait(&empty[s], (use - 1) & 1u);
-        if (lane == 0) {
-          unsigned char* st = stage0 + (size_t)s * cfg.stage_bytes;
-          Csr2Hdr* h = reinterpret_cast<Csr2Hdr*>(st);
-          const int r0 = (int)(t * kCsr2Rows);
-          const int bc = e0 & ~3, bv = e0 & ~1;
-          // aligned-up ends; copying past e1 reads the next tile's entries (in
-          // bounds unless the rounding leaves the arrays: then the tile is fat)
-          const int ec = (e1 + 3) & ~3, ev = (e1 + 1) & ~1;
-          const bool fat = ec > nnz || (ec - bc) > cfg.ecap || (ev - bv) > cfg.ecap;
-          const bool offs = (r0 + kCsr2OffInts <= nrows + 1);
-          h->e0 = e0;
-          h->e1 = e1;
-          h->bc = bc;
-          h->bv = bv;
-          h->fat = fat;
-          h->offs_staged = offs;
-          const uint32_t cbytes = fat ? 0u : 4u * (uint32_t)(ec - bc);
-          const uint32_t vbytes = fat ? 0u : 8u * (uint32_t)(ev - bv);
-          const uint32_t bytes = (offs ? 4u * kCsr2OffInts : 0u) + cbytes + vbytes;
-          mbar_arrive_expect_tx(&full[s], bytes);
-          if (offs) bulk_g2s(csr2_offs(st), off + r0, 4u * kCsr2OffInts, &full[s], pol);
-          if (cbytes) bulk_g2s(csr2_cols(st), col + bc, cbytes, &full[s], pol);
-          if (vbytes) bulk_g2s(csr2_vals(st, cfg.ecap), val + bv, vbytes, &full[s], pol);
-        }
-        __syncwarp();
+  if (tid == 0)
+    for (int s = 0; s < S; ++s) {
+      const int64_t t = blockIdx.x + s * G;
+      if (t < ntiles) {
+        const int64_t r0 = t * T;
+        const int e0 = __ldg(off + r0), e1 = __ldg(off + min64(r0 + T, nrows));
+        csr_pipe_issue(col, val, nnz, e0, e1, cfg, stage0 + (size_t)s * cfg.stage_bytes, &hdr[s],
+                       &full[s], pol);
       }
     }
-  } else {
-    // ------------------------------------------------------------ consumers
-    const int grp = (tid - 32) >> 3, lane8 = tid & 7;
-    const unsigned mask = 0xffu << (tid & 24);
-    int s = 0;
-    uint32_t ph = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += G) {
-      unsigned char* st = stage0 + (size_t)s * cfg.stage_bytes;
-      mbar_wait(&full[s], ph);
-      const Csr2Hdr h = *reinterpret_cast<const Csr2Hdr*>(st);
-      const int r0 = (int)(t * kCsr2Rows);
-      const int row = r0 + grp;
-      if (row < nrows) {
-        int start, end;
-        if (h.offs_staged) {
-          start = csr2_offs(st)[grp];
-          end = csr2_offs(st)[grp + 1];
-        } else {
-          start = __ldg(off + row);
-          end = __ldg(off + row + 1);
-        }
-        const int len = end - start;
-        if (len <= kLongRow) {
-          double res = 0.0, p0 = 0.0;
-          if (len > 0) {
-            if (h.fat) {
-              if (lane8 == 0)
-                p0 = mul(ld_stream(val + start), ld_gather(x + ld_stream(col + start)));
-              res = csr_leaf_g8(col, val, x, (int64_t)start + 1, len - 1, lane8, mask);
-            } else {
-              const int* s_col = csr2_cols(st);
-              const double* s_val = csr2_vals(st, cfg.ecap);
-              if (lane8 == 0) p0 = mul(s_val[start - h.bv], ld_gather(x + s_col[start - h.bc]));
-              res = csr2_leaf_smem(s_col, s_val, start + 1 - h.bc, start + 1 - h.bv, len - 1, x,
-                                   lane8, mask);
-            }
-          }
-          if (lane8 == 0) {
-            const double sres = (len > 0) ? add(p0, res) : 0.0;
-            double out = ACCUM ? add(y[row], sres) : sres;
-            if (dot.plus_zero) out = add(out, 0.0);
-            y[row] = out;
-            if (FUSE_DOT) dsum = add(dsum, mul(dot.other[row], out));
-          }
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-      if (++s == S) {
-        s = 0;
-        ph ^= 1u;
-      }
+  double dsum = 0.0;
+  int s = 0;
+  uint32_t ph = 0;
+  for (int64_t t = blockIdx.x; t < ntiles; t += G) {
+    const int64_t r0 = t * T;
+    const int rows = (int)min64(T, nrows - r0);
+    const int i = (int)r0 + tid;
+    // this row's bounds and (thread 0) the bounds of the tile issued after
+    // this one, loaded before the wait so their latency overlaps it
+    int o0 = 0, o1 = 0;
+    if (tid < rows) {
+      o0 = __ldg(off + i);
+      o1 = __ldg(off + i + 1);
+    }
+    const int64_t tn = t + (int64_t)S * G;
+    int n0 = 0, n1 = 0;
+    if (tid == 0 && tn < ntiles) {
+      n0 = __ldg(off + tn * T);
+      n1 = __ldg(off + min64(tn * T + T, nrows));
+    }
+    unsigned char* st = stage0 + (size_t)s * cfg.stage_bytes;
+    mbar_wait(&full[s], ph);
+    const int len = o1 - o0;
+    const CsrPipeHdr h = hdr[s];
+    const int* s_col = reinterpret_cast<const int*>(st) + (o0 - h.bc);
+    const double* s_val = reinterpret_cast<const double*>(st + 4 * (size_t)cfg.cap) + (o0 - h.bv);
+    CsrRowRegs<LMAX> R;
+    const bool fast = tid < rows && len >= 1 && len <= LMAX;
+    const bool emit = tid < rows && !(SKIP_LONG && len > kLongRow);  // else: long-row kernel
+    double sres = 0.0;
+    // phase 1: everything that reads the stage (rare serial rows entirely)
+    if (fast) {
+      if (!h.fat) R.load(s_col, s_val, len, x);
+      else R.load(col + o0, val + o0, len, x);
+    } else if (emit && len > LMAX) {
+      sres = h.fat ? csr_row_serial(col + o0, val + o0, len, x)
+                   : csr_row_serial(s_col, s_val, len, x);
+    }
+    __syncthreads();  // stage s consumed: refill it while the gathers land
+    if (tid == 0 && tn < ntiles)
+      csr_pipe_issue(col, val, nnz, n0, n1, cfg, st, &hdr[s], &full[s], pol);
+    // phase 2: products and the exact sum from registers
+    if (fast) sres = R.finish(len);
+    if (emit) {
+      double out = ACCUM ? add(y[i], sres) : sres;
+      if (dot.plus_zero) out = add(out, 0.0);
+      y[i] = out;
+      if (FUSE_DOT) dsum = add(dsum, mul(dot.other[i], out));
+    }
+    if (++s == S) {
+      s = 0;
+      ph ^= 1u;
     }
   }
-  if (FUSE_DOT) dot.finish_block<kCsr2Threads>(dsum);
+  if (FUSE_DOT) dot.finish_block<256>(dsum);
 }
 
-static int csr_tiles_launch(int64_t nrows, int64_t nnz, const int* off, const int* col,
-                            const double* val, const double* x, double* y, bool accum, DotOut d,
-                            bool fuse, cudaStream_t st) {
-  static int eS = -2, eE = -2, eC = -2;
-  if (eS == -2) {
-    const char* a = getenv("DS_CSR_S");
-    const char* b = getenv("DS_CSR_ECAP");
-    const char* c = getenv("DS_CSR_CTAS");
-    eS = a ? atoi(a) : -1;
-    eE = b ? atoi(b) : -1;
-    eC = c ? atoi(c) : -1;
-  }
-  Csr2Cfg cfg;
-  cfg.S = eS > 0 ? min(eS, 8) : 6;
-  cfg.ecap = eE > 0 ? (eE & ~3) : 2304;  // 36 entries per row on average + alignment slack
-  cfg.stage_bytes = (int)((64 + 4 * kCsr2OffInts + 12 * (int64_t)cfg.ecap + 127) & ~127);
-  const size_t smem = 128 + (size_t)cfg.S * cfg.stage_bytes;
-  const int64_t ntiles = ceil_div(nrows, kCsr2Rows);
-  int64_t grid = (int64_t)sm_count() * (eC > 0 ? eC : 1);
-  if (grid > ntiles) grid = ntiles;
-  if (fuse) grid = d.clamp_grid(grid);
-  const void* k;
-  if (accum)
-    k = fuse ? (const void*)csr_tiles_tma<true, true> : (const void*)csr_tiles_tma<true, false>;
-  else
-    k = fuse ? (const void*)csr_tiles_tma<false, true> : (const void*)csr_tiles_tma<false, false>;
-  int rc = allow_dynamic_smem(k, smem);
+template <int L, bool A, bool K, bool F>
+static int csr_pipe_launch1(int64_t nrows, int64_t nnz, const int* off, const int* col, const double* val,
+                            const double* x, double* y, DotOut d, CsrPipeCfg cfg, size_t smem,
+                            int64_t grid, cudaStream_t st) {
+  auto k = csr_pipe<L, A, K, F>;
+  int rc = allow_dynamic_smem(reinterpret_cast<const void*>(k), smem);
   if (rc) return rc;
-#define DS_CSR2(A, F)                                                                     \
-  csr_tiles_tma<A, F><<<(unsigned)grid, kCsr2Threads, smem, st>>>((int)nrows, (int)nnz, off, \
-                                                                  col, val, x, y, cfg, d)
-  if (accum) {
-    if (fuse) DS_CSR2(true, true); else DS_CSR2(true, false);
-  } else {
-    if (fuse) DS_CSR2(false, true); else DS_CSR2(false, false);
-  }
-#undef DS_CSR2
-  DS_LAUNCH_CHECK("csr_tiles_tma");
+  k<<<(unsigned)grid, cfg.T, smem, st>>>((int)nrows, (int)nnz, off, col, val, x, y, cfg, d);
+  DS_LAUNCH_CHECK("csr_pipe");
   return DS_OK;
 }
 
+// max_len: longest row if known (<= 27 selects the 27-wide register path),
+// else 0.  Returns DS_ERR_NOT_SUPPORTED (nothing launched) when the pipeline
+// cannot run (misaligned arrays, shared memory).
+static int csr_pipe_launch(int64_t nrows, int64_t nnz, const int* off, const int* col, const double* val,
+                           const double* x, double* y, bool accum, bool skip_long, int max_len,
+                           DotOut d, bool fuse, cudaStream_t st) {
+  static int eT = -2, eS = -2, eC = -2;
+  if (eT == -2) {
+    const char* a = getenv("DS_CSR_T");
+    const char* b = getenv("DS_CSR_S");
+    const char* c = getenv("DS_CSR_CTAS");
+    eT = a ? atoi(a) : -1;
+    eS = b ? atoi(b) : -1;
+    eC = c ? atoi(c) : -1;
+  }
+  const bool aligned = ((reinterpret_cast<uintptr_t>(col) | reinterpret_cast<uintptr_t>(val)) &
+                        15) == 0;
+  if (!aligned) return DS_ERR_NOT_SUPPORTED;
+  const int L = (max_len > 0 && max_len <= 27) ? 27 : 33;
+  CsrPipeCfg cfg;
+  // measured at 104^3 (tools/sweep_csr.sh): 128 rows x 2 stages x 2 CTAs/SM
+  // 59.9 us, 256 x 2 x 1 61.9 us, 192 x 2 x 1 70.1 us, 128 x 4 x 1 86.5 us
+  cfg.T = eT > 0 ? eT : 128;
+  cfg.S = eS > 0 ? min(eS, 8) : 2;
+  cfg.cap = ((cfg.T * (max_len > 0 ? min(max_len, L) : 27) + 8) + 3) & ~3;
+  cfg.stage_bytes = (int)((12 * (int64_t)cfg.cap + 127) & ~127);
+  const size_t smem = 256 + (size_t)cfg.S * cfg.stage_bytes;
+  if (cfg.T > 256 || cfg.T < 32 || smem > (size_t)max_dynamic_smem() - 1024)
+    return DS_ERR_NOT_SUPPORTED;
+  const int64_t ntiles = ceil_div(nrows, cfg.T);
+  int64_t grid = (int64_t)sm_count() * (eC > 0 ? eC : 2);
+  if (grid > ntiles) grid = ntiles;
+  if (fuse) grid = d.clamp_grid(grid);
+#define DS_CSRP(Lv, A, K, F) \
+  return csr_pipe_launch1<Lv, A, K, F>(nrows, nnz, off, col, val, x, y, d, cfg, smem, grid, st)
+#define DS_CSRP_L(A, K, F)          \
+  do {                              \
+    if (L == 27) DS_CSRP(27, A, K, F); \
+    DS_CSRP(33, A, K, F);           \
+  } while (0)
+  if (fuse) {
+    if (accum) DS_CSRP_L(true, false, true); else DS_CSRP_L(false, false, true);
+  } else if (skip_long) {
+    if (accum) DS_CSRP_L(true, true, false); else DS_CSRP_L(false, true, false);
+  } else {
+    if (accum) DS_CSRP_L(true, false, false); else DS_CSRP_L(false, false, false);
+  }
+#undef DS_CSRP_L
+#undef DS_CSRP
+}
 // One CTA per long row: the pairwise recursion tree is cut into subtrees of
 // at most kSub addends; each subtree's leaves (64..128 addends each) are
 // summed by the CTA's 32 lane-groups in parallel, then thread 0 replays the
@@ -848,6 +867,28 @@ __global__ void csr_find_long(int nrows, const int* __restrict__ off, int* long_
   }
 }
 
+// long-row kernels for the rows > kLongRow listed by ds_csr_analyze
+static int launch_csr_long(const int* long_rows, int64_t n_long, const int* off, const int* col,
+                           const double* val, const double* x, double* y, bool accum,
+                           const int* guard, cudaStream_t st) {
+  if (n_long <= 0) return DS_OK;
+  const int64_t lb = min64(n_long, (int64_t)sm_count() * 8);
+  const int64_t lw = min64(ceil_div(n_long, kCsrBlock / 32), (int64_t)sm_count() * 8);
+  if (accum) {
+    csr_long_rows_warp<true><<<(unsigned)lw, kCsrBlock, 0, st>>>(long_rows, (int)n_long, off, col,
+                                                                val, x, y, guard);
+    csr_long_rows<true><<<(unsigned)lb, kCsrBlock, 0, st>>>(long_rows, (int)n_long, off, col, val,
+                                                           x, y, guard);
+  } else {
+    csr_long_rows_warp<false><<<(unsigned)lw, kCsrBlock, 0, st>>>(long_rows, (int)n_long, off,
+                                                                 col, val, x, y, guard);
+    csr_long_rows<false><<<(unsigned)lb, kCsrBlock, 0, st>>>(long_rows, (int)n_long, off, col,
+                                                            val, x, y, guard);
+  }
+  DS_LAUNCH_CHECK("csr_long_rows");
+  return DS_OK;
+}
+
 int launch_csr_binned(int64_t nrows, int64_t ncols, const int* off, const int* col,
                       const double* val, const int* perm, const int64_t* bins, const double* x,
                       double* y, bool accum, const DotOut* dot, cudaStream_t st) {
@@ -886,36 +927,24 @@ int launch_csr_binned(int64_t nrows, int64_t ncols, const int* off, const int* c
 #undef DS_CSRB
   DS_LAUNCH_CHECK("csr_binned");
   if (n_long > 0) {
-    const int* long_rows = perm + bins[6];
-    int64_t lb = n_long < (int64_t)sm_count() * 8 ? n_long : (int64_t)sm_count() * 8;
-    const int64_t lw = min64(ceil_div(n_long, kCsrBlock / 32), (int64_t)sm_count() * 8);
-    if (accum) {
-      csr_long_rows_warp<true><<<(unsigned)lw, kCsrBlock, 0, st>>>(long_rows, (int)n_long, off,
-                                                                  col, val, x, y, d.guard);
-      csr_long_rows<true><<<(unsigned)lb, kCsrBlock, 0, st>>>(long_rows, (int)n_long, off, col,
-                                                             val, x, y, d.guard);
-    } else {
-      csr_long_rows_warp<false><<<(unsigned)lw, kCsrBlock, 0, st>>>(long_rows, (int)n_long, off,
-                                                                   col, val, x, y, d.guard);
-      csr_long_rows<false><<<(unsigned)lb, kCsrBlock, 0, st>>>(long_rows, (int)n_long, off, col,
-                                                              val, x, y, d.guard);
-    }
-    DS_LAUNCH_CHECK("csr_long_rows");
+    const int rc = launch_csr_long(perm + bins[6], n_long, off, col, val, x, y, accum, d.guard, st);
+    if (rc) return rc;
   }
   if (win) x_window_end(st);
   return DS_OK;
 }
 
 int launch_csr(int64_t nrows, int64_t nnz, const int* off, const int* col, const double* val,
-               const int* long_rows, int64_t n_long, const double* x, double* y, bool accum,
-               const DotOut* dot, cudaStream_t st) {
+               const int* long_rows, int64_t n_long, int max_len, const double* x, double* y,
+               bool accum, const DotOut* dot, cudaStream_t st) {
   if (nrows == 0) return DS_OK;
   const int64_t groups = (nrows + 1) / 2;   // one 8-lane group per row pair
   int64_t blocks = ceil_div(groups * 8, kCsrBlock);
-  static int eB = -2;
+  static int eB = -2, use_g8 = -1;
   if (eB == -2) {
     const char* e = getenv("DS_CSR_BLOCKS_PER_SM");
     eB = e ? atoi(e) : -1;
+    use_g8 = getenv("DS_CSR_G8") ? 1 : 0;
   }
   // 8 resident CTAs per SM (measured best: 84 us vs 97 us for a 16-wave grid)
   const int64_t cap = (int64_t)sm_count() * (eB > 0 ? eB : 8);
@@ -923,34 +952,18 @@ int launch_csr(int64_t nrows, int64_t nnz, const int* off, const int* col, const
   const bool skip = (long_rows != nullptr);
   DotOut d = dot ? *dot : DotOut{};
   const bool fuse = d.fused();
-  // the TMA-tiled variant is experimental (slower than the paired direct
-  // kernel on the 104^3 stencil, see profiles/r01/README.md): opt-in only
-  static int use_v1 = -1;
-  if (use_v1 < 0) use_v1 = getenv("DS_CSR_TILES") ? 0 : 1;
-  const bool aligned = ((reinterpret_cast<uintptr_t>(off) | reinterpret_cast<uintptr_t>(col) |
-                         reinterpret_cast<uintptr_t>(val)) & 15) == 0;
-  // the tiled kernel skips rows > kLongRow: it needs the long-row plan
-  // (long_rows != NULL, possibly empty) so those rows are computed elsewhere
-  if (!use_v1 && aligned && skip && !(fuse && n_long > 0)) {
-    int rc = csr_tiles_launch(nrows, nnz, off, col, val, x, y, accum, d, fuse, st);
-    if (rc) return rc;
-    if (skip && n_long > 0) {
-      int64_t lb = n_long < (int64_t)sm_count() * 8 ? n_long : (int64_t)sm_count() * 8;
-      const int64_t lw = min64(ceil_div(n_long, kCsrBlock / 32), (int64_t)sm_count() * 8);
-      if (accum) {
-        csr_long_rows_warp<true><<<(unsigned)lw, kCsrBlock, 0, st>>>(long_rows, (int)n_long,
-                                                                    off, col, val, x, y, d.guard);
-        csr_long_rows<true><<<(unsigned)lb, kCsrBlock, 0, st>>>(long_rows, (int)n_long, off, col,
-                                                               val, x, y, d.guard);
-      } else {
-        csr_long_rows_warp<false><<<(unsigned)lw, kCsrBlock, 0, st>>>(long_rows, (int)n_long,
-                                                                     off, col, val, x, y, d.guard);
-        csr_long_rows<false><<<(unsigned)lb, kCsrBlock, 0, st>>>(long_rows, (int)n_long, off,
-                                                                col, val, x, y, d.guard);
-      }
-      DS_LAUNCH_CHECK("csr_long_rows");
-    }
-    return DS_OK;
+  if (fuse && skip && n_long > 0) {
+    set_error("fused dot with long rows is not supported");
+    return DS_ERR_NOT_SUPPORTED;
+  }
+  // the TMA pipeline needs the long-row plan (long_rows != NULL, possibly
+  // empty): rows > kLongRow are then computed by the long-row kernels
+  if (!use_g8 && skip) {
+    const int rc = csr_pipe_launch(nrows, nnz, off, col, val, x, y, accum, n_long > 0, max_len, d,
+                                   fuse, st);
+    if (rc == DS_OK)
+      return launch_csr_long(long_rows, n_long, off, col, val, x, y, accum, d.guard, st);
+    if (rc != DS_ERR_NOT_SUPPORTED) return rc;
   }
   if (fuse) blocks = d.clamp_grid(blocks);
 #define DS_CSR(A, S, F) \
@@ -968,23 +981,8 @@ int launch_csr(int64_t nrows, int64_t nnz, const int* off, const int* col, const
   }
 #undef DS_CSR
   DS_LAUNCH_CHECK("csr_rows_g8");
-  if (skip && n_long > 0) {
-    int64_t lb = n_long < (int64_t)sm_count() * 8 ? n_long : (int64_t)sm_count() * 8;
-    const int64_t lw = min64(ceil_div(n_long, kCsrBlock / 32), (int64_t)sm_count() * 8);
-    if (accum) {
-      csr_long_rows_warp<true><<<(unsigned)lw, kCsrBlock, 0, st>>>(long_rows, (int)n_long, off,
-                                                                  col, val, x, y, d.guard);
-      csr_long_rows<true><<<(unsigned)lb, kCsrBlock, 0, st>>>(long_rows, (int)n_long, off, col,
-                                                             val, x, y, d.guard);
-    } else {
-      csr_long_rows_warp<false><<<(unsigned)lw, kCsrBlock, 0, st>>>(long_rows, (int)n_long, off,
-                                                                   col, val, x, y, d.guard);
-      csr_long_rows<false><<<(unsigned)lb, kCsrBlock, 0, st>>>(long_rows, (int)n_long, off, col,
-                                                              val, x, y, d.guard);
-    }
-    DS_LAUNCH_CHECK("csr_long_rows");
-  }
-  return DS_OK;
+  return skip ? launch_csr_long(long_rows, n_long, off, col, val, x, y, accum, d.guard, st)
+              : DS_OK;
 }
 
 // ===================================================================== DIA ==
@@ -1648,7 +1646,7 @@ extern "C" int ds_spmv_csr(int64_t nrows, int64_t ncols, int64_t nnz, const int3
     set_error("nrows out of range");
     return DS_ERR_NOT_SUPPORTED;
   }
-  return launch_csr(nrows, nnz, row_offsets, col_indices, values, long_rows, n_long, x, y,
+  return launch_csr(nrows, nnz, row_offsets, col_indices, values, long_rows, n_long, 0, x, y,
                     accumulate != 0, nullptr, as_stream(stream));
 }
 

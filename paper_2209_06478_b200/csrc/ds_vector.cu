@@ -792,7 +792,8 @@ extern "C" int ds_cg_spmv_dot(const ds_matrix* a, const double* x, double* y, in
         break;
       }
       const bool can_fuse = want_dot && (a->long_rows == nullptr || a->n_long == 0);
-      rc = launch_csr(a->nrows, a->nnz, a->idx0, a->idx1, a->values, a->long_rows, a->n_long, x, y, acc,
+      rc = launch_csr(a->nrows, a->nnz, a->idx0, a->idx1, a->values, a->long_rows, a->n_long,
+                      a->max_row_len, x, y, acc,
                       can_fuse ? &fused : &d, st);
       done_dot = can_fuse;
       break;

@@ -105,14 +105,14 @@ def csr_plan(m: CsrMatrix):
         return hit[1], hit[2]
     import torch
     D = _dev()
-    lr, nl = None, 0
+    lr, nl, ml = None, 0, 0
     if m.nrows > 0:
         buf = torch.empty(m.nrows, dtype=torch.int32, device=m.device)
         n_long, max_len = ctypes.c_int64(), ctypes.c_int32()
         with torch.cuda.device(m.device):
             _native.call("ds_csr_analyze", m.nrows, D.ptr(m.row_offsets), D.ptr(buf),
                          ctypes.byref(n_long), ctypes.byref(max_len), D.stream(m.device))
-        nl = int(n_long.value)
+        nl, ml = int(n_long.value), int(max_len.value)
         # keep a valid pointer even when empty: non-NULL tells the C side the
         # matrix was analysed (rows > 129 are then handled by their own kernel)
         lr = buf[:max(nl, 1)].clone()
@@ -126,6 +126,7 @@ def csr_plan(m: CsrMatrix):
                              D.stream(m.device))
             m._cache["bins"] = (k, perm, list(bins))
     m._cache["plan"] = (k, lr, nl)
+    m._cache["max_len"] = (k, ml)
     return lr, nl
 
 
@@ -168,6 +169,7 @@ def descriptor(m) -> _native.DsMatrix:
         d.idx0, d.idx1, d.values = D.ptr(m.row_offsets), D.ptr(m.col_indices), D.ptr(m.values)
         lr, nl = csr_plan(m)
         d.long_rows, d.n_long = (lr.data_ptr() if lr is not None else None), nl
+        d.max_row_len = m._cache["max_len"][1]
         b = csr_bins(m)
         if b is not None:
             d.row_perm = b[0].data_ptr()

@@ -1,0 +1,127 @@
+"""GPU parity of every branch of the CSR SpMV launcher (ds_spmv.cu) against
+the oracle's np.add.reduceat restatement (kernels.py:102-119): bitwise.
+
+Branches: the TMA pipeline's 27- and 33-wide register paths, its serial path
+(rows of 34..129 entries when the longest row is unknown), "fat" tiles that
+do not fit a stage (read from global memory), rows skipped for the long-row
+kernels (> 129 entries), accumulate (spmv_add), empty rows and matrices whose
+row count is not a multiple of the tile.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+import paper_2209_06478_b200 as ds  # noqa: E402
+from paper_2209_06478_b200 import _device, _native  # noqa: E402
+from paper_2209_06478_b200 import kernels as K_  # noqa: E402
+from oracle import dynsparse_oracle as O  # noqa: E402
+
+DEV = torch.device("cuda", 0)
+
+
+def random_csr(rng, nrows, ncols, lengths):
+    offs = np.zeros(nrows + 1, dtype=np.int64)
+    offs[1:] = np.cumsum(lengths)
+    cols = np.empty(offs[-1], dtype=np.int64)
+    for i in range(nrows):
+        L = int(lengths[i])
+        cols[offs[i]:offs[i + 1]] = np.sort(rng.choice(ncols, size=L, replace=False))
+    vals = rng.standard_normal(offs[-1])
+    # signed zeros and exact cancellations exercise the -0.0 identity
+    vals[rng.random(vals.size) < 0.02] = -0.0
+    return offs, cols, vals
+
+
+def oracle_y(offs, cols, vals, x, y0=None, accumulate=False):
+    n = offs.size - 1
+    m = O.csr(n, x.size, offs, cols, vals)
+    y = np.zeros(n) if y0 is None else y0.copy()
+    (O.spmv_add if accumulate else O.spmv)(m, x, y)
+    return y
+
+
+def run_abi(a, x, y0, accumulate, plan):
+    """ds_spmv_csr through the C ABI; plan=False passes no long-row plan."""
+    y = torch.from_numpy(y0.copy()).to(DEV)
+    xt = torch.from_numpy(x).to(DEV)
+    lr, nl = K_.csr_plan(a) if plan else (None, 0)
+    _native.call("ds_spmv_csr", a.nrows, a.ncols, a.nnz, a.row_offsets.data_ptr(),
+                 a.col_indices.data_ptr(), a.values.data_ptr(),
+                 lr.data_ptr() if lr is not None else None, nl,
+                 xt.data_ptr(), y.data_ptr(), int(accumulate), _device.stream(DEV))
+    torch.cuda.synchronize()
+    return y.cpu().numpy()
+
+
+def device_csr(offs, cols, vals, ncols):
+    return ds.CsrMatrix(offs.size - 1, ncols, offs, cols, vals, ds.MemorySpace.DEVICE, DEV)
+
+
+@pytest.mark.parametrize("maxlen", [1, 8, 9, 17, 27, 28, 33])
+def test_pipe_register_paths_bitwise(maxlen):
+    rng = np.random.default_rng(100 + maxlen)
+    n, nc = 5 * 256 + 37, 3000
+    lengths = rng.integers(0, maxlen + 1, n)
+    lengths[rng.integers(0, n, 5)] = maxlen
+    lengths[:3] = 0
+    offs, cols, vals = random_csr(rng, n, nc, lengths)
+    x = rng.standard_normal(nc)
+    a = device_csr(offs, cols, vals, nc)
+    for acc in (False, True):
+        y0 = rng.standard_normal(n)
+        want = oracle_y(offs, cols, vals, x, y0, acc)
+        # descriptor path (max_row_len known -> 27 / 33 register width)
+        y = ds.DenseVector(torch.from_numpy(y0.copy()).to(DEV))
+        (ds.spmv_add if acc else ds.spmv)(ds.SERIAL, a, ds.DenseVector(torch.from_numpy(x).to(DEV)), y)
+        assert y.data.cpu().numpy().tobytes() == want.tobytes(), (maxlen, acc)
+        # direct C ABI (max_row_len unknown -> 33 wide)
+        assert run_abi(a, x, y0, acc, True).tobytes() == want.tobytes(), (maxlen, acc)
+        # no plan: the paired 8-lane kernel
+        assert run_abi(a, x, y0, acc, False).tobytes() == want.tobytes(), (maxlen, acc)
+
+
+def test_pipe_serial_fat_and_long_rows():
+    """Rows of 34..129 (serial path), tiles over the stage capacity (fat:
+    global loads) and rows > 129 (skipped, computed by the long-row kernels)
+    through ds_spmv_csr with a plan."""
+    rng = np.random.default_rng(7)
+    n, nc = 4 * 256 + 5, 20000
+    lengths = rng.integers(20, 34, n)
+    lengths[300:560] = rng.integers(34, 130, 260)    # serial rows, fat tiles
+    lengths[700] = 1000                              # long rows (warp kernel)
+    lengths[701] = 9000                              # (CTA kernel)
+    offs, cols, vals = random_csr(rng, n, nc, lengths)
+    x = rng.standard_normal(nc)
+    a = device_csr(offs, cols, vals, nc)
+    for acc in (False, True):
+        y0 = rng.standard_normal(n)
+        want = oracle_y(offs, cols, vals, x, y0, acc)
+        assert run_abi(a, x, y0, acc, True).tobytes() == want.tobytes(), acc
+        assert run_abi(a, x, y0, acc, False).tobytes() == want.tobytes(), acc
+
+
+def test_pipe_stencil_and_cg_fused_dot():
+    """The 27-point stencil (max row 27) through the CG engine, whose CSR
+    SpMV fuses p.Ap: iterations and history equal the oracle's."""
+    spec = ds.GridSpec(24, 20, 16)
+    part = ds.generate_problem(spec).partitions[0]
+    A = ds.to_device(part.a_full, DEV)
+    assert K_.descriptor(A).max_row_len == 27
+    ref = O.stencil_partition(24, 20, 16)
+    x = np.random.default_rng(3).standard_normal(A.ncols)
+    y = ds.DenseVector.zeros(A.nrows, ds.MemorySpace.DEVICE, DEV)
+    ds.spmv(ds.SERIAL, A, ds.DenseVector(torch.from_numpy(x).to(DEV)), y)
+    want = np.zeros(A.nrows)
+    O.spmv(ref.a_full, x, want)
+    assert y.data.cpu().numpy().tobytes() == want.tobytes()
+    res = ds.cg(ds.SERIAL, A, ds.to_device(part.b, DEV), tol=1e-9, max_iters=500)
+    oref = O.cg(ref.a_full, ref.b, tol=1e-9, max_iters=500)
+    assert res.converged and abs(res.iterations - oref.iterations) <= 1
+    k = min(res.iterations, oref.iterations) + 1
+    h = np.asarray(res.residual_history[:k])
+    assert np.all(np.abs(h - oref.history[:k]) <= 1e-8 * oref.history[:k] + 64 * np.finfo(float).eps)

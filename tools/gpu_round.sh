@@ -1,0 +1,20 @@
+#!/bin/bash
+# One gpurun call: GPU tests, smoke, bench (both arms), the ncu launch list of
+# the bench command and full captures of the hot kernels into gpurun_out/.
+set -u
+OUT=${OUT:-gpurun_out}
+mkdir -p $OUT
+python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1
+timeout 1200 python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log
+timeout 600 python bench.py ${BENCH_ARGS:-} > $OUT/bench.json 2> $OUT/bench.err
+timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $OUT/bench_ref.json 2> $OUT/bench_ref.err
+if [ -z "${NO_NCU:-}" ]; then
+  timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+      --csv --log-file $OUT/launches.csv python bench.py --steps 5 --warmup 3 --no-cpu > $OUT/launches.log 2>&1
+  for k in ${KERNELS:-dia_pipe csr_rows_g8 coo_warp_segments cg_update_deferred_kernel cg_direction_deferred_kernel}; do
+    timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 \
+        -o $OUT/prof_$k -f python tools/profile_kernels.py > $OUT/prof_$k.log 2>&1
+  done
+fi
+ls -la $OUT
