@@ -82,6 +82,17 @@ int ds_spmv_coo(int64_t nrows, int64_t ncols, int64_t nnz, const int32_t* row_in
                 const int32_t* col_indices, const double* values, int rows_sorted,
                 const double* x, double* y, int accumulate, void* stream);
 
+/* Row-sorted COO with a known longest row (ds_coo_max_run): rows of at most
+ * 27 entries run on the TMA-pipelined thread-per-row kernel; max_row_len 0
+ * (unknown) or longer rows use the warp-segment kernel.  Same result bits
+ * as ds_spmv_coo with rows_sorted = 1 (np.bincount order).                 */
+int ds_spmv_coo_sorted(int64_t nrows, int64_t ncols, int64_t nnz, const int32_t* row_indices,
+                       const int32_t* col_indices, const double* values, int32_t max_row_len,
+                       const double* x, double* y, int accumulate, void* stream);
+
+/* Longest run of equal row indices of a row-sorted COO (host, synchronises). */
+int ds_coo_max_run(int64_t nnz, const int32_t* row_indices, int32_t* max_run, void* stream);
+
 /* flags bit0: rows nondecreasing; bit1: (row, col) strictly increasing
  * (already canonical).  Written to host memory (synchronises).              */
 int ds_coo_order_flags(int64_t nnz, const int32_t* row_indices, const int32_t* col_indices,
@@ -188,7 +199,7 @@ typedef struct ds_matrix {
   const int32_t* long_rows;  /* CSR: rows > 129 entries (ds_csr_analyze), or NULL */
   int64_t n_long;
   int32_t rows_sorted;       /* COO: row indices nondecreasing                  */
-  int32_t max_row_len;       /* CSR: longest row if known (ds_csr_analyze), else 0 */
+  int32_t max_row_len;       /* CSR / sorted COO: longest row if known, else 0  */
   const int32_t* row_perm;   /* CSR: rows grouped by length bin (ds_csr_bins), or NULL */
   int64_t bins[8];           /* CSR: bin b = row_perm[bins[b] .. bins[b+1])     */
 } ds_matrix;

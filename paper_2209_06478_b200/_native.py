@@ -87,6 +87,9 @@ _SIGNATURES = {
     "ds_spmv_coo": (c_int, [c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_int, c_vp, c_vp, c_int,
                             c_vp]),
     "ds_coo_order_flags": (c_int, [c_i64, c_vp, c_vp, P_i32, c_vp]),
+    "ds_coo_max_run": (c_int, [c_i64, c_vp, P_i32, c_vp]),
+    "ds_spmv_coo_sorted": (c_int, [c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp,
+                                   c_int, c_vp]),
     "ds_csr_bins": (c_int, [c_i64, c_vp, c_vp, P_i64, c_vp]),
     "ds_dot_workspace_bytes": (c_i64, []),
     "ds_dot": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),

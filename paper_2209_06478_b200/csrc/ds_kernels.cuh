@@ -138,7 +138,7 @@ int launch_csr_binned(int64_t nrows, int64_t ncols, const int* off, const int* c
 int launch_dia(int64_t nrows, int64_t ncols, int ndiags, const int* off, const double* val,
                const double* x, double* y, bool accum, const DotOut* dot, cudaStream_t st);
 int launch_coo(int64_t nrows, int64_t nnz, const int* rows, const int* cols, const double* vals,
-               bool sorted, const double* x, double* y, bool accum, const int* guard,
+               bool sorted, int max_len, const double* x, double* y, bool accum, const int* guard,
                cudaStream_t st, bool plus_zero = false);
 // stand-alone fused dot with the same epilogue (used when a SpMV kernel
 // cannot fuse it): result = a[0:n] . b[0:n]

@@ -1521,6 +1521,308 @@ __global__ void __launch_bounds__(32 * kCooWarps)
   }
 }
 
+// ---------------------------------------------------------------------------
+// COO v3: persistent TMA pipeline (row-sorted COO).
+//
+// CTA c owns the row-aligned entry range [s_c, s_{c+1}), s_c = first row
+// start at or after c*C, and the rows [R_c, R_{c+1}) (R_0 = 0, R_G = nrows:
+// absent rows are written as +0.0 by their owner).  It walks its range in
+// tiles of E entries; thread 0 streams each tile's row indices, column
+// indices and values into a ring of S stages with three 1-D TMA bulk copies.
+//   phase A: thread t takes entries t, t+T, ... (coalesced shared-memory
+//            reads, all gathers in flight), writes the products and row ids
+//            to a private work buffer -- then the stage is released and
+//            refilled while
+//   phase B: thread per row (binary search for the row's segment in the
+//            tile) sums sequentially in stored order from +0.0, exactly
+//            np.bincount (kernels.py:149); the tile's last row is carried
+//            into the next tile unless the CTA's range ends there.
+struct CooPipeCfg {
+  int E;            // entries per tile (multiple of T)
+  int S;            // stages (<= 8)
+  int stage_bytes;  // 16 * (E + 8), 128-B multiple
+  int dry;          // tuning only: stream the tiles, compute nothing
+};
+
+__device__ __forceinline__ void coo_pipe_issue(const int* __restrict__ rows,
+                                               const int* __restrict__ cols,
+                                               const double* __restrict__ vals, int64_t nnz,
+                                               int64_t a, int64_t b, int E, unsigned char* st,
+                                               uint64_t* bar, uint64_t pol) {
+  const int64_t ws = a & ~3ll;
+  int* s_r = reinterpret_cast<int*>(st);
+  int* s_c = s_r + (E + 8);
+  double* s_v = reinterpret_cast<double*>(st + 8 * (size_t)(E + 8));
+  int64_t ib, vb;  // bulk ends (ints, doubles)
+  if (((b + 3) & ~3ll) <= nnz) {
+    ib = (b + 3) & ~3ll;
+    vb = (b + 1) & ~1ll;
+  } else {  // the matrix's last tile: sub-16-byte tails by hand
+    ib = b & ~3ll;
+    vb = b & ~1ll;
+    for (int64_t e = ib; e < b; ++e) {
+      s_r[e - ws] = rows[e];
+      s_c[e - ws] = cols[e];
+    }
+    if (vb < b) s_v[vb - ws] = vals[vb];
+  }
+  const uint32_t ibytes = 4u * (uint32_t)(ib - ws), vbytes = 8u * (uint32_t)(vb - ws);
+  fence_proxy_async();
+  mbar_arrive_expect_tx(bar, 2 * ibytes + vbytes);
+  if (ibytes) {
+    bulk_g2s(s_r, rows + ws, ibytes, bar, pol);
+    bulk_g2s(s_c, cols + ws, ibytes, bar, pol);
+  }
+  if (vbytes) bulk_g2s(s_v, vals + ws, vbytes, bar, pol);
+}
+
+// first index in w[0, n) with w[i] >= r (w nondecreasing)
+__device__ __forceinline__ int lower_bound_smem(const int* w, int n, int r) {
+  int lo = 0, len = n;
+  while (len > 0) {
+    const int h = len >> 1;
+    if (w[lo + h] < r) {
+      lo += h + 1;
+      len -= h + 1;
+    } else {
+      len = h;
+    }
+  }
+  return lo;
+}
+
+// Thread per row (the CSR pipeline's structure: instruction-light, all
+// LMAX gathers of a row in flight).  The rows of a tile are [pend, rlast]
+// (rlast = the tile's last row, carried into the next tile unless the CTA's
+// range ends with this tile, then the range extends to R_{c+1}); thread t
+// takes rows pend + t + T*i.  A row's segment is found by binary search in
+// the staged row indices; its columns and values are copied to registers and
+// its gathers issued before the stage is released (last round only: the
+// round count is uniform across the CTA), the sequential sum follows.
+template <int LMAX>
+struct CooRowRegs {
+  int len;
+  double v[LMAX];
+  double g[LMAX];
+};
+
+template <bool ACCUM, int T, int LMAX, int MINB>
+__global__ void __launch_bounds__(T, MINB)
+    coo_pipe(int nrows, int64_t nnz, const int* __restrict__ rows, const int* __restrict__ cols,
+             const double* __restrict__ vals, const double* __restrict__ x, double* y,
+             CooPipeCfg cfg, const int* guard, int plus_zero) {
+  if (guard && *guard) return;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);          // <= 8 barriers
+  int64_t* s_bounds = reinterpret_cast<int64_t*>(smem + 64);   // s_c, s_{c+1}
+  int* s_R = reinterpret_cast<int*>(smem + 80);                // R_c, R_{c+1}
+  double* s_carry = reinterpret_cast<double*>(smem + 88);
+  const int E = cfg.E, S = cfg.S;
+  unsigned char* stage0 = smem + 128;
+  const int tid = threadIdx.x;
+  const int64_t G = gridDim.x;
+  const int64_t C = (nnz + G - 1) / G;
+  if (tid < 32) {
+    const int64_t s0 = coo_row_start_at_or_after_warp(rows, nnz, blockIdx.x * C);
+    const int64_t s1 = coo_row_start_at_or_after_warp(rows, nnz, (blockIdx.x + 1) * C);
+    if (tid == 0) {
+      s_bounds[0] = s0;
+      s_bounds[1] = s1;
+      s_R[0] = (s0 == 0) ? 0 : (s0 < nnz ? rows[s0] : nrows);
+      s_R[1] = (s1 < nnz) ? rows[s1] : nrows;
+      for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
+      fence_barrier_init();
+    }
+  }
+  __syncthreads();
+  const int64_t s0 = s_bounds[0], s1 = s_bounds[1];
+  const int Rend = s_R[1];
+  const int64_t ntiles = (s1 - s0 + E - 1) / E;
+  uint64_t pol = 0;
+  if (tid == 0) {
+    pol = policy_evict_first();
+    for (int s = 0; s < S && s < ntiles; ++s)
+      coo_pipe_issue(rows, cols, vals, nnz, s0 + (int64_t)s * E,
+                     min64(s0 + (int64_t)(s + 1) * E, s1), E, stage0 + (size_t)s * cfg.stage_bytes,
+                     &full[s], pol);
+  }
+  int pend = s_R[0];    // rows < pend are written
+  int carry_row = -1;   // == pend when a partial sum continues
+  double carry = 0.0;
+  int s = 0;
+  uint32_t ph = 0;
+  for (int64_t k = 0; k < ntiles; ++k) {
+    const int64_t a = s0 + k * E;
+    const int cnt = (int)(min64(a + E, s1) - a);
+    const int off = (int)(a - (a & ~3ll));
+    unsigned char* st = stage0 + (size_t)s * cfg.stage_bytes;
+    const int* s_r = reinterpret_cast<const int*>(st) + off;
+    const int* s_c = reinterpret_cast<const int*>(st) + (E + 8) + off;
+    const double* s_v = reinterpret_cast<const double*>(st + 8 * (size_t)(E + 8)) + off;
+    mbar_wait(&full[s], ph);
+    if (cfg.dry) {
+      __syncthreads();
+      if (tid == 0 && k + S < ntiles)
+        coo_pipe_issue(rows, cols, vals, nnz, s0 + (k + S) * E, min64(s0 + (k + S + 1) * E, s1),
+                       E, st, &full[s], pol);
+      if (++s == S) {
+        s = 0;
+        ph ^= 1u;
+      }
+      continue;
+    }
+    const bool last = (k == ntiles - 1);
+    const int rlast = s_r[cnt - 1];
+    const int hi = last ? Rend : rlast + 1;
+    const int rounds = (hi - pend + T - 1) / T;   // uniform across the CTA
+    for (int it = 0; it < rounds; ++it) {
+      const int r = pend + tid + T * it;
+      CooRowRegs<LMAX> R;
+      R.len = 0;
+      double acc = (r == carry_row) ? carry : 0.0;
+      bool fast = false;
+      if (r < hi) {
+        int q0, q1;
+        if (r > rlast) {   // absent rows after the CTA's last entry
+          q0 = q1 = cnt;
+        } else {
+          q0 = lower_bound_smem(s_r, cnt, r);
+          // end: bounded search over the next LMAX+1 entries, else the rest
+          const int lim = min(q0 + LMAX + 1, cnt);
+          q1 = q0 + lower_bound_smem(s_r + q0, lim - q0, r + 1);
+          if (q1 == lim && lim < cnt && s_r[lim] <= r)
+            q1 = lim + lower_bound_smem(s_r + lim, cnt - lim, r + 1);
+        }
+        const int len = q1 - q0;
+        if (len == 0) {
+          // absent row (or the carried row ending at the tile boundary): acc as is
+        } else if (len <= LMAX) {
+          fast = true;
+          R.len = len;
+          const int lst = max(len - 1, 0);
+          int c[LMAX];
+#pragma unroll
+          for (int j = 0; j < LMAX; ++j) c[j] = s_c[q0 + min(j, lst)];
+#pragma unroll
+          for (int j = 0; j < LMAX; ++j) R.g[j] = ld_gather(x + c[j]);
+#pragma unroll
+          for (int j = 0; j < LMAX; ++j) R.v[j] = s_v[q0 + min(j, lst)];
+        } else {   // long row: sequential from the stage now, 8 gathers in flight
+          for (int qb = q0; qb < q1; qb += 8) {
+            double gg[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) gg[j] = ld_gather(x + s_c[min(qb + j, q1 - 1)]);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (qb + j < q1) acc = add(acc, mul(s_v[qb + j], gg[j]));
+          }
+        }
+      }
+      if (it == rounds - 1) {
+        __syncthreads();  // stage consumed: refill it while the gathers land
+        if (tid == 0 && k + S < ntiles)
+          coo_pipe_issue(rows, cols, vals, nnz, s0 + (k + S) * E,
+                         min64(s0 + (k + S + 1) * E, s1), E, st, &full[s], pol);
+      }
+      if (r < hi) {
+        if (fast) {
+#pragma unroll
+          for (int j = 0; j < LMAX; ++j)
+            if (j < R.len) acc = add(acc, mul(R.v[j], R.g[j]));
+        }
+        if (!last && r == rlast) {
+          *s_carry = acc;
+        } else {
+          double o = ACCUM ? add(y[r], acc) : acc;
+          if (plus_zero) o = add(o, 0.0);
+          y[r] = o;
+        }
+      }
+    }
+    if (rounds == 0) {   // cannot happen (rlast >= pend), kept for the barrier count
+      __syncthreads();
+      if (tid == 0 && k + S < ntiles)
+        coo_pipe_issue(rows, cols, vals, nnz, s0 + (k + S) * E, min64(s0 + (k + S + 1) * E, s1),
+                       E, st, &full[s], pol);
+    }
+    __syncthreads();  // carry published
+    if (!last) {
+      carry_row = rlast;
+      carry = *s_carry;
+      pend = rlast;
+    }
+    if (++s == S) {
+      s = 0;
+      ph ^= 1u;
+    }
+  }
+  if (ntiles == 0)   // empty range (only when the matrix has no entries)
+    for (int r = pend + tid; r < Rend; r += T) y[r] = ACCUM ? add(y[r], 0.0) : 0.0;
+}
+
+template <bool A, int T, int MINB>
+static int coo_pipe_launch1(int64_t nrows, int64_t nnz, const int* rows, const int* cols,
+                            const double* vals, const double* x, double* y, const int* guard,
+                            bool plus_zero, int E, int S, int ctas, cudaStream_t st) {
+  CooPipeCfg cfg;
+  cfg.E = E;
+  cfg.S = S;
+  cfg.stage_bytes = (int)((16 * (int64_t)(cfg.E + 8) + 127) & ~127ll);
+  cfg.dry = getenv("DS_COO_DRY") ? 1 : 0;
+  const size_t smem = 128 + (size_t)cfg.S * cfg.stage_bytes;
+  if (smem > (size_t)max_dynamic_smem() - 1024) return DS_ERR_NOT_SUPPORTED;
+  int64_t grid = (int64_t)sm_count() * ctas;
+  const int64_t want = ceil_div(nnz, cfg.E);
+  if (grid > want) grid = want;
+  if (grid < 1) grid = 1;
+  auto k = coo_pipe<A, T, 27, MINB>;
+  int rc = allow_dynamic_smem(reinterpret_cast<const void*>(k), smem);
+  if (rc) return rc;
+  k<<<(unsigned)grid, T, smem, st>>>((int)nrows, nnz, rows, cols, vals, x, y, cfg, guard,
+                                     (int)plus_zero);
+  DS_LAUNCH_CHECK("coo_pipe");
+  return DS_OK;
+}
+
+// tile shapes (threads, entries per tile, stages, CTAs/SM); DS_COO_CFG picks one
+static int coo_pipe_launch(int64_t nrows, int64_t nnz, const int* rows, const int* cols,
+                           const double* vals, const double* x, double* y, bool accum,
+                           const int* guard, bool plus_zero, cudaStream_t st) {
+  static int eC = -2, eS = -2, eN = -2, eE = -2;
+  if (eC == -2) {
+    const char* a = getenv("DS_COO_CFG");
+    const char* b = getenv("DS_COO_S");
+    const char* c = getenv("DS_COO_CTAS");
+    const char* d = getenv("DS_COO_E");
+    eC = a ? atoi(a) : -1;
+    eS = b ? atoi(b) : -1;
+    eN = c ? atoi(c) : -1;
+    eE = d ? atoi(d) : -1;
+  }
+  if (((reinterpret_cast<uintptr_t>(rows) | reinterpret_cast<uintptr_t>(cols) |
+        reinterpret_cast<uintptr_t>(vals)) & 15) != 0 || nnz <= 0 || nnz >= (1ll << 31))
+    return DS_ERR_NOT_SUPPORTED;
+  const int cfgi = eC >= 0 ? eC : 0;
+#define DS_COOP(T, E, S, N)                                                                     \
+  return accum ? coo_pipe_launch1<true, T, N>(nrows, nnz, rows, cols, vals, x, y, guard, plus_zero, \
+                                           eE > 0 ? eE : E, eS > 0 ? eS : S, eN > 0 ? eN : N, st) \
+               : coo_pipe_launch1<false, T, N>(nrows, nnz, rows, cols, vals, x, y, guard,          \
+                                            plus_zero, eE > 0 ? eE : E, eS > 0 ? eS : S,        \
+                                            eN > 0 ? eN : N, st)
+  switch (cfgi) {
+    // measured at 104^3 (tools/sweep_coo.sh): 64 threads x 1024 entries x 2
+    // stages x 6 CTAs/SM 92.6 us; the register budget (~166 / thread at
+    // LMAX 27) caps residency, so the variants bound registers via MINB
+    case 0: DS_COOP(64, 1024, 2, 6);
+    case 1: DS_COOP(128, 2048, 2, 3);
+    case 2: DS_COOP(128, 1536, 2, 4);
+    case 3: DS_COOP(64, 1024, 2, 8);
+    case 4: DS_COOP(64, 768, 2, 8);
+    default: DS_COOP(96, 1536, 2, 5);
+  }
+#undef DS_COOP
+}
+
 __global__ void coo_atomic(int64_t nnz, const int* __restrict__ rows, const int* __restrict__ cols,
                            const double* __restrict__ vals, const double* __restrict__ x,
                            double* y, const int* guard) {
@@ -1544,11 +1846,21 @@ __global__ void axpy_inplace(int64_t n, double* y, const double* t, const int* g
 }
 
 int launch_coo(int64_t nrows, int64_t nnz, const int* rows, const int* cols, const double* vals,
-               bool sorted, const double* x, double* y, bool accum, const int* guard,
+               bool sorted, int max_len, const double* x, double* y, bool accum, const int* guard,
                cudaStream_t st, bool plus_zero) {
   if (nrows == 0) return DS_OK;
-  static int coo_v1 = -1;
-  if (coo_v1 < 0) coo_v1 = getenv("DS_COO_V1") ? 1 : 0;
+  static int coo_v1 = -1, coo_warp = -1;
+  if (coo_v1 < 0) {
+    coo_v1 = getenv("DS_COO_V1") ? 1 : 0;
+    coo_warp = getenv("DS_COO_WARP") ? 1 : 0;
+  }
+  // thread-per-row pipeline for row-sorted COO whose rows fit its 27-wide
+  // register path (the stencil); long rows (power-law) keep the warp kernel,
+  // whose parallel products leave only the inherent sequential add chain
+  if (sorted && !coo_v1 && !coo_warp && max_len >= 1 && max_len <= 27) {
+    const int rc = coo_pipe_launch(nrows, nnz, rows, cols, vals, x, y, accum, guard, plus_zero, st);
+    if (rc != DS_ERR_NOT_SUPPORTED) return rc;
+  }
   if (sorted && !coo_v1) {
     int64_t blocks = ceil_div(ceil_div(nnz, kCooWarpChunk), kCooWarps);
     const int64_t cap = (int64_t)sm_count() * 8;
@@ -1669,8 +1981,62 @@ extern "C" int ds_spmv_coo(int64_t nrows, int64_t ncols, int64_t nnz, const int3
     set_error("nrows out of range");
     return DS_ERR_NOT_SUPPORTED;
   }
-  return launch_coo(nrows, nnz, row_indices, col_indices, values, rows_sorted != 0, x, y,
+  return launch_coo(nrows, nnz, row_indices, col_indices, values, rows_sorted != 0, 0, x, y,
                     accumulate == 1, nullptr, as_stream(stream), accumulate == 2);
+}
+
+// Longest run of equal row indices (rows nondecreasing): each run head
+// gallops to the end of its run (O(log run) loads), atomicMax of the lengths.
+__global__ void coo_max_run_kernel(int64_t nnz, const int* __restrict__ rows, int* out) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int r = rows[k];
+    if (k > 0 && rows[k - 1] == r) continue;
+    int64_t lo = k, step = 1;   // rows[lo] == r
+    while (lo + step < nnz && rows[lo + step] == r) {
+      lo += step;
+      step <<= 1;
+    }
+    int64_t hi = min64(lo + step, nnz);   // rows[hi] != r or hi == nnz
+    while (hi - lo > 1) {
+      const int64_t mid = lo + (hi - lo) / 2;
+      if (rows[mid] == r) lo = mid; else hi = mid;
+    }
+    const int64_t len = lo - k + 1;
+    atomicMax(out, (int)min64(len, (int64_t)INT_MAX));
+  }
+}
+
+extern "C" int ds_coo_max_run(int64_t nnz, const int32_t* row_indices, int32_t* max_run,
+                              void* stream) {
+  cudaStream_t st = as_stream(stream);
+  *max_run = 0;
+  if (nnz <= 0) return DS_OK;
+  int* d = nullptr;
+  DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(int), st));
+  DS_CUDA(cudaMemsetAsync(d, 0, sizeof(int), st));
+  const unsigned g = (unsigned)min64(ceil_div(nnz, 256), (int64_t)sm_count() * 8);
+  coo_max_run_kernel<<<g, 256, 0, st>>>(nnz, row_indices, d);
+  DS_LAUNCH_CHECK("coo_max_run_kernel");
+  int h = 0;
+  DS_CUDA(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, st));
+  DS_CUDA(cudaFreeAsync(d, st));
+  DS_CUDA(cudaStreamSynchronize(st));
+  *max_run = h;
+  return DS_OK;
+}
+
+extern "C" int ds_spmv_coo_sorted(int64_t nrows, int64_t ncols, int64_t nnz,
+                                  const int32_t* row_indices, const int32_t* col_indices,
+                                  const double* values, int32_t max_row_len, const double* x,
+                                  double* y, int accumulate, void* stream) {
+  (void)ncols;
+  if (nrows < 0 || nrows >= (1ll << 31)) {
+    set_error("nrows out of range");
+    return DS_ERR_NOT_SUPPORTED;
+  }
+  return launch_coo(nrows, nnz, row_indices, col_indices, values, true, max_row_len, x, y,
+                    accumulate != 0, nullptr, as_stream(stream));
 }
 
 extern "C" int ds_coo_order_flags(int64_t nnz, const int32_t* row_indices,

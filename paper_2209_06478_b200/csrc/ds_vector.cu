@@ -807,7 +807,8 @@ extern "C" int ds_cg_spmv_dot(const ds_matrix* a, const double* x, double* y, in
       break;
     }
     case DS_FMT_COO:
-      rc = launch_coo(a->nrows, a->nnz, a->idx0, a->idx1, a->values, a->rows_sorted != 0, x, y,
+      rc = launch_coo(a->nrows, a->nnz, a->idx0, a->idx1, a->values, a->rows_sorted != 0,
+                      a->max_row_len, x, y,
                       acc, d.guard, st, d.plus_zero != 0);
       break;
     default:

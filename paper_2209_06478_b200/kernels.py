@@ -153,8 +153,24 @@ def coo_flags(m: CooMatrix) -> int:
         with torch.cuda.device(m.device):
             _native.call("ds_coo_order_flags", m.nnz, D.ptr(m.row_indices),
                          D.ptr(m.col_indices), ctypes.byref(flags), D.stream(m.device))
+    run = 0
+    if (int(flags.value) & 1) and m.nnz > 0:
+        # longest row of a row-sorted COO: picks the SpMV kernel (<= 27:
+        # thread-per-row pipeline, else warp segments)
+        mr = ctypes.c_int32(0)
+        with torch.cuda.device(m.device):
+            _native.call("ds_coo_max_run", m.nnz, D.ptr(m.row_indices), ctypes.byref(mr),
+                         D.stream(m.device))
+        run = int(mr.value)
     m._cache["flags"] = (k, int(flags.value))
+    m._cache["max_run"] = (k, run)
     return int(flags.value)
+
+
+def coo_max_run(m: CooMatrix) -> int:
+    """Longest run of equal row indices (0 unless rows are sorted)."""
+    coo_flags(m)
+    return m._cache["max_run"][1]
 
 
 def descriptor(m) -> _native.DsMatrix:
@@ -179,6 +195,7 @@ def descriptor(m) -> _native.DsMatrix:
         d.format, d.nnz = int(FormatId.COO), m.nnz
         d.idx0, d.idx1, d.values = D.ptr(m.row_indices), D.ptr(m.col_indices), D.ptr(m.values)
         d.rows_sorted = coo_flags(m) & 1
+        d.max_row_len = coo_max_run(m)
     elif isinstance(m, DiaMatrix):
         d.format, d.ndiags = int(FormatId.DIA), m.ndiags
         d.idx0, d.values = D.ptr(m.offsets), D.ptr(m.values)

@@ -1,0 +1,105 @@
+"""GPU parity of the row-sorted COO SpMV (ds_spmv.cu coo_pipe) against the
+oracle's np.bincount restatement (kernels.py:143-163): bitwise.
+
+Shapes that hit every branch of the pipeline: rows split across tiles and
+across CTA ranges (carries), rows of exactly 27 entries, one row longer than a whole CTA range, runs of
+absent rows (written as +0.0 by their owner), more rows than entries,
+duplicates and signed zeros, spmv_add, and sizes that are not multiples of
+the 16-byte bulk-copy granule (hand-copied tails).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import zlib
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+from paper_2209_06478_b200 import _device, _native  # noqa: E402
+from oracle import dynsparse_oracle as O  # noqa: E402
+
+DEV = torch.device("cuda", 0)
+
+
+def run(nrows, ncols, rows, cols, vals, x, y0, accumulate, planned=True):
+    """ds_spmv_coo_sorted with the longest row from ds_coo_max_run (the
+    pipeline when it is <= 27), or plain ds_spmv_coo (warp kernel)."""
+    t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(DEV)  # noqa: E731
+    r, c, v, xt = t(rows, np.int32), t(cols, np.int32), t(vals, np.float64), t(x, np.float64)
+    y = t(y0, np.float64)
+    st = _device.stream(DEV)
+    if planned:
+        mr = ctypes.c_int32(-1)
+        _native.call("ds_coo_max_run", rows.size, r.data_ptr(), ctypes.byref(mr), st)
+        lens = np.bincount(rows, minlength=nrows) if rows.size else np.zeros(1, np.int64)
+        assert mr.value == int(lens.max())
+        _native.call("ds_spmv_coo_sorted", nrows, ncols, rows.size, r.data_ptr(), c.data_ptr(),
+                     v.data_ptr(), mr.value, xt.data_ptr(), y.data_ptr(), int(accumulate), st)
+    else:
+        _native.call("ds_spmv_coo", nrows, ncols, rows.size, r.data_ptr(), c.data_ptr(),
+                     v.data_ptr(), 1, xt.data_ptr(), y.data_ptr(), int(accumulate), st)
+    torch.cuda.synchronize()
+    return y.cpu().numpy()
+
+
+def want(nrows, ncols, rows, cols, vals, x, y0, accumulate):
+    m = O.coo(nrows, ncols, rows.astype(np.int64), cols.astype(np.int64), vals)
+    y = y0.copy()
+    (O.spmv_add if accumulate else O.spmv)(m, x, y)
+    return y
+
+
+def sorted_coo(rng, nrows, ncols, lengths):
+    rows = np.repeat(np.arange(nrows, dtype=np.int64), lengths)
+    cols = rng.integers(0, ncols, rows.size)          # duplicates allowed, unordered cols
+    vals = rng.standard_normal(rows.size)
+    vals[rng.random(rows.size) < 0.02] = -0.0
+    return rows, cols, vals
+
+
+CASES = {
+    "stencil_like": lambda rng: (20000, 20000, rng.integers(20, 28, 20000)),
+    "ragged_with_gaps": lambda rng: (30011, 5000, np.where(rng.random(30011) < 0.3, 0,
+                                                              rng.integers(1, 40, 30011))),
+    "sparse_rows": lambda rng: (400_000, 1000, (rng.random(400_000) < 0.01).astype(np.int64) * 3),
+    "power_law": lambda rng: (50_000, 50_000, np.minimum(
+        50_000, np.floor(6.0 * (1 - rng.random(50_000)) ** (-1 / 1.8))).astype(np.int64)),
+    "tiny": lambda rng: (7, 5, np.array([0, 3, 1, 0, 0, 2, 1])),
+    "rows_up_to_27": lambda rng: (9000, 4000, rng.integers(0, 28, 9000)),
+}
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_coo_pipe_bitwise(name):
+    rng = np.random.default_rng(zlib.crc32(name.encode()))
+    nrows, ncols, lengths = CASES[name](rng)
+    rows, cols, vals = sorted_coo(rng, nrows, ncols, lengths)
+    x = rng.standard_normal(ncols)
+    for acc in (False, True):
+        y0 = rng.standard_normal(nrows)
+        y0[::7] = -0.0
+        ref = want(nrows, ncols, rows, cols, vals, x, y0, acc).tobytes()
+        for planned in (True, False):
+            got = run(nrows, ncols, rows, cols, vals, x, y0, acc, planned)
+            assert got.tobytes() == ref, (name, acc, planned)
+
+
+def test_coo_pipe_giant_row_and_odd_tail():
+    """One row spanning several CTA ranges, entries count % 4 != 0, leading
+    and trailing absent rows."""
+    rng = np.random.default_rng(11)
+    nrows, ncols = 1000, 3000
+    lengths = np.zeros(nrows, dtype=np.int64)
+    lengths[10] = 3
+    lengths[500] = 700_001
+    lengths[501:990] = rng.integers(0, 5, 489)
+    rows, cols, vals = sorted_coo(rng, nrows, ncols, lengths)
+    x = rng.standard_normal(ncols)
+    for acc in (False, True):
+        y0 = rng.standard_normal(nrows)
+        got = run(nrows, ncols, rows, cols, vals, x, y0, acc)
+        assert got.tobytes() == want(nrows, ncols, rows, cols, vals, x, y0, acc).tobytes(), acc
