@@ -51,6 +51,16 @@ def procs_for(n: int) -> tuple[int, int, int]:
     raise SystemExit(f"unsupported GPU count {n} (use 1, 2, 4 or 8)")
 
 
+def measured_traffic(kernel: str):
+    """DRAM bytes (read + write) per launch of `kernel` from the committed ncu
+    capture (profiles/r01/traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01", "traffic.json")) as fh:
+            return int(json.load(fh)[kernel]["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
 def peaks() -> dict:
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -449,7 +459,8 @@ def run(args, rank: int, world: int) -> int:
     k_ach = kb / (kern["avg_ms"] * 1e-3) / 1e9 if kern["avg_ms"] > 0 else 0.0
     roof = {"kernel": f"{plan[0]} SpMV of the CG step (fused p.Ap)", "bound": "hbm",
             "achieved": round(k_ach, 1), "peak": peak, "unit": "GB/s",
-            "frac": round(k_ach / peak, 3), "traffic": None, "peak_source": pk["source"],
+            "frac": round(k_ach / peak, 3), "traffic": measured_traffic("dia_pipe"),
+            "peak_source": pk["source"],
             "algorithmic_bytes_per_launch": kb, "avg_launch_ms": round(kern["avg_ms"], 5),
             "share_of_step": round(kern["avg_ms"] / kern["step_ms"], 3) if kern["step_ms"] else None}
 
