@@ -201,13 +201,15 @@ typedef struct ds_matrix {
   int32_t rows_sorted;       /* COO: row indices nondecreasing                  */
   int32_t max_row_len;       /* CSR / sorted COO: longest row if known, else 0  */
   const int32_t* row_perm;   /* CSR: rows grouped by length bin (ds_csr_bins), or NULL */
-  int64_t bins[8];           /* CSR: bin b = row_perm[bins[b] .. bins[b+1])     */
+  int64_t bins[9];           /* CSR: bin b = row_perm[bins[b] .. bins[b+1])     */
 } ds_matrix;
 
 /* Row-length bins for irregular CSR (rows stable-sorted by bin):
- *   0: empty, 1: 1-9, 2: 10-17, 3: 18-25, 4: 26-33, 5: 34-129, 6: > 129 entries.
- * Each bin runs with its exact number of load rounds.  perm holds nrows
- * int32; bins[0..7] are written to host memory (synchronises).            */
+ *   0: empty, 1: 1-9, 2: 10-17, 3: 18-25, 4: 26-33, 5: 34-129,
+ *   6: 130-1024 (warp per row), 7: > 1024 entries (CTA per row).
+ * Rows <= 33 run on the TMA pipeline (or, with a fused dot, bins 1-4 with
+ * their exact number of load rounds).  perm holds nrows int32; bins[0..8]
+ * are written to host memory (synchronises).                               */
 int ds_csr_bins(int64_t nrows, const int32_t* row_offsets, int32_t* perm, int64_t* bins,
                 void* stream);
 

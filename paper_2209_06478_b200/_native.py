@@ -47,7 +47,7 @@ class DsMatrix(ctypes.Structure):
         ("nrows", c_i64), ("ncols", c_i64), ("nnz", c_i64),
         ("idx0", c_vp), ("idx1", c_vp), ("values", c_vp), ("long_rows", c_vp),
         ("n_long", c_i64), ("rows_sorted", c_i32), ("max_row_len", c_i32),
-        ("row_perm", c_vp), ("bins", c_i64 * 8),
+        ("row_perm", c_vp), ("bins", c_i64 * 9),
     ]
 
 

@@ -61,15 +61,19 @@ __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, 
 __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
 
 // ---------------------------------------------------------------- loads -----
-// read-only streaming loads of the matrix: do not allocate in L1
+// read-only streaming loads of the matrix: do not allocate in L1.  Not
+// `volatile`: the data is immutable during a kernel, and a volatile asm pins
+// the load in program order -- ptxas then interleaves each load with the
+// gather and the arithmetic that consume it, serialising the memory round
+// trips that batched loads are meant to overlap.
 __device__ __forceinline__ double ld_stream(const double* p) {
   double v;
-  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
   return v;
 }
 __device__ __forceinline__ int ld_stream(const int* p) {
   int v;
-  asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  asm("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
 }
 // gathered vector entries: keep in L1/L2
@@ -92,12 +96,12 @@ __device__ __forceinline__ uint64_t policy_first() {
 }
 __device__ __forceinline__ int ld_hint(const int* p, uint64_t pol) {
   int v;
-  asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  asm("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
   return v;
 }
 __device__ __forceinline__ double ld_hint(const double* p, uint64_t pol) {
   double v;
-  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
   return v;
 }
 

@@ -526,7 +526,8 @@ __device__ __forceinline__ int csr_bin_of(int len) {
   if (len <= 25) return 3;
   if (len <= 33) return 4;
   if (len <= 129) return 5;
-  return 6;
+  if (len <= kCsrWarpRow) return 6;
+  return 7;
 }
 struct IsBin {
   const int* off;
@@ -542,12 +543,12 @@ __global__ void bin_scatter(int nrows, const int* __restrict__ off, int b, const
 extern "C" int ds_csr_bins(int64_t nrows, const int32_t* row_offsets, int32_t* perm, int64_t* bins,
                            void* stream) {
   cudaStream_t st = as_stream(stream);
-  for (int b = 0; b < 8; ++b) bins[b] = 0;
+  for (int b = 0; b <= kCsrBinCount; ++b) bins[b] = 0;
   if (nrows <= 0) return DS_OK;
   int* pos = nullptr;
   DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&pos), nrows * sizeof(int), st));
   int64_t base = 0;
-  for (int b = 0; b < 7; ++b) {   // stable: rows ascending inside every bin
+  for (int b = 0; b < kCsrBinCount; ++b) {   // stable: rows ascending inside every bin
     int64_t cnt = 0;
     int rc = exclusive_scan(nrows, IsBin{row_offsets, b}, pos, &cnt, st);
     if (rc) return rc;
@@ -558,7 +559,7 @@ extern "C" int ds_csr_bins(int64_t nrows, const int32_t* row_offsets, int32_t* p
     }
     base += cnt;
   }
-  bins[7] = base;
+  bins[kCsrBinCount] = base;
   DS_CUDA(cudaFreeAsync(pos, st));
   DS_CUDA(cudaStreamSynchronize(st));
   return DS_OK;

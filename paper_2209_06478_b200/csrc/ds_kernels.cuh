@@ -132,7 +132,7 @@ int launch_csr(int64_t nrows, int64_t nnz, const int* off, const int* col, const
                const int* long_rows, int64_t n_long, int max_len, const double* x, double* y,
                bool accum,
                const DotOut* dot, cudaStream_t st);
-int launch_csr_binned(int64_t nrows, int64_t ncols, const int* off, const int* col,
+int launch_csr_binned(int64_t nrows, int64_t ncols, int64_t nnz, const int* off, const int* col,
                       const double* val, const int* perm, const int64_t* bins, const double* x,
                       double* y, bool accum, const DotOut* dot, cudaStream_t st);
 int launch_dia(int64_t nrows, int64_t ncols, int ndiags, const int* off, const double* val,
@@ -144,5 +144,8 @@ int launch_coo(int64_t nrows, int64_t nnz, const int* rows, const int* cols, con
 // cannot fuse it): result = a[0:n] . b[0:n]
 int launch_dot(int64_t n, const double* a, const double* b, const DotOut& d, cudaStream_t st);
 constexpr int kMaxPartials = 1 << 16;
+// CSR long rows: 130..kCsrWarpRow entries -> warp per row, longer -> CTA per row
+constexpr int kCsrWarpRow = 1024;
+constexpr int kCsrBinCount = 8;   // ds_csr_bins: 8 bins, 9 offsets
 
 }  // namespace ds

@@ -148,6 +148,47 @@ __device__ __forceinline__ double short_leaf_finish(int len, int lane8, unsigned
   return add(L.v0, res);
 }
 
+// Leaf (m <= 128) for the long-row kernels, which are latency bound (a few
+// rows, each a chain of leaves): every lane issues ALL its column / value
+// loads, then all its gathers, before the first add -- one memory round trip
+// per leaf instead of one per batch of 4 rounds.
+__device__ __forceinline__ double csr_leaf_g8_all(const int* __restrict__ col,
+                                                  const double* __restrict__ val,
+                                                  const double* __restrict__ x, int64_t base,
+                                                  int m, int lane8, unsigned mask) {
+  const int full = m & ~7, nfull = full >> 3;
+  int c[16];
+  double v[16], a[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    const int i = min(lane8 + 8 * k, m - 1);
+    c[k] = ld_stream(col + base + i);
+    v[k] = ld_stream(val + base + i);
+  }
+#pragma unroll
+  for (int k = 0; k < 16; ++k) a[k] = mul(v[k], ld_gather(x + c[k]));
+  double r = a[0], tail = 0.0;
+#pragma unroll
+  for (int k = 1; k < 16; ++k) {
+    if (k < nfull) r = add(r, a[k]);
+  }
+#pragma unroll
+  for (int k = 0; k < 16; ++k)
+    if (k == nfull) tail = a[k];
+  double res;
+  if (full > 0) {
+    r = add(r, __shfl_xor_sync(mask, r, 1, 8));
+    r = add(r, __shfl_xor_sync(mask, r, 2, 8));
+    r = add(r, __shfl_xor_sync(mask, r, 4, 8));
+    res = r;
+  } else {
+    res = -0.0;
+  }
+  const int ntail = m - full;
+  for (int t = 0; t < ntail; ++t) res = add(res, __shfl_sync(mask, tail, t, 8));
+  return res;
+}
+
 // Recursion for m > 128 by one 8-lane group (no plan): group-uniform DFS.
 __device__ double csr_group_pairwise(const int* __restrict__ col, const double* __restrict__ val,
                                      const double* __restrict__ x, int64_t base, int64_t m,
@@ -209,7 +250,7 @@ __device__ __forceinline__ void csr_row_general(int row, int start, int len,
   if (len > 0) {
     if (lane8 == 0) p0 = mul(ld_stream(val + start), ld_gather(x + ld_stream(col + start)));
     if (len <= kLongRow)
-      res = csr_leaf_g8(col, val, x, (int64_t)start + 1, len - 1, lane8, mask);
+      res = csr_leaf_g8_all(col, val, x, (int64_t)start + 1, len - 1, lane8, mask);
     else
       res = csr_group_pairwise(col, val, x, (int64_t)start + 1, len - 1, lane8, mask);
   }
@@ -348,7 +389,7 @@ __device__ __forceinline__ void binned_rows(const int* rws, int nr, const int* _
 }
 
 template <bool ACCUM, bool FUSE_DOT>
-__global__ void __launch_bounds__(kCsrBlock)
+__global__ void __launch_bounds__(kCsrBlock, 2)
     csr_binned(const int* __restrict__ off, const int* __restrict__ col,
                const double* __restrict__ val, const double* __restrict__ x, double* y,
                const int* __restrict__ perm, CsrBins bi, DotOut dot) {
@@ -416,6 +457,8 @@ struct CsrPipeCfg {
   int S;            // stages (<= 8)
   int cap;          // entries per stage (multiple of 4)
   int stage_bytes;  // 4*cap (cols) + 8*cap (vals), 128-B multiple
+  int skip_above;   // SKIP_LONG: rows longer than this are left to other kernels
+  int hint;         // gather x with L2 evict_last (irregular matrices: x re-used at random)
 };
 
 struct CsrPipeHdr {  // per stage, written by thread 0 before its arrive (release)
@@ -466,14 +509,18 @@ struct CsrRowRegs {
   double v[LMAX];
   double p[LMAX];
 
-  template <class IP, class VP>
-  __device__ __forceinline__ void load(IP cp, VP vp, int len, const double* __restrict__ x) {
+  template <bool HINT, class IP, class VP>
+  __device__ __forceinline__ void load(IP cp, VP vp, int len, const double* __restrict__ x,
+                                       uint64_t pl) {
     const int last = len - 1;
     int c[LMAX];
 #pragma unroll
     for (int k = 0; k < LMAX; ++k) c[k] = cp[min(k, last)];
+    // irregular matrices (HINT): predicated gathers -- clamped duplicates of
+    // short rows would multiply the random L2 sector traffic that bounds them
 #pragma unroll
-    for (int k = 0; k < LMAX; ++k) p[k] = ld_gather(x + c[k]);
+    for (int k = 0; k < LMAX; ++k)
+      p[k] = HINT ? (k <= last ? ld_hint(x + c[k], pl) : 0.0) : ld_gather(x + c[k]);
 #pragma unroll
     for (int k = 0; k < LMAX; ++k) v[k] = vp[min(k, last)];
   }
@@ -524,6 +571,7 @@ __global__ void __launch_bounds__(256, 1)
   const int64_t ntiles = (nrows + T - 1) / T;
   const int64_t G = gridDim.x;
   uint64_t pol = 0;
+  const uint64_t pl = policy_evict_last();
   if (tid == 0) {
     for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
     fence_barrier_init();
@@ -568,12 +616,17 @@ __global__ void __launch_bounds__(256, 1)
     const double* s_val = reinterpret_cast<const double*>(st + 4 * (size_t)cfg.cap) + (o0 - h.bv);
     CsrRowRegs<LMAX> R;
     const bool fast = tid < rows && len >= 1 && len <= LMAX;
-    const bool emit = tid < rows && !(SKIP_LONG && len > kLongRow);  // else: long-row kernel
+    const bool emit = tid < rows && !(SKIP_LONG && len > cfg.skip_above);  // else: other kernels
     double sres = 0.0;
     // phase 1: everything that reads the stage (rare serial rows entirely)
     if (fast) {
-      if (!h.fat) R.load(s_col, s_val, len, x);
-      else R.load(col + o0, val + o0, len, x);
+      if (cfg.hint) {
+        if (!h.fat) R.template load<true>(s_col, s_val, len, x, pl);
+        else R.template load<true>(col + o0, val + o0, len, x, pl);
+      } else {
+        if (!h.fat) R.template load<false>(s_col, s_val, len, x, pl);
+        else R.template load<false>(col + o0, val + o0, len, x, pl);
+      }
     } else if (emit && len > LMAX) {
       sres = h.fat ? csr_row_serial(col + o0, val + o0, len, x)
                    : csr_row_serial(s_col, s_val, len, x);
@@ -614,7 +667,8 @@ static int csr_pipe_launch1(int64_t nrows, int64_t nnz, const int* off, const in
 // cannot run (misaligned arrays, shared memory).
 static int csr_pipe_launch(int64_t nrows, int64_t nnz, const int* off, const int* col, const double* val,
                            const double* x, double* y, bool accum, bool skip_long, int max_len,
-                           DotOut d, bool fuse, cudaStream_t st) {
+                           DotOut d, bool fuse, cudaStream_t st, int skip_above = kLongRow,
+                           bool hint = false) {
   static int eT = -2, eS = -2, eC = -2;
   if (eT == -2) {
     const char* a = getenv("DS_CSR_T");
@@ -635,6 +689,8 @@ static int csr_pipe_launch(int64_t nrows, int64_t nnz, const int* off, const int
   cfg.S = eS > 0 ? min(eS, 8) : 2;
   cfg.cap = ((cfg.T * (max_len > 0 ? min(max_len, L) : 27) + 8) + 3) & ~3;
   cfg.stage_bytes = (int)((12 * (int64_t)cfg.cap + 127) & ~127);
+  cfg.skip_above = skip_above;
+  cfg.hint = hint ? 1 : 0;
   const size_t smem = 256 + (size_t)cfg.S * cfg.stage_bytes;
   if (cfg.T > 256 || cfg.T < 32 || smem > (size_t)max_dynamic_smem() - 1024)
     return DS_ERR_NOT_SUPPORTED;
@@ -664,14 +720,15 @@ static int csr_pipe_launch(int64_t nrows, int64_t nnz, const int* off, const int
 // summed by the CTA's 32 lane-groups in parallel, then thread 0 replays the
 // recursion to combine them in numpy's order.
 
-// Warp per long row (kLongRow < len <= kSub): lane 0 enumerates the pairwise
+// Warp per long row (kLongRow < len <= kWarpRow): lane 0 enumerates the pairwise
 // recursion's leaves (64..128 addends each) into warp-private shared memory,
 // the warp's four 8-lane groups sum leaves in parallel, lane 0 replays the
 // recursion to combine them.  No block-wide barriers, 8 rows per CTA.
 constexpr int kWarpLeaves = 128;
+constexpr int kWarpRow = kCsrWarpRow;   // warp kernel: rows of kLongRow+1 .. kWarpRow entries
 
 template <bool ACCUM>
-__global__ void __launch_bounds__(kCsrBlock)
+__global__ void __launch_bounds__(kCsrBlock, 2)
     csr_long_rows_warp(const int* __restrict__ rows, int n, const int* __restrict__ off,
                        const int* __restrict__ col, const double* __restrict__ val,
                        const double* __restrict__ x, double* y, const int* guard) {
@@ -689,7 +746,7 @@ __global__ void __launch_bounds__(kCsrBlock)
     const int row = rows[li];
     const int start = off[row];
     const int m = off[row + 1] - start - 1;
-    if (m + 1 > kSub) continue;          // the CTA kernel owns it
+    if (m + 1 > kWarpRow) continue;      // the CTA kernel owns it
     int nl = 0;
     if (lane == 0) {                      // leaves left to right
       Frame st[32];
@@ -712,8 +769,8 @@ __global__ void __launch_bounds__(kCsrBlock)
     nl = __shfl_sync(0xffffffffu, nl, 0);
     __syncwarp();
     for (int l = grp; l < nl; l += 4) {
-      const double v = csr_leaf_g8(col, val, x, (int64_t)start + 1 + s_lo[w][l], s_n[w][l],
-                                   lane8, mask);
+      const double v = csr_leaf_g8_all(col, val, x, (int64_t)start + 1 + s_lo[w][l], s_n[w][l],
+                                       lane8, mask);
       if (lane8 == 0) s_v[w][l] = v;
     }
     __syncwarp();
@@ -747,7 +804,7 @@ __global__ void __launch_bounds__(kCsrBlock)
 }
 
 template <bool ACCUM>
-__global__ void __launch_bounds__(kCsrBlock)
+__global__ void __launch_bounds__(kCsrBlock, 2)
     csr_long_rows(const int* __restrict__ long_rows, int n_long, const int* __restrict__ off,
                   const int* __restrict__ col, const double* __restrict__ val,
                   const double* __restrict__ x, double* y, const int* guard) {
@@ -767,7 +824,7 @@ __global__ void __launch_bounds__(kCsrBlock)
     const int row = long_rows[li];
     const int64_t start = off[row];
     const int64_t m = (int64_t)off[row + 1] - start - 1;
-    if (m + 1 <= kSub) continue;   // csr_long_rows_warp owns it
+    if (m + 1 <= kWarpRow) continue;   // csr_long_rows_warp owns it
     const int64_t base = start + 1;
     // thread-0 top-level DFS state
     Frame st[48];
@@ -820,7 +877,7 @@ __global__ void __launch_bounds__(kCsrBlock)
       __syncthreads();
       if (!s_cmd) break;
       for (int l = grp; l < s_nleaves; l += kCsrBlock / 8) {
-        double v = csr_leaf_g8(col, val, x, base + s_leaf_lo[l], s_leaf_n[l], lane8, mask);
+        double v = csr_leaf_g8_all(col, val, x, base + s_leaf_lo[l], s_leaf_n[l], lane8, mask);
         if (lane8 == 0) s_leaf_v[l] = v;
       }
       __syncthreads();
@@ -868,41 +925,72 @@ __global__ void csr_find_long(int nrows, const int* __restrict__ off, int* long_
 }
 
 // long-row kernels for the rows > kLongRow listed by ds_csr_analyze
-static int launch_csr_long(const int* long_rows, int64_t n_long, const int* off, const int* col,
-                           const double* val, const double* x, double* y, bool accum,
-                           const int* guard, cudaStream_t st) {
-  if (n_long <= 0) return DS_OK;
-  const int64_t lb = min64(n_long, (int64_t)sm_count() * 8);
-  const int64_t lw = min64(ceil_div(n_long, kCsrBlock / 32), (int64_t)sm_count() * 8);
-  if (accum) {
-    csr_long_rows_warp<true><<<(unsigned)lw, kCsrBlock, 0, st>>>(long_rows, (int)n_long, off, col,
-                                                                val, x, y, guard);
-    csr_long_rows<true><<<(unsigned)lb, kCsrBlock, 0, st>>>(long_rows, (int)n_long, off, col, val,
-                                                           x, y, guard);
-  } else {
-    csr_long_rows_warp<false><<<(unsigned)lw, kCsrBlock, 0, st>>>(long_rows, (int)n_long, off,
-                                                                 col, val, x, y, guard);
-    csr_long_rows<false><<<(unsigned)lb, kCsrBlock, 0, st>>>(long_rows, (int)n_long, off, col,
-                                                            val, x, y, guard);
+// Each kernel skips the rows of the other one, so an unsorted list
+// (ds_csr_analyze) may be passed to both; the bins plan passes exact lists.
+static int launch_csr_long2(const int* warp_rows, int64_t n_warp, const int* cta_rows,
+                            int64_t n_cta, const int* off, const int* col, const double* val,
+                            const double* x, double* y, bool accum, const int* guard,
+                            cudaStream_t st) {
+  if (n_warp > 0) {
+    const int64_t lw = min64(ceil_div(n_warp, kCsrBlock / 32), (int64_t)sm_count() * 8);
+    if (accum)
+      csr_long_rows_warp<true><<<(unsigned)lw, kCsrBlock, 0, st>>>(warp_rows, (int)n_warp, off,
+                                                                  col, val, x, y, guard);
+    else
+      csr_long_rows_warp<false><<<(unsigned)lw, kCsrBlock, 0, st>>>(warp_rows, (int)n_warp, off,
+                                                                   col, val, x, y, guard);
+  }
+  if (n_cta > 0) {
+    const int64_t lb = min64(n_cta, (int64_t)sm_count() * 8);
+    if (accum)
+      csr_long_rows<true><<<(unsigned)lb, kCsrBlock, 0, st>>>(cta_rows, (int)n_cta, off, col, val,
+                                                             x, y, guard);
+    else
+      csr_long_rows<false><<<(unsigned)lb, kCsrBlock, 0, st>>>(cta_rows, (int)n_cta, off, col,
+                                                              val, x, y, guard);
   }
   DS_LAUNCH_CHECK("csr_long_rows");
   return DS_OK;
 }
 
-int launch_csr_binned(int64_t nrows, int64_t ncols, const int* off, const int* col,
+static int launch_csr_long(const int* long_rows, int64_t n_long, const int* off, const int* col,
+                           const double* val, const double* x, double* y, bool accum,
+                           const int* guard, cudaStream_t st) {
+  return launch_csr_long2(long_rows, n_long, long_rows, n_long, off, col, val, x, y, accum, guard,
+                          st);
+}
+
+int launch_csr_binned(int64_t nrows, int64_t ncols, int64_t nnz, const int* off, const int* col,
                       const double* val, const int* perm, const int64_t* bins, const double* x,
                       double* y, bool accum, const DotOut* dot, cudaStream_t st) {
   if (nrows == 0) return DS_OK;
   DotOut d = dot ? *dot : DotOut{};
   const bool fuse = d.fused();
-  const int64_t n_long = bins[7] - bins[6];
+  static int binned_only = -1;
+  if (binned_only < 0) binned_only = getenv("DS_CSR_BINNED_ONLY") ? 1 : 0;
+  // Irregular matrix: the TMA pipeline takes every row of <= 33 entries (the
+  // bulk of a power-law matrix), the binned kernel only bin 5 (34..129) and
+  // the long-row kernels bin 6; x gathers carry L2 evict_last.  (A fused dot
+  // needs one kernel to own every row: it keeps the all-binned path.)
+  if (!fuse && !binned_only && nnz > 0 && nnz < (1ll << 31)) {
+    const int rc = csr_pipe_launch(nrows, nnz, off, col, val, x, y, accum, true, 33, d, false, st,
+                                   33, true);
+    if (rc == DS_OK) {
+      int64_t rest[kCsrBinCount + 1];
+      for (int b = 0; b <= kCsrBinCount; ++b) rest[b] = b < 5 ? bins[5] : bins[b];
+      if (rest[kCsrBinCount] == rest[5]) return DS_OK;
+      return launch_csr_binned(nrows, ncols, 0, off, col, val, perm, rest, x, y, accum, dot, st);
+    }
+    if (rc != DS_ERR_NOT_SUPPORTED) return rc;
+  }
+  const int64_t n_long = bins[8] - bins[6];
   if (fuse && n_long > 0) {
     set_error("fused dot with long rows is not supported");
     return DS_ERR_NOT_SUPPORTED;
   }
   CsrBins bi;
   int64_t acc = 0;
-  for (int b = 0; b < 8; ++b) bi.start[b] = bins[b];
+  for (int b = 0; b < 8; ++b) bi.start[b] = bins[b];   // bins 0..5 (+ end of 5)
   for (int b = 0; b < 6; ++b) {
     bi.pair_off[b] = acc;
     acc += ceil_div(bins[b + 1] - bins[b], kBinRowsHost[b]);
@@ -927,7 +1015,8 @@ int launch_csr_binned(int64_t nrows, int64_t ncols, const int* off, const int* c
 #undef DS_CSRB
   DS_LAUNCH_CHECK("csr_binned");
   if (n_long > 0) {
-    const int rc = launch_csr_long(perm + bins[6], n_long, off, col, val, x, y, accum, d.guard, st);
+    const int rc = launch_csr_long2(perm + bins[6], bins[7] - bins[6], perm + bins[7],
+                                    bins[8] - bins[7], off, col, val, x, y, accum, d.guard, st);
     if (rc) return rc;
   }
   if (win) x_window_end(st);

@@ -120,7 +120,7 @@ def csr_plan(m: CsrMatrix):
         # by length once, each bin then runs with its exact load rounds
         if int(max_len.value) > 33:
             perm = torch.empty(m.nrows, dtype=torch.int32, device=m.device)
-            bins = (ctypes.c_int64 * 8)()
+            bins = (ctypes.c_int64 * 9)()
             with torch.cuda.device(m.device):
                 _native.call("ds_csr_bins", m.nrows, D.ptr(m.row_offsets), D.ptr(perm), bins,
                              D.stream(m.device))
@@ -131,7 +131,7 @@ def csr_plan(m: CsrMatrix):
 
 
 def csr_bins(m: CsrMatrix):
-    """(perm tensor, bins[8]) when the matrix was binned, else None."""
+    """(perm tensor, bins[9]) when the matrix was binned, else None."""
     csr_plan(m)
     hit = m._cache.get("bins")
     k = ("plan",) + _key(m.row_offsets)
@@ -189,7 +189,7 @@ def descriptor(m) -> _native.DsMatrix:
         b = csr_bins(m)
         if b is not None:
             d.row_perm = b[0].data_ptr()
-            for i in range(8):
+            for i in range(len(d.bins)):
                 d.bins[i] = b[1][i]
     elif isinstance(m, CooMatrix):
         d.format, d.nnz = int(FormatId.COO), m.nnz

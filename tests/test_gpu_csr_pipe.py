@@ -103,6 +103,12 @@ def test_pipe_serial_fat_and_long_rows():
         want = oracle_y(offs, cols, vals, x, y0, acc)
         assert run_abi(a, x, y0, acc, True).tobytes() == want.tobytes(), acc
         assert run_abi(a, x, y0, acc, False).tobytes() == want.tobytes(), acc
+        # descriptor path: longest row > 33 -> length bins; rows <= 33 on the
+        # pipeline, 34..129 on the binned kernel, > 129 on the long-row kernels
+        assert K_.csr_bins(a) is not None
+        y = ds.DenseVector(torch.from_numpy(y0.copy()).to(DEV))
+        (ds.spmv_add if acc else ds.spmv)(ds.SERIAL, a, ds.DenseVector(torch.from_numpy(x).to(DEV)), y)
+        assert y.data.cpu().numpy().tobytes() == want.tobytes(), ("binned", acc)
 
 
 def test_pipe_stencil_and_cg_fused_dot():
