@@ -18,6 +18,8 @@ if os.environ.get("POWERLAW"):
     rng = np.random.default_rng(2209)
     n = 4_194_304
     L = np.minimum(n, np.floor(6.0 * (1.0 - rng.random(n)) ** (-1 / 1.8))).astype(np.int64)
+    if os.environ.get("POWERLAW_CAP"):   # experiment: cap row lengths
+        L = np.minimum(L, int(os.environ["POWERLAW_CAP"]))
     rows = np.repeat(np.arange(n, dtype=np.int64), L)
     a_csr = ds.convert(ds.CooMatrix(n, n, rows, rng.integers(0, n, rows.size),
                                     rng.standard_normal(rows.size), ds.MemorySpace.DEVICE, dev),
