@@ -289,6 +289,13 @@ int ds_cg_update_deferred(int64_t n, double* x, double* r, const double* p, cons
                           ds_cg_scalars* s, void* workspace, void* stream);
 int ds_cg_direction_deferred(int64_t n, const double* r, double* p, ds_cg_scalars* s,
                              double* history, void* workspace, void* stream);
+/* Both in one launch: update, a grid-wide barrier (co-resident grid,
+ * cooperative launch when available), then every block reduces the r.r
+ * partials and applies the direction.  DS_ERR_NOT_SUPPORTED (nothing
+ * launched) for n < 2 or vectors not 16-byte aligned.                      */
+int ds_cg_update_direction_deferred(int64_t n, double* x, double* r, double* p,
+                                    const double* ap, ds_cg_scalars* s, double* history,
+                                    void* workspace, void* stream);
 /* The same two kernels for one partition per process: the prologue sums the
  * all-gathered partition dots pap_all[0..nparts) / rr_all[0..nparts)
  * sequentially in rank order (solver.py:140-141); the update's partition

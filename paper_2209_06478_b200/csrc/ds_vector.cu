@@ -536,6 +536,153 @@ __global__ void cg_finalize_kernel(int stage, ds_cg_scalars* s, double* history,
   cg_finalize(stage, s, history, parts, nparts);
 }
 
+
+// ---- fused update + direction (single partition, deferred) ----------------
+// One persistent launch per CG iteration tail: the update (x += alpha p,
+// r -= alpha Ap, block r.r partials), a grid-wide barrier, then every block
+// reduces the r.r partials in the same fixed order (history, convergence,
+// beta) and applies p = r + beta p -- r and p are re-read from L2, where the
+// update left them.  Saves the direction kernel's launch and its DRAM re-read
+// of r and p.  The grid is sized to be co-resident (occupancy query) and is
+// launched cooperatively when the driver accepts that, so the barrier cannot
+// deadlock.  Same arithmetic per element as the two kernels; the r.r tree
+// differs only through the grid size (any fixed tree is within the dot
+// tolerance, and it is fixed for a given device).
+__device__ __forceinline__ void grid_barrier(unsigned* count, unsigned* gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned g = *reinterpret_cast<volatile unsigned*>(gen);
+    __threadfence();
+    if (atomicAdd(count, 1u) == gridDim.x - 1) {
+      *count = 0u;
+      __threadfence();
+      atomicExch(gen, g + 1u);
+    } else {
+      while (*reinterpret_cast<volatile unsigned*>(gen) == g) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kVecBlock)
+    cg_update_direction_fused_kernel(int64_t n, double* x, double* r, double* p,
+                                     const double* __restrict__ ap, ds_cg_scalars* s,
+                                     double* history, const double* pap_parts,
+                                     const unsigned* pap_count, double* rr_parts,
+                                     unsigned* bar_count, unsigned* bar_gen) {
+  __shared__ double sh[32];
+  if (s->done) return;
+  const double pap = reduce_partials<kVecBlock>(pap_parts, pap_count, sh);
+  if (pap <= 0.0) {  // breakdown: every block sees the same pap
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      s->pap = pap;
+      s->done = 2;
+    }
+    return;
+  }
+  const double rr = s->rr;
+  const double alpha = rr / pap, nalpha = -alpha;
+  const int it = s->iter + 1;
+  const int64_t gtid = (int64_t)blockIdx.x * kVecBlock + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * kVecBlock;
+  const int64_t n2 = n >> 1;
+  double2* x2 = reinterpret_cast<double2*>(x);
+  double2* r2 = reinterpret_cast<double2*>(r);
+  double2* p2 = reinterpret_cast<double2*>(p);
+  const double2* a2 = reinterpret_cast<const double2*>(ap);
+  double v = 0.0;
+  for (int64_t i0 = gtid; i0 < n2; i0 += stride * kVecUnroll) {
+    double2 xv[kVecUnroll], rv[kVecUnroll], pv[kVecUnroll], av[kVecUnroll];
+#pragma unroll
+    for (int u = 0; u < kVecUnroll; ++u) {
+      const int64_t i = min64(i0 + u * stride, n2 - 1);
+      xv[u] = x2[i];
+      rv[u] = r2[i];
+      pv[u] = p2[i];
+      av[u] = a2[i];
+    }
+#pragma unroll
+    for (int u = 0; u < kVecUnroll; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i < n2) {
+        double2 xo, ro;
+        xo.x = add(mul(1.0, xv[u].x), mul(alpha, pv[u].x));
+        xo.y = add(mul(1.0, xv[u].y), mul(alpha, pv[u].y));
+        ro.x = add(mul(1.0, rv[u].x), mul(nalpha, av[u].x));
+        ro.y = add(mul(1.0, rv[u].y), mul(nalpha, av[u].y));
+        x2[i] = xo;
+        r2[i] = ro;
+        v = add(v, mul(ro.x, ro.x));
+        v = add(v, mul(ro.y, ro.y));
+      }
+    }
+  }
+  if ((n & 1) && gtid == 0) {
+    const int64_t i = n - 1;
+    x[i] = add(mul(1.0, x[i]), mul(alpha, p[i]));
+    const double ri = add(mul(1.0, r[i]), mul(nalpha, ap[i]));
+    r[i] = ri;
+    v = add(v, mul(ri, ri));
+  }
+  v = block_sum<kVecBlock>(v, sh);
+  if (threadIdx.x == 0) rr_parts[blockIdx.x] = v;
+  grid_barrier(bar_count, bar_gen);
+  // direction: every block reduces the G partials in the same order
+  double t = 0.0;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += kVecBlock) t = add(t, __ldcg(rr_parts + i));
+  t = block_sum<kVecBlock>(t, sh);
+  __shared__ double s_rr;
+  if (threadIdx.x == 0) s_rr = t;
+  __syncthreads();
+  const double rr_new = s_rr;
+  const double h = sqrt(rr_new) / s->scale;
+  const bool converged = h <= s->tol;
+  const bool last = it >= s->max_iters;
+  const double beta = rr_new / rr;
+  // every block has read s->rr / s->iter above; block 0 publishes after the
+  // barrier, so no block can observe a half-updated scalar block
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    s->pap = pap;
+    s->alpha = alpha;
+    s->rr_used = rr;
+    s->iter_next = it;
+    history[it] = h;
+    s->iter = it;
+    s->rr_new = rr_new;
+    if (converged) s->done = 1;
+    else if (last) s->done = 3;
+    else {
+      s->beta = beta;
+      s->rr = rr_new;
+    }
+  }
+  if (converged || last) return;
+  for (int64_t i0 = gtid; i0 < n2; i0 += stride * kVecUnroll) {
+    double2 rv[kVecUnroll], pv[kVecUnroll];
+#pragma unroll
+    for (int u = 0; u < kVecUnroll; ++u) {
+      const int64_t i = min64(i0 + u * stride, n2 - 1);
+      rv[u] = __ldcg(r2 + i);
+      pv[u] = p2[i];
+    }
+#pragma unroll
+    for (int u = 0; u < kVecUnroll; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i < n2) {
+        double2 po;
+        po.x = add(mul(1.0, rv[u].x), mul(beta, pv[u].x));
+        po.y = add(mul(1.0, rv[u].y), mul(beta, pv[u].y));
+        p2[i] = po;
+      }
+    }
+  }
+  if ((n & 1) && gtid == 0) {
+    const int64_t i = n - 1;
+    p[i] = add(mul(1.0, __ldcg(r + i)), mul(beta, p[i]));
+  }
+}
+
 }  // namespace ds
 
 // ============================================================== C ABI ======
@@ -883,6 +1030,48 @@ extern "C" int ds_cg_direction(int64_t n, const double* r, double* p, const ds_c
   else
     cg_direction_kernel<false><<<g, kVecBlock, 0, as_stream(stream)>>>(n, r, p, s);
   DS_LAUNCH_CHECK("cg_direction_kernel");
+  return DS_OK;
+}
+
+// Fused update + direction (single partition, deferred): see
+// cg_update_direction_fused_kernel.  Returns DS_ERR_NOT_SUPPORTED (nothing
+// launched) for misaligned vectors or n < 2: use the two kernels then.
+extern "C" int ds_cg_update_direction_deferred(int64_t n, double* x, double* r, double* p,
+                                               const double* ap, ds_cg_scalars* s,
+                                               double* history, void* workspace, void* stream) {
+  if (n < 2 || !aligned16(x, r, p, ap)) return DS_ERR_NOT_SUPPORTED;
+  Workspace w0(reinterpret_cast<char*>(workspace));
+  Workspace w1(reinterpret_cast<char*>(workspace) + kWorkspaceBytes);
+  static int per_sm = -1;
+  if (per_sm < 0) {
+    int b = 0;
+    DS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &b, cg_update_direction_fused_kernel, kVecBlock, 0));
+    per_sm = b > 0 ? b : 1;
+  }
+  int64_t g = vec_grid(n);
+  const int64_t cap = (int64_t)sm_count() * per_sm;   // co-resident: the barrier needs it
+  if (g > cap) g = cap;
+  cudaStream_t st = as_stream(stream);
+  const double* pap_parts = w0.partials;
+  const unsigned* pap_count = w0.ticket + 2;
+  double* rr_parts = w1.partials;
+  unsigned* bar_count = w1.ticket + 1;
+  unsigned* bar_gen = w1.ticket + 3;
+  void* args[] = {&n, &x, &r, &p, const_cast<double**>(&ap), &s, &history,
+                  const_cast<double**>(&pap_parts), const_cast<unsigned**>(&pap_count),
+                  &rr_parts, &bar_count, &bar_gen};
+  cudaError_t e = cudaLaunchCooperativeKernel(
+      reinterpret_cast<const void*>(cg_update_direction_fused_kernel), dim3((unsigned)g),
+      dim3(kVecBlock), args, 0, st);
+  if (e != cudaSuccess) {
+    // not capturable / not supported here: the grid is co-resident by
+    // construction, so a plain launch keeps the barrier safe
+    (void)cudaGetLastError();
+    cg_update_direction_fused_kernel<<<(unsigned)g, kVecBlock, 0, st>>>(
+        n, x, r, p, ap, s, history, pap_parts, pap_count, rr_parts, bar_count, bar_gen);
+  }
+  DS_LAUNCH_CHECK("cg_update_direction_fused_kernel");
   return DS_OK;
 }
 

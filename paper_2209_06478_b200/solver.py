@@ -201,6 +201,13 @@ class CgEngine:
                                     DEFERRED, s, hist, None, 0, ws, stream))
         if marks is not None:
             marks[2].record(marks[0])
+        if not os.environ.get("DS_CG_UNFUSED"):
+            rc = lib.ds_cg_update_direction_deferred(pt.n, self._p(pt.x), self._p(pt.r),
+                                                     self._p(pt.p), self._p(pt.ap), s, hist, ws,
+                                                     stream)
+            if rc != _native.DS_ERR_NOT_SUPPORTED:
+                self._ck(rc)
+                return
         self._ck(lib.ds_cg_update_deferred(pt.n, self._p(pt.x), self._p(pt.r), self._p(pt.p),
                                            self._p(pt.ap), s, ws, stream))
         self._ck(lib.ds_cg_direction_deferred(pt.n, self._p(pt.r), self._p(pt.p), s, hist, ws,
