@@ -249,6 +249,67 @@ def sweep_powerlaw(ds, torch, dev, peak):
     return out
 
 
+def format_switching(ds, torch, dev, peak, nx: int = 192, steps: int = 100) -> dict:
+    """BASELINE config 5 on this GPU: a 192^3 local grid, the per-GPU tuner
+    ('multi': every (local, remote) combination converted in place -- the
+    runtime switching cost -- and timed), the chosen plan applied, then
+    ``steps`` graph-replayed CG iterations.  Reports the conversion cost in
+    SpMV-equivalents and the CG rate with and without it."""
+    from paper_2209_06478_b200 import dist as D
+    from paper_2209_06478_b200 import solver as S
+    spec = ds.GridSpec(nx, nx, nx)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    part = ds.generate_partition(spec, 0, space=ds.MemorySpace.DEVICE, device=dev)
+    split = ds.split_local_remote(ds.PartitionedProblem(spec, [part]), 0)
+    torch.cuda.synchronize()
+    gen_s = time.perf_counter() - t0
+    prof = D.profile_rank(part, split, reps=5)
+    lf, rf = D.select_rank_plan(prof["entries"], "multi", 1)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ds.convert_inplace(split.local, lf)
+    ds.convert_inplace(split.remote, rf)
+    torch.cuda.synchronize()
+    conv_ms = (time.perf_counter() - t0) * 1e3
+    n, nnz = part.a_full.nrows, part.a_full.nnz
+    eng, _ = S.build_engine(S.DistributedOperator(ds.PartitionedProblem(spec, [part]), [split]),
+                            [part.b], None, 1e-300, steps + 16)
+    st = torch.cuda.current_stream(dev)
+    with torch.cuda.device(dev):
+        eng.setup(st.cuda_stream)
+        eng.capture_step()
+        for _ in range(3):
+            eng.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(steps):
+            eng.replay()
+        e1.record(st)
+        torch.cuda.synchronize()
+    step_ms = e0.elapsed_time(e1) / steps
+    fl = flops_per_iter(nnz, n)
+    spmv_ms = prof["entries"][(lf, rf)] * 1e3
+    out = {
+        "grid": [nx, nx, nx], "n": n, "nnz": nnz, "generate_on_device_s": round(gen_s, 3),
+        "plan": [lf.name.lower(), rf.name.lower()],
+        "spmv_us": {f"{a.name.lower()}/{b.name.lower()}": round(t * 1e6, 1)
+                    for (a, b), t in sorted(prof["entries"].items())},
+        "convert_from_csr_ms": {f"{a.name.lower()}/{b.name.lower()}": round(t * 1e3, 3)
+                                for (a, b), t in sorted(prof["convert_s"].items())},
+        "apply_convert_ms": round(conv_ms, 3),
+        "convert_in_spmv_equivalents": round(conv_ms / spmv_ms, 1),
+        "cg_ms_per_step": round(step_ms, 4),
+        "cg_gflops": round(fl / (step_ms * 1e-3) / 1e9, 1),
+        "cg_gflops_incl_conversion": round(steps * fl / ((steps * step_ms + conv_ms) * 1e-3) / 1e9, 1),
+        "steps": steps,
+    }
+    del eng, split, part
+    torch.cuda.empty_cache()
+    return out
+
+
 # ---------------------------------------------------------------------------
 # CPU baseline (oracle port of the reference), bounded sample
 # ---------------------------------------------------------------------------
@@ -478,6 +539,8 @@ def run(args, rank: int, world: int) -> int:
             cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
         if args.powerlaw:
             extras["powerlaw"] = sweep_powerlaw(ds, torch, dev, peak)
+        if not args.no_config5:
+            extras["format_switching_192"] = format_switching(ds, torch, dev, peak)
 
     launches_per_step = eng.launches_per_step()
     line = {
@@ -569,6 +632,8 @@ def main(argv=None) -> int:
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--powerlaw", action="store_true", help="also run BASELINE config 4")
+    ap.add_argument("--no-config5", action="store_true",
+                    help="skip BASELINE config 5 (192^3 format switching incl. conversion)")
     ap.add_argument("--fixed-plan", action="store_true",
                     help="local DIA / remote CSR instead of the per-GPU tuner's choice")
     ap.add_argument("--rank-engine", action="store_true",

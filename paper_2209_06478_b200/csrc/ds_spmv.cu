@@ -1023,10 +1023,30 @@ int launch_csr_binned(int64_t nrows, int64_t ncols, int64_t nnz, const int* off,
   return DS_OK;
 }
 
+// A matrix without entries (e.g. the remote part of a partition without
+// ghosts): y = 0 (spmv) or y = y + 0.0 (spmv_add, kernels.py:196-198: the
+// +0.0 turns -0.0 into +0.0).  One streaming pass instead of a full SpMV
+// kernel walking empty tiles.
+__global__ void empty_matrix_kernel(int64_t n, double* y, int accum, const int* guard) {
+  if (guard && *guard) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = accum ? add(y[i], 0.0) : 0.0;
+}
+static int launch_empty_matrix(int64_t nrows, double* y, bool accum, const int* guard,
+                               cudaStream_t st) {
+  const unsigned g = (unsigned)min64(ceil_div(nrows, 256), (int64_t)sm_count() * 8);
+  empty_matrix_kernel<<<g, 256, 0, st>>>(nrows, y, accum ? 1 : 0, guard);
+  DS_LAUNCH_CHECK("empty_matrix_kernel");
+  return DS_OK;
+}
+
 int launch_csr(int64_t nrows, int64_t nnz, const int* off, const int* col, const double* val,
                const int* long_rows, int64_t n_long, int max_len, const double* x, double* y,
                bool accum, const DotOut* dot, cudaStream_t st) {
   if (nrows == 0) return DS_OK;
+  if (nnz == 0 && !(dot && dot->fused()))
+    return launch_empty_matrix(nrows, y, accum, dot ? dot->guard : nullptr, st);
   const int64_t groups = (nrows + 1) / 2;   // one 8-lane group per row pair
   int64_t blocks = ceil_div(groups * 8, kCsrBlock);
   static int eB = -2, use_g8 = -1;
@@ -1938,6 +1958,7 @@ int launch_coo(int64_t nrows, int64_t nnz, const int* rows, const int* cols, con
                bool sorted, int max_len, const double* x, double* y, bool accum, const int* guard,
                cudaStream_t st, bool plus_zero) {
   if (nrows == 0) return DS_OK;
+  if (nnz == 0) return launch_empty_matrix(nrows, y, accum, guard, st);
   static int coo_v1 = -1, coo_warp = -1;
   if (coo_v1 < 0) {
     coo_v1 = getenv("DS_COO_V1") ? 1 : 0;

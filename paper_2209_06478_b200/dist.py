@@ -355,7 +355,7 @@ def profile_rank(part: PartitionData, split: SplitMatrix, reps: int = 20,
     from .datamove import convert_inplace
     from .errors import DynSparseError
     from .formats import FormatId
-    from .kernels import spmv, spmv_add, SERIAL
+    from .kernels import prepared_spmv, spmv, spmv_add, SERIAL
     from .tuner import FORMATS
     dev = split.local.device
     n = part.a_full.nrows
@@ -382,12 +382,16 @@ def profile_rank(part: PartitionData, split: SplitMatrix, reps: int = 20,
             st = torch.cuda.current_stream(dev)
             spmv(SERIAL, split.local, xo, y)          # warm-up, untimed
             spmv_add(SERIAL, split.remote, xg, y)
+            # the events must bracket device work: launchers prepared up front
+            # (descriptors, plans), so each rep costs two ctypes calls of host time
+            lo = prepared_spmv(split.local, xo, y, 0)
+            ro = prepared_spmv(split.remote, xg, y, 1)
             ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                   for _ in range(reps)]
             for a, b in ev:
                 a.record(st)
-                spmv(SERIAL, split.local, xo, y)
-                spmv_add(SERIAL, split.remote, xg, y)
+                lo()
+                ro()
                 b.record(st)
             torch.cuda.synchronize(dev)
             med = statistics.median(a.elapsed_time(b) for a, b in ev) * 1e-3

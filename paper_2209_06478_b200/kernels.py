@@ -256,6 +256,31 @@ def _spmv(a, x: DenseVector, y: DenseVector, accumulate: int) -> None:
         wb()
 
 
+def prepared_spmv(a, x: DenseVector, y: DenseVector, accumulate: int):
+    """Resolve, validate and build the descriptor once; return a launcher that
+    only enqueues the kernel(s) (two ctypes calls' worth of host time), for
+    timing loops whose CUDA events must bracket device work, not Python.
+    DEVICE containers only."""
+    import torch
+    mat = _resolve(a)
+    if x.length != mat.ncols:
+        raise DimensionMismatch(f"x length {x.length} != ncols {mat.ncols}")
+    if y.length != mat.nrows:
+        raise DimensionMismatch(f"y length {y.length} != nrows {mat.nrows}")
+    dev = _exec_device(mat, x, y)
+    if not (isinstance(x.data, torch.Tensor) and isinstance(y.data, torch.Tensor)):
+        raise TypeError("prepared_spmv needs DEVICE vectors")
+    D = _dev()
+    d = descriptor(_on(mat, dev))
+    xp, yp, st = D.ptr(x.data), D.ptr(y.data), D.stream(dev)
+    lib = _native.load()
+
+    def launch():
+        _native.check(lib.ds_spmv(ctypes.byref(d), xp, yp, accumulate, st))
+    launch.keep = (d, x, y, mat)   # descriptor and buffers outlive the launcher
+    return launch
+
+
 def spmv(backend: ExecBackend, a, x: DenseVector, y: DenseVector) -> None:
     """y = A x, overwriting y (kernels.py:173-186)."""
     _spmv(a, x, y, 0)

@@ -207,7 +207,9 @@ class CgEngine:
                                                      stream)
             if rc != _native.DS_ERR_NOT_SUPPORTED:
                 self._ck(rc)
+                self._tail_launches = 1
                 return
+        self._tail_launches = 2
         self._ck(lib.ds_cg_update_deferred(pt.n, self._p(pt.x), self._p(pt.r), self._p(pt.p),
                                            self._p(pt.ap), s, ws, stream))
         self._ck(lib.ds_cg_direction_deferred(pt.n, self._p(pt.r), self._p(pt.p), s, hist, ws,
@@ -258,6 +260,8 @@ class CgEngine:
         self.graph.replay()
 
     def launches_per_step(self) -> int:
+        if getattr(self, "_tail_launches", None) is not None:   # deferred single-partition step
+            return 1 + self._tail_launches
         n = sum(1 for pt in self.parts for h in pt.halo if h[1])
         for pt in self.parts:
             n += 1 + (pt.d_remote is not None) + 2      # spmv(s), update, direction

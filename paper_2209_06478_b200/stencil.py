@@ -437,13 +437,19 @@ def distributed_spmv(backend: ExecBackend, problem: PartitionedProblem,
     for k, split in enumerate(splits):
         dev = dxs[k].data.device
         if per_partition_ns is not None:
+            # prepare first, so the events bracket the kernels, not Python
+            from .kernels import prepared_spmv
+            lo = prepared_spmv(split.local, DenseVector(dxs[k].data[:n]), dys[k], 0)
+            ro = prepared_spmv(split.remote, DenseVector(dxs[k].data[n:]), dys[k], 1)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(torch.cuda.current_stream(dev))
-        spmv(backend, split.local, DenseVector(dxs[k].data[:n]), dys[k])
-        spmv_add(backend, split.remote, DenseVector(dxs[k].data[n:]), dys[k])
-        if per_partition_ns is not None:
+            lo()
+            ro()
             e1.record(torch.cuda.current_stream(dev))
             events.append((k, e0, e1))
+            continue
+        spmv(backend, split.local, DenseVector(dxs[k].data[:n]), dys[k])
+        spmv_add(backend, split.remote, DenseVector(dxs[k].data[n:]), dys[k])
     if per_partition_ns is not None:
         for k, e0, e1 in events:
             e1.synchronize()

@@ -131,3 +131,21 @@ def test_pipe_stencil_and_cg_fused_dot():
     k = min(res.iterations, oref.iterations) + 1
     h = np.asarray(res.residual_history[:k])
     assert np.all(np.abs(h - oref.history[:k]) <= 1e-8 * oref.history[:k] + 64 * np.finfo(float).eps)
+
+
+@pytest.mark.parametrize("fmt", ["csr", "coo", "dia"])
+def test_empty_matrix_spmv_and_add(fmt):
+    """nnz == 0 (the remote part of a partition without ghosts): y = 0, and
+    spmv_add turns -0.0 into +0.0 exactly like y += 0.0 (kernels.py:196-198)."""
+    n, nc = 1000, 7
+    offs = np.zeros(n + 1, dtype=np.int64)
+    a = ds.convert(ds.CsrMatrix(n, nc, offs, np.zeros(0, np.int64), np.zeros(0), ds.MemorySpace.DEVICE,
+                                DEV), ds.FormatId[fmt.upper()], fill_limit=2**40)
+    x = ds.DenseVector(torch.ones(nc, dtype=torch.float64, device=DEV))
+    y0 = np.random.default_rng(5).standard_normal(n)
+    y0[::3] = -0.0
+    for acc in (False, True):
+        y = ds.DenseVector(torch.from_numpy(y0.copy()).to(DEV))
+        (ds.spmv_add if acc else ds.spmv)(ds.SERIAL, a, x, y)
+        want = y0 + 0.0 if acc else np.zeros(n)
+        assert y.data.cpu().numpy().tobytes() == want.tobytes(), (fmt, acc)
