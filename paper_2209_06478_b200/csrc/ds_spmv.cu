@@ -690,7 +690,12 @@ static int csr_pipe_launch(int64_t nrows, int64_t nnz, const int* off, const int
   cfg.cap = ((cfg.T * (max_len > 0 ? min(max_len, L) : 27) + 8) + 3) & ~3;
   cfg.stage_bytes = (int)((12 * (int64_t)cfg.cap + 127) & ~127);
   cfg.skip_above = skip_above;
-  cfg.hint = hint ? 1 : 0;
+  static int eH = -2;
+  if (eH == -2) {
+    const char* h = getenv("DS_CSR_HINT");
+    eH = h ? atoi(h) : -1;
+  }
+  cfg.hint = eH >= 0 ? eH : (hint ? 1 : 0);
   const size_t smem = 256 + (size_t)cfg.S * cfg.stage_bytes;
   if (cfg.T > 256 || cfg.T < 32 || smem > (size_t)max_dynamic_smem() - 1024)
     return DS_ERR_NOT_SUPPORTED;
