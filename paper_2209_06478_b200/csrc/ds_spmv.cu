@@ -1152,8 +1152,6 @@ __global__ void __launch_bounds__(256, 1)   // 1 CTA/SM: registers for all 27 ga
   }
   for (int j = tid; j < nd; j += blockDim.x) s_off[j] = offsets[j];
   __syncthreads();
-  bool has_main = false;
-  for (int j = 0; j < nd; ++j) has_main |= (s_off[j] == 0);
   if (tid == 0)
     for (int s = 0; s < S; ++s) {
       const int64_t t = blockIdx.x + s * G;
@@ -1180,13 +1178,11 @@ __global__ void __launch_bounds__(256, 1)   // 1 CTA/SM: registers for all 27 ga
       // (kernels.py:133-138).
       double xv[ND > 0 ? ND : 1];
       double acc = 0.0;
-      double xdiag = 0.0;   // x[i] when offset 0 is a diagonal (the fused dot reuses it)
       if (ND > 0) {
 #pragma unroll
         for (int j = 0; j < ND; ++j) {
           const int c = i + s_off[j];
           xv[j] = ld_gather(x + min(max(c, 0), ncols - 1));
-          if (s_off[j] == 0) xdiag = xv[j];
         }
 #pragma unroll
         for (int j = 0; j < ND; ++j) {
@@ -1206,7 +1202,10 @@ __global__ void __launch_bounds__(256, 1)   // 1 CTA/SM: registers for all 27 ga
       if (FUSE_DOT) {
         // p.Ap with p == x (the CG case): x[i] was already gathered for the
         // main diagonal; otherwise load it
-        const double pi = (ND > 0 && has_main && dot.other == x) ? xdiag : dot.other[i];
+        // p.Ap with p == x (the CG case): p[i] was just gathered by this
+        // thread for the main diagonal, so this load hits L1 (selecting the
+        // gathered value instead costs a compare + select per diagonal)
+        const double pi = __ldg(dot.other + i);
         dsum = add(dsum, mul(pi, out));
       }
     }

@@ -36,16 +36,20 @@ y = ds.DenseVector.zeros(n, ds.MemorySpace.DEVICE, dev)
 m = ds.convert(part.a_full, ds.FormatId[fmt.upper()])
 ref = ds.DenseVector.zeros(n, ds.MemorySpace.DEVICE, dev)
 ds.spmv(ds.SERIAL, ds.convert(part.a_full, ds.FormatId.CSR), x, ref)
+from paper_2209_06478_b200.kernels import prepared_spmv  # noqa: E402
+launch = prepared_spmv(m, x, y, 0)
 for _ in range(20):
-    ds.spmv(ds.SERIAL, m, x, y)
+    launch()
 st = torch.cuda.current_stream()
-ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(200)]
+# batches of back-to-back launches (the device never waits for Python)
+ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(5)]
 for a, b in ev:
     a.record(st)
-    ds.spmv(ds.SERIAL, m, x, y)
+    for _ in range(40):
+        launch()
     b.record(st)
 torch.cuda.synchronize()
-ms = statistics.median(a.elapsed_time(b) for a, b in ev)
+ms = statistics.median(a.elapsed_time(b) / 40 for a, b in ev)
 nnz = part.a_full.nnz
 byts = {"dia": 8 * getattr(m, "ndiags", 27) * n + 16 * n, "csr": 12 * nnz + 4 * (n + 1) + 16 * n,
         "coo": 16 * nnz + 16 * n}[fmt]
