@@ -286,6 +286,46 @@ class CgEngine:
         del lib, ws
         return {"avg_ms": sum(k) / len(k), "step_ms": sum(s) / len(s), "launches": len(k)}
 
+    def time_spmv_in_graph(self, steps: int) -> dict | None:
+        """The dominant kernel's duration inside the graph-replayed step:
+        one step captured with external timing events around partition 0's
+        local SpMV node and around the whole step, replayed ``steps`` times
+        (events read after each replay).  The events are recorded by the
+        device right at the node boundaries, so no host latency is counted.
+        None if this torch cannot capture timing events."""
+        import torch
+        from . import _device
+        cap = torch.cuda.Stream(self.dev)
+        cap.wait_stream(torch.cuda.current_stream(self.dev))
+        with torch.cuda.stream(cap):
+            ws = _device.workspace(self.dev)
+        torch.cuda.synchronize(self.dev)
+        try:
+            a, b, c, d = (torch.cuda.Event(enable_timing=True, external=True) for _ in range(4))
+        except TypeError:
+            return None
+        saved, self.ws = self.ws, ws
+        g = torch.cuda.CUDAGraph()
+        try:
+            with torch.cuda.graph(g, stream=cap):
+                a.record(cap)
+                self._marks = (cap, b, c)
+                try:
+                    self.step(cap.cuda_stream)
+                finally:
+                    self._marks = None
+                d.record(cap)
+        finally:
+            self.ws = saved
+        k, s = [], []
+        for _ in range(steps):
+            g.replay()
+            torch.cuda.synchronize(self.dev)
+            k.append(b.elapsed_time(c))
+            s.append(a.elapsed_time(d))
+        return {"avg_ms": sum(k) / len(k), "step_ms": sum(s) / len(s), "launches": len(k),
+                "method": "CUDA-graph step with external timing events around the SpMV node"}
+
     def _step_with_marks(self, st, mark0, mark1) -> None:
         self._marks = (st, mark0, mark1)
         try:
