@@ -553,6 +553,8 @@ def run(args, rank: int, world: int) -> int:
             kern["method"] = "eager steps, CUDA events around the SpMV launch"
         if int(eng.scalars().done) != 0:
             raise RuntimeError("CG stopped inside the measured steps; timings would be no-ops")
+        if hasattr(eng, "release_l2"):
+            eng.release_l2(st.cuda_stream)   # later legs get the whole L2 back
 
     clk = clocks.stop()
     nnz_total, ms_max = nnz_local, ms

@@ -215,6 +215,14 @@ int ds_csr_bins(int64_t nrows, const int32_t* row_offsets, int32_t* perm, int64_
 
 int ds_spmv(const ds_matrix* a, const double* x, double* y, int accumulate, void* stream);
 
+/* Persisting-L2 access-policy window over [base, base+bytes) for kernels
+ * launched or captured on `stream` afterwards (the solver keeps its vectors
+ * L2-resident while the matrix streams with evict_first); _reset clears the
+ * stream attribute, the persisting lines and the carve-out.
+ * DS_ERR_NOT_SUPPORTED when the window exceeds the device's persisting L2.  */
+int ds_l2_persist(const void* base, int64_t bytes, void* stream);
+int ds_l2_persist_reset(void* stream);
+
 /* ---- conjugate gradient building blocks (solver.py:56-189) --------------
  * The CG scalars live on the device in a ds_cg_scalars block.  Every kernel
  * below first tests s->done and returns when set, so a chunk of iterations

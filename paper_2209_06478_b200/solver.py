@@ -83,11 +83,20 @@ class _Part:
         self.d_remote = descriptor(remote) if remote is not None and not self.fold_remote else None
         self.local_mode = 2 if self.fold_remote else 0
         f64 = dict(dtype=torch.float64, device=device)
-        self.p_full = torch.zeros(n + ghosts, **f64)
+        # one allocation for the iteration's vectors (p with its ghost slots,
+        # x, r, Ap), each segment 256-B aligned: one persisting-L2 window
+        # covers them all (CgEngine._capture)
+        seg = lambda m: (m + 31) // 32 * 32   # noqa: E731  (doubles, 256-B multiple)
+        sizes = [seg(n + ghosts), seg(n), seg(n), seg(n)]
+        self.vec_block = torch.zeros(sum(sizes), **f64)
+        offs = [0]
+        for z in sizes[:-1]:
+            offs.append(offs[-1] + z)
+        self.p_full = self.vec_block[offs[0]:offs[0] + n + ghosts]
         self.p = self.p_full[:n]
-        self.x = torch.zeros(n, **f64)
-        self.r = torch.empty(n, **f64)
-        self.ap = torch.empty(n, **f64)
+        self.x = self.vec_block[offs[1]:offs[1] + n]
+        self.r = self.vec_block[offs[2]:offs[2] + n]
+        self.ap = self.vec_block[offs[3]:offs[3] + n]
         self.b = None
         self.halo = []   # (src partition, count, idx tensor, dst offset in p_full)
 
@@ -235,21 +244,33 @@ class CgEngine:
             c = chunk or (8 if use_graph else 4)
             if use_graph and self.graph is None:
                 self._capture(c)
-            rounds = 1
-            while True:
-                # replays between readbacks grow geometrically (1, 1, 2, 4, ...
-                # graphs of c steps): after convergence every kernel is a
-                # no-op, so overshooting costs only launch latency
-                for _ in range(rounds):
-                    if use_graph:
-                        self.graph.replay()
-                    else:
-                        for _ in range(c):
-                            self.step(st)
-                sc = self.scalars()
-                if sc.done:
-                    return sc
-                rounds = min(rounds * 2, 16)
+            try:
+                return self._run_rounds(c, use_graph, st)
+            finally:
+                self.release_l2(st)
+
+    def _run_rounds(self, c: int, use_graph: bool, st) -> _native.DsCgScalars:
+        rounds = 1
+        while True:
+            # replays between readbacks grow geometrically (1, 1, 2, 4, ...
+            # graphs of c steps): after convergence every kernel is a
+            # no-op, so overshooting costs only launch latency
+            for _ in range(rounds):
+                if use_graph:
+                    self.graph.replay()
+                else:
+                    for _ in range(c):
+                        self.step(st)
+            sc = self.scalars()
+            if sc.done:
+                return sc
+            rounds = min(rounds * 2, 16)
+
+    def release_l2(self, stream) -> None:
+        """Give the persisting-L2 carve-out back (set by _capture)."""
+        if getattr(self, "_l2_persist", False):
+            self.lib.ds_l2_persist_reset(stream)
+            self._l2_persist = False
 
     # benchmarking hooks ---------------------------------------------------
     def capture_step(self) -> None:
@@ -342,12 +363,24 @@ class CgEngine:
             ws = _device.workspace(self.dev)  # workspace bound to the capture stream
         torch.cuda.synchronize(self.dev)
         saved, self.ws = self.ws, ws
+        # keep the vectors L2-resident across iterations (captured into the
+        # graph's kernel nodes); the matrix streams with evict_first
+        persist = (self.P == 1 and os.environ.get("DS_CG_L2_PERSIST", "1") != "0")
+        if persist:
+            vb = self.parts[0].vec_block
+            persist = self.lib.ds_l2_persist(vb.data_ptr(), vb.numel() * 8,
+                                             cap.cuda_stream) == 0
+            self._l2_persist = persist
         g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=cap):
-            st = cap.cuda_stream
-            for _ in range(c):
-                self.step(st)
-        self.ws = saved
+        try:
+            with torch.cuda.graph(g, stream=cap):
+                st = cap.cuda_stream
+                for _ in range(c):
+                    self.step(st)
+        finally:
+            self.ws = saved
+        # the window now lives in the graph's kernel nodes; the carve-out
+        # (cudaLimitPersistingL2CacheSize) stays set for the replays
         self.graph = g
 
 
