@@ -486,8 +486,14 @@ def _pinned(eng, name: str, n: int):
 
 
 def _pinned_copy(eng, name: str, dst, src_np) -> None:
-    """Host numpy -> device tensor through a cached pinned staging buffer."""
+    """Host numpy -> device tensor.  A staging copy into a pinned buffer is a
+    host memcpy of the whole vector before the DMA; the driver's pageable
+    path overlaps its own staging with the transfer, so copy directly
+    (DS_PINNED_STAGING=1 restores the pinned route)."""
     import torch
+    if not os.environ.get("DS_PINNED_STAGING"):
+        dst.copy_(torch.from_numpy(np.ascontiguousarray(src_np)))
+        return
     buf = _pinned(eng, name, dst.numel())
     torch.cuda.current_stream(dst.device).synchronize()   # buffer free for reuse
     buf.numpy()[:] = src_np
@@ -533,12 +539,14 @@ def _cg_distributed(op, bs, x0s, tol, max_iters, use_graph):
         sc = eng.run(use_graph=use_graph)
         it, hist, conv = _finish(eng, sc)
     host = bs[0].space == MemorySpace.HOST
-    if host:
+    if host and os.environ.get("DS_PINNED_STAGING"):
         outs = [_pinned(eng, f"x{k}", pt.n) for k, pt in enumerate(parts)]
         for o, pt in zip(outs, parts):
             o.copy_(pt.x, non_blocking=True)
         torch.cuda.synchronize(eng.dev)
         xs = [DenseVector(o.numpy().copy()) for o in outs]
+    elif host:   # fresh arrays (the reference returns new ones): one D2H each
+        xs = [DenseVector(pt.x.cpu().numpy()) for pt in parts]
     else:
         xs = [DenseVector(pt.x.clone()) for pt in parts]
     return CgResult(xs, it, hist, conv)
