@@ -90,6 +90,16 @@ int ds_spmv_coo_sorted(int64_t nrows, int64_t ncols, int64_t nnz, const int32_t*
                        const int32_t* col_indices, const double* values, int32_t max_row_len,
                        const double* x, double* y, int accumulate, void* stream);
 
+/* Long-run plan of a row-sorted COO: the runs of equal row index longer than
+ * `threshold` entries (ds_coo_long_run_threshold() is the kernel's) as int32
+ * (start, end) pairs sorted by start; pass them in ds_matrix.long_rows with
+ * n_long = the number of runs: those rows are summed by a CTA each on a side
+ * stream while the warp kernel skips them.  `runs` holds 2*capacity int32
+ * (capacity >= nnz / threshold + 1 suffices).  Host count, synchronises.   */
+int ds_coo_long_runs(int64_t nnz, const int32_t* row_indices, int32_t threshold, int32_t* runs,
+                     int64_t capacity, int64_t* n_runs, void* stream);
+int ds_coo_long_run_threshold(void);
+
 /* Longest run of equal row indices of a row-sorted COO (host, synchronises). */
 int ds_coo_max_run(int64_t nnz, const int32_t* row_indices, int32_t* max_run, void* stream);
 
@@ -196,7 +206,9 @@ typedef struct ds_matrix {
   const int32_t* idx0;       /* COO row_indices | CSR row_offsets | DIA offsets */
   const int32_t* idx1;       /* COO/CSR col_indices                             */
   const double* values;      /* COO/CSR values | DIA (nrows, ndiags) row-major  */
-  const int32_t* long_rows;  /* CSR: rows > 129 entries (ds_csr_analyze), or NULL */
+  const int32_t* long_rows;  /* CSR: rows > 129 entries (ds_csr_analyze); sorted
+                                COO: long-run (start, end) pairs (ds_coo_long_runs);
+                                or NULL                                           */
   int64_t n_long;
   int32_t rows_sorted;       /* COO: row indices nondecreasing                  */
   int32_t max_row_len;       /* CSR / sorted COO: longest row if known, else 0  */

@@ -88,6 +88,8 @@ _SIGNATURES = {
                             c_vp]),
     "ds_coo_order_flags": (c_int, [c_i64, c_vp, c_vp, P_i32, c_vp]),
     "ds_coo_max_run": (c_int, [c_i64, c_vp, P_i32, c_vp]),
+    "ds_coo_long_runs": (c_int, [c_i64, c_vp, c_i32, c_vp, c_i64, P_i64, c_vp]),
+    "ds_coo_long_run_threshold": (c_int, []),
     "ds_spmv_coo_sorted": (c_int, [c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp,
                                    c_int, c_vp]),
     "ds_csr_bins": (c_int, [c_i64, c_vp, c_vp, P_i64, c_vp]),

@@ -148,6 +148,28 @@ extern "C" int ds_l2_persist_reset(void* stream) {
   return DS_OK;
 }
 
+namespace ds {
+int aux_stream(cudaStream_t* side, cudaEvent_t* fork, cudaEvent_t* join) {
+  static cudaStream_t s[64] = {};
+  static cudaEvent_t f[64] = {}, j[64] = {};
+  int dev = 0;
+  DS_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) {
+    set_error("device index %d out of range", dev);
+    return DS_ERR_NOT_SUPPORTED;
+  }
+  if (!s[dev]) {
+    DS_CUDA(cudaStreamCreateWithFlags(&s[dev], cudaStreamNonBlocking));
+    DS_CUDA(cudaEventCreateWithFlags(&f[dev], cudaEventDisableTiming));
+    DS_CUDA(cudaEventCreateWithFlags(&j[dev], cudaEventDisableTiming));
+  }
+  *side = s[dev];
+  *fork = f[dev];
+  *join = j[dev];
+  return DS_OK;
+}
+}  // namespace ds
+
 extern "C" const char* ds_last_error(void) { return ds::g_err; }
 extern "C" int ds_abi_version(void) { return DS_ABI_VERSION; }
 extern "C" int ds_device_sm_count(int* out) {

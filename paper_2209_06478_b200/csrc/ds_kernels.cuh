@@ -139,7 +139,11 @@ int launch_dia(int64_t nrows, int64_t ncols, int ndiags, const int* off, const d
                const double* x, double* y, bool accum, const DotOut* dot, cudaStream_t st);
 int launch_coo(int64_t nrows, int64_t nnz, const int* rows, const int* cols, const double* vals,
                bool sorted, int max_len, const double* x, double* y, bool accum, const int* guard,
-               cudaStream_t st, bool plus_zero = false);
+               cudaStream_t st, bool plus_zero = false, const int* long_runs = nullptr,
+               int n_long = 0);
+// per-device auxiliary stream + fork/join events (created once) for kernels
+// that run concurrently with the main one
+int aux_stream(cudaStream_t* side, cudaEvent_t* fork, cudaEvent_t* join);
 // stand-alone fused dot with the same epilogue (used when a SpMV kernel
 // cannot fuse it): result = a[0:n] . b[0:n]
 int launch_dot(int64_t n, const double* a, const double* b, const DotOut& d, cudaStream_t st);

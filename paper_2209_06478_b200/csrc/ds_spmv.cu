@@ -22,6 +22,10 @@
 //        sequentially (np.bincount order), carrying across tiles.
 #include <stdlib.h>
 
+#include <algorithm>
+#include <utility>
+#include <vector>
+
 #include "ds_common.cuh"
 #include "ds_kernels.cuh"
 
@@ -1526,7 +1530,8 @@ template <bool ACCUM>
 __global__ void __launch_bounds__(32 * kCooWarps)
     coo_warp_segments(int nrows, int64_t nnz, const int* __restrict__ rows,
                       const int* __restrict__ cols, const double* __restrict__ vals,
-                      const double* __restrict__ x, double* y, const int* guard, int plus_zero) {
+                      const double* __restrict__ x, double* y, const int* guard, int plus_zero,
+                      const int* __restrict__ long_runs, int n_long) {
   if (guard && *guard) return;
   __shared__ double s_p[kCooWarps][kCooWTile];
   __shared__ int s_r[kCooWarps][kCooWTile];
@@ -1548,12 +1553,27 @@ __global__ void __launch_bounds__(32 * kCooWarps)
     return;
   }
   for (int64_t c = gw; c < nchunks; c += nw) {
-    const int64_t start = coo_row_start_at_or_after_warp(rows, nnz, c * kCooWarpChunk);
-    const int64_t end = coo_row_start_at_or_after_warp(rows, nnz, (c + 1) * kCooWarpChunk);
-    const int R0 = (start == 0) ? 0 : (start < nnz ? rows[start] : nrows);
-    const int R1 = (end < nnz) ? rows[end] : nrows;
+    const int64_t cstart = coo_row_start_at_or_after_warp(rows, nnz, c * kCooWarpChunk);
+    const int64_t cend = coo_row_start_at_or_after_warp(rows, nnz, (c + 1) * kCooWarpChunk);
+    const int R0 = (cstart == 0) ? 0 : (cstart < nnz ? rows[cstart] : nrows);
+    const int R1 = (cend < nnz) ? rows[cend] : nrows;
     int prev_row = R0 - 1, carry_row = -1;
     double carry = 0.0;
+    // long runs (whole rows, sorted by start; coo_long_runs_kernel sums them
+    // concurrently) are cut out of the chunk: it is processed as the
+    // sub-ranges between them
+    int lr = 0;
+    if (n_long > 0) {
+      int lo = 0, hi = n_long;   // first run with start >= cstart
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (long_runs[2 * mid] < cstart) lo = mid + 1; else hi = mid;
+      }
+      lr = lo;
+    }
+    int64_t start = cstart;
+    for (;;) {
+    const int64_t end = (lr < n_long && long_runs[2 * lr] < cend) ? long_runs[2 * lr] : cend;
     CooTileRegs T;
     if (start < end) coo_tile_load(rows, cols, vals, start, (int)min64(kCooWTile, end - start), lane, T);
     for (int64_t t0 = start; t0 < end; t0 += kCooWTile) {
@@ -1628,9 +1648,70 @@ __global__ void __launch_bounds__(32 * kCooWarps)
       }
       __syncwarp();
     }
+    if (end == cend) break;
+    // skip long run lr: zero the absent rows before it; its own row is
+    // written by the long-run kernel
+    {
+      const int lrow = rows[long_runs[2 * lr]];
+      for (int r = prev_row + 1 + lane; r < lrow; r += 32) y[r] = ACCUM ? add(y[r], 0.0) : 0.0;
+      prev_row = lrow;
+      carry_row = -1;
+      start = long_runs[2 * lr + 1];
+      ++lr;
+      __syncwarp();
+    }
+    }
     // rows after the chunk's last entry up to the next chunk's first row
     for (int r = prev_row + 1 + lane; r < R1; r += 32) y[r] = ACCUM ? add(y[r], 0.0) : 0.0;
     __syncwarp();
+  }
+}
+
+// Long runs of a row-sorted COO (rows longer than kCooLongRun entries, e.g.
+// the power-law matrix's 14687-entry row): one CTA per run.  All threads form
+// the products of a piece of the run into shared memory (coalesced loads,
+// every gather in flight), then thread 0 adds them in stored order -- the
+// np.bincount chain, carried from piece to piece -- with the next shared
+// loads issued ahead of the adds.  Runs on a side stream concurrently with
+// coo_warp_segments, which skips these rows.
+constexpr int kCooLongRun = 2048;
+constexpr int kCooLongPiece = 8192;   // products per shared-memory piece (64 KB)
+
+template <bool ACCUM>
+__global__ void __launch_bounds__(512)
+    coo_long_runs_kernel(const int* __restrict__ long_runs, int n_long,
+                         const int* __restrict__ rows, const int* __restrict__ cols,
+                         const double* __restrict__ vals, const double* __restrict__ x,
+                         double* y, const int* guard, int plus_zero) {
+  if (guard && *guard) return;
+  extern __shared__ __align__(16) double s_p[];
+  for (int li = blockIdx.x; li < n_long; li += gridDim.x) {
+    const int64_t b = long_runs[2 * li], e = long_runs[2 * li + 1];
+    double acc = 0.0;
+    for (int64_t p0 = b; p0 < e; p0 += kCooLongPiece) {
+      const int cnt = (int)min64(kCooLongPiece, e - p0);
+      for (int k = threadIdx.x; k < cnt; k += blockDim.x)
+        s_p[k] = mul(vals[p0 + k], ld_gather(x + cols[p0 + k]));
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int k = 0;
+        for (; k + 8 <= cnt; k += 8) {
+          double q[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) q[j] = s_p[k + j];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc = add(acc, q[j]);
+        }
+        for (; k < cnt; ++k) acc = add(acc, s_p[k]);
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      const int row = rows[b];
+      double o = ACCUM ? add(y[row], acc) : acc;
+      if (plus_zero) o = add(o, 0.0);
+      y[row] = o;
+    }
   }
 }
 
@@ -1960,7 +2041,7 @@ __global__ void axpy_inplace(int64_t n, double* y, const double* t, const int* g
 
 int launch_coo(int64_t nrows, int64_t nnz, const int* rows, const int* cols, const double* vals,
                bool sorted, int max_len, const double* x, double* y, bool accum, const int* guard,
-               cudaStream_t st, bool plus_zero) {
+               cudaStream_t st, bool plus_zero, const int* long_runs, int n_long) {
   if (nrows == 0) return DS_OK;
   if (nnz == 0) return launch_empty_matrix(nrows, y, accum, guard, st);
   static int coo_v1 = -1, coo_warp = -1;
@@ -1980,13 +2061,40 @@ int launch_coo(int64_t nrows, int64_t nnz, const int* rows, const int* cols, con
     const int64_t cap = (int64_t)sm_count() * 8;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
+    const bool split = long_runs != nullptr && n_long > 0;
+    cudaEvent_t joined = nullptr;
+    if (split) {   // the long runs on a side stream, launched first (fork / join)
+      cudaStream_t side;
+      cudaEvent_t fork;
+      int rc = aux_stream(&side, &fork, &joined);
+      if (rc) return rc;
+      DS_CUDA(cudaEventRecord(fork, st));
+      DS_CUDA(cudaStreamWaitEvent(side, fork, 0));
+      const size_t smem = (size_t)kCooLongPiece * 8;
+      const void* lk = accum ? (const void*)coo_long_runs_kernel<true>
+                             : (const void*)coo_long_runs_kernel<false>;
+      rc = allow_dynamic_smem(lk, smem);
+      if (rc) return rc;
+      const unsigned lg = (unsigned)min64(n_long, (int64_t)sm_count());
+      if (accum)
+        coo_long_runs_kernel<true><<<lg, 512, smem, side>>>(long_runs, n_long, rows, cols, vals,
+                                                            x, y, guard, (int)plus_zero);
+      else
+        coo_long_runs_kernel<false><<<lg, 512, smem, side>>>(long_runs, n_long, rows, cols, vals,
+                                                             x, y, guard, (int)plus_zero);
+      DS_LAUNCH_CHECK("coo_long_runs_kernel");
+      DS_CUDA(cudaEventRecord(joined, side));
+    }
     if (accum)
       coo_warp_segments<true><<<(unsigned)blocks, 32 * kCooWarps, 0, st>>>(
-          (int)nrows, nnz, rows, cols, vals, x, y, guard, (int)plus_zero);
+          (int)nrows, nnz, rows, cols, vals, x, y, guard, (int)plus_zero,
+          split ? long_runs : nullptr, split ? n_long : 0);
     else
       coo_warp_segments<false><<<(unsigned)blocks, 32 * kCooWarps, 0, st>>>(
-          (int)nrows, nnz, rows, cols, vals, x, y, guard, (int)plus_zero);
+          (int)nrows, nnz, rows, cols, vals, x, y, guard, (int)plus_zero,
+          split ? long_runs : nullptr, split ? n_long : 0);
     DS_LAUNCH_CHECK("coo_warp_segments");
+    if (split) DS_CUDA(cudaStreamWaitEvent(st, joined, 0));
     return DS_OK;
   }
   if (sorted) {
@@ -2140,6 +2248,71 @@ extern "C" int ds_coo_max_run(int64_t nnz, const int32_t* row_indices, int32_t* 
   return DS_OK;
 }
 
+// Runs of equal row index longer than `threshold` (whole rows) as (start,
+// end) int32 pairs sorted by start -- the long-run plan of a row-sorted COO.
+__global__ void coo_long_runs_find(int64_t nnz, const int* __restrict__ rows, int threshold,
+                                   int* out, int64_t capacity, unsigned long long* count) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int r = rows[k];
+    if (k > 0 && rows[k - 1] == r) continue;
+    if (k + threshold >= nnz || rows[k + threshold] != r) continue;   // run <= threshold
+    int64_t lo = k + threshold, step = 1;   // rows[lo] == r: gallop to the run's end
+    while (lo + step < nnz && rows[lo + step] == r) {
+      lo += step;
+      step <<= 1;
+    }
+    int64_t hi = min64(lo + step, nnz);
+    while (hi - lo > 1) {
+      const int64_t mid = lo + (hi - lo) / 2;
+      if (rows[mid] == r) lo = mid; else hi = mid;
+    }
+    const unsigned long long slot = atomicAdd(count, 1ull);
+    if ((int64_t)slot < capacity) {
+      out[2 * slot] = (int)k;
+      out[2 * slot + 1] = (int)(lo + 1);
+    }
+  }
+}
+
+extern "C" int ds_coo_long_runs(int64_t nnz, const int32_t* row_indices, int32_t threshold,
+                                int32_t* runs, int64_t capacity, int64_t* n_runs, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  *n_runs = 0;
+  if (nnz <= 0 || threshold < 1) return DS_OK;
+  unsigned long long* d = nullptr;
+  DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(*d), st));
+  DS_CUDA(cudaMemsetAsync(d, 0, sizeof(*d), st));
+  const unsigned g = (unsigned)min64(ceil_div(nnz, 256), (int64_t)sm_count() * 8);
+  coo_long_runs_find<<<g, 256, 0, st>>>(nnz, row_indices, threshold, runs, capacity, d);
+  DS_LAUNCH_CHECK("coo_long_runs_find");
+  unsigned long long h = 0;
+  DS_CUDA(cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, st));
+  DS_CUDA(cudaFreeAsync(d, st));
+  DS_CUDA(cudaStreamSynchronize(st));
+  if ((int64_t)h > capacity) {
+    set_error("ds_coo_long_runs: %llu runs exceed the capacity %lld", h, (long long)capacity);
+    return DS_ERR_NOT_SUPPORTED;
+  }
+  if (h > 1) {   // sort the (few) pairs by start on the host
+    std::vector<std::pair<int, int>> v(h);
+    DS_CUDA(cudaMemcpy(v.data(), runs, h * 2 * sizeof(int), cudaMemcpyDeviceToHost));
+    std::sort(v.begin(), v.end());
+    DS_CUDA(cudaMemcpy(runs, v.data(), h * 2 * sizeof(int), cudaMemcpyHostToDevice));
+  }
+  *n_runs = (int64_t)h;
+  return DS_OK;
+}
+
+extern "C" int ds_coo_long_run_threshold(void) {
+  static int e = -2;
+  if (e == -2) {
+    const char* v = getenv("DS_COO_LONG_RUN");
+    e = v ? atoi(v) : -1;
+  }
+  return e > 0 ? e : kCooLongRun;
+}
+
 extern "C" int ds_spmv_coo_sorted(int64_t nrows, int64_t ncols, int64_t nnz,
                                   const int32_t* row_indices, const int32_t* col_indices,
                                   const double* values, int32_t max_row_len, const double* x,
@@ -2150,7 +2323,7 @@ extern "C" int ds_spmv_coo_sorted(int64_t nrows, int64_t ncols, int64_t nnz,
     return DS_ERR_NOT_SUPPORTED;
   }
   return launch_coo(nrows, nnz, row_indices, col_indices, values, true, max_row_len, x, y,
-                    accumulate != 0, nullptr, as_stream(stream));
+                    accumulate != 0, nullptr, as_stream(stream), false, nullptr, 0);
 }
 
 extern "C" int ds_coo_order_flags(int64_t nnz, const int32_t* row_indices,

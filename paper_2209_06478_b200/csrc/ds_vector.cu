@@ -954,9 +954,11 @@ extern "C" int ds_cg_spmv_dot(const ds_matrix* a, const double* x, double* y, in
       break;
     }
     case DS_FMT_COO:
+      // COO plans reuse long_rows / n_long: the long-run (start, end) pairs
       rc = launch_coo(a->nrows, a->nnz, a->idx0, a->idx1, a->values, a->rows_sorted != 0,
-                      a->max_row_len, x, y,
-                      acc, d.guard, st, d.plus_zero != 0);
+                      a->max_row_len, x, y, acc, d.guard, st, d.plus_zero != 0,
+                      a->rows_sorted ? a->long_rows : nullptr,
+                      a->rows_sorted ? (int)a->n_long : 0);
       break;
     default:
       set_error("unknown format %d", a->format);

@@ -23,6 +23,7 @@ kernels.py:38-57); on the device the grid replaces the host thread pool.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -173,6 +174,32 @@ def coo_max_run(m: CooMatrix) -> int:
     return m._cache["max_run"][1]
 
 
+def coo_long_runs(m: CooMatrix):
+    """(int32 tensor of (start, end) pairs, count) of the rows longer than the
+    long-run kernel's threshold, for a row-sorted COO; (None, 0) otherwise.
+    Cached per buffer version (ds_coo_long_runs)."""
+    k = ("runs",) + _key(m.row_indices, m.col_indices)
+    hit = m._cache.get("runs")
+    if hit is not None and hit[0] == k:
+        return hit[1], hit[2]
+    import torch
+    D = _dev()
+    runs, cnt = None, 0
+    thr = int(_native.load().ds_coo_long_run_threshold())
+    if (coo_flags(m) & 1) and coo_max_run(m) > thr and \
+            not os.environ.get("DS_COO_NO_LONG_RUNS"):
+        cap = m.nnz // thr + 1
+        buf = torch.empty(2 * cap, dtype=torch.int32, device=m.device)
+        n = ctypes.c_int64(0)
+        with torch.cuda.device(m.device):
+            _native.call("ds_coo_long_runs", m.nnz, D.ptr(m.row_indices), thr, D.ptr(buf), cap,
+                         ctypes.byref(n), D.stream(m.device))
+        cnt = int(n.value)
+        runs = buf[:2 * max(cnt, 1)].clone() if cnt else None
+    m._cache["runs"] = (k, runs, cnt)
+    return runs, cnt
+
+
 def descriptor(m) -> _native.DsMatrix:
     """ds_matrix for a DEVICE container (the C-side dispatch record)."""
     m = _resolve(m)
@@ -196,6 +223,9 @@ def descriptor(m) -> _native.DsMatrix:
         d.idx0, d.idx1, d.values = D.ptr(m.row_indices), D.ptr(m.col_indices), D.ptr(m.values)
         d.rows_sorted = coo_flags(m) & 1
         d.max_row_len = coo_max_run(m)
+        runs, cnt = coo_long_runs(m)
+        if runs is not None:
+            d.long_rows, d.n_long = runs.data_ptr(), cnt
     elif isinstance(m, DiaMatrix):
         d.format, d.ndiags = int(FormatId.DIA), m.ndiags
         d.idx0, d.values = D.ptr(m.offsets), D.ptr(m.values)

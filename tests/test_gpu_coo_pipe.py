@@ -103,3 +103,36 @@ def test_coo_pipe_giant_row_and_odd_tail():
         y0 = rng.standard_normal(nrows)
         got = run(nrows, ncols, rows, cols, vals, x, y0, acc)
         assert got.tobytes() == want(nrows, ncols, rows, cols, vals, x, y0, acc).tobytes(), acc
+
+
+def test_coo_long_runs_split_bitwise():
+    """Rows longer than the long-run threshold are summed by their own kernel
+    on a side stream while the warp kernel skips them (descriptor path): runs
+    at the start, back to back, spanning many warp chunks, at the end."""
+    import paper_2209_06478_b200 as ds
+    from paper_2209_06478_b200 import kernels as K_
+    thr = int(_native.load().ds_coo_long_run_threshold())
+    rng = np.random.default_rng(31)
+    nrows, ncols = 3000, 40000
+    lengths = rng.integers(0, 30, nrows)
+    lengths[0] = thr + 1            # first row long
+    lengths[10] = 3 * thr + 7       # two long rows back to back
+    lengths[11] = 20000             # spans several 4096-entry chunks
+    lengths[1500] = thr + 1
+    lengths[2999] = 2 * thr + 5     # last row long
+    lengths[[5, 6, 2000, 2001]] = 0
+    rows, cols, vals = sorted_coo(rng, nrows, ncols, lengths)
+    x = rng.standard_normal(ncols)
+    a = ds.CooMatrix(nrows, ncols, rows, cols, vals, ds.MemorySpace.DEVICE, DEV)
+    runs, cnt = K_.coo_long_runs(a)
+    assert cnt == 5
+    r = runs.cpu().numpy().reshape(-1, 2)
+    assert np.all(np.diff(r[:, 0]) > 0) and np.all(r[:, 1] - r[:, 0] > thr)
+    for acc in (False, True):
+        y0 = rng.standard_normal(nrows)
+        y0[::5] = -0.0
+        yd = ds.DenseVector(torch.from_numpy(y0.copy()).to(DEV))
+        (ds.spmv_add if acc else ds.spmv)(ds.SERIAL, a, ds.DenseVector(torch.from_numpy(x).to(DEV)), yd)
+        torch.cuda.synchronize()
+        want_y = want(nrows, ncols, rows, cols, vals, x, y0, acc)
+        assert yd.data.cpu().numpy().tobytes() == want_y.tobytes(), acc
