@@ -104,11 +104,17 @@ class RankCG:
         self.d_remote = None if self.fold else descriptor(self.remote)
         f64 = dict(dtype=torch.float64, device=device)
         g = part.halo.ghost_count
-        self.p_full = torch.zeros(n + g, **f64)
+        # one allocation for the iteration's vectors (256-B aligned segments)
+        # so one persisting-L2 window covers them (capture_step)
+        seg = lambda m: (m + 31) // 32 * 32   # noqa: E731
+        sizes = [seg(n + g), seg(n), seg(n), seg(n)]
+        self.vec_block = torch.zeros(sum(sizes), **f64)
+        o = [0, sizes[0], sizes[0] + sizes[1], sizes[0] + sizes[1] + sizes[2]]
+        self.p_full = self.vec_block[o[0]:o[0] + n + g]
         self.p = self.p_full[:n]
-        self.x = torch.zeros(n, **f64)
-        self.r = torch.empty(n, **f64)
-        self.ap = torch.empty(n, **f64)
+        self.x = self.vec_block[o[1]:o[1] + n]
+        self.r = self.vec_block[o[2]:o[2] + n]
+        self.ap = self.vec_block[o[3]:o[3] + n]
         self.b = to_device(part.b, device).data
         self.scal = torch.zeros(_native.CG_SCALARS_BYTES // 8, **f64)
         self.hist = torch.zeros(self.max_iters + 1, **f64)
@@ -230,6 +236,10 @@ class RankCG:
             ws = _device.workspace(self.dev)
         torch.cuda.synchronize(self.dev)
         saved, self.ws = self.ws, ws
+        import os
+        if os.environ.get("DS_CG_L2_PERSIST", "1") != "0":
+            self._l2_persist = self.lib.ds_l2_persist(
+                self.vec_block.data_ptr(), self.vec_block.numel() * 8, cap.cuda_stream) == 0
         g = torch.cuda.CUDAGraph()
         try:
             with torch.cuda.graph(g, stream=cap):
@@ -239,6 +249,12 @@ class RankCG:
             self.graph = None
         finally:
             self.ws = saved
+
+    def release_l2(self, stream) -> None:
+        """Give the persisting-L2 carve-out back (set by capture_step)."""
+        if getattr(self, "_l2_persist", False):
+            self.lib.ds_l2_persist_reset(stream)
+            self._l2_persist = False
 
     def replay(self) -> None:
         import torch
