@@ -152,12 +152,14 @@ namespace ds {
 int aux_stream(cudaStream_t* side, cudaEvent_t* fork, cudaEvent_t* join) {
   static cudaStream_t s[64] = {};
   static cudaEvent_t f[64] = {}, j[64] = {};
+  static std::mutex mu;
   int dev = 0;
   DS_CUDA(cudaGetDevice(&dev));
   if (dev < 0 || dev >= 64) {
     set_error("device index %d out of range", dev);
     return DS_ERR_NOT_SUPPORTED;
   }
+  std::lock_guard<std::mutex> lock(mu);
   if (!s[dev]) {
     DS_CUDA(cudaStreamCreateWithFlags(&s[dev], cudaStreamNonBlocking));
     DS_CUDA(cudaEventCreateWithFlags(&f[dev], cudaEventDisableTiming));

@@ -74,3 +74,17 @@ def test_fused_entry_reports_unsupported_for_misaligned():
     x = buf.data_ptr() + 8   # 8-byte offset: not 16-byte aligned
     rc = lib.ds_cg_update_direction_deferred(n, x, x, x, x, None, None, None, None)
     assert rc == _native.DS_ERR_NOT_SUPPORTED
+
+
+def test_l2_persist_window_fits_or_refuses():
+    """ds_l2_persist takes whole windows only: a small one is set (and the
+    reset gives the carve-out back); one larger than the persisting L2 is
+    refused without side effects."""
+    lib = _native.load()
+    st = torch.cuda.current_stream(DEV).cuda_stream
+    small = torch.zeros(1 << 20, dtype=torch.float64, device=DEV)          # 8 MB
+    assert lib.ds_l2_persist(small.data_ptr(), small.numel() * 8, st) == 0
+    assert lib.ds_l2_persist_reset(st) == 0
+    huge_bytes = 1 << 40
+    assert lib.ds_l2_persist(small.data_ptr(), huge_bytes, st) == _native.DS_ERR_NOT_SUPPORTED
+    assert lib.ds_l2_persist_reset(st) == 0
