@@ -495,7 +495,7 @@ def _pinned_copy(eng, name: str, dst, src_np) -> None:
         return
     buf = _pinned(eng, name, dst.numel())
     torch.cuda.current_stream(dst.device).synchronize()   # buffer free for reuse
-    buf.numpy()[:] = src_np
+    buf.copy_(torch.from_numpy(np.ascontiguousarray(src_np)))   # multi-threaded host copy
     dst.copy_(buf, non_blocking=True)
 
 
@@ -543,7 +543,9 @@ def _cg_distributed(op, bs, x0s, tol, max_iters, use_graph):
         for o, pt in zip(outs, parts):
             o.copy_(pt.x, non_blocking=True)
         torch.cuda.synchronize(eng.dev)
-        xs = [DenseVector(o.numpy().copy()) for o in outs]
+        # fresh arrays (the reference returns new ones), filled by torch's
+        # multi-threaded host copy
+        xs = [DenseVector(torch.empty_like(o).copy_(o).numpy()) for o in outs]
     elif host:   # fresh arrays (the reference returns new ones): one D2H each
         xs = [DenseVector(pt.x.cpu().numpy()) for pt in parts]
     else:
