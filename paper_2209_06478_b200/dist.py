@@ -324,7 +324,7 @@ class RankCG:
                 pin = (torch.empty(self.n, dtype=torch.float64, pin_memory=True),
                        torch.empty(self.n, dtype=torch.float64, pin_memory=True))
                 self._pin = pin
-            pin[0].numpy()[:] = b_host
+            pin[0].copy_(torch.from_numpy(np.ascontiguousarray(b_host)))   # multi-threaded
             self.b.copy_(pin[0], non_blocking=True)
             self.x.zero_()
             self.p.zero_()
@@ -333,7 +333,7 @@ class RankCG:
                 self.replay()
             pin[1].copy_(self.x, non_blocking=True)
             st.synchronize()
-            return pin[1].numpy().copy()
+            return torch.empty_like(pin[1]).copy_(pin[1]).numpy()
 
     def close(self) -> None:
         if self.comm:
