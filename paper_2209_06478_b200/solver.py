@@ -273,9 +273,9 @@ class CgEngine:
             self._l2_persist = False
 
     # benchmarking hooks ---------------------------------------------------
-    def capture_step(self) -> None:
-        """Capture ONE iteration as a CUDA graph (replayed by ``replay``)."""
-        self._capture(1)
+    def capture_step(self, steps: int = 1) -> None:
+        """Capture ``steps`` iterations as one CUDA graph (replayed by ``replay``)."""
+        self._capture(steps)
 
     def replay(self) -> None:
         self.graph.replay()
