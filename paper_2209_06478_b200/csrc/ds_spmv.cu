@@ -1138,7 +1138,6 @@ __global__ void __launch_bounds__(256, 1)   // 1 CTA/SM: registers for all 27 ga
     dia_pipe(int nrows, int ncols, int ndiags_rt, const int* __restrict__ offsets,
              const double* __restrict__ vals, const double* __restrict__ x, double* y,
              DiaPipeCfg cfg, DotOut dot) {
-  if (dot.skip()) return;
   extern __shared__ __align__(128) unsigned char smem[];
   const int nd = ND > 0 ? ND : ndiags_rt;
   const int T = cfg.T, S = cfg.S;
@@ -1164,6 +1163,17 @@ __global__ void __launch_bounds__(256, 1)   // 1 CTA/SM: registers for all 27 ga
                        reinterpret_cast<double*>(stage0 + (size_t)s * cfg.stage_bytes), &full[s],
                        pol);
     }
+  // Programmatic dependent launch (the CG step): the matrix prefetch above
+  // depends on nothing the previous kernel writes; everything below does
+  // (x, the guard, y and the partials the previous kernel reads).  A no-op
+  // for a normal launch.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (dot.skip()) {   // converged: drain the issued copies before exiting
+    if (tid == 0)
+      for (int s = 0; s < S; ++s)
+        if (blockIdx.x + (int64_t)s * G < ntiles) mbar_wait(&full[s], 0);
+    return;
+  }
   double dsum = 0.0;
   int s = 0;
   uint32_t ph = 0;
@@ -1261,6 +1271,25 @@ static int dia_pipe_launch(int64_t nrows, int64_t ncols, int ndiags, const int* 
   auto k = dia_pipe<A, F, ND>;
   int rc = allow_dynamic_smem(reinterpret_cast<const void*>(k), smem);
   if (rc) return rc;
+  static int no_pdl = -1;
+  if (no_pdl < 0) no_pdl = getenv("DS_NO_PDL") ? 1 : 0;
+  if (F && d.partials_only && !no_pdl) {
+    // single-partition CG step: may start while the previous kernel (the
+    // fused update/direction) finishes -- the kernel waits (griddepcontrol)
+    // before touching anything that kernel writes
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3((unsigned)grid);
+    lc.blockDim = dim3((unsigned)cfg.T);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    DS_CUDA(cudaLaunchKernelEx(&lc, k, (int)nrows, (int)ncols, ndiags, off, val, x, y, cfg, d));
+    return DS_OK;
+  }
   k<<<(unsigned)grid, cfg.T, smem, st>>>((int)nrows, (int)ncols, ndiags, off, val, x, y, cfg, d);
   DS_LAUNCH_CHECK("dia_pipe");
   return DS_OK;

@@ -628,6 +628,10 @@ __global__ void __launch_bounds__(kVecBlock)
   v = block_sum<kVecBlock>(v, sh);
   if (threadIdx.x == 0) rr_parts[blockIdx.x] = v;
   grid_barrier(bar_count, bar_gen);
+  // the next SpMV (launched with programmatic stream serialization) may now
+  // be scheduled: it prefetches matrix tiles and waits for this grid before
+  // reading p
+  asm volatile("griddepcontrol.launch_dependents;");
   // direction: every block reduces the G partials in the same order
   double t = 0.0;
   for (int i = threadIdx.x; i < (int)gridDim.x; i += kVecBlock) t = add(t, __ldcg(rr_parts + i));
