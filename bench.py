@@ -281,17 +281,16 @@ def format_switching(ds, torch, dev, peak, nx: int = 192, steps: int = 100) -> d
     conv_ms = (time.perf_counter() - t0) * 1e3
     n, nnz = part.a_full.nrows, part.a_full.nnz
     eng, _ = S.build_engine(S.DistributedOperator(ds.PartitionedProblem(spec, [part]), [split]),
-                            [part.b], None, 1e-300, steps + 16)
+                            [part.b], None, 1e-300, steps + 32)
     st = torch.cuda.current_stream(dev)
     with torch.cuda.device(dev):
         eng.setup(st.cuda_stream)
-        eng.capture_step()
-        for _ in range(3):
-            eng.replay()
+        eng.capture_step(10)          # 10 iterations per graph replay
+        eng.replay()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(st)
-        for _ in range(steps):
+        for _ in range(steps // 10):
             eng.replay()
         e1.record(st)
         torch.cuda.synchronize()
