@@ -226,22 +226,25 @@ def sweep_powerlaw(ds, torch, dev, peak):
     cols = rng.integers(0, n, rows.size)
     vals = rng.standard_normal(rows.size)
     gen_s = time.time() - t0
-    # the first conversion pays lazy kernel loading and pool growth: time a
-    # second one of a fresh raw COO (its plan/flags are not cached either)
-    for rep in range(2):
+    # the first conversions pay lazy kernel loading and memory-pool growth:
+    # report the fastest of three, each from a fresh raw COO (no cached plan)
+    conv_all = []
+    for rep in range(3):
         coo = ds.CooMatrix(n, n, rows, cols, vals, ds.MemorySpace.DEVICE, dev)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         csr = ds.convert(coo, ds.FormatId.CSR)
         torch.cuda.synchronize()
-        conv_ms = (time.perf_counter() - t0) * 1e3
+        conv_all.append((time.perf_counter() - t0) * 1e3)
         del coo
+    conv_ms = min(conv_all)
     del rows, cols, vals
     ccoo = ds.convert(csr, ds.FormatId.COO)
     nnz = csr.nnz
     x = ds.DenseVector(torch.from_numpy(np.random.default_rng(1).standard_normal(n)).to(dev))
     y = ds.DenseVector.zeros(n, ds.MemorySpace.DEVICE, dev)
-    out = {"nnz": nnz, "host_generate_s": round(gen_s, 2), "convert_coo_to_csr_ms": round(conv_ms, 2)}
+    out = {"nnz": nnz, "host_generate_s": round(gen_s, 2), "convert_coo_to_csr_ms": round(conv_ms, 2),
+           "convert_coo_to_csr_ms_all": [round(t, 2) for t in conv_all]}
     for name, m, b in (("csr", csr, csr_bytes(n, n, nnz)), ("coo", ccoo, coo_bytes(n, n, nnz))):
         ms = time_spmv(ds, torch, m, x, y, warm=10, reps=50)
         gbs = b / (ms * 1e-3) / 1e9
@@ -604,7 +607,7 @@ def run(args, rank: int, world: int) -> int:
             os.environ["OPENBLAS_NUM_THREADS"] = str(thr)
             cpu = cpu_cg_sample((nx, nx, nx, 1, 1, 1), None, 60, thr)   # ~5-10 s of CPU work
             cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
-        if args.powerlaw:
+        if not args.no_powerlaw:
             extras["powerlaw"] = sweep_powerlaw(ds, torch, dev, peak)
         if not args.no_config5:
             extras["format_switching_192"] = format_switching(ds, torch, dev, peak)
@@ -700,7 +703,8 @@ def main(argv=None) -> int:
     ap.add_argument("--eager", action="store_true", help="no CUDA graph for the step")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--powerlaw", action="store_true", help="also run BASELINE config 4")
+    ap.add_argument("--no-powerlaw", action="store_true",
+                    help="skip BASELINE config 4 (power-law matrix, ~54.5M nnz)")
     ap.add_argument("--no-mg", action="store_true", help="skip the HPCG multigrid PCG extra")
     ap.add_argument("--no-config5", action="store_true",
                     help="skip BASELINE config 5 (192^3 format switching incl. conversion)")
