@@ -1613,10 +1613,7 @@ __global__ void __launch_bounds__(32 * kCooWarps)
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int k = lane + 32 * i;
-        if (k < cnt) {
-          sr[k] = T.r[i];
-          sp[k] = T.v[i];
-        }
+        if (k < cnt) sp[k] = T.v[i];
       }
       // segment heads from registers: position k = lane + 32 i, its
       // predecessor is lane-1 of round i (lane 31 of round i-1 for lane 0);
@@ -1630,7 +1627,11 @@ __global__ void __launch_bounds__(32 * kCooWarps)
         const int k = lane + 32 * i;
         const bool head = (k < cnt) && (k == 0 || T.r[i] != prev_r);
         const unsigned m = __ballot_sync(0xffffffffu, head);
-        if (head) sg[nseg + __popc(m & ((1u << lane) - 1u))] = k;
+        if (head) {   // segment start and its row (rows only at heads: 1/8 the stores)
+          const int si = nseg + __popc(m & ((1u << lane) - 1u));
+          sg[si] = k;
+          sr[si] = T.r[i];
+        }
         nseg += __popc(m);
       }
       if (lane == 0) sg[nseg] = cnt;
@@ -1644,7 +1645,7 @@ __global__ void __launch_bounds__(32 * kCooWarps)
       double last_acc = 0.0;
       for (int sgi = lane; sgi < nseg; sgi += 32) {
         const int hs = sg[sgi], he = sg[sgi + 1];
-        const int row = sr[hs];
+        const int row = sr[sgi];
         const bool cont = (sgi == 0 && row == carry_row);
         double acc = cont ? carry : 0.0;
         int k = hs;
@@ -1653,7 +1654,7 @@ __global__ void __launch_bounds__(32 * kCooWarps)
           acc = add(add(add(add(acc, p0), p1), p2), p3);
         }
         for (; k < he; ++k) acc = add(acc, sp[k]);
-        const int prev = (sgi == 0) ? prev_row : sr[sg[sgi - 1]];
+        const int prev = (sgi == 0) ? prev_row : sr[sgi - 1];
         if (!cont) coo_fill_gap<ACCUM>(y, prev + 1, row);
         if (sgi == nseg - 1) {
           last_row = row;
