@@ -1437,14 +1437,17 @@ int launch_dia(int64_t nrows, int64_t ncols, int ndiags, const int* off, const d
   const bool aligned = (reinterpret_cast<uintptr_t>(val) & 15) == 0;
   int T, S, ctas;
   dia_shape(ndiags, &T, &S, &ctas);
-  static int no_xw = -1;
-  if (no_xw < 0) no_xw = getenv("DS_DIA_NO_XWIN") ? 1 : 0;
+  static int no_xw = -1, force_xw = 0;
+  if (no_xw < 0) {
+    no_xw = getenv("DS_DIA_NO_XWIN") ? 1 : 0;
+    force_xw = getenv("DS_DIA_XWIN_FORCE") ? 1 : 0;   // tests: windows at any size
+  }
   // x windows next to the value slab (27 diagonals, 16-B aligned x)
   // The window area shrinks the L1 that the gathers of smaller grids live on
   // (104^3: 43 -> 45.5 us standalone, 44 -> 50 us inside the CG step), so it
   // is only laid out for large operators (192^3: 285 -> 267 us); the kernel
   // also checks the offsets' span.
-  const bool xwin = !no_xw && ndiags == 27 && nrows >= (4ll << 20) &&
+  const bool xwin = !no_xw && ndiags == 27 && (nrows >= (4ll << 20) || force_xw) &&
                     (reinterpret_cast<uintptr_t>(x) & 15) == 0;
   const int slab = (int)((((int64_t)T * ndiags * 8) + 127) & ~127ll);
   const int wl = (T + kXwSpan + 4 + 1) & ~1;
