@@ -1,25 +1,22 @@
 // ds_spmv.cu -- SpMV over CSR / DIA / COO for sm_100a.
 //
 // Replaces the reference's format-dispatched kernels (kernels.py:102-198):
-//   _csr_spmv  kernels.py:102-119   -> csr_rows_g8 (+ csr_long_rows)
+//   _csr_spmv  kernels.py:102-119   -> csr_pipe (rows <= 33) / csr_binned / csr_long_rows*
+//                                      (csr_rows_g8 without a plan)
 //   _dia_spmv  kernels.py:122-140   -> dia_pipe (+ dia_rows_direct)
-//   _coo_spmv  kernels.py:143-163   -> coo_sorted_segments / coo_atomic
+//   _coo_spmv  kernels.py:143-163   -> coo_pipe / coo_warp_segments (+ coo_long_runs_kernel)
+//                                      / coo_atomic
 // Results are bitwise equal to the reference (see include/dynsparse_b200.h)
 // except for unsorted COO (atomics; within 1e-13 like the reference's
 // threaded COO, kernels.py:13-15).
 //
 // HBM is the roofline for every kernel here (no tensor cores: SpMV is not a
-// dense contraction).  The design goals per format:
-//   CSR: 8 lanes per row (the exact numpy pairwise structure), all loads of a
-//        row issued before the dependent add chain; matrix arrays streamed
-//        with L1::no_allocate, x gathered through L1/L2 (x stays L2-resident).
-//   DIA: persistent CTAs stream (T rows x ndiags) value slabs into a ring of
-//        shared-memory stages with 1-D TMA bulk copies (cp.async.bulk +
-//        mbarrier, L2 evict_first); each thread walks its row from shared
-//        memory (odd row stride in 8-B words -> conflict-free) and gathers x.
-//   COO: blocks own row-aligned entry ranges; entries are staged to shared
-//        memory with their products, then one thread per row segment sums
-//        sequentially (np.bincount order), carrying across tiles.
+// dense contraction).  The common design: persistent
+// CTAs stream their tiles' matrix arrays into a ring of shared-memory stages
+// with 1-D TMA bulk copies (cp.async.bulk + mbarrier transaction counts, L2
+// evict_first so x stays L2-resident); one thread per row copies its entries
+// to registers, issues every gather, and the CTA releases the stage before
+// the exact (numpy-order) sums run from registers.
 #include <stdlib.h>
 
 #include <algorithm>
@@ -1499,10 +1496,6 @@ int launch_dia(int64_t nrows, int64_t ncols, int ndiags, const int* off, const d
 
 // ===================================================================== COO ==
 
-constexpr int kCooBlock = 256;
-constexpr int kCooTile = 2048;            // entries staged per tile
-constexpr int kCooPerBlock = 4 * kCooTile; // nominal entries per block
-
 // First entry index >= k that starts a row (rows sorted); k in [0, nnz].
 // Called by one full warp: 32 row ids per step, ballot for the first change,
 // so a boundary inside a row costs ceil(row_len / 32) coalesced loads.
@@ -1524,137 +1517,6 @@ __device__ __forceinline__ int64_t coo_row_start_at_or_after_warp(const int* row
 template <bool ACCUM>
 __device__ __forceinline__ void coo_fill_gap(double* y, int from, int to) {
   for (int r = from; r < to; ++r) y[r] = ACCUM ? add(y[r], 0.0) : 0.0;  // +0.0 either way
-}
-
-template <bool ACCUM>
-__global__ void __launch_bounds__(kCooBlock)
-    coo_sorted_segments(int nrows, int64_t nnz, const int* __restrict__ rows,
-                        const int* __restrict__ cols, const double* __restrict__ vals,
-                        const double* __restrict__ x, double* y, const int* guard,
-                        int plus_zero) {
-  if (guard && *guard) return;
-  __shared__ int s_row[kCooTile];
-  __shared__ double s_p[kCooTile];
-  __shared__ int s_seg[kCooTile + 1];
-  __shared__ int s_wsum[kCooBlock / 32];
-  __shared__ int s_nseg;
-  __shared__ double s_carry;
-  __shared__ int s_carry_row, s_prev_row;
-  __shared__ int64_t s_start, s_end;
-  __shared__ int s_R0, s_R1;
-  const int tid = threadIdx.x;
-  if (tid < 32) {  // warp 0: row-aligned bounds of this block's entry range
-    const int64_t st = coo_row_start_at_or_after_warp(rows, nnz,
-                                                      (int64_t)blockIdx.x * kCooPerBlock);
-    const int64_t en = coo_row_start_at_or_after_warp(rows, nnz,
-                                                      (int64_t)(blockIdx.x + 1) * kCooPerBlock);
-    if (tid == 0) {
-      s_start = st;
-      s_end = en;
-      s_R0 = (st == 0) ? 0 : (st < nnz ? rows[st] : nrows);
-      s_R1 = (en < nnz) ? rows[en] : nrows;
-      s_carry_row = -1;
-      s_carry = 0.0;
-      s_prev_row = s_R0 - 1;
-    }
-  }
-  __syncthreads();
-  const int64_t start = s_start, end = s_end;
-  const int R1 = s_R1;
-  for (int64_t t0 = start; t0 < end; t0 += kCooTile) {
-    const int cnt = (int)min64(kCooTile, end - t0);
-    {
-      // all loads of the thread's entries first (clamped, unpredicated), then
-      // the gathers, then the stores: PER independent chains in flight
-      constexpr int PER = kCooTile / kCooBlock;
-      int rr[PER], cc[PER];
-      double vv[PER];
-#pragma unroll
-      for (int q = 0; q < PER; ++q) {
-        const int k = min(tid + q * kCooBlock, cnt - 1);
-        rr[q] = ld_stream(rows + t0 + k);
-        cc[q] = ld_stream(cols + t0 + k);
-        vv[q] = ld_stream(vals + t0 + k);
-      }
-#pragma unroll
-      for (int q = 0; q < PER; ++q) vv[q] = mul(vv[q], ld_gather(x + cc[q]));
-#pragma unroll
-      for (int q = 0; q < PER; ++q) {
-        const int k = tid + q * kCooBlock;
-        if (k < cnt) {
-          s_row[k] = rr[q];
-          s_p[k] = vv[q];
-        }
-      }
-    }
-    __syncthreads();
-    // segment heads: 8 consecutive entries per thread, block exclusive scan
-    constexpr int PER = kCooTile / kCooBlock;
-    int myh = 0;
-    const int k0 = tid * PER;
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-      const int k = k0 + q;
-      if (k < cnt && (k == 0 || s_row[k] != s_row[k - 1])) ++myh;
-    }
-    int incl = myh;
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, incl, o);
-      if ((tid & 31) >= o) incl += t;
-    }
-    if ((tid & 31) == 31) s_wsum[tid >> 5] = incl;
-    __syncthreads();
-    int wpre = 0;
-    for (int w = 0; w < (tid >> 5); ++w) wpre += s_wsum[w];
-    int pos = wpre + incl - myh;
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-      const int k = k0 + q;
-      if (k < cnt && (k == 0 || s_row[k] != s_row[k - 1])) s_seg[pos++] = k;
-    }
-    if (tid == kCooBlock - 1) {
-      s_nseg = wpre + incl;
-      s_seg[wpre + incl] = cnt;
-    }
-    __syncthreads();
-    const int nseg = s_nseg;
-    const bool more = (t0 + cnt < end);
-    const int next_row = more ? rows[t0 + cnt] : -1;
-    const double carry_in = s_carry;       // read before any thread rewrites it
-    const int carry_row_in = s_carry_row;
-    const int prev_row_in = s_prev_row;
-    __syncthreads();
-    for (int s = tid; s < nseg; s += kCooBlock) {
-      const int hs = s_seg[s], he = s_seg[s + 1];
-      const int r = s_row[hs];
-      const bool cont = (s == 0 && r == carry_row_in);
-      double acc = cont ? carry_in : 0.0;
-      int k = hs;
-      for (; k + 4 <= he; k += 4) {  // 4 independent shared loads per dependent chain step
-        const double p0 = s_p[k], p1 = s_p[k + 1], p2 = s_p[k + 2], p3 = s_p[k + 3];
-        acc = add(add(add(add(acc, p0), p1), p2), p3);
-      }
-      for (; k < he; ++k) acc = add(acc, s_p[k]);
-      const int prev = (s == 0) ? prev_row_in : s_row[s_seg[s - 1]];
-      if (!cont) coo_fill_gap<ACCUM>(y, prev + 1, r);
-      if (s == nseg - 1 && more && next_row == r) {
-        s_carry = acc;  // row continues in the next tile
-        s_carry_row = r;
-      } else {
-        double out = ACCUM ? add(y[r], acc) : acc;
-        if (plus_zero) out = add(out, 0.0);
-        y[r] = out;
-      }
-    }
-    __syncthreads();
-    if (tid == 0) {
-      const int last = s_row[s_seg[nseg - 1]];
-      s_prev_row = last;
-      if (!(more && next_row == last)) s_carry_row = -1;
-    }
-    __syncthreads();
-  }
-  if (tid == 0) coo_fill_gap<ACCUM>(y, s_prev_row + 1, R1);
 }
 
 // ---------------------------------------------------------------------------
@@ -1899,7 +1761,6 @@ struct CooPipeCfg {
   int E;            // entries per tile (multiple of T)
   int S;            // stages (<= 8)
   int stage_bytes;  // 16 * (E + 8), 128-B multiple
-  int dry;          // tuning only: stream the tiles, compute nothing
 };
 
 __device__ __forceinline__ void coo_pipe_issue(const int* __restrict__ rows,
@@ -2018,17 +1879,6 @@ __global__ void __launch_bounds__(T, MINB)
     const int* s_c = reinterpret_cast<const int*>(st) + (E + 8) + off;
     const double* s_v = reinterpret_cast<const double*>(st + 8 * (size_t)(E + 8)) + off;
     mbar_wait(&full[s], ph);
-    if (cfg.dry) {
-      __syncthreads();
-      if (tid == 0 && k + S < ntiles)
-        coo_pipe_issue(rows, cols, vals, nnz, s0 + (k + S) * E, min64(s0 + (k + S + 1) * E, s1),
-                       E, st, &full[s], pol);
-      if (++s == S) {
-        s = 0;
-        ph ^= 1u;
-      }
-      continue;
-    }
     const bool last = (k == ntiles - 1);
     const int rlast = s_r[cnt - 1];
     const int hi = last ? Rend : rlast + 1;
@@ -2126,7 +1976,6 @@ static int coo_pipe_launch1(int64_t nrows, int64_t nnz, const int* rows, const i
   cfg.E = E;
   cfg.S = S;
   cfg.stage_bytes = (int)((16 * (int64_t)(cfg.E + 8) + 127) & ~127ll);
-  cfg.dry = getenv("DS_COO_DRY") ? 1 : 0;
   const size_t smem = 128 + (size_t)cfg.S * cfg.stage_bytes;
   if (smem > (size_t)max_dynamic_smem() - 1024) return DS_ERR_NOT_SUPPORTED;
   int64_t grid = (int64_t)sm_count() * ctas;
@@ -2208,19 +2057,16 @@ int launch_coo(int64_t nrows, int64_t nnz, const int* rows, const int* cols, con
                cudaStream_t st, bool plus_zero, const int* long_runs, int n_long) {
   if (nrows == 0) return DS_OK;
   if (nnz == 0) return launch_empty_matrix(nrows, y, accum, guard, st);
-  static int coo_v1 = -1, coo_warp = -1;
-  if (coo_v1 < 0) {
-    coo_v1 = getenv("DS_COO_V1") ? 1 : 0;
-    coo_warp = getenv("DS_COO_WARP") ? 1 : 0;
-  }
+  static int coo_warp = -1;
+  if (coo_warp < 0) coo_warp = getenv("DS_COO_WARP") ? 1 : 0;
   // thread-per-row pipeline for row-sorted COO whose rows fit its 27-wide
   // register path (the stencil); long rows (power-law) keep the warp kernel,
   // whose parallel products leave only the inherent sequential add chain
-  if (sorted && !coo_v1 && !coo_warp && max_len >= 1 && max_len <= 27) {
+  if (sorted && !coo_warp && max_len >= 1 && max_len <= 27) {
     const int rc = coo_pipe_launch(nrows, nnz, rows, cols, vals, x, y, accum, guard, plus_zero, st);
     if (rc != DS_ERR_NOT_SUPPORTED) return rc;
   }
-  if (sorted && !coo_v1) {
+  if (sorted) {
     int64_t blocks = ceil_div(ceil_div(nnz, kCooWarpChunk), kCooWarps);
     const int64_t cap = (int64_t)sm_count() * 8;
     if (blocks > cap) blocks = cap;
@@ -2259,17 +2105,6 @@ int launch_coo(int64_t nrows, int64_t nnz, const int* rows, const int* cols, con
           split ? long_runs : nullptr, split ? n_long : 0);
     DS_LAUNCH_CHECK("coo_warp_segments");
     if (split) DS_CUDA(cudaStreamWaitEvent(st, joined, 0));
-    return DS_OK;
-  }
-  if (sorted) {
-    const int64_t blocks = nnz == 0 ? 1 : ceil_div(nnz, kCooPerBlock);
-    if (accum)
-      coo_sorted_segments<true><<<(unsigned)blocks, kCooBlock, 0, st>>>((int)nrows, nnz, rows,
-                                                                        cols, vals, x, y, guard, (int)plus_zero);
-    else
-      coo_sorted_segments<false><<<(unsigned)blocks, kCooBlock, 0, st>>>((int)nrows, nnz, rows,
-                                                                         cols, vals, x, y, guard, (int)plus_zero);
-    DS_LAUNCH_CHECK("coo_sorted_segments");
     return DS_OK;
   }
   const unsigned g = (unsigned)min64(ceil_div(nrows, 256), (int64_t)sm_count() * 8);

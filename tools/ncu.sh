@@ -7,7 +7,7 @@ mkdir -p $OUT
 NCU=${NCU:-ncu}
 $NCU --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
     --csv --log-file $OUT/launches.csv python tools/profile_kernels.py > $OUT/launches.log 2>&1
-for k in ${KERNELS:-dia_slab_tma csr_rows_g8 coo_sorted_segments cg_update_kernel cg_direction_kernel}; do
+for k in ${KERNELS:-dia_pipe csr_pipe coo_pipe cg_update_direction_fused}; do
   $NCU --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 \
       -o $OUT/prof_$k -f python tools/profile_kernels.py > $OUT/prof_$k.log 2>&1
 done
