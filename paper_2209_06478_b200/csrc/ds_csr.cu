@@ -1,0 +1,1126 @@
+// ds_csr.cu -- CSR SpMV for sm_100a (kernels.py:102-119 _csr_spmv; np.add.reduceat order).
+//
+// csr_pipe: persistent TMA pipeline, one thread per row (rows <= 33);
+// csr_binned / csr_long_rows_warp / csr_long_rows for irregular matrices by
+// length bin (ds_csr_bins); csr_rows_g8 when no plan is given.  Bitwise equal
+// to the reference: see DESIGN.md section 4 and include/dynsparse_b200.h.
+#include <stdlib.h>
+
+#include "ds_common.cuh"
+#include "ds_kernels.cuh"
+
+namespace ds {
+
+// ===================================================================== CSR ==
+
+// Sum of one row in np.add.reduceat order, computed by an aligned 8-lane
+// group; m = row_len - 1 addends after the first product, m <= 128 handled as
+// one pairwise leaf; longer rows walk the recursion (slow path, used only
+// when no long-row plan was supplied).
+struct CsrElem {
+  const int* col;
+  const double* val;
+  const double* x;
+  int64_t base;
+  __device__ __forceinline__ double operator()(int64_t i) const {
+    return mul(ld_stream(val + base + i), ld_gather(x + ld_stream(col + base + i)));
+  }
+};
+
+// Leaf (m <= 128) with loads batched 4 rounds at a time so every lane has up
+// to 4 independent col->x chains in flight before the dependent adds.
+__device__ __forceinline__ double csr_leaf_g8(const int* __restrict__ col,
+                                              const double* __restrict__ val,
+                                              const double* __restrict__ x, int64_t base, int m,
+                                              int lane8, unsigned mask) {
+  const int full = m & ~7;
+  const int nfull = full >> 3;                 // full rounds of 8
+  const int rounds = (m + 7) >> 3;             // rounds incl. the tail round
+  double r = 0.0, tail = 0.0;
+  for (int k0 = 0; k0 < rounds; k0 += 4) {
+    int c[4];
+    double v[4], a[4];
+    // unpredicated loads of a clamped index (m >= 1 here): every lane keeps
+    // 4 col->x chains in flight; products of clamped slots are never used
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      const int i = min(lane8 + 8 * (k0 + kk), m - 1);
+      c[kk] = ld_stream(col + base + i);
+      v[kk] = ld_stream(val + base + i);
+    }
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) a[kk] = mul(v[kk], ld_gather(x + c[kk]));
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      const int k = k0 + kk;
+      if (k < nfull) {
+        r = (k == 0) ? a[kk] : add(r, a[kk]);
+      } else if (k == nfull) {
+        tail = a[kk];  // i == full + lane8 (zero when lane8 >= m - full)
+      }
+    }
+  }
+  double res;
+  if (full > 0) {
+    r = add(r, __shfl_xor_sync(mask, r, 1, 8));
+    r = add(r, __shfl_xor_sync(mask, r, 2, 8));
+    r = add(r, __shfl_xor_sync(mask, r, 4, 8));
+    res = r;
+  } else {
+    res = -0.0;  // numpy's pairwise_sum identity for n < 8
+  }
+  const int ntail = m - full;
+  for (int t = 0; t < ntail; ++t) res = add(res, __shfl_sync(mask, tail, t, 8));
+  return res;
+}
+
+// Short-row leaf (m <= 32: one batch of 4 rounds) split into phases so two
+// rows can be interleaved: all loads of both rows are issued before either
+// row's dependent gathers and adds.
+struct ShortLeaf {
+  int c[4];
+  double v[4];
+  double a[4];
+  int c0;
+  double v0;
+};
+
+__device__ __forceinline__ void short_leaf_load(const int* __restrict__ col,
+                                                const double* __restrict__ val, int start,
+                                                int len, int lane8, ShortLeaf& L) {
+  const int m = len - 1;  // addends after p[first]
+  // clamped indices keep every load unpredicated; L1-allocating loads make
+  // the clamped duplicates (rows shorter than 33) hit L1 instead of L2
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) {
+    const int i = max(min(lane8 + 8 * kk, m - 1), 0);   // clamped: always in the row
+    L.c[kk] = __ldg(col + start + 1 + i);
+    L.v[kk] = __ldg(val + start + 1 + i);
+  }
+  L.c0 = ld_stream(col + start);
+  L.v0 = ld_stream(val + start);
+}
+
+__device__ __forceinline__ void short_leaf_gather(const double* __restrict__ x, ShortLeaf& L) {
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) L.a[kk] = mul(L.v[kk], ld_gather(x + L.c[kk]));
+  L.v0 = mul(L.v0, ld_gather(x + L.c0));   // p[first]
+}
+
+// y-value of a row with 1 <= len <= 33 (bitwise np.add.reduceat order)
+__device__ __forceinline__ double short_leaf_finish(int len, int lane8, unsigned mask,
+                                                    const ShortLeaf& L) {
+  const int m = len - 1;
+  const int full = m & ~7, nfull = full >> 3;
+  double r = 0.0, tail = 0.0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (k < nfull) r = (k == 0) ? L.a[k] : add(r, L.a[k]);
+    else if (k == nfull) tail = L.a[k];
+  }
+  double res;
+  if (full > 0) {
+    r = add(r, __shfl_xor_sync(mask, r, 1, 8));
+    r = add(r, __shfl_xor_sync(mask, r, 2, 8));
+    r = add(r, __shfl_xor_sync(mask, r, 4, 8));
+    res = r;
+  } else {
+    res = -0.0;
+  }
+  const int ntail = m - full;
+  for (int t = 0; t < ntail; ++t) res = add(res, __shfl_sync(mask, tail, t, 8));
+  return add(L.v0, res);
+}
+
+// Leaf (m <= 128) for the long-row kernels, which are latency bound (a few
+// rows, each a chain of leaves): every lane issues ALL its column / value
+// loads, then all its gathers, before the first add -- one memory round trip
+// per leaf instead of one per batch of 4 rounds.
+__device__ __forceinline__ double csr_leaf_g8_all(const int* __restrict__ col,
+                                                  const double* __restrict__ val,
+                                                  const double* __restrict__ x, int64_t base,
+                                                  int m, int lane8, unsigned mask) {
+  const int full = m & ~7, nfull = full >> 3;
+  int c[16];
+  double v[16], a[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    const int i = min(lane8 + 8 * k, m - 1);
+    c[k] = ld_stream(col + base + i);
+    v[k] = ld_stream(val + base + i);
+  }
+#pragma unroll
+  for (int k = 0; k < 16; ++k) a[k] = mul(v[k], ld_gather(x + c[k]));
+  double r = a[0], tail = 0.0;
+#pragma unroll
+  for (int k = 1; k < 16; ++k) {
+    if (k < nfull) r = add(r, a[k]);
+  }
+#pragma unroll
+  for (int k = 0; k < 16; ++k)
+    if (k == nfull) tail = a[k];
+  double res;
+  if (full > 0) {
+    r = add(r, __shfl_xor_sync(mask, r, 1, 8));
+    r = add(r, __shfl_xor_sync(mask, r, 2, 8));
+    r = add(r, __shfl_xor_sync(mask, r, 4, 8));
+    res = r;
+  } else {
+    res = -0.0;
+  }
+  const int ntail = m - full;
+  for (int t = 0; t < ntail; ++t) res = add(res, __shfl_sync(mask, tail, t, 8));
+  return res;
+}
+
+// Recursion for m > 128 by one 8-lane group (no plan): group-uniform DFS.
+__device__ double csr_group_pairwise(const int* __restrict__ col, const double* __restrict__ val,
+                                     const double* __restrict__ x, int64_t base, int64_t m,
+                                     int lane8, unsigned mask) {
+  if (m <= 128) return csr_leaf_g8(col, val, x, base, (int)m, lane8, mask);
+  struct Frame {
+    int64_t lo, n;
+    int expanded;
+  };
+  Frame st[64];
+  double vs[64];
+  int ft = 0, vt = 0;
+  st[ft++] = {0, m, 0};
+  while (ft > 0) {
+    Frame f = st[--ft];
+    if (f.n <= 128) {
+      vs[vt++] = csr_leaf_g8(col, val, x, base + f.lo, (int)f.n, lane8, mask);
+    } else if (!f.expanded) {
+      int64_t n2 = f.n / 2;
+      n2 -= n2 % 8;
+      st[ft++] = {f.lo, f.n, 1};
+      st[ft++] = {f.lo + n2, f.n - n2, 0};
+      st[ft++] = {f.lo, n2, 0};
+    } else {
+      double b = vs[--vt];
+      double a = vs[--vt];
+      vs[vt++] = add(a, b);
+    }
+  }
+  return vs[0];
+}
+
+constexpr int kCsrBlock = 256;
+constexpr int kLongRow = 129;  // rows longer than this need the recursion
+constexpr int kSub = 8192;     // <= 128 leaves per subtree / warp-kernel row limit
+constexpr int kMaxLeaves = 160;
+
+// One 8-lane group per PAIR of consecutive rows; grid-stride over pairs.
+// Rows of <= 33 entries (the stencil's 8..27, the power-law's typical 6..33)
+// take the interleaved fast path; longer ones the general leaf / recursion.
+template <bool ACCUM, bool SKIP_LONG, bool FUSE_DOT>
+__device__ __forceinline__ void csr_emit(int row, int len, double sres, double* y,
+                                         const DotOut& dot, double& dsum) {
+  double out = ACCUM ? add(y[row], sres) : sres;
+  if (dot.plus_zero) out = add(out, 0.0);
+  y[row] = out;
+  if (FUSE_DOT) dsum = add(dsum, mul(dot.other[row], out));
+}
+
+template <bool ACCUM, bool SKIP_LONG, bool FUSE_DOT>
+__device__ __forceinline__ void csr_row_general(int row, int start, int len,
+                                                const int* __restrict__ col,
+                                                const double* __restrict__ val,
+                                                const double* __restrict__ x, double* y,
+                                                int lane8, unsigned mask, const DotOut& dot,
+                                                double& dsum) {
+  if (SKIP_LONG && len > kLongRow) return;  // the long-row kernel owns it
+  double res = 0.0, p0 = 0.0;
+  if (len > 0) {
+    if (lane8 == 0) p0 = mul(ld_stream(val + start), ld_gather(x + ld_stream(col + start)));
+    if (len <= kLongRow)
+      res = csr_leaf_g8_all(col, val, x, (int64_t)start + 1, len - 1, lane8, mask);
+    else
+      res = csr_group_pairwise(col, val, x, (int64_t)start + 1, len - 1, lane8, mask);
+  }
+  if (lane8 == 0) csr_emit<ACCUM, SKIP_LONG, FUSE_DOT>(row, len, len > 0 ? add(p0, res) : 0.0,
+                                                      y, dot, dsum);
+}
+
+template <bool ACCUM, bool SKIP_LONG, bool FUSE_DOT>
+__global__ void __launch_bounds__(kCsrBlock)
+    csr_rows_g8(int nrows, const int* __restrict__ off, const int* __restrict__ col,
+                const double* __restrict__ val, const double* __restrict__ x, double* y,
+                DotOut dot) {
+  if (dot.skip()) return;
+  const int lane8 = threadIdx.x & 7;
+  const unsigned mask = 0xffu << (threadIdx.x & 24);
+  const int groups_per_grid = (gridDim.x * kCsrBlock) >> 3;
+  const int npairs = (nrows + 1) >> 1;
+  double dsum = 0.0;
+  for (int pr = (blockIdx.x * kCsrBlock + threadIdx.x) >> 3; pr < npairs;
+       pr += groups_per_grid) {
+    const int ra = 2 * pr, rb = ra + 1;
+    const bool has_b = rb < nrows;
+    const int sa = __ldg(off + ra), ea = __ldg(off + ra + 1);
+    const int eb = has_b ? __ldg(off + rb + 1) : ea;
+    const int la = ea - sa, lb = eb - ea;
+    if (la >= 1 && la <= 33 && lb >= 1 && lb <= 33) {
+      ShortLeaf A, B;
+      short_leaf_load(col, val, sa, la, lane8, A);
+      short_leaf_load(col, val, ea, lb, lane8, B);
+      short_leaf_gather(x, A);
+      short_leaf_gather(x, B);
+      const double ya = short_leaf_finish(la, lane8, mask, A);
+      const double yb = short_leaf_finish(lb, lane8, mask, B);
+      if (lane8 == 0) {
+        csr_emit<ACCUM, SKIP_LONG, FUSE_DOT>(ra, la, ya, y, dot, dsum);
+        csr_emit<ACCUM, SKIP_LONG, FUSE_DOT>(rb, lb, yb, y, dot, dsum);
+      }
+    } else {
+      csr_row_general<ACCUM, SKIP_LONG, FUSE_DOT>(ra, sa, la, col, val, x, y, lane8, mask, dot,
+                                                  dsum);
+      if (has_b)
+        csr_row_general<ACCUM, SKIP_LONG, FUSE_DOT>(rb, ea, lb, col, val, x, y, lane8, mask,
+                                                    dot, dsum);
+    }
+  }
+  if (FUSE_DOT) dot.finish_block<kCsrBlock>(dsum);
+}
+
+// ---------------------------------------------------------------------------
+// Binned CSR (irregular matrices).  Rows are grouped by length bin
+// (ds_csr_bins): each bin runs with its exact number of load rounds R
+// (bin b in 1..4: rows of <= 8b+1 entries -> R = b), so there is neither
+// round padding nor per-lane predication; two rows per 8-lane group keep
+// 2R load chains in flight.  Work item = a pair of consecutive rows of the
+// permuted list; items of all bins are enumerated in one grid-stride loop.
+struct CsrBins {
+  int64_t start[8];     // bin b rows = perm[start[b] .. start[b+1])
+  int64_t pair_off[8];  // cumulative work items (kBinRows[b] rows each) before bin b
+};
+// rows per work item (8-lane group) per bin: empty, R=1, R=2, R=3, R=4, general
+__constant__ int kBinRows[7] = {4, 4, 4, 2, 2, 2, 1};
+static const int kBinRowsHost[7] = {4, 4, 4, 2, 2, 2, 1};
+
+template <int R>
+__device__ __forceinline__ void binned_load(const int* __restrict__ col,
+                                            const double* __restrict__ val, int start, int len,
+                                            int lane8, int (&c)[R], double (&v)[R], int& c0,
+                                            double& v0, uint64_t pol) {
+  const int m = len - 1;
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const int i = max(min(lane8 + 8 * k, m - 1), -1);   // -1 -> p[first]: in bounds
+    c[k] = ld_hint(col + start + 1 + i, pol);
+    v[k] = ld_hint(val + start + 1 + i, pol);
+  }
+  c0 = ld_hint(col + start, pol);
+  v0 = ld_hint(val + start, pol);
+}
+
+template <int R>
+__device__ __forceinline__ double binned_finish(int len, int lane8, unsigned mask,
+                                                const double (&a)[R], double p0) {
+  const int m = len - 1;
+  const int full = m & ~7, nfull = full >> 3;
+  double r = 0.0, tail = 0.0;
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    if (k < nfull) r = (k == 0) ? a[k] : add(r, a[k]);
+    else if (k == nfull) tail = a[k];
+  }
+  double res;
+  if (full > 0) {
+    r = add(r, __shfl_xor_sync(mask, r, 1, 8));
+    r = add(r, __shfl_xor_sync(mask, r, 2, 8));
+    r = add(r, __shfl_xor_sync(mask, r, 4, 8));
+    res = r;
+  } else {
+    res = -0.0;
+  }
+  const int ntail = m - full;
+  for (int t = 0; t < ntail; ++t) res = add(res, __shfl_sync(mask, tail, t, 8));
+  return add(p0, res);
+}
+
+// U rows per 8-lane group, all U*R loads and gathers issued before any
+// reduction (short rows have little work each: more rows = more MLP)
+template <int R, int U, bool ACCUM, bool FUSE_DOT>
+__device__ __forceinline__ void binned_rows(const int* rws, int nr, const int* __restrict__ off,
+                                            const int* __restrict__ col,
+                                            const double* __restrict__ val,
+                                            const double* __restrict__ x, double* y, int lane8,
+                                            unsigned mask, const DotOut& dot, double& dsum,
+                                            uint64_t pf, uint64_t pl) {
+  int st[U], ln[U], c[U][R], c0[U];
+  double v[U][R], v0[U], a[U][R], p0[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int row = rws[min(u, nr - 1)];
+    st[u] = __ldg(off + row);
+    ln[u] = __ldg(off + row + 1) - st[u];
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+    binned_load<R>(col, val, st[u], ln[u], lane8, c[u], v[u], c0[u], v0[u], pf);
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+#pragma unroll
+    for (int k = 0; k < R; ++k) a[u][k] = mul(v[u][k], ld_hint(x + c[u][k], pl));
+    p0[u] = mul(v0[u], ld_hint(x + c0[u], pl));
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const double yv = binned_finish<R>(ln[u], lane8, mask, a[u], p0[u]);
+    if (lane8 == 0 && u < nr) csr_emit<ACCUM, false, FUSE_DOT>(rws[u], ln[u], yv, y, dot, dsum);
+  }
+}
+
+template <bool ACCUM, bool FUSE_DOT>
+__global__ void __launch_bounds__(kCsrBlock, 2)
+    csr_binned(const int* __restrict__ off, const int* __restrict__ col,
+               const double* __restrict__ val, const double* __restrict__ x, double* y,
+               const int* __restrict__ perm, CsrBins bi, DotOut dot) {
+  if (dot.skip()) return;
+  const int lane8 = threadIdx.x & 7;
+  const unsigned mask = 0xffu << (threadIdx.x & 24);
+  const int64_t groups = ((int64_t)gridDim.x * kCsrBlock) >> 3;
+  const int64_t W = bi.pair_off[6];
+  const uint64_t pf = policy_first(), pl = policy_evict_last();
+  double dsum = 0.0;
+  for (int64_t w = ((int64_t)blockIdx.x * kCsrBlock + threadIdx.x) >> 3; w < W; w += groups) {
+    int b = 0;
+#pragma unroll
+    for (int k = 1; k < 6; ++k) b += (w >= bi.pair_off[k]);
+    const int U = kBinRows[b];
+    const int64_t q = bi.start[b] + (int64_t)U * (w - bi.pair_off[b]);
+    const int nr = (int)min64(U, bi.start[b + 1] - q);
+    const int* rws = perm + q;
+    switch (b) {
+      case 0:
+        if (lane8 == 0)
+          for (int u = 0; u < nr; ++u) csr_emit<ACCUM, false, FUSE_DOT>(rws[u], 0, 0.0, y, dot, dsum);
+        break;
+      case 1: binned_rows<1, 4, ACCUM, FUSE_DOT>(rws, nr, off, col, val, x, y, lane8, mask, dot, dsum, pf, pl); break;
+      case 2: binned_rows<2, 4, ACCUM, FUSE_DOT>(rws, nr, off, col, val, x, y, lane8, mask, dot, dsum, pf, pl); break;
+      case 3: binned_rows<3, 2, ACCUM, FUSE_DOT>(rws, nr, off, col, val, x, y, lane8, mask, dot, dsum, pf, pl); break;
+      case 4: binned_rows<4, 2, ACCUM, FUSE_DOT>(rws, nr, off, col, val, x, y, lane8, mask, dot, dsum, pf, pl); break;
+      default:
+        for (int u = 0; u < nr; ++u) {
+          const int row = rws[u];
+          const int sr = __ldg(off + row);
+          csr_row_general<ACCUM, true, FUSE_DOT>(row, sr, __ldg(off + row + 1) - sr, col, val, x,
+                                                 y, lane8, mask, dot, dsum);
+        }
+    }
+  }
+  if (FUSE_DOT) dot.finish_block<kCsrBlock>(dsum);
+}
+
+// ---------------------------------------------------------------------------
+// CSR v3: persistent TMA pipeline, one thread per row (the DIA design).
+//
+// Regular matrices (every row <= 33 entries: the stencil) are HBM-bound only
+// if each SM keeps enough gathers in flight; the 8-lane-group kernels above
+// hold ~1.7K per SM.  Here the matrix stream is decoupled from the gathers:
+// thread 0 copies each tile's entry range [off[r0], off[r0+T]) -- column
+// indices and values, contiguous in CSR -- into a ring of S shared-memory
+// stages with two 1-D TMA bulk copies (mbarrier transaction counts, L2
+// evict_first so x stays L2-resident), and refills a stage as soon as the
+// CTA has consumed it.  Each thread then reads its row from shared memory
+// (a row stride of 27 words / doubles is bank-conflict free) and issues all
+// LMAX gathers unpredicated (clamped to the row's last entry) before any add,
+// so 256 x LMAX gathers per SM are in flight.
+//
+// Sum order (np.add.reduceat, kernels.py:117): y = p[0] + pw(p[1..m]), m =
+// len-1, pw(n < 8) = sequential from -0.0, pw(8 <= n <= 128) = 8 strided
+// accumulators combined ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) then the n%8
+// tail.  With every index static (register arrays) this is: r[j] = p[1+j]
+// (+ p[1+j+8q] while 8q < full), res = full ? combine(r) : -0.0, then
+// res += p[k] for full < k <= m ascending -- exactly the tail of either case.
+// Rows longer than LMAX (<= kLongRow) take the serial emulation; a tile whose
+// entries do not fit a stage ("fat") is read straight from global memory.
+struct CsrPipeCfg {
+  int T;            // rows per tile == blockDim.x
+  int S;            // stages (<= 8)
+  int cap;          // entries per stage (multiple of 4)
+  int stage_bytes;  // 4*cap (cols) + 8*cap (vals), 128-B multiple
+  int skip_above;   // SKIP_LONG: rows longer than this are left to other kernels
+  int hint;         // gather x with L2 evict_last (irregular matrices: x re-used at random)
+};
+
+struct CsrPipeHdr {  // per stage, written by thread 0 before its arrive (release)
+  int bc, bv;        // first staged col / val entry (aligned down to 16 B)
+  int fat;
+  int pad;
+};
+
+__device__ __forceinline__ void csr_pipe_issue(const int* __restrict__ col,
+                                               const double* __restrict__ val, int nnz, int e0,
+                                               int e1, const CsrPipeCfg& cfg, unsigned char* st,
+                                               CsrPipeHdr* h, uint64_t* bar, uint64_t pol) {
+  const int bc = e0 & ~3, bv = e0 & ~1;
+  // copy up to the 16-B aligned end: the few entries past e1 belong to the
+  // next tile (never read here).  Only where that would leave the arrays
+  // (the last tile) is the sub-16-byte tail copied by hand -- a dependent
+  // global load on thread 0, so it is kept off every other tile.
+  const int cu = (e1 + 3) & ~3, vu = (e1 + 1) & ~1;
+  const bool fat = (cu - bc) > cfg.cap;
+  h->bc = bc;
+  h->bv = bv;
+  h->fat = fat;
+  uint32_t bytes = 0;
+  int* s_col = reinterpret_cast<int*>(st);
+  double* s_val = reinterpret_cast<double*>(st + 4 * (size_t)cfg.cap);
+  int cb = 0, vb = 0;
+  if (!fat) {
+    cb = cu <= nnz ? cu : (e1 & ~3);
+    vb = vu <= nnz ? vu : (e1 & ~1);
+    for (int e = cb; e < e1; ++e) s_col[e - bc] = col[e];
+    if (vb < e1) s_val[vb - bv] = val[vb];
+    bytes = 4u * (uint32_t)(cb - bc) + 8u * (uint32_t)(vb - bv);
+  }
+  fence_proxy_async();
+  mbar_arrive_expect_tx(bar, bytes);
+  if (!fat) {
+    if (cb > bc) bulk_g2s(s_col, col + bc, 4u * (uint32_t)(cb - bc), bar, pol);
+    if (vb > bv) bulk_g2s(s_val, val + bv, 8u * (uint32_t)(vb - bv), bar, pol);
+  }
+}
+
+// One row with 1 <= len <= LMAX in two phases around the stage release:
+// load() copies the row's columns and values into registers and issues all
+// LMAX gathers (unpredicated, clamped to the row's last entry); finish()
+// forms the products and the exact np.add.reduceat sum.
+template <int LMAX>
+struct CsrRowRegs {
+  double v[LMAX];
+  double p[LMAX];
+
+  template <bool HINT, class IP, class VP>
+  __device__ __forceinline__ void load(IP cp, VP vp, int len, const double* __restrict__ x,
+                                       uint64_t pl) {
+    const int last = len - 1;
+    int c[LMAX];
+#pragma unroll
+    for (int k = 0; k < LMAX; ++k) c[k] = cp[min(k, last)];
+    // irregular matrices (HINT): predicated gathers -- clamped duplicates of
+    // short rows would multiply the random L2 sector traffic that bounds them
+#pragma unroll
+    for (int k = 0; k < LMAX; ++k)
+      p[k] = HINT ? (k <= last ? ld_hint(x + c[k], pl) : 0.0) : ld_gather(x + c[k]);
+#pragma unroll
+    for (int k = 0; k < LMAX; ++k) v[k] = vp[min(k, last)];
+  }
+
+  __device__ __forceinline__ double finish(int len) {
+#pragma unroll
+    for (int k = 0; k < LMAX; ++k) p[k] = mul(v[k], p[k]);
+    const int m = len - 1, full = m & ~7;
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = (1 + j < LMAX) ? p[(1 + j) % LMAX] : 0.0;
+#pragma unroll
+    for (int q = 1; 1 + 8 * q < LMAX; ++q)
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (1 + j + 8 * q < LMAX && 8 * q < full) r[j] = add(r[j], p[(1 + j + 8 * q) % LMAX]);
+    double res = -0.0;
+    if (full > 0)
+      res = add(add(add(r[0], r[1]), add(r[2], r[3])), add(add(r[4], r[5]), add(r[6], r[7])));
+#pragma unroll
+    for (int k = 1; k < LMAX; ++k)
+      if (k > full && k <= m) res = add(res, p[k]);
+    return add(p[0], res);
+  }
+};
+
+template <class IP, class VP>
+__device__ __noinline__ double csr_row_serial(IP cp, VP vp, int len,
+                                              const double* __restrict__ x) {
+  const double p0 = mul(vp[0], ld_gather(x + cp[0]));
+  const double rest =
+      pairwise_serial(len - 1, [&](int64_t i) { return mul(vp[1 + i], ld_gather(x + cp[1 + i])); });
+  return add(p0, rest);
+}
+
+template <int LMAX, bool ACCUM, bool SKIP_LONG, bool FUSE_DOT>
+__global__ void __launch_bounds__(256, 1)
+    csr_pipe(int nrows, int nnz, const int* __restrict__ off, const int* __restrict__ col,
+             const double* __restrict__ val, const double* __restrict__ x, double* y,
+             CsrPipeCfg cfg, DotOut dot) {
+  if (dot.skip()) return;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);                   // <= 8 barriers
+  CsrPipeHdr* hdr = reinterpret_cast<CsrPipeHdr*>(smem + 64);            // <= 8 headers
+  unsigned char* stage0 = smem + 256;
+  const int tid = threadIdx.x;
+  const int T = cfg.T, S = cfg.S;
+  const int64_t ntiles = (nrows + T - 1) / T;
+  const int64_t G = gridDim.x;
+  uint64_t pol = 0;
+  const uint64_t pl = policy_evict_last();
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
+    fence_barrier_init();
+    pol = policy_evict_first();
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int s = 0; s < S; ++s) {
+      const int64_t t = blockIdx.x + s * G;
+      if (t < ntiles) {
+        const int64_t r0 = t * T;
+        const int e0 = __ldg(off + r0), e1 = __ldg(off + min64(r0 + T, nrows));
+        csr_pipe_issue(col, val, nnz, e0, e1, cfg, stage0 + (size_t)s * cfg.stage_bytes, &hdr[s],
+                       &full[s], pol);
+      }
+    }
+  double dsum = 0.0;
+  int s = 0;
+  uint32_t ph = 0;
+  for (int64_t t = blockIdx.x; t < ntiles; t += G) {
+    const int64_t r0 = t * T;
+    const int rows = (int)min64(T, nrows - r0);
+    const int i = (int)r0 + tid;
+    // this row's bounds and (thread 0) the bounds of the tile issued after
+    // this one, loaded before the wait so their latency overlaps it
+    int o0 = 0, o1 = 0;
+    if (tid < rows) {
+      o0 = __ldg(off + i);
+      o1 = __ldg(off + i + 1);
+    }
+    const int64_t tn = t + (int64_t)S * G;
+    int n0 = 0, n1 = 0;
+    if (tid == 0 && tn < ntiles) {
+      n0 = __ldg(off + tn * T);
+      n1 = __ldg(off + min64(tn * T + T, nrows));
+    }
+    unsigned char* st = stage0 + (size_t)s * cfg.stage_bytes;
+    mbar_wait(&full[s], ph);
+    const int len = o1 - o0;
+    const CsrPipeHdr h = hdr[s];
+    const int* s_col = reinterpret_cast<const int*>(st) + (o0 - h.bc);
+    const double* s_val = reinterpret_cast<const double*>(st + 4 * (size_t)cfg.cap) + (o0 - h.bv);
+    CsrRowRegs<LMAX> R;
+    const bool fast = tid < rows && len >= 1 && len <= LMAX;
+    const bool emit = tid < rows && !(SKIP_LONG && len > cfg.skip_above);  // else: other kernels
+    double sres = 0.0;
+    // phase 1: everything that reads the stage (rare serial rows entirely)
+    if (fast) {
+      if (cfg.hint) {
+        if (!h.fat) R.template load<true>(s_col, s_val, len, x, pl);
+        else R.template load<true>(col + o0, val + o0, len, x, pl);
+      } else {
+        if (!h.fat) R.template load<false>(s_col, s_val, len, x, pl);
+        else R.template load<false>(col + o0, val + o0, len, x, pl);
+      }
+    } else if (emit && len > LMAX) {
+      sres = h.fat ? csr_row_serial(col + o0, val + o0, len, x)
+                   : csr_row_serial(s_col, s_val, len, x);
+    }
+    __syncthreads();  // stage s consumed: refill it while the gathers land
+    if (tid == 0 && tn < ntiles)
+      csr_pipe_issue(col, val, nnz, n0, n1, cfg, st, &hdr[s], &full[s], pol);
+    // phase 2: products and the exact sum from registers
+    if (fast) sres = R.finish(len);
+    if (emit) {
+      double out = ACCUM ? add(y[i], sres) : sres;
+      if (dot.plus_zero) out = add(out, 0.0);
+      y[i] = out;
+      if (FUSE_DOT) dsum = add(dsum, mul(dot.other[i], out));
+    }
+    if (++s == S) {
+      s = 0;
+      ph ^= 1u;
+    }
+  }
+  if (FUSE_DOT) dot.finish_block<256>(dsum);
+}
+
+template <int L, bool A, bool K, bool F>
+static int csr_pipe_launch1(int64_t nrows, int64_t nnz, const int* off, const int* col, const double* val,
+                            const double* x, double* y, DotOut d, CsrPipeCfg cfg, size_t smem,
+                            int64_t grid, cudaStream_t st) {
+  auto k = csr_pipe<L, A, K, F>;
+  int rc = allow_dynamic_smem(reinterpret_cast<const void*>(k), smem);
+  if (rc) return rc;
+  k<<<(unsigned)grid, cfg.T, smem, st>>>((int)nrows, (int)nnz, off, col, val, x, y, cfg, d);
+  DS_LAUNCH_CHECK("csr_pipe");
+  return DS_OK;
+}
+
+// max_len: longest row if known (<= 27 selects the 27-wide register path),
+// else 0.  Returns DS_ERR_NOT_SUPPORTED (nothing launched) when the pipeline
+// cannot run (misaligned arrays, shared memory).
+static int csr_pipe_launch(int64_t nrows, int64_t nnz, const int* off, const int* col, const double* val,
+                           const double* x, double* y, bool accum, bool skip_long, int max_len,
+                           DotOut d, bool fuse, cudaStream_t st, int skip_above = kLongRow,
+                           bool hint = false) {
+  static int eT = -2, eS = -2, eC = -2;
+  if (eT == -2) {
+    const char* a = getenv("DS_CSR_T");
+    const char* b = getenv("DS_CSR_S");
+    const char* c = getenv("DS_CSR_CTAS");
+    eT = a ? atoi(a) : -1;
+    eS = b ? atoi(b) : -1;
+    eC = c ? atoi(c) : -1;
+  }
+  const bool aligned = ((reinterpret_cast<uintptr_t>(col) | reinterpret_cast<uintptr_t>(val)) &
+                        15) == 0;
+  if (!aligned) return DS_ERR_NOT_SUPPORTED;
+  const int L = (max_len > 0 && max_len <= 27) ? 27 : 33;
+  CsrPipeCfg cfg;
+  // measured at 104^3 (tools/sweep_csr.sh): 128 rows x 2 stages x 2 CTAs/SM
+  // 59.9 us, 256 x 2 x 1 61.9 us, 192 x 2 x 1 70.1 us, 128 x 4 x 1 86.5 us
+  cfg.T = eT > 0 ? eT : 128;
+  cfg.S = eS > 0 ? min(eS, 8) : 2;
+  cfg.cap = ((cfg.T * (max_len > 0 ? min(max_len, L) : 27) + 8) + 3) & ~3;
+  cfg.stage_bytes = (int)((12 * (int64_t)cfg.cap + 127) & ~127);
+  cfg.skip_above = skip_above;
+  static int eH = -2;
+  if (eH == -2) {
+    const char* h = getenv("DS_CSR_HINT");
+    eH = h ? atoi(h) : -1;
+  }
+  cfg.hint = eH >= 0 ? eH : (hint ? 1 : 0);
+  const size_t smem = 256 + (size_t)cfg.S * cfg.stage_bytes;
+  if (cfg.T > 256 || cfg.T < 32 || smem > (size_t)max_dynamic_smem() - 1024)
+    return DS_ERR_NOT_SUPPORTED;
+  const int64_t ntiles = ceil_div(nrows, cfg.T);
+  int64_t grid = (int64_t)sm_count() * (eC > 0 ? eC : 2);
+  if (grid > ntiles) grid = ntiles;
+  if (fuse) grid = d.clamp_grid(grid);
+#define DS_CSRP(Lv, A, K, F) \
+  return csr_pipe_launch1<Lv, A, K, F>(nrows, nnz, off, col, val, x, y, d, cfg, smem, grid, st)
+#define DS_CSRP_L(A, K, F)          \
+  do {                              \
+    if (L == 27) DS_CSRP(27, A, K, F); \
+    DS_CSRP(33, A, K, F);           \
+  } while (0)
+  if (fuse) {
+    if (accum) DS_CSRP_L(true, false, true); else DS_CSRP_L(false, false, true);
+  } else if (skip_long) {
+    if (accum) DS_CSRP_L(true, true, false); else DS_CSRP_L(false, true, false);
+  } else {
+    if (accum) DS_CSRP_L(true, false, false); else DS_CSRP_L(false, false, false);
+  }
+#undef DS_CSRP_L
+#undef DS_CSRP
+}
+// One CTA per long row: the pairwise recursion tree is cut into subtrees of
+// at most kSub addends; each subtree's leaves (64..128 addends each) are
+// summed by the CTA's 32 lane-groups in parallel, then thread 0 replays the
+// recursion to combine them in numpy's order.
+
+// Warp per long row (kLongRow < len <= kWarpRow): lane 0 enumerates the pairwise
+// recursion's leaves (64..128 addends each) into warp-private shared memory,
+// the warp's four 8-lane groups sum leaves in parallel, lane 0 replays the
+// recursion to combine them.  No block-wide barriers, 8 rows per CTA.
+constexpr int kWarpLeaves = 128;
+constexpr int kWarpRow = kCsrWarpRow;   // warp kernel: rows of kLongRow+1 .. kWarpRow entries
+
+template <bool ACCUM>
+__global__ void __launch_bounds__(kCsrBlock, 2)
+    csr_long_rows_warp(const int* __restrict__ rows, int n, const int* __restrict__ off,
+                       const int* __restrict__ col, const double* __restrict__ val,
+                       const double* __restrict__ x, double* y, const int* guard) {
+  if (guard && *guard) return;
+  __shared__ int s_lo[kCsrBlock / 32][kWarpLeaves];
+  __shared__ short s_n[kCsrBlock / 32][kWarpLeaves];
+  __shared__ double s_v[kCsrBlock / 32][kWarpLeaves];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, lane8 = lane & 7, grp = lane >> 3;
+  const unsigned mask = 0xffu << (lane & 24);
+  struct Frame {
+    int lo, n, expanded;
+  };
+  const int nw = gridDim.x * (kCsrBlock / 32);
+  for (int li = blockIdx.x * (kCsrBlock / 32) + w; li < n; li += nw) {
+    const int row = rows[li];
+    const int start = off[row];
+    const int m = off[row + 1] - start - 1;
+    if (m + 1 > kWarpRow) continue;      // the CTA kernel owns it
+    int nl = 0;
+    if (lane == 0) {                      // leaves left to right
+      Frame st[32];
+      int ft = 0;
+      st[ft++] = {0, m, 0};
+      while (ft > 0) {
+        Frame f = st[--ft];
+        if (f.n <= 128) {
+          s_lo[w][nl] = f.lo;
+          s_n[w][nl] = (short)f.n;
+          ++nl;
+        } else {
+          int n2 = f.n / 2;
+          n2 -= n2 % 8;
+          st[ft++] = {f.lo + n2, f.n - n2, 0};
+          st[ft++] = {f.lo, n2, 0};
+        }
+      }
+    }
+    nl = __shfl_sync(0xffffffffu, nl, 0);
+    __syncwarp();
+    for (int l = grp; l < nl; l += 4) {
+      const double v = csr_leaf_g8_all(col, val, x, (int64_t)start + 1 + s_lo[w][l], s_n[w][l],
+                                       lane8, mask);
+      if (lane8 == 0) s_v[w][l] = v;
+    }
+    __syncwarp();
+    if (lane == 0) {                      // combine in recursion order
+      Frame st[32];
+      double vs[32];
+      int ft = 0, vt = 0, next = 0;
+      st[ft++] = {0, m, 0};
+      while (ft > 0) {
+        Frame f = st[--ft];
+        if (f.n <= 128) {
+          vs[vt++] = s_v[w][next++];
+        } else if (!f.expanded) {
+          int n2 = f.n / 2;
+          n2 -= n2 % 8;
+          st[ft++] = {f.lo, f.n, 1};
+          st[ft++] = {f.lo + n2, f.n - n2, 0};
+          st[ft++] = {f.lo, n2, 0};
+        } else {
+          const double b = vs[--vt];
+          const double a = vs[--vt];
+          vs[vt++] = add(a, b);
+        }
+      }
+      const double p0 = mul(val[start], __ldg(x + col[start]));
+      const double sres = add(p0, vs[0]);
+      y[row] = ACCUM ? add(y[row], sres) : sres;
+    }
+    __syncwarp();
+  }
+}
+
+template <bool ACCUM>
+__global__ void __launch_bounds__(kCsrBlock, 2)
+    csr_long_rows(const int* __restrict__ long_rows, int n_long, const int* __restrict__ off,
+                  const int* __restrict__ col, const double* __restrict__ val,
+                  const double* __restrict__ x, double* y, const int* guard) {
+  if (guard && *guard) return;
+  __shared__ int64_t s_leaf_lo[kMaxLeaves];
+  __shared__ int s_leaf_n[kMaxLeaves];
+  __shared__ double s_leaf_v[kMaxLeaves];
+  __shared__ int64_t s_lo, s_n;
+  __shared__ int s_cmd, s_nleaves;
+  const int tid = threadIdx.x, lane8 = tid & 7, grp = tid >> 3;
+  const unsigned mask = 0xffu << (tid & 24);
+  struct Frame {
+    int64_t lo, n;
+    int expanded;
+  };
+  for (int li = blockIdx.x; li < n_long; li += gridDim.x) {
+    const int row = long_rows[li];
+    const int64_t start = off[row];
+    const int64_t m = (int64_t)off[row + 1] - start - 1;
+    if (m + 1 <= kWarpRow) continue;   // csr_long_rows_warp owns it
+    const int64_t base = start + 1;
+    // thread-0 top-level DFS state
+    Frame st[48];
+    double vs[48];
+    int ft = 0, vt = 0;
+    if (tid == 0) st[ft++] = {0, m, 0};
+    for (;;) {
+      if (tid == 0) {
+        s_cmd = 0;
+        while (ft > 0) {
+          Frame f = st[--ft];
+          if (f.n <= kSub) {
+            s_lo = f.lo;
+            s_n = f.n;
+            s_cmd = 1;
+            break;
+          }
+          if (!f.expanded) {
+            int64_t n2 = f.n / 2;
+            n2 -= n2 % 8;
+            st[ft++] = {f.lo, f.n, 1};
+            st[ft++] = {f.lo + n2, f.n - n2, 0};
+            st[ft++] = {f.lo, n2, 0};
+          } else {
+            double b = vs[--vt];
+            double a = vs[--vt];
+            vs[vt++] = add(a, b);
+          }
+        }
+        if (s_cmd) {  // enumerate this subtree's leaves left to right
+          Frame sst[32];
+          int sft = 0, nl = 0;
+          sst[sft++] = {s_lo, s_n, 0};
+          while (sft > 0) {
+            Frame f = sst[--sft];
+            if (f.n <= 128) {
+              s_leaf_lo[nl] = f.lo;
+              s_leaf_n[nl] = (int)f.n;
+              ++nl;
+            } else {
+              int64_t n2 = f.n / 2;
+              n2 -= n2 % 8;
+              sst[sft++] = {f.lo + n2, f.n - n2, 0};
+              sst[sft++] = {f.lo, n2, 0};
+            }
+          }
+          s_nleaves = nl;
+        }
+      }
+      __syncthreads();
+      if (!s_cmd) break;
+      for (int l = grp; l < s_nleaves; l += kCsrBlock / 8) {
+        double v = csr_leaf_g8_all(col, val, x, base + s_leaf_lo[l], s_leaf_n[l], lane8, mask);
+        if (lane8 == 0) s_leaf_v[l] = v;
+      }
+      __syncthreads();
+      if (tid == 0) {  // combine the subtree in recursion order
+        Frame sst[32];
+        double svs[32];
+        int sft = 0, svt = 0, next_leaf = 0;
+        sst[sft++] = {s_lo, s_n, 0};
+        while (sft > 0) {
+          Frame f = sst[--sft];
+          if (f.n <= 128) {
+            svs[svt++] = s_leaf_v[next_leaf++];
+          } else if (!f.expanded) {
+            int64_t n2 = f.n / 2;
+            n2 -= n2 % 8;
+            sst[sft++] = {f.lo, f.n, 1};
+            sst[sft++] = {f.lo + n2, f.n - n2, 0};
+            sst[sft++] = {f.lo, n2, 0};
+          } else {
+            double b = svs[--svt];
+            double a = svs[--svt];
+            svs[svt++] = add(a, b);
+          }
+        }
+        vs[vt++] = svs[0];
+      }
+      __syncthreads();
+    }
+    if (tid == 0) {
+      const double p0 = mul(val[start], __ldg(x + col[start]));
+      const double s = add(p0, vs[0]);
+      y[row] = ACCUM ? add(y[row], s) : s;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void csr_find_long(int nrows, const int* __restrict__ off, int* long_rows,
+                              unsigned* count, int* max_len) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += gridDim.x * blockDim.x) {
+    const int len = off[r + 1] - off[r];
+    if (len > kLongRow) long_rows[atomicAdd(count, 1u)] = r;
+    atomicMax(max_len, len);
+  }
+}
+
+// long-row kernels for the rows > kLongRow listed by ds_csr_analyze
+// Each kernel skips the rows of the other one, so an unsorted list
+// (ds_csr_analyze) may be passed to both; the bins plan passes exact lists.
+static int launch_csr_long2(const int* warp_rows, int64_t n_warp, const int* cta_rows,
+                            int64_t n_cta, const int* off, const int* col, const double* val,
+                            const double* x, double* y, bool accum, const int* guard,
+                            cudaStream_t st) {
+  if (n_warp > 0) {
+    const int64_t lw = min64(ceil_div(n_warp, kCsrBlock / 32), (int64_t)sm_count() * 8);
+    if (accum)
+      csr_long_rows_warp<true><<<(unsigned)lw, kCsrBlock, 0, st>>>(warp_rows, (int)n_warp, off,
+                                                                  col, val, x, y, guard);
+    else
+      csr_long_rows_warp<false><<<(unsigned)lw, kCsrBlock, 0, st>>>(warp_rows, (int)n_warp, off,
+                                                                   col, val, x, y, guard);
+  }
+  if (n_cta > 0) {
+    const int64_t lb = min64(n_cta, (int64_t)sm_count() * 8);
+    if (accum)
+      csr_long_rows<true><<<(unsigned)lb, kCsrBlock, 0, st>>>(cta_rows, (int)n_cta, off, col, val,
+                                                             x, y, guard);
+    else
+      csr_long_rows<false><<<(unsigned)lb, kCsrBlock, 0, st>>>(cta_rows, (int)n_cta, off, col,
+                                                              val, x, y, guard);
+  }
+  DS_LAUNCH_CHECK("csr_long_rows");
+  return DS_OK;
+}
+
+static int launch_csr_long(const int* long_rows, int64_t n_long, const int* off, const int* col,
+                           const double* val, const double* x, double* y, bool accum,
+                           const int* guard, cudaStream_t st) {
+  return launch_csr_long2(long_rows, n_long, long_rows, n_long, off, col, val, x, y, accum, guard,
+                          st);
+}
+
+int launch_csr_binned(int64_t nrows, int64_t ncols, int64_t nnz, const int* off, const int* col,
+                      const double* val, const int* perm, const int64_t* bins, const double* x,
+                      double* y, bool accum, const DotOut* dot, cudaStream_t st) {
+  if (nrows == 0) return DS_OK;
+  DotOut d = dot ? *dot : DotOut{};
+  const bool fuse = d.fused();
+  static int binned_only = -1;
+  if (binned_only < 0) binned_only = getenv("DS_CSR_BINNED_ONLY") ? 1 : 0;
+  // Irregular matrix: the TMA pipeline takes every row of <= 33 entries (the
+  // bulk of a power-law matrix), the binned kernel only bin 5 (34..129) and
+  // the long-row kernels bin 6; x gathers carry L2 evict_last.  (A fused dot
+  // needs one kernel to own every row: it keeps the all-binned path.)
+  if (!fuse && !binned_only && nnz > 0 && nnz < (1ll << 31)) {
+    const int rc = csr_pipe_launch(nrows, nnz, off, col, val, x, y, accum, true, 33, d, false, st,
+                                   33, true);
+    if (rc == DS_OK) {
+      int64_t rest[kCsrBinCount + 1];
+      for (int b = 0; b <= kCsrBinCount; ++b) rest[b] = b < 5 ? bins[5] : bins[b];
+      if (rest[kCsrBinCount] == rest[5]) return DS_OK;
+      return launch_csr_binned(nrows, ncols, 0, off, col, val, perm, rest, x, y, accum, dot, st);
+    }
+    if (rc != DS_ERR_NOT_SUPPORTED) return rc;
+  }
+  const int64_t n_long = bins[8] - bins[6];
+  if (fuse && n_long > 0) {
+    set_error("fused dot with long rows is not supported");
+    return DS_ERR_NOT_SUPPORTED;
+  }
+  CsrBins bi;
+  int64_t acc = 0;
+  for (int b = 0; b < 8; ++b) bi.start[b] = bins[b];   // bins 0..5 (+ end of 5)
+  for (int b = 0; b < 6; ++b) {
+    bi.pair_off[b] = acc;
+    acc += ceil_div(bins[b + 1] - bins[b], kBinRowsHost[b]);
+  }
+  bi.pair_off[6] = acc;
+  bi.pair_off[7] = acc;
+  int64_t blocks = ceil_div(acc * 8, kCsrBlock);
+  const int64_t cap = (int64_t)sm_count() * 8;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  if (fuse) blocks = d.clamp_grid(blocks);
+  // the binned path serves irregular matrices whose x is gathered at random:
+  // keep x persisting in L2 while the row stream passes through
+  const bool win = x_window_begin(st, x, (size_t)ncols * 8);
+#define DS_CSRB(A, F) \
+  csr_binned<A, F><<<(unsigned)blocks, kCsrBlock, 0, st>>>(off, col, val, x, y, perm, bi, d)
+  if (accum) {
+    if (fuse) DS_CSRB(true, true); else DS_CSRB(true, false);
+  } else {
+    if (fuse) DS_CSRB(false, true); else DS_CSRB(false, false);
+  }
+#undef DS_CSRB
+  DS_LAUNCH_CHECK("csr_binned");
+  if (n_long > 0) {
+    const int rc = launch_csr_long2(perm + bins[6], bins[7] - bins[6], perm + bins[7],
+                                    bins[8] - bins[7], off, col, val, x, y, accum, d.guard, st);
+    if (rc) return rc;
+  }
+  if (win) x_window_end(st);
+  return DS_OK;
+}
+
+// A matrix without entries (e.g. the remote part of a partition without
+// ghosts): y = 0 (spmv) or y = y + 0.0 (spmv_add, kernels.py:196-198: the
+// +0.0 turns -0.0 into +0.0).  One streaming pass instead of a full SpMV
+// kernel walking empty tiles.
+__global__ void empty_matrix_kernel(int64_t n, double* y, int accum, const int* guard) {
+  if (guard && *guard) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = accum ? add(y[i], 0.0) : 0.0;
+}
+int launch_empty_matrix(int64_t nrows, double* y, bool accum, const int* guard,
+                        cudaStream_t st) {
+  const unsigned g = (unsigned)min64(ceil_div(nrows, 256), (int64_t)sm_count() * 8);
+  empty_matrix_kernel<<<g, 256, 0, st>>>(nrows, y, accum ? 1 : 0, guard);
+  DS_LAUNCH_CHECK("empty_matrix_kernel");
+  return DS_OK;
+}
+
+int launch_csr(int64_t nrows, int64_t nnz, const int* off, const int* col, const double* val,
+               const int* long_rows, int64_t n_long, int max_len, const double* x, double* y,
+               bool accum, const DotOut* dot, cudaStream_t st) {
+  if (nrows == 0) return DS_OK;
+  if (nnz == 0 && !(dot && dot->fused()))
+    return launch_empty_matrix(nrows, y, accum, dot ? dot->guard : nullptr, st);
+  const int64_t groups = (nrows + 1) / 2;   // one 8-lane group per row pair
+  int64_t blocks = ceil_div(groups * 8, kCsrBlock);
+  static int eB = -2, use_g8 = -1;
+  if (eB == -2) {
+    const char* e = getenv("DS_CSR_BLOCKS_PER_SM");
+    eB = e ? atoi(e) : -1;
+    use_g8 = getenv("DS_CSR_G8") ? 1 : 0;
+  }
+  // 8 resident CTAs per SM (measured best: 84 us vs 97 us for a 16-wave grid)
+  const int64_t cap = (int64_t)sm_count() * (eB > 0 ? eB : 8);
+  if (blocks > cap) blocks = cap;
+  const bool skip = (long_rows != nullptr);
+  DotOut d = dot ? *dot : DotOut{};
+  const bool fuse = d.fused();
+  if (fuse && skip && n_long > 0) {
+    set_error("fused dot with long rows is not supported");
+    return DS_ERR_NOT_SUPPORTED;
+  }
+  // the TMA pipeline needs the long-row plan (long_rows != NULL, possibly
+  // empty): rows > kLongRow are then computed by the long-row kernels
+  if (!use_g8 && skip) {
+    const int rc = csr_pipe_launch(nrows, nnz, off, col, val, x, y, accum, n_long > 0, max_len, d,
+                                   fuse, st);
+    if (rc == DS_OK)
+      return launch_csr_long(long_rows, n_long, off, col, val, x, y, accum, d.guard, st);
+    if (rc != DS_ERR_NOT_SUPPORTED) return rc;
+  }
+  if (fuse) blocks = d.clamp_grid(blocks);
+#define DS_CSR(A, S, F) \
+  csr_rows_g8<A, S, F><<<(unsigned)blocks, kCsrBlock, 0, st>>>((int)nrows, off, col, val, x, y, d)
+  if (fuse) {
+    if (skip && n_long > 0) {
+      set_error("fused dot with long rows is not supported");
+      return DS_ERR_NOT_SUPPORTED;
+    }
+    if (accum) DS_CSR(true, false, true); else DS_CSR(false, false, true);
+  } else if (skip) {
+    if (accum) DS_CSR(true, true, false); else DS_CSR(false, true, false);
+  } else {
+    if (accum) DS_CSR(true, false, false); else DS_CSR(false, false, false);
+  }
+#undef DS_CSR
+  DS_LAUNCH_CHECK("csr_rows_g8");
+  return skip ? launch_csr_long(long_rows, n_long, off, col, val, x, y, accum, d.guard, st)
+              : DS_OK;
+}
+
+}  // namespace ds
+
+// ============================================================== C ABI ======
+using namespace ds;
+
+extern "C" int ds_csr_analyze(int64_t nrows, const int32_t* row_offsets, int32_t* long_rows,
+                              int64_t* n_long, int32_t* max_row_len, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  *n_long = 0;
+  if (max_row_len) *max_row_len = 0;
+  if (nrows <= 0) return DS_OK;
+  int* d = nullptr;  // [count, maxlen]
+  DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), 2 * sizeof(int), st));
+  DS_CUDA(cudaMemsetAsync(d, 0, 2 * sizeof(int), st));
+  const unsigned g = (unsigned)min64(ceil_div(nrows, 256), (int64_t)sm_count() * 8);
+  csr_find_long<<<g, 256, 0, st>>>((int)nrows, row_offsets, long_rows,
+                                   reinterpret_cast<unsigned*>(d), d + 1);
+  DS_LAUNCH_CHECK("csr_find_long");
+  int h[2];
+  DS_CUDA(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, st));
+  DS_CUDA(cudaFreeAsync(d, st));
+  DS_CUDA(cudaStreamSynchronize(st));
+  *n_long = h[0];
+  if (max_row_len) *max_row_len = h[1];
+  return DS_OK;
+}
+
+extern "C" int ds_spmv_csr(int64_t nrows, int64_t ncols, int64_t nnz, const int32_t* row_offsets,
+                           const int32_t* col_indices, const double* values,
+                           const int32_t* long_rows, int64_t n_long, const double* x, double* y,
+                           int accumulate, void* stream) {
+  (void)ncols;
+  (void)nnz;
+  if (nrows < 0 || nrows >= (1ll << 31)) {
+    set_error("nrows out of range");
+    return DS_ERR_NOT_SUPPORTED;
+  }
+  return launch_csr(nrows, nnz, row_offsets, col_indices, values, long_rows, n_long, 0, x, y,
+                    accumulate != 0, nullptr, as_stream(stream));
+}
+

@@ -141,6 +141,8 @@ int launch_coo(int64_t nrows, int64_t nnz, const int* rows, const int* cols, con
                bool sorted, int max_len, const double* x, double* y, bool accum, const int* guard,
                cudaStream_t st, bool plus_zero = false, const int* long_runs = nullptr,
                int n_long = 0);
+// y = 0 / y = y + 0.0 for a matrix without entries (ds_csr.cu)
+int launch_empty_matrix(int64_t nrows, double* y, bool accum, const int* guard, cudaStream_t st);
 // per-device auxiliary stream + fork/join events (created once) for kernels
 // that run concurrently with the main one
 int aux_stream(cudaStream_t* side, cudaEvent_t* fork, cudaEvent_t* join);

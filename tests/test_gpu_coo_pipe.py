@@ -1,4 +1,4 @@
-"""GPU parity of the row-sorted COO SpMV (ds_spmv.cu coo_pipe) against the
+"""GPU parity of the row-sorted COO SpMV (ds_coo.cu coo_pipe) against the
 oracle's np.bincount restatement (kernels.py:143-163): bitwise.
 
 Shapes that hit every branch of the pipeline: rows split across tiles and

@@ -1,4 +1,4 @@
-"""GPU parity of every branch of the CSR SpMV launcher (ds_spmv.cu) against
+"""GPU parity of every branch of the CSR SpMV launcher (ds_csr.cu) against
 the oracle's np.add.reduceat restatement (kernels.py:102-119): bitwise.
 
 Branches: the TMA pipeline's 27- and 33-wide register paths, its serial path

@@ -1,4 +1,4 @@
-"""DIA SpMV with the TMA-staged x windows (ds_spmv.cu dia_issue_windows),
+"""DIA SpMV with the TMA-staged x windows (ds_dia.cu dia_issue_windows),
 forced at small sizes in a subprocess (the launcher reads DS_DIA_XWIN_FORCE /
 DS_DIA_XWIN_SPAN once): bitwise equal to the oracle on stencils whose edges
 clip the windows (odd and even column counts, ragged last tiles), spmv_add,
