@@ -317,7 +317,12 @@ static int dia_pipe_launch(int64_t nrows, int64_t ncols, int ndiags, const int* 
 }
 
 // tile shape: env DS_DIA_T / DS_DIA_S / DS_DIA_CTAS override (tuning only)
-static void dia_shape(int ndiags, int* T, int* S, int* ctas) {
+// Measured at 104^3 (one gpurun call, bench CG step / standalone SpMV):
+// 128 rows x 3 stages x 2 CTAs/SM 53.7 / 41.2 us, 256 x 3 x 1 55.6 / 43.1,
+// 128 x 4 x 2 54.6 / 42.6, 64 x 3-4 x 4 59-62 / 46-47, 2 stages 67-69 in
+// the step (the programmatic-launch prefetch wants 3).  With the x windows
+// (>= 4M rows) 256 x 3 x 1 (192^3: 266 us vs 270).
+static void dia_shape(int ndiags, int64_t nrows, int* T, int* S, int* ctas) {
   static int eT = -2, eS = -2, eC = -2;
   if (eT == -2) {
     const char* a = getenv("DS_DIA_T");
@@ -327,9 +332,10 @@ static void dia_shape(int ndiags, int* T, int* S, int* ctas) {
     eS = b ? atoi(b) : -1;
     eC = c ? atoi(c) : -1;
   }
-  *T = 256;
+  const bool big = nrows >= (4ll << 20);   // the x-window layout (launch_dia)
+  *T = big ? 256 : 128;
   *S = 3;
-  *ctas = 1;
+  *ctas = big ? 1 : 2;
   // keep each stage <= ~64 KB
   while (*T > 32 && (int64_t)(*T) * ndiags * 8 > 64 * 1024) *T /= 2;
   if (eT > 0) *T = eT;
@@ -344,7 +350,7 @@ int launch_dia(int64_t nrows, int64_t ncols, int ndiags, const int* off, const d
   const bool fuse = d.fused();
   const bool aligned = (reinterpret_cast<uintptr_t>(val) & 15) == 0;
   int T, S, ctas;
-  dia_shape(ndiags, &T, &S, &ctas);
+  dia_shape(ndiags, nrows, &T, &S, &ctas);
   static int no_xw = -1, force_xw = 0;
   if (no_xw < 0) {
     no_xw = getenv("DS_DIA_NO_XWIN") ? 1 : 0;
