@@ -147,8 +147,12 @@ int ds_dia_count_nonzero(int64_t nrows, int64_t ncols, int32_t ndiags, const int
  * COO (stable (row,col) sort + duplicate sums in reduceat order) on the
  * device, sizes the target and -- for DIA -- applies the fill-limit test
  * BEFORE any target allocation (datamove.py:246-252): it returns
- * DS_ERR_DIA_FILL_OVERFLOW with *out_ndiags set.  finish_* writes the target
- * arrays and frees the job; abort frees it without writing.                */
+ * DS_ERR_DIA_FILL_OVERFLOW with *out_ndiags set.  fill_limit < 0 selects
+ * the reference default 10 * max(nnz, nrows) of the source (datamove.py:55-57;
+ * for a DIA source nnz = its nonzero in-range slots, counted by begin).
+ * finish_* writes the target arrays and frees the job; abort frees it
+ * without writing.  A DIA or canonical-CSR source is read again by finish_*
+ * (its entries go straight into the target): keep it alive until then.     */
 typedef struct ds_convert_job ds_convert_job;
 enum { DS_FMT_COO = 0, DS_FMT_CSR = 1, DS_FMT_DIA = 2 };   /* FormatId, formats.py:33-42 */
 

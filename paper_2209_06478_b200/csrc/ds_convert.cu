@@ -35,6 +35,17 @@ struct ds_convert_job {
   int64_t ndiags = 0;          // DIA target
   int* diag_map = nullptr;     // exclusive scan of diagonal presence (nrows+ncols-1)
   int* dia_off = nullptr;      // (ndiags)
+  // DIA source, CSR / COO target: the canonical entries are emitted straight
+  // into the target at finish (row offsets = the exclusive scan of the row
+  // counts), instead of into job buffers that are then copied
+  const int* dsrc_off = nullptr;
+  const double* dsrc_vals = nullptr;
+  int dsrc_nd = 0;
+  int* dsrc_start = nullptr;   // first entry of each row group (ceil(nrows / kDiaGroupRows))
+  // canonical CSR source, DIA target: no COO proxy at all; the diagonal
+  // census is taken while checking the order, the slab is filled per row
+  const int* csr_off = nullptr;
+  unsigned char* flags = nullptr;   // diagonal presence (nrows+ncols-1), already marked
 };
 
 namespace ds {
@@ -212,112 +223,96 @@ __global__ void reduce_runs(int64_t nnz, int64_t ncols, const unsigned long long
   }
 }
 
-// DIA source: the (rows x ndiags) slab of a block is copied to shared
-// memory with coalesced loads, then one thread per row walks its row there
-// (a thread-per-row walk over global memory reads 8*ndiags-byte strided rows
-// and thrashes L1: 1 ms -> ~0.1 ms at 104^3).
-// DIA source fallback for slabs that do not fit shared memory
-struct DiaRowCount {
-  int nrows, ncols, nd;
+// DIA source as a stream compaction.  The offsets ascend, so the canonical
+// COO order of a DIA matrix is its row-major slot order filtered by "column
+// in range and value != 0" (datamove.py:169-190 via formats.py:239-255).  One
+// warp owns kDiaGroupRows consecutive rows, i.e. a contiguous run of slots:
+// it reads them 32 at a time (coalesced, 4 chunks in flight) and a ballot
+// gives each valid slot its position.  Pass 1 counts per group, an exclusive
+// scan over the groups gives each warp its base, pass 2 writes the entries
+// (and, for a CSR target, row_offsets[i] = the position of row i's first slot)
+// straight into the target arrays.
+constexpr int kDiaGroupRows = 32;
+constexpr int kDiaChunks = 4;
+
+struct DiaSlots {
+  int ncols, nd, q, rmd;   // 32 = q * nd + rmd
   const int* off;
   const double* vals;
-  __device__ int operator()(int64_t i) const {
-    int cnt = 0;
-    for (int j = 0; j < nd; ++j) {
-      const int64_t col = i + off[j];
-      if (col >= 0 && col < ncols && vals[i * nd + j] != 0.0) ++cnt;
+  __device__ DiaSlots(int ncols_, int nd_, const int* off_, const double* vals_)
+      : ncols(ncols_), nd(nd_), q(32 / nd_), rmd(32 % nd_), off(off_), vals(vals_) {}
+  // walk the slots [e_begin, e_end) of one group; f(valid, e, i, j) per lane
+  template <class F>
+  __device__ __forceinline__ void walk(int64_t r0, int64_t e_begin, int64_t e_end, F&& f) const {
+    const int lane = threadIdx.x & 31;
+    int64_t i = r0 + lane / nd;
+    int j = lane % nd;
+    for (int64_t e0 = e_begin; e0 < e_end; e0 += 32 * kDiaChunks) {
+      double x[kDiaChunks];
+#pragma unroll
+      for (int u = 0; u < kDiaChunks; ++u) {
+        const int64_t e = e0 + u * 32 + lane;
+        x[u] = e < e_end ? __ldg(vals + e) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < kDiaChunks; ++u) {
+        const int64_t e = e0 + u * 32 + lane;
+        const int64_t col = i + __ldg(off + j);
+        const bool valid = e < e_end && col >= 0 && col < ncols && x[u] != 0.0;
+        f(valid, e < e_end, i, j, (int)col, x[u]);
+        i += q;
+        j += rmd;
+        if (j >= nd) {
+          j -= nd;
+          ++i;
+        }
+      }
     }
-    return cnt;
   }
 };
-__global__ void dia_emit_direct(int nrows, int ncols, int nd, const int* __restrict__ off,
-                                const double* __restrict__ vals, const int* __restrict__ start,
-                                int* r, int* c, double* v) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nrows; i += gridDim.x * blockDim.x) {
-    int o = start[i];
-    for (int j = 0; j < nd; ++j) {
-      const int64_t col = (int64_t)i + off[j];
-      const double x = vals[(int64_t)i * nd + j];
-      if (col >= 0 && col < ncols && x != 0.0) {
-        r[o] = i;
-        c[o] = (int)col;
-        v[o] = x;
-        ++o;
-      }
-    }
-  }
-}
-
-constexpr int kDiaWalkRows = 128;
-
-__device__ __forceinline__ int dia_stage_slab(const double* __restrict__ vals, int nrows, int nd,
-                                              int r0, double* slab) {
-  const int rows = min(kDiaWalkRows, nrows - r0);
-  const int64_t base = (int64_t)r0 * nd;
-  const int total = rows * nd;
-  for (int k = threadIdx.x; k < total; k += blockDim.x) slab[k] = vals[base + k];
-  __syncthreads();
-  return rows;
-}
-
-__global__ void dia_row_counts(int nrows, int ncols, int nd, const int* __restrict__ off,
-                               const double* __restrict__ vals, int* counts) {
-  extern __shared__ double slab[];
-  for (int r0 = blockIdx.x * kDiaWalkRows; r0 < nrows; r0 += gridDim.x * kDiaWalkRows) {
-    const int rows = dia_stage_slab(vals, nrows, nd, r0, slab);
-    if (threadIdx.x < rows) {
-      const int i = r0 + threadIdx.x;
-      int cnt = 0;
-      for (int j = 0; j < nd; ++j) {
-        const int64_t col = (int64_t)i + off[j];
-        if (col >= 0 && col < ncols && slab[threadIdx.x * nd + j] != 0.0) ++cnt;
-      }
-      counts[i] = cnt;
-    }
-    __syncthreads();
-  }
-}
 
 struct ArrayAt {
   const int* a;
   __device__ int operator()(int64_t k) const { return a[k]; }
 };
 
-// emit with both the input slab and the output range staged in shared
-// memory: the block's entries are contiguous in the canonical COO
-// ([start[r0], start[r0+rows])), so the final copy-out is coalesced
-__global__ void dia_emit(int nrows, int ncols, int nd, const int* __restrict__ off,
-                         const double* __restrict__ vals, const int* __restrict__ start,
-                         int nnz_total, int* r, int* c, double* v) {
-  extern __shared__ double slab[];
-  double* ov = slab + (size_t)kDiaWalkRows * nd;                 // rows*nd values
-  int* orow = reinterpret_cast<int*>(ov + (size_t)kDiaWalkRows * nd);
-  int* ocol = orow + kDiaWalkRows * nd;
-  for (int r0 = blockIdx.x * kDiaWalkRows; r0 < nrows; r0 += gridDim.x * kDiaWalkRows) {
-    const int rows = dia_stage_slab(vals, nrows, nd, r0, slab);
-    const int e0 = start[r0];
-    const int e1 = (r0 + rows < nrows) ? start[r0 + rows] : nnz_total;
-    if (threadIdx.x < rows) {
-      const int i = r0 + threadIdx.x;
-      int o = start[i] - e0;
-      for (int j = 0; j < nd; ++j) {
-        const int64_t col = (int64_t)i + off[j];
-        const double x = slab[threadIdx.x * nd + j];
-        if (col >= 0 && col < ncols && x != 0.0) {
-          orow[o] = i;
-          ocol[o] = (int)col;
-          ov[o] = x;
-          ++o;
-        }
+__global__ void dia_group_counts(int64_t nrows, int ncols, int nd, const int* __restrict__ off,
+                                 const double* __restrict__ vals, int64_t ngroups, int* gcount) {
+  const DiaSlots s(ncols, nd, off, vals);
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < ngroups; g += nwarps) {
+    const int64_t r0 = g * kDiaGroupRows;
+    const int64_t r1 = r0 + kDiaGroupRows < nrows ? r0 + kDiaGroupRows : nrows;
+    int cnt = 0;
+    s.walk(r0, r0 * nd, r1 * nd, [&](bool valid, bool, int64_t, int, int, double) {
+      cnt += __popc(__ballot_sync(0xffffffffu, valid));
+    });
+    if ((threadIdx.x & 31) == 0) gcount[g] = cnt;
+  }
+}
+
+__global__ void dia_group_emit(int64_t nrows, int ncols, int nd, const int* __restrict__ off,
+                               const double* __restrict__ vals, int64_t ngroups,
+                               const int* __restrict__ gstart, int* row_off, int* r, int* c,
+                               double* v) {
+  const DiaSlots s(ncols, nd, off, vals);
+  const unsigned lt = (1u << (threadIdx.x & 31)) - 1u;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < ngroups; g += nwarps) {
+    const int64_t r0 = g * kDiaGroupRows;
+    const int64_t r1 = r0 + kDiaGroupRows < nrows ? r0 + kDiaGroupRows : nrows;
+    int base = gstart[g];
+    s.walk(r0, r0 * nd, r1 * nd, [&](bool valid, bool in, int64_t i, int j, int col, double x) {
+      const unsigned m = __ballot_sync(0xffffffffu, valid);
+      const int pos = base + __popc(m & lt);
+      if (row_off && in && j == 0) row_off[i] = pos;
+      if (valid) {
+        if (r) r[pos] = (int)i;
+        c[pos] = col;
+        v[pos] = x;
       }
-    }
-    __syncthreads();
-    for (int k = threadIdx.x; k < e1 - e0; k += blockDim.x) {
-      r[e0 + k] = orow[k];
-      c[e0 + k] = ocol[k];
-      v[e0 + k] = ov[k];
-    }
-    __syncthreads();
+      base += __popc(m);
+    });
   }
 }
 
@@ -352,6 +347,132 @@ __global__ void mark_diags(int64_t nnz, int nrows, const int* __restrict__ r,
     if (v == 0) flags[d] = 1;
   }
 }
+// CSR source, DIA target: one pass over the column indices checks the
+// canonical order (strictly ascending columns in every row: OrderBad without
+// expanding the rows) and marks the diagonals; then the DIA slab of a block
+// of rows is zeroed in shared memory, the block's entries are dropped into
+// their (row, diagonal) slots and the slab is written out with coalesced
+// stores (values are row-major (nrows, ndiags)).  Both walk the entries of a
+// warp's rows 32 at a time (coalesced, U chunks of loads in flight); each
+// lane tracks the row of its entry incrementally (rows are monotone in k, so
+// a lane moves ~1 row per chunk) instead of searching the offsets.
+constexpr int kCsrWalkRows = 16;    // rows per warp
+// body(kb, k1, rows[U], loaded[U]): lane's entry of chunk u is kb + 32u + lane
+template <int U, class Load, class Body>
+__device__ __forceinline__ void csr_warp_walk(const int* __restrict__ off, int r0, int r1,
+                                              Load&& load, Body&& body) {
+  const int lane = threadIdx.x & 31;
+  const int k1 = __ldg(off + r1);
+  int row = r0;
+  for (int kb = __ldg(off + r0); kb < k1; kb += 32 * U) {
+    decltype(load(0)) x[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = kb + 32 * u + lane;
+      if (k < k1) x[u] = load(k);
+    }
+    int rr[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = kb + 32 * u + lane;
+      if (k < k1)
+        while (__ldg(off + row + 1) <= k) ++row;
+      rr[u] = row;
+    }
+    body(kb, k1, rr, x);
+  }
+}
+
+struct ColVal {
+  int c;
+  double v;
+};
+
+__global__ void csr_check_mark(int nrows, const int* __restrict__ off, const int* __restrict__ c,
+                               unsigned char* flags, int* bad) {
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  int mybad = 0;
+  for (int r0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kCsrWalkRows; r0 < nrows;
+       r0 += nwarps * kCsrWalkRows) {
+    const int r1 = min(r0 + kCsrWalkRows, nrows);
+    int carry = -1, carry_row = -1;   // previous chunk's last entry (lane 31)
+    csr_warp_walk<8>(off, r0, r1, [&](int k) { return __ldg(c + k); },
+                     [&](int kb, int k1, const int (&rr)[8], const int (&cc)[8]) {
+#pragma unroll
+                       for (int u = 0; u < 8; ++u) {
+                         const int row = rr[u], ck = cc[u];
+                         int prev = __shfl_up_sync(0xffffffffu, ck, 1);
+                         int prev_row = __shfl_up_sync(0xffffffffu, row, 1);
+                         if (lane == 0) {
+                           prev = carry;
+                           prev_row = carry_row;
+                         }
+                         carry = __shfl_sync(0xffffffffu, ck, 31);
+                         carry_row = __shfl_sync(0xffffffffu, row, 31);
+                         if (kb + 32 * u + lane < k1) {
+                           if (prev_row == row && prev >= ck) mybad = 1;
+                           if (flags) {
+                             const int64_t d = (int64_t)ck - row + nrows - 1;
+                             unsigned short f;
+                             asm volatile("ld.global.ca.u8 %0, [%1];" : "=h"(f) : "l"(flags + d));
+                             if (f == 0) flags[d] = 1;
+                           }
+                         }
+                       }
+                     });
+  }
+  if (__syncthreads_or(mybad) && threadIdx.x == 0) atomicOr(bad, 1);
+}
+
+__global__ void dia_fill_csr(int nrows, int nd, int R, const int* __restrict__ off,
+                             const int* __restrict__ c, const double* __restrict__ v,
+                             const int* __restrict__ map, double* vals) {
+  extern __shared__ double slab[];   // R * nd, R = kCsrWalkRows * warps per block
+  const int warp = threadIdx.x >> 5;
+  for (int b0 = blockIdx.x * R; b0 < nrows; b0 += gridDim.x * R) {
+    const int rows = min(R, nrows - b0);
+    const int total = rows * nd;
+    for (int t = threadIdx.x; t < total; t += blockDim.x) slab[t] = 0.0;
+    __syncthreads();
+    const int r0 = b0 + warp * kCsrWalkRows;
+    if (r0 < b0 + rows) {
+      const int r1 = min(r0 + kCsrWalkRows, b0 + rows);
+      csr_warp_walk<4>(off, r0, r1, [&](int k) { return ColVal{__ldg(c + k), __ldg(v + k)}; },
+                       [&](int kb, int k1, const int (&rr)[4], const ColVal (&e)[4]) {
+                         const int lane = threadIdx.x & 31;
+                         int j[4];
+#pragma unroll
+                         for (int u = 0; u < 4; ++u)   // the map loads in flight together
+                           j[u] = kb + 32 * u + lane < k1
+                                      ? __ldg(map + ((int64_t)e[u].c - rr[u] + nrows - 1))
+                                      : 0;
+#pragma unroll
+                         for (int u = 0; u < 4; ++u)
+                           if (kb + 32 * u + lane < k1) slab[(rr[u] - b0) * nd + j[u]] = e[u].v;
+                       });
+    }
+    __syncthreads();
+    double* out = vals + (int64_t)b0 * nd;
+    for (int t = threadIdx.x; t < total; t += blockDim.x) out[t] = slab[t];
+    __syncthreads();
+  }
+}
+
+// row index of every entry (COO target from a canonical CSR source)
+__global__ void csr_rows_walk(int nrows, const int* __restrict__ off, int* rows) {
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int r0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kCsrWalkRows; r0 < nrows;
+       r0 += nwarps * kCsrWalkRows)
+    csr_warp_walk<4>(off, r0, min(r0 + kCsrWalkRows, nrows), [](int) { return 0; },
+                     [&](int kb, int k1, const int (&rr)[4], const int (&)[4]) {
+                       const int lane = threadIdx.x & 31;
+#pragma unroll
+                       for (int u = 0; u < 4; ++u)
+                         if (kb + 32 * u + lane < k1) rows[kb + 32 * u + lane] = rr[u];
+                     });
+}
+
 struct FlagAt {
   const unsigned char* f;
   __device__ int operator()(int64_t k) const { return f[k]; }
@@ -460,6 +581,8 @@ static void free_job(ds_convert_job* job) {
   if (job->own_v && job->v) cudaFreeAsync(job->v, st);
   if (job->diag_map) cudaFreeAsync(job->diag_map, st);
   if (job->dia_off) cudaFreeAsync(job->dia_off, st);
+  if (job->dsrc_start) cudaFreeAsync(job->dsrc_start, st);
+  if (job->flags) cudaFreeAsync(job->flags, st);
   delete job;
 }
 
@@ -473,12 +596,15 @@ static int size_target(ds_convert_job* job, int64_t fill_limit, int64_t* out_nnz
   const int64_t D = job->nrows + job->ncols - 1;
   int64_t nd = 0;
   if (D > 0 && job->nnz > 0) {
-    unsigned char* flags = nullptr;
-    DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&flags), D, st));
-    DS_CUDA(cudaMemsetAsync(flags, 0, D, st));
-    mark_diags<<<grid1d(job->nnz), 256, 0, st>>>(job->nnz, (int)job->nrows, job->r, job->c,
-                                                 flags);
-    DS_LAUNCH_CHECK("mark_diags");
+    unsigned char* flags = job->flags;
+    job->flags = nullptr;
+    if (!flags) {
+      DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&flags), D, st));
+      DS_CUDA(cudaMemsetAsync(flags, 0, D, st));
+      mark_diags<<<grid1d(job->nnz), 256, 0, st>>>(job->nnz, (int)job->nrows, job->r, job->c,
+                                                   flags);
+      DS_LAUNCH_CHECK("mark_diags");
+    }
     DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&job->diag_map), D * sizeof(int), st));
     int rc = exclusive_scan(D, FlagAt{flags}, job->diag_map, &nd, st);
     if (rc) return rc;
@@ -826,6 +952,7 @@ extern "C" int ds_convert_begin_coo(int64_t nrows, int64_t ncols, int64_t nnz, c
                                     int64_t fill_limit, void* stream, ds_convert_job** job,
                                     int64_t* out_nnz, int64_t* out_ndiags) {
   *job = nullptr;
+  if (fill_limit < 0) fill_limit = 10 * std::max(nnz, nrows);   // datamove.py:55-57
   if (!dims_ok(nrows, ncols, nnz)) return DS_ERR_NOT_SUPPORTED;
   ds_convert_job* j = new_job(nrows, ncols, target, stream);
   int rc = canonicalize(j, nnz, rows, cols, values, false);
@@ -836,14 +963,48 @@ extern "C" int ds_convert_begin_coo(int64_t nrows, int64_t ncols, int64_t nnz, c
   return begin_common(j, fill_limit, job, out_nnz, out_ndiags);
 }
 
+static unsigned csr_walk_grid(int64_t nrows) {   // 8 warps per block
+  return (unsigned)std::max<int64_t>(
+      1, min64(ceil_div(nrows, kCsrWalkRows * 8), (int64_t)sm_count() * 8));
+}
+
 extern "C" int ds_convert_begin_csr(int64_t nrows, int64_t ncols, int64_t nnz,
                                     const int32_t* row_offsets, const int32_t* cols,
                                     const double* values, int target, int64_t fill_limit,
                                     void* stream, ds_convert_job** job, int64_t* out_nnz,
                                     int64_t* out_ndiags) {
   *job = nullptr;
+  if (fill_limit < 0) fill_limit = 10 * std::max(nnz, nrows);   // datamove.py:55-57
   if (!dims_ok(nrows, ncols, nnz)) return DS_ERR_NOT_SUPPORTED;
   ds_convert_job* j = new_job(nrows, ncols, target, stream);
+  if (nnz > 0 && nrows > 0) {
+    // canonical already (the common case)?  then no COO proxy at all: a DIA
+    // target takes its diagonal census in the same pass, a CSR / COO target
+    // copies (expands) the source at finish
+    cudaStream_t st = j->st;
+    const bool dia = target == DS_FMT_DIA;
+    const int64_t flag_bytes = dia ? (nrows + ncols - 1 + 3) & ~int64_t(3) : 0;
+    unsigned char* scratch = nullptr;
+    DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scratch), flag_bytes + 4, st));
+    DS_CUDA(cudaMemsetAsync(scratch, 0, flag_bytes + 4, st));
+    int* bad = reinterpret_cast<int*>(scratch + flag_bytes);
+    csr_check_mark<<<csr_walk_grid(nrows), 256, 0, st>>>((int)nrows, row_offsets, cols,
+                                                         dia ? scratch : nullptr, bad);
+    DS_LAUNCH_CHECK("csr_check_mark");
+    int bad_h = 1;
+    DS_CUDA(cudaMemcpyAsync(&bad_h, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+    DS_CUDA(cudaStreamSynchronize(st));
+    if (!bad_h) {
+      j->nnz = nnz;
+      j->csr_off = row_offsets;
+      j->c = const_cast<int*>(cols);
+      j->v = const_cast<double*>(values);
+      if (dia) j->flags = scratch;
+      else DS_CUDA(cudaFreeAsync(scratch, st));
+      return begin_common(j, fill_limit, job, out_nnz, out_ndiags);
+    }
+    DS_CUDA(cudaFreeAsync(scratch, st));   // not canonical: the general path
+  }
   int* rows = nullptr;
   if (nnz > 0) {
     DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&rows), nnz * 4, j->st));
@@ -858,6 +1019,20 @@ extern "C" int ds_convert_begin_csr(int64_t nrows, int64_t ncols, int64_t nnz,
   return begin_common(j, fill_limit, job, out_nnz, out_ndiags);
 }
 
+static unsigned dia_walk_grid(int64_t ngroups) {   // 8 warps (groups) per block
+  return (unsigned)std::max<int64_t>(1, min64(ceil_div(ngroups, 8), (int64_t)sm_count() * 8));
+}
+
+// entries of a DIA source straight into the target (row_offsets: CSR target)
+static int dia_emit_into(ds_convert_job* job, int* row_off, int* rows, int* cols, double* values) {
+  const int64_t ngroups = ceil_div(job->nrows, kDiaGroupRows);
+  dia_group_emit<<<dia_walk_grid(ngroups), 256, 0, job->st>>>(
+      job->nrows, (int)job->ncols, job->dsrc_nd, job->dsrc_off, job->dsrc_vals, ngroups,
+      job->dsrc_start, row_off, rows, cols, values);
+  DS_LAUNCH_CHECK("dia_group_emit");
+  return DS_OK;
+}
+
 extern "C" int ds_convert_begin_dia(int64_t nrows, int64_t ncols, int32_t ndiags,
                                     const int32_t* offsets, const double* values, int target,
                                     int64_t fill_limit, void* stream, ds_convert_job** job,
@@ -868,55 +1043,64 @@ extern "C" int ds_convert_begin_dia(int64_t nrows, int64_t ncols, int32_t ndiags
   cudaStream_t st = j->st;
   int64_t nc = 0;
   if (nrows > 0 && ndiags > 0) {
-    int *counts = nullptr, *start = nullptr;
-    DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&counts), nrows * sizeof(int), st));
-    DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&start), nrows * sizeof(int), st));
-    const size_t slab = (size_t)kDiaWalkRows * ndiags * sizeof(double);
-    const size_t emit_smem = slab * 2 + (size_t)kDiaWalkRows * ndiags * 8;   // + rows, cols
-    const bool staged = emit_smem <= 200 * 1024;
-    const unsigned gw = (unsigned)min64(ceil_div(nrows, kDiaWalkRows), (int64_t)sm_count() * 8);
-    if (staged) {
-      int rc0 = allow_dynamic_smem(reinterpret_cast<const void*>(dia_row_counts), slab);
-      if (!rc0) rc0 = allow_dynamic_smem(reinterpret_cast<const void*>(dia_emit), emit_smem);
-      if (rc0) {
-        free_job(j);
-        return rc0;
-      }
-      dia_row_counts<<<gw, kDiaWalkRows, slab, st>>>((int)nrows, (int)ncols, ndiags, offsets,
-                                                     values, counts);
-      DS_LAUNCH_CHECK("dia_row_counts");
-    }
-    int rc = staged ? exclusive_scan(nrows, ArrayAt{counts}, start, &nc, st)
-                    : exclusive_scan(nrows,
-                                     DiaRowCount{(int)nrows, (int)ncols, ndiags, offsets, values},
-                                     start, &nc, st);
+    const int64_t ngroups = ceil_div(nrows, kDiaGroupRows);
+    int *gcount = nullptr, *gstart = nullptr;
+    DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&gcount), ngroups * sizeof(int), st));
+    DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&gstart), ngroups * sizeof(int), st));
+    dia_group_counts<<<dia_walk_grid(ngroups), 256, 0, st>>>(nrows, (int)ncols, ndiags, offsets,
+                                                             values, ngroups, gcount);
+    DS_LAUNCH_CHECK("dia_group_counts");
+    int rc = exclusive_scan(ngroups, ArrayAt{gcount}, gstart, &nc, st);
+    DS_CUDA(cudaFreeAsync(gcount, st));
     if (rc) {
+      cudaFreeAsync(gstart, st);
       free_job(j);
       return rc;
     }
-    if (nc > 0) {
-      DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&j->r), nc * 4, st));
-      DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&j->c), nc * 4, st));
-      DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&j->v), nc * 8, st));
-      j->own_r = j->own_c = j->own_v = true;
-      if (staged)
-        dia_emit<<<gw, kDiaWalkRows, emit_smem, st>>>((int)nrows, (int)ncols, ndiags, offsets,
-                                                      values, start, (int)nc, j->r, j->c, j->v);
-      else
-        dia_emit_direct<<<grid1d(nrows), 256, 0, st>>>((int)nrows, (int)ncols, ndiags, offsets,
-                                                       values, start, j->r, j->c, j->v);
-      DS_LAUNCH_CHECK("dia_emit");
+    j->dsrc_off = offsets;
+    j->dsrc_vals = values;
+    j->dsrc_nd = ndiags;
+    j->dsrc_start = gstart;
+    if (target == DS_FMT_DIA) {   // the canonical COO feeds the diagonal census
+      if (nc > 0) {
+        DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&j->r), nc * 4, st));
+        DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&j->c), nc * 4, st));
+        DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&j->v), nc * 8, st));
+        j->own_r = j->own_c = j->own_v = true;
+        j->nnz = nc;
+        rc = dia_emit_into(j, nullptr, j->r, j->c, j->v);
+        if (rc) {
+          free_job(j);
+          return rc;
+        }
+      }
+      cudaFreeAsync(gstart, st);
+      j->dsrc_start = nullptr;
     }
-    DS_CUDA(cudaFreeAsync(counts, st));
-    DS_CUDA(cudaFreeAsync(start, st));
   }
   j->nnz = nc;
+  if (fill_limit < 0) fill_limit = 10 * std::max(nc, nrows);   // DIA nnz = the compacted count
   return begin_common(j, fill_limit, job, out_nnz, out_ndiags);
 }
+
+__global__ void set_last_offset(int* off, int64_t nrows, int64_t nnz) { off[nrows] = (int)nnz; }
 
 extern "C" int ds_convert_finish_coo(ds_convert_job* job, int32_t* rows, int32_t* cols,
                                      double* values) {
   cudaStream_t st = job->st;
+  if (job->dsrc_start) {
+    const int rc = job->nnz > 0 ? dia_emit_into(job, nullptr, rows, cols, values) : DS_OK;
+    free_job(job);
+    return rc;
+  }
+  if (job->csr_off && job->nnz > 0) {   // canonical CSR source: expand the rows in place
+    csr_rows_walk<<<csr_walk_grid(job->nrows), 256, 0, st>>>((int)job->nrows, job->csr_off, rows);
+    DS_LAUNCH_CHECK("csr_rows_walk");
+    DS_CUDA(cudaMemcpyAsync(cols, job->c, job->nnz * 4, cudaMemcpyDeviceToDevice, st));
+    DS_CUDA(cudaMemcpyAsync(values, job->v, job->nnz * 8, cudaMemcpyDeviceToDevice, st));
+    free_job(job);
+    return DS_OK;
+  }
   if (job->nnz > 0) {
     DS_CUDA(cudaMemcpyAsync(rows, job->r, job->nnz * 4, cudaMemcpyDeviceToDevice, st));
     DS_CUDA(cudaMemcpyAsync(cols, job->c, job->nnz * 4, cudaMemcpyDeviceToDevice, st));
@@ -929,6 +1113,23 @@ extern "C" int ds_convert_finish_coo(ds_convert_job* job, int32_t* rows, int32_t
 extern "C" int ds_convert_finish_csr(ds_convert_job* job, int32_t* row_offsets, int32_t* cols,
                                      double* values) {
   cudaStream_t st = job->st;
+  if (job->dsrc_start) {   // row offsets written by the emit pass
+    set_last_offset<<<1, 1, 0, st>>>(row_offsets, job->nrows, job->nnz);
+    DS_LAUNCH_CHECK("set_last_offset");
+    const int rc = dia_emit_into(job, row_offsets, nullptr, cols, values);
+    free_job(job);
+    return rc;
+  }
+  if (job->csr_off) {   // canonical CSR source: a copy
+    DS_CUDA(cudaMemcpyAsync(row_offsets, job->csr_off, (job->nrows + 1) * 4,
+                            cudaMemcpyDeviceToDevice, st));
+    if (job->nnz > 0) {
+      DS_CUDA(cudaMemcpyAsync(cols, job->c, job->nnz * 4, cudaMemcpyDeviceToDevice, st));
+      DS_CUDA(cudaMemcpyAsync(values, job->v, job->nnz * 8, cudaMemcpyDeviceToDevice, st));
+    }
+    free_job(job);
+    return DS_OK;
+  }
   rows_to_offsets<<<grid1d(job->nnz + 1 > job->nrows + 1 ? job->nnz + 1 : job->nrows + 1), 256, 0,
                     st>>>(job->nnz, (int)job->nrows, job->r, row_offsets);
   DS_LAUNCH_CHECK("rows_to_offsets");
@@ -947,6 +1148,21 @@ extern "C" int ds_convert_finish_dia(ds_convert_job* job, int32_t* offsets, doub
     DS_CUDA(cudaMemcpyAsync(offsets, job->dia_off, nd * sizeof(int), cudaMemcpyDeviceToDevice,
                             st));
     const int64_t slots = nd * job->nrows;
+    const int R = kCsrWalkRows * 8;   // 8 warps
+    if (job->csr_off && (int64_t)R * nd * 8 <= 48 * 1024) {
+      dia_fill_csr<<<csr_walk_grid(job->nrows), 256, (size_t)R * nd * 8, st>>>(
+          (int)job->nrows, (int)nd, R, job->csr_off, job->c, job->v, job->diag_map, values);
+      DS_LAUNCH_CHECK("dia_fill_csr");
+      free_job(job);
+      return DS_OK;
+    }
+    if (job->csr_off && job->nnz > 0) {   // slab too wide for shared memory: expand the rows
+      DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&job->r), job->nnz * 4, st));
+      job->own_r = true;
+      csr_expand_rows<<<grid1d(job->nrows * 8), 256, 0, st>>>((int)job->nrows, job->csr_off,
+                                                               job->r);
+      DS_LAUNCH_CHECK("csr_expand_rows");
+    }
     zero_f64<<<grid1d(slots), 256, 0, st>>>(slots, values);
     dia_scatter<<<grid1d(job->nnz), 256, 0, st>>>(job->nnz, (int)job->nrows, nd, job->r, job->c,
                                                   job->v, job->diag_map, values);

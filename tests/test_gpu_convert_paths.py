@@ -1,0 +1,217 @@
+"""GPU parity of the conversion fast paths (ds_convert.cu) against the
+oracle's COO-proxy restatement (datamove.py:208-295): bitwise.
+
+- DIA source: the warp-group stream compaction (dia_group_counts /
+  dia_group_emit) for CSR, COO and DIA targets -- ragged diagonal counts
+  (1, below / at / above a warp), rows not a multiple of the group, slots
+  outside the matrix, explicit and signed zeros (dropped);
+- CSR source, DIA target: the order check + diagonal census in one pass
+  (csr_check_mark) and the shared-memory slab fill (dia_fill_csr); rows that
+  are not canonical (unsorted, duplicates) take the general path; slabs too
+  wide for shared memory take the expanded-rows scatter.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+import paper_2209_06478_b200 as ds  # noqa: E402
+from oracle import dynsparse_oracle as O  # noqa: E402
+
+DEV = torch.device("cuda", 0)
+BIG = 2 ** 40
+
+
+def host_arrays(m):
+    p = m.payload if isinstance(m, ds.DynamicMatrix) else m
+    if isinstance(p, ds.CsrMatrix):
+        return [p.row_offsets, p.col_indices, p.values]
+    if isinstance(p, ds.CooMatrix):
+        return [p.row_indices, p.col_indices, p.values]
+    return [p.offsets, p.values]
+
+
+def oracle_arrays(m):
+    if isinstance(m, O.OCsr):
+        return [m.offsets, m.cols, m.vals]
+    if isinstance(m, O.OCoo):
+        return [m.rows, m.cols, m.vals]
+    return [m.offsets, m.values]
+
+
+def assert_same(dev_m, ora_m, what):
+    got = [t.cpu().numpy() for t in host_arrays(dev_m)]
+    want = oracle_arrays(ora_m)
+    assert len(got) == len(want), what
+    for g, w in zip(got, want):
+        assert g.shape == np.asarray(w).shape, what
+        if g.dtype.kind == "f":
+            assert g.tobytes() == np.asarray(w, dtype=np.float64).tobytes(), what
+        else:
+            assert np.array_equal(g.astype(np.int64), np.asarray(w).astype(np.int64)), what
+
+
+def random_dia(rng, nrows, ncols, nd):
+    offs = np.sort(rng.choice(np.arange(-nrows + 1, ncols), size=nd, replace=False))
+    vals = rng.standard_normal((nrows, nd))
+    vals[rng.random(vals.shape) < 0.1] = 0.0
+    vals[rng.random(vals.shape) < 0.05] = -0.0
+    return offs.astype(np.int64), vals
+
+
+@pytest.mark.parametrize("nrows,ncols,nd", [(1, 1, 1), (37, 37, 1), (1000, 1000, 27),
+                                            (333, 500, 31), (257, 300, 32), (129, 90, 33),
+                                            (70, 2000, 70)])
+def test_dia_source_every_target(nrows, ncols, nd):
+    rng = np.random.default_rng(nrows * 7 + nd)
+    offs, vals = random_dia(rng, nrows, ncols, nd)
+    src = ds.DiaMatrix(nrows, ncols, offs, vals, ds.MemorySpace.DEVICE, DEV)
+    ora = O.dia(nrows, ncols, offs, vals)
+    for tgt, fid in ((O.CSR, ds.FormatId.CSR), (O.COO, ds.FormatId.COO),
+                     (O.DIA, ds.FormatId.DIA)):
+        want = O.convert(ora, tgt, fill_limit=BIG)
+        got = ds.convert(src, fid, fill_limit=BIG)
+        assert_same(got, want, (nrows, ncols, nd, fid))
+
+
+def test_dia_source_all_zero_and_out_of_range():
+    """Every slot zero or outside the matrix: nnz == 0, row offsets all 0."""
+    nrows, ncols = 100, 50
+    offs = np.array([-200, 0, 60], dtype=np.int64)
+    vals = np.zeros((nrows, 3))
+    vals[:, 0] = 1.0     # diagonal -200: entirely outside
+    vals[:, 2] = 2.0     # diagonal 60: outside (ncols 50)
+    vals[:, 1] = -0.0
+    src = ds.DiaMatrix(nrows, ncols, offs, vals, ds.MemorySpace.DEVICE, DEV)
+    ora = O.dia(nrows, ncols, offs, vals)
+    for tgt, fid in ((O.CSR, ds.FormatId.CSR), (O.COO, ds.FormatId.COO)):
+        assert_same(ds.convert(src, fid, fill_limit=BIG), O.convert(ora, tgt, fill_limit=BIG), fid)
+
+
+def random_csr(rng, nrows, ncols, lengths, sort=True):
+    offs = np.zeros(nrows + 1, dtype=np.int64)
+    offs[1:] = np.cumsum(lengths)
+    cols = np.empty(offs[-1], dtype=np.int64)
+    for i in range(nrows):
+        c = rng.choice(ncols, size=int(lengths[i]), replace=False)
+        cols[offs[i]:offs[i + 1]] = np.sort(c) if sort else c
+    vals = rng.standard_normal(offs[-1])
+    vals[rng.random(vals.size) < 0.05] = -0.0
+    return offs, cols, vals
+
+
+@pytest.mark.parametrize("nrows,ncols,maxlen", [(1, 1, 1), (300, 300, 7), (1000, 1200, 27),
+                                                (513, 40, 30)])
+def test_csr_to_dia_canonical(nrows, ncols, maxlen):
+    rng = np.random.default_rng(nrows + maxlen)
+    lengths = rng.integers(0, min(maxlen, ncols) + 1, nrows)
+    offs, cols, vals = random_csr(rng, nrows, ncols, lengths)
+    src = ds.CsrMatrix(nrows, ncols, offs, cols, vals, ds.MemorySpace.DEVICE, DEV)
+    want = O.convert(O.csr(nrows, ncols, offs, cols, vals), O.DIA, fill_limit=BIG)
+    assert_same(ds.convert(src, ds.FormatId.DIA, fill_limit=BIG), want, (nrows, ncols))
+
+
+def banded_csr(rng, nrows, ncols, band):
+    """Rows take a random subset of the in-range diagonals of ``band``."""
+    lengths, cols = [], []
+    for i in range(nrows):
+        c = np.array([i + d for d in band if 0 <= i + d < ncols], dtype=np.int64)
+        c = c[rng.random(c.size) < 0.8]
+        if 5 <= i < 8:
+            c = c[:0]                      # empty rows
+        lengths.append(c.size)
+        cols.append(c)
+    offs = np.zeros(nrows + 1, dtype=np.int64)
+    offs[1:] = np.cumsum(lengths)
+    cols = np.concatenate(cols) if cols else np.zeros(0, np.int64)
+    vals = rng.standard_normal(offs[-1])
+    vals[rng.random(vals.size) < 0.05] = -0.0
+    return offs, cols, vals
+
+
+@pytest.mark.parametrize("nrows,ncols,nbands", [(1, 1, 1), (129, 129, 5), (1000, 900, 27),
+                                                (2047, 2100, 48), (300, 310, 49)])
+def test_csr_to_dia_banded_slab_fill(nrows, ncols, nbands):
+    """A few diagonals (the slab fits shared memory: the warp-walk fill), rows
+    not a multiple of the block, empty rows, signed zeros; 49 diagonals take
+    the expanded-rows scatter."""
+    rng = np.random.default_rng(nrows + nbands)
+    band = np.sort(rng.choice(np.arange(-60, 61), size=nbands, replace=False))
+    offs, cols, vals = banded_csr(rng, nrows, ncols, band)
+    src = ds.CsrMatrix(nrows, ncols, offs, cols, vals, ds.MemorySpace.DEVICE, DEV)
+    want = O.convert(O.csr(nrows, ncols, offs, cols, vals), O.DIA, fill_limit=BIG)
+    assert want.offsets.size <= nbands
+    assert_same(ds.convert(src, ds.FormatId.DIA, fill_limit=BIG), want, (nrows, nbands))
+    # a duplicate in one row: not canonical -> general path (summed)
+    if offs[-1] > 2 and nrows > 10:
+        cols2 = cols.copy()
+        k = int(offs[nrows // 2])
+        if offs[nrows // 2 + 1] - k >= 2:
+            cols2[k + 1] = cols2[k]
+            src = ds.CsrMatrix(nrows, ncols, offs, cols2, vals, ds.MemorySpace.DEVICE, DEV)
+            want = O.convert(O.csr(nrows, ncols, offs, cols2, vals), O.DIA, fill_limit=BIG)
+            assert_same(ds.convert(src, ds.FormatId.DIA, fill_limit=BIG), want, "dup")
+
+
+def test_csr_to_dia_not_canonical_takes_general_path():
+    rng = np.random.default_rng(11)
+    nrows, ncols = 400, 400
+    lengths = rng.integers(1, 12, nrows)
+    offs, cols, vals = random_csr(rng, nrows, ncols, lengths, sort=False)
+    cols[offs[5] + 1] = cols[offs[5]]   # a duplicate (summed)
+    src = ds.CsrMatrix(nrows, ncols, offs, cols, vals, ds.MemorySpace.DEVICE, DEV)
+    want = O.convert(O.csr(nrows, ncols, offs, cols, vals), O.DIA, fill_limit=BIG)
+    assert_same(ds.convert(src, ds.FormatId.DIA, fill_limit=BIG), want, "unsorted")
+
+
+def test_csr_to_dia_wide_slab_and_fill_limit():
+    """> 6143 diagonals: the slab does not fit shared memory (expanded-rows
+    scatter); the fill limit still trips before allocation."""
+    rng = np.random.default_rng(12)
+    nrows, ncols = 40, 9000
+    lengths = np.full(nrows, 300)
+    offs, cols, vals = random_csr(rng, nrows, ncols, lengths)
+    src = ds.CsrMatrix(nrows, ncols, offs, cols, vals, ds.MemorySpace.DEVICE, DEV)
+    want = O.convert(O.csr(nrows, ncols, offs, cols, vals), O.DIA, fill_limit=BIG)
+    assert want.offsets.size > 6143
+    assert_same(ds.convert(src, ds.FormatId.DIA, fill_limit=BIG), want, "wide")
+    with pytest.raises(ds.DiaFillOverflow):
+        ds.convert(src, ds.FormatId.DIA, fill_limit=int(want.offsets.size) * nrows - 1)
+
+
+def test_stencil_round_trip_dia_csr():
+    """The 27-point stencil CSR -> DIA -> CSR -> COO -> DIA: every hop bitwise
+    equal to the oracle's."""
+    part = ds.generate_problem(ds.GridSpec(20, 18, 16), space=ds.MemorySpace.DEVICE,
+                               device=DEV).partitions[0]
+    ref = O.stencil_partition(20, 18, 16).a_full
+    d = ds.convert(part.a_full, ds.FormatId.DIA)
+    od = O.convert(ref, O.DIA)
+    assert_same(d, od, "csr->dia")
+    c = ds.convert(d, ds.FormatId.CSR)
+    oc = O.convert(od, O.CSR)
+    assert_same(c, oc, "dia->csr")
+    q = ds.convert(c, ds.FormatId.COO)
+    oq = O.convert(oc, O.COO)
+    assert_same(q, oq, "csr->coo")
+    assert_same(ds.convert(q, ds.FormatId.DIA), O.convert(oq, O.DIA), "coo->dia")
+
+
+@pytest.mark.parametrize("sort", [True, False])
+def test_csr_source_to_csr_and_coo(sort):
+    """Canonical CSR: copied / rows expanded in place (csr_rows_walk);
+    unsorted rows: sorted through the general path."""
+    rng = np.random.default_rng(21 + sort)
+    nrows, ncols = 1500, 700
+    lengths = rng.integers(0, 40, nrows)
+    lengths[100] = 600                      # a long row (many chunks for one lane group)
+    offs, cols, vals = random_csr(rng, nrows, ncols, lengths, sort=sort)
+    src = ds.CsrMatrix(nrows, ncols, offs, cols, vals, ds.MemorySpace.DEVICE, DEV)
+    ora = O.csr(nrows, ncols, offs, cols, vals)
+    for tgt, fid in ((O.CSR, ds.FormatId.CSR), (O.COO, ds.FormatId.COO)):
+        assert_same(ds.convert(src, fid, fill_limit=BIG), O.convert(ora, tgt, fill_limit=BIG),
+                    (sort, fid))
