@@ -356,30 +356,45 @@ __global__ void mark_diags(int64_t nnz, int nrows, const int* __restrict__ r,
 // warp's rows 32 at a time (coalesced, U chunks of loads in flight); each
 // lane tracks the row of its entry incrementally (rows are monotone in k, so
 // a lane moves ~1 row per chunk) instead of searching the offsets.
-constexpr int kCsrWalkRows = 16;    // rows per warp
+constexpr int kCsrWalkRows = 16;    // rows per warp (<= 31: the offsets live in one lane each)
+// Lane t <= r1 - r0 holds off[r0 + t] (the rest INT_MAX): an entry's row is
+// found by a 5-step binary search over the lanes (shuffles, no memory).  The
+// callers load the next group's offsets before walking the current group.
+__device__ __forceinline__ int walk_offsets(const int* __restrict__ off, int nrows, int r0) {
+  const int lane = threadIdx.x & 31;
+  const int r1 = min(r0 + kCsrWalkRows, nrows);
+  return r0 < nrows && lane <= r1 - r0 ? __ldg(off + r0 + lane) : 0x7fffffff;
+}
 // body(kb, k1, rows[U], loaded[U]): lane's entry of chunk u is kb + 32u + lane
 template <int U, class Load, class Body>
-__device__ __forceinline__ void csr_warp_walk(const int* __restrict__ off, int r0, int r1,
-                                              Load&& load, Body&& body) {
+__device__ __forceinline__ void csr_warp_walk(int ot, int r0, int r1, Load&& load, Body&& body) {
   const int lane = threadIdx.x & 31;
-  const int k1 = __ldg(off + r1);
-  int row = r0;
-  for (int kb = __ldg(off + r0); kb < k1; kb += 32 * U) {
-    decltype(load(0)) x[U];
+  const int k1 = __shfl_sync(0xffffffffu, ot, r1 - r0);
+  int kb = __shfl_sync(0xffffffffu, ot, 0);
+  decltype(load(0)) x[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+    if (kb + 32 * u + lane < k1) x[u] = load(kb + 32 * u + lane);
+  for (; kb < k1; kb += 32 * U) {
+    decltype(load(0)) xn[U];   // the next chunks' loads in flight while this one is processed
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int k = kb + 32 * u + lane;
-      if (k < k1) x[u] = load(k);
+      const int k = kb + 32 * (U + u) + lane;
+      if (k < k1) xn[u] = load(k);
     }
     int rr[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int k = kb + 32 * u + lane;
-      if (k < k1)
-        while (__ldg(off + row + 1) <= k) ++row;
-      rr[u] = row;
+      int lo = 0;
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1)
+        if (__shfl_sync(0xffffffffu, ot, lo + step) <= k) lo += step;
+      rr[u] = r0 + lo;
     }
     body(kb, k1, rr, x);
+#pragma unroll
+    for (int u = 0; u < U; ++u) x[u] = xn[u];
   }
 }
 
@@ -393,11 +408,13 @@ __global__ void csr_check_mark(int nrows, const int* __restrict__ off, const int
   const int lane = threadIdx.x & 31;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   int mybad = 0;
-  for (int r0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kCsrWalkRows; r0 < nrows;
-       r0 += nwarps * kCsrWalkRows) {
+  int r0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kCsrWalkRows;
+  int ot = walk_offsets(off, nrows, r0);
+  for (; r0 < nrows; r0 += nwarps * kCsrWalkRows) {
     const int r1 = min(r0 + kCsrWalkRows, nrows);
+    const int ot_next = walk_offsets(off, nrows, r0 + nwarps * kCsrWalkRows);
     int carry = -1, carry_row = -1;   // previous chunk's last entry (lane 31)
-    csr_warp_walk<8>(off, r0, r1, [&](int k) { return __ldg(c + k); },
+    csr_warp_walk<8>(ot, r0, r1, [&](int k) { return __ldg(c + k); },
                      [&](int kb, int k1, const int (&rr)[8], const int (&cc)[8]) {
 #pragma unroll
                        for (int u = 0; u < 8; ++u) {
@@ -421,6 +438,7 @@ __global__ void csr_check_mark(int nrows, const int* __restrict__ off, const int
                          }
                        }
                      });
+    ot = ot_next;
   }
   if (__syncthreads_or(mybad) && threadIdx.x == 0) atomicOr(bad, 1);
 }
@@ -430,15 +448,17 @@ __global__ void dia_fill_csr(int nrows, int nd, int R, const int* __restrict__ o
                              const int* __restrict__ map, double* vals) {
   extern __shared__ double slab[];   // R * nd, R = kCsrWalkRows * warps per block
   const int warp = threadIdx.x >> 5;
+  int ot = walk_offsets(off, nrows, blockIdx.x * R + warp * kCsrWalkRows);
   for (int b0 = blockIdx.x * R; b0 < nrows; b0 += gridDim.x * R) {
     const int rows = min(R, nrows - b0);
     const int total = rows * nd;
+    const int r0 = b0 + warp * kCsrWalkRows;
+    const int ot_next = walk_offsets(off, nrows, r0 + gridDim.x * R);
     for (int t = threadIdx.x; t < total; t += blockDim.x) slab[t] = 0.0;
     __syncthreads();
-    const int r0 = b0 + warp * kCsrWalkRows;
     if (r0 < b0 + rows) {
       const int r1 = min(r0 + kCsrWalkRows, b0 + rows);
-      csr_warp_walk<4>(off, r0, r1, [&](int k) { return ColVal{__ldg(c + k), __ldg(v + k)}; },
+      csr_warp_walk<4>(ot, r0, r1, [&](int k) { return ColVal{__ldg(c + k), __ldg(v + k)}; },
                        [&](int kb, int k1, const int (&rr)[4], const ColVal (&e)[4]) {
                          const int lane = threadIdx.x & 31;
                          int j[4];
@@ -456,21 +476,26 @@ __global__ void dia_fill_csr(int nrows, int nd, int R, const int* __restrict__ o
     double* out = vals + (int64_t)b0 * nd;
     for (int t = threadIdx.x; t < total; t += blockDim.x) out[t] = slab[t];
     __syncthreads();
+    ot = ot_next;
   }
 }
 
 // row index of every entry (COO target from a canonical CSR source)
 __global__ void csr_rows_walk(int nrows, const int* __restrict__ off, int* rows) {
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (int r0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kCsrWalkRows; r0 < nrows;
-       r0 += nwarps * kCsrWalkRows)
-    csr_warp_walk<4>(off, r0, min(r0 + kCsrWalkRows, nrows), [](int) { return 0; },
+  int r0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kCsrWalkRows;
+  int ot = walk_offsets(off, nrows, r0);
+  for (; r0 < nrows; r0 += nwarps * kCsrWalkRows) {
+    const int ot_next = walk_offsets(off, nrows, r0 + nwarps * kCsrWalkRows);
+    csr_warp_walk<4>(ot, r0, min(r0 + kCsrWalkRows, nrows), [](int) { return 0; },
                      [&](int kb, int k1, const int (&rr)[4], const int (&)[4]) {
                        const int lane = threadIdx.x & 31;
 #pragma unroll
                        for (int u = 0; u < 4; ++u)
                          if (kb + 32 * u + lane < k1) rows[kb + 32 * u + lane] = rr[u];
                      });
+    ot = ot_next;
+  }
 }
 
 struct FlagAt {
