@@ -19,6 +19,7 @@
 // SortPairs on (row*ncols+col, index) keys limited to the needed bits) -- a
 // documented stop-gap until a hand-written onesweep lands.
 #include <cub/device/device_radix_sort.cuh>
+#include <vector>
 
 #include "ds_common.cuh"
 #include "ds_kernels.cuh"
@@ -1086,21 +1087,47 @@ extern "C" int ds_convert_begin_dia(int64_t nrows, int64_t ncols, int32_t ndiags
     j->dsrc_vals = values;
     j->dsrc_nd = ndiags;
     j->dsrc_start = gstart;
-    if (target == DS_FMT_DIA) {   // the canonical COO feeds the diagonal census
+    // slot order is canonical only for strictly ascending offsets; otherwise
+    // (unsorted or repeated diagonals) the entries go through the proxy's sort
+    // and duplicate sums like any other source (datamove.py:208-235)
+    std::vector<int> h_off(ndiags);
+    DS_CUDA(cudaMemcpyAsync(h_off.data(), offsets, ndiags * sizeof(int), cudaMemcpyDeviceToHost, st));
+    DS_CUDA(cudaStreamSynchronize(st));
+    bool ascending = true;
+    for (int q = 1; q < ndiags; ++q) ascending = ascending && h_off[q - 1] < h_off[q];
+    if (target == DS_FMT_DIA || !ascending) {   // materialise the (slot-order) COO
+      int *tr = nullptr, *tc = nullptr;
+      double* tv = nullptr;
       if (nc > 0) {
-        DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&j->r), nc * 4, st));
-        DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&j->c), nc * 4, st));
-        DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&j->v), nc * 8, st));
-        j->own_r = j->own_c = j->own_v = true;
+        DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tr), nc * 4, st));
+        DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tc), nc * 4, st));
+        DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tv), nc * 8, st));
         j->nnz = nc;
-        rc = dia_emit_into(j, nullptr, j->r, j->c, j->v);
-        if (rc) {
-          free_job(j);
-          return rc;
-        }
+        rc = dia_emit_into(j, nullptr, tr, tc, tv);
       }
       cudaFreeAsync(gstart, st);
       j->dsrc_start = nullptr;
+      if (!rc && ascending) {
+        j->r = tr;
+        j->c = tc;
+        j->v = tv;
+        j->own_r = j->own_c = j->own_v = nc > 0;
+      } else if (!rc) {
+        rc = canonicalize(j, nc, tr, tc, tv, true);   // frees tr (or adopts it)
+        if (j->c == tc) j->own_c = true;
+        else if (tc) cudaFreeAsync(tc, st);
+        if (j->v == tv) j->own_v = true;
+        else if (tv) cudaFreeAsync(tv, st);
+        if (!rc) {
+          const int64_t src_nnz = nc;
+          nc = j->nnz;
+          if (fill_limit < 0) fill_limit = 10 * std::max(src_nnz, nrows);
+        }
+      }
+      if (rc) {
+        free_job(j);
+        return rc;
+      }
     }
   }
   j->nnz = nc;

@@ -143,6 +143,10 @@ __global__ void __launch_bounds__(256, 1)   // 1 CTA/SM: registers for all 27 ga
   if (tid == 0) {
     int ng = 0, ok = nd <= 32;
     for (int j = 0; ok && j < nd; ++j) {
+      if (j > 0 && s_off[j] <= s_off[j - 1]) {   // windows need ascending offsets
+        ok = 0;
+        break;
+      }
       if (j == 0 || s_off[j] - s_off[j - 1] > 1) {
         if (ng == kXwGroups) { ok = 0; break; }
         s_pl.first[ng] = s_off[j];

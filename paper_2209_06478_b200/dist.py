@@ -357,8 +357,9 @@ def rank_cg(spec: GridSpec, part: PartitionData, split: SplitMatrix, tol: float 
 def profile_rank(part: PartitionData, split: SplitMatrix, reps: int = 20,
                  fill_limit: int | None = None) -> dict:
     """This rank's row of the tuner's TimingTable (tuner.py:53-120): every
-    (local, remote) combination converted in place (conversion wall time
-    recorded -- the cost of runtime switching), one warm-up, then the median
+    (local, remote) combination converted in place (wall time of a second,
+    warm-pool conversion recorded -- the cost of runtime switching; the first
+    also grows the memory pool), one warm-up, then the median
     of ``reps`` CUDA-event timings of local SpMV + remote spmv_add (the halo
     exchange excluded, like the reference's per_partition_ns).  Failed
     conversions are skipped; both parts are restored to CSR at the end.
@@ -383,9 +384,7 @@ def profile_rank(part: PartitionData, split: SplitMatrix, reps: int = 20,
     entries, skipped, conv = {}, [], {}
     for lf in FORMATS:
         for rf in remote_axis:
-            torch.cuda.synchronize(dev)
-            t0 = time.perf_counter()
-            try:
+            try:   # once untimed: fill-limit check, and the memory pool grows here
                 convert_inplace(split.local, lf, fill_limit)
                 convert_inplace(split.remote, rf, fill_limit)
             except DynSparseError:
@@ -393,6 +392,12 @@ def profile_rank(part: PartitionData, split: SplitMatrix, reps: int = 20,
                 convert_inplace(split.local, FormatId.CSR)
                 convert_inplace(split.remote, FormatId.CSR)
                 continue
+            convert_inplace(split.local, FormatId.CSR)
+            convert_inplace(split.remote, FormatId.CSR)
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()   # the switching cost proper (warm pool)
+            convert_inplace(split.local, lf, fill_limit)
+            convert_inplace(split.remote, rf, fill_limit)
             torch.cuda.synchronize(dev)
             conv[(lf, rf)] = time.perf_counter() - t0
             st = torch.cuda.current_stream(dev)

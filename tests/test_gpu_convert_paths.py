@@ -215,3 +215,22 @@ def test_csr_source_to_csr_and_coo(sort):
     for tgt, fid in ((O.CSR, ds.FormatId.CSR), (O.COO, ds.FormatId.COO)):
         assert_same(ds.convert(src, fid, fill_limit=BIG), O.convert(ora, tgt, fill_limit=BIG),
                     (sort, fid))
+
+
+@pytest.mark.parametrize("kind", ["unsorted", "repeated"])
+def test_dia_source_unsorted_or_repeated_offsets(kind):
+    """Offsets that are not strictly ascending: slot order is not canonical,
+    so the entries take the proxy's stable sort + duplicate sums (the oracle's
+    diagonal-major walk then lexsort, datamove.py:208-235)."""
+    rng = np.random.default_rng(31)
+    nrows, ncols = 300, 280
+    offs = np.array([5, -3, 0, 40, -100, 2], dtype=np.int64)
+    if kind == "repeated":
+        offs = np.array([-3, 0, 0, 2, 2, 2, 40], dtype=np.int64)
+    vals = rng.standard_normal((nrows, offs.size))
+    vals[rng.random(vals.shape) < 0.1] = 0.0
+    src = ds.DiaMatrix(nrows, ncols, offs, vals, ds.MemorySpace.DEVICE, DEV)
+    ora = O.dia(nrows, ncols, offs, vals)
+    for tgt, fid in ((O.CSR, ds.FormatId.CSR), (O.COO, ds.FormatId.COO),
+                     (O.DIA, ds.FormatId.DIA)):
+        assert_same(ds.convert(src, fid), O.convert(ora, tgt), (kind, fid))

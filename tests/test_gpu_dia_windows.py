@@ -2,7 +2,8 @@
 forced at small sizes in a subprocess (the launcher reads DS_DIA_XWIN_FORCE /
 DS_DIA_XWIN_SPAN once): bitwise equal to the oracle on stencils whose edges
 clip the windows (odd and even column counts, ragged last tiles), spmv_add,
-and inside CG (the windows are issued after the programmatic-launch wait)."""
+and inside CG (the windows are issued after the programmatic-launch wait);
+unsorted offsets fall back to plain gathers."""
 
 from __future__ import annotations
 
@@ -40,6 +41,19 @@ for dims in [(24, 20, 16), (9, 7, 5), (33, 17, 11), (40, 40, 40)]:
     k = min(res.iterations, oref.iterations) + 1
     h = np.asarray(res.residual_history[:k])
     assert np.all(np.abs(h - oref.history[:k]) <= 1e-8 * oref.history[:k] + 1e-14), dims
+# unsorted offsets (the same 27 diagonals permuted): no windows, j-order sums
+rng = np.random.default_rng(5)
+perm = rng.permutation(27)
+offs = A.offsets.cpu().numpy()[perm]
+vals = np.ascontiguousarray(A.values.cpu().numpy()[:, perm])
+Ap = ds.DiaMatrix(A.nrows, A.ncols, offs, vals, ds.MemorySpace.DEVICE, dev)
+refp = O.dia(A.nrows, A.ncols, offs, vals)
+x = rng.standard_normal(A.ncols)
+y = ds.DenseVector.zeros(A.nrows, ds.MemorySpace.DEVICE, dev)
+ds.spmv(ds.SERIAL, Ap, ds.DenseVector(torch.from_numpy(x).to(dev)), y)
+want = np.zeros(A.nrows)
+O.spmv(refp, x, want)
+assert y.data.cpu().numpy().tobytes() == want.tobytes(), "permuted offsets"
 print("ok")
 '''
 
