@@ -47,6 +47,8 @@ struct ds_convert_job {
   // census is taken while checking the order, the slab is filled per row
   const int* csr_off = nullptr;
   unsigned char* flags = nullptr;   // diagonal presence (nrows+ncols-1), already marked
+  // DIA source (ascending offsets), DIA target: a column selection
+  int* dia_jsrc = nullptr;          // (ndiags) source column of each target diagonal
 };
 
 namespace ds {
@@ -176,14 +178,6 @@ __global__ void csr_expand_rows(int nrows, const int* __restrict__ off, int* row
     for (int k = off[r] + lane8; k < off[r + 1]; k += 8) rows[k] = r;
 }
 
-struct OrderBad {  // 1 where (row, col) is not strictly greater than its predecessor
-  const int* r;
-  const int* c;
-  __device__ int operator()(int64_t k) const {
-    if (k == 0) return 0;
-    return (r[k] < r[k - 1] || (r[k] == r[k - 1] && c[k] <= c[k - 1])) ? 1 : 0;
-  }
-};
 
 __global__ void make_keys(int64_t nnz, int64_t ncols, const int* __restrict__ r,
                           const int* __restrict__ c, unsigned long long* keys, int* idx) {
@@ -272,21 +266,48 @@ struct DiaSlots {
   }
 };
 
+// DIA -> DIA: the target keeps the source diagonals that hold an entry
+// (jsrc[t] = source column of target diagonal t); a slot keeps its value iff
+// it is in range and nonzero (-0.0 and padding become +0.0, exactly as the
+// canonical COO proxy's zero fill).  Thread per target slot, coalesced stores.
+__global__ void dia_copy_diags(int64_t nrows, int ncols, int nd, int nd_out,
+                               const int* __restrict__ off, const double* __restrict__ vals,
+                               const int* __restrict__ jsrc, double* out) {
+  const int64_t total = nrows * nd_out;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = total < (int64_t(1) << 32) ? (int64_t)((unsigned)t / (unsigned)nd_out)
+                                                 : t / nd_out;
+    const int j = __ldg(jsrc + (int)(t - i * nd_out));
+    const int64_t col = i + __ldg(off + j);
+    const double x = __ldg(vals + i * nd + j);
+    out[t] = (col >= 0 && col < ncols && x != 0.0) ? x : 0.0;
+  }
+}
+
 struct ArrayAt {
   const int* a;
   __device__ int operator()(int64_t k) const { return a[k]; }
 };
 
+// present != nullptr (DIA target): also the census of diagonals holding at
+// least one entry (L1-cached test-before-set, as mark_diags)
 __global__ void dia_group_counts(int64_t nrows, int ncols, int nd, const int* __restrict__ off,
-                                 const double* __restrict__ vals, int64_t ngroups, int* gcount) {
+                                 const double* __restrict__ vals, int64_t ngroups, int* gcount,
+                                 unsigned char* present) {
   const DiaSlots s(ncols, nd, off, vals);
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < ngroups; g += nwarps) {
     const int64_t r0 = g * kDiaGroupRows;
     const int64_t r1 = r0 + kDiaGroupRows < nrows ? r0 + kDiaGroupRows : nrows;
     int cnt = 0;
-    s.walk(r0, r0 * nd, r1 * nd, [&](bool valid, bool, int64_t, int, int, double) {
+    s.walk(r0, r0 * nd, r1 * nd, [&](bool valid, bool, int64_t, int j, int, double) {
       cnt += __popc(__ballot_sync(0xffffffffu, valid));
+      if (present && valid) {
+        unsigned short f;
+        asm volatile("ld.global.ca.u8 %0, [%1];" : "=h"(f) : "l"(present + j));
+        if (f == 0) present[j] = 1;
+      }
     });
     if ((threadIdx.x & 31) == 0) gcount[g] = cnt;
   }
@@ -349,7 +370,7 @@ __global__ void mark_diags(int64_t nnz, int nrows, const int* __restrict__ r,
   }
 }
 // CSR source, DIA target: one pass over the column indices checks the
-// canonical order (strictly ascending columns in every row: OrderBad without
+// canonical order (strictly ascending columns in every row: coo_check_mark's test without
 // expanding the rows) and marks the diagonals; then the DIA slab of a block
 // of rows is zeroed in shared memory, the block's entries are dropped into
 // their (row, diagonal) slots and the slab is written out with coalesced
@@ -499,6 +520,26 @@ __global__ void csr_rows_walk(int nrows, const int* __restrict__ off, int* rows)
   }
 }
 
+__global__ void coo_check_mark(int64_t nnz, int nrows, const int* __restrict__ r,
+                               const int* __restrict__ c, unsigned char* flags, int* bad) {
+  int mybad = 0;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int rk = __ldg(r + k), ck = __ldg(c + k);
+    if (k > 0) {
+      const int rp = __ldg(r + k - 1), cp = __ldg(c + k - 1);
+      if (rk < rp || (rk == rp && ck <= cp)) mybad = 1;
+    }
+    if (flags) {
+      const int64_t d = (int64_t)ck - rk + nrows - 1;
+      unsigned short f;
+      asm volatile("ld.global.ca.u8 %0, [%1];" : "=h"(f) : "l"(flags + d));
+      if (f == 0) flags[d] = 1;
+    }
+  }
+  if (__syncthreads_or(mybad) && threadIdx.x == 0) atomicOr(bad, 1);
+}
+
 struct FlagAt {
   const unsigned char* f;
   __device__ int operator()(int64_t k) const { return f[k]; }
@@ -547,9 +588,24 @@ static int canonicalize(ds_convert_job* job, int64_t nnz, const int* rows, const
     if (rows_owned) DS_CUDA(cudaFreeAsync(const_cast<int*>(rows), st));
     return DS_OK;
   }
-  int64_t bad = 0;
-  int rc = exclusive_scan(nnz, OrderBad{rows, cols}, nullptr, &bad, st);
-  if (rc) return rc;
+  // one pass: the order check ((row, col) strictly ascending) and, for a DIA target, the
+  // diagonal census -- the set of diagonals does not depend on the order or on
+  // duplicates (their sums are kept even when zero), so it holds either way
+  const bool dia = job->target == DS_FMT_DIA;
+  const int64_t flag_bytes = dia ? (job->nrows + job->ncols - 1 + 3) & ~int64_t(3) : 0;
+  unsigned char* scratch = nullptr;
+  DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scratch), flag_bytes + 4, st));
+  DS_CUDA(cudaMemsetAsync(scratch, 0, flag_bytes + 4, st));
+  int* bad_d = reinterpret_cast<int*>(scratch + flag_bytes);
+  coo_check_mark<<<grid1d(nnz), 256, 0, st>>>(nnz, (int)job->nrows, rows, cols,
+                                               dia ? scratch : nullptr, bad_d);
+  DS_LAUNCH_CHECK("coo_check_mark");
+  int bad = 1;
+  DS_CUDA(cudaMemcpyAsync(&bad, bad_d, sizeof(int), cudaMemcpyDeviceToHost, st));
+  DS_CUDA(cudaStreamSynchronize(st));
+  if (dia) job->flags = scratch;
+  else DS_CUDA(cudaFreeAsync(scratch, st));
+  int rc = DS_OK;
   if (bad == 0) {  // already canonical: borrow (copied into the target at finish)
     job->nnz = nnz;
     job->r = const_cast<int*>(rows);
@@ -609,6 +665,7 @@ static void free_job(ds_convert_job* job) {
   if (job->dia_off) cudaFreeAsync(job->dia_off, st);
   if (job->dsrc_start) cudaFreeAsync(job->dsrc_start, st);
   if (job->flags) cudaFreeAsync(job->flags, st);
+  if (job->dia_jsrc) cudaFreeAsync(job->dia_jsrc, st);
   delete job;
 }
 
@@ -1073,20 +1130,6 @@ extern "C" int ds_convert_begin_dia(int64_t nrows, int64_t ncols, int32_t ndiags
     int *gcount = nullptr, *gstart = nullptr;
     DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&gcount), ngroups * sizeof(int), st));
     DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&gstart), ngroups * sizeof(int), st));
-    dia_group_counts<<<dia_walk_grid(ngroups), 256, 0, st>>>(nrows, (int)ncols, ndiags, offsets,
-                                                             values, ngroups, gcount);
-    DS_LAUNCH_CHECK("dia_group_counts");
-    int rc = exclusive_scan(ngroups, ArrayAt{gcount}, gstart, &nc, st);
-    DS_CUDA(cudaFreeAsync(gcount, st));
-    if (rc) {
-      cudaFreeAsync(gstart, st);
-      free_job(j);
-      return rc;
-    }
-    j->dsrc_off = offsets;
-    j->dsrc_vals = values;
-    j->dsrc_nd = ndiags;
-    j->dsrc_start = gstart;
     // slot order is canonical only for strictly ascending offsets; otherwise
     // (unsorted or repeated diagonals) the entries go through the proxy's sort
     // and duplicate sums like any other source (datamove.py:208-235)
@@ -1095,6 +1138,63 @@ extern "C" int ds_convert_begin_dia(int64_t nrows, int64_t ncols, int32_t ndiags
     DS_CUDA(cudaStreamSynchronize(st));
     bool ascending = true;
     for (int q = 1; q < ndiags; ++q) ascending = ascending && h_off[q - 1] < h_off[q];
+    const bool select = target == DS_FMT_DIA && ascending;   // DIA -> DIA: a column selection
+    unsigned char* present = nullptr;
+    if (select) {
+      DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&present), ndiags, st));
+      DS_CUDA(cudaMemsetAsync(present, 0, ndiags, st));
+    }
+    dia_group_counts<<<dia_walk_grid(ngroups), 256, 0, st>>>(nrows, (int)ncols, ndiags, offsets,
+                                                             values, ngroups, gcount, present);
+    DS_LAUNCH_CHECK("dia_group_counts");
+    int rc = exclusive_scan(ngroups, ArrayAt{gcount}, gstart, &nc, st);
+    DS_CUDA(cudaFreeAsync(gcount, st));
+    if (rc) {
+      cudaFreeAsync(gstart, st);
+      if (present) cudaFreeAsync(present, st);
+      free_job(j);
+      return rc;
+    }
+    j->dsrc_off = offsets;
+    j->dsrc_vals = values;
+    j->dsrc_nd = ndiags;
+    j->dsrc_start = gstart;
+    if (select) {
+      std::vector<unsigned char> h_present(ndiags);
+      DS_CUDA(cudaMemcpyAsync(h_present.data(), present, ndiags, cudaMemcpyDeviceToHost, st));
+      DS_CUDA(cudaStreamSynchronize(st));
+      cudaFreeAsync(present, st);
+      cudaFreeAsync(gstart, st);
+      j->dsrc_start = nullptr;
+      std::vector<int> jsrc, off_out;
+      for (int q = 0; q < ndiags; ++q)
+        if (h_present[q]) {
+          jsrc.push_back(q);
+          off_out.push_back(h_off[q]);
+        }
+      const int64_t nd_out = (int64_t)jsrc.size();
+      if (nd_out > 0) {
+        DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&j->dia_off), nd_out * 4, st));
+        DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&j->dia_jsrc), nd_out * 4, st));
+        DS_CUDA(cudaMemcpyAsync(j->dia_off, off_out.data(), nd_out * 4, cudaMemcpyHostToDevice, st));
+        DS_CUDA(cudaMemcpyAsync(j->dia_jsrc, jsrc.data(), nd_out * 4, cudaMemcpyHostToDevice, st));
+        DS_CUDA(cudaStreamSynchronize(st));   // the host vectors die here
+      }
+      j->nnz = nc;
+      j->ndiags = nd_out;
+      *out_nnz = nc;
+      *out_ndiags = nd_out;
+      if (fill_limit < 0) fill_limit = 10 * std::max(nc, nrows);
+      if ((__int128)nd_out * (__int128)nrows > (__int128)fill_limit) {
+        set_error("%lld diagonals x %lld rows = %lld value slots exceed the fill limit of %lld",
+                  (long long)nd_out, (long long)nrows, (long long)(nd_out * nrows),
+                  (long long)fill_limit);
+        free_job(j);
+        return DS_ERR_DIA_FILL_OVERFLOW;
+      }
+      *job = j;
+      return DS_OK;
+    }
     if (target == DS_FMT_DIA || !ascending) {   // materialise the (slot-order) COO
       int *tr = nullptr, *tc = nullptr;
       double* tv = nullptr;
@@ -1200,6 +1300,14 @@ extern "C" int ds_convert_finish_dia(ds_convert_job* job, int32_t* offsets, doub
     DS_CUDA(cudaMemcpyAsync(offsets, job->dia_off, nd * sizeof(int), cudaMemcpyDeviceToDevice,
                             st));
     const int64_t slots = nd * job->nrows;
+    if (job->dia_jsrc) {   // DIA source: the selected columns, masked
+      dia_copy_diags<<<grid1d(slots), 256, 0, st>>>(job->nrows, (int)job->ncols, job->dsrc_nd,
+                                                    (int)nd, job->dsrc_off, job->dsrc_vals,
+                                                    job->dia_jsrc, values);
+      DS_LAUNCH_CHECK("dia_copy_diags");
+      free_job(job);
+      return DS_OK;
+    }
     const int R = kCsrWalkRows * 8;   // 8 warps
     if (job->csr_off && (int64_t)R * nd * 8 <= 48 * 1024) {
       dia_fill_csr<<<csr_walk_grid(job->nrows), 256, (size_t)R * nd * 8, st>>>(

@@ -88,8 +88,30 @@ def test_dia_source_all_zero_and_out_of_range():
     vals[:, 1] = -0.0
     src = ds.DiaMatrix(nrows, ncols, offs, vals, ds.MemorySpace.DEVICE, DEV)
     ora = O.dia(nrows, ncols, offs, vals)
-    for tgt, fid in ((O.CSR, ds.FormatId.CSR), (O.COO, ds.FormatId.COO)):
+    for tgt, fid in ((O.CSR, ds.FormatId.CSR), (O.COO, ds.FormatId.COO),
+                     (O.DIA, ds.FormatId.DIA)):
         assert_same(ds.convert(src, fid, fill_limit=BIG), O.convert(ora, tgt, fill_limit=BIG), fid)
+
+
+def test_dia_to_dia_selection_and_fill_limit():
+    """DIA -> DIA keeps the diagonals holding an entry (a column selection):
+    padding and -0.0 become +0.0; the default limit counts the source's
+    nonzero slots; an explicit limit one slot short raises before allocation."""
+    rng = np.random.default_rng(41)
+    nrows, ncols = 500, 450
+    offs = np.array([-600, -7, -1, 0, 3, 449, 460], dtype=np.int64)
+    vals = rng.standard_normal((nrows, offs.size))
+    vals[:, 2] = 0.0                      # an all-zero diagonal: dropped
+    vals[::3, 3] = -0.0
+    src = ds.DiaMatrix(nrows, ncols, offs, vals, ds.MemorySpace.DEVICE, DEV)
+    ora = O.dia(nrows, ncols, offs, vals)
+    want = O.convert(ora, O.DIA)
+    got = ds.convert(src, ds.FormatId.DIA)
+    assert_same(got, want, "dia->dia")
+    assert list(want.offsets) == [-7, 0, 3, 449]
+    with pytest.raises(ds.DiaFillOverflow):
+        ds.convert(src, ds.FormatId.DIA, fill_limit=4 * nrows - 1)
+    assert_same(ds.convert(src, ds.FormatId.DIA, fill_limit=4 * nrows), want, "exact limit")
 
 
 def random_csr(rng, nrows, ncols, lengths, sort=True):
