@@ -572,7 +572,27 @@ __global__ void __launch_bounds__(kVecBlock)
                                      const unsigned* pap_count, double* rr_parts,
                                      unsigned* bar_count, unsigned* bar_gen) {
   __shared__ double sh[32];
+  // Launched as a programmatic dependent of the SpMV: everything up to the
+  // griddepcontrol.wait reads only what the SpMV does not write -- s->done and
+  // x / r / p of the first sweep (the previous tail wrote them, and it is
+  // complete: every SpMV block waited on it before this grid could start).
   if (s->done) return;
+  const int64_t gtid = (int64_t)blockIdx.x * kVecBlock + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * kVecBlock;
+  const int64_t n2 = n >> 1;
+  double2* x2 = reinterpret_cast<double2*>(x);
+  double2* r2 = reinterpret_cast<double2*>(r);
+  double2* p2 = reinterpret_cast<double2*>(p);
+  const double2* a2 = reinterpret_cast<const double2*>(ap);
+  double2 xv[kVecUnroll], rv[kVecUnroll], pv[kVecUnroll];
+#pragma unroll
+  for (int u = 0; u < kVecUnroll; ++u) {
+    const int64_t i = min64(gtid + u * stride, n2 - 1);
+    xv[u] = x2[i];
+    rv[u] = r2[i];
+    pv[u] = p2[i];
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const double pap = reduce_partials<kVecBlock>(pap_parts, pap_count, sh);
   if (pap <= 0.0) {  // breakdown: every block sees the same pap
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -584,22 +604,17 @@ __global__ void __launch_bounds__(kVecBlock)
   const double rr = s->rr;
   const double alpha = rr / pap, nalpha = -alpha;
   const int it = s->iter + 1;
-  const int64_t gtid = (int64_t)blockIdx.x * kVecBlock + threadIdx.x;
-  const int64_t stride = (int64_t)gridDim.x * kVecBlock;
-  const int64_t n2 = n >> 1;
-  double2* x2 = reinterpret_cast<double2*>(x);
-  double2* r2 = reinterpret_cast<double2*>(r);
-  double2* p2 = reinterpret_cast<double2*>(p);
-  const double2* a2 = reinterpret_cast<const double2*>(ap);
   double v = 0.0;
   for (int64_t i0 = gtid; i0 < n2; i0 += stride * kVecUnroll) {
-    double2 xv[kVecUnroll], rv[kVecUnroll], pv[kVecUnroll], av[kVecUnroll];
+    double2 av[kVecUnroll];
 #pragma unroll
     for (int u = 0; u < kVecUnroll; ++u) {
       const int64_t i = min64(i0 + u * stride, n2 - 1);
-      xv[u] = x2[i];
-      rv[u] = r2[i];
-      pv[u] = p2[i];
+      if (i0 != gtid) {   // the first sweep's x / r / p are already loaded
+        xv[u] = x2[i];
+        rv[u] = r2[i];
+        pv[u] = p2[i];
+      }
       av[u] = a2[i];
     }
 #pragma unroll
@@ -663,7 +678,6 @@ __global__ void __launch_bounds__(kVecBlock)
   }
   if (converged || last) return;
   for (int64_t i0 = gtid; i0 < n2; i0 += stride * kVecUnroll) {
-    double2 rv[kVecUnroll], pv[kVecUnroll];
 #pragma unroll
     for (int u = 0; u < kVecUnroll; ++u) {
       const int64_t i = min64(i0 + u * stride, n2 - 1);
@@ -1067,6 +1081,30 @@ extern "C" int ds_cg_update_direction_deferred(int64_t n, double* x, double* r, 
   void* args[] = {&n, &x, &r, &p, const_cast<double**>(&ap), &s, &history,
                   const_cast<double**>(&pap_parts), const_cast<unsigned**>(&pap_count),
                   &rr_parts, &bar_count, &bar_gen};
+  // cooperative AND a programmatic dependent of the SpMV before it (its
+  // x / r / p loads overlap the SpMV's last wave); without PDL support the
+  // plain cooperative launch below
+  static int no_pdl = -1;
+  if (no_pdl < 0) no_pdl = getenv("DS_NO_PDL") || getenv("DS_NO_TAIL_PDL") ? 1 : 0;
+  if (!no_pdl) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)g);
+    cfg.blockDim = dim3(kVecBlock);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    if (cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(cg_update_direction_fused_kernel),
+                            args) == cudaSuccess) {
+      DS_LAUNCH_CHECK("cg_update_direction_fused_kernel");
+      return DS_OK;
+    }
+    (void)cudaGetLastError();
+  }
   cudaError_t e = cudaLaunchCooperativeKernel(
       reinterpret_cast<const void*>(cg_update_direction_fused_kernel), dim3((unsigned)g),
       dim3(kVecBlock), args, 0, st);
