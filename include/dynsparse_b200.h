@@ -152,7 +152,9 @@ int ds_dia_count_nonzero(int64_t nrows, int64_t ncols, int32_t ndiags, const int
  * for a DIA source nnz = its nonzero in-range slots, counted by begin).
  * finish_* writes the target arrays and frees the job; abort frees it
  * without writing.  A DIA or canonical-CSR source is read again by finish_*
- * (its entries go straight into the target): keep it alive until then.     */
+ * (its entries go straight into the target): keep it alive until then.
+ * DIA offsets need not ascend: unsorted or repeated diagonals are sorted and
+ * summed like duplicate COO entries (datamove.py:208-235).                 */
 typedef struct ds_convert_job ds_convert_job;
 enum { DS_FMT_COO = 0, DS_FMT_CSR = 1, DS_FMT_DIA = 2 };   /* FormatId, formats.py:33-42 */
 
