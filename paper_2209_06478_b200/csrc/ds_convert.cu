@@ -291,7 +291,7 @@ struct ArrayAt {
 };
 
 // present != nullptr (DIA target): also the census of diagonals holding at
-// least one entry (L1-cached test-before-set, as mark_diags)
+// least one entry (L1-cached test-before-set, see the diagonal flags below)
 __global__ void dia_group_counts(int64_t nrows, int ncols, int nd, const int* __restrict__ off,
                                  const double* __restrict__ vals, int64_t ngroups, int* gcount,
                                  unsigned char* present) {
@@ -354,21 +354,13 @@ __global__ void rows_to_offsets(int64_t nnz, int nrows, const int* __restrict__ 
   }
 }
 
-// Presence flags of every diagonal.  Few distinct diagonals are hit by very
+// Presence flags of every diagonal (taken by coo_check_mark /
+// csr_check_mark / dia_group_counts).  Few distinct diagonals are hit by very
 // many entries (27 for the stencil) and same-address stores serialise in L2.
-// Test first with an L1-CACHED load: an SM's own store invalidates its L1
-// line, the next miss brings back the 1, so every SM writes each flag about
-// once and all other tests hit L1 (a racing duplicate store of 1 is harmless).
-__global__ void mark_diags(int64_t nnz, int nrows, const int* __restrict__ r,
-                           const int* __restrict__ c, unsigned char* flags) {
-  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz;
-       k += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t d = (int64_t)c[k] - r[k] + nrows - 1;
-    unsigned short v;
-    asm volatile("ld.global.ca.u8 %0, [%1];" : "=h"(v) : "l"(flags + d));
-    if (v == 0) flags[d] = 1;
-  }
-}
+// Each marker tests first with an L1-CACHED load: an SM's own store
+// invalidates its L1 line, the next miss brings back the 1, so every SM writes
+// each flag about once and all other tests hit L1 (a racing duplicate store
+// of 1 is harmless).
 // CSR source, DIA target: one pass over the column indices checks the
 // canonical order (strictly ascending columns in every row: coo_check_mark's test without
 // expanding the rows) and marks the diagonals; then the DIA slab of a block
@@ -679,14 +671,11 @@ static int size_target(ds_convert_job* job, int64_t fill_limit, int64_t* out_nnz
   const int64_t D = job->nrows + job->ncols - 1;
   int64_t nd = 0;
   if (D > 0 && job->nnz > 0) {
-    unsigned char* flags = job->flags;
+    unsigned char* flags = job->flags;   // marked by the order-check pass
     job->flags = nullptr;
     if (!flags) {
-      DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&flags), D, st));
-      DS_CUDA(cudaMemsetAsync(flags, 0, D, st));
-      mark_diags<<<grid1d(job->nnz), 256, 0, st>>>(job->nnz, (int)job->nrows, job->r, job->c,
-                                                   flags);
-      DS_LAUNCH_CHECK("mark_diags");
+      set_error("conversion job without a diagonal census");
+      return DS_ERR_CUDA;
     }
     DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&job->diag_map), D * sizeof(int), st));
     int rc = exclusive_scan(D, FlagAt{flags}, job->diag_map, &nd, st);
