@@ -37,7 +37,9 @@ enum {
   DS_ERR_DIA_FILL_OVERFLOW = 3,         /* DiaFillOverflow        errors.py:52-53        */
   DS_ERR_STRUCTURALLY_ABSENT_DIAG = 4,  /* StructurallyAbsentDiagonal errors.py:73-78    */
   DS_ERR_BREAKDOWN = 5,                 /* BreakdownZeroCurvature errors.py:81-82        */
-  DS_ERR_NOT_SUPPORTED = 6              /* dims >= 2^31 or a layout the kernels refuse   */
+  DS_ERR_NOT_SUPPORTED = 6,             /* dims >= 2^31 or a layout the kernels refuse   */
+  DS_ERR_INDEX_OUT_OF_RANGE = 7         /* IndexOutOfRange errors.py:17: an entry's row /
+                                           column outside the shape (conversion sources)  */
 };
 
 /* Message of the last failing call on this host thread ("" if none). */
@@ -147,14 +149,19 @@ int ds_dia_count_nonzero(int64_t nrows, int64_t ncols, int32_t ndiags, const int
  * COO (stable (row,col) sort + duplicate sums in reduceat order) on the
  * device, sizes the target and -- for DIA -- applies the fill-limit test
  * BEFORE any target allocation (datamove.py:246-252): it returns
- * DS_ERR_DIA_FILL_OVERFLOW with *out_ndiags set.  fill_limit < 0 selects
- * the reference default 10 * max(nnz, nrows) of the source (datamove.py:55-57;
- * for a DIA source nnz = its nonzero in-range slots, counted by begin).
+ * DS_ERR_DIA_FILL_OVERFLOW with *out_ndiags set.  fill_limit ==
+ * DS_FILL_LIMIT_DEFAULT (INT64_MIN) selects the reference default
+ * 10 * max(nnz, nrows) of the source (datamove.py:55-57; for a DIA source
+ * nnz = its nonzero in-range slots, counted by begin); any other value --
+ * negative ones included -- is the limit itself (slots > fill_limit raises,
+ * datamove.py:250-252).  An entry outside the shape returns
+ * DS_ERR_INDEX_OUT_OF_RANGE (nothing is written for it).
  * finish_* writes the target arrays and frees the job; abort frees it
  * without writing.  A DIA or canonical-CSR source is read again by finish_*
  * (its entries go straight into the target): keep it alive until then.
  * DIA offsets need not ascend: unsorted or repeated diagonals are sorted and
  * summed like duplicate COO entries (datamove.py:208-235).                 */
+#define DS_FILL_LIMIT_DEFAULT ((int64_t)(-9223372036854775807LL - 1))
 typedef struct ds_convert_job ds_convert_job;
 enum { DS_FMT_COO = 0, DS_FMT_CSR = 1, DS_FMT_DIA = 2 };   /* FormatId, formats.py:33-42 */
 
@@ -345,14 +352,51 @@ int ds_nccl_unique_id(char* out, int nbytes);
 int ds_nccl_comm_init(const char* id_bytes, int nranks, int rank, void** comm);
 int ds_nccl_comm_destroy(void* comm);
 /* For each neighbour q (ascending rank): gather x_full[send_idx[q][k]] into
- * send_bufs[q] (skipped when *guard != 0), then in one NCCL group send it to
- * peers[q] and receive recv_counts[q] doubles into x_full + recv_starts[q]. */
+ * send_bufs[q] (the gathers are skipped once s->done != 0: p no longer
+ * changes; s may be NULL = never skipped), then in one NCCL group send it to
+ * peers[q] and receive recv_counts[q] doubles into x_full + recv_starts[q].
+ * The sends and receives themselves are unconditional, so every rank posts
+ * the same operations.                                                      */
 int ds_halo_exchange(int nnbr, const int32_t* peers, const int64_t* send_counts,
                      const int32_t* const* send_idx, double* const* send_bufs,
                      const int64_t* recv_counts, const int64_t* recv_starts, double* x_full,
-                     const int32_t* guard, void* comm, void* stream);
+                     const ds_cg_scalars* s, void* comm, void* stream);
 /* recv[r*count : (r+1)*count] = rank r's send (ncclAllGather, float64).   */
 int ds_allgather_f64(const double* send, double* recv, int64_t count, void* comm, void* stream);
+
+/* ---- one partition per process: peer-memory transport (CUDA IPC over
+ * NVLink / NVSwitch; several ranks may also share one GPU) -----------------
+ * The same exchanges as above with plain loads / stores on mapped peer
+ * memory instead of NCCL.  Flags are uint32 words, raised (1) by their
+ * producer and cleared (0) by their consumer.  wait_mode: DS_PEER_WAIT_SPIN
+ * polls inside a kernel (traps after 30 s), DS_PEER_WAIT_MEMOP blocks the
+ * stream with cuStreamWaitValue32 and clears with cuStreamWriteValue32.    */
+#define DS_PEER_MAX_RANKS 64
+#define DS_PEER_MAX_NBR 26
+enum { DS_PEER_WAIT_SPIN = 0, DS_PEER_WAIT_MEMOP = 1 };
+/* export: CUDA IPC handle of ptr's allocation + ptr's byte offset in it
+ * (ds_ipc_handle_bytes() bytes); import maps it (lazy peer access) and
+ * returns the address of ptr in this process; close unmaps.               */
+int ds_ipc_handle_bytes(void);
+int ds_ipc_export(const void* ptr, char* out);
+int ds_ipc_import(const char* in, void** ptr);
+int ds_ipc_close(void* ptr);
+/* all_ptrs[r][stage*nranks + rank] = *mine and flag_ptrs[r][same] = 1 for
+ * every rank r (r == rank: this rank's own, unmapped block), then wait until
+ * my_flags[stage*nranks + r] is raised for every r and clear them: after it,
+ * all_ptrs[rank][stage*nranks + 0..nranks) holds every partition's dot.    */
+int ds_peer_allgather_f64(const double* mine, int stage, int rank, int nranks,
+                          double* const* all_ptrs, unsigned* const* flag_ptrs,
+                          unsigned* my_flags, int wait_mode, void* stream);
+/* dst[q][j] = p[idx[q][j]] for j < counts[q] (remote stores into neighbour
+ * q's ghost slots), then -- every store fenced at system scope -- raise
+ * flags[q] (neighbour q's flag for this rank).  ticket: a zeroed device word
+ * owned by this call site.                                                 */
+int ds_peer_halo_push(int nnbr, const int64_t* counts, const int32_t* const* idx,
+                      const double* p, double* const* dst, unsigned* const* flags,
+                      unsigned* ticket, void* stream);
+/* wait until each of flags[0..n) is raised, then clear it                   */
+int ds_peer_wait_flags(int n, unsigned* const* flags, int wait_mode, void* stream);
 
 /* ---- HPCG smoother and multigrid transfers (NOT in the
  * reference -- parity pinned to the oracle's restatement of HPCG's

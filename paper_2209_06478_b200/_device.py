@@ -43,13 +43,22 @@ def ptr(t: torch.Tensor | None) -> int | None:
     return t.data_ptr()
 
 
+def new_workspace(device: torch.device) -> torch.Tensor:
+    """A fresh zero-initialised reduction workspace (partials, tickets, the
+    grid-barrier words) owned by the caller -- what a captured CUDA graph
+    embeds, so two graphs never share one even when their capture streams'
+    handles were recycled."""
+    nbytes = int(_native.load().ds_cg_workspace_bytes())
+    return torch.zeros(nbytes, dtype=torch.uint8, device=device)
+
+
 def workspace(device: torch.device) -> torch.Tensor:
-    """Zero-initialised reduction workspace for (device, current stream)."""
+    """Zero-initialised reduction workspace for eager launches on (device,
+    current stream): work on one stream is serialised, so it is shared."""
     key = (device.index, stream(device))
     ws = _WORKSPACES.get(key)
     if ws is None:
-        nbytes = int(_native.load().ds_cg_workspace_bytes())
-        ws = torch.zeros(nbytes, dtype=torch.uint8, device=device)
+        ws = new_workspace(device)
         _WORKSPACES[key] = ws
     return ws
 

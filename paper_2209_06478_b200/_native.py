@@ -16,6 +16,7 @@ from .errors import (
     BreakdownZeroCurvature,
     DeviceError,
     DiaFillOverflow,
+    IndexOutOfRange,
     StructurallyAbsentDiagonal,
 )
 
@@ -29,6 +30,8 @@ DS_ERR_DIA_FILL_OVERFLOW = 3
 DS_ERR_STRUCTURALLY_ABSENT_DIAG = 4
 DS_ERR_BREAKDOWN = 5
 DS_ERR_NOT_SUPPORTED = 6
+DS_ERR_INDEX_OUT_OF_RANGE = 7
+DS_FILL_LIMIT_DEFAULT = -(2**63)   # include/dynsparse_b200.h: the reference default limit
 
 DS_CG_STAGE_NONE, DS_CG_STAGE_PAP, DS_CG_STAGE_RR, DS_CG_STAGE_SETUP = 0, 1, 2, 3
 DS_CG_STAGE_DEFERRED = 4
@@ -160,7 +163,17 @@ _SIGNATURES = {
     "ds_halo_exchange": (c_int, [c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                                  c_vp]),
     "ds_allgather_f64": (c_int, [c_vp, c_vp, c_i64, c_vp, c_vp]),
+    "ds_ipc_handle_bytes": (c_int, []),
+    "ds_ipc_export": (c_int, [c_vp, ctypes.c_char_p]),
+    "ds_ipc_import": (c_int, [ctypes.c_char_p, ctypes.POINTER(c_vp)]),
+    "ds_ipc_close": (c_int, [c_vp]),
+    "ds_peer_allgather_f64": (c_int, [c_vp, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_int, c_vp]),
+    "ds_peer_halo_push": (c_int, [c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "ds_peer_wait_flags": (c_int, [c_int, c_vp, c_int, c_vp]),
 }
+
+DS_PEER_WAIT_SPIN, DS_PEER_WAIT_MEMOP = 0, 1
+DS_PEER_MAX_RANKS, DS_PEER_MAX_NBR = 64, 26
 
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)
 
@@ -204,6 +217,8 @@ def check(status: int, *, index: int | None = None) -> None:
         raise StructurallyAbsentDiagonal(int(index if index is not None else 0))
     if status == DS_ERR_BREAKDOWN:
         raise BreakdownZeroCurvature(msg)
+    if status == DS_ERR_INDEX_OUT_OF_RANGE:
+        raise IndexOutOfRange(msg)
     raise DeviceError(f"dynsparse native error {status}: {msg}")
 
 

@@ -49,10 +49,13 @@ struct ds_convert_job {
   unsigned char* flags = nullptr;   // diagonal presence (nrows+ncols-1), already marked
   // DIA source (ascending offsets), DIA target: a column selection
   int* dia_jsrc = nullptr;          // (ndiags) source column of each target diagonal
+  unsigned char* scratch = nullptr; // begin-phase temporaries (order flag, census), freed with the job
+  int* gtmp = nullptr;
 };
 
 namespace ds {
 
+constexpr int64_t kDefaultFillLimit = DS_FILL_LIMIT_DEFAULT;
 constexpr int kScanBlock = 256;
 constexpr int kScanPer = 8;
 constexpr int kScanTile = kScanBlock * kScanPer;
@@ -417,8 +420,12 @@ struct ColVal {
   double v;
 };
 
-__global__ void csr_check_mark(int nrows, const int* __restrict__ off, const int* __restrict__ c,
-                               unsigned char* flags, int* bad) {
+// *bad bits: kBadOrder (not canonical), kBadIndex (a column outside [0, ncols):
+// nothing is marked for it, the caller raises IndexOutOfRange)
+constexpr int kBadOrder = 1, kBadIndex = 2;
+
+__global__ void csr_check_mark(int nrows, int ncols, const int* __restrict__ off,
+                               const int* __restrict__ c, unsigned char* flags, int* bad) {
   const int lane = threadIdx.x & 31;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   int mybad = 0;
@@ -442,8 +449,10 @@ __global__ void csr_check_mark(int nrows, const int* __restrict__ off, const int
                          carry = __shfl_sync(0xffffffffu, ck, 31);
                          carry_row = __shfl_sync(0xffffffffu, row, 31);
                          if (kb + 32 * u + lane < k1) {
-                           if (prev_row == row && prev >= ck) mybad = 1;
-                           if (flags) {
+                           if (prev_row == row && prev >= ck) mybad |= kBadOrder;
+                           if ((unsigned)ck >= (unsigned)ncols) {
+                             mybad |= kBadIndex;
+                           } else if (flags) {
                              const int64_t d = (int64_t)ck - row + nrows - 1;
                              unsigned short f;
                              asm volatile("ld.global.ca.u8 %0, [%1];" : "=h"(f) : "l"(flags + d));
@@ -454,7 +463,8 @@ __global__ void csr_check_mark(int nrows, const int* __restrict__ off, const int
                      });
     ot = ot_next;
   }
-  if (__syncthreads_or(mybad) && threadIdx.x == 0) atomicOr(bad, 1);
+  mybad = __reduce_or_sync(0xffffffffu, mybad);
+  if ((threadIdx.x & 31) == 0 && mybad) atomicOr(bad, mybad);
 }
 
 __global__ void dia_fill_csr(int nrows, int nd, int R, const int* __restrict__ off,
@@ -512,7 +522,7 @@ __global__ void csr_rows_walk(int nrows, const int* __restrict__ off, int* rows)
   }
 }
 
-__global__ void coo_check_mark(int64_t nnz, int nrows, const int* __restrict__ r,
+__global__ void coo_check_mark(int64_t nnz, int nrows, int ncols, const int* __restrict__ r,
                                const int* __restrict__ c, unsigned char* flags, int* bad) {
   int mybad = 0;
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz;
@@ -520,16 +530,25 @@ __global__ void coo_check_mark(int64_t nnz, int nrows, const int* __restrict__ r
     const int rk = __ldg(r + k), ck = __ldg(c + k);
     if (k > 0) {
       const int rp = __ldg(r + k - 1), cp = __ldg(c + k - 1);
-      if (rk < rp || (rk == rp && ck <= cp)) mybad = 1;
+      if (rk < rp || (rk == rp && ck <= cp)) mybad |= kBadOrder;
     }
-    if (flags) {
+    if ((unsigned)rk >= (unsigned)nrows || (unsigned)ck >= (unsigned)ncols) {
+      mybad |= kBadIndex;
+    } else if (flags) {
       const int64_t d = (int64_t)ck - rk + nrows - 1;
       unsigned short f;
       asm volatile("ld.global.ca.u8 %0, [%1];" : "=h"(f) : "l"(flags + d));
       if (f == 0) flags[d] = 1;
     }
   }
-  if (__syncthreads_or(mybad) && threadIdx.x == 0) atomicOr(bad, 1);
+  mybad = __reduce_or_sync(0xffffffffu, mybad);
+  if ((threadIdx.x & 31) == 0 && mybad) atomicOr(bad, mybad);
+}
+
+static int index_error(int64_t nrows, int64_t ncols) {
+  set_error("an entry's row or column lies outside the %lld x %lld shape", (long long)nrows,
+            (long long)ncols);
+  return DS_ERR_INDEX_OUT_OF_RANGE;
 }
 
 struct FlagAt {
@@ -571,32 +590,40 @@ static int bits_for(unsigned long long maxkey) {
   return b < 1 ? 1 : b;
 }
 
-// canonicalise raw (rows, cols, vals) into job->{r,c,v}
+// canonicalise raw (rows, cols, vals) into job->{r,c,v}.  Owned rows hang on
+// the job from the start, so every error return frees them with it.
 static int canonicalize(ds_convert_job* job, int64_t nnz, const int* rows, const int* cols,
                         const double* vals, bool rows_owned) {
   cudaStream_t st = job->st;
+  if (rows_owned) {
+    job->r = const_cast<int*>(rows);
+    job->own_r = true;
+  }
   if (nnz == 0) {
     job->nnz = 0;
-    if (rows_owned) DS_CUDA(cudaFreeAsync(const_cast<int*>(rows), st));
     return DS_OK;
   }
-  // one pass: the order check ((row, col) strictly ascending) and, for a DIA target, the
-  // diagonal census -- the set of diagonals does not depend on the order or on
-  // duplicates (their sums are kept even when zero), so it holds either way
+  // one pass: the order check ((row, col) strictly ascending), the index range
+  // and, for a DIA target, the diagonal census -- the set of diagonals does not
+  // depend on the order or on duplicates (their sums are kept even when zero)
   const bool dia = job->target == DS_FMT_DIA;
   const int64_t flag_bytes = dia ? (job->nrows + job->ncols - 1 + 3) & ~int64_t(3) : 0;
-  unsigned char* scratch = nullptr;
-  DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scratch), flag_bytes + 4, st));
-  DS_CUDA(cudaMemsetAsync(scratch, 0, flag_bytes + 4, st));
-  int* bad_d = reinterpret_cast<int*>(scratch + flag_bytes);
-  coo_check_mark<<<grid1d(nnz), 256, 0, st>>>(nnz, (int)job->nrows, rows, cols,
-                                               dia ? scratch : nullptr, bad_d);
+  DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&job->scratch), flag_bytes + 4, st));
+  DS_CUDA(cudaMemsetAsync(job->scratch, 0, flag_bytes + 4, st));
+  int* bad_d = reinterpret_cast<int*>(job->scratch + flag_bytes);
+  coo_check_mark<<<grid1d(nnz), 256, 0, st>>>(nnz, (int)job->nrows, (int)job->ncols, rows, cols,
+                                               dia ? job->scratch : nullptr, bad_d);
   DS_LAUNCH_CHECK("coo_check_mark");
   int bad = 1;
   DS_CUDA(cudaMemcpyAsync(&bad, bad_d, sizeof(int), cudaMemcpyDeviceToHost, st));
   DS_CUDA(cudaStreamSynchronize(st));
-  if (dia) job->flags = scratch;
-  else DS_CUDA(cudaFreeAsync(scratch, st));
+  if (bad & kBadIndex) return index_error(job->nrows, job->ncols);
+  if (dia) {
+    job->flags = job->scratch;
+  } else {
+    DS_CUDA(cudaFreeAsync(job->scratch, st));
+  }
+  job->scratch = nullptr;
   int rc = DS_OK;
   if (bad == 0) {  // already canonical: borrow (copied into the target at finish)
     job->nnz = nnz;
@@ -628,7 +655,11 @@ static int canonicalize(ds_convert_job* job, int64_t nnz, const int* rows, const
   DS_CUDA(cudaFreeAsync(tmp, st));
   DS_CUDA(cudaFreeAsync(keys, st));
   DS_CUDA(cudaFreeAsync(idx, st));
-  if (rows_owned) DS_CUDA(cudaFreeAsync(const_cast<int*>(rows), st));
+  if (rows_owned) {
+    job->r = nullptr;
+    job->own_r = false;
+    DS_CUDA(cudaFreeAsync(const_cast<int*>(rows), st));
+  }
   DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&pos), nnz * 4, st));
   int64_t nc = 0;
   rc = exclusive_scan(nnz, RunHead{keys_s}, pos, &nc, st);
@@ -658,6 +689,8 @@ static void free_job(ds_convert_job* job) {
   if (job->dsrc_start) cudaFreeAsync(job->dsrc_start, st);
   if (job->flags) cudaFreeAsync(job->flags, st);
   if (job->dia_jsrc) cudaFreeAsync(job->dia_jsrc, st);
+  if (job->scratch) cudaFreeAsync(job->scratch, st);
+  if (job->gtmp) cudaFreeAsync(job->gtmp, st);
   delete job;
 }
 
@@ -697,18 +730,6 @@ static int size_target(ds_convert_job* job, int64_t fill_limit, int64_t* out_nnz
               (long long)fill_limit);
     return DS_ERR_DIA_FILL_OVERFLOW;
   }
-  return DS_OK;
-}
-
-static int begin_common(ds_convert_job* job, int64_t fill_limit, ds_convert_job** out,
-                        int64_t* out_nnz, int64_t* out_ndiags) {
-  int rc = size_target(job, fill_limit, out_nnz, out_ndiags);
-  if (rc) {
-    free_job(job);
-    *out = nullptr;
-    return rc;
-  }
-  *out = job;
   return DS_OK;
 }
 
@@ -1019,25 +1040,84 @@ static bool dims_ok(int64_t nrows, int64_t ncols, int64_t nnz) {
   return true;
 }
 
+// Every begin_* wrapper owns the job: the *_impl bodies never free it, so
+// every failure after new_job -- a DS_CUDA early return included -- lands in
+// one free_job (the pool allocations hung on the job go back with it).
+static int begin_coo_impl(ds_convert_job* j, int64_t nnz, const int32_t* rows, const int32_t* cols,
+                          const double* values, int64_t fill_limit, int64_t* out_nnz,
+                          int64_t* out_ndiags) {
+  int rc = canonicalize(j, nnz, rows, cols, values, false);
+  if (rc) return rc;
+  return size_target(j, fill_limit, out_nnz, out_ndiags);
+}
+
 extern "C" int ds_convert_begin_coo(int64_t nrows, int64_t ncols, int64_t nnz, const int32_t* rows,
                                     const int32_t* cols, const double* values, int target,
                                     int64_t fill_limit, void* stream, ds_convert_job** job,
                                     int64_t* out_nnz, int64_t* out_ndiags) {
   *job = nullptr;
-  if (fill_limit < 0) fill_limit = 10 * std::max(nnz, nrows);   // datamove.py:55-57
+  if (fill_limit == kDefaultFillLimit) fill_limit = 10 * std::max(nnz, nrows);   // datamove.py:55-57
   if (!dims_ok(nrows, ncols, nnz)) return DS_ERR_NOT_SUPPORTED;
   ds_convert_job* j = new_job(nrows, ncols, target, stream);
-  int rc = canonicalize(j, nnz, rows, cols, values, false);
+  const int rc = begin_coo_impl(j, nnz, rows, cols, values, fill_limit, out_nnz, out_ndiags);
   if (rc) {
     free_job(j);
     return rc;
   }
-  return begin_common(j, fill_limit, job, out_nnz, out_ndiags);
+  *job = j;
+  return DS_OK;
 }
 
 static unsigned csr_walk_grid(int64_t nrows) {   // 8 warps per block
   return (unsigned)std::max<int64_t>(
       1, min64(ceil_div(nrows, kCsrWalkRows * 8), (int64_t)sm_count() * 8));
+}
+
+static int begin_csr_impl(ds_convert_job* j, int64_t nnz, const int32_t* row_offsets,
+                          const int32_t* cols, const double* values, int64_t fill_limit,
+                          int64_t* out_nnz, int64_t* out_ndiags) {
+  const int64_t nrows = j->nrows, ncols = j->ncols;
+  const int target = j->target;
+  cudaStream_t st = j->st;
+  if (nnz > 0 && nrows > 0) {
+    // canonical already (the common case)?  then no COO proxy at all: a DIA
+    // target takes its diagonal census in the same pass, a CSR / COO target
+    // copies (expands) the source at finish
+    const bool dia = target == DS_FMT_DIA;
+    const int64_t flag_bytes = dia ? (nrows + ncols - 1 + 3) & ~int64_t(3) : 0;
+    DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&j->scratch), flag_bytes + 4, st));
+    DS_CUDA(cudaMemsetAsync(j->scratch, 0, flag_bytes + 4, st));
+    int* bad = reinterpret_cast<int*>(j->scratch + flag_bytes);
+    csr_check_mark<<<csr_walk_grid(nrows), 256, 0, st>>>((int)nrows, (int)ncols, row_offsets, cols,
+                                                         dia ? j->scratch : nullptr, bad);
+    DS_LAUNCH_CHECK("csr_check_mark");
+    int bad_h = 1;
+    DS_CUDA(cudaMemcpyAsync(&bad_h, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+    DS_CUDA(cudaStreamSynchronize(st));
+    if (bad_h & kBadIndex) return index_error(nrows, ncols);
+    if (!bad_h) {
+      j->nnz = nnz;
+      j->csr_off = row_offsets;
+      j->c = const_cast<int*>(cols);
+      j->v = const_cast<double*>(values);
+      if (dia) {   // the census becomes the job's diagonal flags
+        j->flags = j->scratch;
+        j->scratch = nullptr;
+      }
+      return size_target(j, fill_limit, out_nnz, out_ndiags);
+    }
+    DS_CUDA(cudaFreeAsync(j->scratch, st));   // not canonical: the general path
+    j->scratch = nullptr;
+  }
+  int* rows = nullptr;
+  if (nnz > 0) {
+    DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&rows), nnz * 4, st));
+    csr_expand_rows<<<grid1d(nrows * 8), 256, 0, st>>>((int)nrows, row_offsets, rows);
+    DS_LAUNCH_CHECK("csr_expand_rows");
+  }
+  int rc = canonicalize(j, nnz, rows, cols, values, true);
+  if (rc) return rc;
+  return size_target(j, fill_limit, out_nnz, out_ndiags);
 }
 
 extern "C" int ds_convert_begin_csr(int64_t nrows, int64_t ncols, int64_t nnz,
@@ -1046,49 +1126,17 @@ extern "C" int ds_convert_begin_csr(int64_t nrows, int64_t ncols, int64_t nnz,
                                     void* stream, ds_convert_job** job, int64_t* out_nnz,
                                     int64_t* out_ndiags) {
   *job = nullptr;
-  if (fill_limit < 0) fill_limit = 10 * std::max(nnz, nrows);   // datamove.py:55-57
+  if (fill_limit == kDefaultFillLimit) fill_limit = 10 * std::max(nnz, nrows);   // datamove.py:55-57
   if (!dims_ok(nrows, ncols, nnz)) return DS_ERR_NOT_SUPPORTED;
   ds_convert_job* j = new_job(nrows, ncols, target, stream);
-  if (nnz > 0 && nrows > 0) {
-    // canonical already (the common case)?  then no COO proxy at all: a DIA
-    // target takes its diagonal census in the same pass, a CSR / COO target
-    // copies (expands) the source at finish
-    cudaStream_t st = j->st;
-    const bool dia = target == DS_FMT_DIA;
-    const int64_t flag_bytes = dia ? (nrows + ncols - 1 + 3) & ~int64_t(3) : 0;
-    unsigned char* scratch = nullptr;
-    DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scratch), flag_bytes + 4, st));
-    DS_CUDA(cudaMemsetAsync(scratch, 0, flag_bytes + 4, st));
-    int* bad = reinterpret_cast<int*>(scratch + flag_bytes);
-    csr_check_mark<<<csr_walk_grid(nrows), 256, 0, st>>>((int)nrows, row_offsets, cols,
-                                                         dia ? scratch : nullptr, bad);
-    DS_LAUNCH_CHECK("csr_check_mark");
-    int bad_h = 1;
-    DS_CUDA(cudaMemcpyAsync(&bad_h, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
-    DS_CUDA(cudaStreamSynchronize(st));
-    if (!bad_h) {
-      j->nnz = nnz;
-      j->csr_off = row_offsets;
-      j->c = const_cast<int*>(cols);
-      j->v = const_cast<double*>(values);
-      if (dia) j->flags = scratch;
-      else DS_CUDA(cudaFreeAsync(scratch, st));
-      return begin_common(j, fill_limit, job, out_nnz, out_ndiags);
-    }
-    DS_CUDA(cudaFreeAsync(scratch, st));   // not canonical: the general path
-  }
-  int* rows = nullptr;
-  if (nnz > 0) {
-    DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&rows), nnz * 4, j->st));
-    csr_expand_rows<<<grid1d(nrows * 8), 256, 0, j->st>>>((int)nrows, row_offsets, rows);
-    DS_LAUNCH_CHECK("csr_expand_rows");
-  }
-  int rc = canonicalize(j, nnz, rows, cols, values, true);
+  const int rc = begin_csr_impl(j, nnz, row_offsets, cols, values, fill_limit, out_nnz,
+                                out_ndiags);
   if (rc) {
     free_job(j);
     return rc;
   }
-  return begin_common(j, fill_limit, job, out_nnz, out_ndiags);
+  *job = j;
+  return DS_OK;
 }
 
 static unsigned dia_walk_grid(int64_t ngroups) {   // 8 warps (groups) per block
@@ -1105,20 +1153,17 @@ static int dia_emit_into(ds_convert_job* job, int* row_off, int* rows, int* cols
   return DS_OK;
 }
 
-extern "C" int ds_convert_begin_dia(int64_t nrows, int64_t ncols, int32_t ndiags,
-                                    const int32_t* offsets, const double* values, int target,
-                                    int64_t fill_limit, void* stream, ds_convert_job** job,
-                                    int64_t* out_nnz, int64_t* out_ndiags) {
-  *job = nullptr;
-  if (!dims_ok(nrows, ncols, 0)) return DS_ERR_NOT_SUPPORTED;
-  ds_convert_job* j = new_job(nrows, ncols, target, stream);
+static int begin_dia_impl(ds_convert_job* j, int32_t ndiags, const int32_t* offsets,
+                          const double* values, int64_t fill_limit, int64_t* out_nnz,
+                          int64_t* out_ndiags) {
+  const int64_t nrows = j->nrows, ncols = j->ncols;
+  const int target = j->target;
   cudaStream_t st = j->st;
   int64_t nc = 0;
   if (nrows > 0 && ndiags > 0) {
     const int64_t ngroups = ceil_div(nrows, kDiaGroupRows);
-    int *gcount = nullptr, *gstart = nullptr;
-    DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&gcount), ngroups * sizeof(int), st));
-    DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&gstart), ngroups * sizeof(int), st));
+    DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&j->gtmp), ngroups * sizeof(int), st));
+    DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&j->dsrc_start), ngroups * sizeof(int), st));
     // slot order is canonical only for strictly ascending offsets; otherwise
     // (unsorted or repeated diagonals) the entries go through the proxy's sort
     // and duplicate sums like any other source (datamove.py:208-235)
@@ -1128,32 +1173,27 @@ extern "C" int ds_convert_begin_dia(int64_t nrows, int64_t ncols, int32_t ndiags
     bool ascending = true;
     for (int q = 1; q < ndiags; ++q) ascending = ascending && h_off[q - 1] < h_off[q];
     const bool select = target == DS_FMT_DIA && ascending;   // DIA -> DIA: a column selection
-    unsigned char* present = nullptr;
-    if (select) {
-      DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&present), ndiags, st));
-      DS_CUDA(cudaMemsetAsync(present, 0, ndiags, st));
+    if (select) {   // census of the source diagonals holding an entry
+      DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&j->scratch), ndiags, st));
+      DS_CUDA(cudaMemsetAsync(j->scratch, 0, ndiags, st));
     }
     dia_group_counts<<<dia_walk_grid(ngroups), 256, 0, st>>>(nrows, (int)ncols, ndiags, offsets,
-                                                             values, ngroups, gcount, present);
+                                                             values, ngroups, j->gtmp, j->scratch);
     DS_LAUNCH_CHECK("dia_group_counts");
-    int rc = exclusive_scan(ngroups, ArrayAt{gcount}, gstart, &nc, st);
-    DS_CUDA(cudaFreeAsync(gcount, st));
-    if (rc) {
-      cudaFreeAsync(gstart, st);
-      if (present) cudaFreeAsync(present, st);
-      free_job(j);
-      return rc;
-    }
+    int rc = exclusive_scan(ngroups, ArrayAt{j->gtmp}, j->dsrc_start, &nc, st);
+    if (rc) return rc;
+    DS_CUDA(cudaFreeAsync(j->gtmp, st));
+    j->gtmp = nullptr;
     j->dsrc_off = offsets;
     j->dsrc_vals = values;
     j->dsrc_nd = ndiags;
-    j->dsrc_start = gstart;
     if (select) {
       std::vector<unsigned char> h_present(ndiags);
-      DS_CUDA(cudaMemcpyAsync(h_present.data(), present, ndiags, cudaMemcpyDeviceToHost, st));
+      DS_CUDA(cudaMemcpyAsync(h_present.data(), j->scratch, ndiags, cudaMemcpyDeviceToHost, st));
       DS_CUDA(cudaStreamSynchronize(st));
-      cudaFreeAsync(present, st);
-      cudaFreeAsync(gstart, st);
+      DS_CUDA(cudaFreeAsync(j->scratch, st));
+      j->scratch = nullptr;
+      DS_CUDA(cudaFreeAsync(j->dsrc_start, st));
       j->dsrc_start = nullptr;
       std::vector<int> jsrc, off_out;
       for (int q = 0; q < ndiags; ++q)
@@ -1173,73 +1213,85 @@ extern "C" int ds_convert_begin_dia(int64_t nrows, int64_t ncols, int32_t ndiags
       j->ndiags = nd_out;
       *out_nnz = nc;
       *out_ndiags = nd_out;
-      if (fill_limit < 0) fill_limit = 10 * std::max(nc, nrows);
+      if (fill_limit == kDefaultFillLimit) fill_limit = 10 * std::max(nc, nrows);
       if ((__int128)nd_out * (__int128)nrows > (__int128)fill_limit) {
         set_error("%lld diagonals x %lld rows = %lld value slots exceed the fill limit of %lld",
                   (long long)nd_out, (long long)nrows, (long long)(nd_out * nrows),
                   (long long)fill_limit);
-        free_job(j);
         return DS_ERR_DIA_FILL_OVERFLOW;
       }
-      *job = j;
       return DS_OK;
     }
     if (target == DS_FMT_DIA || !ascending) {   // materialise the (slot-order) COO
       int *tr = nullptr, *tc = nullptr;
       double* tv = nullptr;
-      if (nc > 0) {
+      if (nc > 0) {   // hung on the job at once: freed with it on any error
         DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tr), nc * 4, st));
+        j->r = tr;
+        j->own_r = true;
         DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tc), nc * 4, st));
+        j->c = tc;
+        j->own_c = true;
         DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tv), nc * 8, st));
+        j->v = tv;
+        j->own_v = true;
         j->nnz = nc;
         rc = dia_emit_into(j, nullptr, tr, tc, tv);
+        if (rc) return rc;
       }
-      cudaFreeAsync(gstart, st);
+      DS_CUDA(cudaFreeAsync(j->dsrc_start, st));
       j->dsrc_start = nullptr;
-      if (!rc && ascending) {
-        j->r = tr;
-        j->c = tc;
-        j->v = tv;
-        j->own_r = j->own_c = j->own_v = nc > 0;
-      } else if (!rc) {
-        rc = canonicalize(j, nc, tr, tc, tv, true);   // frees tr (or adopts it)
+      if (!ascending) {
+        // the proxy's sort: canonicalize adopts tr (own_r) and builds fresh c / v
+        j->r = nullptr;
+        j->c = nullptr;
+        j->v = nullptr;
+        j->own_r = j->own_c = j->own_v = false;
+        rc = canonicalize(j, nc, tr, tc, tv, true);
         if (j->c == tc) j->own_c = true;
         else if (tc) cudaFreeAsync(tc, st);
         if (j->v == tv) j->own_v = true;
         else if (tv) cudaFreeAsync(tv, st);
-        if (!rc) {
-          const int64_t src_nnz = nc;
-          nc = j->nnz;
-          if (fill_limit < 0) fill_limit = 10 * std::max(src_nnz, nrows);
-        }
-      }
-      if (rc) {
-        free_job(j);
-        return rc;
+        if (rc) return rc;
+        if (fill_limit == kDefaultFillLimit) fill_limit = 10 * std::max(nc, nrows);
+        nc = j->nnz;
       }
     }
   }
   j->nnz = nc;
-  if (fill_limit < 0) fill_limit = 10 * std::max(nc, nrows);   // DIA nnz = the compacted count
-  return begin_common(j, fill_limit, job, out_nnz, out_ndiags);
+  if (fill_limit == kDefaultFillLimit) fill_limit = 10 * std::max(nc, nrows);   // DIA nnz = the compacted count
+  return size_target(j, fill_limit, out_nnz, out_ndiags);
+}
+
+extern "C" int ds_convert_begin_dia(int64_t nrows, int64_t ncols, int32_t ndiags,
+                                    const int32_t* offsets, const double* values, int target,
+                                    int64_t fill_limit, void* stream, ds_convert_job** job,
+                                    int64_t* out_nnz, int64_t* out_ndiags) {
+  *job = nullptr;
+  if (!dims_ok(nrows, ncols, 0)) return DS_ERR_NOT_SUPPORTED;
+  ds_convert_job* j = new_job(nrows, ncols, target, stream);
+  const int rc = begin_dia_impl(j, ndiags, offsets, values, fill_limit, out_nnz, out_ndiags);
+  if (rc) {
+    free_job(j);
+    return rc;
+  }
+  *job = j;
+  return DS_OK;
 }
 
 __global__ void set_last_offset(int* off, int64_t nrows, int64_t nnz) { off[nrows] = (int)nnz; }
 
-extern "C" int ds_convert_finish_coo(ds_convert_job* job, int32_t* rows, int32_t* cols,
+static int finish_coo_impl(ds_convert_job* job, int32_t* rows, int32_t* cols,
                                      double* values) {
   cudaStream_t st = job->st;
   if (job->dsrc_start) {
-    const int rc = job->nnz > 0 ? dia_emit_into(job, nullptr, rows, cols, values) : DS_OK;
-    free_job(job);
-    return rc;
+    return job->nnz > 0 ? dia_emit_into(job, nullptr, rows, cols, values) : DS_OK;
   }
   if (job->csr_off && job->nnz > 0) {   // canonical CSR source: expand the rows in place
     csr_rows_walk<<<csr_walk_grid(job->nrows), 256, 0, st>>>((int)job->nrows, job->csr_off, rows);
     DS_LAUNCH_CHECK("csr_rows_walk");
     DS_CUDA(cudaMemcpyAsync(cols, job->c, job->nnz * 4, cudaMemcpyDeviceToDevice, st));
     DS_CUDA(cudaMemcpyAsync(values, job->v, job->nnz * 8, cudaMemcpyDeviceToDevice, st));
-    free_job(job);
     return DS_OK;
   }
   if (job->nnz > 0) {
@@ -1247,19 +1299,16 @@ extern "C" int ds_convert_finish_coo(ds_convert_job* job, int32_t* rows, int32_t
     DS_CUDA(cudaMemcpyAsync(cols, job->c, job->nnz * 4, cudaMemcpyDeviceToDevice, st));
     DS_CUDA(cudaMemcpyAsync(values, job->v, job->nnz * 8, cudaMemcpyDeviceToDevice, st));
   }
-  free_job(job);
   return DS_OK;
 }
 
-extern "C" int ds_convert_finish_csr(ds_convert_job* job, int32_t* row_offsets, int32_t* cols,
+static int finish_csr_impl(ds_convert_job* job, int32_t* row_offsets, int32_t* cols,
                                      double* values) {
   cudaStream_t st = job->st;
   if (job->dsrc_start) {   // row offsets written by the emit pass
     set_last_offset<<<1, 1, 0, st>>>(row_offsets, job->nrows, job->nnz);
     DS_LAUNCH_CHECK("set_last_offset");
-    const int rc = dia_emit_into(job, row_offsets, nullptr, cols, values);
-    free_job(job);
-    return rc;
+    return dia_emit_into(job, row_offsets, nullptr, cols, values);
   }
   if (job->csr_off) {   // canonical CSR source: a copy
     DS_CUDA(cudaMemcpyAsync(row_offsets, job->csr_off, (job->nrows + 1) * 4,
@@ -1268,7 +1317,6 @@ extern "C" int ds_convert_finish_csr(ds_convert_job* job, int32_t* row_offsets, 
       DS_CUDA(cudaMemcpyAsync(cols, job->c, job->nnz * 4, cudaMemcpyDeviceToDevice, st));
       DS_CUDA(cudaMemcpyAsync(values, job->v, job->nnz * 8, cudaMemcpyDeviceToDevice, st));
     }
-    free_job(job);
     return DS_OK;
   }
   rows_to_offsets<<<grid1d(job->nnz + 1 > job->nrows + 1 ? job->nnz + 1 : job->nrows + 1), 256, 0,
@@ -1278,11 +1326,10 @@ extern "C" int ds_convert_finish_csr(ds_convert_job* job, int32_t* row_offsets, 
     DS_CUDA(cudaMemcpyAsync(cols, job->c, job->nnz * 4, cudaMemcpyDeviceToDevice, st));
     DS_CUDA(cudaMemcpyAsync(values, job->v, job->nnz * 8, cudaMemcpyDeviceToDevice, st));
   }
-  free_job(job);
   return DS_OK;
 }
 
-extern "C" int ds_convert_finish_dia(ds_convert_job* job, int32_t* offsets, double* values) {
+static int finish_dia_impl(ds_convert_job* job, int32_t* offsets, double* values) {
   cudaStream_t st = job->st;
   const int64_t nd = job->ndiags;
   if (nd > 0) {
@@ -1294,16 +1341,14 @@ extern "C" int ds_convert_finish_dia(ds_convert_job* job, int32_t* offsets, doub
                                                     (int)nd, job->dsrc_off, job->dsrc_vals,
                                                     job->dia_jsrc, values);
       DS_LAUNCH_CHECK("dia_copy_diags");
-      free_job(job);
-      return DS_OK;
+        return DS_OK;
     }
     const int R = kCsrWalkRows * 8;   // 8 warps
     if (job->csr_off && (int64_t)R * nd * 8 <= 48 * 1024) {
       dia_fill_csr<<<csr_walk_grid(job->nrows), 256, (size_t)R * nd * 8, st>>>(
           (int)job->nrows, (int)nd, R, job->csr_off, job->c, job->v, job->diag_map, values);
       DS_LAUNCH_CHECK("dia_fill_csr");
-      free_job(job);
-      return DS_OK;
+        return DS_OK;
     }
     if (job->csr_off && job->nnz > 0) {   // slab too wide for shared memory: expand the rows
       DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&job->r), job->nnz * 4, st));
@@ -1317,8 +1362,28 @@ extern "C" int ds_convert_finish_dia(ds_convert_job* job, int32_t* offsets, doub
                                                   job->v, job->diag_map, values);
     DS_LAUNCH_CHECK("dia_scatter");
   }
-  free_job(job);
   return DS_OK;
+}
+
+// finish_* frees the job on every path (a DS_CUDA early return included)
+extern "C" int ds_convert_finish_coo(ds_convert_job* job, int32_t* rows, int32_t* cols,
+                                     double* values) {
+  const int rc = finish_coo_impl(job, rows, cols, values);
+  free_job(job);
+  return rc;
+}
+
+extern "C" int ds_convert_finish_csr(ds_convert_job* job, int32_t* row_offsets, int32_t* cols,
+                                     double* values) {
+  const int rc = finish_csr_impl(job, row_offsets, cols, values);
+  free_job(job);
+  return rc;
+}
+
+extern "C" int ds_convert_finish_dia(ds_convert_job* job, int32_t* offsets, double* values) {
+  const int rc = finish_dia_impl(job, offsets, values);
+  free_job(job);
+  return rc;
 }
 
 extern "C" void ds_convert_abort(ds_convert_job* job) { free_job(job); }

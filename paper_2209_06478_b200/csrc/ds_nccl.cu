@@ -84,8 +84,8 @@ static int nccl_fail(ncclResult_t r, const char* what) {
 
 __global__ void pack_kernel(int64_t count, const int* __restrict__ idx,
                             const double* __restrict__ src, double* __restrict__ dst,
-                            const int* guard) {
-  if (guard && *guard) return;
+                            const ds_cg_scalars* s) {
+  if (s && s->done) return;   // converged / stopped: p is final, the buffer already holds it
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < count;
        k += (int64_t)gridDim.x * blockDim.x)
     dst[k] = src[idx[k]];
@@ -131,7 +131,8 @@ extern "C" int ds_nccl_comm_destroy(void* comm) {
 extern "C" int ds_halo_exchange(int nnbr, const int32_t* peers, const int64_t* send_counts,
                                 const int32_t* const* send_idx, double* const* send_bufs,
                                 const int64_t* recv_counts, const int64_t* recv_starts,
-                                double* x_full, const int32_t* guard, void* comm, void* stream) {
+                                double* x_full, const ds_cg_scalars* s, void* comm,
+                                void* stream) {
   int rc = nccl_ready();
   if (rc) return rc;
   cudaStream_t st = as_stream(stream);
@@ -139,8 +140,7 @@ extern "C" int ds_halo_exchange(int nnbr, const int32_t* peers, const int64_t* s
     if (send_counts[q] <= 0) continue;
     int64_t g = ceil_div(send_counts[q], 256);
     if (g > (int64_t)sm_count() * 4) g = (int64_t)sm_count() * 4;
-    pack_kernel<<<(unsigned)g, 256, 0, st>>>(send_counts[q], send_idx[q], x_full, send_bufs[q],
-                                             guard);
+    pack_kernel<<<(unsigned)g, 256, 0, st>>>(send_counts[q], send_idx[q], x_full, send_bufs[q], s);
   }
   DS_LAUNCH_CHECK("pack_kernel");
   ncclComm_t c = reinterpret_cast<ncclComm_t>(comm);

@@ -320,8 +320,7 @@ class PcgEngine:
         from . import _device
         cap = torch.cuda.Stream(self.dev)
         cap.wait_stream(torch.cuda.current_stream(self.dev))
-        with torch.cuda.stream(cap):
-            ws = _device.workspace(self.dev)       # workspace bound to the capture stream
+        ws = _device.new_workspace(self.dev)   # owned by this graph (kept on the engine)
         torch.cuda.synchronize(self.dev)
         saved, self.ws = self.ws, ws
         g = torch.cuda.CUDAGraph()
@@ -330,6 +329,7 @@ class PcgEngine:
                 self.step(cap.cuda_stream)
         self.ws = saved
         self.graph = g
+        self._graph_ws = ws
 
     def run(self, use_graph: bool = True, chunk: int = 4) -> CgResult:
         from . import _device

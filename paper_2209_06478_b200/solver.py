@@ -318,8 +318,7 @@ class CgEngine:
         from . import _device
         cap = torch.cuda.Stream(self.dev)
         cap.wait_stream(torch.cuda.current_stream(self.dev))
-        with torch.cuda.stream(cap):
-            ws = _device.workspace(self.dev)
+        ws = _device.new_workspace(self.dev)   # owned by this graph (kept on the engine)
         torch.cuda.synchronize(self.dev)
         try:
             a, b, c, d = (torch.cuda.Event(enable_timing=True, external=True) for _ in range(4))
@@ -359,8 +358,7 @@ class CgEngine:
         from . import _device
         cap = torch.cuda.Stream(self.dev)
         cap.wait_stream(torch.cuda.current_stream(self.dev))
-        with torch.cuda.stream(cap):
-            ws = _device.workspace(self.dev)  # workspace bound to the capture stream
+        ws = _device.new_workspace(self.dev)   # owned by this graph (kept on the engine)
         torch.cuda.synchronize(self.dev)
         saved, self.ws = self.ws, ws
         # keep the vectors L2-resident across iterations (captured into the
@@ -382,12 +380,13 @@ class CgEngine:
         # the window now lives in the graph's kernel nodes; the carve-out
         # (cudaLimitPersistingL2CacheSize) stays set for the replays
         self.graph = g
+        self._graph_ws = ws
 
 
 # graph replays between two scalar readbacks at most (each replay = chunk
 # iterations): converged iterations still launch (as no-ops), so the cap
 # bounds that overshoot against the cost of a readback
-_MAX_ROUNDS = int(os.environ.get("DS_CG_MAX_ROUNDS", "4"))   # e2e solve: 4 -> 1068 vs 16 -> 994 GFLOP/s
+_MAX_ROUNDS = max(1, int(os.environ.get("DS_CG_MAX_ROUNDS", "4")))   # e2e solve: 4 -> 1068 vs 16 -> 994 GFLOP/s
 
 
 def _finish(engine: CgEngine, sc) -> tuple[int, np.ndarray, bool]:
