@@ -300,12 +300,64 @@ def large(ds, hashes):
     print(f"power-law done in {time.time() - t0:.1f}s", flush=True)
 
 
+def config_sizes(ds, hashes):
+    """BASELINE config sizes the GPU parity tests pin (round 2):
+
+    * config 3: the reference's CG at 104^3 (local DIA, tol 1e-9, the
+      defaults): iteration count, the whole residual history and every
+      997th entry of x -> cg104.npz (x itself is 9 MB);
+    * config 5: the 192^3 partition's conversions (CSR->DIA, DIA->CSR,
+      CSR->COO) and SpMV digests (DIA takes the x-window kernel on the GPU)."""
+    t0 = time.time()
+    F = ds.FormatId
+    prob = ds.generate_problem(ds.GridSpec(104, 104, 104))
+    part = prob.partitions[0]
+    d = ds.convert(part.a_full, F.DIA)
+    res = ds.cg(ds.ExecBackend.threaded(os.cpu_count() or 1), d, part.b, tol=1e-9, max_iters=500)
+    x = np.asarray(res.x.data)
+    np.savez_compressed(os.path.join(HERE, "cg104.npz"), history=np.asarray(res.residual_history),
+                        iterations=res.iterations, converged=res.converged,
+                        x_sample=x[::997].copy(), x_min=x.min(), x_max=x.max())
+    hashes["cg104/iterations"] = int(res.iterations)
+    print(f"cg104: {res.iterations} iterations in {time.time() - t0:.1f}s", flush=True)
+    del prob, part, d, res
+    t0 = time.time()
+    prob = ds.generate_problem(ds.GridSpec(192, 192, 192))
+    a = prob.partitions[0].a_full
+    hashes["st192/csr"] = digest(a.row_offsets, a.col_indices, a.values)
+    n = a.nrows
+    xv = np.random.default_rng(0).standard_normal(n)
+    y = ds.DenseVector.zeros(n)
+    ds.spmv(ds.SERIAL, a, ds.DenseVector(xv), y)
+    hashes["st192/spmv_csr"] = digest(y.data)
+    d = ds.convert(a, F.DIA)
+    hashes["st192/convert_dia"] = digest(d.offsets, d.values)
+    ds.spmv(ds.SERIAL, d, ds.DenseVector(xv), y)
+    hashes["st192/spmv_dia"] = digest(y.data)
+    back = ds.convert(d, F.CSR)
+    hashes["st192/dia_to_csr"] = digest(back.row_offsets, back.col_indices, back.values)
+    del back, d
+    c = ds.convert(a, F.COO)
+    hashes["st192/convert_coo"] = digest(c.row_indices, c.col_indices, c.values)
+    print(f"192^3 done in {time.time() - t0:.1f}s", flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--large", action="store_true")
+    ap.add_argument("--config-sizes", action="store_true",
+                    help="only add the config-3/5 keys (cg104.npz, st192/*) to golden_hashes.json")
     args = ap.parse_args()
     sys.path.insert(0, REF)
     import dynsparse as ds  # the real reference, read-only
+    if args.config_sizes:
+        path = os.path.join(HERE, "golden_hashes.json")
+        with open(path) as fh:
+            hashes = json.load(fh)
+        config_sizes(ds, hashes)
+        with open(path, "w") as fh:
+            json.dump(hashes, fh, indent=1, sort_keys=True)
+        return
     out: dict[str, np.ndarray] = {}
     small(ds, out)
     np.savez_compressed(os.path.join(HERE, "kat_small.npz"), **out)

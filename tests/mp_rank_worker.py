@@ -39,6 +39,13 @@ def main() -> None:
     import paper_2209_06478_b200 as ds
     from paper_2209_06478_b200 import dist as D
 
+    rank = int(os.environ["RANK"])
+    if os.environ.get("DS_TEST_NCCL_FAKE_HOSTS") == "1":
+        # several NCCL ranks on ONE GPU: NCCL refuses two ranks of a
+        # communicator on one device of one host, so each rank claims its own
+        # host id and the ranks talk through NCCL's socket transport (loopback)
+        os.environ["NCCL_HOSTID"] = f"ds-test-host-{rank}"
+        os.environ.setdefault("NCCL_SOCKET_IFNAME", "lo")
     dist.init_process_group("gloo")
     rank, world = dist.get_rank(), dist.get_world_size()
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", rank)) % torch.cuda.device_count())

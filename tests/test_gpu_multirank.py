@@ -39,6 +39,9 @@ def run_ranks(tmp_path, grid, procs, *, local_format="dia", transport="peer", wa
     world = procs[0] * procs[1] * procs[2]
     env = dict(os.environ, DS_PEER_WAIT=wait, OMP_NUM_THREADS="1",
                OPENBLAS_NUM_THREADS="1", PYTHONPATH=ROOT)
+    import torch
+    if transport == "nccl" and torch.cuda.device_count() < world:
+        env["DS_TEST_NCCL_FAKE_HOSTS"] = "1"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={world}", "--master-addr=127.0.0.1",
            f"--master-port={_free_port()}", os.path.join(ROOT, "tests", "mp_rank_worker.py"),
@@ -121,4 +124,14 @@ def test_tuner_modes_agree_across_ranks(tmp_path):
     csr = 1
     assert (plans[:, 1, 1] == csr).all() and (plans[:, 2, 0] == csr).all()
     assert (plans[:, 2, 1] != 2).all()       # the remote part overflows DIA: never chosen
+    check_against_oracle(outs, oracle_dist(grid, procs))
+
+
+@pytest.mark.parametrize("procs", [(2, 1, 1), (2, 2, 2)])
+def test_nccl_rank_cg_matches_oracle(tmp_path, procs):
+    """The NCCL transport (pack kernels + grouped send/recv + ncclAllGather)
+    at world 2 and 8.  On one GPU the ranks claim distinct NCCL host ids and
+    talk over NCCL's socket transport; on a node they use NVLink."""
+    grid = (8, 6, 6)
+    outs = run_ranks(tmp_path, grid, procs, transport="nccl", graph_steps=4, timeout=900)
     check_against_oracle(outs, oracle_dist(grid, procs))
