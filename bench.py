@@ -191,14 +191,31 @@ def time_spmv(ds, torch, m, x, y, warm=20, reps=200, batch=40):
     return statistics.median(e0.elapsed_time(e1) / batch for e0, e1 in ev)
 
 
-def sweep_104(ds, torch, a_full, dev, peak):
+def _gpu_ms(torch, fn, reps: int = 3) -> float:
+    """Best-of wall ms of a device operation, CUDA-synchronised on both sides."""
+    best = float("inf")
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        fn()
+        torch.cuda.synchronize()
+        best = min(best, (time.perf_counter() - t0) * 1e3)
+    return round(best, 3)
+
+
+def sweep_104(ds, torch, a_full, dev, peak, cpu=None):
+    """BASELINE config 2: COO / CSR / DIA SpMV of the 104^3 stencil (median
+    per launch), the four conversions between them, and -- with ``cpu`` (the
+    oracle's numbers on this host) -- the CPU serial / threaded times beside."""
     import numpy as np
     n = a_full.nrows
     x = ds.DenseVector(torch.from_numpy(np.random.default_rng(0).standard_normal(n)).to(dev))
     y = ds.DenseVector.zeros(n, ds.MemorySpace.DEVICE, dev)
     out = {}
+    mats = {}
     for name in ("coo", "csr", "dia"):
         m = ds.convert(a_full, ds.FormatId[name.upper()])
+        mats[name] = m
         ms = time_spmv(ds, torch, m, x, y)
         nnz = a_full.nnz
         if name == "csr":
@@ -210,11 +227,25 @@ def sweep_104(ds, torch, a_full, dev, peak):
         gbs = b / (ms * 1e-3) / 1e9
         out[name] = {"ms": round(ms, 5), "gflops": round(2 * nnz / (ms * 1e-3) / 1e9, 1),
                      "gbs": round(gbs, 1), "frac": round(gbs / peak, 3), "bytes": b}
-        del m
+        if cpu and name in cpu.get("spmv", {}):
+            c = cpu["spmv"][name]
+            out[name]["cpu_serial_ms"] = c["serial_ms"]
+            out[name]["cpu_threaded_ms"] = c["threaded_ms"]
+            out[name]["speedup_vs_cpu_threaded"] = round(c["threaded_ms"] / ms, 1)
+    F = ds.FormatId
+    conv = {"csr->dia": _gpu_ms(torch, lambda: ds.convert(mats["csr"], F.DIA)),
+            "dia->csr": _gpu_ms(torch, lambda: ds.convert(mats["dia"], F.CSR)),
+            "csr->coo": _gpu_ms(torch, lambda: ds.convert(mats["csr"], F.COO)),
+            "coo->csr": _gpu_ms(torch, lambda: ds.convert(mats["coo"], F.CSR))}
+    out["convert_ms"] = conv
+    if cpu and "convert_ms" in cpu:
+        out["cpu_convert_ms"] = cpu["convert_ms"]
+        out["cpu_cores"] = cpu["cores"]
+    del mats
     return out
 
 
-def sweep_powerlaw(ds, torch, dev, peak):
+def sweep_powerlaw(ds, torch, dev, peak, cpu_threads: int = 0):
     """BASELINE config 4: generator of BASELINE.md §2, device conversion, CSR vs
     COO SpMV, DIA overflow; the tuner's choice is the measured-fastest format."""
     import numpy as np
@@ -250,6 +281,15 @@ def sweep_powerlaw(ds, torch, dev, peak):
         gbs = b / (ms * 1e-3) / 1e9
         out[name] = {"ms": round(ms, 4), "gflops": round(2 * nnz / (ms * 1e-3) / 1e9, 1),
                      "gbs": round(gbs, 1), "frac": round(gbs / peak, 3)}
+    if cpu_threads:
+        a_host = (n, csr.row_offsets.cpu().numpy(), csr.col_indices.cpu().numpy(),
+                  csr.values.cpu().numpy())
+        c = cpu_formats_sample(a_host, cpu_threads, convert=False)["spmv"]
+        for name in ("csr", "coo"):
+            out[name]["cpu_serial_ms"] = c[name]["serial_ms"]
+            out[name]["cpu_threaded_ms"] = c[name]["threaded_ms"]
+            out[name]["speedup_vs_cpu_threaded"] = round(c[name]["threaded_ms"] / out[name]["ms"], 1)
+        out["cpu_cores"] = cpu_threads
     try:
         ds.convert(csr, ds.FormatId.DIA)
         out["dia"] = "converted"
@@ -371,17 +411,20 @@ def hpcg_mg(ds, torch, dev, nx: int = 104, iters: int = 50) -> dict:
 # CPU baseline (oracle port of the reference), bounded sample
 # ---------------------------------------------------------------------------
 
-def cpu_cg_sample(spec_args, rank_list, iters: int, threads: int) -> dict:
+def cpu_cg_sample(spec_args, iters: int, threads: int, local_fmt: str = "csr") -> dict:
     """Time ``iters`` CG iterations of the oracle on the host (untimed setup),
-    the reference's own loop (solver.py:170-188) with its threaded backend."""
+    the reference's own loop (solver.py:170-188) with its threaded backend.
+    The local part runs in ``local_fmt`` -- CSR by default, the CPU's fastest
+    format with threads; the remote part is CSR."""
     import numpy as np
     from oracle import dynsparse_oracle as O
     nx, ny, nz, px, py, pz = spec_args
     parts = [O.stencil_partition(nx, ny, nz, px, py, pz, r) for r in range(px * py * pz)]
+    fmt = {"coo": O.COO, "csr": O.CSR, "dia": O.DIA}[local_fmt]
     splits = []
     for p in parts:
         loc, rem = O.split(p)
-        splits.append((O.convert(loc, O.DIA), rem))
+        splits.append((loc if fmt == O.CSR else O.convert(loc, fmt), rem))
     P = len(parts)
     n = parts[0].a_full.nrows
     bs = [p.b for p in parts]
@@ -413,9 +456,56 @@ def cpu_cg_sample(spec_args, rank_list, iters: int, threads: int) -> dict:
     return {"value": round(fl / dt / 1e9, 4), "unit": "GFLOP/s", "cores": threads,
             "kind": "port", "seconds": round(dt, 3),
             "sample": f"{iters} CG iterations of the oracle (numpy port of the reference), "
-                      f"grid {nx}^3 x {P} partition(s), local DIA + remote CSR, "
+                      f"grid {nx}^3 x {P} partition(s), local {local_fmt.upper()} + remote CSR, "
                       f"ExecBackend.threaded({threads}), OPENBLAS_NUM_THREADS="
                       f"{os.environ.get('OPENBLAS_NUM_THREADS')}"}
+
+
+def _best_ms(fn, reps: int) -> float:
+    best = float("inf")
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        fn()
+        best = min(best, (time.perf_counter() - t0) * 1e3)
+    return round(best, 2)
+
+
+def cpu_formats_sample(a_host, threads: int, convert: bool = True) -> dict:
+    """BASELINE.md §3's CPU rows on the oracle: per-format SpMV serial and
+    threaded(N) (kernels.py:102-163) and, with ``convert``, the conversions
+    CSR<->DIA and CSR<->COO (datamove.py:261-281); best-of wall ms.
+    ``a_host`` = (nrows, offsets, cols, vals) of a canonical CSR."""
+    import numpy as np
+    from oracle import dynsparse_oracle as O
+    n, off, cols, vals = a_host
+    a = O.csr(n, n, off.astype(np.int64), cols.astype(np.int64), vals)
+    out = {"cores": threads, "kind": "port"}
+    mats = {"csr": a}
+    if convert:
+        conv = {}
+        t0 = time.perf_counter()
+        mats["dia"] = O.convert(a, O.DIA)
+        conv["csr->dia"] = round((time.perf_counter() - t0) * 1e3, 1)
+        conv["dia->csr"] = _best_ms(lambda: O.convert(mats["dia"], O.CSR), 1)
+        t0 = time.perf_counter()
+        mats["coo"] = O.convert(a, O.COO)
+        conv["csr->coo"] = round((time.perf_counter() - t0) * 1e3, 1)
+        conv["coo->csr"] = _best_ms(lambda: O.convert(mats["coo"], O.CSR), 1)
+        out["convert_ms"] = conv
+    else:   # the canonical COO of a canonical CSR: its rows expanded
+        mats["coo"] = O.coo(n, n, np.repeat(np.arange(n, dtype=np.int64), np.diff(a.offsets)),
+                            a.cols, a.vals)
+    x = np.random.default_rng(0).standard_normal(n)
+    y = np.zeros(n)
+    spmv = {}
+    for name in ("coo", "csr", "dia"):
+        if name not in mats:
+            continue
+        m = mats[name]
+        spmv[name] = {"serial_ms": _best_ms(lambda: O.spmv(m, x, y, 1), 2),
+                      "threaded_ms": _best_ms(lambda: O.spmv(m, x, y, threads), 3)}
+    out["spmv"] = spmv
+    return out
 
 
 def host_threads() -> int:
@@ -429,6 +519,14 @@ def host_threads() -> int:
 # reference arm
 # ---------------------------------------------------------------------------
 
+def config_of(nx: int, px: int, py: int, pz: int) -> dict:
+    """The workload both arms run (the per-arm format plan is reported apart)."""
+    return {"workload": f"hpcg_cg_27pt_{nx}^3_per_gpu", "grid_per_gpu": [nx, nx, nx],
+            "procs": [px, py, pz], "tol_timed": "1e-300 (fixed step count)",
+            "l2": f"no flush: the matrix ({8 * 27 * nx ** 3 / 1e6:.0f} MB/GPU as DIA) exceeds "
+                  f"the 126 MB L2 and is re-streamed every step"}
+
+
 def reference_arm(args, rank: int, world: int) -> int:
     if rank != 0:
         return 0
@@ -438,14 +536,15 @@ def reference_arm(args, rank: int, world: int) -> int:
     nx = args.nx
     # bounded sample: enough iterations for ~10-60 s of CPU work
     iters = max(1, min(args.steps, 10 if world == 1 else 3))
-    res = cpu_cg_sample((nx, nx, nx, px, py, pz), None, iters, threads)
+    res = cpu_cg_sample((nx, nx, nx, px, py, pz), iters, threads, "csr")
     line = {
         "impl": "reference", "metric": METRIC, "value": res["value"], "unit": "GFLOP/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(res["seconds"] / iters * 1e3, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"hpcg_cg_27pt_{nx}^3_per_gpu", "grid_per_gpu": [nx, nx, nx],
-                   "procs": [px, py, pz], "local_format": "dia", "remote_format": "csr"},
+        "config": config_of(nx, px, py, pz),
+        "plan": {"local_format": "csr", "remote_format": "csr",
+                 "why": "CSR is the CPU's fastest local format with threads (BASELINE.md §3)"},
         "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": res["value"], "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -508,8 +607,17 @@ def run(args, rank: int, world: int) -> int:
             "tune_s": round(t_conv - t_tune, 3), "apply_convert_ms": round((t_end - t_conv) * 1e3, 3)}
     n = part.a_full.nrows
     nnz_local = part.a_full.nnz
+    cpu_fmt = None
+    thr = host_threads()
+    if world == 1 and rank == 0 and not args.no_cpu:
+        # BASELINE.md §3 on this host: the oracle's per-format SpMV (serial /
+        # threaded) and conversions at 104^3 (about 20 s of CPU work)
+        os.environ["OPENBLAS_NUM_THREADS"] = str(thr)
+        a = part.a_full
+        cpu_fmt = cpu_formats_sample((n, a.row_offsets.cpu().numpy(), a.col_indices.cpu().numpy(),
+                                      a.values.cpu().numpy()), thr)
     if world == 1 and not args.no_sweep:
-        extras["spmv_sweep"] = sweep_104(ds, torch, part.a_full, dev, peak)
+        extras["spmv_sweep"] = sweep_104(ds, torch, part.a_full, dev, peak, cpu_fmt)
     torch.cuda.synchronize()
 
     kern_steps = min(args.steps, 200)
@@ -523,7 +631,7 @@ def run(args, rank: int, world: int) -> int:
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             os.environ.setdefault("MASTER_PORT", "29533")
             torch.distributed.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
-        eng = D.RankCG(spec, part, split, dev, 1e-300, budget)
+        eng = D.RankCG(spec, part, split, dev, 1e-300, budget, transport=args.transport)
     st = torch.cuda.current_stream(dev)
     with torch.cuda.device(dev):
         eng.setup(st.cuda_stream)
@@ -531,7 +639,7 @@ def run(args, rank: int, world: int) -> int:
         # several iterations per graph (fewer graph-launch gaps) when both
         # counts divide; each replay then advances `spg` CG iterations
         spg = 1
-        if use_graph and isinstance(eng, S.CgEngine):
+        if use_graph:
             for c in (10, 5, 4, 2):
                 if args.steps % c == 0 and args.warmup % c == 0:
                     spg = c
@@ -600,18 +708,25 @@ def run(args, rank: int, world: int) -> int:
 
     e2e = None
     cpu = None
+    parity = None
     if world > 1 or args.rank_engine:
         e2e = measure_e2e_ranks(torch, eng, part, n, nnz_total, world)
+        if world > 1:
+            parity = parity_ranks(ds, torch, dev, world, rank, args.transport)
     elif rank == 0:
         e2e = measure_e2e(ds, torch, spec, split, part, n, nnz_local)
     if rank == 0 and world == 1:
         if not args.no_cpu:
             thr = host_threads()
             os.environ["OPENBLAS_NUM_THREADS"] = str(thr)
-            cpu = cpu_cg_sample((nx, nx, nx, 1, 1, 1), None, 60, thr)   # ~5-10 s of CPU work
+            cpu = cpu_cg_sample((nx, nx, nx, 1, 1, 1), 60, thr, "csr")   # ~5-10 s of CPU work
             cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            if cpu_fmt is not None:
+                cpu["spmv_104"] = cpu_fmt["spmv"]
+                cpu["convert_104_ms"] = cpu_fmt["convert_ms"]
         if not args.no_powerlaw:
-            extras["powerlaw"] = sweep_powerlaw(ds, torch, dev, peak)
+            extras["powerlaw"] = sweep_powerlaw(ds, torch, dev, peak,
+                                                0 if args.no_cpu else thr)
         if not args.no_config5:
             extras["format_switching_192"] = format_switching(ds, torch, dev, peak)
         if not args.no_mg:
@@ -623,16 +738,16 @@ def run(args, rank: int, world: int) -> int:
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 5),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": f"hpcg_cg_27pt_{nx}^3_per_gpu", "grid_per_gpu": [nx, nx, nx],
-                   "procs": [px, py, pz], "local_format": plan[0], "remote_format": plan[1],
-                   "format_selection": "fixed" if args.fixed_plan else "tuner multi (per GPU)",
-                   "flops_per_step": flops_per_iter(nnz_total, n * world),
-                   "graph": not args.eager, "steps_per_graph": spg,
-                   "l2": f"no flush: the DIA matrix ({8 * 27 * n / 1e6:.0f} MB/GPU) exceeds the "
-                         f"126 MB L2 and is re-streamed every step"},
+        "config": config_of(nx, px, py, pz),
+        "plan": {"local_format": plan[0], "remote_format": plan[1],
+                 "format_selection": "fixed" if args.fixed_plan else "tuner multi (per GPU)",
+                 "flops_per_step": flops_per_iter(nnz_total, n * world),
+                 "graph": not args.eager, "steps_per_graph": spg,
+                 "transport": getattr(getattr(eng, "T", None), "name", "in-process")},
         "roofline": roof,
         "e2e": e2e,
         "cpu_baseline": cpu,
+        "parity": parity if parity is not None else (e2e or {}).get("parity"),
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk,
         "cg_state": state,
@@ -644,6 +759,52 @@ def run(args, rank: int, world: int) -> int:
     if torch.distributed.is_initialized():
         torch.distributed.destroy_process_group()
     return 0
+
+
+def _golden(name: str) -> dict:
+    import numpy as np
+    with np.load(os.path.join(ROOT, "tests", "golden", name)) as z:
+        return {k: z[k] for k in z.files}
+
+
+def _history_parity(hist, it, ref_hist, ref_it) -> dict:
+    import numpy as np
+    k = min(int(it), int(ref_it)) + 1
+    rel = float(np.max(np.abs(hist[:k] - ref_hist[:k]) / ref_hist[:k]))
+    return {"iterations": int(it), "reference_iterations": int(ref_it),
+            "max_history_rel_diff": rel,
+            "pass": abs(int(it) - int(ref_it)) <= 1 and rel <= 1e-8}
+
+
+def parity_ranks(ds, torch, dev, world, rank, transport) -> dict:
+    """N > 1: the REFERENCE's distributed CG at 16^3 per rank on this job's
+    process grid (tests/golden/cgdist16.npz, written by the real reference
+    with tests/golden/make_golden.py) re-run through dist.RankCG with the
+    bench's transport; iterations +-1, history within 1e-8, x within 1e-8."""
+    import numpy as np
+    from paper_2209_06478_b200 import dist as D
+    px, py, pz = procs_for(world)
+    key = f"p{px}{py}{pz}"
+    ref = _golden("cgdist16.npz")
+    spec = ds.GridSpec(16, 16, 16, px, py, pz)
+    part = ds.generate_partition(spec, rank, space=ds.MemorySpace.DEVICE, device=dev)
+    split = ds.split_local_remote(ds.PartitionedProblem(spec, [part]), 0)
+    ds.convert_inplace(split.local, ds.FormatId.DIA)
+    eng = D.RankCG(spec, part, split, dev, 1e-9, 500, transport=transport)
+    try:
+        x, it, hist, conv = eng.solve()
+    finally:
+        eng.close()
+    out = _history_parity(hist, it, ref[f"{key}/history"], ref[f"{key}/iterations"])
+    xerr = float(np.max(np.abs(x.data.cpu().numpy() - ref[f"{key}/x{rank}"])))
+    t = torch.tensor([out["max_history_rel_diff"], xerr, 0.0 if out["pass"] else 1.0],
+                     dtype=torch.float64, device=dev)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    out["max_history_rel_diff"], out["max_x_abs_diff_over_ranks"] = float(t[0]), float(t[1])
+    out["pass"] = bool(t[2] == 0.0 and t[1] <= 1e-8)
+    out.update({"grid_per_rank": [16, 16, 16], "procs": [px, py, pz], "transport": transport,
+                "against": "reference golden tests/golden/cgdist16.npz"})
+    return out
 
 
 def measure_e2e(ds, torch, spec, split, part, n, nnz, reps=3):
@@ -665,11 +826,22 @@ def measure_e2e(ds, torch, spec, split, part, n, nnz, reps=3):
         iters = res.iterations
     t = statistics.median(times[1:])
     fl = iters * flops_per_iter(nnz, n)
-    return {"value": round(fl / t / 1e9, 2), "unit": "GFLOP/s", "h2d_bytes_per_step": 8 * n,
-            "d2h_bytes_per_step": 8 * n + 8 * (iters + 1),
-            "step": f"one ds.cg() solve with the reference's defaults (tol 1e-9): {iters} "
-                    f"iterations, host numpy b -> host numpy x",
-            "iterations": iters, "seconds": round(t, 5)}
+    out = {"value": round(fl / t / 1e9, 2), "unit": "GFLOP/s", "h2d_bytes_per_step": 8 * n,
+           "d2h_bytes_per_step": 8 * n + 8 * (iters + 1),
+           "step": f"one ds.cg() solve with the reference's defaults (tol 1e-9): {iters} "
+                   f"iterations, host numpy b -> host numpy x",
+           "iterations": iters, "seconds": round(t, 5)}
+    if spec.nx == 104 and spec.npartitions == 1:
+        # the solve's history and x against the REFERENCE's own 104^3 CG
+        ref = _golden("cg104.npz")
+        par = _history_parity(res.residual_history, res.iterations, ref["history"],
+                              ref["iterations"])
+        x = res.x[0].data
+        par["max_x_sample_abs_diff"] = float(np.max(np.abs(x[::997] - ref["x_sample"])))
+        par["pass"] = par["pass"] and par["max_x_sample_abs_diff"] <= 1e-8
+        par["against"] = "reference golden tests/golden/cg104.npz"
+        out["parity"] = par
+    return out
 
 
 def measure_e2e_ranks(torch, eng, part, n, nnz_total, world, iters=50, reps=3):
@@ -719,7 +891,9 @@ def main(argv=None) -> int:
     ap.add_argument("--fixed-plan", action="store_true",
                     help="local DIA / remote CSR instead of the per-GPU tuner's choice")
     ap.add_argument("--rank-engine", action="store_true",
-                    help="at N=1 use the NCCL one-partition-per-process engine (dist.RankCG)")
+                    help="at N=1 use the one-partition-per-process engine (dist.RankCG)")
+    ap.add_argument("--transport", choices=("peer", "nccl"), default="peer",
+                    help="dist.RankCG's halo / dot transport at N > 1 (default: peer memory)")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")

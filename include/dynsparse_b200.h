@@ -163,6 +163,12 @@ int ds_dia_count_nonzero(int64_t nrows, int64_t ncols, int32_t ndiags, const int
  * summed like duplicate COO entries (datamove.py:208-235).                 */
 #define DS_FILL_LIMIT_DEFAULT ((int64_t)(-9223372036854775807LL - 1))
 typedef struct ds_convert_job ds_convert_job;
+/* The canonicalisation's stable sort, exposed for tests: keys_in[0..n) <
+ * 2^bits sorted ascending into keys_out, perm_out[i] = the input position of
+ * keys_out[i]; equal keys keep their input order (np.lexsort's stability,
+ * datamove.py:212).  Hand-written onesweep LSD radix sort, 8 bits a pass. */
+int ds_radix_sort_pairs(const unsigned long long* keys_in, int64_t n, int bits,
+                        unsigned long long* keys_out, int32_t* perm_out, void* stream);
 enum { DS_FMT_COO = 0, DS_FMT_CSR = 1, DS_FMT_DIA = 2 };   /* FormatId, formats.py:33-42 */
 
 int ds_convert_begin_coo(int64_t nrows, int64_t ncols, int64_t nnz, const int32_t* rows,

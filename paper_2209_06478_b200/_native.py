@@ -163,6 +163,7 @@ _SIGNATURES = {
     "ds_halo_exchange": (c_int, [c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                                  c_vp]),
     "ds_allgather_f64": (c_int, [c_vp, c_vp, c_i64, c_vp, c_vp]),
+    "ds_radix_sort_pairs": (c_int, [c_vp, c_i64, c_int, c_vp, c_vp, c_vp]),
     "ds_ipc_handle_bytes": (c_int, []),
     "ds_ipc_export": (c_int, [c_vp, ctypes.c_char_p]),
     "ds_ipc_import": (c_int, [ctypes.c_char_p, ctypes.POINTER(c_vp)]),

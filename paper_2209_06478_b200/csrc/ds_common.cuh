@@ -51,6 +51,11 @@ void x_window_end(cudaStream_t st);
 int max_dynamic_smem();   // opt-in shared memory per block (bytes), cached per device
 // raise a kernel's dynamic shared-memory limit to `bytes` (minus its static use)
 int allow_dynamic_smem(const void* kernel, size_t bytes);
+// stable LSD radix sort (ds_sort.cu): keys (or rows[k]*ncols+cols[k] when
+// keys == nullptr) <= max_key -> sorted keys + the stable permutation
+int radix_sort_pairs(const unsigned long long* keys, const int* rows, const int* cols,
+                     unsigned long long ncols, int64_t n, unsigned long long max_key,
+                     unsigned long long* keys_out, int* perm_out, cudaStream_t st);
 constexpr int kWarp = 32;
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }

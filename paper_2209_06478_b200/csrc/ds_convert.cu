@@ -14,11 +14,9 @@
 // the identity); a DIA source yields canonical order directly (row-major walk
 // of the slab, columns ascending because offsets ascend).
 //
-// Integer scans and histograms are hand-written (3-phase block scan).  The
-// general-case stable sort uses CUB's LSD radix sort (DeviceRadixSort::
-// SortPairs on (row*ncols+col, index) keys limited to the needed bits) -- a
-// documented stop-gap until a hand-written onesweep lands.
-#include <cub/device/device_radix_sort.cuh>
+// Integer scans and histograms are hand-written (3-phase block scan); the
+// general-case stable sort is ds_sort.cu's onesweep LSD radix sort on
+// (row*ncols+col, index) keys limited to the needed bits.
 #include <vector>
 
 #include "ds_common.cuh"
@@ -634,27 +632,21 @@ static int canonicalize(ds_convert_job* job, int64_t nnz, const int* rows, const
     return DS_OK;
   }
   // stable radix sort of (row*ncols + col) keys with the entry index
-  unsigned long long *keys = nullptr, *keys_s = nullptr;
-  int *idx = nullptr, *perm = nullptr, *pos = nullptr;
-  DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&keys), nnz * 8, st));
+  // (np.lexsort((cols, rows)) is stable, datamove.py:212); ds_sort.cu builds
+  // the keys from the index arrays in its first pass
+  unsigned long long* keys_s = nullptr;
+  int *perm = nullptr, *pos = nullptr;
   DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&keys_s), nnz * 8, st));
-  DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&idx), nnz * 4, st));
   DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&perm), nnz * 4, st));
-  make_keys<<<grid1d(nnz), 256, 0, st>>>(nnz, job->ncols, rows, cols, keys, idx);
-  DS_LAUNCH_CHECK("make_keys");
   const unsigned long long maxkey =
-      (unsigned long long)(job->nrows > 0 ? job->nrows : 1) * (unsigned long long)(job->ncols > 0 ? job->ncols : 1);
-  const int end_bit = bits_for(maxkey - 1);
-  size_t tmp_bytes = 0;
-  DS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys_s, idx, perm, (int)nnz, 0,
-                                          end_bit, st));
-  void* tmp = nullptr;
-  DS_CUDA(cudaMallocAsync(&tmp, tmp_bytes, st));
-  DS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys_s, idx, perm, (int)nnz, 0,
-                                          end_bit, st));
-  DS_CUDA(cudaFreeAsync(tmp, st));
-  DS_CUDA(cudaFreeAsync(keys, st));
-  DS_CUDA(cudaFreeAsync(idx, st));
+      (unsigned long long)(job->nrows > 0 ? job->nrows : 1) * (unsigned long long)(job->ncols > 0 ? job->ncols : 1) - 1ull;
+  rc = radix_sort_pairs(nullptr, rows, cols, (unsigned long long)job->ncols, nnz, maxkey, keys_s,
+                        perm, st);
+  if (rc) {
+    cudaFreeAsync(keys_s, st);
+    cudaFreeAsync(perm, st);
+    return rc;
+  }
   if (rows_owned) {
     job->r = nullptr;
     job->own_r = false;
@@ -915,15 +907,17 @@ extern "C" int ds_stencil_begin(int nx, int ny, int nz, int px, int py, int pz, 
     int* pos = nullptr;
     DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&keys), gtotal * 8, st));
     DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&sorted), gtotal * 8, st));
+    int* perm_unused = nullptr;
+    DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&perm_unused), gtotal * 4, st));
     DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&pos), gtotal * 4, st));
     stencil_ghost_keys<<<grid1d(n), 256, 0, st>>>(g, n, gpos, keys);
     DS_LAUNCH_CHECK("stencil_ghost_keys");
-    size_t tmp_bytes = 0;
-    DS_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, keys, sorted, (int)gtotal, 0, 64, st));
-    void* tmp = nullptr;
-    DS_CUDA(cudaMallocAsync(&tmp, tmp_bytes, st));
-    DS_CUDA(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, keys, sorted, (int)gtotal, 0, 64, st));
-    DS_CUDA(cudaFreeAsync(tmp, st));
+    // ghost keys = owner * n + owner-local < P * n
+    rc = radix_sort_pairs(keys, nullptr, nullptr, 0, gtotal,
+                          (unsigned long long)(px * py * pz) * (unsigned long long)n - 1ull, sorted,
+                          perm_unused, st);
+    if (rc) return rc;
+    DS_CUDA(cudaFreeAsync(perm_unused, st));
     rc = exclusive_scan(gtotal, KeyHead{sorted}, pos, &G, st);
     if (rc) return rc;
     DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&j->ukeys), (G > 0 ? G : 1) * 8, st));

@@ -321,6 +321,21 @@ def config_sizes(ds, hashes):
     hashes["cg104/iterations"] = int(res.iterations)
     print(f"cg104: {res.iterations} iterations in {time.time() - t0:.1f}s", flush=True)
     del prob, part, d, res
+    # the reference's distributed CG at 16^3 per partition for the bench's
+    # process grids of 2 / 4 / 8 GPUs (stencil.py:280-319, solver.py:120-189)
+    dist = {}
+    for procs in ((2, 1, 1), (2, 2, 1), (2, 2, 2)):
+        prob = ds.generate_problem(ds.GridSpec(16, 16, 16, *procs))
+        splits = [ds.split_local_remote(prob, k) for k in range(prob.npartitions)]
+        res = ds.cg(ds.SERIAL, ds.DistributedOperator(prob, splits),
+                    [p.b for p in prob.partitions], tol=1e-9, max_iters=500)
+        key = "p%d%d%d" % procs
+        dist[f"{key}/iterations"] = np.array(res.iterations)
+        dist[f"{key}/history"] = np.asarray(res.residual_history)
+        for k in range(prob.npartitions):
+            dist[f"{key}/x{k}"] = np.asarray(res.x[k].data)
+    np.savez_compressed(os.path.join(HERE, "cgdist16.npz"), **dist)
+    print("cgdist16 done", flush=True)
     t0 = time.time()
     prob = ds.generate_problem(ds.GridSpec(192, 192, 192))
     a = prob.partitions[0].a_full

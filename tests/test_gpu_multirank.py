@@ -135,3 +135,18 @@ def test_nccl_rank_cg_matches_oracle(tmp_path, procs):
     grid = (8, 6, 6)
     outs = run_ranks(tmp_path, grid, procs, transport="nccl", graph_steps=4, timeout=900)
     check_against_oracle(outs, oracle_dist(grid, procs))
+
+
+@pytest.mark.parametrize("procs", [(2, 1, 1), (2, 2, 1), (2, 2, 2)])
+def test_peer_rank_cg_matches_reference_golden(tmp_path, procs):
+    """16^3 per rank on the bench's process grids against the REFERENCE's own
+    distributed CG (tests/golden/cgdist16.npz from make_golden.py)."""
+    from conftest import GOLDEN
+    with np.load(os.path.join(GOLDEN, "cgdist16.npz")) as z:
+        key = "p%d%d%d" % procs
+        ref = type("Ref", (), {})()
+        ref.iterations = int(z[f"{key}/iterations"])
+        ref.history = z[f"{key}/history"]
+        ref.x = [z[f"{key}/x{k}"] for k in range(procs[0] * procs[1] * procs[2])]
+    outs = run_ranks(tmp_path, (16, 16, 16), procs, graph_steps=4)
+    check_against_oracle(outs, ref)
