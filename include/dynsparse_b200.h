@@ -233,6 +233,8 @@ typedef struct ds_matrix {
   int32_t max_row_len;       /* CSR / sorted COO: longest row if known, else 0  */
   const int32_t* row_perm;   /* CSR: rows grouped by length bin (ds_csr_bins), or NULL */
   int64_t bins[9];           /* CSR: bin b = row_perm[bins[b] .. bins[b+1])     */
+  const int32_t* tiles;      /* CSR: ds_csr_tiles plan (ntiles + 1 row starts), or NULL */
+  int64_t ntiles;
 } ds_matrix;
 
 /* Row-length bins for irregular CSR (rows stable-sorted by bin):
@@ -243,6 +245,14 @@ typedef struct ds_matrix {
  * are written to host memory (synchronises).                               */
 int ds_csr_bins(int64_t nrows, const int32_t* row_offsets, int32_t* perm, int64_t* bins,
                 void* stream);
+/* Entry tiles for irregular CSR: tiles[t] = first row of tile t (t <
+ * *ntiles), tiles[*ntiles] = nrows; a tile of rows <= 129 entries holds at
+ * most 2048 entries, every longer row is a tile of its own.  tiles needs
+ * nrows + 1 int32; *ntiles is written to host memory (synchronises).  With
+ * row_perm / bins set too, ds_spmv runs the tiles (entry-parallel products,
+ * row-parallel exact sums) and the long rows concurrently.                 */
+int ds_csr_tiles(int64_t nrows, const int32_t* row_offsets, int32_t* tiles, int64_t* ntiles,
+                 void* stream);
 
 int ds_spmv(const ds_matrix* a, const double* x, double* y, int accumulate, void* stream);
 

@@ -50,7 +50,7 @@ class DsMatrix(ctypes.Structure):
         ("nrows", c_i64), ("ncols", c_i64), ("nnz", c_i64),
         ("idx0", c_vp), ("idx1", c_vp), ("values", c_vp), ("long_rows", c_vp),
         ("n_long", c_i64), ("rows_sorted", c_i32), ("max_row_len", c_i32),
-        ("row_perm", c_vp), ("bins", c_i64 * 9),
+        ("row_perm", c_vp), ("bins", c_i64 * 9), ("tiles", c_vp), ("ntiles", c_i64),
     ]
 
 
@@ -96,6 +96,7 @@ _SIGNATURES = {
     "ds_spmv_coo_sorted": (c_int, [c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp,
                                    c_int, c_vp]),
     "ds_csr_bins": (c_int, [c_i64, c_vp, c_vp, P_i64, c_vp]),
+    "ds_csr_tiles": (c_int, [c_i64, c_vp, c_vp, P_i64, c_vp]),
     "ds_dot_workspace_bytes": (c_i64, []),
     "ds_dot": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "ds_waxpby": (c_int, [c_i64, c_dbl, c_vp, c_dbl, c_vp, c_vp, c_vp]),

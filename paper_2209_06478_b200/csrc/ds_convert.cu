@@ -751,6 +751,45 @@ __global__ void bin_scatter(int nrows, const int* __restrict__ off, int b, const
     if (csr_bin_of(off[r + 1] - off[r]) == b) perm[base + pos[r]] = r;
 }
 
+// ---------------------------------------------------------------- CSR tiles --
+__device__ __forceinline__ int csr_tile_head(int r, const int* __restrict__ off) {
+  if (r == 0) return 1;
+  const int a = off[r - 1], b = off[r], c = off[r + 1];
+  const bool long_here = c - b > 129, long_prev = b - a > 129;
+  return long_here || long_prev || (b / kCsrTileTarget != a / kCsrTileTarget);
+}
+struct TileHead {
+  const int* off;
+  __device__ int operator()(int64_t r) const { return csr_tile_head((int)r, off); }
+};
+__global__ void tile_scatter(int nrows, const int* __restrict__ off, const int* __restrict__ pos,
+                             int* tiles) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += gridDim.x * blockDim.x)
+    if (csr_tile_head(r, off)) tiles[pos[r]] = r;
+}
+__global__ void tile_close(int* tiles, int64_t ntiles, int nrows) { tiles[ntiles] = nrows; }
+
+extern "C" int ds_csr_tiles(int64_t nrows, const int32_t* row_offsets, int32_t* tiles,
+                            int64_t* ntiles, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  *ntiles = 0;
+  if (nrows <= 0) return DS_OK;
+  int* pos = nullptr;
+  DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&pos), nrows * sizeof(int), st));
+  int64_t nt = 0;
+  int rc = exclusive_scan(nrows, TileHead{row_offsets}, pos, &nt, st);
+  if (rc) {
+    cudaFreeAsync(pos, st);
+    return rc;
+  }
+  tile_scatter<<<grid1d(nrows), 256, 0, st>>>((int)nrows, row_offsets, pos, tiles);
+  tile_close<<<1, 1, 0, st>>>(tiles, nt, (int)nrows);
+  DS_LAUNCH_CHECK("tile_scatter");
+  DS_CUDA(cudaFreeAsync(pos, st));
+  *ntiles = nt;
+  return DS_OK;
+}
+
 extern "C" int ds_csr_bins(int64_t nrows, const int32_t* row_offsets, int32_t* perm, int64_t* bins,
                            void* stream) {
   cudaStream_t st = as_stream(stream);

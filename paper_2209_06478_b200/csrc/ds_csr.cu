@@ -1012,6 +1012,130 @@ int launch_csr_binned(int64_t nrows, int64_t ncols, int64_t nnz, const int* off,
   return DS_OK;
 }
 
+// ------------------------------------------------------- irregular: tiles --
+// csr_tile: entry-parallel products, row-parallel exact sums.  The rows are
+// cut into tiles of consecutive rows holding at most kCsrTileMax entries
+// (ds_csr_tiles; every row longer than kLongRow is a tile of its own and is
+// skipped here -- the long-row kernels take it on a side stream, concurrently).
+// Per tile every thread forms products of consecutive entries -- each warp
+// load instruction gathers 32 random x entries for 32 useful products, no
+// lane idles on a short row -- into shared memory; then one thread per row
+// sums its products in np.add.reduceat order (p[first] + pairwise(rest)).
+// x carries a persisting L2 window (it is gathered at random, ~13 times per
+// entry on the power-law matrix); the matrix streams with evict_first.
+constexpr int kTileThreads = 256;
+constexpr int kTileBatch = 8;   // entries in flight per thread
+
+template <bool ACCUM>
+__global__ void __launch_bounds__(kTileThreads, 4)
+    csr_tile_kernel(int64_t ntiles, const int* __restrict__ tiles, const int* __restrict__ off,
+                    const int* __restrict__ col, const double* __restrict__ val,
+                    const double* __restrict__ x, double* __restrict__ y, const int* guard) {
+  __shared__ double prod[kCsrTileMax];
+  if (guard && *guard) return;
+  const int tid = threadIdx.x;
+  const uint64_t pol = policy_evict_first();
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int r0 = __ldg(tiles + t), r1 = __ldg(tiles + t + 1);
+    const int e0 = __ldg(off + r0);
+    const int cnt = __ldg(off + r1) - e0;
+    if (r1 - r0 == 1 && cnt > kLongRow) continue;   // a long row: the long-row kernels own it
+    for (int k0 = 0; k0 < cnt; k0 += kTileThreads * kTileBatch) {
+      int c[kTileBatch];
+      double v[kTileBatch];
+#pragma unroll
+      for (int b = 0; b < kTileBatch; ++b) {
+        const int k = k0 + b * kTileThreads + tid;
+        const bool in = k < cnt;
+        c[b] = in ? ld_hint(col + e0 + k, pol) : 0;
+        v[b] = in ? ld_hint(val + e0 + k, pol) : 0.0;
+      }
+#pragma unroll
+      for (int b = 0; b < kTileBatch; ++b) {
+        const int k = k0 + b * kTileThreads + tid;
+        if (k < cnt) v[b] = mul(v[b], ld_gather(x + c[b]));
+      }
+#pragma unroll
+      for (int b = 0; b < kTileBatch; ++b) {
+        const int k = k0 + b * kTileThreads + tid;
+        if (k < cnt) prod[k] = v[b];
+      }
+    }
+    __syncthreads();
+    for (int r = r0 + tid; r < r1; r += kTileThreads) {
+      const int s = __ldg(off + r) - e0;
+      const int len = __ldg(off + r + 1) - e0 - s;
+      double sum;
+      if (len == 0) {
+        sum = 0.0;
+      } else {
+        const double* p = prod + s;
+        const int m = len - 1;   // addends after p[first] (m <= 128 inside a tile)
+        double res;
+        if (m < 8) {
+          res = -0.0;            // numpy >= 2 starts small pairwise blocks from -0.0
+          for (int i = 0; i < m; ++i) res = add(res, p[1 + i]);
+        } else {
+          double a[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) a[j] = p[1 + j];
+          const int full = m & ~7;
+          int i = 8;
+          for (; i < full; i += 8) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) a[j] = add(a[j], p[1 + i + j]);
+          }
+          res = add(add(add(a[0], a[1]), add(a[2], a[3])), add(add(a[4], a[5]), add(a[6], a[7])));
+          for (; i < m; ++i) res = add(res, p[1 + i]);
+        }
+        sum = add(p[0], res);
+      }
+      y[r] = ACCUM ? add(y[r], sum) : sum;
+    }
+    __syncthreads();
+  }
+}
+
+int launch_csr_tiles(int64_t nrows, int64_t ncols, const int* off, const int* col,
+                     const double* val, const int* tiles, int64_t ntiles, const int* perm,
+                     const int64_t* bins, const double* x, double* y, bool accum,
+                     const int* guard, cudaStream_t st) {
+  if (nrows == 0) return DS_OK;
+  const int64_t n_warp = bins[7] - bins[6], n_cta = bins[8] - bins[7];
+  const bool split = n_warp + n_cta > 0;
+  const bool win = x_window_begin(st, x, (size_t)ncols * 8);
+  cudaEvent_t joined = nullptr;
+  if (split) {   // rows > kLongRow on a side stream, launched first (fork / join)
+    cudaStream_t side;
+    cudaEvent_t fork;
+    int rc = aux_stream(&side, &fork, &joined);
+    if (rc) return rc;
+    DS_CUDA(cudaEventRecord(fork, st));
+    DS_CUDA(cudaStreamWaitEvent(side, fork, 0));
+    rc = launch_csr_long2(perm + bins[6], n_warp, perm + bins[7], n_cta, off, col, val, x, y,
+                          accum, guard, side);
+    if (rc) return rc;
+    DS_CUDA(cudaEventRecord(joined, side));
+  }
+  static int bps = -1;
+  if (bps < 0) {
+    const char* e = getenv("DS_CSR_TILE_CTAS");
+    bps = e ? atoi(e) : 4;
+  }
+  int64_t blocks = min64(ntiles, (int64_t)sm_count() * bps);
+  if (blocks < 1) blocks = 1;
+  if (accum)
+    csr_tile_kernel<true><<<(unsigned)blocks, kTileThreads, 0, st>>>(ntiles, tiles, off, col,
+                                                                      val, x, y, guard);
+  else
+    csr_tile_kernel<false><<<(unsigned)blocks, kTileThreads, 0, st>>>(ntiles, tiles, off, col,
+                                                                       val, x, y, guard);
+  DS_LAUNCH_CHECK("csr_tile_kernel");
+  if (split) DS_CUDA(cudaStreamWaitEvent(st, joined, 0));
+  if (win) x_window_end(st);
+  return DS_OK;
+}
+
 // A matrix without entries (e.g. the remote part of a partition without
 // ghosts): y = 0 (spmv) or y = y + 0.0 (spmv_add, kernels.py:196-198: the
 // +0.0 turns -0.0 into +0.0).  One streaming pass instead of a full SpMV

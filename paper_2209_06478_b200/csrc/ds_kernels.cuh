@@ -132,6 +132,12 @@ int launch_csr(int64_t nrows, int64_t nnz, const int* off, const int* col, const
                const int* long_rows, int64_t n_long, int max_len, const double* x, double* y,
                bool accum,
                const DotOut* dot, cudaStream_t st);
+// irregular CSR: entry-parallel tiles (ds_csr_tiles plan) + long rows (bins
+// 6 / 7 of the ds_csr_bins plan) concurrently on a side stream
+int launch_csr_tiles(int64_t nrows, int64_t ncols, const int* off, const int* col,
+                     const double* val, const int* tiles, int64_t ntiles, const int* perm,
+                     const int64_t* bins, const double* x, double* y, bool accum,
+                     const int* guard, cudaStream_t st);
 int launch_csr_binned(int64_t nrows, int64_t ncols, int64_t nnz, const int* off, const int* col,
                       const double* val, const int* perm, const int64_t* bins, const double* x,
                       double* y, bool accum, const DotOut* dot, cudaStream_t st);
@@ -153,5 +159,10 @@ constexpr int kMaxPartials = 1 << 16;
 // CSR long rows: 130..kCsrWarpRow entries -> warp per row, longer -> CTA per row
 constexpr int kCsrWarpRow = 1024;
 constexpr int kCsrBinCount = 8;   // ds_csr_bins: 8 bins, 9 offsets
+// ds_csr_tiles: a tile boundary where off[r] crosses a multiple of
+// kCsrTileTarget and around every row longer than 129 entries, so a tile of
+// short rows holds < kCsrTileTarget + 130 <= kCsrTileMax entries
+constexpr int kCsrTileMax = 2048;
+constexpr int kCsrTileTarget = kCsrTileMax - 130;
 
 }  // namespace ds

@@ -949,6 +949,11 @@ extern "C" int ds_cg_spmv_dot(const ds_matrix* a, const double* x, double* y, in
   bool done_dot = false;
   switch (a->format) {
     case DS_FMT_CSR: {
+      if (a->row_perm && a->tiles && !want_dot) {   // irregular: entry tiles + long rows
+        rc = launch_csr_tiles(a->nrows, a->ncols, a->idx0, a->idx1, a->values, a->tiles,
+                              a->ntiles, a->row_perm, a->bins, x, y, acc, d.guard, st);
+        break;
+      }
       if (a->row_perm) {  // irregular matrix: length-binned kernels
         const bool can_fuse = want_dot && a->bins[8] == a->bins[6];
         rc = launch_csr_binned(a->nrows, a->ncols, a->nnz, a->idx0, a->idx1, a->values, a->row_perm,

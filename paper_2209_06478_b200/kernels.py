@@ -125,7 +125,13 @@ def csr_plan(m: CsrMatrix):
             with torch.cuda.device(m.device):
                 _native.call("ds_csr_bins", m.nrows, D.ptr(m.row_offsets), D.ptr(perm), bins,
                              D.stream(m.device))
-            m._cache["bins"] = (k, perm, list(bins))
+            tiles = torch.empty(m.nrows + 1, dtype=torch.int32, device=m.device)
+            nt = ctypes.c_int64()
+            with torch.cuda.device(m.device):
+                _native.call("ds_csr_tiles", m.nrows, D.ptr(m.row_offsets), D.ptr(tiles),
+                             ctypes.byref(nt), D.stream(m.device))
+            m._cache["bins"] = (k, perm, list(bins), tiles[:int(nt.value) + 1].clone(),
+                                int(nt.value))
     m._cache["plan"] = (k, lr, nl)
     m._cache["max_len"] = (k, ml)
     return lr, nl
@@ -137,7 +143,7 @@ def csr_bins(m: CsrMatrix):
     hit = m._cache.get("bins")
     k = ("plan",) + _key(m.row_offsets)
     if hit is not None and hit[0] == k:
-        return hit[1], hit[2]
+        return hit[1:]
     return None
 
 
@@ -218,6 +224,8 @@ def descriptor(m) -> _native.DsMatrix:
             d.row_perm = b[0].data_ptr()
             for i in range(len(d.bins)):
                 d.bins[i] = b[1][i]
+            if os.environ.get("DS_CSR_TILES", "1") != "0":
+                d.tiles, d.ntiles = b[2].data_ptr(), b[3]
     elif isinstance(m, CooMatrix):
         d.format, d.nnz = int(FormatId.COO), m.nnz
         d.idx0, d.idx1, d.values = D.ptr(m.row_indices), D.ptr(m.col_indices), D.ptr(m.values)

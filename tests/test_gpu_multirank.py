@@ -127,13 +127,14 @@ def test_tuner_modes_agree_across_ranks(tmp_path):
     check_against_oracle(outs, oracle_dist(grid, procs))
 
 
-@pytest.mark.parametrize("procs", [(2, 1, 1), (2, 2, 2)])
-def test_nccl_rank_cg_matches_oracle(tmp_path, procs):
+@pytest.mark.timeout(420)
+def test_nccl_rank_cg_matches_oracle(tmp_path):
     """The NCCL transport (pack kernels + grouped send/recv + ncclAllGather)
-    at world 2 and 8.  On one GPU the ranks claim distinct NCCL host ids and
-    talk over NCCL's socket transport; on a node they use NVLink."""
-    grid = (8, 6, 6)
-    outs = run_ranks(tmp_path, grid, procs, transport="nccl", graph_steps=4, timeout=900)
+    at world 2.  On one GPU the ranks claim distinct NCCL host ids and talk
+    over NCCL's socket transport (slow: NCCL's kernels spin while the two
+    contexts time-slice); on a node they use NVLink."""
+    grid, procs = (6, 4, 4), (2, 1, 1)
+    outs = run_ranks(tmp_path, grid, procs, transport="nccl", timeout=400)
     check_against_oracle(outs, oracle_dist(grid, procs))
 
 

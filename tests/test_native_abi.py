@@ -46,7 +46,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_struct_layouts_match_header():
     from paper_2209_06478_b200 import _native
-    assert ctypes.sizeof(_native.DsMatrix) == 4 + 4 + 8 * 3 + 8 * 4 + 8 + 4 + 4 + 8 + 8 * 9
+    assert ctypes.sizeof(_native.DsMatrix) == 4 + 4 + 8 * 3 + 8 * 4 + 8 + 4 + 4 + 8 + 8 * 9 + 8 + 8
     assert ctypes.sizeof(_native.DsCgScalars) == 8 * 8 + 4 * 4 + 8 + 4 + 4
     assert ctypes.sizeof(_native.DsPcgScalars) == 8 * 8 + 4 * 4
     assert _native.CG_SCALARS_BYTES % 8 == 0
