@@ -359,6 +359,18 @@ int ds_cg_direction_gathered(int64_t n, const double* r, double* p, ds_cg_scalar
 int ds_cg_gather(int64_t count, const int32_t* idx, const double* src, double* dst,
                  const ds_cg_scalars* s, void* stream);
 
+/* ---- the solve loop on the device ---------------------------------------
+ * begin: a graph with one WHILE conditional node (condition default 1 at
+ * every launch) and `stream` capturing into its body; enqueue K iterations
+ * and ds_cg_while_continue (condition = s->done == 0) on `stream`; end:
+ * stop capturing, instantiate.  One ds_graph_exec_launch then iterates until
+ * convergence / breakdown / max_iters without host round trips.            */
+int ds_while_graph_begin(void* stream, void** graph, unsigned long long* handle);
+int ds_cg_while_continue(unsigned long long handle, const ds_cg_scalars* s, void* stream);
+int ds_while_graph_end(void* stream, void* graph, void** exec);
+int ds_graph_exec_launch(void* exec, void* stream);
+int ds_graph_destroy(void* graph, void* exec);
+
 /* ---- one partition per process: NCCL halo exchange + global dots --------
  * (stencil.py:280-295 / solver.py:140-141 across processes).  NCCL is
  * resolved at run time from the libnccl.so.2 already loaded in the process.

@@ -164,6 +164,11 @@ _SIGNATURES = {
     "ds_halo_exchange": (c_int, [c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                                  c_vp]),
     "ds_allgather_f64": (c_int, [c_vp, c_vp, c_i64, c_vp, c_vp]),
+    "ds_while_graph_begin": (c_int, [c_vp, ctypes.POINTER(c_vp), ctypes.POINTER(ctypes.c_ulonglong)]),
+    "ds_while_graph_end": (c_int, [c_vp, c_vp, ctypes.POINTER(c_vp)]),
+    "ds_cg_while_continue": (c_int, [ctypes.c_ulonglong, c_vp, c_vp]),
+    "ds_graph_exec_launch": (c_int, [c_vp, c_vp]),
+    "ds_graph_destroy": (c_int, [c_vp, c_vp]),
     "ds_radix_sort_pairs": (c_int, [c_vp, c_i64, c_int, c_vp, c_vp, c_vp]),
     "ds_ipc_handle_bytes": (c_int, []),
     "ds_ipc_export": (c_int, [c_vp, ctypes.c_char_p]),

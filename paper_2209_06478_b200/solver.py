@@ -241,6 +241,16 @@ class CgEngine:
                 return sc
             if use_graph is None:
                 use_graph = self.max_iters >= 16
+            if use_graph and _WHILE_STEPS > 0:
+                # the whole loop on the device: one graph launch, one readback
+                if getattr(self, "_while", None) is None:
+                    self._capture_while(_WHILE_STEPS)
+                if self._while:
+                    try:
+                        _native.check(self.lib.ds_graph_exec_launch(self._while[1], st))
+                        return self.scalars()
+                    finally:
+                        self.release_l2(st)
             c = chunk or (8 if use_graph else 4)
             if use_graph and self.graph is None:
                 self._capture(c)
@@ -265,6 +275,48 @@ class CgEngine:
             if sc.done:
                 return sc
             rounds = min(rounds * 2, _MAX_ROUNDS)
+
+    def _capture_while(self, k: int) -> None:
+        """Capture the solve loop as ONE graph: a WHILE conditional node whose
+        body is ``k`` iterations + the continue kernel (condition = not
+        done).  Sets self._while = (graph, exec, workspace) or False when the
+        driver refuses (the chunked replays are used then)."""
+        import torch
+        from . import _device
+        cap = torch.cuda.Stream(self.dev)
+        cap.wait_stream(torch.cuda.current_stream(self.dev))
+        ws = _device.new_workspace(self.dev)   # owned by this graph
+        torch.cuda.synchronize(self.dev)
+        saved, self.ws = self.ws, ws
+        if self.P == 1 and os.environ.get("DS_CG_L2_PERSIST", "1") != "0":
+            vb = self.parts[0].vec_block
+            self._l2_persist = self.lib.ds_l2_persist(vb.data_ptr(), vb.numel() * 8,
+                                                      cap.cuda_stream) == 0
+        g, h, ex = ctypes.c_void_p(), ctypes.c_ulonglong(), ctypes.c_void_p()
+        self._while = False
+        if self.lib.ds_while_graph_begin(cap.cuda_stream, ctypes.byref(g), ctypes.byref(h)):
+            self.ws = saved
+            return
+        rc = 0
+        try:
+            for _ in range(k):
+                self.step(cap.cuda_stream)
+            rc = self.lib.ds_cg_while_continue(h.value, self._p(self.scal), cap.cuda_stream)
+        finally:
+            rc = self.lib.ds_while_graph_end(cap.cuda_stream, g, ctypes.byref(ex)) or rc
+            self.ws = saved
+        if rc:
+            self.lib.ds_graph_destroy(g, ex)
+            return
+        self._while = (g.value, ex.value, ws)
+
+    def __del__(self):
+        w = getattr(self, "_while", None)
+        if w:
+            try:
+                self.lib.ds_graph_destroy(w[0], w[1])
+            except Exception:  # pragma: no cover - interpreter shutdown
+                pass
 
     def release_l2(self, stream) -> None:
         """Give the persisting-L2 carve-out back (set by _capture)."""
@@ -386,7 +438,9 @@ class CgEngine:
 # graph replays between two scalar readbacks at most (each replay = chunk
 # iterations): converged iterations still launch (as no-ops), so the cap
 # bounds that overshoot against the cost of a readback
-_MAX_ROUNDS = max(1, int(os.environ.get("DS_CG_MAX_ROUNDS", "4")))   # e2e solve: 4 -> 1068 vs 16 -> 994 GFLOP/s
+_MAX_ROUNDS = max(1, int(os.environ.get("DS_CG_MAX_ROUNDS", "4")))
+# iterations per body of the device-side WHILE loop (0: chunked replays)
+_WHILE_STEPS = max(0, int(os.environ.get("DS_CG_WHILE_STEPS", "2")))   # e2e solve: 4 -> 1068 vs 16 -> 994 GFLOP/s
 
 
 def _finish(engine: CgEngine, sc) -> tuple[int, np.ndarray, bool]:
