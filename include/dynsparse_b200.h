@@ -247,7 +247,7 @@ int ds_csr_bins(int64_t nrows, const int32_t* row_offsets, int32_t* perm, int64_
                 void* stream);
 /* Entry tiles for irregular CSR: tiles[t] = first row of tile t (t <
  * *ntiles), tiles[*ntiles] = nrows; a tile of rows <= 129 entries holds at
- * most 2048 entries, every longer row is a tile of its own.  tiles needs
+ * most 256 entries, every longer row is a tile of its own.  tiles needs
  * nrows + 1 int32; *ntiles is written to host memory (synchronises).  With
  * row_perm / bins set too, ds_spmv runs the tiles (entry-parallel products,
  * row-parallel exact sums) and the long rows concurrently.                 */

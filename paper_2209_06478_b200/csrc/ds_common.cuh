@@ -281,8 +281,11 @@ __device__ bool grid_sum_last_block(double block_partial, double* partials, unsi
   __threadfence();
   double v = 0.0;
   const int G = gridDim.x;
-  // fixed assignment: thread t sums partials t, t+BLOCK, ... sequentially
-  for (int i = threadIdx.x; i < G; i += BLOCK) v = add(v, *((volatile double*)&partials[i]));
+  // fixed assignment: thread t sums partials t, t+NT, ... sequentially, NT =
+  // the threads present (kernels whose tile size sets blockDim run with fewer
+  // than BLOCK: a BLOCK stride would skip partials NT..BLOCK-1 of each round)
+  const int NT = min(BLOCK, (int)blockDim.x);
+  for (int i = threadIdx.x; i < G; i += NT) v = add(v, *((volatile double*)&partials[i]));
   v = block_sum<BLOCK>(v, sh);
   if (threadIdx.x == 0) {
     *total = v;

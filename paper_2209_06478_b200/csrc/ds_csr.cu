@@ -1013,86 +1013,108 @@ int launch_csr_binned(int64_t nrows, int64_t ncols, int64_t nnz, const int* off,
 }
 
 // ------------------------------------------------------- irregular: tiles --
-// csr_tile: entry-parallel products, row-parallel exact sums.  The rows are
-// cut into tiles of consecutive rows holding at most kCsrTileMax entries
-// (ds_csr_tiles; every row longer than kLongRow is a tile of its own and is
-// skipped here -- the long-row kernels take it on a side stream, concurrently).
-// Per tile every thread forms products of consecutive entries -- each warp
-// load instruction gathers 32 random x entries for 32 useful products, no
-// lane idles on a short row -- into shared memory; then one thread per row
-// sums its products in np.add.reduceat order (p[first] + pairwise(rest)).
-// x carries a persisting L2 window (it is gathered at random, ~13 times per
-// entry on the power-law matrix); the matrix streams with evict_first.
-constexpr int kTileThreads = 256;
-constexpr int kTileBatch = 8;   // entries in flight per thread
+// csr_warp_tiles: entry-parallel products, row-parallel exact sums, one WARP
+// per tile.  The rows are cut into tiles of consecutive rows holding at most
+// kCsrTileMax = 256 entries (ds_csr_tiles; every row longer than kLongRow is
+// a tile of its own and is skipped here -- the long-row kernels take it on a
+// side stream, concurrently).  Per tile each lane forms the products of 8
+// entries (consecutive lanes, consecutive entries: every warp gather
+// instruction carries 32 useful random x loads, no lane idles on a short
+// row) into the warp's shared-memory slice; then one lane per row sums its
+// products in np.add.reduceat order (p[first] + pairwise(rest)).  Warps never
+// wait for each other (no block barrier), so ~48 independent warps per SM
+// keep the gather latency covered; the next tile's bounds are loaded before
+// the current tile's sums.  x carries a persisting L2 window (gathered ~13
+// times per entry at random on the power-law matrix); the matrix streams
+// with evict_first.
+constexpr int kTileWarps = 8;
+constexpr int kTilePer = kCsrTileMax / 32;   // entries per lane
 
 template <bool ACCUM>
-__global__ void __launch_bounds__(kTileThreads, 4)
+__global__ void __launch_bounds__(32 * kTileWarps, 6)
     csr_tile_kernel(int64_t ntiles, const int* __restrict__ tiles, const int* __restrict__ off,
                     const int* __restrict__ col, const double* __restrict__ val,
                     const double* __restrict__ x, double* __restrict__ y, const int* guard) {
-  __shared__ double prod[kCsrTileMax];
+  __shared__ double prod_all[kTileWarps][kCsrTileMax];
   if (guard && *guard) return;
-  const int tid = threadIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* prod = prod_all[warp];
   const uint64_t pol = policy_evict_first();
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const int r0 = __ldg(tiles + t), r1 = __ldg(tiles + t + 1);
-    const int e0 = __ldg(off + r0);
-    const int cnt = __ldg(off + r1) - e0;
-    if (r1 - r0 == 1 && cnt > kLongRow) continue;   // a long row: the long-row kernels own it
-    for (int k0 = 0; k0 < cnt; k0 += kTileThreads * kTileBatch) {
-      int c[kTileBatch];
-      double v[kTileBatch];
+  const int64_t nw = (int64_t)gridDim.x * kTileWarps;
+  int64_t t = (int64_t)blockIdx.x * kTileWarps + warp;
+  int r0 = 0, r1 = 0, e0 = 0, e1 = 0;
+  if (t < ntiles) {
+    r0 = __ldg(tiles + t);
+    r1 = __ldg(tiles + t + 1);
+    e0 = __ldg(off + r0);
+    e1 = __ldg(off + r1);
+  }
+  for (; t < ntiles; t += nw) {
+    const int cnt = e1 - e0;
+    const bool is_long = r1 - r0 == 1 && cnt > kLongRow;   // the long-row kernels own it
+    if (!is_long) {
+      int c[kTilePer];
+      double v[kTilePer];
 #pragma unroll
-      for (int b = 0; b < kTileBatch; ++b) {
-        const int k = k0 + b * kTileThreads + tid;
-        const bool in = k < cnt;
-        c[b] = in ? ld_hint(col + e0 + k, pol) : 0;
-        v[b] = in ? ld_hint(val + e0 + k, pol) : 0.0;
+      for (int j = 0; j < kTilePer; ++j) {
+        const int k = j * 32 + lane;
+        c[j] = k < cnt ? ld_hint(col + e0 + k, pol) : 0;
+        v[j] = k < cnt ? ld_hint(val + e0 + k, pol) : 0.0;
       }
 #pragma unroll
-      for (int b = 0; b < kTileBatch; ++b) {
-        const int k = k0 + b * kTileThreads + tid;
-        if (k < cnt) v[b] = mul(v[b], ld_gather(x + c[b]));
-      }
+      for (int j = 0; j < kTilePer; ++j)
+        if (j * 32 + lane < cnt) v[j] = mul(v[j], ld_gather(x + c[j]));
 #pragma unroll
-      for (int b = 0; b < kTileBatch; ++b) {
-        const int k = k0 + b * kTileThreads + tid;
-        if (k < cnt) prod[k] = v[b];
-      }
+      for (int j = 0; j < kTilePer; ++j)
+        if (j * 32 + lane < cnt) prod[j * 32 + lane] = v[j];
     }
-    __syncthreads();
-    for (int r = r0 + tid; r < r1; r += kTileThreads) {
-      const int s = __ldg(off + r) - e0;
-      const int len = __ldg(off + r + 1) - e0 - s;
-      double sum;
-      if (len == 0) {
-        sum = 0.0;
-      } else {
-        const double* p = prod + s;
-        const int m = len - 1;   // addends after p[first] (m <= 128 inside a tile)
-        double res;
-        if (m < 8) {
-          res = -0.0;            // numpy >= 2 starts small pairwise blocks from -0.0
-          for (int i = 0; i < m; ++i) res = add(res, p[1 + i]);
+    // the next tile's bounds, in flight during the sums
+    const int64_t tn = t + nw;
+    int n0 = 0, n1 = 0, f0 = 0, f1 = 0;
+    if (tn < ntiles) {
+      n0 = __ldg(tiles + tn);
+      n1 = __ldg(tiles + tn + 1);
+      f0 = __ldg(off + n0);
+      f1 = __ldg(off + n1);
+    }
+    __syncwarp();
+    if (!is_long) {
+      for (int r = r0 + lane; r < r1; r += 32) {
+        const int s = __ldg(off + r) - e0;
+        const int len = __ldg(off + r + 1) - e0 - s;
+        double sum;
+        if (len == 0) {
+          sum = 0.0;
         } else {
-          double a[8];
+          const double* p = prod + s;
+          const int m = len - 1;   // addends after p[first] (m <= 128 inside a tile)
+          double res;
+          if (m < 8) {
+            res = -0.0;            // numpy >= 2 starts small pairwise blocks from -0.0
+            for (int i = 0; i < m; ++i) res = add(res, p[1 + i]);
+          } else {
+            double a[8];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) a[j] = p[1 + j];
-          const int full = m & ~7;
-          int i = 8;
-          for (; i < full; i += 8) {
+            for (int j = 0; j < 8; ++j) a[j] = p[1 + j];
+            const int full = m & ~7;
+            int i = 8;
+            for (; i < full; i += 8) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) a[j] = add(a[j], p[1 + i + j]);
+              for (int j = 0; j < 8; ++j) a[j] = add(a[j], p[1 + i + j]);
+            }
+            res = add(add(add(a[0], a[1]), add(a[2], a[3])), add(add(a[4], a[5]), add(a[6], a[7])));
+            for (; i < m; ++i) res = add(res, p[1 + i]);
           }
-          res = add(add(add(a[0], a[1]), add(a[2], a[3])), add(add(a[4], a[5]), add(a[6], a[7])));
-          for (; i < m; ++i) res = add(res, p[1 + i]);
+          sum = add(p[0], res);
         }
-        sum = add(p[0], res);
+        y[r] = ACCUM ? add(y[r], sum) : sum;
       }
-      y[r] = ACCUM ? add(y[r], sum) : sum;
     }
-    __syncthreads();
+    __syncwarp();
+    r0 = n0;
+    r1 = n1;
+    e0 = f0;
+    e1 = f1;
   }
 }
 
@@ -1120,16 +1142,16 @@ int launch_csr_tiles(int64_t nrows, int64_t ncols, const int* off, const int* co
   static int bps = -1;
   if (bps < 0) {
     const char* e = getenv("DS_CSR_TILE_CTAS");
-    bps = e ? atoi(e) : 4;
+    bps = e ? atoi(e) : 6;
   }
-  int64_t blocks = min64(ntiles, (int64_t)sm_count() * bps);
+  int64_t blocks = min64(ceil_div(ntiles, kTileWarps), (int64_t)sm_count() * bps);
   if (blocks < 1) blocks = 1;
   if (accum)
-    csr_tile_kernel<true><<<(unsigned)blocks, kTileThreads, 0, st>>>(ntiles, tiles, off, col,
-                                                                      val, x, y, guard);
+    csr_tile_kernel<true><<<(unsigned)blocks, 32 * kTileWarps, 0, st>>>(ntiles, tiles, off, col,
+                                                                         val, x, y, guard);
   else
-    csr_tile_kernel<false><<<(unsigned)blocks, kTileThreads, 0, st>>>(ntiles, tiles, off, col,
-                                                                       val, x, y, guard);
+    csr_tile_kernel<false><<<(unsigned)blocks, 32 * kTileWarps, 0, st>>>(ntiles, tiles, off, col,
+                                                                          val, x, y, guard);
   DS_LAUNCH_CHECK("csr_tile_kernel");
   if (split) DS_CUDA(cudaStreamWaitEvent(st, joined, 0));
   if (win) x_window_end(st);

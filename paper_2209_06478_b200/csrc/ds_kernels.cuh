@@ -118,8 +118,9 @@ struct DotOut {
 template <int BLOCK>
 __device__ double reduce_partials(const double* partials, const unsigned* count, double* sh) {
   const int G = (int)*count;
+  const int NT = min(BLOCK, (int)blockDim.x);   // threads present (see grid_sum_last_block)
   double v = 0.0;
-  for (int i = threadIdx.x; i < G; i += BLOCK) v = add(v, partials[i]);
+  for (int i = threadIdx.x; i < G; i += NT) v = add(v, partials[i]);
   v = block_sum<BLOCK>(v, sh);
   __shared__ double s_tot;
   if (threadIdx.x == 0) s_tot = v;
@@ -161,8 +162,8 @@ constexpr int kCsrWarpRow = 1024;
 constexpr int kCsrBinCount = 8;   // ds_csr_bins: 8 bins, 9 offsets
 // ds_csr_tiles: a tile boundary where off[r] crosses a multiple of
 // kCsrTileTarget and around every row longer than 129 entries, so a tile of
-// short rows holds < kCsrTileTarget + 130 <= kCsrTileMax entries
-constexpr int kCsrTileMax = 2048;
+// short rows holds < kCsrTileTarget + 130 <= kCsrTileMax entries (one warp)
+constexpr int kCsrTileMax = 256;
 constexpr int kCsrTileTarget = kCsrTileMax - 130;
 
 }  // namespace ds

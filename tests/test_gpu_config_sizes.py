@@ -127,3 +127,28 @@ def test_192_cubed_conversions_and_spmv():
     c = ds.convert(a, F.COO)
     assert digest(host64(c.row_indices), host64(c.col_indices), host(c.values)) == \
         H["st192/convert_coo"]
+
+
+@pytest.mark.slow
+def test_single_controller_distributed_dia_48_matches_oracle():
+    """Four partitions of 48^3 in one process (CgEngine, P > 1: ticket-completed
+    partition dots fused into the DIA SpMV, whose CTAs have 128 threads and
+    whose grid exceeds 128 -- the shape that once dropped partials) against
+    the oracle's distributed CG (reference solver.py:120-189)."""
+    from oracle import dynsparse_oracle as O
+    spec = ds.GridSpec(48, 48, 48, 2, 2, 1)
+    prob = ds.generate_problem(spec, space=ds.MemorySpace.DEVICE, device=DEV)
+    splits = [ds.split_local_remote(prob, k) for k in range(prob.npartitions)]
+    for sp in splits:
+        ds.convert_inplace(sp.local, F.DIA)
+    res = ds.cg(ds.SERIAL, ds.DistributedOperator(prob, splits),
+                [p.b for p in prob.partitions], tol=1e-9)
+    parts = O.stencil_problem(48, 48, 48, 2, 2, 1)
+    ref = O.cg_dist(parts, [O.split(p) for p in parts], [p.b for p in parts], tol=1e-9,
+                    nthreads=8)
+    assert res.converged and abs(res.iterations - ref.iterations) <= 1
+    k = min(res.iterations, ref.iterations) + 1
+    h, rh = res.residual_history, ref.history
+    assert np.all(np.abs(h[:k] - rh[:k]) <= 1e-8 * rh[:k] + 1e-14)
+    for k_, xv in enumerate(res.x):
+        assert np.max(np.abs(host(xv.data) - ref.x[k_])) < 1e-8
