@@ -151,3 +151,11 @@ def test_peer_rank_cg_matches_reference_golden(tmp_path, procs):
         ref.x = [z[f"{key}/x{k}"] for k in range(procs[0] * procs[1] * procs[2])]
     outs = run_ranks(tmp_path, (16, 16, 16), procs, graph_steps=4)
     check_against_oracle(outs, ref)
+
+
+def test_peer_rank_cg_40_cubed_two_ranks(tmp_path):
+    """40^3 per rank: the DIA pipeline's grid exceeds 128 CTAs (the fused,
+    ticket-completed partition p.Ap must see every CTA's partial)."""
+    grid, procs = (40, 40, 40), (2, 1, 1)
+    outs = run_ranks(tmp_path, grid, procs, graph_steps=5)
+    check_against_oracle(outs, oracle_dist(grid, procs))
