@@ -56,6 +56,12 @@ int allow_dynamic_smem(const void* kernel, size_t bytes);
 int radix_sort_pairs(const unsigned long long* keys, const int* rows, const int* cols,
                      unsigned long long ncols, int64_t n, unsigned long long max_key,
                      unsigned long long* keys_out, int* perm_out, cudaStream_t st);
+// row-sorted input: sort inside each row (ds_sort.cu); tiles = a
+// tile_plan(off, 128, 128) plan; DS_ERR_NOT_SUPPORTED when a row is longer
+// than the shared-memory sort takes (nothing written; fall back to the radix)
+int segmented_sort_rows(const int* off, const int* rows, const int* cols,
+                        unsigned long long ncols, const int* tiles, int64_t ntiles,
+                        unsigned long long* keys_out, int* perm_out, cudaStream_t st);
 constexpr int kWarp = 32;
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }

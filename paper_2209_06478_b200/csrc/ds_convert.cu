@@ -420,7 +420,7 @@ struct ColVal {
 
 // *bad bits: kBadOrder (not canonical), kBadIndex (a column outside [0, ncols):
 // nothing is marked for it, the caller raises IndexOutOfRange)
-constexpr int kBadOrder = 1, kBadIndex = 2;
+constexpr int kBadOrder = 1, kBadIndex = 2, kBadRowOrder = 4;   // 4: rows decrease somewhere
 
 __global__ void csr_check_mark(int nrows, int ncols, const int* __restrict__ off,
                                const int* __restrict__ c, unsigned char* flags, int* bad) {
@@ -528,7 +528,8 @@ __global__ void coo_check_mark(int64_t nnz, int nrows, int ncols, const int* __r
     const int rk = __ldg(r + k), ck = __ldg(c + k);
     if (k > 0) {
       const int rp = __ldg(r + k - 1), cp = __ldg(c + k - 1);
-      if (rk < rp || (rk == rp && ck <= cp)) mybad |= kBadOrder;
+      if (rk < rp) mybad |= kBadOrder | kBadRowOrder;
+      else if (rk == rp && ck <= cp) mybad |= kBadOrder;
     }
     if ((unsigned)rk >= (unsigned)nrows || (unsigned)ck >= (unsigned)ncols) {
       mybad |= kBadIndex;
@@ -588,10 +589,14 @@ static int bits_for(unsigned long long maxkey) {
   return b < 1 ? 1 : b;
 }
 
+static int tile_plan(int64_t nrows, const int* off, int lng, int target, int* tiles,
+                     int64_t* ntiles, cudaStream_t st);
+
 // canonicalise raw (rows, cols, vals) into job->{r,c,v}.  Owned rows hang on
 // the job from the start, so every error return frees them with it.
+// row_off: the CSR source's offsets (rows then known to be sorted), or null.
 static int canonicalize(ds_convert_job* job, int64_t nnz, const int* rows, const int* cols,
-                        const double* vals, bool rows_owned) {
+                        const double* vals, bool rows_owned, const int* row_off = nullptr) {
   cudaStream_t st = job->st;
   if (rows_owned) {
     job->r = const_cast<int*>(rows);
@@ -631,17 +636,46 @@ static int canonicalize(ds_convert_job* job, int64_t nnz, const int* rows, const
     job->v = const_cast<double*>(vals);
     return DS_OK;
   }
-  // stable radix sort of (row*ncols + col) keys with the entry index
-  // (np.lexsort((cols, rows)) is stable, datamove.py:212); ds_sort.cu builds
-  // the keys from the index arrays in its first pass
+  // the stable (row, col) sort (np.lexsort((cols, rows)) is stable,
+  // datamove.py:212): rows already non-decreasing -> a sort inside each row
+  // (ds_sort.cu segmented_sort_rows); otherwise the onesweep LSD radix sort,
+  // which builds the keys from the index arrays in its first pass
   unsigned long long* keys_s = nullptr;
   int *perm = nullptr, *pos = nullptr;
   DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&keys_s), nnz * 8, st));
   DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&perm), nnz * 4, st));
-  const unsigned long long maxkey =
-      (unsigned long long)(job->nrows > 0 ? job->nrows : 1) * (unsigned long long)(job->ncols > 0 ? job->ncols : 1) - 1ull;
-  rc = radix_sort_pairs(nullptr, rows, cols, (unsigned long long)job->ncols, nnz, maxkey, keys_s,
-                        perm, st);
+  rc = DS_ERR_NOT_SUPPORTED;
+  static int no_seg = -1;
+  if (no_seg < 0) no_seg = getenv("DS_SORT_NO_SEGMENTED") ? 1 : 0;
+  if (!(bad & kBadRowOrder) && !no_seg) {
+    int *off = nullptr, *tiles = nullptr;
+    DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tiles), (job->nrows + 1) * 4, st));
+    if (!row_off) {
+      DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&off), (job->nrows + 1) * 4, st));
+      rows_to_offsets<<<grid1d(nnz + 1 > job->nrows + 1 ? nnz + 1 : job->nrows + 1), 256, 0, st>>>(
+          nnz, (int)job->nrows, rows, off);
+      row_off = off;
+    }
+    int64_t nt = 0;
+    rc = tile_plan(job->nrows, row_off, 128, 128, tiles, &nt, st);
+    if (!rc)
+      rc = segmented_sort_rows(row_off, rows, cols, (unsigned long long)job->ncols, tiles, nt,
+                               keys_s, perm, st);
+    cudaFreeAsync(tiles, st);
+    if (off) cudaFreeAsync(off, st);
+    if (rc && rc != DS_ERR_NOT_SUPPORTED) {
+      cudaFreeAsync(keys_s, st);
+      cudaFreeAsync(perm, st);
+      return rc;
+    }
+  }
+  if (rc == DS_ERR_NOT_SUPPORTED) {
+    const unsigned long long maxkey = (unsigned long long)(job->nrows > 0 ? job->nrows : 1) *
+                                          (unsigned long long)(job->ncols > 0 ? job->ncols : 1) -
+                                      1ull;
+    rc = radix_sort_pairs(nullptr, rows, cols, (unsigned long long)job->ncols, nnz, maxkey,
+                          keys_s, perm, st);
+  }
   if (rc) {
     cudaFreeAsync(keys_s, st);
     cudaFreeAsync(perm, st);
@@ -752,42 +786,51 @@ __global__ void bin_scatter(int nrows, const int* __restrict__ off, int b, const
 }
 
 // ---------------------------------------------------------------- CSR tiles --
-__device__ __forceinline__ int csr_tile_head(int r, const int* __restrict__ off) {
+namespace ds {
+// A tile starts at row 0, at every row longer than `lng` entries, right after
+// one, and where off[r] crosses a multiple of `target`: a tile of rows of at
+// most `lng` entries then holds fewer than target + lng entries.
+__device__ __forceinline__ int tile_head(int r, const int* __restrict__ off, int lng, int target) {
   if (r == 0) return 1;
   const int a = off[r - 1], b = off[r], c = off[r + 1];
-  const bool long_here = c - b > 129, long_prev = b - a > 129;
-  return long_here || long_prev || (b / kCsrTileTarget != a / kCsrTileTarget);
+  return c - b > lng || b - a > lng || (b / target != a / target);
 }
 struct TileHead {
   const int* off;
-  __device__ int operator()(int64_t r) const { return csr_tile_head((int)r, off); }
+  int lng, target;
+  __device__ int operator()(int64_t r) const { return tile_head((int)r, off, lng, target); }
 };
-__global__ void tile_scatter(int nrows, const int* __restrict__ off, const int* __restrict__ pos,
-                             int* tiles) {
+__global__ void tile_scatter(int nrows, const int* __restrict__ off, int lng, int target,
+                             const int* __restrict__ pos, int* tiles) {
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += gridDim.x * blockDim.x)
-    if (csr_tile_head(r, off)) tiles[pos[r]] = r;
+    if (tile_head(r, off, lng, target)) tiles[pos[r]] = r;
 }
 __global__ void tile_close(int* tiles, int64_t ntiles, int nrows) { tiles[ntiles] = nrows; }
 
-extern "C" int ds_csr_tiles(int64_t nrows, const int32_t* row_offsets, int32_t* tiles,
-                            int64_t* ntiles, void* stream) {
-  cudaStream_t st = as_stream(stream);
+static int tile_plan(int64_t nrows, const int* off, int lng, int target, int* tiles,
+                     int64_t* ntiles, cudaStream_t st) {
   *ntiles = 0;
   if (nrows <= 0) return DS_OK;
   int* pos = nullptr;
   DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&pos), nrows * sizeof(int), st));
   int64_t nt = 0;
-  int rc = exclusive_scan(nrows, TileHead{row_offsets}, pos, &nt, st);
+  int rc = exclusive_scan(nrows, TileHead{off, lng, target}, pos, &nt, st);
   if (rc) {
     cudaFreeAsync(pos, st);
     return rc;
   }
-  tile_scatter<<<grid1d(nrows), 256, 0, st>>>((int)nrows, row_offsets, pos, tiles);
+  tile_scatter<<<grid1d(nrows), 256, 0, st>>>((int)nrows, off, lng, target, pos, tiles);
   tile_close<<<1, 1, 0, st>>>(tiles, nt, (int)nrows);
   DS_LAUNCH_CHECK("tile_scatter");
   DS_CUDA(cudaFreeAsync(pos, st));
   *ntiles = nt;
   return DS_OK;
+}
+}  // namespace ds
+
+extern "C" int ds_csr_tiles(int64_t nrows, const int32_t* row_offsets, int32_t* tiles,
+                            int64_t* ntiles, void* stream) {
+  return tile_plan(nrows, row_offsets, 129, kCsrTileTarget, tiles, ntiles, as_stream(stream));
 }
 
 extern "C" int ds_csr_bins(int64_t nrows, const int32_t* row_offsets, int32_t* perm, int64_t* bins,
@@ -1148,7 +1191,7 @@ static int begin_csr_impl(ds_convert_job* j, int64_t nnz, const int32_t* row_off
     csr_expand_rows<<<grid1d(nrows * 8), 256, 0, st>>>((int)nrows, row_offsets, rows);
     DS_LAUNCH_CHECK("csr_expand_rows");
   }
-  int rc = canonicalize(j, nnz, rows, cols, values, true);
+  int rc = canonicalize(j, nnz, rows, cols, values, true, row_offsets);
   if (rc) return rc;
   return size_target(j, fill_limit, out_nnz, out_ndiags);
 }

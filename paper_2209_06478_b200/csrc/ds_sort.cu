@@ -278,6 +278,173 @@ int radix_sort_pairs(const u64* keys, const int* rows, const int* cols, u64 ncol
   return rc;
 }
 
+// ------------------------------------------------------ row-sorted input --
+// When the rows are already non-decreasing (a CSR source; a COO built row by
+// row, like the power-law matrix) the stable (row, col) sort is a sort INSIDE
+// each row: one read and one write of the entries instead of 8-bit LSD
+// passes over row AND column bits.  Rows are cut into warp tiles of at most
+// kSegTile entries (rows of up to kSegShort entries, grouped); a warp sorts
+// its tile in shared memory with a bitonic network over unique composite keys
+// (local row | column | local index -- unique, so the unstable network
+// yields the stable order).  Longer rows (up to kSegLong) are sorted one per
+// CTA the same way with (column | local index) keys.
+constexpr int kSegShort = 128;          // rows up to this many entries share warp tiles
+constexpr int kSegTile = 2 * kSegShort; // entries per warp tile (< kSegShort + 129)
+constexpr int kSegLong = 16384;         // longest row the CTA kernel sorts in shared memory
+constexpr int kSegWarps = 8;
+
+__device__ __forceinline__ void bitonic_warp(u64* s, int n2) {
+  const int lane = threadIdx.x & 31;
+  for (int k = 2; k <= n2; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = lane; t < (n2 >> 1); t += 32) {
+        const int i = ((t & ~(j - 1)) << 1) | (t & (j - 1));
+        const u64 a = s[i], b = s[i + j];
+        if ((a > b) == ((i & k) == 0)) {
+          s[i] = b;
+          s[i + j] = a;
+        }
+      }
+      __syncwarp();
+    }
+}
+
+__global__ void __launch_bounds__(32 * kSegWarps)
+    seg_sort_tiles(int64_t ntiles, const int* __restrict__ tiles, const int* __restrict__ off,
+                   const int* __restrict__ rows, const int* __restrict__ cols, u64 ncols,
+                   u64* __restrict__ keys_out, int* __restrict__ perm_out) {
+  __shared__ u64 sk_all[kSegWarps][kSegTile];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  u64* sk = sk_all[warp];
+  for (int64_t t = (int64_t)blockIdx.x * kSegWarps + warp; t < ntiles;
+       t += (int64_t)gridDim.x * kSegWarps) {
+    const int r0 = __ldg(tiles + t), r1 = __ldg(tiles + t + 1);
+    const int e0 = __ldg(off + r0), cnt = __ldg(off + r1) - e0;
+    if (r1 - r0 == 1 && cnt > kSegShort) continue;   // a long row: the CTA kernel sorts it
+    if (cnt <= 1) {                                  // nothing to sort
+      if (lane < cnt) {
+        keys_out[e0] = (u64)(unsigned)r0 * ncols + (u64)(unsigned)__ldg(cols + e0);
+        perm_out[e0] = e0;
+      }
+      continue;
+    }
+    int n2 = 32;
+    while (n2 < cnt) n2 <<= 1;
+    for (int k = lane; k < n2; k += 32) {
+      u64 key = ~0ull;
+      if (k < cnt) {
+        const u64 lr = (u64)(unsigned)(__ldg(rows + e0 + k) - r0);
+        key = (lr << 40) | ((u64)(unsigned)__ldg(cols + e0 + k) << 8) | (u64)k;
+      }
+      sk[k] = key;
+    }
+    __syncwarp();
+    bitonic_warp(sk, n2);
+    for (int k = lane; k < cnt; k += 32) {
+      const u64 key = sk[k];
+      const u64 r = (u64)(unsigned)r0 + (key >> 40);
+      keys_out[e0 + k] = r * ncols + ((key >> 8) & 0xffffffffull);
+      perm_out[e0 + k] = e0 + (int)(key & 255);
+    }
+    __syncwarp();
+  }
+}
+
+// one CTA per long row: bitonic sort of (column << 32 | local index) in
+// shared memory (next power of two of the row length, padded with ~0)
+__global__ void __launch_bounds__(512)
+    seg_sort_long(const int* __restrict__ long_rows, const int* __restrict__ off,
+                  const int* __restrict__ cols, u64 ncols, u64* __restrict__ keys_out,
+                  int* __restrict__ perm_out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  u64* sk = reinterpret_cast<u64*>(smem_raw);
+  const int r = __ldg(long_rows + blockIdx.x);
+  const int e0 = __ldg(off + r), len = __ldg(off + r + 1) - e0;
+  int n2 = 1;
+  while (n2 < len) n2 <<= 1;
+  for (int k = threadIdx.x; k < n2; k += blockDim.x)
+    sk[k] = k < len ? (((u64)(unsigned)__ldg(cols + e0 + k) << 32) | (u64)k) : ~0ull;
+  __syncthreads();
+  for (int k = 2; k <= n2; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = threadIdx.x; t < (n2 >> 1); t += blockDim.x) {
+        const int i = ((t & ~(j - 1)) << 1) | (t & (j - 1));
+        const u64 a = sk[i], b = sk[i + j];
+        if ((a > b) == ((i & k) == 0)) {
+          sk[i] = b;
+          sk[i + j] = a;
+        }
+      }
+      __syncthreads();
+    }
+  const u64 rb = (u64)(unsigned)r * ncols;
+  for (int k = threadIdx.x; k < len; k += blockDim.x) {
+    const u64 key = sk[k];
+    keys_out[e0 + k] = rb + (key >> 32);
+    perm_out[e0 + k] = e0 + (int)(key & 0xffffffffull);
+  }
+}
+
+// the long rows of a tile plan (tiles of one row with more than kSegShort entries)
+__global__ void seg_collect_long(int64_t ntiles, const int* __restrict__ tiles,
+                                 const int* __restrict__ off, int* long_rows, int* count,
+                                 int* max_len) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ntiles;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int r0 = tiles[t], r1 = tiles[t + 1];
+    const int len = off[r1] - off[r0];
+    if (r1 - r0 == 1 && len > kSegShort) {
+      long_rows[atomicAdd(count, 1)] = r0;
+      atomicMax(max_len, len);
+    }
+  }
+}
+
+int segmented_sort_rows(const int* off, const int* rows, const int* cols, u64 ncols,
+                        const int* tiles, int64_t ntiles, u64* keys_out, int* perm_out,
+                        cudaStream_t st) {
+  if (ntiles <= 0) return DS_OK;
+  int* scratch = nullptr;   // [count, max_len, long rows ...]
+  DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scratch), (ntiles + 2) * sizeof(int), st));
+  int rc = DS_OK;
+  do {
+    if (cudaMemsetAsync(scratch, 0, 2 * sizeof(int), st) != cudaSuccess) {
+      rc = cuda_fail(cudaGetLastError(), "segmented sort scratch");
+      break;
+    }
+    const unsigned g = (unsigned)std::max<int64_t>(1, min64(ceil_div(ntiles, 256),
+                                                              (int64_t)sm_count() * 4));
+    seg_collect_long<<<g, 256, 0, st>>>(ntiles, tiles, off, scratch + 2, scratch, scratch + 1);
+    int h[2] = {0, 0};
+    if (cudaMemcpyAsync(h, scratch, sizeof(h), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess) {
+      rc = cuda_fail(cudaGetLastError(), "segmented sort plan");
+      break;
+    }
+    if (h[1] > kSegLong) {   // a row too long for shared memory: the caller falls back
+      set_error("row of %d entries exceeds the segmented sort's %d", h[1], kSegLong);
+      rc = DS_ERR_NOT_SUPPORTED;
+      break;
+    }
+    if (h[0] > 0) {
+      int n2 = 1;
+      while (n2 < h[1]) n2 <<= 1;
+      const size_t smem = (size_t)n2 * sizeof(u64);
+      if ((rc = allow_dynamic_smem((const void*)seg_sort_long, smem))) break;
+      seg_sort_long<<<(unsigned)h[0], 512, smem, st>>>(scratch + 2, off, cols, ncols, keys_out,
+                                                       perm_out);
+    }
+    const unsigned gt = (unsigned)std::max<int64_t>(
+        1, min64(ceil_div(ntiles, kSegWarps), (int64_t)sm_count() * 8));
+    seg_sort_tiles<<<gt, 32 * kSegWarps, 0, st>>>(ntiles, tiles, off, rows, cols, ncols, keys_out,
+                                                  perm_out);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) rc = cuda_fail(e, "segmented sort");
+  } while (false);
+  cudaFreeAsync(scratch, st);
+  return rc;
+}
+
 }  // namespace ds
 
 using namespace ds;

@@ -256,3 +256,54 @@ def test_dia_source_unsorted_or_repeated_offsets(kind):
     for tgt, fid in ((O.CSR, ds.FormatId.CSR), (O.COO, ds.FormatId.COO),
                      (O.DIA, ds.FormatId.DIA)):
         assert_same(ds.convert(src, fid), O.convert(ora, tgt), (kind, fid))
+
+
+def _row_sorted_coo(rng, nrows, ncols, lengths, dup_frac=0.1):
+    rows = np.repeat(np.arange(nrows, dtype=np.int64), lengths)
+    cols = rng.integers(0, ncols, rows.size)
+    dup = rng.random(rows.size) < dup_frac           # duplicates inside rows
+    if rows.size > 1:
+        src = np.maximum(np.arange(rows.size) - 1, 0)
+        same = dup & (rows == rows[src])
+        cols[same] = cols[src[same]]
+    vals = rng.standard_normal(rows.size)
+    vals[rng.random(rows.size) < 0.02] = -0.0
+    return rows, cols, vals
+
+
+@pytest.mark.parametrize("case", ["short", "mixed", "long", "too_long", "empty_rows"])
+def test_row_sorted_coo_segmented_sort(case):
+    """Row-sorted COO with unsorted columns and duplicates takes the sort
+    inside each row (warp tiles <= 128-entry rows, one CTA per longer row up
+    to 16384; a longer row falls back to the LSD radix sort): canonical COO,
+    CSR and the duplicate sums bitwise equal to the oracle (datamove.py:208-243)."""
+    rng = np.random.default_rng({"short": 1, "mixed": 2, "long": 3, "too_long": 4,
+                                 "empty_rows": 5}[case])
+    nrows, ncols = 3000, 50_000
+    if case == "short":
+        lengths = rng.integers(0, 20, nrows)
+    elif case == "mixed":
+        lengths = np.minimum(nrows, np.floor(6.0 * (1 - rng.random(nrows)) ** (-1 / 1.8))).astype(int)
+    elif case == "long":
+        lengths = rng.integers(0, 8, nrows)
+        lengths[[5, 700, 2999]] = [129, 2049, 16384]
+    elif case == "too_long":
+        lengths = rng.integers(0, 8, nrows)
+        lengths[17] = 20_000
+    else:
+        lengths = np.where(rng.random(nrows) < 0.9, 0, rng.integers(1, 300, nrows))
+    rows, cols, vals = _row_sorted_coo(rng, nrows, ncols, lengths)
+    coo = ds.CooMatrix(nrows, ncols, rows, cols, vals, ds.MemorySpace.DEVICE, DEV)
+    src = O.coo(nrows, ncols, rows, cols, vals)
+    for target, name in ((ds.FormatId.COO, "coo"), (ds.FormatId.CSR, "csr")):
+        got = ds.convert(coo, target)
+        want = O.convert(src, O.COO if name == "coo" else O.CSR)
+        assert_same(got, want, f"{case} -> {name}")
+    # a CSR source with unsorted columns / duplicates: same path via its offsets
+    off = np.zeros(nrows + 1, np.int64)
+    np.cumsum(lengths, out=off[1:])
+    csr = ds.CsrMatrix(nrows, ncols, torch.from_numpy(off.astype(np.int32)).to(DEV),
+                       torch.from_numpy(cols.astype(np.int32)).to(DEV),
+                       torch.from_numpy(vals).to(DEV), ds.MemorySpace.DEVICE)
+    assert_same(ds.convert(csr, ds.FormatId.CSR),
+                O.convert(O.csr(nrows, ncols, off, cols, vals), O.CSR), f"{case} csr src")
