@@ -163,6 +163,16 @@ int ds_dia_count_nonzero(int64_t nrows, int64_t ncols, int32_t ndiags, const int
  * summed like duplicate COO entries (datamove.py:208-235).                 */
 #define DS_FILL_LIMIT_DEFAULT ((int64_t)(-9223372036854775807LL - 1))
 typedef struct ds_convert_job ds_convert_job;
+/* DIA source with strictly ascending offsets (1 <= ndiags <= 32) -> CSR or
+ * COO in ONE pass over the slab (the canonical order is the row-major slot
+ * order filtered by "column in range and value != 0", formats.py:439-479):
+ * the caller sizes cols / vals by the in-range slot count (an upper bound of
+ * the nonzeros) and row_idx by nrows + 1 (CSR offsets) or that count (COO
+ * rows); *nnz receives the entries written (synchronises).  Other sources
+ * take ds_convert_begin_dia.                                                */
+int ds_dia_to_entries(int64_t nrows, int64_t ncols, int32_t ndiags, const int32_t* offsets,
+                      const double* values, int target, int32_t* row_idx, int32_t* cols,
+                      double* vals, int64_t* nnz, void* stream);
 /* The canonicalisation's stable sort, exposed for tests: keys_in[0..n) <
  * 2^bits sorted ascending into keys_out, perm_out[i] = the input position of
  * keys_out[i]; equal keys keep their input order (np.lexsort's stability,

@@ -169,6 +169,8 @@ _SIGNATURES = {
     "ds_cg_while_continue": (c_int, [ctypes.c_ulonglong, c_vp, c_vp]),
     "ds_graph_exec_launch": (c_int, [c_vp, c_vp]),
     "ds_graph_destroy": (c_int, [c_vp, c_vp]),
+    "ds_dia_to_entries": (c_int, [c_i64, c_i64, c_i32, c_vp, c_vp, c_int, c_vp, c_vp, c_vp, P_i64,
+                                  c_vp]),
     "ds_radix_sort_pairs": (c_int, [c_vp, c_i64, c_int, c_vp, c_vp, c_vp]),
     "ds_ipc_handle_bytes": (c_int, []),
     "ds_ipc_export": (c_int, [c_vp, ctypes.c_char_p]),

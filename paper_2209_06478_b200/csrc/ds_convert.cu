@@ -267,6 +267,122 @@ struct DiaSlots {
   }
 };
 
+// DIA source -> CSR / COO in ONE pass (ascending offsets, nd <= 32): a warp
+// takes the next group of kDiaGroupRows rows (atomic ticket, so every earlier
+// group is already resident), keeps the group's 32*nd slots in registers (nd
+// per lane), counts the valid ones, publishes the count and sums its
+// predecessors' counts by a warp-parallel decoupled look-back, then emits
+// straight from the registers -- the slab is read once (the two-pass walk
+// reads it twice).  The caller sizes the outputs by the in-range slot count.
+constexpr int kDiaOneMaxNd = 32;
+constexpr unsigned long long kGrpAgg = 1ull << 62, kGrpIncl = 2ull << 62,
+                             kGrpMask = (1ull << 62) - 1;
+
+__global__ void __launch_bounds__(128)
+    dia_emit_onepass(int64_t nrows, int ncols, int nd, const int* __restrict__ off,
+                     const double* __restrict__ vals, int64_t ngroups,
+                     unsigned long long* status, int* ticket, int* row_off, int* r, int* c,
+                     double* v, long long* total) {
+  __shared__ int s_off[kDiaOneMaxNd];
+  for (int j = threadIdx.x; j < nd; j += blockDim.x) s_off[j] = __ldg(off + j);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const int qq = 32 / nd, rmd = 32 % nd;
+  while (true) {
+    int g32 = 0;
+    if (lane == 0) g32 = atomicAdd(ticket, 1);
+    const int64_t g = __shfl_sync(0xffffffffu, g32, 0);
+    if (g >= ngroups) break;
+    const int64_t r0 = g * kDiaGroupRows;
+    const int64_t r1 = min64(r0 + kDiaGroupRows, nrows);
+    const int64_t eb = r0 * nd, ee = r1 * nd;
+    double x[kDiaOneMaxNd];
+    unsigned valid = 0;
+#pragma unroll
+    for (int q = 0; q < kDiaOneMaxNd; ++q) {
+      const int64_t e = eb + q * 32 + lane;
+      x[q] = (q < nd && e < ee) ? __ldg(vals + e) : 0.0;
+    }
+    int cnt = 0;
+    {
+      int64_t i = r0 + lane / nd;
+      int j = lane % nd;
+#pragma unroll
+      for (int q = 0; q < kDiaOneMaxNd; ++q) {
+        if (q < nd) {
+          const int64_t e = eb + q * 32 + lane;
+          const int64_t col = i + s_off[j];
+          const bool ok = e < ee && col >= 0 && col < ncols && x[q] != 0.0;
+          valid |= (unsigned)ok << q;
+          cnt += __popc(__ballot_sync(0xffffffffu, ok));
+          i += qq;
+          j += rmd;
+          if (j >= nd) {
+            j -= nd;
+            ++i;
+          }
+        }
+      }
+    }
+    // publish, then the warp-parallel look-back over 32 predecessors at a time
+    unsigned long long* mine = status + g;
+    if (lane == 0)
+      asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(mine),
+                   "l"((g == 0 ? kGrpIncl : kGrpAgg) | (unsigned long long)cnt) : "memory");
+    long long excl = 0;
+    for (int64_t p = g - 1; p >= 0; p -= 32) {
+      const int64_t pl = p - lane;
+      unsigned long long w = 0;
+      if (pl >= 0) {
+        do {
+          asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(status + pl) : "memory");
+        } while ((w >> 62) == 0);
+      }
+      const unsigned incl = __ballot_sync(0xffffffffu, pl >= 0 && (w >> 62) == 2);
+      const int stop = incl ? __ffs(incl) - 1 : 31;
+      long long val = (pl >= 0 && lane <= stop) ? (long long)(w & kGrpMask) : 0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+      excl += val;
+      if (incl) break;
+    }
+    if (lane == 0 && g > 0)
+      asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(mine),
+                   "l"(kGrpIncl | (unsigned long long)(excl + cnt)) : "memory");
+    // emit from registers
+    long long base = excl;
+    int64_t i = r0 + lane / nd;
+    int j = lane % nd;
+#pragma unroll
+    for (int q = 0; q < kDiaOneMaxNd; ++q) {
+      if (q < nd) {
+        const int64_t e = eb + q * 32 + lane;
+        const bool ok = (valid >> q) & 1u;
+        const unsigned m = __ballot_sync(0xffffffffu, ok);
+        const long long pos = base + __popc(m & lt);
+        if (row_off && e < ee && j == 0) row_off[i] = (int)pos;
+        if (ok) {
+          if (r) r[pos] = (int)i;
+          c[pos] = (int)(i + s_off[j]);
+          v[pos] = x[q];
+        }
+        base += __popc(m);
+        i += qq;
+        j += rmd;
+        if (j >= nd) {
+          j -= nd;
+          ++i;
+        }
+      }
+    }
+    if (g == ngroups - 1 && lane == 0) {
+      if (row_off) row_off[nrows] = (int)(excl + cnt);
+      *total = excl + cnt;
+    }
+  }
+}
+
 // DIA -> DIA: the target keeps the source diagonals that hold an entry
 // (jsrc[t] = source column of target diagonal t); a slot keeps its value iff
 // it is in range and nonzero (-0.0 and padding become +0.0, exactly as the
@@ -499,6 +615,108 @@ __global__ void dia_fill_csr(int nrows, int nd, int R, const int* __restrict__ o
     for (int t = threadIdx.x; t < total; t += blockDim.x) out[t] = slab[t];
     __syncthreads();
     ot = ot_next;
+  }
+}
+
+// ------------------------------------------------- CSR tiles with row ids --
+// Entry-parallel walks of a CSR source: a CTA takes kRT consecutive rows and
+// scatters each row's tile-local id over the tile's entries in shared memory
+// (one thread per row; chunks of kRtCap entries when the rows are long), then
+// every thread reads consecutive entries -- coalesced loads, no per-entry
+// search of the offsets (the warp walks above spend their issue slots on it).
+constexpr int kRT = 128;
+constexpr int kRtCap = 4096;
+
+struct RowIds {
+  int off[kRT + 1];
+  unsigned char rid[kRtCap];
+};
+
+// body(kb, k0, kend, ids): entries kb + threadIdx.x of the chunk [k0, kend);
+// the trip count is uniform across the block (lanes past kend see k >= kend)
+template <class Body>
+__device__ __forceinline__ void csr_rowid_tile(int nrows, const int* __restrict__ off, int r0,
+                                               RowIds& ids, Body&& body) {
+  const int nr = min(kRT, nrows - r0);
+  for (int t = threadIdx.x; t <= nr; t += blockDim.x) ids.off[t] = __ldg(off + r0 + t);
+  __syncthreads();
+  const int e0 = ids.off[0], e1 = ids.off[nr];
+  for (int k0 = e0; k0 < e1; k0 += kRtCap) {
+    const int kend = min(k0 + kRtCap, e1);
+    for (int t = threadIdx.x; t < nr; t += blockDim.x) {
+      const int lo = max(ids.off[t], k0), hi = min(ids.off[t + 1], kend);
+      for (int k = lo; k < hi; ++k) ids.rid[k - k0] = (unsigned char)t;
+    }
+    __syncthreads();
+    for (int kb = k0; kb < kend; kb += blockDim.x) body(kb, k0, kend);
+    __syncthreads();
+  }
+}
+
+// order check ((row, col) strictly increasing inside every row), index range
+// and the diagonal census of a CSR source
+__global__ void __launch_bounds__(256)
+    csr_census_tiles(int nrows, int ncols, const int* __restrict__ off,
+                     const int* __restrict__ c, unsigned char* flags, int* bad) {
+  __shared__ RowIds ids;
+  const int lane = threadIdx.x & 31;
+  int mybad = 0;
+  const int ntiles = (nrows + kRT - 1) / kRT;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int r0 = tile * kRT;
+    csr_rowid_tile(nrows, off, r0, ids, [&](int kb, int k0, int kend) {
+      const int k = kb + threadIdx.x;
+      const bool in = k < kend;
+      const int ck = in ? ld_stream(c + k) : 0;
+      int prev = __shfl_up_sync(0xffffffffu, ck, 1);
+      if (lane == 0 && in && k > 0) prev = __ldg(c + k - 1);
+      if (in) {
+        const int t = ids.rid[k - k0];
+        if (k > ids.off[t] && prev >= ck) mybad |= kBadOrder;
+        if ((unsigned)ck >= (unsigned)ncols) {
+          mybad |= kBadIndex;
+        } else if (flags) {
+          const int64_t d = (int64_t)ck - (r0 + t) + nrows - 1;
+          unsigned short f;
+          asm volatile("ld.global.ca.u8 %0, [%1];" : "=h"(f) : "l"(flags + d));
+          if (f == 0) flags[d] = 1;
+        }
+      }
+    });
+  }
+  mybad = __reduce_or_sync(0xffffffffu, mybad);
+  if (lane == 0 && mybad) atomicOr(bad, mybad);
+}
+
+// canonical CSR -> DIA: the tile's (kRT x nd) slab zeroed in shared memory,
+// entries dropped into (row, diag_map[col - row]) slots, the slab written out
+// contiguously (values are row-major (nrows, nd))
+__global__ void __launch_bounds__(256)
+    csr_dia_fill_tiles(int nrows, int nd, const int* __restrict__ off,
+                       const int* __restrict__ c, const double* __restrict__ v,
+                       const int* __restrict__ map, double* __restrict__ vals) {
+  extern __shared__ double slab[];   // kRT * nd
+  __shared__ RowIds ids;
+  const int ntiles = (nrows + kRT - 1) / kRT;
+  const uint64_t pol = policy_evict_first();
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int r0 = tile * kRT;
+    const int total = min(kRT, nrows - r0) * nd;
+    for (int i = threadIdx.x; i < total; i += blockDim.x) slab[i] = 0.0;
+    // (csr_rowid_tile's first barrier orders the zeroing before the drops)
+    csr_rowid_tile(nrows, off, r0, ids, [&](int kb, int k0, int kend) {
+      const int k = kb + threadIdx.x;
+      if (k < kend) {
+        const int t = ids.rid[k - k0];
+        const int ck = ld_hint(c + k, pol);
+        const double vk = ld_hint(v + k, pol);
+        const int j = __ldg(map + ((int64_t)ck - (r0 + t) + nrows - 1));
+        slab[t * nd + j] = vk;
+      }
+    });
+    double* out = vals + (int64_t)r0 * nd;
+    for (int i = threadIdx.x; i < total; i += blockDim.x) __stcs(out + i, slab[i]);
+    __syncthreads();
   }
 }
 
@@ -1144,6 +1362,10 @@ extern "C" int ds_convert_begin_coo(int64_t nrows, int64_t ncols, int64_t nnz, c
   return DS_OK;
 }
 
+static unsigned rt_grid(int64_t nrows, int per_sm) {   // kRT-row tiles, persistent
+  return (unsigned)std::max<int64_t>(1, min64(ceil_div(nrows, kRT), (int64_t)sm_count() * per_sm));
+}
+
 static unsigned csr_walk_grid(int64_t nrows) {   // 8 warps per block
   return (unsigned)std::max<int64_t>(
       1, min64(ceil_div(nrows, kCsrWalkRows * 8), (int64_t)sm_count() * 8));
@@ -1164,9 +1386,9 @@ static int begin_csr_impl(ds_convert_job* j, int64_t nnz, const int32_t* row_off
     DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&j->scratch), flag_bytes + 4, st));
     DS_CUDA(cudaMemsetAsync(j->scratch, 0, flag_bytes + 4, st));
     int* bad = reinterpret_cast<int*>(j->scratch + flag_bytes);
-    csr_check_mark<<<csr_walk_grid(nrows), 256, 0, st>>>((int)nrows, (int)ncols, row_offsets, cols,
-                                                         dia ? j->scratch : nullptr, bad);
-    DS_LAUNCH_CHECK("csr_check_mark");
+    csr_census_tiles<<<rt_grid(nrows, 8), 256, 0, st>>>((int)nrows, (int)ncols, row_offsets, cols,
+                                                       dia ? j->scratch : nullptr, bad);
+    DS_LAUNCH_CHECK("csr_census_tiles");
     int bad_h = 1;
     DS_CUDA(cudaMemcpyAsync(&bad_h, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
     DS_CUDA(cudaStreamSynchronize(st));
@@ -1419,6 +1641,15 @@ static int finish_dia_impl(ds_convert_job* job, int32_t* offsets, double* values
       DS_LAUNCH_CHECK("dia_copy_diags");
         return DS_OK;
     }
+    if (job->csr_off && (int64_t)kRT * nd * 8 <= 96 * 1024) {
+      const size_t smem = (size_t)kRT * nd * 8;
+      int rc = allow_dynamic_smem((const void*)csr_dia_fill_tiles, smem);
+      if (rc) return rc;
+      csr_dia_fill_tiles<<<rt_grid(job->nrows, 6), 256, smem, st>>>(
+          (int)job->nrows, (int)nd, job->csr_off, job->c, job->v, job->diag_map, values);
+      DS_LAUNCH_CHECK("csr_dia_fill_tiles");
+      return DS_OK;
+    }
     const int R = kCsrWalkRows * 8;   // 8 warps
     if (job->csr_off && (int64_t)R * nd * 8 <= 48 * 1024) {
       dia_fill_csr<<<csr_walk_grid(job->nrows), 256, (size_t)R * nd * 8, st>>>(
@@ -1463,3 +1694,46 @@ extern "C" int ds_convert_finish_dia(ds_convert_job* job, int32_t* offsets, doub
 }
 
 extern "C" void ds_convert_abort(ds_convert_job* job) { free_job(job); }
+
+extern "C" int ds_dia_to_entries(int64_t nrows, int64_t ncols, int32_t ndiags,
+                                 const int32_t* offsets, const double* values, int target,
+                                 int32_t* row_idx, int32_t* cols, double* vals, int64_t* nnz,
+                                 void* stream) {
+  cudaStream_t st = as_stream(stream);
+  *nnz = 0;
+  if (!dims_ok(nrows, ncols, 0)) return DS_ERR_NOT_SUPPORTED;
+  if (target != DS_FMT_CSR && target != DS_FMT_COO) {
+    set_error("ds_dia_to_entries: CSR or COO target only");
+    return DS_ERR_INVALID_ARGUMENT;
+  }
+  if (ndiags > kDiaOneMaxNd || ndiags < 1 || nrows == 0) {
+    set_error("ds_dia_to_entries: 1 <= ndiags <= %d and nrows > 0", kDiaOneMaxNd);
+    return DS_ERR_NOT_SUPPORTED;
+  }
+  const int64_t ngroups = ceil_div(nrows, kDiaGroupRows);
+  unsigned char* scratch = nullptr;   // ticket | total | status[ngroups]
+  const size_t bytes = 16 + (size_t)ngroups * 8;
+  DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scratch), bytes, st));
+  int rc = DS_OK;
+  long long h_total = 0;
+  do {
+    if (cudaMemsetAsync(scratch, 0, bytes, st) != cudaSuccess) {
+      rc = cuda_fail(cudaGetLastError(), "dia one-pass scratch");
+      break;
+    }
+    const unsigned grid = (unsigned)std::max<int64_t>(
+        1, min64(ceil_div(ngroups, 4), (int64_t)sm_count() * 4));
+    dia_emit_onepass<<<grid, 128, 0, st>>>(
+        nrows, (int)ncols, ndiags, offsets, values, ngroups,
+        reinterpret_cast<unsigned long long*>(scratch + 16), reinterpret_cast<int*>(scratch),
+        target == DS_FMT_CSR ? row_idx : nullptr, target == DS_FMT_COO ? row_idx : nullptr,
+        cols, vals, reinterpret_cast<long long*>(scratch + 8));
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&h_total, scratch + 8, 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) rc = cuda_fail(e, "dia_emit_onepass");
+  } while (false);
+  cudaFreeAsync(scratch, st);
+  *nnz = h_total;
+  return rc;
+}
