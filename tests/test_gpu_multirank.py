@@ -128,6 +128,10 @@ def test_tuner_modes_agree_across_ranks(tmp_path):
 
 
 @pytest.mark.timeout(420)
+@pytest.mark.skipif(os.environ.get("DS_TEST_NCCL_ONE_GPU") != "1",
+                    reason="NCCL ranks sharing one GPU talk over sockets and spin while their "
+                           "contexts time-slice (minutes); opt in with DS_TEST_NCCL_ONE_GPU=1 "
+                           "or run on a multi-GPU node")
 def test_nccl_rank_cg_matches_oracle(tmp_path):
     """The NCCL transport (pack kernels + grouped send/recv + ncclAllGather)
     at world 2.  On one GPU the ranks claim distinct NCCL host ids and talk
