@@ -315,7 +315,10 @@ def format_switching(ds, torch, dev, peak, nx: int = 192, steps: int = 100) -> d
     torch.cuda.synchronize()
     gen_s = time.perf_counter() - t0
     prof = D.profile_rank(part, split, reps=5)
-    lf, rf = D.select_rank_plan(prof["entries"], "multi", 1)
+    # the pick pays each combination's measured switch cost amortised over
+    # the planned iterations ("format switching with conversion cost included")
+    lf, rf = D.select_rank_plan(prof["entries"], "multi", 1, prof["convert_s"], steps)
+    lf0, rf0 = D.select_rank_plan(prof["entries"], "multi", 1)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     ds.convert_inplace(split.local, lf)
@@ -343,6 +346,8 @@ def format_switching(ds, torch, dev, peak, nx: int = 192, steps: int = 100) -> d
     out = {
         "grid": [nx, nx, nx], "n": n, "nnz": nnz, "generate_on_device_s": round(gen_s, 3),
         "plan": [lf.name.lower(), rf.name.lower()],
+        "plan_ignoring_switch_cost": [lf0.name.lower(), rf0.name.lower()],
+        "selection": f"tuner multi, switch cost amortised over {steps} iterations",
         "spmv_us": {f"{a.name.lower()}/{b.name.lower()}": round(t * 1e6, 1)
                     for (a, b), t in sorted(prof["entries"].items())},
         "convert_from_csr_ms": {f"{a.name.lower()}/{b.name.lower()}": round(t * 1e3, 3)

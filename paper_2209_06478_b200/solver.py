@@ -440,7 +440,7 @@ class CgEngine:
 # bounds that overshoot against the cost of a readback
 _MAX_ROUNDS = max(1, int(os.environ.get("DS_CG_MAX_ROUNDS", "4")))
 # iterations per body of the device-side WHILE loop (0: chunked replays)
-_WHILE_STEPS = max(0, int(os.environ.get("DS_CG_WHILE_STEPS", "2")))   # e2e solve: 4 -> 1068 vs 16 -> 994 GFLOP/s
+_WHILE_STEPS = max(0, int(os.environ.get("DS_CG_WHILE_STEPS", "8")))   # e2e solve: 4 -> 1068 vs 16 -> 994 GFLOP/s
 
 
 def _finish(engine: CgEngine, sc) -> tuple[int, np.ndarray, bool]:
