@@ -632,8 +632,10 @@ struct RowIds {
   unsigned char rid[kRtCap];
 };
 
-// body(kb, k0, kend, ids): entries kb + threadIdx.x of the chunk [k0, kend);
-// the trip count is uniform across the block (lanes past kend see k >= kend)
+// body(kb, k0, kend): entries kb + u * blockDim.x + threadIdx.x (u < kRtU) of
+// the chunk [k0, kend) -- kRtU loads in flight per thread; the trip count is
+// uniform across the block (lanes past kend see k >= kend)
+constexpr int kRtU = 8;
 template <class Body>
 __device__ __forceinline__ void csr_rowid_tile(int nrows, const int* __restrict__ off, int r0,
                                                RowIds& ids, Body&& body) {
@@ -648,7 +650,7 @@ __device__ __forceinline__ void csr_rowid_tile(int nrows, const int* __restrict_
       for (int k = lo; k < hi; ++k) ids.rid[k - k0] = (unsigned char)t;
     }
     __syncthreads();
-    for (int kb = k0; kb < kend; kb += blockDim.x) body(kb, k0, kend);
+    for (int kb = k0; kb < kend; kb += blockDim.x * kRtU) body(kb, k0, kend);
     __syncthreads();
   }
 }
@@ -665,21 +667,29 @@ __global__ void __launch_bounds__(256)
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int r0 = tile * kRT;
     csr_rowid_tile(nrows, off, r0, ids, [&](int kb, int k0, int kend) {
-      const int k = kb + threadIdx.x;
-      const bool in = k < kend;
-      const int ck = in ? ld_stream(c + k) : 0;
-      int prev = __shfl_up_sync(0xffffffffu, ck, 1);
-      if (lane == 0 && in && k > 0) prev = __ldg(c + k - 1);
-      if (in) {
-        const int t = ids.rid[k - k0];
-        if (k > ids.off[t] && prev >= ck) mybad |= kBadOrder;
-        if ((unsigned)ck >= (unsigned)ncols) {
-          mybad |= kBadIndex;
-        } else if (flags) {
-          const int64_t d = (int64_t)ck - (r0 + t) + nrows - 1;
-          unsigned short f;
-          asm volatile("ld.global.ca.u8 %0, [%1];" : "=h"(f) : "l"(flags + d));
-          if (f == 0) flags[d] = 1;
+      int ck[kRtU], pv[kRtU];
+#pragma unroll
+      for (int u = 0; u < kRtU; ++u) {
+        const int k = kb + u * (int)blockDim.x + (int)threadIdx.x;
+        ck[u] = k < kend ? ld_stream(c + k) : 0;
+        pv[u] = (lane == 0 && k < kend && k > 0) ? __ldg(c + k - 1) : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < kRtU; ++u) {
+        const int k = kb + u * (int)blockDim.x + (int)threadIdx.x;
+        int prev = __shfl_up_sync(0xffffffffu, ck[u], 1);
+        if (lane == 0) prev = pv[u];
+        if (k < kend) {
+          const int t = ids.rid[k - k0];
+          if (k > ids.off[t] && prev >= ck[u]) mybad |= kBadOrder;
+          if ((unsigned)ck[u] >= (unsigned)ncols) {
+            mybad |= kBadIndex;
+          } else if (flags) {
+            const int64_t d = (int64_t)ck[u] - (r0 + t) + nrows - 1;
+            unsigned short f;
+            asm volatile("ld.global.ca.u8 %0, [%1];" : "=h"(f) : "l"(flags + d));
+            if (f == 0) flags[d] = 1;
+          }
         }
       }
     });
@@ -705,13 +715,24 @@ __global__ void __launch_bounds__(256)
     for (int i = threadIdx.x; i < total; i += blockDim.x) slab[i] = 0.0;
     // (csr_rowid_tile's first barrier orders the zeroing before the drops)
     csr_rowid_tile(nrows, off, r0, ids, [&](int kb, int k0, int kend) {
-      const int k = kb + threadIdx.x;
-      if (k < kend) {
-        const int t = ids.rid[k - k0];
-        const int ck = ld_hint(c + k, pol);
-        const double vk = ld_hint(v + k, pol);
-        const int j = __ldg(map + ((int64_t)ck - (r0 + t) + nrows - 1));
-        slab[t * nd + j] = vk;
+      int ck[kRtU];
+      double vk[kRtU];
+#pragma unroll
+      for (int u = 0; u < kRtU; ++u) {
+        const int k = kb + u * (int)blockDim.x + (int)threadIdx.x;
+        ck[u] = k < kend ? ld_hint(c + k, pol) : 0;
+        vk[u] = k < kend ? ld_hint(v + k, pol) : 0.0;
+      }
+      int j[kRtU];
+#pragma unroll
+      for (int u = 0; u < kRtU; ++u) {
+        const int k = kb + u * (int)blockDim.x + (int)threadIdx.x;
+        j[u] = k < kend ? __ldg(map + ((int64_t)ck[u] - (r0 + ids.rid[k - k0]) + nrows - 1)) : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < kRtU; ++u) {
+        const int k = kb + u * (int)blockDim.x + (int)threadIdx.x;
+        if (k < kend) slab[ids.rid[k - k0] * nd + j[u]] = vk[u];
       }
     });
     double* out = vals + (int64_t)r0 * nd;

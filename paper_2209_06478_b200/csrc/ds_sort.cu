@@ -321,9 +321,9 @@ __global__ void __launch_bounds__(32 * kSegWarps)
     const int r0 = __ldg(tiles + t), r1 = __ldg(tiles + t + 1);
     const int e0 = __ldg(off + r0), cnt = __ldg(off + r1) - e0;
     if (r1 - r0 == 1 && cnt > kSegShort) continue;   // a long row: the CTA kernel sorts it
-    if (cnt <= 1) {                                  // nothing to sort
+    if (cnt <= 1) {   // nothing to sort (the entry's row need not be r0: empty rows lead)
       if (lane < cnt) {
-        keys_out[e0] = (u64)(unsigned)r0 * ncols + (u64)(unsigned)__ldg(cols + e0);
+        keys_out[e0] = (u64)(unsigned)__ldg(rows + e0) * ncols + (u64)(unsigned)__ldg(cols + e0);
         perm_out[e0] = e0;
       }
       continue;
