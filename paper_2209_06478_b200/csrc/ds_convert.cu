@@ -1662,7 +1662,9 @@ static int finish_dia_impl(ds_convert_job* job, int32_t* offsets, double* values
       DS_LAUNCH_CHECK("dia_copy_diags");
         return DS_OK;
     }
-    if (job->csr_off && (int64_t)kRT * nd * 8 <= 96 * 1024) {
+    static int fill_tiles = -1;   // measured slower at 192^3 (1.28 vs 0.81 ms): opt-in
+    if (fill_tiles < 0) fill_tiles = getenv("DS_DIA_FILL_TILES") ? 1 : 0;
+    if (fill_tiles && job->csr_off && (int64_t)kRT * nd * 8 <= 96 * 1024) {
       const size_t smem = (size_t)kRT * nd * 8;
       int rc = allow_dynamic_smem((const void*)csr_dia_fill_tiles, smem);
       if (rc) return rc;

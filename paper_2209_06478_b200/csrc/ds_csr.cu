@@ -1079,35 +1079,44 @@ __global__ void __launch_bounds__(32 * kTileWarps, 6)
     }
     __syncwarp();
     if (!is_long) {
-      for (int r = r0 + lane; r < r1; r += 32) {
-        const int s = __ldg(off + r) - e0;
-        const int len = __ldg(off + r + 1) - e0 - s;
+      // an aligned group of 8 lanes per row, numpy's pairwise leaf exactly
+      // as csr_leaf_g8 (lane j = accumulator r[j]; xor butterfly 1, 2, 4 =
+      // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)); the tail added in order): 32
+      // lanes read 4 rows' products 8 at a time instead of one lane per row
+      // walking rows of very different lengths
+      const int g8 = lane >> 3, l8 = lane & 7;
+      const unsigned gmask = 0xffu << (8 * g8);
+      for (int rb = r0; rb < r1; rb += 4) {
+        const int r = rb + g8;
+        const bool has = r < r1;
+        int s = 0, len = 0;
+        if (has) {
+          s = __ldg(off + r) - e0;
+          len = __ldg(off + r + 1) - e0 - s;
+        }
+        if (!has) continue;   // whole groups only: the shuffles below stay inside the group
         double sum;
         if (len == 0) {
           sum = 0.0;
         } else {
           const double* p = prod + s;
           const int m = len - 1;   // addends after p[first] (m <= 128 inside a tile)
+          const int full = m & ~7;
           double res;
-          if (m < 8) {
-            res = -0.0;            // numpy >= 2 starts small pairwise blocks from -0.0
-            for (int i = 0; i < m; ++i) res = add(res, p[1 + i]);
+          if (full > 0) {
+            double acc = p[1 + l8];
+            for (int q = 8; q < full; q += 8) acc = add(acc, p[1 + q + l8]);
+            acc = add(acc, __shfl_xor_sync(gmask, acc, 1));
+            acc = add(acc, __shfl_xor_sync(gmask, acc, 2));
+            acc = add(acc, __shfl_xor_sync(gmask, acc, 4));
+            res = acc;
           } else {
-            double a[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) a[j] = p[1 + j];
-            const int full = m & ~7;
-            int i = 8;
-            for (; i < full; i += 8) {
-#pragma unroll
-              for (int j = 0; j < 8; ++j) a[j] = add(a[j], p[1 + i + j]);
-            }
-            res = add(add(add(a[0], a[1]), add(a[2], a[3])), add(add(a[4], a[5]), add(a[6], a[7])));
-            for (; i < m; ++i) res = add(res, p[1 + i]);
+            res = -0.0;            // numpy >= 2 starts small pairwise blocks from -0.0
           }
+          for (int i = full; i < m; ++i) res = add(res, p[1 + i]);
           sum = add(p[0], res);
         }
-        y[r] = ACCUM ? add(y[r], sum) : sum;
+        if (l8 == 0) y[r] = ACCUM ? add(y[r], sum) : sum;
       }
     }
     __syncwarp();
