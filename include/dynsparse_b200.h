@@ -243,7 +243,7 @@ typedef struct ds_matrix {
   int32_t max_row_len;       /* CSR / sorted COO: longest row if known, else 0  */
   const int32_t* row_perm;   /* CSR: rows grouped by length bin (ds_csr_bins), or NULL */
   int64_t bins[9];           /* CSR: bin b = row_perm[bins[b] .. bins[b+1])     */
-  const int32_t* tiles;      /* CSR: ds_csr_tiles plan (ntiles + 1 row starts), or NULL */
+  const int32_t* tiles;      /* CSR: ds_csr_tiles plan (header, tiles, leaves, scratch), or NULL */
   int64_t ntiles;
 } ds_matrix;
 
@@ -255,14 +255,26 @@ typedef struct ds_matrix {
  * are written to host memory (synchronises).                               */
 int ds_csr_bins(int64_t nrows, const int32_t* row_offsets, int32_t* perm, int64_t* bins,
                 void* stream);
-/* Entry tiles for irregular CSR: tiles[t] = first row of tile t (t <
- * *ntiles), tiles[*ntiles] = nrows; a tile of rows <= 129 entries holds at
- * most 256 entries, every longer row is a tile of its own.  tiles needs
- * nrows + 1 int32; *ntiles is written to host memory (synchronises).  With
- * row_perm / bins set too, ds_spmv runs the tiles (entry-parallel products,
- * row-parallel exact sums) and the long rows concurrently.                 */
-int ds_csr_tiles(int64_t nrows, const int32_t* row_offsets, int32_t* tiles, int64_t* ntiles,
-                 void* stream);
+/* SpMV tile plan for irregular CSR (csr_tile_kernel): the rows are cut into
+ * "row tiles" of consecutive rows of <= 129 entries holding < 512 entries
+ * (a tile boundary where row_offsets crosses a multiple of 382), and every
+ * longer row into "leaf tiles": np.add.reduceat sums a row as p[first] +
+ * pairwise(rest), numpy's pairwise recursion splits n > 128 addends at
+ * n/2 - (n/2)%8, and its leaves (64..128 addends) are packed 4 per tile.
+ * All tiles run in one grid (entry-parallel products, one lane per row or
+ * leaf for the exact sums); a second small kernel replays each long row's
+ * recursion over its leaf sums.  plan (int32 words, capacity >= 
+ * ds_csr_tiles_capacity(nrows, nnz)): [0..7] header {tiles, leaves, long
+ * rows, leaf-list offset, long-row-list offset, scratch offset, row tiles},
+ * then one int4 {A, B, E0, E1} per tile (row tile: rows [A, B); leaf tile,
+ * A < 0: leaves -A-1 ..; entries [E0, E1)), (start, len) per leaf, (row,
+ * first leaf) per long row, and one double of SCRATCH per leaf that every
+ * SpMV writes -- SpMVs sharing one plan must not run concurrently.  Writes
+ * *ntiles (= the descriptor's ntiles) and *words_used (the plan may be
+ * copied to a buffer of that size); synchronises.                           */
+int64_t ds_csr_tiles_capacity(int64_t nrows, int64_t nnz);
+int ds_csr_tiles(int64_t nrows, const int32_t* row_offsets, int32_t* plan, int64_t capacity,
+                 int64_t* ntiles, int64_t* words_used, void* stream);
 
 int ds_spmv(const ds_matrix* a, const double* x, double* y, int accumulate, void* stream);
 

@@ -96,7 +96,8 @@ _SIGNATURES = {
     "ds_spmv_coo_sorted": (c_int, [c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp,
                                    c_int, c_vp]),
     "ds_csr_bins": (c_int, [c_i64, c_vp, c_vp, P_i64, c_vp]),
-    "ds_csr_tiles": (c_int, [c_i64, c_vp, c_vp, P_i64, c_vp]),
+    "ds_csr_tiles_capacity": (c_i64, [c_i64, c_i64]),
+    "ds_csr_tiles": (c_int, [c_i64, c_vp, c_vp, c_i64, P_i64, P_i64, c_vp]),
     "ds_dot_workspace_bytes": (c_i64, []),
     "ds_dot": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "ds_waxpby": (c_int, [c_i64, c_dbl, c_vp, c_dbl, c_vp, c_vp, c_vp]),

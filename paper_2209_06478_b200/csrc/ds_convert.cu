@@ -1067,9 +1067,189 @@ static int tile_plan(int64_t nrows, const int* off, int lng, int target, int* ti
 }
 }  // namespace ds
 
-extern "C" int ds_csr_tiles(int64_t nrows, const int32_t* row_offsets, int32_t* tiles,
-                            int64_t* ntiles, void* stream) {
-  return tile_plan(nrows, row_offsets, 129, kCsrTileTarget, tiles, ntiles, as_stream(stream));
+namespace ds {
+// ---- the SpMV tile plan of an irregular CSR (csr_tile_kernel, ds_csr.cu) ----
+// Layout (int32 words), see include/dynsparse_b200.h ds_csr_tiles:
+//   [0..7] header: total tiles, leaves, long rows, LV, LR, SCR (word offsets), row tiles
+//   [8 ..) one int4 per tile {A, B, E0, E1}: a row tile (A >= 0) holds rows
+//          [A, B) and entries [E0, E1); a leaf tile (A < 0) holds the B
+//          consecutive pairwise leaves -A-1 .. -A-2+B of one long row, entries [E0, E1)
+//   LV: (start, len) of every leaf;  LR: (row, first leaf) of every long row
+//   SCR: one double per leaf (the leaf sums, written by every SpMV)
+// A long row (> 129 entries) is reduced by np.add.reduceat as p[first] +
+// pairwise(p[first+1 .. end]); pairwise splits n > 128 addends at
+// n/2 - (n/2)%8, so its leaves hold 64..128 addends.  They become leaf tiles
+// of <= 4 leaves (<= 512 entries), spread over the whole grid with the row
+// tiles; a small kernel then replays the recursion over the leaf sums.
+constexpr int kLeavesPerTile = kCsrTileMax / 128;
+constexpr int kPlanHeader = 8;
+
+__device__ __forceinline__ int pw_split(int n) {
+  const int n2 = n / 2;
+  return n2 - n2 % 8;
+}
+__device__ int pw_count_leaves(int m) {
+  int stack[48], sp = 0, cnt = 0;
+  stack[sp++] = m;
+  while (sp) {
+    const int n = stack[--sp];
+    if (n <= 128) {
+      ++cnt;
+      continue;
+    }
+    const int n2 = pw_split(n);
+    stack[sp++] = n - n2;   // right pushed first: the left half is visited first
+    stack[sp++] = n2;
+  }
+  return cnt;
+}
+struct IsLongRow {
+  const int* off;
+  __device__ int operator()(int64_t r) const { return off[r + 1] - off[r] > 129 ? 1 : 0; }
+};
+struct TilesOf {
+  const int* a;
+  __device__ int operator()(int64_t k) const { return (a[k] + kLeavesPerTile - 1) / kLeavesPerTile; }
+};
+__global__ void long_rows_scatter(int nrows, const int* __restrict__ off, const int* __restrict__ pos,
+                                  int* longs) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += gridDim.x * blockDim.x)
+    if (off[r + 1] - off[r] > 129) longs[pos[r]] = r;
+}
+__global__ void long_rows_leaf_counts(int64_t nlong, const int* __restrict__ longs,
+                                      const int* __restrict__ off, int* cnt) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nlong;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = longs[i];
+    cnt[i] = pw_count_leaves(off[r + 1] - off[r] - 1);
+  }
+}
+__global__ void row_tiles_write(int64_t nt, const int* __restrict__ rs, const int* __restrict__ off,
+                                int4* plan4) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nt;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int r0 = rs[t], r1 = rs[t + 1], e0 = off[r0], e1 = off[r1];
+    // a long row's own tile stays as an empty placeholder: its leaf tiles carry it
+    plan4[t] = (r1 - r0 == 1 && e1 - e0 > 129) ? make_int4(r0, r0, e0, e0)
+                                                : make_int4(r0, r1, e0, e1);
+  }
+}
+// one thread per long row: its leaves in recursion order, its leaf tiles
+__global__ void long_rows_leaves(int64_t nlong, const int* __restrict__ longs,
+                                 const int* __restrict__ off, const int* __restrict__ leaf0,
+                                 const int* __restrict__ tile0, int64_t nt, int4* plan4, int* lv,
+                                 int* lr) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nlong;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = longs[i], first = off[r];
+    const int L0 = leaf0[i];
+    lr[2 * i] = r;
+    lr[2 * i + 1] = L0;
+    int st_s[48], st_n[48], sp = 0, k = 0, tstart = 0, tlo = 0;
+    int64_t tj = nt + tile0[i];
+    st_s[sp] = first + 1;
+    st_n[sp++] = off[r + 1] - first - 1;
+    while (sp) {
+      --sp;
+      const int a = st_s[sp], n = st_n[sp];
+      if (n <= 128) {
+        lv[2 * (L0 + k)] = a;
+        lv[2 * (L0 + k) + 1] = n;
+        if (k % kLeavesPerTile == 0) {
+          tstart = a;
+          tlo = k;
+        }
+        ++k;
+        const bool last = sp == 0;
+        if (k % kLeavesPerTile == 0 || last) {
+          plan4[tj++] = make_int4(-(L0 + tlo) - 1, k - tlo, tstart, a + n);
+        }
+        continue;
+      }
+      const int n2 = pw_split(n);
+      st_s[sp] = a + n2;
+      st_n[sp++] = n - n2;
+      st_s[sp] = a;
+      st_n[sp++] = n2;
+    }
+  }
+}
+__global__ void plan_header(int* h, int a, int b, int c, int d, int e, int f, int g) {
+  h[0] = a; h[1] = b; h[2] = c; h[3] = d; h[4] = e; h[5] = f; h[6] = g; h[7] = 0;
+}
+}  // namespace ds
+
+extern "C" int64_t ds_csr_tiles_capacity(int64_t nrows, int64_t nnz) {
+  const int64_t leaves = nnz / 64 + 1, longs = nnz / 130 + 1;
+  return kPlanHeader + 4 * (nrows + 1 + leaves) + 2 * leaves + 2 * longs + 2 * leaves + 2;
+}
+
+extern "C" int ds_csr_tiles(int64_t nrows, const int32_t* row_offsets, int32_t* plan,
+                            int64_t capacity, int64_t* ntiles, int64_t* words, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  *ntiles = 0;
+  if (words) *words = 0;
+  if (nrows <= 0) return DS_OK;
+  int64_t nnz = 0;
+  {
+    int h = 0;
+    DS_CUDA(cudaMemcpyAsync(&h, row_offsets + nrows, sizeof(int), cudaMemcpyDeviceToHost, st));
+    DS_CUDA(cudaStreamSynchronize(st));
+    nnz = h;
+  }
+  if (capacity < ds_csr_tiles_capacity(nrows, nnz)) {
+    set_error("ds_csr_tiles: capacity %lld < %lld words", (long long)capacity,
+              (long long)ds_csr_tiles_capacity(nrows, nnz));
+    return DS_ERR_INVALID_ARGUMENT;
+  }
+  // scratch: row starts of the row tiles, long rows, per-long-row leaf / tile counts and starts
+  int* tmp = nullptr;
+  const int64_t lcap = nnz / 130 + 1;
+  DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tmp), (nrows + 1 + 5 * lcap) * sizeof(int), st));
+  int *rs = tmp, *longs = rs + nrows + 1, *cnt = longs + lcap, *leaf0 = cnt + lcap,
+      *tile0 = leaf0 + lcap, *pos = tile0 + lcap;
+  int64_t nt = 0, nlong = 0, nleaves = 0, nlt = 0;
+  int rc = tile_plan(nrows, row_offsets, 129, kCsrTileTarget, rs, &nt, st);
+  int* rpos = nullptr;
+  if (!rc) {
+    DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&rpos), nrows * sizeof(int), st));
+    rc = exclusive_scan(nrows, IsLongRow{row_offsets}, rpos, &nlong, st);
+  }
+  if (!rc && nlong > 0) {
+    long_rows_scatter<<<grid1d(nrows), 256, 0, st>>>((int)nrows, row_offsets, rpos, longs);
+    long_rows_leaf_counts<<<grid1d(nlong), 256, 0, st>>>(nlong, longs, row_offsets, cnt);
+    DS_LAUNCH_CHECK("long_rows_leaf_counts");
+    rc = exclusive_scan(nlong, ArrayAt{cnt}, leaf0, &nleaves, st);
+    if (!rc) rc = exclusive_scan(nlong, TilesOf{cnt}, tile0, &nlt, st);
+  }
+  (void)pos;
+  if (rpos) cudaFreeAsync(rpos, st);
+  if (rc) {
+    cudaFreeAsync(tmp, st);
+    return rc;
+  }
+  const int64_t LV = kPlanHeader + 4 * (nt + nlt);
+  const int64_t LR = LV + 2 * nleaves;
+  const int64_t SCR = (LR + 2 * nlong + 1) & ~int64_t(1);
+  const int64_t used = SCR + 2 * nleaves;
+  if (used > capacity) {   // cannot happen with ds_csr_tiles_capacity
+    cudaFreeAsync(tmp, st);
+    set_error("ds_csr_tiles: plan needs %lld words", (long long)used);
+    return DS_ERR_INVALID_ARGUMENT;
+  }
+  int4* plan4 = reinterpret_cast<int4*>(plan + kPlanHeader);
+  if (nt > 0) row_tiles_write<<<grid1d(nt), 256, 0, st>>>(nt, rs, row_offsets, plan4);
+  if (nlong > 0)
+    long_rows_leaves<<<grid1d(nlong), 128, 0, st>>>(nlong, longs, row_offsets, leaf0, tile0, nt,
+                                                    plan4, plan + LV, plan + LR);
+  plan_header<<<1, 1, 0, st>>>(plan, (int)(nt + nlt), (int)nleaves, (int)nlong, (int)LV, (int)LR,
+                               (int)SCR, (int)nt);
+  DS_LAUNCH_CHECK("ds_csr_tiles");
+  DS_CUDA(cudaFreeAsync(tmp, st));
+  DS_CUDA(cudaStreamSynchronize(st));
+  *ntiles = nt + nlt;
+  if (words) *words = used;
+  return DS_OK;
 }
 
 extern "C" int ds_csr_bins(int64_t nrows, const int32_t* row_offsets, int32_t* perm, int64_t* bins,

@@ -1013,117 +1013,191 @@ int launch_csr_binned(int64_t nrows, int64_t ncols, int64_t nnz, const int* off,
 }
 
 // ------------------------------------------------------- irregular: tiles --
-// csr_warp_tiles: entry-parallel products, row-parallel exact sums, one WARP
+// csr_tile_kernel: entry-parallel products, row-parallel exact sums, one WARP
 // per tile.  The rows are cut into tiles of consecutive rows holding at most
-// kCsrTileMax = 256 entries (ds_csr_tiles; every row longer than kLongRow is
+// kCsrTileMax = 512 entries (ds_csr_tiles; every row longer than kLongRow is
 // a tile of its own and is skipped here -- the long-row kernels take it on a
-// side stream, concurrently).  Per tile each lane forms the products of 8
+// side stream, concurrently).  Per tile each lane forms the products of 16
 // entries (consecutive lanes, consecutive entries: every warp gather
 // instruction carries 32 useful random x loads, no lane idles on a short
-// row) into the warp's shared-memory slice; then one lane per row sums its
-// products in np.add.reduceat order (p[first] + pairwise(rest)).  Warps never
-// wait for each other (no block barrier), so ~48 independent warps per SM
-// keep the gather latency covered; the next tile's bounds are loaded before
-// the current tile's sums.  x carries a persisting L2 window (gathered ~13
-// times per entry at random on the power-law matrix); the matrix streams
-// with evict_first.
+// row) into the warp's shared-memory slice; then ONE LANE PER ROW sums its
+// products in np.add.reduceat order (p[first] + pairwise(rest): 8 register
+// accumulators for 8 <= m <= 128 addends, sequential from -0.0 below).  A
+// tile holds ~30 power-law rows, so the sum phase keeps most lanes busy; the
+// previous design (8 lanes per row, 256-entry tiles) spent ~4 warp
+// instructions per entry there (ncu r2j: 235M instructions, issue-bound at
+// 55% SM throughput) against the 217 us random-gather floor of
+// tools/gather_floor.cu.  Warps never wait for each other (no block
+// barrier); the next tile's bounds are loaded before the current tile's sums.
+// x carries a persisting L2 window (gathered ~13 times per entry at random on
+// the power-law matrix, L1 bypassed); the matrix streams with evict_first.
 constexpr int kTileWarps = 8;
 constexpr int kTilePer = kCsrTileMax / 32;   // entries per lane
 
-template <bool ACCUM>
-__global__ void __launch_bounds__(32 * kTileWarps, 6)
-    csr_tile_kernel(int64_t ntiles, const int* __restrict__ tiles, const int* __restrict__ off,
+__device__ __forceinline__ double ld_gather_na(const double* p) {
+  double v;
+  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
+// numpy's pairwise sum of n <= 128 addends a[0..n): sequential from -0.0
+// below 8 (numpy >= 2), else 8 accumulators combined
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) and the n%8 tail added in order
+__device__ __forceinline__ double pairwise_block(const double* a, int n) {
+  double res;
+  int i;
+  if (n >= 8) {
+    double a0 = a[0], a1 = a[1], a2 = a[2], a3 = a[3], a4 = a[4], a5 = a[5], a6 = a[6], a7 = a[7];
+    const int full = n & ~7;
+    for (int q = 8; q < full; q += 8) {
+      const double* b = a + q;
+      a0 = add(a0, b[0]);
+      a1 = add(a1, b[1]);
+      a2 = add(a2, b[2]);
+      a3 = add(a3, b[3]);
+      a4 = add(a4, b[4]);
+      a5 = add(a5, b[5]);
+      a6 = add(a6, b[6]);
+      a7 = add(a7, b[7]);
+    }
+    res = add(add(add(a0, a1), add(a2, a3)), add(add(a4, a5), add(a6, a7)));
+    i = full;
+  } else {
+    res = -0.0;
+    i = 0;
+  }
+  for (; i < n; ++i) res = add(res, a[i]);
+  return res;
+}
+
+// np.add.reduceat value of one row of len <= kLongRow products p[0..len)
+__device__ __forceinline__ double csr_row_sum_serial(const double* p, int len) {
+  if (len == 0) return 0.0;
+  return add(p[0], pairwise_block(p + 1, len - 1));
+}
+
+// Software pipeline over a warp's tiles t, t+nw, ...: the next tile's
+// columns and values are loaded before this tile's sums, so the DRAM latency
+// of the matrix stream is off the per-tile critical path (a deeper pipeline
+// -- the next tile's gathers in flight too -- measured slower: 490 vs 412 us).
+// Tiles come from the ds_csr_tiles plan (one int4 per tile): row tiles are
+// summed one lane per row; leaf tiles (<= 4 pairwise leaves of one long row)
+// one lane per leaf into the plan's scratch, combined by csr_leaf_combine.
+template <bool ACCUM, bool NA, int MINB>
+__global__ void __launch_bounds__(32 * kTileWarps, MINB)
+    csr_tile_kernel(const int* __restrict__ plan, const int* __restrict__ off,
                     const int* __restrict__ col, const double* __restrict__ val,
                     const double* __restrict__ x, double* __restrict__ y, const int* guard) {
   __shared__ double prod_all[kTileWarps][kCsrTileMax];
   if (guard && *guard) return;
+  const int64_t ntiles = __ldg(plan);
+  const int4* __restrict__ p4 = reinterpret_cast<const int4*>(plan + 8);
+  const int* __restrict__ lv = plan + __ldg(plan + 3);
+  double* scr = reinterpret_cast<double*>(const_cast<int*>(plan) + __ldg(plan + 5));
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* prod = prod_all[warp];
   const uint64_t pol = policy_evict_first();
   const int64_t nw = (int64_t)gridDim.x * kTileWarps;
   int64_t t = (int64_t)blockIdx.x * kTileWarps + warp;
-  int r0 = 0, r1 = 0, e0 = 0, e1 = 0;
-  if (t < ntiles) {
-    r0 = __ldg(tiles + t);
-    r1 = __ldg(tiles + t + 1);
-    e0 = __ldg(off + r0);
-    e1 = __ldg(off + r1);
+  const int4 none = make_int4(0, 0, 0, 0);
+  int4 b = t < ntiles ? __ldg(p4 + t) : none;            // this tile
+  int4 nb = t + nw < ntiles ? __ldg(p4 + t + nw) : none;   // the next one
+  int c[kTilePer];
+  double v[kTilePer];
+  {
+    const int cnt = b.w - b.z;
+#pragma unroll
+    for (int j = 0; j < kTilePer; ++j) {
+      const int k = j * 32 + lane;
+      c[j] = k < cnt ? ld_hint(col + b.z + k, pol) : 0;
+      v[j] = k < cnt ? ld_hint(val + b.z + k, pol) : 0.0;
+    }
   }
   for (; t < ntiles; t += nw) {
-    const int cnt = e1 - e0;
-    const bool is_long = r1 - r0 == 1 && cnt > kLongRow;   // the long-row kernels own it
-    if (!is_long) {
-      int c[kTilePer];
-      double v[kTilePer];
+    const int cnt = b.w - b.z;
+    const bool leaf = b.x < 0;
+    // this lane's first row (or leaf) bounds, in flight with the gathers
+    int rs = 0, re = 0;
+    if (!leaf) {
+      if (b.x + lane < b.y) {
+        rs = __ldg(off + b.x + lane);
+        re = __ldg(off + b.x + lane + 1);
+      }
+    } else if (lane < b.y) {
+      const int l = -b.x - 1 + lane;
+      rs = __ldg(lv + 2 * l);
+      re = rs + __ldg(lv + 2 * l + 1);
+    }
+#pragma unroll
+    for (int j = 0; j < kTilePer; ++j)
+      if (j * 32 + lane < cnt) v[j] = mul(v[j], NA ? ld_gather_na(x + c[j]) : ld_gather(x + c[j]));
+#pragma unroll
+    for (int j = 0; j < kTilePer; ++j)
+      if (j * 32 + lane < cnt) prod[j * 32 + lane] = v[j];
+    // the tile after next: its bounds; the next tile: its columns and values
+    const int64_t t2 = t + 2 * nw;
+    const int4 nnb = t2 < ntiles ? __ldg(p4 + t2) : none;
+    {
+      const int ncnt = nb.w - nb.z;
 #pragma unroll
       for (int j = 0; j < kTilePer; ++j) {
         const int k = j * 32 + lane;
-        c[j] = k < cnt ? ld_hint(col + e0 + k, pol) : 0;
-        v[j] = k < cnt ? ld_hint(val + e0 + k, pol) : 0.0;
-      }
-#pragma unroll
-      for (int j = 0; j < kTilePer; ++j)
-        if (j * 32 + lane < cnt) v[j] = mul(v[j], ld_gather(x + c[j]));
-#pragma unroll
-      for (int j = 0; j < kTilePer; ++j)
-        if (j * 32 + lane < cnt) prod[j * 32 + lane] = v[j];
-    }
-    // the next tile's bounds, in flight during the sums
-    const int64_t tn = t + nw;
-    int n0 = 0, n1 = 0, f0 = 0, f1 = 0;
-    if (tn < ntiles) {
-      n0 = __ldg(tiles + tn);
-      n1 = __ldg(tiles + tn + 1);
-      f0 = __ldg(off + n0);
-      f1 = __ldg(off + n1);
-    }
-    __syncwarp();
-    if (!is_long) {
-      // an aligned group of 8 lanes per row, numpy's pairwise leaf exactly
-      // as csr_leaf_g8 (lane j = accumulator r[j]; xor butterfly 1, 2, 4 =
-      // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)); the tail added in order): 32
-      // lanes read 4 rows' products 8 at a time instead of one lane per row
-      // walking rows of very different lengths
-      const int g8 = lane >> 3, l8 = lane & 7;
-      const unsigned gmask = 0xffu << (8 * g8);
-      for (int rb = r0; rb < r1; rb += 4) {
-        const int r = rb + g8;
-        const bool has = r < r1;
-        int s = 0, len = 0;
-        if (has) {
-          s = __ldg(off + r) - e0;
-          len = __ldg(off + r + 1) - e0 - s;
-        }
-        if (!has) continue;   // whole groups only: the shuffles below stay inside the group
-        double sum;
-        if (len == 0) {
-          sum = 0.0;
-        } else {
-          const double* p = prod + s;
-          const int m = len - 1;   // addends after p[first] (m <= 128 inside a tile)
-          const int full = m & ~7;
-          double res;
-          if (full > 0) {
-            double acc = p[1 + l8];
-            for (int q = 8; q < full; q += 8) acc = add(acc, p[1 + q + l8]);
-            acc = add(acc, __shfl_xor_sync(gmask, acc, 1));
-            acc = add(acc, __shfl_xor_sync(gmask, acc, 2));
-            acc = add(acc, __shfl_xor_sync(gmask, acc, 4));
-            res = acc;
-          } else {
-            res = -0.0;            // numpy >= 2 starts small pairwise blocks from -0.0
-          }
-          for (int i = full; i < m; ++i) res = add(res, p[1 + i]);
-          sum = add(p[0], res);
-        }
-        if (l8 == 0) y[r] = ACCUM ? add(y[r], sum) : sum;
+        c[j] = k < ncnt ? ld_hint(col + nb.z + k, pol) : 0;
+        v[j] = k < ncnt ? ld_hint(val + nb.z + k, pol) : 0.0;
       }
     }
     __syncwarp();
-    r0 = n0;
-    r1 = n1;
-    e0 = f0;
-    e1 = f1;
+    if (!leaf) {
+      for (int r = b.x + lane; r < b.y; r += 32) {
+        if (r != b.x + lane) {   // tiles of > 32 rows (rows of < 12 entries)
+          rs = __ldg(off + r);
+          re = __ldg(off + r + 1);
+        }
+        const double sum = csr_row_sum_serial(prod + (rs - b.z), re - rs);
+        y[r] = ACCUM ? add(y[r], sum) : sum;
+      }
+    } else if (lane < b.y) {
+      scr[-b.x - 1 + lane] = pairwise_block(prod + (rs - b.z), re - rs);
+    }
+    __syncwarp();
+    b = nb;
+    nb = nnb;
+  }
+}
+
+__device__ __forceinline__ int pw_split_(int n) {
+  const int n2 = n / 2;
+  return n2 - n2 % 8;
+}
+// numpy's pairwise recursion over n > 128 addends, its leaves' sums taken
+// in order from ls[k...]
+__device__ double pw_replay(int n, const double* __restrict__ ls, int& k) {
+  if (n <= 128) return ls[k++];
+  const int n2 = pw_split_(n);
+  const double a = pw_replay(n2, ls, k);
+  const double b = pw_replay(n - n2, ls, k);
+  return add(a, b);
+}
+
+// one thread per long row: y = p[first] + pairwise(leaf sums)
+template <bool ACCUM>
+__global__ void csr_leaf_combine(const int* __restrict__ plan, const int* __restrict__ off,
+                                 const int* __restrict__ col, const double* __restrict__ val,
+                                 const double* __restrict__ x, double* __restrict__ y,
+                                 const int* guard) {
+  if (guard && *guard) return;
+  const int64_t nlong = __ldg(plan + 2);
+  const int* __restrict__ lr = plan + __ldg(plan + 4);
+  const double* scr = reinterpret_cast<const double*>(plan + __ldg(plan + 5));
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nlong;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = __ldg(lr + 2 * i);
+    int k = __ldg(lr + 2 * i + 1);
+    const int first = __ldg(off + r);
+    const int m = __ldg(off + r + 1) - first - 1;
+    const double p0 = mul(__ldg(val + first), ld_gather(x + __ldg(col + first)));
+    const double sum = add(p0, pw_replay(m, scr, k));
+    y[r] = ACCUM ? add(y[r], sum) : sum;
   }
 }
 
@@ -1131,38 +1205,42 @@ int launch_csr_tiles(int64_t nrows, int64_t ncols, const int* off, const int* co
                      const double* val, const int* tiles, int64_t ntiles, const int* perm,
                      const int64_t* bins, const double* x, double* y, bool accum,
                      const int* guard, cudaStream_t st) {
+  (void)perm;
   if (nrows == 0) return DS_OK;
-  const int64_t n_warp = bins[7] - bins[6], n_cta = bins[8] - bins[7];
-  const bool split = n_warp + n_cta > 0;
+  const int64_t nlong = bins[8] - bins[6];   // rows > 129 entries: leaf tiles + combine
   const bool win = x_window_begin(st, x, (size_t)ncols * 8);
-  cudaEvent_t joined = nullptr;
-  if (split) {   // rows > kLongRow on a side stream, launched first (fork / join)
-    cudaStream_t side;
-    cudaEvent_t fork;
-    int rc = aux_stream(&side, &fork, &joined);
-    if (rc) return rc;
-    DS_CUDA(cudaEventRecord(fork, st));
-    DS_CUDA(cudaStreamWaitEvent(side, fork, 0));
-    rc = launch_csr_long2(perm + bins[6], n_warp, perm + bins[7], n_cta, off, col, val, x, y,
-                          accum, guard, side);
-    if (rc) return rc;
-    DS_CUDA(cudaEventRecord(joined, side));
-  }
-  static int bps = -1;
+  static int bps = -1, na = 0;
   if (bps < 0) {
     const char* e = getenv("DS_CSR_TILE_CTAS");
-    bps = e ? atoi(e) : 6;
+    bps = e ? atoi(e) : 2;
+    na = getenv("DS_CSR_TILE_NA") ? 1 : 0;
   }
   int64_t blocks = min64(ceil_div(ntiles, kTileWarps), (int64_t)sm_count() * bps);
   if (blocks < 1) blocks = 1;
-  if (accum)
-    csr_tile_kernel<true><<<(unsigned)blocks, 32 * kTileWarps, 0, st>>>(ntiles, tiles, off, col,
-                                                                         val, x, y, guard);
-  else
-    csr_tile_kernel<false><<<(unsigned)blocks, 32 * kTileWarps, 0, st>>>(ntiles, tiles, off, col,
-                                                                          val, x, y, guard);
+#define DS_TILE(A, N)                                                                         \
+  do {                                                                                         \
+    if (bps >= 3)                                                                              \
+      csr_tile_kernel<A, N, 3><<<(unsigned)blocks, 32 * kTileWarps, 0, st>>>(tiles, off, col,  \
+                                                                             val, x, y, guard); \
+    else                                                                                       \
+      csr_tile_kernel<A, N, 2><<<(unsigned)blocks, 32 * kTileWarps, 0, st>>>(tiles, off, col,  \
+                                                                             val, x, y, guard); \
+  } while (0)
+  if (accum) {
+    if (na) DS_TILE(true, true); else DS_TILE(true, false);
+  } else {
+    if (na) DS_TILE(false, true); else DS_TILE(false, false);
+  }
+#undef DS_TILE
   DS_LAUNCH_CHECK("csr_tile_kernel");
-  if (split) DS_CUDA(cudaStreamWaitEvent(st, joined, 0));
+  if (nlong > 0) {
+    const unsigned g = (unsigned)min64(ceil_div(nlong, 128), (int64_t)sm_count() * 4);
+    if (accum)
+      csr_leaf_combine<true><<<g, 128, 0, st>>>(tiles, off, col, val, x, y, guard);
+    else
+      csr_leaf_combine<false><<<g, 128, 0, st>>>(tiles, off, col, val, x, y, guard);
+    DS_LAUNCH_CHECK("csr_leaf_combine");
+  }
   if (win) x_window_end(st);
   return DS_OK;
 }

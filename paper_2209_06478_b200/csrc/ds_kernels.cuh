@@ -163,7 +163,7 @@ constexpr int kCsrBinCount = 8;   // ds_csr_bins: 8 bins, 9 offsets
 // ds_csr_tiles: a tile boundary where off[r] crosses a multiple of
 // kCsrTileTarget and around every row longer than 129 entries, so a tile of
 // short rows holds < kCsrTileTarget + 130 <= kCsrTileMax entries (one warp)
-constexpr int kCsrTileMax = 256;
+constexpr int kCsrTileMax = 512;
 constexpr int kCsrTileTarget = kCsrTileMax - 130;
 
 }  // namespace ds

@@ -125,12 +125,15 @@ def csr_plan(m: CsrMatrix):
             with torch.cuda.device(m.device):
                 _native.call("ds_csr_bins", m.nrows, D.ptr(m.row_offsets), D.ptr(perm), bins,
                              D.stream(m.device))
-            tiles = torch.empty(m.nrows + 1, dtype=torch.int32, device=m.device)
-            nt = ctypes.c_int64()
+            # tile plan: row tiles + pairwise-leaf tiles of the long rows, with
+            # the per-SpMV leaf-sum scratch at its end (ds_csr_tiles)
+            cap = int(_native.load().ds_csr_tiles_capacity(m.nrows, m.nnz))
+            tiles = torch.empty(cap, dtype=torch.int32, device=m.device)
+            nt, used = ctypes.c_int64(), ctypes.c_int64()
             with torch.cuda.device(m.device):
-                _native.call("ds_csr_tiles", m.nrows, D.ptr(m.row_offsets), D.ptr(tiles),
-                             ctypes.byref(nt), D.stream(m.device))
-            m._cache["bins"] = (k, perm, list(bins), tiles[:int(nt.value) + 1].clone(),
+                _native.call("ds_csr_tiles", m.nrows, D.ptr(m.row_offsets), D.ptr(tiles), cap,
+                             ctypes.byref(nt), ctypes.byref(used), D.stream(m.device))
+            m._cache["bins"] = (k, perm, list(bins), tiles[:int(used.value)].clone(),
                                 int(nt.value))
     m._cache["plan"] = (k, lr, nl)
     m._cache["max_len"] = (k, ml)

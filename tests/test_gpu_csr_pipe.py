@@ -149,3 +149,37 @@ def test_empty_matrix_spmv_and_add(fmt):
         (ds.spmv_add if acc else ds.spmv)(ds.SERIAL, a, x, y)
         want = y0 + 0.0 if acc else np.zeros(n)
         assert y.data.cpu().numpy().tobytes() == want.tobytes(), (fmt, acc)
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_tiles_irregular_bitwise(seed):
+    """The entry-tile kernel of irregular matrices (csr_tile_kernel: products
+    entry-parallel, one lane per row summing in np.add.reduceat order) with
+    tiles of > 32 rows (runs of 1-entry rows), long runs of empty rows, every
+    pairwise boundary (m = 7 / 8 / 15 / 16 / 128 addends), rows just past
+    kLongRow (130..138: the first pairwise splits) and rows cut into
+    pairwise-leaf tiles up to 15000 entries -- bitwise."""
+    rng = np.random.default_rng(300 + seed)
+    n, nc = 6000, 50000
+    lengths = np.minimum(n, np.floor(6.0 * (1.0 - rng.random(n)) ** (-1 / 1.8))).astype(np.int64)
+    lengths = np.minimum(lengths, 2000)
+    lengths[100:900] = 1                               # ~380 rows per tile
+    lengths[1000:3000:2] = 0                           # empty rows inside tiles
+    lengths[3000:3100] = 0
+    for i, L in enumerate([8, 9, 16, 17, 128, 129, 130, 131, 137, 138, 256, 257, 1024, 1025,
+                           0, 2]):
+        lengths[4000 + 7 * i] = L
+    lengths[5000] = 15000                              # ~150 pairwise leaves, 38 leaf tiles
+    offs, cols, vals = random_csr(rng, n, nc, lengths)
+    x = rng.standard_normal(nc)
+    x[rng.random(nc) < 0.01] = -0.0
+    a = device_csr(offs, cols, vals, nc)
+    assert K_.csr_bins(a) is not None
+    xt = ds.DenseVector(torch.from_numpy(x).to(DEV))
+    for acc in (False, True):
+        y0 = rng.standard_normal(n)
+        y0[:50] = -0.0
+        want = oracle_y(offs, cols, vals, x, y0, acc)
+        y = ds.DenseVector(torch.from_numpy(y0.copy()).to(DEV))
+        (ds.spmv_add if acc else ds.spmv)(ds.SERIAL, a, xt, y)
+        assert y.data.cpu().numpy().tobytes() == want.tobytes(), ("tiles", acc)

@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(e)); return 1; } } while (0)
@@ -49,7 +50,8 @@ __global__ void init(int64_t nnz, int n, int* col, double* val) {
   }
 }
 
-// MODE 0 stream, 1 gather (col + x), 2 col + val + x
+// MODE 0 stream, 1 gather (col + x), 2 col + val + x, 3 = 2 with the x
+// gathers through L1 (__ldg) instead of L1::no_allocate
 template <int MODE, int U>
 __global__ void kern(int64_t nnz, const int* __restrict__ col, const double* __restrict__ val,
                      const double* __restrict__ x, double* out) {
@@ -72,7 +74,7 @@ __global__ void kern(int64_t nnz, const int* __restrict__ col, const double* __r
     } else {
       double g[U];
 #pragma unroll
-      for (int j = 0; j < U; ++j) g[j] = ldx(x + c[j]);
+      for (int j = 0; j < U; ++j) g[j] = MODE == 3 ? __ldg(x + c[j]) : ldx(x + c[j]);
 #pragma unroll
       for (int j = 0; j < U; ++j) acc += v[j] * g[j];
     }
@@ -115,12 +117,24 @@ int main() {
   init<<<sms * 8, 256>>>(nnz, n, col, val);
   CK(cudaMemset(x, 0, (size_t)n * 8));
   CK(cudaDeviceSynchronize());
-  const char* names[3] = {"stream(col+val)", "gather(col+x)", "col+val+x"};
-  const double bytes[3] = {12.0 * nnz, 4.0 * nnz, 12.0 * nnz};
+  const char* names[4] = {"stream(col+val)", "gather(col+x)", "col+val+x", "col+val+x(ldg)"};
+  const double bytes[4] = {12.0 * nnz, 4.0 * nnz, 12.0 * nnz, 12.0 * nnz};
   printf("{\"nnz\": %lld, \"n\": %d, \"sms\": %d, \"runs\": [\n", (long long)nnz, n, sms);
   bool first = true;
+  const bool quick = getenv("QUICK") != nullptr;
+  if (getenv("WINDOW")) {   // persisting L2 window over x, as the SpMV launcher sets it
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)n * 8);
+    cudaStreamAttrValue a = {};
+    a.accessPolicyWindow.base_ptr = x;
+    a.accessPolicyWindow.num_bytes = (size_t)n * 8;
+    a.accessPolicyWindow.hitRatio = 1.0f;
+    a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cudaStreamSetAttribute(0, cudaStreamAttributeAccessPolicyWindow, &a);
+  }
   for (int threads : {256, 512}) {
     for (int bpsm : {1, 2, 4, 8}) {
+      if (quick && !(threads == 256 && bpsm == 4)) continue;
       if (threads * bpsm > 2048) continue;
 #define RUN(M, U)                                                                              \
   {                                                                                            \
@@ -132,6 +146,7 @@ int main() {
     first = false;                                                                             \
   }
       RUN(0, 4) RUN(0, 8) RUN(1, 4) RUN(1, 8) RUN(1, 16) RUN(2, 4) RUN(2, 8) RUN(2, 16)
+      RUN(3, 4) RUN(3, 8) RUN(3, 16)
     }
   }
   printf("]}\n");
