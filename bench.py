@@ -570,11 +570,21 @@ def run(args, rank: int, world: int) -> int:
     from paper_2209_06478_b200 import solver as S
 
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # DS_BENCH_SAME_GPU=1: every rank on cuda:0 (exercises the N > 1 path on a
+    # one-GPU box: IPC peer memory between the ranks' contexts, gloo for the
+    # host-side collectives, stream-memop waits since the contexts time-slice)
+    same_gpu = world > 1 and os.environ.get("DS_BENCH_SAME_GPU") == "1"
+    if same_gpu:
+        local_rank = 0
+        os.environ.setdefault("DS_PEER_WAIT", "memop")
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if same_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     pk = peaks()
     peak = pk["hbm_gbs"]
     px, py, pz = procs_for(world)
