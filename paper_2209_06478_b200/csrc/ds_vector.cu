@@ -565,7 +565,8 @@ __device__ __forceinline__ void grid_barrier(unsigned* count, unsigned* gen) {
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(kVecBlock)
+template <int U, int MINB>
+__global__ void __launch_bounds__(kVecBlock, MINB)
     cg_update_direction_fused_kernel(int64_t n, double* x, double* r, double* p,
                                      const double* __restrict__ ap, ds_cg_scalars* s,
                                      double* history, const double* pap_parts,
@@ -584,9 +585,9 @@ __global__ void __launch_bounds__(kVecBlock)
   double2* r2 = reinterpret_cast<double2*>(r);
   double2* p2 = reinterpret_cast<double2*>(p);
   const double2* a2 = reinterpret_cast<const double2*>(ap);
-  double2 xv[kVecUnroll], rv[kVecUnroll], pv[kVecUnroll];
+  double2 xv[U], rv[U], pv[U];
 #pragma unroll
-  for (int u = 0; u < kVecUnroll; ++u) {
+  for (int u = 0; u < U; ++u) {
     const int64_t i = min64(gtid + u * stride, n2 - 1);
     xv[u] = x2[i];
     rv[u] = r2[i];
@@ -605,10 +606,10 @@ __global__ void __launch_bounds__(kVecBlock)
   const double alpha = rr / pap, nalpha = -alpha;
   const int it = s->iter + 1;
   double v = 0.0;
-  for (int64_t i0 = gtid; i0 < n2; i0 += stride * kVecUnroll) {
-    double2 av[kVecUnroll];
+  for (int64_t i0 = gtid; i0 < n2; i0 += stride * U) {
+    double2 av[U];
 #pragma unroll
-    for (int u = 0; u < kVecUnroll; ++u) {
+    for (int u = 0; u < U; ++u) {
       const int64_t i = min64(i0 + u * stride, n2 - 1);
       if (i0 != gtid) {   // the first sweep's x / r / p are already loaded
         xv[u] = x2[i];
@@ -618,7 +619,7 @@ __global__ void __launch_bounds__(kVecBlock)
       av[u] = a2[i];
     }
 #pragma unroll
-    for (int u = 0; u < kVecUnroll; ++u) {
+    for (int u = 0; u < U; ++u) {
       const int64_t i = i0 + u * stride;
       if (i < n2) {
         double2 xo, ro;
@@ -677,15 +678,15 @@ __global__ void __launch_bounds__(kVecBlock)
     }
   }
   if (converged || last) return;
-  for (int64_t i0 = gtid; i0 < n2; i0 += stride * kVecUnroll) {
+  for (int64_t i0 = gtid; i0 < n2; i0 += stride * U) {
 #pragma unroll
-    for (int u = 0; u < kVecUnroll; ++u) {
+    for (int u = 0; u < U; ++u) {
       const int64_t i = min64(i0 + u * stride, n2 - 1);
       rv[u] = __ldcg(r2 + i);
       pv[u] = p2[i];
     }
 #pragma unroll
-    for (int u = 0; u < kVecUnroll; ++u) {
+    for (int u = 0; u < U; ++u) {
       const int64_t i = i0 + u * stride;
       if (i < n2) {
         double2 po;
@@ -700,6 +701,7 @@ __global__ void __launch_bounds__(kVecBlock)
     p[i] = add(mul(1.0, __ldcg(r + i)), mul(beta, p[i]));
   }
 }
+
 
 }  // namespace ds
 
@@ -1067,11 +1069,14 @@ extern "C" int ds_cg_update_direction_deferred(int64_t n, double* x, double* r, 
   if (n < 2 || !aligned16(x, r, p, ap)) return DS_ERR_NOT_SUPPORTED;
   Workspace w0(reinterpret_cast<char*>(workspace));
   Workspace w1(reinterpret_cast<char*>(workspace) + kWorkspaceBytes);
+  // 2 CTAs of 256 threads per SM, 4 double2 per thread and sweep (measured
+  // against 3-4 CTAs/SM, unroll 1-2, and a single-sweep variant holding r and
+  // p in registers across the barrier: all 0.5-2 us per step slower)
   static int per_sm = -1;
+  const void* fn = reinterpret_cast<const void*>(cg_update_direction_fused_kernel<4, 2>);
   if (per_sm < 0) {
     int b = 0;
-    DS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &b, cg_update_direction_fused_kernel, kVecBlock, 0));
+    DS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, kVecBlock, 0));
     per_sm = b > 0 ? b : 1;
   }
   int64_t g = vec_grid(n);
@@ -1103,22 +1108,18 @@ extern "C" int ds_cg_update_direction_deferred(int64_t n, double* x, double* r, 
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    if (cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(cg_update_direction_fused_kernel),
-                            args) == cudaSuccess) {
+    if (cudaLaunchKernelExC(&cfg, fn, args) == cudaSuccess) {
       DS_LAUNCH_CHECK("cg_update_direction_fused_kernel");
       return DS_OK;
     }
     (void)cudaGetLastError();
   }
-  cudaError_t e = cudaLaunchCooperativeKernel(
-      reinterpret_cast<const void*>(cg_update_direction_fused_kernel), dim3((unsigned)g),
-      dim3(kVecBlock), args, 0, st);
+  cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)g), dim3(kVecBlock), args, 0, st);
   if (e != cudaSuccess) {
     // not capturable / not supported here: the grid is co-resident by
     // construction, so a plain launch keeps the barrier safe
     (void)cudaGetLastError();
-    cg_update_direction_fused_kernel<<<(unsigned)g, kVecBlock, 0, st>>>(
-        n, x, r, p, ap, s, history, pap_parts, pap_count, rr_parts, bar_count, bar_gen);
+    DS_CUDA(cudaLaunchKernel(fn, dim3((unsigned)g), dim3(kVecBlock), args, 0, st));
   }
   DS_LAUNCH_CHECK("cg_update_direction_fused_kernel");
   return DS_OK;

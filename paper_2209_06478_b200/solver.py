@@ -236,13 +236,12 @@ class CgEngine:
         with torch.cuda.device(dev):
             st = _device.stream(dev)
             self.setup(st)
-            sc = self.scalars()
-            if sc.done:
-                return sc
             if use_graph is None:
                 use_graph = self.max_iters >= 16
-            if use_graph and _WHILE_STEPS > 0:
-                # the whole loop on the device: one graph launch, one readback
+            # the whole loop on the device (one graph launch, one readback);
+            # no readback first: a solve that setup already finished (b = 0,
+            # max_iters = 0) makes every step a no-op
+            if use_graph and _WHILE_STEPS > 0 and getattr(self, "_while", None) is not False:
                 if getattr(self, "_while", None) is None:
                     self._capture_while(_WHILE_STEPS)
                 if self._while:
@@ -251,6 +250,9 @@ class CgEngine:
                         return self.scalars()
                     finally:
                         self.release_l2(st)
+            sc = self.scalars()
+            if sc.done:
+                return sc
             c = chunk or (8 if use_graph else 4)
             if use_graph and self.graph is None:
                 self._capture(c)
@@ -544,6 +546,26 @@ def _pinned(eng, name: str, n: int):
     return buf
 
 
+def _pinned_result(eng, k: int, n: int):
+    """A pinned host buffer for a result array handed to the caller: a pool
+    per partition on the engine; an entry is reused only once every numpy
+    array (or view) over it has been released -- the numpy arrays reference a
+    ctypes view of the buffer, whose reference count tells.  The ctypes view
+    keeps the pinned tensor alive, so a returned array outlives the engine."""
+    import sys
+    import torch
+    pool = eng.__dict__.setdefault("_xpool", {}).setdefault((k, n), [])
+    for ent in pool:
+        if sys.getrefcount(ent[1]) == 2:   # only the pool entry and the argument
+            return ent
+    t = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    c = (ctypes.c_double * n).from_address(t.data_ptr())
+    c._keep = t
+    ent = (t, c)
+    pool.append(ent)
+    return ent
+
+
 def _pinned_copy(eng, name: str, dst, src_np) -> None:
     """Host numpy -> device tensor through a cached pinned staging buffer
     (DS_PAGEABLE_STAGING=1: a direct pageable copy -- faster in a fresh
@@ -554,8 +576,14 @@ def _pinned_copy(eng, name: str, dst, src_np) -> None:
         return
     buf = _pinned(eng, name, dst.numel())
     torch.cuda.current_stream(dst.device).synchronize()   # buffer free for reuse
-    buf.copy_(torch.from_numpy(np.ascontiguousarray(src_np)))   # multi-threaded host copy
-    dst.copy_(buf, non_blocking=True)
+    src = torch.from_numpy(np.ascontiguousarray(src_np))
+    # in 4 pieces: the DMA of a piece overlaps the host copy of the next
+    n = dst.numel()
+    step = max(1 << 16, -(-n // 4))
+    for a in range(0, n, step):
+        b = min(n, a + step)
+        buf[a:b].copy_(src[a:b])   # multi-threaded host copy
+        dst[a:b].copy_(buf[a:b], non_blocking=True)
 
 
 def _reload(eng: CgEngine, bs, x0s) -> None:
@@ -598,13 +626,14 @@ def _cg_distributed(op, bs, x0s, tol, max_iters, use_graph):
         it, hist, conv = _finish(eng, sc)
     host = bs[0].space == MemorySpace.HOST
     if host and not os.environ.get("DS_PAGEABLE_STAGING"):
-        outs = [_pinned(eng, f"x{k}", pt.n) for k, pt in enumerate(parts)]
-        for o, pt in zip(outs, parts):
-            o.copy_(pt.x, non_blocking=True)
+        # fresh arrays (the reference returns new ones) in pinned memory: the
+        # D2H lands in the returned array itself (no host-side copy, no page
+        # faults on freshly allocated pages)
+        outs = [_pinned_result(eng, k, pt.n) for k, pt in enumerate(parts)]
+        for (t, _), pt in zip(outs, parts):
+            t.copy_(pt.x, non_blocking=True)
         torch.cuda.synchronize(eng.dev)
-        # fresh arrays (the reference returns new ones), filled by torch's
-        # multi-threaded host copy
-        xs = [DenseVector(torch.empty_like(o).copy_(o).numpy()) for o in outs]
+        xs = [DenseVector(np.ctypeslib.as_array(c)) for _, c in outs]
     elif host:   # fresh arrays (the reference returns new ones): one D2H each
         xs = [DenseVector(pt.x.cpu().numpy()) for pt in parts]
     else:

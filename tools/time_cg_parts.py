@@ -29,8 +29,23 @@ dirn = lambda: lib.ds_cg_direction_deferred(pt.n, eng._p(pt.r), eng._p(pt.p), s,
 fused = lambda: lib.ds_cg_update_direction_deferred(pt.n, eng._p(pt.x), eng._p(pt.r),  # noqa
                                                     eng._p(pt.p), eng._p(pt.ap), s, hist, ws, sp)
 variants = {"full": (spmv, upd, dirn), "fused": (spmv, fused), "no_direction": (spmv, upd), "spmv_only": (spmv,),
-            "spmv_direction": (spmv, dirn)}
+            "spmv_direction": (spmv, dirn), "tail_only": (fused,), "update_only": (upd,),
+            "direction_only": (dirn,)}
+cudart = ctypes.CDLL("libcudart.so.12") if False else None
+try:
+    from cuda.bindings import runtime as rt
+    attrs = {}
+    for nm in ("cudaDevAttrMaxPersistingL2CacheSize", "cudaDevAttrMaxAccessPolicyWindowSize",
+               "cudaDevAttrL2CacheSize"):
+        err, v = rt.cudaDeviceGetAttribute(getattr(rt.cudaDeviceAttr, nm), 0)
+        attrs[nm] = v
+    print(json.dumps(attrs), file=sys.stderr)
+except Exception as e:  # noqa: BLE001
+    print("attrs:", e, file=sys.stderr)
 out = {}
+if os.environ.get("PERSIST") == "1":   # the bench's persisting-L2 window over the CG vectors
+    vb = eng.parts[0].vec_block
+    print("persist rc", lib.ds_l2_persist(vb.data_ptr(), vb.numel() * 8, sp), file=sys.stderr)
 for name, fns in variants.items():
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=side):
@@ -49,4 +64,4 @@ for name, fns in variants.items():
         torch.cuda.synchronize()
         ts.append(a.elapsed_time(b) * 1e3 / 20)
     out[name] = round(statistics.median(ts), 2)
-print(json.dumps({"us_per_step": out}))
+print(json.dumps({"persist": os.environ.get("PERSIST") == "1", "us_per_step": out}))
