@@ -281,6 +281,34 @@ def sweep_powerlaw(ds, torch, dev, peak, cpu_threads: int = 0):
         gbs = b / (ms * 1e-3) / 1e9
         out[name] = {"ms": round(ms, 4), "gflops": round(2 * nnz / (ms * 1e-3) / 1e9, 1),
                      "gbs": round(gbs, 1), "frac": round(gbs / peak, 3)}
+    # the random-gather floor measured on this GPU in this run: the CSR
+    # SpMV's column + value stream and x gathers without the row structure
+    # (ds_probe_gather); the SpMVs are reported against it too
+    from paper_2209_06478_b200 import _native
+    lib = _native.load()
+    sink = torch.zeros(1, dtype=torch.float64, device=dev)
+    st = torch.cuda.current_stream(dev)
+    probe = lambda: _native.check(lib.ds_probe_gather(  # noqa: E731
+        nnz, csr.col_indices.data_ptr(), csr.values.data_ptr(), x.data.data_ptr(),
+        sink.data_ptr(), st.cuda_stream))
+    for _ in range(5):
+        probe()
+    ts = []
+    for _ in range(20):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        probe()
+        e1.record(st)
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    floor_ms = statistics.median(ts)
+    out["gather_floor"] = {
+        "ms": round(floor_ms, 4), "gathers_per_s": round(nnz / (floor_ms * 1e-3), 0),
+        "hbm_frac_ceiling_csr": round(csr_bytes(n, n, nnz) / (floor_ms * 1e-3) / 1e9 / peak, 3),
+        "what": "ds_probe_gather: stream cols + values, gather x[col] (no rows); every 8-B "
+                "random gather costs one L1 tag request, which bounds the irregular SpMV"}
+    for name in ("csr", "coo"):
+        out[name]["frac_of_gather_floor"] = round(floor_ms / out[name]["ms"], 3)
     if cpu_threads:
         a_host = (n, csr.row_offsets.cpu().numpy(), csr.col_indices.cpu().numpy(),
                   csr.values.cpu().numpy())

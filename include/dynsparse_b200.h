@@ -276,6 +276,14 @@ int64_t ds_csr_tiles_capacity(int64_t nrows, int64_t nnz);
 int ds_csr_tiles(int64_t nrows, const int32_t* row_offsets, int32_t* plan, int64_t capacity,
                  int64_t* ntiles, int64_t* words_used, void* stream);
 
+/* Measurement probe, not part of the path: streams col_indices + values and
+ * gathers x[col] for nnz entries (no row structure), a running sum per
+ * thread (sink is written only in a never-taken branch).  Timing it gives
+ * the random-gather floor of an irregular SpMV on this device (bench.py,
+ * BASELINE config 4).                                                      */
+int ds_probe_gather(int64_t nnz, const int32_t* col_indices, const double* values,
+                    const double* x, double* sink, void* stream);
+
 int ds_spmv(const ds_matrix* a, const double* x, double* y, int accumulate, void* stream);
 
 /* Persisting-L2 access-policy window over [base, base+bytes) for kernels

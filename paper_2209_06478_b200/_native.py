@@ -153,6 +153,7 @@ _SIGNATURES = {
     "ds_cg_direction_deferred": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "ds_l2_persist": (c_int, [c_vp, c_i64, c_vp]),
     "ds_l2_persist_reset": (c_int, [c_vp]),
+    "ds_probe_gather": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "ds_cg_update_direction_deferred": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                                                 c_vp, c_vp]),
     "ds_cg_update_gathered": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_int, c_vp,

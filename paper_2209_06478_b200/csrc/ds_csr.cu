@@ -1318,6 +1318,34 @@ int launch_csr(int64_t nrows, int64_t nnz, const int* off, const int* col, const
 
 }  // namespace ds
 
+namespace ds {
+// Measurement probe (not an SpMV): the traffic of a CSR SpMV of an irregular
+// matrix without its row structure -- stream col + val, gather x[col], one
+// running sum per thread.  Its time is the floor the random gathers set
+// (every gather is one L1 tag request); bench.py reports the power-law SpMV
+// against it beside the HBM roofline.
+__global__ void __launch_bounds__(256)
+    gather_probe_kernel(int64_t nnz, const int* __restrict__ col, const double* __restrict__ val,
+                        const double* __restrict__ x, double* sink) {
+  const uint64_t pol = policy_evict_first();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  double acc = 0.0;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nnz; b += 4 * stride) {
+    int c[4];
+    double v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t k = b + j * stride;
+      c[j] = k < nnz ? ld_hint(col + k, pol) : 0;
+      v[j] = k < nnz ? ld_hint(val + k, pol) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc += v[j] * ld_gather(x + c[j]);
+  }
+  if (acc == 1.2345e300) sink[0] = acc;   // keeps the loads
+}
+}  // namespace ds
+
 // ============================================================== C ABI ======
 using namespace ds;
 
@@ -1357,3 +1385,11 @@ extern "C" int ds_spmv_csr(int64_t nrows, int64_t ncols, int64_t nnz, const int3
                     accumulate != 0, nullptr, as_stream(stream));
 }
 
+extern "C" int ds_probe_gather(int64_t nnz, const int32_t* col_indices, const double* values,
+                               const double* x, double* sink, void* stream) {
+  if (nnz <= 0) return DS_OK;
+  const unsigned g = (unsigned)min64(ceil_div(nnz, 256), (int64_t)sm_count() * 4);
+  gather_probe_kernel<<<g, 256, 0, as_stream(stream)>>>(nnz, col_indices, values, x, sink);
+  DS_LAUNCH_CHECK("gather_probe_kernel");
+  return DS_OK;
+}
