@@ -136,3 +136,39 @@ def test_coo_long_runs_split_bitwise():
         torch.cuda.synchronize()
         want_y = want(nrows, ncols, rows, cols, vals, x, y0, acc)
         assert yd.data.cpu().numpy().tobytes() == want_y.tobytes(), acc
+
+
+TILE_CASES = dict(CASES)
+TILE_CASES["long_rows_and_gaps"] = lambda rng: (6000, 30000, np.concatenate([
+    rng.integers(0, 40, 2000), np.zeros(1500, np.int64),                    # a long gap
+    np.array([130, 511, 512, 513, 1500, 2049, 5000, 1, 0, 1]),              # chains, long runs
+    rng.integers(5, 20, 2490)]))
+
+
+@pytest.mark.parametrize("long_runs", [True, False])
+@pytest.mark.parametrize("name", sorted(TILE_CASES))
+def test_coo_descriptor_path_bitwise(name, long_runs, monkeypatch):
+    """Row-sorted COO through the descriptor (ds_spmv: the pipeline for rows
+    <= 27, else the warp-segment kernel, rows past the long-run threshold on
+    the side kernel -- or, without that plan, in the warp kernel): absent
+    rows, long gaps, rows around every tile size -- bitwise vs np.bincount."""
+    import paper_2209_06478_b200 as ds
+    from paper_2209_06478_b200 import kernels as K_
+    if not long_runs:
+        monkeypatch.setenv("DS_COO_NO_LONG_RUNS", "1")
+    rng = np.random.default_rng(zlib.crc32(name.encode()) + 7)
+    nrows, ncols, lengths = TILE_CASES[name](rng)
+    rows, cols, vals = sorted_coo(rng, nrows, ncols, lengths)
+    x = rng.standard_normal(ncols)
+    a = ds.CooMatrix(nrows, ncols, rows, cols, vals, ds.MemorySpace.DEVICE, DEV)
+    runs, cnt = K_.coo_long_runs(a)
+    assert (cnt > 0) == (long_runs and lengths.max() > int(_native.load().ds_coo_long_run_threshold()))
+    xt = ds.DenseVector(torch.from_numpy(x).to(DEV))
+    for acc in (False, True):
+        y0 = rng.standard_normal(nrows)
+        y0[::7] = -0.0
+        yd = ds.DenseVector(torch.from_numpy(y0.copy()).to(DEV))
+        (ds.spmv_add if acc else ds.spmv)(ds.SERIAL, a, xt, yd)
+        torch.cuda.synchronize()
+        ref = want(nrows, ncols, rows, cols, vals, x, y0, acc)
+        assert yd.data.cpu().numpy().tobytes() == ref.tobytes(), (name, acc)
