@@ -1070,8 +1070,10 @@ extern "C" int ds_cg_update_direction_deferred(int64_t n, double* x, double* r, 
   Workspace w0(reinterpret_cast<char*>(workspace));
   Workspace w1(reinterpret_cast<char*>(workspace) + kWorkspaceBytes);
   // 2 CTAs of 256 threads per SM, 4 double2 per thread and sweep (measured
-  // against 3-4 CTAs/SM, unroll 1-2, and a single-sweep variant holding r and
-  // p in registers across the barrier: all 0.5-2 us per step slower)
+  // against 3-4 CTAs/SM, unroll 1-2, a single-sweep variant holding r and p
+  // in registers across the barrier, and 64-register variants at 1-2 CTAs/SM
+  // that leave room for the next SpMV's programmatic CTAs: all 0.5-3 us per
+  // step slower)
   static int per_sm = -1;
   const void* fn = reinterpret_cast<const void*>(cg_update_direction_fused_kernel<4, 2>);
   if (per_sm < 0) {
