@@ -8,6 +8,10 @@ compute-sanitizer --tool memcheck --print-limit 20 python -m pytest tests/test_g
     tests/test_gpu_csr_pipe.py tests/test_gpu_coo_pipe.py tests/test_gpu_cg_fused.py \
     tests/test_gpu_hpcg.py tests/test_gpu_convert_paths.py tests/test_gpu_sort.py -q -x \
     -k "not hashes" > gpurun_out/memcheck.txt 2>&1
+# racecheck / synccheck: the solver's device WHILE-loop graph (a conditional
+# node) is replaced by chunked graph replays (DS_CG_WHILE_STEPS=0): under these
+# two tools the conditional-node solve faults inside the tool (memcheck runs it)
+export DS_CG_WHILE_STEPS=0
 compute-sanitizer --tool racecheck --print-limit 20 python -m pytest tests/test_gpu_csr_pipe.py \
     tests/test_gpu_coo_pipe.py tests/test_gpu_parity.py -q -x \
     -k "pipe or tiles or descriptor or spmv_and_spmv_add or long_rows or signed_zeros" \
