@@ -324,7 +324,9 @@ static int dia_pipe_launch(int64_t nrows, int64_t ncols, int ndiags, const int* 
 // Measured at 104^3 (one gpurun call, bench CG step / standalone SpMV):
 // 128 rows x 3 stages x 2 CTAs/SM 53.7 / 41.2 us, 256 x 3 x 1 55.6 / 43.1,
 // 128 x 4 x 2 54.6 / 42.6, 64 x 3-4 x 4 59-62 / 46-47, 2 stages 67-69 in
-// the step (the programmatic-launch prefetch wants 3).  Round 2: an L2 bulk
+// the step (the programmatic-launch prefetch wants 3).  Round 2: x gathers
+// bypassing L1 (to free it for a 4th stage or a 3rd CTA) 48.9-61 us
+// standalone: the gathers need L1 (~70% hits).  An L2 bulk
 // prefetch one / two ring rounds beyond the next copy (cp.async.bulk.prefetch.L2)
 // was slower: 40.9 -> 44.9 / 47.4 us standalone.  With the x windows
 // (>= 4M rows) 256 x 3 x 1 (192^3: 266 us vs 270).
