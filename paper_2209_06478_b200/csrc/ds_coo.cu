@@ -540,7 +540,10 @@ static int coo_pipe_launch(int64_t nrows, int64_t nnz, const int* rows, const in
   switch (cfgi) {
     // measured at 104^3 (tools/sweep_coo.sh): 64 threads x 1024 entries x 2
     // stages x 6 CTAs/SM 92.6 us; the register budget (~166 / thread at
-    // LMAX 27) caps residency, so the variants bound registers via MINB
+    // LMAX 27) caps residency, so the variants bound registers via MINB.
+    // Round 2 (tools/gpu_coosweep.sh, gpu_coo104.sh): 3-4 stages at 2-5
+    // CTAs/SM 121-192 us; row starts scattered to a per-tile slot table (two
+    // more barriers) instead of the per-row binary search 127 us -- rejected
     case 0: DS_COOP(64, 1024, 2, 6);
     case 1: DS_COOP(128, 2048, 2, 3);
     case 2: DS_COOP(128, 1536, 2, 4);
