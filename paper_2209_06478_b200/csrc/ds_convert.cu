@@ -1232,6 +1232,11 @@ extern "C" int ds_csr_tiles(int64_t nrows, const int32_t* row_offsets, int32_t* 
   const int64_t LR = LV + 2 * nleaves;
   const int64_t SCR = (LR + 2 * nlong + 1) & ~int64_t(1);
   const int64_t used = SCR + 2 * nleaves;
+  if (used > (int64_t)INT32_MAX) {   // the header holds int32 word offsets
+    cudaFreeAsync(tmp, st);
+    set_error("ds_csr_tiles: a plan of %lld words exceeds int32 offsets", (long long)used);
+    return DS_ERR_NOT_SUPPORTED;
+  }
   if (used > capacity) {   // cannot happen with ds_csr_tiles_capacity
     cudaFreeAsync(tmp, st);
     set_error("ds_csr_tiles: plan needs %lld words", (long long)used);
