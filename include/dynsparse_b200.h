@@ -481,6 +481,23 @@ int ds_symgs_ell(int64_t nrows, int32_t width, const int32_t* color_rows,
                  const int64_t* color_start, int ncolors, const int32_t* ell_cols,
                  const double* ell_vals, const int32_t* ell_len, const double* diag,
                  const double* r, double* x, void* stream);
+/* Offset ELL (the sweep without column indices): for an operator whose
+ * off-diagonals fall on <= 32 distinct offsets (col - row, ascending in
+ * `offsets`, padded with 0 to `width` = 26 or 32), slot q of colour-ordered
+ * position k is offset q: oell_vals[q * nrows + k] (0.0 where absent), mask[k]
+ * bit q = present, diag[k].  Same arithmetic as ds_symgs_ell, operation for
+ * operation; 8 B per slot streamed instead of 12.  The fill returns
+ * DS_ERR_NOT_SUPPORTED if a row holds an offset outside the list.  The fill
+ * takes the offsets in DEVICE memory, the sweep in HOST memory (they travel
+ * as a kernel parameter).                                                  */
+int ds_symgs_oell_fill(int64_t nrows, int32_t width, const int32_t* offsets,
+                       const int32_t* row_offsets, const int32_t* cols, const double* values,
+                       const int32_t* color_rows, double* oell_vals, uint32_t* mask,
+                       double* diag, void* stream);
+int ds_symgs_oell(int64_t nrows, int32_t width, const int32_t* offsets_host,
+                  const int32_t* color_rows, const int64_t* color_start, int ncolors,
+                  const double* oell_vals, const uint32_t* mask, const double* diag,
+                  const double* r, double* x, void* stream);
 /* Device-resident PCG (ComputeCG_ref with z = M r): the host writes the block
  * after setup; each iteration is spmv(p) -> ds_dot(p,Ap -> &pap) ->
  * ds_pcg_alpha -> ds_pcg_axpy(x += alpha p) -> ds_pcg_axpy(r -= alpha Ap) ->

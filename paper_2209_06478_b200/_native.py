@@ -125,6 +125,10 @@ _SIGNATURES = {
                                   c_vp]),
     "ds_symgs_ell": (c_int, [c_i64, c_i32, c_vp, P_i64, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                              c_vp]),
+    "ds_symgs_oell_fill": (c_int, [c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                   c_vp, c_vp]),
+    "ds_symgs_oell": (c_int, [c_i64, c_i32, c_vp, c_vp, P_i64, c_int, c_vp, c_vp, c_vp, c_vp,
+                              c_vp, c_vp]),
     "ds_pcg_alpha": (c_int, [c_vp, c_vp]),
     "ds_pcg_check": (c_int, [c_vp, c_vp, c_vp]),
     "ds_pcg_beta": (c_int, [c_vp, c_vp]),

@@ -233,6 +233,125 @@ static int symgs_ell_launch(unsigned g, int64_t nrows, int64_t k0, int64_t k1,
   return DS_OK;
 }
 
+// ---- offset ELL: the ELL sweep without column indices --------------------
+// For an operator whose off-diagonals fall on at most 32 distinct offsets
+// (col - row; the 27-point stencil: 26), slot q of every row is offset q
+// (ascending), its value at [q * n + k] (colour-ordered position k, 0.0 where
+// the row has no entry there) and a per-position presence mask says which
+// slots the row holds.  The column is i + off[q], so the sweep streams 8 B per
+// slot instead of the ELL's 12 (level 0 of the 104^3 hierarchy: 243 instead of
+// 365 MB per colour pass pair).  Slots are visited in ascending offset = the
+// CSR row's stored (ascending column) order and absent ones are selected
+// away, so the arithmetic is the ELL / CSR walk's operation for operation.
+__global__ void oell_fill_kernel(int64_t n, int W, const int* __restrict__ offs,
+                                 const int* __restrict__ rows, const int* __restrict__ off,
+                                 const int* __restrict__ col, const double* __restrict__ val,
+                                 double* ovals, unsigned* mask, double* diag, int* bad) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int i = rows[k];
+    unsigned m = 0;
+    double d = 0.0;
+    for (int q = 0; q < W; ++q) ovals[(int64_t)q * n + k] = 0.0;
+    int q = 0;
+    for (int e = off[i]; e < off[i + 1]; ++e) {
+      const int j = col[e];
+      if (j == i) {
+        d = val[e];
+        continue;
+      }
+      const int o = j - i;
+      while (q < W && offs[q] < o) ++q;   // columns ascend, so does the slot
+      if (q == W || offs[q] != o || (m >> q) & 1u) {
+        *bad = 1;
+        break;
+      }
+      ovals[(int64_t)q * n + k] = val[e];
+      m |= 1u << q;
+    }
+    mask[k] = m;
+    diag[k] = d;
+  }
+}
+
+struct OellOffsets {
+  int o[32];
+};
+
+template <int W, int CH>
+__global__ void __launch_bounds__(128, 8) symgs_oell_kernel(
+    int64_t n, int64_t k0, int64_t k1, const OellOffsets offs,
+    const int* __restrict__ rows, const double* __restrict__ ovals,
+    const unsigned* __restrict__ mask, const double* __restrict__ diag,
+    const double* __restrict__ r, double* x) {
+  static_assert(W % CH == 0, "chunk must divide the width");
+  int64_t k = k0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t k_first = k;
+  int i = 0;
+  unsigned m = 0;
+  double dk = 1.0;
+  double a0[CH];
+  if (k < k1) {   // static matrix data only (before the programmatic wait)
+    i = rows[k];
+    m = mask[k];
+    dk = diag[k];
+#pragma unroll
+    for (int q = 0; q < CH; ++q) a0[q] = __ldg(ovals + (int64_t)q * n + k);
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
+  const int ni = (int)n;
+  for (; k < k1; k += (int64_t)gridDim.x * blockDim.x) {
+    if (k != k_first) {
+      i = rows[k];
+      m = mask[k];
+      dk = diag[k];
+#pragma unroll
+      for (int q = 0; q < CH; ++q) a0[q] = __ldg(ovals + (int64_t)q * n + k);
+    }
+    double s = r[i];
+#pragma unroll
+    for (int c0 = 0; c0 < W; c0 += CH) {
+      double a[CH], xv[CH];
+#pragma unroll
+      for (int q = 0; q < CH; ++q) {
+        const int c = i + offs.o[c0 + q];   // kernel parameter: constant bank
+        xv[q] = x[min(max(c, 0), ni - 1)];
+      }
+#pragma unroll
+      for (int q = 0; q < CH; ++q)
+        a[q] = c0 == 0 ? a0[q] : __ldg(ovals + (int64_t)(c0 + q) * n + k);
+#pragma unroll
+      for (int q = 0; q < CH; ++q) {
+        const double t = __dadd_rn(s, -__dmul_rn(a[q], xv[q]));
+        s = (m >> (c0 + q)) & 1u ? t : s;
+      }
+    }
+    x[i] = __ddiv_rn(s, dk);
+  }
+}
+
+template <int W, int CH>
+static int symgs_oell_launch(unsigned g, int64_t nrows, int64_t k0, int64_t k1,
+                             const OellOffsets& offs,
+                             const int32_t* rows, const double* ovals, const unsigned* mask,
+                             const double* diag, const double* r, double* x, cudaStream_t st) {
+  static int no_pdl = -1;
+  if (no_pdl < 0) no_pdl = getenv("DS_NO_PDL") ? 1 : 0;
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(g);
+  lc.blockDim = dim3(128);
+  lc.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = no_pdl ? 0 : 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  DS_CUDA(cudaLaunchKernelEx(&lc, symgs_oell_kernel<W, CH>, nrows, k0, k1, offs, rows, ovals,
+                             mask, diag, r, x));
+  return DS_OK;
+}
+
 // ---- device-resident PCG scalars (ComputeCG_ref's scalar recurrences) ------
 // Tiny single-thread kernels carry the scalar recurrences so an iteration
 // never returns to the host and can be captured as a CUDA graph; every
@@ -456,5 +575,59 @@ extern "C" int ds_mg_prolong(int64_t ncoarse, const int32_t* f2c, const double* 
   if (ncoarse <= 0) return DS_OK;
   prolong_kernel<<<grid_n(ncoarse), 256, 0, as_stream(stream)>>>(ncoarse, f2c, xc, x);
   DS_LAUNCH_CHECK("prolong_kernel");
+  return DS_OK;
+}
+
+extern "C" int ds_symgs_oell_fill(int64_t nrows, int32_t width, const int32_t* offsets,
+                                  const int32_t* row_offsets, const int32_t* cols,
+                                  const double* values, const int32_t* color_rows,
+                                  double* oell_vals, uint32_t* mask, double* diag, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  if (nrows <= 0) return DS_OK;
+  if (width != 26 && width != 32) {
+    set_error("ds_symgs_oell_fill: width %d must be 26 or 32", width);
+    return DS_ERR_NOT_SUPPORTED;
+  }
+  int* bad = nullptr;
+  DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&bad), sizeof(int), st));
+  DS_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
+  oell_fill_kernel<<<grid_n(nrows), 256, 0, st>>>(nrows, width, offsets, color_rows, row_offsets,
+                                                   cols, values, oell_vals, mask, diag, bad);
+  DS_LAUNCH_CHECK("oell_fill_kernel");
+  int h = 0;
+  DS_CUDA(cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+  DS_CUDA(cudaFreeAsync(bad, st));
+  DS_CUDA(cudaStreamSynchronize(st));
+  if (h) {
+    set_error("ds_symgs_oell_fill: a row holds an offset outside the list (or a duplicate)");
+    return DS_ERR_NOT_SUPPORTED;
+  }
+  return DS_OK;
+}
+
+extern "C" int ds_symgs_oell(int64_t nrows, int32_t width, const int32_t* offsets_host,
+                             const int32_t* color_rows, const int64_t* color_start, int ncolors,
+                             const double* oell_vals, const uint32_t* mask, const double* diag,
+                             const double* r, double* x, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  if (width != 26 && width != 32) {
+    set_error("ds_symgs_oell: width %d must be 26 or 32", width);
+    return DS_ERR_NOT_SUPPORTED;
+  }
+  OellOffsets offsets{};
+  for (int q = 0; q < width; ++q) offsets.o[q] = offsets_host[q];
+  int rc = DS_OK;
+  for (int q = 0; q < 2 * ncolors - 1; ++q) {
+    const int c = sweep_color(q, ncolors);
+    const int64_t k0 = color_start[c], k1 = color_start[c + 1];
+    if (k1 <= k0) continue;
+    const unsigned g = (unsigned)min64(ceil_div(k1 - k0, 128), (int64_t)sm_count() * 32);
+    rc = width == 26 ? symgs_oell_launch<26, 13>(g, nrows, k0, k1, offsets, color_rows, oell_vals,
+                                                 mask, diag, r, x, st)
+                     : symgs_oell_launch<32, 8>(g, nrows, k0, k1, offsets, color_rows, oell_vals,
+                                                mask, diag, r, x, st);
+    if (rc) return rc;
+  }
+  DS_LAUNCH_CHECK("symgs_oell_kernel");
   return DS_OK;
 }

@@ -63,6 +63,7 @@ class MgLevel:
     x: object = None
     axf: object = None
     ell: tuple | None = None    # (width, cols, vals, len, diag) colour-ordered ELL
+    oell: tuple | None = None   # (width, host offsets, vals, mask, diag) offset ELL (no columns)
     op: object = None           # the level operator in the SpMV format
     desc: object = None         # cached ds_matrix descriptor of ``op``
 
@@ -81,16 +82,22 @@ class MgHierarchy:
               layout: str = "ell", spmv_format="dia") -> "MgHierarchy":
         """GenerateProblem + GenerateCoarseProblem: each coarse grid halves
         every dimension while all three stay even (at most ``nlevels``).
-        ``layout`` "ell" adds the colour-ordered ELL copy the sweep reads
-        (coalesced); "csr" sweeps the CSR operator directly.  The residual
+        ``layout`` "ell" adds the colour-ordered copy the sweep reads
+        (coalesced): on levels of >= 2^20 rows the offset ELL (slot q =
+        offset q, a presence mask, no column indices: 8 B per slot instead
+        of 12; 104^3 sweep 125 -> 110 us) when the off-diagonals fall on <= 32
+        offsets, else -- and on the latency-bound coarse levels, where it
+        measured slower (35 -> 44 us at 52^3) -- the ELL with columns;
+        "oell" / "ell-cols" force one of them; "csr" sweeps the CSR operator
+        directly.  The residual
         SpMVs (PCG's A p and the V-cycle's A z) run on the level operator
         converted to ``spmv_format`` -- the runtime format switch applied to
         HPCG (DIA streams the 27 diagonals at ~90% of HBM)."""
         from .datamove import convert
         from .formats import as_format_id
         fmt = as_format_id(spmv_format)
-        if layout not in ("ell", "csr"):
-            raise ValueError(f"layout must be 'ell' or 'csr', got {layout!r}")
+        if layout not in ("ell", "oell", "ell-cols", "csr"):
+            raise ValueError(f"layout must be 'ell', 'oell', 'ell-cols' or 'csr', got {layout!r}")
         import torch
         from . import _device
         dev = _device.require_cuda(device)
@@ -112,7 +119,9 @@ class MgHierarchy:
                 dims=(nx, ny, nz), a=part.a_full, color_rows=torch.from_numpy(rows).to(dev),
                 color_start=start, f2c=f2c, r=torch.empty(n, **f64), x=torch.empty(n, **f64),
                 axf=torch.empty(n, **f64)))
-            if layout == "ell":
+            if layout == "oell" or (layout == "ell" and n >= _OELL_MIN_ROWS):
+                h.levels[-1].oell = _oell(h.levels[-1], dev)
+            if layout in ("ell", "oell", "ell-cols") and h.levels[-1].oell is None:
                 h.levels[-1].ell = _ell(h.levels[-1], dev)
             h.levels[-1].op = part.a_full if fmt == FormatId.CSR else convert(part.a_full, fmt)
             if not coarsen:
@@ -132,6 +141,12 @@ class MgHierarchy:
         a = L.a
         cs = L.color_start.ctypes.data_as(_native.P_i64)
         st = self._stream() if st is None else st
+        if L.oell is not None:
+            w, of, ov, mk, dg = L.oell
+            _native.call("ds_symgs_oell", a.nrows, w, of.ctypes.data, L.color_rows.data_ptr(), cs,
+                         NCOLORS, ov.data_ptr(), mk.data_ptr(), dg.data_ptr(), r.data_ptr(),
+                         x.data_ptr(), st)
+            return
         if L.ell is not None:
             w, ec, ev, el, dg = L.ell
             _native.call("ds_symgs_ell", a.nrows, w, L.color_rows.data_ptr(), cs, NCOLORS,
@@ -178,6 +193,7 @@ class MgHierarchy:
 
 
 _ELL_WIDTHS = (8, 16, 26, 32)
+_OELL_MIN_ROWS = 1 << 20
 
 
 def _ell(L: MgLevel, dev):
@@ -202,6 +218,36 @@ def _ell(L: MgLevel, dev):
                  a.col_indices.data_ptr(), a.values.data_ptr(), L.color_rows.data_ptr(),
                  ec.data_ptr(), ev.data_ptr(), el.data_ptr(), dg.data_ptr(), st)
     return (width, ec, ev, el, dg)
+
+
+def _oell(L: MgLevel, dev):
+    """Offset-ELL copy of the level operator (ds_symgs_oell_fill): None when
+    its off-diagonals fall on more than 32 distinct offsets."""
+    import torch
+    from . import _device
+    a = L.a
+    n = a.nrows
+    ro = a.row_offsets.to(torch.int64)
+    rows = torch.repeat_interleave(torch.arange(n, device=dev), ro[1:] - ro[:-1])
+    d = a.col_indices.to(torch.int64) - rows
+    u = torch.unique(d[d != 0])   # ascending
+    del rows, d
+    if u.numel() > 32:
+        return None
+    width = 26 if u.numel() <= 26 else 32
+    offs = torch.zeros(width, dtype=torch.int32, device=dev)   # padding 0: never an off-diagonal
+    offs[:u.numel()] = u.to(torch.int32)
+    ov = torch.empty(width * n, dtype=torch.float64, device=dev)
+    mk = torch.empty(n, dtype=torch.int32, device=dev)
+    dg = torch.empty(n, dtype=torch.float64, device=dev)
+    rc = _native.load().ds_symgs_oell_fill(
+        n, width, offs.data_ptr(), a.row_offsets.data_ptr(), a.col_indices.data_ptr(),
+        a.values.data_ptr(), L.color_rows.data_ptr(), ov.data_ptr(), mk.data_ptr(),
+        dg.data_ptr(), _device.stream(dev))
+    if rc == _native.DS_ERR_NOT_SUPPORTED:
+        return None
+    _native.check(rc)
+    return (width, offs.cpu().numpy().copy(), ov, mk, dg)
 
 
 def _t(v):

@@ -25,12 +25,15 @@ def dev(a):
     return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(DEV)
 
 
-@pytest.mark.parametrize("layout", ["ell", "csr"])
+@pytest.mark.parametrize("layout", ["oell", "ell-cols", "ell", "csr"])
 @pytest.mark.parametrize("dims", [(8, 8, 8), (5, 6, 7), (16, 8, 4), (1, 1, 3), (2, 1, 1)])
 def test_symgs_bitwise(dims, layout):
     nx, ny, nz = dims
     h = hpcg.MgHierarchy.build(nx, ny, nz, nlevels=1, device=DEV, layout=layout)
-    assert (h.levels[0].ell is not None) == (layout == "ell")
+    # "oell": the offset ELL (the stencil's off-diagonals fall on <= 26
+    # offsets); "ell" picks it only from 2^20 rows, the column ELL below
+    assert (h.levels[0].oell is not None) == (layout == "oell")
+    assert (h.levels[0].ell is not None) == (layout in ("ell-cols", "ell"))
     m = O.stencil_partition(nx, ny, nz).a_full
     rng = np.random.default_rng(sum(dims))
     r = rng.standard_normal(m.nrows)
@@ -43,7 +46,8 @@ def test_symgs_bitwise(dims, layout):
 
 
 @pytest.mark.parametrize("dims", [(16, 16, 16), (8, 12, 16)])
-@pytest.mark.parametrize("layout,fmt", [("ell", "dia"), ("csr", "csr"), ("ell", "coo")])
+@pytest.mark.parametrize("layout,fmt", [("ell", "dia"), ("csr", "csr"), ("ell", "coo"),
+                                        ("oell", "dia")])
 def test_vcycle_bitwise(dims, layout, fmt):
     h = hpcg.MgHierarchy.build(*dims, nlevels=4, device=DEV, layout=layout, spmv_format=fmt)
     levels = O.mg_levels(*dims, levels=4, fmt={"dia": O.DIA, "csr": O.CSR, "coo": O.COO}[fmt])
@@ -65,13 +69,13 @@ def test_symgs_large_level_layouts_agree():
     rng = np.random.default_rng(5)
     r, x = rng.standard_normal(m.nrows), rng.standard_normal(m.nrows)
     outs = []
-    for layout in ("ell", "csr"):
+    for layout in ("oell", "ell-cols", "csr"):
         h = hpcg.MgHierarchy.build(*dims, nlevels=1, device=DEV, layout=layout)
         xd = dev(x)
         for _ in range(3):
             hpcg.symgs(h, dev(r), xd)
         outs.append(xd.cpu().numpy())
-    assert outs[0].tobytes() == outs[1].tobytes()
+    assert outs[0].tobytes() == outs[1].tobytes() == outs[2].tobytes()
     ref = x.copy()
     O.symgs_colored(m, r, ref, O.stencil_colors(*dims))
     h = hpcg.MgHierarchy.build(*dims, nlevels=1, device=DEV)
@@ -80,15 +84,20 @@ def test_symgs_large_level_layouts_agree():
     assert xd.cpu().numpy().tobytes() == ref.tobytes()
 
 
-def test_symgs_signed_zero_and_padding():
-    """Padding slots never touch the arithmetic: r = -0 rows with x = -1
-    neighbours keep their signed zeros exactly like the CSR walk."""
+@pytest.mark.parametrize("layout", ["oell", "ell-cols"])
+def test_symgs_signed_zero_and_padding(layout):
+    """Padding / absent slots never touch the arithmetic: r = -0 rows with
+    x = -0 neighbours keep their signed zeros exactly like the CSR walk (the
+    offset ELL's absent slots hold 0.0 and gather real x values: both are
+    selected away by the presence mask)."""
     dims = (3, 3, 3)                      # corner rows have 7 entries, pad to 26
-    h = hpcg.MgHierarchy.build(*dims, nlevels=1, device=DEV)
-    assert h.levels[0].ell[0] == 26
+    h = hpcg.MgHierarchy.build(*dims, nlevels=1, device=DEV, layout=layout)
+    L = h.levels[0]
+    assert (L.oell if layout == "oell" else L.ell)[0] == 26
     m = O.stencil_partition(*dims).a_full
     r = np.full(m.nrows, -0.0)
     x = np.full(m.nrows, -0.0)
+    x[::5] = -1.0
     xd = dev(x)
     O.symgs_colored(m, r, x, O.stencil_colors(*dims))
     hpcg.symgs(h, dev(r), xd)
@@ -124,3 +133,26 @@ def test_pcg_max_iters_and_zero_rhs():
     assert np.allclose(res.residual_history, ref.history, rtol=1e-8, atol=0)
     z = hpcg.pcg(h, dev(np.zeros_like(b)))
     assert z.converged and z.iterations == 0 and not z.x.data.abs().sum().item()
+
+
+def test_symgs_offset_ell_at_hpcg_size():
+    """104^3 (the bench's level 0, >= 2^20 rows): the default layout takes the
+    offset ELL and its sweep is bitwise the column ELL's and the restatement's."""
+    dims = (104, 104, 104)
+    h = hpcg.MgHierarchy.build(*dims, nlevels=1, device=DEV)
+    assert h.levels[0].oell is not None and h.levels[0].ell is None
+    hc = hpcg.MgHierarchy.build(*dims, nlevels=1, device=DEV, layout="ell-cols")
+    rng = np.random.default_rng(104)
+    n = h.levels[0].nrows
+    r, x = rng.standard_normal(n), rng.standard_normal(n)
+    xa, xb = dev(x), dev(x)
+    for _ in range(2):
+        hpcg.symgs(h, dev(r), xa)
+        hpcg.symgs(hc, dev(r), xb)
+    assert xa.cpu().numpy().tobytes() == xb.cpu().numpy().tobytes()
+    m = O.stencil_partition(*dims).a_full
+    ref = x.copy()
+    cols = O.stencil_colors(*dims)
+    for _ in range(2):
+        O.symgs_colored(m, r, ref, cols)
+    assert xa.cpu().numpy().tobytes() == ref.tobytes()
