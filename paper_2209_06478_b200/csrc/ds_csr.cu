@@ -1014,31 +1014,26 @@ int launch_csr_binned(int64_t nrows, int64_t ncols, int64_t nnz, const int* off,
 
 // ------------------------------------------------------- irregular: tiles --
 // csr_tile_kernel: entry-parallel products, row-parallel exact sums, one WARP
-// per tile.  The rows are cut into tiles of consecutive rows holding at most
-// kCsrTileMax = 512 entries (ds_csr_tiles; every row longer than kLongRow is
-// a tile of its own and is skipped here -- the long-row kernels take it on a
-// side stream, concurrently).  Per tile each lane forms the products of 16
-// entries (consecutive lanes, consecutive entries: every warp gather
-// instruction carries 32 useful random x loads, no lane idles on a short
-// row) into the warp's shared-memory slice; then ONE LANE PER ROW sums its
-// products in np.add.reduceat order (p[first] + pairwise(rest): 8 register
-// accumulators for 8 <= m <= 128 addends, sequential from -0.0 below).  A
-// tile holds ~30 power-law rows, so the sum phase keeps most lanes busy; the
-// previous design (8 lanes per row, 256-entry tiles) spent ~4 warp
-// instructions per entry there (ncu r2j: 235M instructions, issue-bound at
-// 55% SM throughput) against the 217 us random-gather floor of
-// tools/gather_floor.cu.  Warps never wait for each other (no block
-// barrier); the next tile's bounds are loaded before the current tile's sums.
-// x carries a persisting L2 window (gathered ~13 times per entry at random on
-// the power-law matrix, L1 bypassed); the matrix streams with evict_first.
+// per tile, every row of the matrix in one grid (ds_csr_tiles plan).  Row
+// tiles hold consecutive rows of <= kLongRow entries, < kCsrTileMax = 512
+// entries in all; a longer row is cut into leaf tiles: np.add.reduceat sums a
+// row as p[first] + pairwise(rest), numpy's pairwise recursion splits n > 128
+// addends at n/2 - (n/2)%8, and its leaves (64..128 addends) are independent
+// -- up to 4 per tile, their sums go to the plan's scratch and
+// csr_leaf_combine replays each row's recursion over them.  Per tile each
+// lane forms the products of 16 entries (consecutive lanes, consecutive
+// entries: every warp gather instruction carries 32 useful random x loads) in
+// the warp's shared-memory slice; then ONE LANE PER ROW (or leaf) sums them in
+// numpy's order (8 register accumulators for 8 <= m <= 128 addends,
+// sequential from -0.0 below).  Round 1's 8 lanes per row spent ~4 warp
+// instructions per entry in the sums (235 M, issue-bound); now the kernel is
+// bound by the L1 data path: one tag request per random gather plus the
+// shared-memory wavefronts of the sums (profiles/r02/README.md), against the
+// ~220 us random-gather floor (ds_probe_gather).  Warps never wait for each
+// other; the next tile's columns and values are loaded before this tile's
+// sums.  The matrix streams with evict_first, x goes through L1.
 constexpr int kTileWarps = 8;
 constexpr int kTilePer = kCsrTileMax / 32;   // entries per lane
-
-__device__ __forceinline__ double ld_gather_na(const double* p) {
-  double v;
-  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
-  return v;
-}
 
 // numpy's pairwise sum of n <= 128 addends a[0..n): sequential from -0.0
 // below 8 (numpy >= 2), else 8 accumulators combined
@@ -1083,8 +1078,8 @@ __device__ __forceinline__ double csr_row_sum_serial(const double* p, int len) {
 // Tiles come from the ds_csr_tiles plan (one int4 per tile): row tiles are
 // summed one lane per row; leaf tiles (<= 4 pairwise leaves of one long row)
 // one lane per leaf into the plan's scratch, combined by csr_leaf_combine.
-template <bool ACCUM, bool NA, int MINB>
-__global__ void __launch_bounds__(32 * kTileWarps, MINB)
+template <bool ACCUM>
+__global__ void __launch_bounds__(32 * kTileWarps, 2)
     csr_tile_kernel(const int* __restrict__ plan, const int* __restrict__ off,
                     const int* __restrict__ col, const double* __restrict__ val,
                     const double* __restrict__ x, double* __restrict__ y, const int* guard) {
@@ -1130,7 +1125,7 @@ __global__ void __launch_bounds__(32 * kTileWarps, MINB)
     }
 #pragma unroll
     for (int j = 0; j < kTilePer; ++j)
-      if (j * 32 + lane < cnt) v[j] = mul(v[j], NA ? ld_gather_na(x + c[j]) : ld_gather(x + c[j]));
+      if (j * 32 + lane < cnt) v[j] = mul(v[j], ld_gather(x + c[j]));
 #pragma unroll
     for (int j = 0; j < kTilePer; ++j)
       if (j * 32 + lane < cnt) prod[j * 32 + lane] = v[j];
@@ -1209,29 +1204,16 @@ int launch_csr_tiles(int64_t nrows, int64_t ncols, const int* off, const int* co
   if (nrows == 0) return DS_OK;
   const int64_t nlong = bins[8] - bins[6];   // rows > 129 entries: leaf tiles + combine
   const bool win = x_window_begin(st, x, (size_t)ncols * 8);
-  static int bps = -1, na = 0;
-  if (bps < 0) {
-    const char* e = getenv("DS_CSR_TILE_CTAS");
-    bps = e ? atoi(e) : 2;
-    na = getenv("DS_CSR_TILE_NA") ? 1 : 0;
-  }
-  int64_t blocks = min64(ceil_div(ntiles, kTileWarps), (int64_t)sm_count() * bps);
+  // 2 CTAs of 8 warps per SM (128 registers: this tile's columns and
+  // values plus the next tile's in flight); 3 CTAs spill (452 vs 412 us)
+  int64_t blocks = min64(ceil_div(ntiles, kTileWarps), (int64_t)sm_count() * 2);
   if (blocks < 1) blocks = 1;
-#define DS_TILE(A, N)                                                                         \
-  do {                                                                                         \
-    if (bps >= 3)                                                                              \
-      csr_tile_kernel<A, N, 3><<<(unsigned)blocks, 32 * kTileWarps, 0, st>>>(tiles, off, col,  \
-                                                                             val, x, y, guard); \
-    else                                                                                       \
-      csr_tile_kernel<A, N, 2><<<(unsigned)blocks, 32 * kTileWarps, 0, st>>>(tiles, off, col,  \
-                                                                             val, x, y, guard); \
-  } while (0)
-  if (accum) {
-    if (na) DS_TILE(true, true); else DS_TILE(true, false);
-  } else {
-    if (na) DS_TILE(false, true); else DS_TILE(false, false);
-  }
-#undef DS_TILE
+  if (accum)
+    csr_tile_kernel<true><<<(unsigned)blocks, 32 * kTileWarps, 0, st>>>(tiles, off, col, val, x,
+                                                                         y, guard);
+  else
+    csr_tile_kernel<false><<<(unsigned)blocks, 32 * kTileWarps, 0, st>>>(tiles, off, col, val, x,
+                                                                          y, guard);
   DS_LAUNCH_CHECK("csr_tile_kernel");
   if (nlong > 0) {
     const unsigned g = (unsigned)min64(ceil_div(nlong, 128), (int64_t)sm_count() * 4);
