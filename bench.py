@@ -52,13 +52,15 @@ def procs_for(n: int) -> tuple[int, int, int]:
 
 
 def measured_traffic(kernel: str):
-    """DRAM bytes (read + write) per launch of `kernel` from the committed ncu
-    capture (profiles/r01/traffic.json), or None."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01", "traffic.json")) as fh:
-            return int(json.load(fh)[kernel]["dram_bytes_per_launch"])
-    except Exception:
-        return None
+    """DRAM bytes (read + write) per launch of `kernel` from the latest
+    committed ncu capture (profiles/r02/traffic.json, else r01), or None."""
+    for rnd in ("r02", "r01"):
+        try:
+            with open(os.path.join(ROOT, "profiles", rnd, "traffic.json")) as fh:
+                return int(json.load(fh)[kernel]["dram_bytes_per_launch"])
+        except Exception:
+            continue
+    return None
 
 
 def peaks() -> dict:
