@@ -21,7 +21,8 @@ from .errors import (
 )
 
 LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib")
-LIB_PATH = os.path.join(LIB_DIR, "libdynsparse_b200.so")
+LIB_PATH = os.environ.get("DS_NATIVE_LIB") or os.path.join(LIB_DIR, "libdynsparse_b200.so")
+# (DS_NATIVE_LIB: an alternate build of the same library, for A/B timing runs)
 
 DS_OK = 0
 DS_ERR_INVALID_ARGUMENT = 1

@@ -1174,7 +1174,10 @@ __device__ double pw_replay(int n, const double* __restrict__ ls, int& k) {
   return add(a, b);
 }
 
-// one thread per long row: y = p[first] + pairwise(leaf sums)
+// one thread per long row: y = p[first] + pairwise(leaf sums).  Measured
+// against (tools/gpu_ab.sh, one box): a warp per row replaying from leaf sums
+// staged in shared memory 398 vs 360 us per power-law SpMV, and that plus
+// rows of 130..512 entries summed leaf-parallel inside the tile kernel 391.
 template <bool ACCUM>
 __global__ void csr_leaf_combine(const int* __restrict__ plan, const int* __restrict__ off,
                                  const int* __restrict__ col, const double* __restrict__ val,

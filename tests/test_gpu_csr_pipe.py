@@ -166,8 +166,8 @@ def test_tiles_irregular_bitwise(seed):
     lengths[100:900] = 1                               # ~380 rows per tile
     lengths[1000:3000:2] = 0                           # empty rows inside tiles
     lengths[3000:3100] = 0
-    for i, L in enumerate([8, 9, 16, 17, 128, 129, 130, 131, 137, 138, 256, 257, 1024, 1025,
-                           0, 2]):
+    for i, L in enumerate([8, 9, 16, 17, 128, 129, 130, 131, 137, 138, 256, 257, 511, 512, 513,
+                           1024, 1025, 0, 2]):
         lengths[4000 + 7 * i] = L
     lengths[5000] = 15000                              # ~150 pairwise leaves, 38 leaf tiles
     offs, cols, vals = random_csr(rng, n, nc, lengths)
