@@ -656,7 +656,11 @@ __device__ __forceinline__ void csr_rowid_tile(int nrows, const int* __restrict_
 }
 
 // order check ((row, col) strictly increasing inside every row), index range
-// and the diagonal census of a CSR source
+// and the diagonal census of a CSR source.  Round 2 (tools/gpu_ab_conv.sh):
+// a row-uniform warp walk (a warp takes 32 rows one row at a time, no row-id
+// lookup per entry, 8 rows' columns in flight) was slower -- 192^3 census
+// 1.13 -> 1.26 ms wall, and with the matching slab-per-row DIA fill CSR->DIA
+// 1.46 -> 1.85 ms: latency-bound on the per-row chain.
 __global__ void __launch_bounds__(256)
     csr_census_tiles(int nrows, int ncols, const int* __restrict__ off,
                      const int* __restrict__ c, unsigned char* flags, int* bad) {
