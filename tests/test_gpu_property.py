@@ -1,0 +1,113 @@
+"""Property-based GPU parity (hypothesis): random small COO matrices -- any
+shape including empty, duplicates, explicit zeros and -0.0, unsorted entries
+-- converted to every format on the device and multiplied, against the
+oracle's restatement of the reference (datamove.py:208-295, kernels.py:102-198).
+
+Bitwise: the converted index structures and values (one hop from COO, a
+second hop from each result), the DIA fill-limit decision, CSR / DIA /
+canonical-COO SpMV and spmv_add.  Each example is a few
+kernel launches, so a hundred examples run in seconds.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+hypothesis = pytest.importorskip("hypothesis")
+from hypothesis import HealthCheck, given, settings  # noqa: E402
+from hypothesis import strategies as st  # noqa: E402
+
+import paper_2209_06478_b200 as ds  # noqa: E402
+from oracle import dynsparse_oracle as O  # noqa: E402
+
+DEV = torch.device("cuda", 0)
+FMT = {ds.FormatId.COO: O.COO, ds.FormatId.CSR: O.CSR, ds.FormatId.DIA: O.DIA}
+
+
+@st.composite
+def coo_inputs(draw):
+    nrows = draw(st.integers(0, 40))
+    ncols = draw(st.integers(0, 40))
+    nnz = draw(st.integers(0, 160)) if nrows and ncols else 0
+    seed = draw(st.integers(0, 2**31 - 1))
+    rng = np.random.default_rng(seed)
+    rows = rng.integers(0, max(nrows, 1), nnz)
+    cols = rng.integers(0, max(ncols, 1), nnz)
+    if nnz and draw(st.booleans()):            # force duplicates
+        k = rng.integers(0, nnz, nnz // 3 + 1)
+        rows[k], cols[k] = rows[0], cols[0]
+    vals = rng.standard_normal(nnz)
+    mask = rng.random(nnz)
+    vals[mask < 0.1] = 0.0
+    vals[(mask >= 0.1) & (mask < 0.2)] = -0.0
+    if nnz and draw(st.booleans()):            # exact cancellation inside a duplicate run
+        vals[0] = 1.5
+        vals[rng.integers(0, nnz)] = -1.5
+    return nrows, ncols, rows, cols, vals, seed
+
+
+def _host(m):
+    """Device container -> the oracle's record (int64 indices, f64 values)."""
+    if isinstance(m, ds.CooMatrix):
+        return O.coo(m.nrows, m.ncols, m.row_indices.cpu().numpy(), m.col_indices.cpu().numpy(),
+                     m.values.cpu().numpy())
+    if isinstance(m, ds.CsrMatrix):
+        return O.csr(m.nrows, m.ncols, m.row_offsets.cpu().numpy(), m.col_indices.cpu().numpy(),
+                     m.values.cpu().numpy())
+    return O.dia(m.nrows, m.ncols, m.offsets.cpu().numpy(), m.values.cpu().numpy())
+
+
+def _same(a, b):
+    if isinstance(a, O.OCoo):
+        return (np.array_equal(a.rows, b.rows) and np.array_equal(a.cols, b.cols)
+                and a.vals.tobytes() == b.vals.tobytes())
+    if isinstance(a, O.OCsr):
+        return (np.array_equal(a.offsets, b.offsets) and np.array_equal(a.cols, b.cols)
+                and a.vals.tobytes() == b.vals.tobytes())
+    return (np.array_equal(a.offsets, b.offsets) and a.values.shape == b.values.shape
+            and a.values.tobytes() == b.values.tobytes())
+
+
+@settings(max_examples=120, deadline=None, suppress_health_check=[HealthCheck.too_slow])
+@given(coo_inputs(), st.sampled_from([None, 0, 5, 40]))
+def test_convert_and_spmv_match_oracle(inp, fill_limit):
+    nrows, ncols, rows, cols, vals, seed = inp
+    src = ds.CooMatrix(nrows, ncols, rows, cols, vals, ds.MemorySpace.DEVICE, DEV)
+    osrc = O.coo(nrows, ncols, rows, cols, vals)
+    rng = np.random.default_rng(seed + 1)
+    x = rng.standard_normal(ncols)
+    x[rng.random(ncols) < 0.1] = -0.0
+    xt = ds.DenseVector(torch.from_numpy(x).to(DEV))
+    for target in (ds.FormatId.COO, ds.FormatId.CSR, ds.FormatId.DIA):
+        try:
+            want = O.convert(osrc, FMT[target], fill_limit)
+        except O.OracleFillOverflow:
+            with pytest.raises(ds.DiaFillOverflow):
+                ds.convert(src, target, fill_limit)
+            continue
+        got = ds.convert(src, target, fill_limit)
+        assert _same(_host(got), want), (target, nrows, ncols, len(vals))
+        # second hop from the device result (the canonical-CSR and DIA-source
+        # fast paths): every target again, default fill limit
+        for t2 in (ds.FormatId.COO, ds.FormatId.CSR, ds.FormatId.DIA):
+            try:
+                want2 = O.convert(want, FMT[t2])
+            except O.OracleFillOverflow:
+                with pytest.raises(ds.DiaFillOverflow):
+                    ds.convert(got, t2)
+                continue
+            assert _same(_host(ds.convert(got, t2)), want2), (target, t2)
+        # SpMV / spmv_add of the converted matrix: bitwise against the oracle
+        # (COO: the canonical, row-sorted order -> np.bincount's sums)
+        for acc in (False, True):
+            y0 = rng.standard_normal(nrows)
+            y0[::3] = -0.0
+            yw = y0.copy()
+            (O.spmv_add if acc else O.spmv)(want, x, yw)
+            yd = ds.DenseVector(torch.from_numpy(y0.copy()).to(DEV))
+            (ds.spmv_add if acc else ds.spmv)(ds.SERIAL, got, xt, yd)
+            assert yd.data.cpu().numpy().tobytes() == yw.tobytes(), (target, acc)
