@@ -111,3 +111,61 @@ def test_convert_and_spmv_match_oracle(inp, fill_limit):
             yd = ds.DenseVector(torch.from_numpy(y0.copy()).to(DEV))
             (ds.spmv_add if acc else ds.spmv)(ds.SERIAL, got, xt, yd)
             assert yd.data.cpu().numpy().tobytes() == yw.tobytes(), (target, acc)
+
+
+@settings(max_examples=30, deadline=None, suppress_health_check=[HealthCheck.too_slow])
+@given(st.integers(2, 9), st.integers(2, 9), st.integers(2, 9), st.integers(1, 2),
+       st.integers(1, 2), st.integers(1, 2),
+       st.sampled_from(["coo", "csr", "dia"]), st.sampled_from(["coo", "csr"]),
+       st.booleans())
+def test_stencil_decompositions_match_oracle(nx, ny, nz, px, py, pz, lf, rf, use_graph):
+    """Random 27-point decompositions generated on the device: each partition
+    bitwise equal to the oracle's generator, the split's distributed SpMV
+    bitwise against the oracle's in the same formats (local part COO / CSR /
+    DIA, remote COO / CSR), and the distributed
+    CG against the oracle's (iterations +-1, history within 1e-8, x within
+    1e-8) -- the reference's stencil.py:143-319 and solver.py:120-189."""
+    spec = ds.GridSpec(nx, ny, nz, px, py, pz)
+    prob = ds.generate_problem(spec, space=ds.MemorySpace.DEVICE, device=DEV)
+    oparts = O.stencil_problem(nx, ny, nz, px, py, pz)
+    n = spec.local_points
+    splits, osplits = [], []
+    for k, (part, op) in enumerate(zip(prob.partitions, oparts)):
+        a = _host(part.a_full)
+        assert np.array_equal(a.offsets, op.a_full.offsets)
+        assert np.array_equal(a.cols, op.a_full.cols)
+        assert a.vals.tobytes() == op.a_full.vals.tobytes()
+        sp = ds.split_local_remote(prob, k)
+        if lf != "csr":
+            ds.convert_inplace(sp.local, ds.FormatId[lf.upper()])
+        if rf != "csr":
+            ds.convert_inplace(sp.remote, ds.FormatId[rf.upper()])
+        splits.append(sp)
+        oloc, orem = O.split(op)
+        # the oracle's parts in the same formats (the remote part of a
+        # partition without ghosts is empty in any format)
+        osplits.append((O.convert(oloc, FMT[ds.FormatId[lf.upper()]]),
+                        O.convert(orem, FMT[ds.FormatId[rf.upper()]])))
+    rng = np.random.default_rng(nx * 100 + ny * 10 + nz)
+    xs_h = []
+    for op in oparts:
+        x = np.zeros(op.a_full.ncols)
+        x[:n] = rng.standard_normal(n)
+        xs_h.append(x)
+    xs = [ds.DenseVector(torch.from_numpy(x.copy()).to(DEV)) for x in xs_h]
+    ys = [ds.DenseVector.zeros(n, ds.MemorySpace.DEVICE, DEV) for _ in oparts]
+    ds.distributed_spmv(ds.SERIAL, prob, splits, xs, ys)
+    ys_h = [np.zeros(n) for _ in oparts]
+    O.dist_spmv(oparts, osplits, xs_h, ys_h)
+    for k in range(len(oparts)):
+        assert xs[k].data.cpu().numpy().tobytes() == xs_h[k].tobytes()   # halo filled
+        assert ys[k].data.cpu().numpy().tobytes() == ys_h[k].tobytes(), (k, lf, rf)
+    res = ds.cg(ds.SERIAL, ds.DistributedOperator(prob, splits), [p.b for p in prob.partitions],
+                tol=1e-9, max_iters=500, use_graph=use_graph)
+    ref = O.cg_dist(oparts, osplits, [op.b for op in oparts], tol=1e-9, max_iters=500)
+    assert abs(res.iterations - ref.iterations) <= 1 and res.converged == ref.converged
+    k = min(res.iterations, ref.iterations) + 1
+    h, w = np.asarray(res.residual_history[:k]), np.asarray(ref.history[:k])
+    assert np.all(np.abs(h - w) <= 1e-8 * w + 64 * np.finfo(np.float64).eps)
+    for kk in range(len(oparts)):
+        assert np.max(np.abs(res.x[kk].data.cpu().numpy() - ref.x[kk])) < 1e-8
