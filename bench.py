@@ -685,7 +685,7 @@ def run(args, rank: int, world: int) -> int:
         # counts divide; each replay then advances `spg` CG iterations
         spg = 1
         if use_graph:
-            for c in (10, 5, 4, 2):
+            for c in (20, 10, 5, 4, 2):
                 if args.steps % c == 0 and args.warmup % c == 0:
                     spg = c
                     break
