@@ -558,8 +558,10 @@ def config_of(nx: int, px: int, py: int, pz: int) -> dict:
     """The workload both arms run (the per-arm format plan is reported apart)."""
     return {"workload": f"hpcg_cg_27pt_{nx}^3_per_gpu", "grid_per_gpu": [nx, nx, nx],
             "procs": [px, py, pz], "tol_timed": "1e-300 (fixed step count)",
-            "l2": f"no flush: the matrix ({8 * 27 * nx ** 3 / 1e6:.0f} MB/GPU as DIA) exceeds "
-                  f"the 126 MB L2 and is re-streamed every step"}
+            "l2": (f"no flush: the matrix ({8 * 27 * nx ** 3 / 1e6:.0f} MB/GPU as DIA) exceeds "
+                   f"the 126 MB L2 and is re-streamed every step") if 8 * 27 * nx ** 3 > 126e6
+            else (f"no flush; the matrix ({8 * 27 * nx ** 3 / 1e6:.0f} MB/GPU as DIA) fits the "
+                  f"126 MB L2 -- a test size, not a bench configuration")}
 
 
 def reference_arm(args, rank: int, world: int) -> int:
