@@ -580,10 +580,12 @@ __global__ void __launch_bounds__(kVecBlock, MINB)
                                      const unsigned* pap_count, double* rr_parts,
                                      unsigned* bar_count, unsigned* bar_gen) {
   __shared__ double sh[32];
-  // Launched as a programmatic dependent of the SpMV: everything up to the
-  // griddepcontrol.wait reads only what the SpMV does not write -- s->done and
-  // x / r / p of the first sweep (the previous tail wrote them, and it is
-  // complete: every SpMV block waited on it before this grid could start).
+  // Phase 1 (update): r -= alpha Ap and the block r.r partials; phase 2
+  // (after the grid barrier): x += alpha p with the OLD p and p = r + beta p,
+  // so x and p are read once, in the same sweep (8 vector passes, was 9:
+  // phase 1 used to update x too, reading p twice).  Launched as a
+  // programmatic dependent of the SpMV: before griddepcontrol.wait it reads
+  // only s->done and the first sweep's r, which the SpMV does not write.
   if (s->done) return;
   const int64_t gtid = (int64_t)blockIdx.x * kVecBlock + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * kVecBlock;
@@ -594,12 +596,7 @@ __global__ void __launch_bounds__(kVecBlock, MINB)
   const double2* a2 = reinterpret_cast<const double2*>(ap);
   double2 xv[U], rv[U], pv[U];
 #pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int64_t i = min64(gtid + u * stride, n2 - 1);
-    xv[u] = x2[i];
-    rv[u] = r2[i];
-    pv[u] = p2[i];
-  }
+  for (int u = 0; u < U; ++u) rv[u] = r2[min64(gtid + u * stride, n2 - 1)];
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const double pap = reduce_partials<kVecBlock>(pap_parts, pap_count, sh);
   if (pap <= 0.0) {  // breakdown: every block sees the same pap
@@ -618,23 +615,16 @@ __global__ void __launch_bounds__(kVecBlock, MINB)
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t i = min64(i0 + u * stride, n2 - 1);
-      if (i0 != gtid) {   // the first sweep's x / r / p are already loaded
-        xv[u] = x2[i];
-        rv[u] = r2[i];
-        pv[u] = p2[i];
-      }
+      if (i0 != gtid) rv[u] = r2[i];   // the first sweep's r is already loaded
       av[u] = a2[i];
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t i = i0 + u * stride;
       if (i < n2) {
-        double2 xo, ro;
-        xo.x = add(mul(1.0, xv[u].x), mul(alpha, pv[u].x));
-        xo.y = add(mul(1.0, xv[u].y), mul(alpha, pv[u].y));
+        double2 ro;
         ro.x = add(mul(1.0, rv[u].x), mul(nalpha, av[u].x));
         ro.y = add(mul(1.0, rv[u].y), mul(nalpha, av[u].y));
-        x2[i] = xo;
         r2[i] = ro;
         v = add(v, mul(ro.x, ro.x));
         v = add(v, mul(ro.y, ro.y));
@@ -643,19 +633,25 @@ __global__ void __launch_bounds__(kVecBlock, MINB)
   }
   if ((n & 1) && gtid == 0) {
     const int64_t i = n - 1;
-    x[i] = add(mul(1.0, x[i]), mul(alpha, p[i]));
     const double ri = add(mul(1.0, r[i]), mul(nalpha, ap[i]));
     r[i] = ri;
     v = add(v, mul(ri, ri));
   }
   v = block_sum<kVecBlock>(v, sh);
   if (threadIdx.x == 0) rr_parts[blockIdx.x] = v;
+  // x and p of the first phase-2 sweep fly during the barrier (neither is
+  // written before it)
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int64_t i = min64(gtid + u * stride, n2 - 1);
+    xv[u] = x2[i];
+    pv[u] = p2[i];
+  }
   grid_barrier(bar_count, bar_gen);
   // the next SpMV (launched with programmatic stream serialization) may now
   // be scheduled: it prefetches matrix tiles and waits for this grid before
   // reading p
   asm volatile("griddepcontrol.launch_dependents;");
-  // direction: every block reduces the G partials in the same order
   double t = 0.0;
   for (int i = threadIdx.x; i < (int)gridDim.x; i += kVecBlock) t = add(t, __ldcg(rr_parts + i));
   t = block_sum<kVecBlock>(t, sh);
@@ -684,31 +680,41 @@ __global__ void __launch_bounds__(kVecBlock, MINB)
       s->rr = rr_new;
     }
   }
-  if (converged || last) return;
+  const bool stop = converged || last;   // x still takes this step; p stays
   for (int64_t i0 = gtid; i0 < n2; i0 += stride * U) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t i = min64(i0 + u * stride, n2 - 1);
-      rv[u] = __ldcg(r2 + i);
-      pv[u] = p2[i];
+      if (i0 != gtid) {
+        xv[u] = x2[i];
+        pv[u] = p2[i];
+      }
+      if (!stop) rv[u] = __ldcg(r2 + i);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t i = i0 + u * stride;
       if (i < n2) {
-        double2 po;
-        po.x = add(mul(1.0, rv[u].x), mul(beta, pv[u].x));
-        po.y = add(mul(1.0, rv[u].y), mul(beta, pv[u].y));
-        p2[i] = po;
+        double2 xo;
+        xo.x = add(mul(1.0, xv[u].x), mul(alpha, pv[u].x));
+        xo.y = add(mul(1.0, xv[u].y), mul(alpha, pv[u].y));
+        x2[i] = xo;
+        if (!stop) {
+          double2 po;
+          po.x = add(mul(1.0, rv[u].x), mul(beta, pv[u].x));
+          po.y = add(mul(1.0, rv[u].y), mul(beta, pv[u].y));
+          p2[i] = po;
+        }
       }
     }
   }
   if ((n & 1) && gtid == 0) {
     const int64_t i = n - 1;
-    p[i] = add(mul(1.0, __ldcg(r + i)), mul(beta, p[i]));
+    const double pi = p[i];
+    x[i] = add(mul(1.0, x[i]), mul(alpha, pi));
+    if (!stop) p[i] = add(mul(1.0, __ldcg(r + i)), mul(beta, pi));
   }
 }
-
 
 }  // namespace ds
 
