@@ -589,15 +589,24 @@ def _pinned_copy(eng, name: str, dst, src_np) -> None:
         dst.copy_(torch.from_numpy(np.ascontiguousarray(src_np)))
         return
     buf = _pinned(eng, name, dst.numel())
-    torch.cuda.current_stream(dst.device).synchronize()   # buffer free for reuse
+    main = torch.cuda.current_stream(dst.device)
+    main.synchronize()   # buffer free for reuse
     src = torch.from_numpy(np.ascontiguousarray(src_np))
-    # in 4 pieces: the DMA of a piece overlaps the host copy of the next
+    # in 4 pieces: the DMA of a piece overlaps the host copy of the next, and
+    # the pieces alternate between two streams (two copy engines: a 9 MB H2D
+    # 0.25 -> 0.19 ms, tools/h2d_probe2.py)
+    side = eng.__dict__.get("_h2d_side")
+    if side is None:
+        side = eng._h2d_side = torch.cuda.Stream(dst.device)
+    side.wait_stream(main)
     n = dst.numel()
     step = max(1 << 16, -(-n // 4))
-    for a in range(0, n, step):
+    for i, a in enumerate(range(0, n, step)):
         b = min(n, a + step)
         buf[a:b].copy_(src[a:b])   # multi-threaded host copy
-        dst[a:b].copy_(buf[a:b], non_blocking=True)
+        with torch.cuda.stream(side if i % 2 else main):
+            dst[a:b].copy_(buf[a:b], non_blocking=True)
+    main.wait_stream(side)
 
 
 def _reload(eng: CgEngine, bs, x0s) -> None:
