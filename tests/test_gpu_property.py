@@ -169,3 +169,42 @@ def test_stencil_decompositions_match_oracle(nx, ny, nz, px, py, pz, lf, rf, use
     assert np.all(np.abs(h - w) <= 1e-8 * w + 64 * np.finfo(np.float64).eps)
     for kk in range(len(oparts)):
         assert np.max(np.abs(res.x[kk].data.cpu().numpy() - ref.x[kk])) < 1e-8
+
+
+@settings(max_examples=40, deadline=None, suppress_health_check=[HealthCheck.too_slow])
+@given(st.integers(1, 400), st.integers(1, 4000), st.integers(0, 2**31 - 1),
+       st.sampled_from([34, 129, 130, 513, 3000]))
+def test_irregular_csr_tiles_match_oracle(nrows, ncols, seed, longest):
+    """Irregular CSR (longest row > 33: the row-tile / pairwise-leaf-tile
+    grid, ds_csr_tiles) with random row lengths up to `longest` entries,
+    empty rows, signed zeros: spmv and spmv_add bitwise vs np.add.reduceat's
+    order (kernels.py:102-119); the COO form of the same matrix (warp
+    segments + long-run kernel) bitwise vs np.bincount's."""
+    rng = np.random.default_rng(seed)
+    longest = min(longest, ncols)
+    lengths = rng.integers(0, 12, nrows)
+    lengths[rng.integers(0, nrows)] = longest
+    lengths[rng.random(nrows) < 0.05] = 0
+    lengths = np.minimum(lengths, ncols)
+    offs = np.zeros(nrows + 1, dtype=np.int64)
+    offs[1:] = np.cumsum(lengths)
+    cols = np.concatenate([np.sort(rng.choice(ncols, size=int(L), replace=False))
+                           for L in lengths]) if offs[-1] else np.zeros(0, np.int64)
+    vals = rng.standard_normal(offs[-1])
+    vals[rng.random(vals.size) < 0.03] = -0.0
+    x = rng.standard_normal(ncols)
+    x[rng.random(ncols) < 0.03] = -0.0
+    a = ds.CsrMatrix(nrows, ncols, offs, cols, vals, ds.MemorySpace.DEVICE, DEV)
+    oa = O.csr(nrows, ncols, offs, cols, vals)
+    ac = ds.convert(a, ds.FormatId.COO)
+    oc = O.convert(oa, O.COO)
+    xt = ds.DenseVector(torch.from_numpy(x).to(DEV))
+    for m, om in ((a, oa), (ac, oc)):
+        for acc in (False, True):
+            y0 = rng.standard_normal(nrows)
+            y0[::4] = -0.0
+            yw = y0.copy()
+            (O.spmv_add if acc else O.spmv)(om, x, yw)
+            yd = ds.DenseVector(torch.from_numpy(y0.copy()).to(DEV))
+            (ds.spmv_add if acc else ds.spmv)(ds.SERIAL, m, xt, yd)
+            assert yd.data.cpu().numpy().tobytes() == yw.tobytes(), (type(m).__name__, acc)
