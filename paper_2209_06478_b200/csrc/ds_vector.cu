@@ -594,10 +594,13 @@ __global__ void __launch_bounds__(kVecBlock, MINB)
   double2* r2 = reinterpret_cast<double2*>(r);
   double2* p2 = reinterpret_cast<double2*>(p);
   const double2* a2 = reinterpret_cast<const double2*>(ap);
-  double2 xv[U], rv[U], pv[U];
+  double2 xv[U], rv[U], pv[U], av[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) rv[u] = r2[min64(gtid + u * stride, n2 - 1)];
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  // the first sweep's Ap flies during the pAp partials reduction
+#pragma unroll
+  for (int u = 0; u < U; ++u) av[u] = a2[min64(gtid + u * stride, n2 - 1)];
   const double pap = reduce_partials<kVecBlock>(pap_parts, pap_count, sh);
   if (pap <= 0.0) {  // breakdown: every block sees the same pap
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -611,12 +614,13 @@ __global__ void __launch_bounds__(kVecBlock, MINB)
   const int it = s->iter + 1;
   double v = 0.0;
   for (int64_t i0 = gtid; i0 < n2; i0 += stride * U) {
-    double2 av[U];
+    if (i0 != gtid) {   // the first sweep's r and Ap are already loaded
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t i = min64(i0 + u * stride, n2 - 1);
-      if (i0 != gtid) rv[u] = r2[i];   // the first sweep's r is already loaded
-      av[u] = a2[i];
+      for (int u = 0; u < U; ++u) {
+        const int64_t i = min64(i0 + u * stride, n2 - 1);
+        rv[u] = r2[i];
+        av[u] = a2[i];
+      }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
