@@ -192,6 +192,20 @@ int ds_convert_begin_csr(int64_t nrows, int64_t ncols, int64_t nnz, const int32_
 int ds_convert_begin_dia(int64_t nrows, int64_t ncols, int32_t ndiags, const int32_t* offsets,
                          const double* values, int target, int64_t fill_limit, void* stream,
                          ds_convert_job** job, int64_t* out_nnz, int64_t* out_ndiags);
+/* One pass for a canonical COO / CSR source ((row, col) strictly increasing,
+ * every index in range) and a COO / CSR target -- the common case of the
+ * reference's convert (datamove.py:261-281: the proxy's sort and duplicate
+ * sums are the identity there).  src_idx = rows (COO) or row_offsets (CSR);
+ * out_idx = target rows (nnz) or row_offsets (nrows + 1); out_cols /
+ * out_values hold nnz.  The check and the target writes share the pass;
+ * *done = 1: the target is complete.  *done = 0: not applicable (empty,
+ * arrays not 16-B aligned) or not canonical -- the target arrays may have
+ * been written; run begin / finish.  DS_ERR_INDEX_OUT_OF_RANGE like
+ * begin_*.  Synchronises the stream.                                        */
+int ds_convert_direct(int src_format, int target, int64_t nrows, int64_t ncols, int64_t nnz,
+                      const int32_t* src_idx, const int32_t* cols, const double* values,
+                      int32_t* out_idx, int32_t* out_cols, double* out_values, void* stream,
+                      int* done);
 int ds_convert_finish_coo(ds_convert_job* job, int32_t* rows, int32_t* cols, double* values);
 int ds_convert_finish_csr(ds_convert_job* job, int32_t* row_offsets, int32_t* cols,
                           double* values);

@@ -115,6 +115,8 @@ _SIGNATURES = {
                                      ctypes.POINTER(c_vp), P_i64, P_i64]),
     "ds_convert_begin_dia": (c_int, [c_i64, c_i64, c_i32, c_vp, c_vp, c_int, c_i64, c_vp,
                                      ctypes.POINTER(c_vp), P_i64, P_i64]),
+    "ds_convert_direct": (c_int, [c_int, c_int, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                  c_vp, c_vp, P_i32]),
     "ds_convert_finish_coo": (c_int, [c_vp, c_vp, c_vp, c_vp]),
     "ds_convert_finish_csr": (c_int, [c_vp, c_vp, c_vp, c_vp]),
     "ds_convert_finish_dia": (c_int, [c_vp, c_vp, c_vp]),

@@ -702,6 +702,246 @@ __global__ void __launch_bounds__(256)
   if (lane == 0 && mybad) atomicOr(bad, mybad);
 }
 
+// The same census, entries taken four at a time (round 2, second pass): a
+// thread loads one 16-B aligned quad of columns and the quad's four row ids
+// with one 32-bit shared load, so the per-entry work is the order compare,
+// the range check and the flag test (~12 instructions per entry, was ~40:
+// csr_census_tiles was issue-bound, ncu sm__throughput 62-69% at 2 warp
+// instructions per entry).  "Same row as the previous entry" is a row-id
+// compare inside the quad and `k > off[row]` at its first entry; the previous
+// column comes from the lane before (lane 0: one scalar load).  Quads that
+// straddle the array bounds or a chunk edge load their entries one by one.
+// The next tile's offsets are loaded before the current tile is walked.
+constexpr int kCqU = 4;             // quads in flight per thread
+constexpr int kCqCap = 8192;        // entries per row-id chunk (multiple of 4)
+struct QuadIds {
+  int off[kRT + 1];
+  unsigned char rid[kCqCap + 4];
+};
+
+__device__ __forceinline__ double2 ld_stream2(const double* p) {
+  double2 v;
+  asm("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int4 ld_stream4(const int* p) {
+  int4 v;
+  asm("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+
+// flag test of one entry: the L1-cached load is predicated (no branch) on
+// `ok` (the column in range); a zero flag is set
+__device__ __forceinline__ void census_flag(unsigned char* flags, unsigned d, bool ok) {
+  unsigned short f = 1;
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t@p ld.global.ca.u8 %0, [%1];\n\t}"
+               : "+h"(f) : "l"(flags + d), "r"((int)ok));
+  if (f == 0) flags[d] = 1;
+}
+
+// COPY (ds_convert_direct, a canonical CSR source to a COO / CSR target):
+// the same walk also writes the columns, values and -- ROWS -- the row index
+// of every entry (tile row + row id) into the target, so the source is read
+// once; the caller discards the target if the census finds the source not
+// canonical.  Needs 16-B aligned columns / values / targets (s == 0).
+template <bool FLAGS, bool COPY = false, bool ROWS = false>
+__global__ void __launch_bounds__(256)
+    csr_census_quads(int nrows, int ncols, int64_t nnz, const int* __restrict__ off,
+                     const int* __restrict__ c, unsigned char* flags, int* bad,
+                     const double* __restrict__ v = nullptr, int* __restrict__ orow = nullptr,
+                     int* __restrict__ ocol = nullptr, double* __restrict__ oval = nullptr) {
+  constexpr int U = COPY ? 2 : kCqU;
+  __shared__ QuadIds ids;
+  const int lane = threadIdx.x & 31;
+  const int tid = threadIdx.x;
+  // entry k lives in address quad (k + s) >> 2
+  const int s = (int)((reinterpret_cast<uintptr_t>(c) >> 2) & 3);
+  int mybad = 0;
+  const int ntiles = (nrows + kRT - 1) / kRT;
+  int tile = blockIdx.x;
+  int o_next = 0;
+  if (tile < ntiles && tid <= min(kRT, nrows - tile * kRT)) o_next = __ldg(off + tile * kRT + tid);
+  for (; tile < ntiles; tile += gridDim.x) {
+    const int r0 = tile * kRT;
+    const int nr = min(kRT, nrows - r0);
+    if (tid <= nr) ids.off[tid] = o_next;
+    {
+      const int nt = tile + gridDim.x;
+      if (nt < ntiles && tid <= min(kRT, nrows - nt * kRT)) o_next = __ldg(off + nt * kRT + tid);
+    }
+    __syncthreads();
+    const int e0 = ids.off[0], e1 = ids.off[nr];
+    // d = column - row + nrows - 1 = column - t + dbase for tile-local row t
+    const unsigned dbase = (unsigned)(nrows - 1) - (unsigned)r0;
+    for (int kq0 = ((e0 + s) & ~3) - s; kq0 < e1; kq0 += kCqCap) {
+      const int k0 = max(kq0, e0), kend = min(kq0 + kCqCap, e1);
+      for (int t = tid; t < nr; t += blockDim.x) {
+        const int lo = max(ids.off[t], k0), hi = min(ids.off[t + 1], kend);
+        for (int k = lo; k < hi; ++k) ids.rid[k - kq0] = (unsigned char)t;
+      }
+      if (tid < k0 - kq0) ids.rid[tid] = 0xff;   // head entries before the tile: no row
+      __syncthreads();
+      const int nq = (kend - kq0 + 3) >> 2;
+      const int4* cq = reinterpret_cast<const int4*>(c + kq0);   // 16-B aligned: (kq0 + s) % 4 == 0
+      for (int qb = 0; qb < nq; qb += (int)blockDim.x * U) {
+        int4 cv[U];
+        int pv[U];
+        double ve[COPY ? U : 1][4];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int q = qb + u * (int)blockDim.x + tid;
+          const int kq = kq0 + 4 * q;
+          if (q < nq && kq >= k0 && kq + 3 < kend) {
+            cv[u] = ld_stream4(reinterpret_cast<const int*>(cq + q));
+            if (COPY) {
+              const double2 a = ld_stream2(v + kq), b = ld_stream2(v + kq + 2);
+              ve[u][0] = a.x; ve[u][1] = a.y; ve[u][2] = b.x; ve[u][3] = b.y;
+            }
+          } else {
+            cv[u] = make_int4(0, 0, 0, 0);
+            if (COPY) ve[u][0] = ve[u][1] = ve[u][2] = ve[u][3] = 0.0;
+            if (q < nq) {   // a quad across the chunk's head or tail: entries one by one
+              if (kq >= k0) cv[u].x = ld_stream(c + kq);
+              if (kq + 1 >= k0 && kq + 1 < kend) cv[u].y = ld_stream(c + kq + 1);
+              if (kq + 2 >= k0 && kq + 2 < kend) cv[u].z = ld_stream(c + kq + 2);
+              if (kq + 3 < kend) cv[u].w = ld_stream(c + kq + 3);
+              if (COPY) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                  if (kq + e >= k0 && kq + e < kend) ve[u][e] = ld_stream(v + kq + e);
+              }
+            }
+          }
+          pv[u] = (lane == 0 && q < nq && kq > 0) ? __ldg(c + kq - 1) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int q = qb + u * (int)blockDim.x + tid;
+          const int kq = kq0 + 4 * q;
+          int prev = __shfl_up_sync(0xffffffffu, cv[u].w, 1);
+          if (lane == 0) prev = pv[u];
+          if (q < nq) {
+            const unsigned r4 = *reinterpret_cast<const unsigned*>(&ids.rid[4 * q]);
+            const int ce[4] = {cv[u].x, cv[u].y, cv[u].z, cv[u].w};
+            const bool full = kq >= k0 && kq + 3 < kend;
+            int tprev = -1, pc = prev;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int k = kq + e;
+              const int t = (int)((r4 >> (8 * e)) & 0xffu);
+              const bool valid = full || (k >= k0 && k < kend);
+              // an entry continues its row unless it is the row's first;
+              // entries before k0 carry row id 0xff (no row)
+              const bool same = e == 0 ? (valid && k > ids.off[t & 0x7f]) : t == tprev;
+              const bool inr = (unsigned)ce[e] < (unsigned)ncols;
+              mybad |= (valid && same && pc >= ce[e]) ? kBadOrder : 0;
+              mybad |= (valid && !inr) ? kBadIndex : 0;
+              if (FLAGS) census_flag(flags, (unsigned)ce[e] - (unsigned)t + dbase, valid && inr);
+              if (COPY && !full && valid) {
+                ocol[k] = ce[e];
+                __stcs(oval + k, ve[u][e]);
+                if (ROWS) orow[k] = r0 + t;
+              }
+              tprev = t;
+              pc = ce[e];
+            }
+            if (COPY && full) {
+              __stcs(reinterpret_cast<int4*>(ocol + kq), cv[u]);
+              __stcs(reinterpret_cast<double2*>(oval + kq), make_double2(ve[u][0], ve[u][1]));
+              __stcs(reinterpret_cast<double2*>(oval + kq + 2), make_double2(ve[u][2], ve[u][3]));
+              if (ROWS)
+                __stcs(reinterpret_cast<int4*>(orow + kq),
+                       make_int4(r0 + (int)(r4 & 0xffu), r0 + (int)((r4 >> 8) & 0xffu),
+                                 r0 + (int)((r4 >> 16) & 0xffu), r0 + (int)(r4 >> 24)));
+            }
+          }
+        }
+      }
+      __syncthreads();
+    }
+    __syncthreads();   // ids.off[0] / ids.off[nr] read above (a tile without entries skips the chunk loop)
+  }
+  mybad = __reduce_or_sync(0xffffffffu, mybad);
+  if (lane == 0 && mybad) atomicOr(bad, mybad);
+}
+
+// COO source, canonical ((row, col) strictly increasing, every index in
+// range) -> COO / CSR target in one pass (ds_convert_direct): one address
+// quad of entries per lane, the previous entry from the lane before (lane 0:
+// scalar loads); the CSR offsets are written at row changes (rows_to_offsets'
+// rule, clamped so that a non-canonical source stays in bounds -- its target
+// is discarded).  Needs 16-B aligned arrays.
+template <bool ROWS_OUT, bool OFF_OUT>
+__global__ void __launch_bounds__(256)
+    coo_direct_kernel(int64_t nnz, int nrows, int ncols, const int* __restrict__ r,
+                      const int* __restrict__ c, const double* __restrict__ v,
+                      int* __restrict__ orow, int* __restrict__ ocol, double* __restrict__ oval,
+                      int* __restrict__ ooff, int* bad) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nqa = (nnz + 3) >> 2;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int mybad = 0;
+  for (int64_t qw = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); qw < nqa; qw += stride) {
+    const int64_t q = qw + lane;   // the warp's quads are consecutive
+    const int64_t kq = 4 * q;
+    const bool full = kq + 3 < nnz;
+    int4 rv = make_int4(0, 0, 0, 0), cv = make_int4(0, 0, 0, 0);
+    double ve[4] = {0.0, 0.0, 0.0, 0.0};
+    if (full) {
+      rv = ld_stream4(r + kq);
+      cv = ld_stream4(c + kq);
+      const double2 a = ld_stream2(v + kq), b = ld_stream2(v + kq + 2);
+      ve[0] = a.x; ve[1] = a.y; ve[2] = b.x; ve[3] = b.y;
+    } else if (kq < nnz) {
+      rv.x = ld_stream(r + kq); cv.x = ld_stream(c + kq); ve[0] = ld_stream(v + kq);
+      if (kq + 1 < nnz) { rv.y = ld_stream(r + kq + 1); cv.y = ld_stream(c + kq + 1); ve[1] = ld_stream(v + kq + 1); }
+      if (kq + 2 < nnz) { rv.z = ld_stream(r + kq + 2); cv.z = ld_stream(c + kq + 2); ve[2] = ld_stream(v + kq + 2); }
+    }
+    int pr = __shfl_up_sync(0xffffffffu, rv.w, 1), pc = __shfl_up_sync(0xffffffffu, cv.w, 1);
+    if (lane == 0 && kq > 0 && kq < nnz) {
+      pr = __ldg(r + kq - 1);
+      pc = __ldg(c + kq - 1);
+    }
+    const int re[4] = {rv.x, rv.y, rv.z, rv.w}, ce[4] = {cv.x, cv.y, cv.z, cv.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int64_t k = kq + e;
+      if (k < nnz) {
+        const int rk = re[e], ck = ce[e];
+        if (k > 0) {
+          if (rk < pr) mybad |= kBadOrder | kBadRowOrder;
+          else if (rk == pr && ck <= pc) mybad |= kBadOrder;
+        }
+        if ((unsigned)rk >= (unsigned)nrows || (unsigned)ck >= (unsigned)ncols) mybad |= kBadIndex;
+        if (OFF_OUT) {
+          // off[i] = k for the rows i in (r[k-1], r[k]]; the last entry also
+          // closes (r[nnz-1], nrows]
+          const int lo = k == 0 ? 0 : max(pr + 1, 0), hi = min(rk, nrows);
+          for (int i = lo; i <= hi; ++i) ooff[i] = (int)k;
+          if (k == nnz - 1)
+            for (int i = max(rk + 1, 0); i <= nrows; ++i) ooff[i] = (int)nnz;
+        }
+        if (!full) {
+          ocol[k] = ck;
+          __stcs(oval + k, ve[e]);
+          if (ROWS_OUT) orow[k] = rk;
+        }
+        pr = rk;
+        pc = ck;
+      }
+    }
+    if (full) {
+      __stcs(reinterpret_cast<int4*>(ocol + kq), cv);
+      __stcs(reinterpret_cast<double2*>(oval + kq), make_double2(ve[0], ve[1]));
+      __stcs(reinterpret_cast<double2*>(oval + kq + 2), make_double2(ve[2], ve[3]));
+      if (ROWS_OUT) __stcs(reinterpret_cast<int4*>(orow + kq), rv);
+    }
+  }
+  mybad = __reduce_or_sync(0xffffffffu, mybad);
+  if (lane == 0 && mybad) atomicOr(bad, mybad);
+}
+
 // canonical CSR -> DIA: the tile's (kRT x nd) slab zeroed in shared memory,
 // entries dropped into (row, diag_map[col - row]) slots, the slab written out
 // contiguously (values are row-major (nrows, nd))
@@ -1596,9 +1836,13 @@ static int begin_csr_impl(ds_convert_job* j, int64_t nnz, const int32_t* row_off
     DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&j->scratch), flag_bytes + 4, st));
     DS_CUDA(cudaMemsetAsync(j->scratch, 0, flag_bytes + 4, st));
     int* bad = reinterpret_cast<int*>(j->scratch + flag_bytes);
-    csr_census_tiles<<<rt_grid(nrows, 8), 256, 0, st>>>((int)nrows, (int)ncols, row_offsets, cols,
-                                                       dia ? j->scratch : nullptr, bad);
-    DS_LAUNCH_CHECK("csr_census_tiles");
+    if (dia)
+      csr_census_quads<true><<<rt_grid(nrows, 8), 256, 0, st>>>((int)nrows, (int)ncols, nnz,
+                                                               row_offsets, cols, j->scratch, bad);
+    else
+      csr_census_quads<false><<<rt_grid(nrows, 8), 256, 0, st>>>((int)nrows, (int)ncols, nnz,
+                                                                row_offsets, cols, nullptr, bad);
+    DS_LAUNCH_CHECK("csr_census_quads");
     int bad_h = 1;
     DS_CUDA(cudaMemcpyAsync(&bad_h, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
     DS_CUDA(cudaStreamSynchronize(st));
@@ -1644,6 +1888,65 @@ extern "C" int ds_convert_begin_csr(int64_t nrows, int64_t ncols, int64_t nnz,
     return rc;
   }
   *job = j;
+  return DS_OK;
+}
+
+// ---------------------------------------- one-pass canonical conversions --
+// A canonical COO / CSR source to a COO / CSR target: the order / range
+// check and the target writes in one pass over the source (the begin /
+// finish pair reads it twice and copies with cudaMemcpy).  *done = 0 when
+// the path does not apply (empty, misaligned arrays) or the source is not
+// canonical -- the caller then runs begin / finish; the target arrays may
+// have been written either way.
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+extern "C" int ds_convert_direct(int src_format, int target, int64_t nrows, int64_t ncols,
+                                 int64_t nnz, const int32_t* src_idx, const int32_t* cols,
+                                 const double* values, int32_t* out_idx, int32_t* out_cols,
+                                 double* out_values, void* stream, int* done) {
+  *done = 0;
+  if ((src_format != DS_FMT_COO && src_format != DS_FMT_CSR) ||
+      (target != DS_FMT_COO && target != DS_FMT_CSR))
+    return DS_ERR_INVALID_ARGUMENT;
+  if (!dims_ok(nrows, ncols, nnz)) return DS_ERR_NOT_SUPPORTED;
+  if (nnz <= 0 || nrows <= 0) return DS_OK;
+  if (!aligned16(cols) || !aligned16(values) || !aligned16(out_cols) || !aligned16(out_values))
+    return DS_OK;
+  if (src_format == DS_FMT_COO && !aligned16(src_idx)) return DS_OK;
+  if (target == DS_FMT_COO && !aligned16(out_idx)) return DS_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int* bad = nullptr;
+  DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&bad), sizeof(int), st));
+  DS_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
+  const int nr = (int)nrows, nc = (int)ncols;
+  if (src_format == DS_FMT_CSR) {
+    if (target == DS_FMT_COO)
+      csr_census_quads<false, true, true><<<rt_grid(nrows, 4), 256, 0, st>>>(
+          nr, nc, nnz, src_idx, cols, nullptr, bad, values, out_idx, out_cols, out_values);
+    else
+      csr_census_quads<false, true, false><<<rt_grid(nrows, 4), 256, 0, st>>>(
+          nr, nc, nnz, src_idx, cols, nullptr, bad, values, nullptr, out_cols, out_values);
+    DS_LAUNCH_CHECK("csr_census_quads(copy)");
+    if (target == DS_FMT_CSR)
+      DS_CUDA(cudaMemcpyAsync(out_idx, src_idx, (nrows + 1) * sizeof(int32_t),
+                              cudaMemcpyDeviceToDevice, st));
+  } else {
+    const unsigned g = (unsigned)std::max<int64_t>(
+        1, min64(ceil_div(ceil_div(nnz, 4), 256), (int64_t)sm_count() * 4));
+    if (target == DS_FMT_COO)
+      coo_direct_kernel<true, false><<<g, 256, 0, st>>>(nnz, nr, nc, src_idx, cols, values,
+                                                         out_idx, out_cols, out_values, nullptr, bad);
+    else
+      coo_direct_kernel<false, true><<<g, 256, 0, st>>>(nnz, nr, nc, src_idx, cols, values,
+                                                         nullptr, out_cols, out_values, out_idx, bad);
+    DS_LAUNCH_CHECK("coo_direct_kernel");
+  }
+  int bad_h = 1;
+  DS_CUDA(cudaMemcpyAsync(&bad_h, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+  DS_CUDA(cudaFreeAsync(bad, st));
+  DS_CUDA(cudaStreamSynchronize(st));
+  if (bad_h & kBadIndex) return index_error(nrows, ncols);
+  *done = bad_h == 0;
   return DS_OK;
 }
 

@@ -307,3 +307,62 @@ def test_row_sorted_coo_segmented_sort(case):
                        torch.from_numpy(vals).to(DEV), ds.MemorySpace.DEVICE)
     assert_same(ds.convert(csr, ds.FormatId.CSR),
                 O.convert(O.csr(nrows, ncols, off, cols, vals), O.CSR), f"{case} csr src")
+
+
+@pytest.mark.parametrize("shift", [0, 1, 2, 3])
+def test_csr_census_quads_edges(shift):
+    """The quad census (csr_census_quads): columns misaligned by 0-3 ints, a
+    row longer than two row-id chunks (8192 entries), rows across 128-row
+    tiles; a single duplicate / descending pair placed at every position of
+    a quad, at warp (128-entry) and chunk edges and at a tile's first row
+    must send the conversion down the general path (oracle-equal), while the
+    same columns across a row boundary must not."""
+    rng = np.random.default_rng(70 + shift)
+    nrows, ncols = 400, 30000
+    lengths = rng.integers(0, 40, nrows)
+    lengths[130] = 20000                    # three chunks inside tile 1
+    lengths[255] = 0
+    offs, cols, vals = random_csr(rng, nrows, ncols, lengths)
+    def conv(c, tgt):
+        src = ds.CsrMatrix(nrows, ncols, torch.from_numpy(offs.astype(np.int32)).to(DEV), c,
+                           torch.from_numpy(vals).to(DEV), ds.MemorySpace.DEVICE, DEV)
+        return ds.convert(src, tgt, fill_limit=BIG)
+    def dev_cols(cc):
+        buf = torch.zeros(cc.size + 4, dtype=torch.int32, device=DEV)
+        buf[shift:shift + cc.size] = torch.from_numpy(cc.astype(np.int32)).to(DEV)
+        v = buf[shift:shift + cc.size]
+        assert (v.data_ptr() >> 2) & 3 == ((buf.data_ptr() >> 2) + shift) & 3
+        return v
+    ora = O.csr(nrows, ncols, offs, cols, vals)
+    for tgt, fid in ((O.CSR, ds.FormatId.CSR), (O.DIA, ds.FormatId.DIA)):
+        assert_same(conv(dev_cols(cols), fid), O.convert(ora, tgt, fill_limit=BIG), (shift, fid))
+    # positions: entry k's quad is (k + s) >> 2 with s the pointer's int offset
+    s = (int(dev_cols(cols).data_ptr()) >> 2) & 3
+    e0 = int(offs[128])
+    kq0 = ((e0 + s) & ~3) - s
+    L = int(offs[130])
+    cand = [L + j for j in range(1, 9)] + [kq0 + 8192 + d for d in (-1, 0, 1)] \
+        + [kq0 + 16384 + d for d in (0, 1)] + [kq0 + 128 * 7, kq0 + 128 * 7 + 1] \
+        + [int(offs[256]) + 1, int(offs[1]) + 1]
+    for k in cand:
+        row = int(np.searchsorted(offs, k, side="right") - 1)
+        assert offs[row] < k < offs[row + 1]          # k and k - 1 in one row
+        for kind in ("swap", "dup"):
+            c2 = cols.copy()
+            if kind == "swap":
+                c2[k - 1], c2[k] = c2[k], c2[k - 1]
+                tgt, fid = O.CSR, ds.FormatId.CSR
+            else:
+                c2[k] = c2[k - 1]
+                tgt, fid = O.DIA, ds.FormatId.DIA
+            want = O.convert(O.csr(nrows, ncols, offs, c2, vals), tgt, fill_limit=BIG)
+            assert_same(conv(dev_cols(c2), fid), want, (shift, k, kind))
+    # a row's first column below the previous row's last: still canonical
+    k = int(offs[200])
+    c3 = cols.copy()
+    c3[k] = 0
+    c3[k:offs[201]] = np.sort(c3[k:offs[201]])
+    if offs[201] - k > 1 and c3[k + 1] != 0:
+        want = O.convert(O.csr(nrows, ncols, offs, c3, vals), O.CSR, fill_limit=BIG)
+        got = conv(dev_cols(c3), ds.FormatId.CSR)
+        assert_same(got, want, "row boundary")
