@@ -472,21 +472,21 @@ __global__ void rows_to_offsets(int64_t nnz, int nrows, const int* __restrict__ 
 }
 
 // Presence flags of every diagonal (taken by coo_check_mark /
-// csr_check_mark / dia_group_counts).  Few distinct diagonals are hit by very
+// csr_census_quads / dia_group_counts).  Few distinct diagonals are hit by very
 // many entries (27 for the stencil) and same-address stores serialise in L2.
 // Each marker tests first with an L1-CACHED load: an SM's own store
 // invalidates its L1 line, the next miss brings back the 1, so every SM writes
 // each flag about once and all other tests hit L1 (a racing duplicate store
 // of 1 is harmless).
 // CSR source, DIA target: one pass over the column indices checks the
-// canonical order (strictly ascending columns in every row: coo_check_mark's test without
-// expanding the rows) and marks the diagonals; then the DIA slab of a block
-// of rows is zeroed in shared memory, the block's entries are dropped into
-// their (row, diagonal) slots and the slab is written out with coalesced
-// stores (values are row-major (nrows, ndiags)).  Both walk the entries of a
-// warp's rows 32 at a time (coalesced, U chunks of loads in flight); each
-// lane tracks the row of its entry incrementally (rows are monotone in k, so
-// a lane moves ~1 row per chunk) instead of searching the offsets.
+// canonical order (strictly ascending columns in every row: coo_check_mark's
+// test without expanding the rows) and marks the diagonals (csr_census_quads);
+// then the DIA slab of a block of rows is zeroed in shared memory, the
+// block's entries are dropped into their (row, diagonal) slots and the slab
+// is written out with coalesced stores (values are row-major (nrows,
+// ndiags)).  The fill walks the entries of a warp's rows 32 at a time
+// (coalesced, U chunks of loads in flight), finding each entry's row by a
+// shuffle search over the warp's offsets.
 constexpr int kCsrWalkRows = 16;    // rows per warp (<= 31: the offsets live in one lane each)
 // Lane t <= r1 - r0 holds off[r0 + t] (the rest INT_MAX): an entry's row is
 // found by a 5-step binary search over the lanes (shuffles, no memory).  The
@@ -538,48 +538,6 @@ struct ColVal {
 // nothing is marked for it, the caller raises IndexOutOfRange)
 constexpr int kBadOrder = 1, kBadIndex = 2, kBadRowOrder = 4;   // 4: rows decrease somewhere
 
-__global__ void csr_check_mark(int nrows, int ncols, const int* __restrict__ off,
-                               const int* __restrict__ c, unsigned char* flags, int* bad) {
-  const int lane = threadIdx.x & 31;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  int mybad = 0;
-  int r0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kCsrWalkRows;
-  int ot = walk_offsets(off, nrows, r0);
-  for (; r0 < nrows; r0 += nwarps * kCsrWalkRows) {
-    const int r1 = min(r0 + kCsrWalkRows, nrows);
-    const int ot_next = walk_offsets(off, nrows, r0 + nwarps * kCsrWalkRows);
-    int carry = -1, carry_row = -1;   // previous chunk's last entry (lane 31)
-    csr_warp_walk<8>(ot, r0, r1, [&](int k) { return __ldg(c + k); },
-                     [&](int kb, int k1, const int (&rr)[8], const int (&cc)[8]) {
-#pragma unroll
-                       for (int u = 0; u < 8; ++u) {
-                         const int row = rr[u], ck = cc[u];
-                         int prev = __shfl_up_sync(0xffffffffu, ck, 1);
-                         int prev_row = __shfl_up_sync(0xffffffffu, row, 1);
-                         if (lane == 0) {
-                           prev = carry;
-                           prev_row = carry_row;
-                         }
-                         carry = __shfl_sync(0xffffffffu, ck, 31);
-                         carry_row = __shfl_sync(0xffffffffu, row, 31);
-                         if (kb + 32 * u + lane < k1) {
-                           if (prev_row == row && prev >= ck) mybad |= kBadOrder;
-                           if ((unsigned)ck >= (unsigned)ncols) {
-                             mybad |= kBadIndex;
-                           } else if (flags) {
-                             const int64_t d = (int64_t)ck - row + nrows - 1;
-                             unsigned short f;
-                             asm volatile("ld.global.ca.u8 %0, [%1];" : "=h"(f) : "l"(flags + d));
-                             if (f == 0) flags[d] = 1;
-                           }
-                         }
-                       }
-                     });
-    ot = ot_next;
-  }
-  mybad = __reduce_or_sync(0xffffffffu, mybad);
-  if ((threadIdx.x & 31) == 0 && mybad) atomicOr(bad, mybad);
-}
 
 __global__ void dia_fill_csr(int nrows, int nd, int R, const int* __restrict__ off,
                              const int* __restrict__ c, const double* __restrict__ v,
@@ -660,47 +618,9 @@ __device__ __forceinline__ void csr_rowid_tile(int nrows, const int* __restrict_
 // a row-uniform warp walk (a warp takes 32 rows one row at a time, no row-id
 // lookup per entry, 8 rows' columns in flight) was slower -- 192^3 census
 // 1.13 -> 1.26 ms wall, and with the matching slab-per-row DIA fill CSR->DIA
-// 1.46 -> 1.85 ms: latency-bound on the per-row chain.
-__global__ void __launch_bounds__(256)
-    csr_census_tiles(int nrows, int ncols, const int* __restrict__ off,
-                     const int* __restrict__ c, unsigned char* flags, int* bad) {
-  __shared__ RowIds ids;
-  const int lane = threadIdx.x & 31;
-  int mybad = 0;
-  const int ntiles = (nrows + kRT - 1) / kRT;
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int r0 = tile * kRT;
-    csr_rowid_tile(nrows, off, r0, ids, [&](int kb, int k0, int kend) {
-      int ck[kRtU], pv[kRtU];
-#pragma unroll
-      for (int u = 0; u < kRtU; ++u) {
-        const int k = kb + u * (int)blockDim.x + (int)threadIdx.x;
-        ck[u] = k < kend ? ld_stream(c + k) : 0;
-        pv[u] = (lane == 0 && k < kend && k > 0) ? __ldg(c + k - 1) : 0;
-      }
-#pragma unroll
-      for (int u = 0; u < kRtU; ++u) {
-        const int k = kb + u * (int)blockDim.x + (int)threadIdx.x;
-        int prev = __shfl_up_sync(0xffffffffu, ck[u], 1);
-        if (lane == 0) prev = pv[u];
-        if (k < kend) {
-          const int t = ids.rid[k - k0];
-          if (k > ids.off[t] && prev >= ck[u]) mybad |= kBadOrder;
-          if ((unsigned)ck[u] >= (unsigned)ncols) {
-            mybad |= kBadIndex;
-          } else if (flags) {
-            const int64_t d = (int64_t)ck[u] - (r0 + t) + nrows - 1;
-            unsigned short f;
-            asm volatile("ld.global.ca.u8 %0, [%1];" : "=h"(f) : "l"(flags + d));
-            if (f == 0) flags[d] = 1;
-          }
-        }
-      }
-    });
-  }
-  mybad = __reduce_or_sync(0xffffffffu, mybad);
-  if (lane == 0 && mybad) atomicOr(bad, mybad);
-}
+// 1.46 -> 1.85 ms: latency-bound on the per-row chain.  The entry-at-a-time
+// row-id tile walk (csr_census_tiles, round 2 first pass) was issue-bound at
+// ~2 warp instructions per entry; csr_census_quads below replaces it.
 
 // The same census, entries taken four at a time (round 2, second pass): a
 // thread loads one 16-B aligned quad of columns and the quad's four row ids
