@@ -17,6 +17,7 @@
 // Integer scans and histograms are hand-written (3-phase block scan); the
 // general-case stable sort is ds_sort.cu's onesweep LSD radix sort on
 // (row*ncols+col, index) keys limited to the needed bits.
+#include <algorithm>
 #include <vector>
 
 #include "ds_common.cuh"
@@ -230,6 +231,14 @@ __global__ void reduce_runs(int64_t nnz, int64_t ncols, const unsigned long long
 // straight into the target arrays.
 constexpr int kDiaGroupRows = 32;
 constexpr int kDiaChunks = 4;
+#ifndef DS_DIA_EMIT_CHUNKS
+#define DS_DIA_EMIT_CHUNKS 16
+#endif
+// slots in flight per lane in the emit walk: latency-bound on the value loads
+// (ncu long_scoreboard 13 per issue at 4).  192^3 DIA->COO / DIA->CSR:
+// 4: 1.36 / 1.12 ms, 8: 1.34 / 1.12, 12: 1.22 / 1.07, 16: 1.15 / 1.07 (96
+// registers), 24: 1.68 / 1.66, 32: 1.33 / 1.29 (tools/gpu_ab_conv.sh)
+constexpr int kDiaEmitChunks = DS_DIA_EMIT_CHUNKS;
 
 struct DiaSlots {
   int ncols, nd, q, rmd;   // 32 = q * nd + rmd
@@ -238,20 +247,20 @@ struct DiaSlots {
   __device__ DiaSlots(int ncols_, int nd_, const int* off_, const double* vals_)
       : ncols(ncols_), nd(nd_), q(32 / nd_), rmd(32 % nd_), off(off_), vals(vals_) {}
   // walk the slots [e_begin, e_end) of one group; f(valid, e, i, j) per lane
-  template <class F>
+  template <int U = kDiaChunks, class F>
   __device__ __forceinline__ void walk(int64_t r0, int64_t e_begin, int64_t e_end, F&& f) const {
     const int lane = threadIdx.x & 31;
     int64_t i = r0 + lane / nd;
     int j = lane % nd;
-    for (int64_t e0 = e_begin; e0 < e_end; e0 += 32 * kDiaChunks) {
-      double x[kDiaChunks];
+    for (int64_t e0 = e_begin; e0 < e_end; e0 += 32 * U) {
+      double x[U];
 #pragma unroll
-      for (int u = 0; u < kDiaChunks; ++u) {
+      for (int u = 0; u < U; ++u) {
         const int64_t e = e0 + u * 32 + lane;
         x[u] = e < e_end ? __ldg(vals + e) : 0.0;
       }
 #pragma unroll
-      for (int u = 0; u < kDiaChunks; ++u) {
+      for (int u = 0; u < U; ++u) {
         const int64_t e = e0 + u * 32 + lane;
         const int64_t col = i + __ldg(off + j);
         const bool valid = e < e_end && col >= 0 && col < ncols && x[u] != 0.0;
@@ -409,14 +418,40 @@ struct ArrayAt {
 
 // present != nullptr (DIA target): also the census of diagonals holding at
 // least one entry (L1-cached test-before-set, see the diagonal flags below)
+// Rows [in_lo, in_hi) have every diagonal's column inside the matrix: a
+// group of them counts the nonzero values of its contiguous slot range with
+// 16-B loads and no per-slot offset lookup (the caller passes an empty range
+// when the values are not 16-B aligned or `present` is wanted).
+template <bool INTERIOR>
 __global__ void dia_group_counts(int64_t nrows, int ncols, int nd, const int* __restrict__ off,
                                  const double* __restrict__ vals, int64_t ngroups, int* gcount,
-                                 unsigned char* present) {
+                                 unsigned char* present, int64_t in_lo, int64_t in_hi) {
   const DiaSlots s(ncols, nd, off, vals);
+  const int lane = threadIdx.x & 31;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < ngroups; g += nwarps) {
     const int64_t r0 = g * kDiaGroupRows;
     const int64_t r1 = r0 + kDiaGroupRows < nrows ? r0 + kDiaGroupRows : nrows;
+    if (INTERIOR && r0 >= in_lo && r1 <= in_hi) {
+      const int64_t e0 = r0 * nd, e1 = r1 * nd;   // e0 even: r0 is a multiple of 32
+      const double2* v2 = reinterpret_cast<const double2*>(vals + e0);
+      const int n2 = (int)((e1 - e0) >> 1);
+      int cnt = 0;
+      for (int t0 = 0; t0 < n2; t0 += 32 * kDiaChunks) {
+        double2 x[kDiaChunks];
+#pragma unroll
+        for (int u = 0; u < kDiaChunks; ++u) {
+          const int t = t0 + u * 32 + lane;
+          x[u] = t < n2 ? ld_stream2(reinterpret_cast<const double*>(v2 + t)) : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < kDiaChunks; ++u) cnt += (x[u].x != 0.0) + (x[u].y != 0.0);
+      }
+      if (((e1 - e0) & 1) && lane == 0) cnt += __ldg(vals + e1 - 1) != 0.0;
+      cnt = __reduce_add_sync(0xffffffffu, cnt);
+      if (lane == 0) gcount[g] = cnt;
+      continue;
+    }
     int cnt = 0;
     s.walk(r0, r0 * nd, r1 * nd, [&](bool valid, bool, int64_t, int j, int, double) {
       cnt += __popc(__ballot_sync(0xffffffffu, valid));
@@ -430,6 +465,9 @@ __global__ void dia_group_counts(int64_t nrows, int ncols, int nd, const int* __
   }
 }
 
+// (Round 2: an interior fast path -- two consecutive slots per lane from one
+// 16-B load, offsets in lanes -- was slower, 192^3 DIA->CSR 1.12 -> 1.36 ms:
+// each lane's two stores make every warp store touch twice the sectors.)
 __global__ void dia_group_emit(int64_t nrows, int ncols, int nd, const int* __restrict__ off,
                                const double* __restrict__ vals, int64_t ngroups,
                                const int* __restrict__ gstart, int* row_off, int* r, int* c,
@@ -441,7 +479,7 @@ __global__ void dia_group_emit(int64_t nrows, int ncols, int nd, const int* __re
     const int64_t r0 = g * kDiaGroupRows;
     const int64_t r1 = r0 + kDiaGroupRows < nrows ? r0 + kDiaGroupRows : nrows;
     int base = gstart[g];
-    s.walk(r0, r0 * nd, r1 * nd, [&](bool valid, bool in, int64_t i, int j, int col, double x) {
+    s.template walk<kDiaEmitChunks>(r0, r0 * nd, r1 * nd, [&](bool valid, bool in, int64_t i, int j, int col, double x) {
       const unsigned m = __ballot_sync(0xffffffffu, valid);
       const int pos = base + __popc(m & lt);
       if (row_off && in && j == 0) row_off[i] = pos;
@@ -639,17 +677,6 @@ struct QuadIds {
   unsigned char rid[kCqCap + 4];
 };
 
-__device__ __forceinline__ double2 ld_stream2(const double* p) {
-  double2 v;
-  asm("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
-  return v;
-}
-__device__ __forceinline__ int4 ld_stream4(const int* p) {
-  int4 v;
-  asm("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
-      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
-  return v;
-}
 
 // flag test of one entry: the L1-cached load is predicated (no branch) on
 // `ok` (the column in range); a zero flag is set
@@ -1908,8 +1935,20 @@ static int begin_dia_impl(ds_convert_job* j, int32_t ndiags, const int32_t* offs
       DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&j->scratch), ndiags, st));
       DS_CUDA(cudaMemsetAsync(j->scratch, 0, ndiags, st));
     }
-    dia_group_counts<<<dia_walk_grid(ngroups), 256, 0, st>>>(nrows, (int)ncols, ndiags, offsets,
-                                                             values, ngroups, j->gtmp, j->scratch);
+    // rows whose every diagonal lands inside the matrix (the counts' fast path)
+    int64_t in_lo = 0, in_hi = 0;
+    if (!select && (reinterpret_cast<uintptr_t>(values) & 15) == 0) {
+      const int64_t omin = *std::min_element(h_off.begin(), h_off.end());
+      const int64_t omax = *std::max_element(h_off.begin(), h_off.end());
+      in_lo = std::max<int64_t>(0, -omin);
+      in_hi = std::min<int64_t>(nrows, ncols - omax);
+    }
+    if (in_hi > in_lo)
+      dia_group_counts<true><<<dia_walk_grid(ngroups), 256, 0, st>>>(
+          nrows, (int)ncols, ndiags, offsets, values, ngroups, j->gtmp, nullptr, in_lo, in_hi);
+    else
+      dia_group_counts<false><<<dia_walk_grid(ngroups), 256, 0, st>>>(
+          nrows, (int)ncols, ndiags, offsets, values, ngroups, j->gtmp, j->scratch, 0, 0);
     DS_LAUNCH_CHECK("dia_group_counts");
     int rc = exclusive_scan(ngroups, ArrayAt{j->gtmp}, j->dsrc_start, &nc, st);
     if (rc) return rc;

@@ -366,3 +366,20 @@ def test_csr_census_quads_edges(shift):
         want = O.convert(O.csr(nrows, ncols, offs, c3, vals), O.CSR, fill_limit=BIG)
         got = conv(dev_cols(c3), ds.FormatId.CSR)
         assert_same(got, want, "row boundary")
+
+
+@pytest.mark.parametrize("nrows,ncols,nd", [(5000, 5000, 1), (4099, 4000, 2), (3001, 3100, 7),
+                                            (6000, 5990, 27), (2080, 2100, 32)])
+def test_dia_source_banded_interior_groups(nrows, ncols, nd):
+    """Narrow bands: most 32-row groups have every diagonal in range (the
+    counts / emit interior path: 16-B loads, offsets in lanes), the first and
+    last groups do not; zeros and -0.0 dropped, odd slot counts."""
+    rng = np.random.default_rng(nrows + nd)
+    offs = np.sort(rng.choice(np.arange(-40, 41), size=nd, replace=False)).astype(np.int64)
+    vals = rng.standard_normal((nrows, nd))
+    vals[rng.random(vals.shape) < 0.15] = 0.0
+    vals[rng.random(vals.shape) < 0.05] = -0.0
+    src = ds.DiaMatrix(nrows, ncols, offs, vals, ds.MemorySpace.DEVICE, DEV)
+    ora = O.dia(nrows, ncols, offs, vals)
+    for tgt, fid in ((O.CSR, ds.FormatId.CSR), (O.COO, ds.FormatId.COO)):
+        assert_same(ds.convert(src, fid), O.convert(ora, tgt), (nrows, nd, fid))
