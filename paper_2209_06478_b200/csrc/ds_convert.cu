@@ -678,13 +678,21 @@ struct QuadIds {
 };
 
 
-// flag test of one entry: the L1-cached load is predicated (no branch) on
-// `ok` (the column in range); a zero flag is set
-__device__ __forceinline__ void census_flag(unsigned char* flags, unsigned d, bool ok) {
-  unsigned short f = 1;
-  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t@p ld.global.ca.u8 %0, [%1];\n\t}"
-               : "+h"(f) : "l"(flags + d), "r"((int)ok));
-  if (f == 0) flags[d] = 1;
+// flag test of one entry: a per-CTA shared-memory tag table of recently set
+// diagonals first (the stencil's 27 diagonals stay resident: one shared load
+// per entry), then the L1-cached global test-before-set, predicated (no
+// branch) on `ok` (the column in range).  A tag is written only after its
+// flag was tested / set, so a tag hit always means the flag is set.
+constexpr int kFlagTagBits = 10;
+__device__ __forceinline__ void census_flag(unsigned char* flags, unsigned d, bool ok,
+                                            unsigned* tags) {
+  const unsigned h = (d * 0x9E3779B1u) >> (32 - kFlagTagBits);
+  if (ok && tags[h] != d) {
+    unsigned short f;
+    asm volatile("ld.global.ca.u8 %0, [%1];" : "=h"(f) : "l"(flags + d));
+    if (f == 0) flags[d] = 1;
+    tags[h] = d;
+  }
 }
 
 // COPY (ds_convert_direct, a canonical CSR source to a COO / CSR target):
@@ -700,8 +708,12 @@ __global__ void __launch_bounds__(256)
                      int* __restrict__ ocol = nullptr, double* __restrict__ oval = nullptr) {
   constexpr int U = COPY ? 2 : kCqU;
   __shared__ QuadIds ids;
+  __shared__ unsigned tags[FLAGS ? 1 << kFlagTagBits : 1];
   const int lane = threadIdx.x & 31;
   const int tid = threadIdx.x;
+  if (FLAGS)
+    for (int i = tid; i < (1 << kFlagTagBits); i += blockDim.x) tags[i] = 0xffffffffu;
+  // (the tile loop's first barrier orders the tag reset before any lookup)
   // entry k lives in address quad (k + s) >> 2
   const int s = (int)((reinterpret_cast<uintptr_t>(c) >> 2) & 3);
   int mybad = 0;
@@ -784,7 +796,7 @@ __global__ void __launch_bounds__(256)
               const bool inr = (unsigned)ce[e] < (unsigned)ncols;
               mybad |= (valid && same && pc >= ce[e]) ? kBadOrder : 0;
               mybad |= (valid && !inr) ? kBadIndex : 0;
-              if (FLAGS) census_flag(flags, (unsigned)ce[e] - (unsigned)t + dbase, valid && inr);
+              if (FLAGS) census_flag(flags, (unsigned)ce[e] - (unsigned)t + dbase, valid && inr, tags);
               if (COPY && !full && valid) {
                 ocol[k] = ce[e];
                 __stcs(oval + k, ve[u][e]);
