@@ -41,6 +41,7 @@ struct ds_convert_job {
   const int* dsrc_off = nullptr;
   const double* dsrc_vals = nullptr;
   int dsrc_nd = 0;
+  int64_t dsrc_in_lo = 0, dsrc_in_hi = 0;   // rows whose every diagonal is in range
   int* dsrc_start = nullptr;   // first entry of each row group (ceil(nrows / kDiaGroupRows))
   // canonical CSR source, DIA target: no COO proxy at all; the diagonal
   // census is taken while checking the order, the slab is filled per row
@@ -396,11 +397,12 @@ __global__ void __launch_bounds__(128)
 // (jsrc[t] = source column of target diagonal t); a slot keeps its value iff
 // it is in range and nonzero (-0.0 and padding become +0.0, exactly as the
 // canonical COO proxy's zero fill).  Thread per target slot, coalesced stores.
-__global__ void dia_copy_diags(int64_t nrows, int ncols, int nd, int nd_out,
+// rows [row0, row1) of the selection
+__global__ void dia_copy_diags(int64_t row0, int64_t row1, int ncols, int nd, int nd_out,
                                const int* __restrict__ off, const double* __restrict__ vals,
                                const int* __restrict__ jsrc, double* out) {
-  const int64_t total = nrows * nd_out;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+  const int64_t total = row1 * nd_out;
+  for (int64_t t = row0 * nd_out + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = total < (int64_t(1) << 32) ? (int64_t)((unsigned)t / (unsigned)nd_out)
                                                  : t / nd_out;
@@ -408,6 +410,27 @@ __global__ void dia_copy_diags(int64_t nrows, int ncols, int nd, int nd_out,
     const int64_t col = i + __ldg(off + j);
     const double x = __ldg(vals + i * nd + j);
     out[t] = (col >= 0 && col < ncols && x != 0.0) ? x : 0.0;
+  }
+}
+
+// every diagonal kept, rows whose columns are all in range: the selection
+// is the slab itself with -0.0 turned into +0.0 (a 16-B stream over the
+// slots [s0, s1); s0 even, values 16-B aligned)
+__global__ void dia_copy_interior(int64_t s0, int64_t s1, const double* __restrict__ vals,
+                                  double* __restrict__ out) {
+  const int64_t n2 = (s1 - s0) >> 1;
+  const double2* v2 = reinterpret_cast<const double2*>(vals + s0);
+  double2* o2 = reinterpret_cast<double2*>(out + s0);
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n2;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    double2 x = ld_stream2(reinterpret_cast<const double*>(v2 + t));
+    x.x = x.x != 0.0 ? x.x : 0.0;
+    x.y = x.y != 0.0 ? x.y : 0.0;
+    __stcs(o2 + t, x);
+  }
+  if (((s1 - s0) & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const double x = __ldg(vals + s1 - 1);
+    out[s1 - 1] = x != 0.0 ? x : 0.0;
   }
 }
 
@@ -437,6 +460,11 @@ __global__ void dia_group_counts(int64_t nrows, int ncols, int nd, const int* __
       const double2* v2 = reinterpret_cast<const double2*>(vals + e0);
       const int n2 = (int)((e1 - e0) >> 1);
       int cnt = 0;
+      // present (DIA target, nd <= 32): lane bit j = a nonzero on diagonal j;
+      // a lane's slots advance by 64 per step, so its diagonal advances by 64 % nd
+      unsigned mask = 0;
+      int j0 = present ? (2 * lane) % nd : 0;
+      const int rm = present ? 64 % nd : 0;
       for (int t0 = 0; t0 < n2; t0 += 32 * kDiaChunks) {
         double2 x[kDiaChunks];
 #pragma unroll
@@ -445,11 +473,31 @@ __global__ void dia_group_counts(int64_t nrows, int ncols, int nd, const int* __
           x[u] = t < n2 ? ld_stream2(reinterpret_cast<const double*>(v2 + t)) : make_double2(0.0, 0.0);
         }
 #pragma unroll
-        for (int u = 0; u < kDiaChunks; ++u) cnt += (x[u].x != 0.0) + (x[u].y != 0.0);
+        for (int u = 0; u < kDiaChunks; ++u) {
+          cnt += (x[u].x != 0.0) + (x[u].y != 0.0);
+          if (present) {
+            const int j1 = j0 + 1 == nd ? 0 : j0 + 1;
+            mask |= ((unsigned)(x[u].x != 0.0) << j0) | ((unsigned)(x[u].y != 0.0) << j1);
+            j0 += rm;
+            if (j0 >= nd) j0 -= nd;
+          }
+        }
       }
-      if (((e1 - e0) & 1) && lane == 0) cnt += __ldg(vals + e1 - 1) != 0.0;
+      if (((e1 - e0) & 1) && lane == 0) {   // the odd last slot: diagonal nd - 1
+        const bool nz = __ldg(vals + e1 - 1) != 0.0;
+        cnt += nz;
+        mask |= (unsigned)nz << (nd - 1);
+      }
       cnt = __reduce_add_sync(0xffffffffu, cnt);
       if (lane == 0) gcount[g] = cnt;
+      if (present) {
+        mask = __reduce_or_sync(0xffffffffu, mask);
+        if (lane < nd && ((mask >> lane) & 1u)) {
+          unsigned short f;
+          asm volatile("ld.global.ca.u8 %0, [%1];" : "=h"(f) : "l"(present + lane));
+          if (f == 0) present[lane] = 1;
+        }
+      }
       continue;
     }
     int cnt = 0;
@@ -1953,7 +2001,7 @@ static int begin_dia_impl(ds_convert_job* j, int32_t ndiags, const int32_t* offs
     }
     // rows whose every diagonal lands inside the matrix (the counts' fast path)
     int64_t in_lo = 0, in_hi = 0;
-    if (!select && (reinterpret_cast<uintptr_t>(values) & 15) == 0) {
+    if ((!select || ndiags <= 32) && (reinterpret_cast<uintptr_t>(values) & 15) == 0) {
       const int64_t omin = *std::min_element(h_off.begin(), h_off.end());
       const int64_t omax = *std::max_element(h_off.begin(), h_off.end());
       in_lo = std::max<int64_t>(0, -omin);
@@ -1961,7 +2009,7 @@ static int begin_dia_impl(ds_convert_job* j, int32_t ndiags, const int32_t* offs
     }
     if (in_hi > in_lo)
       dia_group_counts<true><<<dia_walk_grid(ngroups), 256, 0, st>>>(
-          nrows, (int)ncols, ndiags, offsets, values, ngroups, j->gtmp, nullptr, in_lo, in_hi);
+          nrows, (int)ncols, ndiags, offsets, values, ngroups, j->gtmp, j->scratch, in_lo, in_hi);
     else
       dia_group_counts<false><<<dia_walk_grid(ngroups), 256, 0, st>>>(
           nrows, (int)ncols, ndiags, offsets, values, ngroups, j->gtmp, j->scratch, 0, 0);
@@ -1973,6 +2021,8 @@ static int begin_dia_impl(ds_convert_job* j, int32_t ndiags, const int32_t* offs
     j->dsrc_off = offsets;
     j->dsrc_vals = values;
     j->dsrc_nd = ndiags;
+    j->dsrc_in_lo = in_lo;
+    j->dsrc_in_hi = in_hi;
     if (select) {
       std::vector<unsigned char> h_present(ndiags);
       DS_CUDA(cudaMemcpyAsync(h_present.data(), j->scratch, ndiags, cudaMemcpyDeviceToHost, st));
@@ -2123,9 +2173,26 @@ static int finish_dia_impl(ds_convert_job* job, int32_t* offsets, double* values
                             st));
     const int64_t slots = nd * job->nrows;
     if (job->dia_jsrc) {   // DIA source: the selected columns, masked
-      dia_copy_diags<<<grid1d(slots), 256, 0, st>>>(job->nrows, (int)job->ncols, job->dsrc_nd,
-                                                    (int)nd, job->dsrc_off, job->dsrc_vals,
-                                                    job->dia_jsrc, values);
+      // every diagonal kept: the in-range rows are a plain stream of the slab
+      const bool all = nd == job->dsrc_nd && job->dsrc_in_hi > job->dsrc_in_lo &&
+                       (reinterpret_cast<uintptr_t>(values) & 15) == 0;
+      const int64_t lo = all ? job->dsrc_in_lo : job->nrows, hi = all ? job->dsrc_in_hi : job->nrows;
+      if (all) {
+        const int64_t a = lo * nd + ((lo * nd) & 1), b = hi * nd;   // even start
+        dia_copy_interior<<<grid1d((b - a) / 2), 256, 0, st>>>(a, b, job->dsrc_vals, values);
+        DS_LAUNCH_CHECK("dia_copy_interior");
+        if (a > lo * nd)   // the odd first slot of the interior goes with the head rows
+          dia_copy_diags<<<1, 32, 0, st>>>(lo, lo + 1, (int)job->ncols, job->dsrc_nd, (int)nd,
+                                           job->dsrc_off, job->dsrc_vals, job->dia_jsrc, values);
+      }
+      if (lo > 0)
+        dia_copy_diags<<<grid1d(lo * nd), 256, 0, st>>>(0, lo, (int)job->ncols, job->dsrc_nd,
+                                                        (int)nd, job->dsrc_off, job->dsrc_vals,
+                                                        job->dia_jsrc, values);
+      if (hi < job->nrows)
+        dia_copy_diags<<<grid1d((job->nrows - hi) * nd), 256, 0, st>>>(
+            hi, job->nrows, (int)job->ncols, job->dsrc_nd, (int)nd, job->dsrc_off, job->dsrc_vals,
+            job->dia_jsrc, values);
       DS_LAUNCH_CHECK("dia_copy_diags");
       return DS_OK;
     }

@@ -381,5 +381,16 @@ def test_dia_source_banded_interior_groups(nrows, ncols, nd):
     vals[rng.random(vals.shape) < 0.05] = -0.0
     src = ds.DiaMatrix(nrows, ncols, offs, vals, ds.MemorySpace.DEVICE, DEV)
     ora = O.dia(nrows, ncols, offs, vals)
-    for tgt, fid in ((O.CSR, ds.FormatId.CSR), (O.COO, ds.FormatId.COO)):
+    for tgt, fid in ((O.CSR, ds.FormatId.CSR), (O.COO, ds.FormatId.COO),
+                     (O.DIA, ds.FormatId.DIA)):
         assert_same(ds.convert(src, fid), O.convert(ora, tgt), (nrows, nd, fid))
+    # DIA -> DIA with one diagonal all zero (dropped: the masked selection)
+    # and with one diagonal nonzero only in the last row
+    if nd > 1:
+        v2 = vals.copy()
+        v2[:, nd // 2] = 0.0
+        v2[:, 0] = 0.0
+        v2[-1, 0] = 3.0
+        src = ds.DiaMatrix(nrows, ncols, offs, v2, ds.MemorySpace.DEVICE, DEV)
+        want = O.convert(O.dia(nrows, ncols, offs, v2), O.DIA)
+        assert_same(ds.convert(src, ds.FormatId.DIA), want, (nrows, nd, "drop"))
