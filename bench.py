@@ -153,6 +153,27 @@ def coo_bytes(n: int, ncols: int, nnz: int) -> int:
     return 16 * nnz + 8 * ncols + 8 * n
 
 
+def format_array_bytes(fmt: str, n: int, nnz: int, ndiags: int) -> int:
+    """Bytes of a matrix's arrays (int32 indices, f64 values)."""
+    if fmt == "csr":
+        return 4 * (n + 1) + 12 * nnz
+    if fmt == "coo":
+        return 16 * nnz
+    return 8 * n * ndiags + 4 * ndiags
+
+
+def convert_floor(pairs_ms: dict, n: int, nnz: int, ndiags: int, peak_gbs: float) -> dict:
+    """Each conversion against its byte floor: the source's arrays read once
+    and the target's written once at the measured copy bandwidth."""
+    out = {}
+    for pair, ms in pairs_ms.items():
+        a, b = pair.split("->")
+        by = format_array_bytes(a, n, nnz, ndiags) + format_array_bytes(b, n, nnz, ndiags)
+        floor_ms = by / (peak_gbs * 1e9) * 1e3
+        out[pair] = {"bytes": by, "floor_ms": round(floor_ms, 3), "frac": round(floor_ms / ms, 3)}
+    return out
+
+
 def build_rank(ds, spec, rank, dev, local_fmt, remote_fmt):
     """This rank's partition on the device, split and converted (host setup)."""
     part = ds.generate_partition(spec, rank, space=ds.MemorySpace.DEVICE, device=dev)
@@ -240,6 +261,7 @@ def sweep_104(ds, torch, a_full, dev, peak, cpu=None):
             "csr->coo": _gpu_ms(torch, lambda: ds.convert(mats["csr"], F.COO)),
             "coo->csr": _gpu_ms(torch, lambda: ds.convert(mats["coo"], F.CSR))}
     out["convert_ms"] = conv
+    out["convert_vs_byte_floor"] = convert_floor(conv, n, a_full.nnz, mats["dia"].ndiags, peak)
     if cpu and "convert_ms" in cpu:
         out["cpu_convert_ms"] = cpu["convert_ms"]
         out["cpu_cores"] = cpu["cores"]

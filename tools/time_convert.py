@@ -22,4 +22,9 @@ for src in ("csr", "coo", "dia"):
             torch.cuda.synchronize()
             ts.append(time.perf_counter() - t0)
         out[f"{src}->{dst}"] = round(min(ts) * 1e3, 3)
-print(json.dumps({"nx": nx, "convert_ms": out}))
+import bench  # noqa: E402
+peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                   "MEASURED_PEAKS.json")))["hbm_gbs"]
+fl = bench.convert_floor(out, part.a_full.nrows, part.a_full.nnz, mats["dia"].ndiags, peak)
+print(json.dumps({"nx": nx, "convert_ms": out,
+                  "frac_of_byte_floor": {k: v["frac"] for k, v in fl.items()}}))
