@@ -573,6 +573,8 @@ __global__ void rows_to_offsets(int64_t nnz, int nrows, const int* __restrict__ 
 // ndiags)).  The fill walks the entries of a warp's rows 32 at a time
 // (coalesced, U chunks of loads in flight), finding each entry's row by a
 // shuffle search over the warp's offsets.
+// shared-memory caches of diagonal flags / diag_map entries: 2^kFlagTagBits slots
+constexpr int kFlagTagBits = 10;
 constexpr int kCsrWalkRows = 16;    // rows per warp (<= 31: the offsets live in one lane each)
 // Lane t <= r1 - r0 holds off[r0 + t] (the rest INT_MAX): an entry's row is
 // found by a 5-step binary search over the lanes (shuffles, no memory).  The
@@ -629,6 +631,10 @@ __global__ void dia_fill_csr(int nrows, int nd, int R, const int* __restrict__ o
                              const int* __restrict__ c, const double* __restrict__ v,
                              const int* __restrict__ map, double* vals) {
   extern __shared__ double slab[];   // R * nd, R = kCsrWalkRows * warps per block
+  // recently used diag_map entries, (j << 32 | d) in one 64-bit word so a
+  // racing writer can never pair one diagonal's key with another's column
+  __shared__ unsigned long long mcache[1 << kFlagTagBits];
+  for (int i = threadIdx.x; i < (1 << kFlagTagBits); i += blockDim.x) mcache[i] = ~0ull;
   const int warp = threadIdx.x >> 5;
   int ot = walk_offsets(off, nrows, blockIdx.x * R + warp * kCsrWalkRows);
   for (int b0 = blockIdx.x * R; b0 < nrows; b0 += gridDim.x * R) {
@@ -645,10 +651,20 @@ __global__ void dia_fill_csr(int nrows, int nd, int R, const int* __restrict__ o
                          const int lane = threadIdx.x & 31;
                          int j[4];
 #pragma unroll
-                         for (int u = 0; u < 4; ++u)   // the map loads in flight together
-                           j[u] = kb + 32 * u + lane < k1
-                                      ? __ldg(map + ((int64_t)e[u].c - rr[u] + nrows - 1))
-                                      : 0;
+                         for (int u = 0; u < 4; ++u) {
+                           j[u] = 0;
+                           if (kb + 32 * u + lane < k1) {
+                             const unsigned d = (unsigned)e[u].c - (unsigned)rr[u] + (unsigned)(nrows - 1);
+                             const unsigned h = (d * 0x9E3779B1u) >> (32 - kFlagTagBits);
+                             const unsigned long long m = mcache[h];
+                             if ((unsigned)m == d) {
+                               j[u] = (int)(m >> 32);
+                             } else {
+                               j[u] = __ldg(map + d);
+                               mcache[h] = ((unsigned long long)(unsigned)j[u] << 32) | d;
+                             }
+                           }
+                         }
 #pragma unroll
                          for (int u = 0; u < 4; ++u)
                            if (kb + 32 * u + lane < k1) slab[(rr[u] - b0) * nd + j[u]] = e[u].v;
@@ -731,7 +747,6 @@ struct QuadIds {
 // per entry), then the L1-cached global test-before-set, predicated (no
 // branch) on `ok` (the column in range).  A tag is written only after its
 // flag was tested / set, so a tag hit always means the flag is set.
-constexpr int kFlagTagBits = 10;
 __device__ __forceinline__ void census_flag(unsigned char* flags, unsigned d, bool ok,
                                             unsigned* tags) {
   const unsigned h = (d * 0x9E3779B1u) >> (32 - kFlagTagBits);
@@ -2209,6 +2224,10 @@ static int finish_dia_impl(ds_convert_job* job, int32_t* offsets, double* values
     }
     const int R = kCsrWalkRows * 8;   // 8 warps
     if (job->csr_off && (int64_t)R * nd * 8 <= 48 * 1024) {
+      if ((int64_t)R * nd * 8 > 40 * 1024) {   // + the 8 KB map cache
+        int rc = allow_dynamic_smem((const void*)dia_fill_csr, (size_t)R * nd * 8);
+        if (rc) return rc;
+      }
       dia_fill_csr<<<csr_walk_grid(job->nrows), 256, (size_t)R * nd * 8, st>>>(
           (int)job->nrows, (int)nd, R, job->csr_off, job->c, job->v, job->diag_map, values);
       DS_LAUNCH_CHECK("dia_fill_csr");
