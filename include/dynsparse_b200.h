@@ -38,8 +38,10 @@ enum {
   DS_ERR_STRUCTURALLY_ABSENT_DIAG = 4,  /* StructurallyAbsentDiagonal errors.py:73-78    */
   DS_ERR_BREAKDOWN = 5,                 /* BreakdownZeroCurvature errors.py:81-82        */
   DS_ERR_NOT_SUPPORTED = 6,             /* dims >= 2^31 or a layout the kernels refuse   */
-  DS_ERR_INDEX_OUT_OF_RANGE = 7         /* IndexOutOfRange errors.py:17: an entry's row /
+  DS_ERR_INDEX_OUT_OF_RANGE = 7,        /* IndexOutOfRange errors.py:17: an entry's row /
                                            column outside the shape (conversion sources)  */
+  DS_ERR_RETRY = 8                      /* a speculative fast path did not apply: run the
+                                           general entry point (never surfaces in Python) */
 };
 
 /* Message of the last failing call on this host thread ("" if none). */
@@ -206,6 +208,19 @@ int ds_convert_direct(int src_format, int target, int64_t nrows, int64_t ncols, 
                       const int32_t* src_idx, const int32_t* cols, const double* values,
                       int32_t* out_idx, int32_t* out_cols, double* out_values, void* stream,
                       int* done);
+/* Speculative CSR -> DIA: the diagonal set is taken from a sample of row
+ * tiles (every ntiles/256-th 128-row tile and the last) and finish_dia
+ * fills the slab in ONE pass that also checks the order, the index range and
+ * that no entry lies outside the sampled set (the sample is a subset of the
+ * true set, so no miss means equal).  DS_ERR_RETRY from begin (empty source,
+ * arrays not 16-B aligned, fill limit exceeded by the sample, > 160 sampled
+ * diagonals) or from finish_dia (a miss, not canonical): the target is
+ * garbage -- run ds_convert_begin_csr / finish_dia.  Otherwise the result is
+ * the census path's, bit for bit.                                           */
+int ds_convert_begin_csr_dia_spec(int64_t nrows, int64_t ncols, int64_t nnz,
+                                  const int32_t* row_offsets, const int32_t* cols,
+                                  const double* values, int64_t fill_limit, void* stream,
+                                  ds_convert_job** job, int64_t* out_ndiags);
 int ds_convert_finish_coo(ds_convert_job* job, int32_t* rows, int32_t* cols, double* values);
 int ds_convert_finish_csr(ds_convert_job* job, int32_t* row_offsets, int32_t* cols,
                           double* values);

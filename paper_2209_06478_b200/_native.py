@@ -32,6 +32,7 @@ DS_ERR_STRUCTURALLY_ABSENT_DIAG = 4
 DS_ERR_BREAKDOWN = 5
 DS_ERR_NOT_SUPPORTED = 6
 DS_ERR_INDEX_OUT_OF_RANGE = 7
+DS_ERR_RETRY = 8   # a speculative fast path did not apply (handled by the caller)
 DS_FILL_LIMIT_DEFAULT = -(2**63)   # include/dynsparse_b200.h: the reference default limit
 
 DS_CG_STAGE_NONE, DS_CG_STAGE_PAP, DS_CG_STAGE_RR, DS_CG_STAGE_SETUP = 0, 1, 2, 3
@@ -115,6 +116,8 @@ _SIGNATURES = {
                                      ctypes.POINTER(c_vp), P_i64, P_i64]),
     "ds_convert_begin_dia": (c_int, [c_i64, c_i64, c_i32, c_vp, c_vp, c_int, c_i64, c_vp,
                                      ctypes.POINTER(c_vp), P_i64, P_i64]),
+    "ds_convert_begin_csr_dia_spec": (c_int, [c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_i64, c_vp,
+                                              ctypes.POINTER(c_vp), P_i64]),
     "ds_convert_direct": (c_int, [c_int, c_int, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp,
                                   c_vp, c_vp, P_i32]),
     "ds_convert_finish_coo": (c_int, [c_vp, c_vp, c_vp, c_vp]),

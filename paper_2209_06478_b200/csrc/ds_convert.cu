@@ -32,6 +32,7 @@ struct ds_convert_job {
   int* c = nullptr;
   double* v = nullptr;
   bool own_r = false, own_c = false, own_v = false;
+  bool spec = false;           // speculative CSR -> DIA (diagonal set from sampled tiles)
   int64_t ndiags = 0;          // DIA target
   int* diag_map = nullptr;     // exclusive scan of diagonal presence (nrows+ncols-1)
   int* dia_off = nullptr;      // (ndiags)
@@ -625,17 +626,27 @@ struct ColVal {
 // *bad bits: kBadOrder (not canonical), kBadIndex (a column outside [0, ncols):
 // nothing is marked for it, the caller raises IndexOutOfRange)
 constexpr int kBadOrder = 1, kBadIndex = 2, kBadRowOrder = 4;   // 4: rows decrease somewhere
+constexpr int kBadMiss = 8;   // a diagonal outside the speculative set (dia_fill_csr<true>)
 
 
+// CHECK (the speculative CSR -> DIA, ds_convert_begin_csr_dia_spec): the
+// walk also checks the order ((row, col) strictly increasing in every row),
+// the column range and that every entry's diagonal is in `map` (the
+// exclusive scan of the sampled presence: d present iff map[d+1] > map[d]),
+// setting kBadOrder / kBadIndex / kBadMiss in *bad instead of storing.
+template <bool CHECK>
 __global__ void dia_fill_csr(int nrows, int nd, int R, const int* __restrict__ off,
                              const int* __restrict__ c, const double* __restrict__ v,
-                             const int* __restrict__ map, double* vals) {
+                             const int* __restrict__ map, double* vals, int ncols = 0,
+                             int* bad = nullptr) {
   extern __shared__ double slab[];   // R * nd, R = kCsrWalkRows * warps per block
   // recently used diag_map entries, (j << 32 | d) in one 64-bit word so a
   // racing writer can never pair one diagonal's key with another's column
   __shared__ unsigned long long mcache[1 << kFlagTagBits];
   for (int i = threadIdx.x; i < (1 << kFlagTagBits); i += blockDim.x) mcache[i] = ~0ull;
   const int warp = threadIdx.x >> 5;
+  const unsigned D = (unsigned)nrows + (unsigned)ncols - 1u;
+  int mybad = 0;
   int ot = walk_offsets(off, nrows, blockIdx.x * R + warp * kCsrWalkRows);
   for (int b0 = blockIdx.x * R; b0 < nrows; b0 += gridDim.x * R) {
     const int rows = min(R, nrows - b0);
@@ -646,14 +657,34 @@ __global__ void dia_fill_csr(int nrows, int nd, int R, const int* __restrict__ o
     __syncthreads();
     if (r0 < b0 + rows) {
       const int r1 = min(r0 + kCsrWalkRows, b0 + rows);
+      int carry = -1, carry_row = -1;   // CHECK: the previous chunk's last entry (lane 31)
       csr_warp_walk<4>(ot, r0, r1, [&](int k) { return ColVal{__ldg(c + k), __ldg(v + k)}; },
                        [&](int kb, int k1, const int (&rr)[4], const ColVal (&e)[4]) {
                          const int lane = threadIdx.x & 31;
                          int j[4];
+                         bool ok[4];
 #pragma unroll
                          for (int u = 0; u < 4; ++u) {
                            j[u] = 0;
-                           if (kb + 32 * u + lane < k1) {
+                           ok[u] = kb + 32 * u + lane < k1;
+                           if (CHECK) {
+                             int prev = __shfl_up_sync(0xffffffffu, e[u].c, 1);
+                             int prev_row = __shfl_up_sync(0xffffffffu, rr[u], 1);
+                             if (lane == 0) {
+                               prev = carry;
+                               prev_row = carry_row;
+                             }
+                             carry = __shfl_sync(0xffffffffu, e[u].c, 31);
+                             carry_row = __shfl_sync(0xffffffffu, rr[u], 31);
+                             if (ok[u]) {
+                               if (prev_row == rr[u] && prev >= e[u].c) mybad |= kBadOrder;
+                               if ((unsigned)e[u].c >= (unsigned)ncols) {
+                                 mybad |= kBadIndex;
+                                 ok[u] = false;
+                               }
+                             }
+                           }
+                           if (ok[u]) {
                              const unsigned d = (unsigned)e[u].c - (unsigned)rr[u] + (unsigned)(nrows - 1);
                              const unsigned h = (d * 0x9E3779B1u) >> (32 - kFlagTagBits);
                              const unsigned long long m = mcache[h];
@@ -661,13 +692,21 @@ __global__ void dia_fill_csr(int nrows, int nd, int R, const int* __restrict__ o
                                j[u] = (int)(m >> 32);
                              } else {
                                j[u] = __ldg(map + d);
+                               if (CHECK) {
+                                 const int jn = d + 1 < D ? __ldg(map + d + 1) : nd;
+                                 if (jn == j[u]) j[u] = -1;
+                               }
                                mcache[h] = ((unsigned long long)(unsigned)j[u] << 32) | d;
+                             }
+                             if (CHECK && j[u] < 0) {
+                               mybad |= kBadMiss;
+                               ok[u] = false;
                              }
                            }
                          }
 #pragma unroll
                          for (int u = 0; u < 4; ++u)
-                           if (kb + 32 * u + lane < k1) slab[(rr[u] - b0) * nd + j[u]] = e[u].v;
+                           if (ok[u]) slab[(rr[u] - b0) * nd + j[u]] = e[u].v;
                        });
     }
     __syncthreads();
@@ -675,6 +714,10 @@ __global__ void dia_fill_csr(int nrows, int nd, int R, const int* __restrict__ o
     for (int t = threadIdx.x; t < total; t += blockDim.x) out[t] = slab[t];
     __syncthreads();
     ot = ot_next;
+  }
+  if (CHECK) {
+    mybad = __reduce_or_sync(0xffffffffu, mybad);
+    if ((threadIdx.x & 31) == 0 && mybad) atomicOr(bad, mybad);
   }
 }
 
@@ -768,8 +811,10 @@ __global__ void __launch_bounds__(256)
     csr_census_quads(int nrows, int ncols, int64_t nnz, const int* __restrict__ off,
                      const int* __restrict__ c, unsigned char* flags, int* bad,
                      const double* __restrict__ v = nullptr, int* __restrict__ orow = nullptr,
-                     int* __restrict__ ocol = nullptr, double* __restrict__ oval = nullptr) {
-  constexpr int U = COPY ? 2 : kCqU;
+                     int* __restrict__ ocol = nullptr, double* __restrict__ oval = nullptr,
+                     int tile0 = 0, int tile_step = 1) {
+  constexpr bool LOADV = COPY;
+  constexpr int U = LOADV ? 2 : kCqU;
   __shared__ QuadIds ids;
   __shared__ unsigned tags[FLAGS ? 1 << kFlagTagBits : 1];
   const int lane = threadIdx.x & 31;
@@ -781,15 +826,15 @@ __global__ void __launch_bounds__(256)
   const int s = (int)((reinterpret_cast<uintptr_t>(c) >> 2) & 3);
   int mybad = 0;
   const int ntiles = (nrows + kRT - 1) / kRT;
-  int tile = blockIdx.x;
+  int tile = tile0 + (int)blockIdx.x * tile_step;
   int o_next = 0;
   if (tile < ntiles && tid <= min(kRT, nrows - tile * kRT)) o_next = __ldg(off + tile * kRT + tid);
-  for (; tile < ntiles; tile += gridDim.x) {
+  for (; tile < ntiles; tile += (int)gridDim.x * tile_step) {
     const int r0 = tile * kRT;
     const int nr = min(kRT, nrows - r0);
     if (tid <= nr) ids.off[tid] = o_next;
     {
-      const int nt = tile + gridDim.x;
+      const int nt = tile + (int)gridDim.x * tile_step;
       if (nt < ntiles && tid <= min(kRT, nrows - nt * kRT)) o_next = __ldg(off + nt * kRT + tid);
     }
     __syncthreads();
@@ -809,26 +854,26 @@ __global__ void __launch_bounds__(256)
       for (int qb = 0; qb < nq; qb += (int)blockDim.x * U) {
         int4 cv[U];
         int pv[U];
-        double ve[COPY ? U : 1][4];
+        double ve[LOADV ? U : 1][4];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int q = qb + u * (int)blockDim.x + tid;
           const int kq = kq0 + 4 * q;
           if (q < nq && kq >= k0 && kq + 3 < kend) {
             cv[u] = ld_stream4(reinterpret_cast<const int*>(cq + q));
-            if (COPY) {
+            if (LOADV) {
               const double2 a = ld_stream2(v + kq), b = ld_stream2(v + kq + 2);
               ve[u][0] = a.x; ve[u][1] = a.y; ve[u][2] = b.x; ve[u][3] = b.y;
             }
           } else {
             cv[u] = make_int4(0, 0, 0, 0);
-            if (COPY) ve[u][0] = ve[u][1] = ve[u][2] = ve[u][3] = 0.0;
+            if (LOADV) ve[u][0] = ve[u][1] = ve[u][2] = ve[u][3] = 0.0;
             if (q < nq) {   // a quad across the chunk's head or tail: entries one by one
               if (kq >= k0) cv[u].x = ld_stream(c + kq);
               if (kq + 1 >= k0 && kq + 1 < kend) cv[u].y = ld_stream(c + kq + 1);
               if (kq + 2 >= k0 && kq + 2 < kend) cv[u].z = ld_stream(c + kq + 2);
               if (kq + 3 < kend) cv[u].w = ld_stream(c + kq + 3);
-              if (COPY) {
+              if (LOADV) {
 #pragma unroll
                 for (int e = 0; e < 4; ++e)
                   if (kq + e >= k0 && kq + e < kend) ve[u][e] = ld_stream(v + kq + e);
@@ -1917,6 +1962,73 @@ extern "C" int ds_convert_begin_csr(int64_t nrows, int64_t ncols, int64_t nnz,
   return DS_OK;
 }
 
+// ------------------------------------------- speculative CSR -> DIA ------
+// The census pass exists only to learn the diagonal set before the slab is
+// sized.  Speculation: take the census of a sample of row tiles (every
+// ntiles/256-th and the last), size the target by it, and let finish_dia run
+// ONE pass that checks the order, the index range and that every entry's
+// diagonal is in the sampled set while it fills the slab.  A sampled set is
+// a subset of the true one, so "no entry outside it" means they are equal;
+// otherwise finish returns DS_ERR_RETRY and the caller runs begin_csr /
+// finish_dia (the census path).  A fill-limit overflow of the sample also
+// returns DS_ERR_RETRY (the census path raises it with the true count).
+extern "C" int ds_convert_begin_csr_dia_spec(int64_t nrows, int64_t ncols, int64_t nnz,
+                                             const int32_t* row_offsets, const int32_t* cols,
+                                             const double* values, int64_t fill_limit,
+                                             void* stream, ds_convert_job** job,
+                                             int64_t* out_ndiags) {
+  *job = nullptr;
+  *out_ndiags = 0;
+  if (fill_limit == kDefaultFillLimit) fill_limit = 10 * std::max(nnz, nrows);   // datamove.py:55-57
+  if (!dims_ok(nrows, ncols, nnz)) return DS_ERR_NOT_SUPPORTED;
+  if (nnz <= 0 || nrows <= 0 || (reinterpret_cast<uintptr_t>(values) & 15) ||
+      (reinterpret_cast<uintptr_t>(cols) & 15))
+    return DS_ERR_RETRY;
+  ds_convert_job* j = new_job(nrows, ncols, DS_FMT_DIA, stream);
+  cudaStream_t st = j->st;
+  const int64_t flag_bytes = (nrows + ncols - 1 + 3) & ~int64_t(3);
+  int rc = DS_OK;
+  do {
+    if (cudaMallocAsync(reinterpret_cast<void**>(&j->flags), flag_bytes + 4, st) != cudaSuccess ||
+        cudaMemsetAsync(j->flags, 0, flag_bytes + 4, st) != cudaSuccess) {
+      rc = cuda_fail(cudaGetLastError(), "speculative census flags");
+      break;
+    }
+    int* bad = reinterpret_cast<int*>(j->flags + flag_bytes);   // ignored: finish re-checks
+    const int ntiles = (int)ceil_div(nrows, kRT);
+    const int S = std::min(ntiles, 256), step = std::max(1, ntiles / S);
+    csr_census_quads<true><<<S, 256, 0, st>>>((int)nrows, (int)ncols, nnz, row_offsets, cols,
+                                             j->flags, bad, nullptr, nullptr, nullptr, nullptr, 0,
+                                             step);
+    csr_census_quads<true><<<1, 256, 0, st>>>((int)nrows, (int)ncols, nnz, row_offsets, cols,
+                                             j->flags, bad, nullptr, nullptr, nullptr, nullptr,
+                                             ntiles - 1, 1);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      rc = cuda_fail(e, "csr_census_quads(sample)");
+      break;
+    }
+    j->nnz = nnz;
+    j->csr_off = row_offsets;
+    j->c = const_cast<int*>(cols);
+    j->v = const_cast<double*>(values);
+    j->spec = true;
+    int64_t nnz_out = 0;
+    rc = size_target(j, fill_limit, &nnz_out, out_ndiags);
+    if (rc == DS_ERR_DIA_FILL_OVERFLOW) rc = DS_ERR_RETRY;
+    // the fill keeps a 128-row slab in shared memory
+    if (rc == DS_OK && (*out_ndiags < 1 || *out_ndiags * kCsrWalkRows * 8 * 8 > 160 * 1024))
+      rc = DS_ERR_RETRY;
+  } while (false);
+  if (rc) {
+    free_job(j);
+    *out_ndiags = 0;
+    return rc;
+  }
+  *job = j;
+  return DS_OK;
+}
+
 // ---------------------------------------- one-pass canonical conversions --
 // A canonical COO / CSR source to a COO / CSR target: the order / range
 // check and the target writes in one pass over the source (the begin /
@@ -2187,6 +2299,28 @@ static int finish_dia_impl(ds_convert_job* job, int32_t* offsets, double* values
     DS_CUDA(cudaMemcpyAsync(offsets, job->dia_off, nd * sizeof(int), cudaMemcpyDeviceToDevice,
                             st));
     const int64_t slots = nd * job->nrows;
+    if (job->spec) {   // one pass: order check + fill; a miss -> DS_ERR_RETRY
+      const int R = kCsrWalkRows * 8;   // 8 warps
+      const size_t smem = (size_t)R * nd * 8;
+      int rc = allow_dynamic_smem((const void*)dia_fill_csr<true>, smem);
+      if (rc) return rc;
+      DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&job->scratch), 4, st));
+      DS_CUDA(cudaMemsetAsync(job->scratch, 0, 4, st));
+      int* bad = reinterpret_cast<int*>(job->scratch);
+      dia_fill_csr<true><<<csr_walk_grid(job->nrows), 256, smem, st>>>(
+          (int)job->nrows, (int)nd, R, job->csr_off, job->c, job->v, job->diag_map, values,
+          (int)job->ncols, bad);
+      DS_LAUNCH_CHECK("dia_fill_csr(check)");
+      int bad_h = 1;
+      DS_CUDA(cudaMemcpyAsync(&bad_h, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+      DS_CUDA(cudaStreamSynchronize(st));
+      if (bad_h & kBadIndex) return index_error(job->nrows, job->ncols);
+      if (bad_h) {
+        set_error("speculative CSR -> DIA: diagonal set or order differs; use the census path");
+        return DS_ERR_RETRY;
+      }
+      return DS_OK;
+    }
     if (job->dia_jsrc) {   // DIA source: the selected columns, masked
       // every diagonal kept: the in-range rows are a plain stream of the slab
       const bool all = nd == job->dsrc_nd && job->dsrc_in_hi > job->dsrc_in_lo &&
@@ -2225,10 +2359,10 @@ static int finish_dia_impl(ds_convert_job* job, int32_t* offsets, double* values
     const int R = kCsrWalkRows * 8;   // 8 warps
     if (job->csr_off && (int64_t)R * nd * 8 <= 48 * 1024) {
       if ((int64_t)R * nd * 8 > 40 * 1024) {   // + the 8 KB map cache
-        int rc = allow_dynamic_smem((const void*)dia_fill_csr, (size_t)R * nd * 8);
+        int rc = allow_dynamic_smem((const void*)dia_fill_csr<false>, (size_t)R * nd * 8);
         if (rc) return rc;
       }
-      dia_fill_csr<<<csr_walk_grid(job->nrows), 256, (size_t)R * nd * 8, st>>>(
+      dia_fill_csr<false><<<csr_walk_grid(job->nrows), 256, (size_t)R * nd * 8, st>>>(
           (int)job->nrows, (int)nd, R, job->csr_off, job->c, job->v, job->diag_map, values);
       DS_LAUNCH_CHECK("dia_fill_csr");
       return DS_OK;

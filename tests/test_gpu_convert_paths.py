@@ -394,3 +394,77 @@ def test_dia_source_banded_interior_groups(nrows, ncols, nd):
         src = ds.DiaMatrix(nrows, ncols, offs, v2, ds.MemorySpace.DEVICE, DEV)
         want = O.convert(O.dia(nrows, ncols, offs, v2), O.DIA)
         assert_same(ds.convert(src, ds.FormatId.DIA), want, (nrows, nd, "drop"))
+
+
+def _banded_rows(nrows, ncols, band, rng):
+    offs = np.zeros(nrows + 1, dtype=np.int64)
+    cols = []
+    for i in range(nrows):
+        c = np.array([i + d for d in band if 0 <= i + d < ncols], dtype=np.int64)
+        cols.append(c)
+        offs[i + 1] = offs[i] + c.size
+    return offs, cols
+
+
+def _spec_direct(src, fill_limit=-(2 ** 63)):
+    """ds_convert_begin_csr_dia_spec + finish_dia through ctypes: (rc_begin,
+    nd_sampled, rc_finish)."""
+    import ctypes
+    from paper_2209_06478_b200 import _device, _native
+    lib = _native.load()
+    p = _device.ptr
+    job, nd = ctypes.c_void_p(), ctypes.c_int64()
+    rc = lib.ds_convert_begin_csr_dia_spec(src.nrows, src.ncols, src.nnz, p(src.row_offsets),
+                                           p(src.col_indices), p(src.values), fill_limit,
+                                           _device.stream(DEV), ctypes.byref(job),
+                                           ctypes.byref(nd))
+    if rc:
+        return rc, nd.value, None
+    o = torch.empty(nd.value, dtype=torch.int32, device=DEV)
+    v = torch.empty((src.nrows, nd.value), dtype=torch.float64, device=DEV)
+    return rc, nd.value, lib.ds_convert_finish_dia(job, p(o), p(v))
+
+
+def test_csr_to_dia_speculative_hit_and_miss():
+    """The speculative one-pass CSR -> DIA (diagonal set from sampled 128-row
+    tiles): a band present in every tile is a hit (rc 0, bitwise equal to the
+    oracle); one extra diagonal only in an unsampled tile is a miss
+    (DS_ERR_RETRY) and the public convert still returns the oracle's DIA
+    through the census path; a sample inside the fill limit whose true set is
+    not raises DiaFillOverflow; a column out of range in an unsampled tile
+    raises IndexOutOfRange."""
+    rng = np.random.default_rng(77)
+    nrows = ncols = 128 * 600            # 600 tiles: every 2nd sampled (+ the last)
+    band = [-300, -1, 0, 1, 300]
+    offs, cl = _banded_rows(nrows, ncols, band, rng)
+    cols = np.concatenate(cl)
+    vals = rng.standard_normal(cols.size)
+    vals[rng.random(cols.size) < 0.05] = -0.0
+    src = ds.CsrMatrix(nrows, ncols, offs, cols, vals, ds.MemorySpace.DEVICE, DEV)
+    rc, nd, rcf = _spec_direct(src)
+    assert (rc, nd, rcf) == (0, 5, 0)
+    want = O.convert(O.csr(nrows, ncols, offs, cols, vals), O.DIA)
+    assert_same(ds.convert(src, ds.FormatId.DIA), want, "hit")
+    # one entry on diagonal +777 in row 3*128+5 (tile 3: not sampled)
+    r = 3 * 128 + 5
+    cl2 = [c.copy() for c in cl]
+    cl2[r] = np.sort(np.append(cl2[r], r + 777))
+    offs2 = np.zeros(nrows + 1, np.int64)
+    offs2[1:] = np.cumsum([c.size for c in cl2])
+    cols2 = np.concatenate(cl2)
+    vals2 = rng.standard_normal(cols2.size)
+    src2 = ds.CsrMatrix(nrows, ncols, offs2, cols2, vals2, ds.MemorySpace.DEVICE, DEV)
+    rc, nd, rcf = _spec_direct(src2)
+    assert (rc, nd, rcf) == (0, 5, 8)
+    want2 = O.convert(O.csr(nrows, ncols, offs2, cols2, vals2), O.DIA)
+    assert want2.offsets.size == 6
+    assert_same(ds.convert(src2, ds.FormatId.DIA), want2, "miss")
+    # the sample's 5 diagonals fit the limit, the true 6 do not
+    with pytest.raises(ds.DiaFillOverflow):
+        ds.convert(src2, ds.FormatId.DIA, fill_limit=5 * nrows)
+    # a column outside the shape in an unsampled tile
+    cols3 = cols.copy()
+    cols3[int(offs[r])] = ncols + 5
+    src3 = ds.CsrMatrix(nrows, ncols, offs, cols3, vals, ds.MemorySpace.DEVICE, DEV)
+    with pytest.raises(ds.IndexOutOfRange):
+        ds.convert(src3, ds.FormatId.DIA)
