@@ -221,6 +221,12 @@ int ds_convert_begin_csr_dia_spec(int64_t nrows, int64_t ncols, int64_t nnz,
                                   const int32_t* row_offsets, const int32_t* cols,
                                   const double* values, int64_t fill_limit, void* stream,
                                   ds_convert_job** job, int64_t* out_ndiags);
+/* The same for a COO source (rows, cols, values): the census of 256 evenly
+ * spaced 4096-entry chunks and the last one; finish_dia clears the slab and
+ * scatters with the order / range / membership checks.                    */
+int ds_convert_begin_coo_dia_spec(int64_t nrows, int64_t ncols, int64_t nnz, const int32_t* rows,
+                                  const int32_t* cols, const double* values, int64_t fill_limit,
+                                  void* stream, ds_convert_job** job, int64_t* out_ndiags);
 int ds_convert_finish_coo(ds_convert_job* job, int32_t* rows, int32_t* cols, double* values);
 int ds_convert_finish_csr(ds_convert_job* job, int32_t* row_offsets, int32_t* cols,
                           double* values);

@@ -118,6 +118,8 @@ _SIGNATURES = {
                                      ctypes.POINTER(c_vp), P_i64, P_i64]),
     "ds_convert_begin_csr_dia_spec": (c_int, [c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_i64, c_vp,
                                               ctypes.POINTER(c_vp), P_i64]),
+    "ds_convert_begin_coo_dia_spec": (c_int, [c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_i64, c_vp,
+                                              ctypes.POINTER(c_vp), P_i64]),
     "ds_convert_direct": (c_int, [c_int, c_int, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp,
                                   c_vp, c_vp, P_i32]),
     "ds_convert_finish_coo": (c_int, [c_vp, c_vp, c_vp, c_vp]),

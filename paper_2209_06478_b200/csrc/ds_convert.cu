@@ -1119,13 +1119,77 @@ __global__ void zero_f64(int64_t n, double* p) {
        i += (int64_t)gridDim.x * blockDim.x)
     p[i] = 0.0;
 }
+// CHECK (the speculative COO -> DIA, ds_convert_begin_coo_dia_spec): the
+// scatter also checks the canonical order against the previous entry, the
+// index range and that the entry's diagonal is in `map` (the exclusive scan
+// of the sampled presence: d present iff map[d+1] > map[d]), setting
+// kBadOrder / kBadIndex / kBadMiss in *bad instead of storing.  The map
+// lookups go through a shared-memory cache of (j << 32 | d) words.
+template <bool CHECK>
 __global__ void dia_scatter(int64_t nnz, int nrows, int64_t nd, const int* __restrict__ r,
                             const int* __restrict__ c, const double* __restrict__ v,
-                            const int* __restrict__ map, double* vals) {
+                            const int* __restrict__ map, double* vals, int ncols = 0,
+                            int* bad = nullptr) {
+  __shared__ unsigned long long mcache[1 << kFlagTagBits];
+  for (int i = threadIdx.x; i < (1 << kFlagTagBits); i += blockDim.x) mcache[i] = ~0ull;
+  __syncthreads();
+  const unsigned D = (unsigned)nrows + (unsigned)ncols - 1u;
+  int mybad = 0;
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz;
        k += (int64_t)gridDim.x * blockDim.x) {
-    const int j = map[(int64_t)c[k] - r[k] + nrows - 1];
-    vals[(int64_t)r[k] * nd + j] = v[k];
+    const int rk = __ldg(r + k), ck = __ldg(c + k);
+    if (CHECK) {
+      if (k > 0) {
+        const int rp = __ldg(r + k - 1), cp = __ldg(c + k - 1);
+        if (rk < rp || (rk == rp && ck <= cp)) mybad |= kBadOrder;
+      }
+      if ((unsigned)rk >= (unsigned)nrows || (unsigned)ck >= (unsigned)ncols) {
+        mybad |= kBadIndex;
+        continue;
+      }
+    }
+    const unsigned d = (unsigned)ck - (unsigned)rk + (unsigned)(nrows - 1);
+    const unsigned h = (d * 0x9E3779B1u) >> (32 - kFlagTagBits);
+    const unsigned long long m = mcache[h];
+    int j;
+    if ((unsigned)m == d) {
+      j = (int)(m >> 32);
+    } else {
+      j = __ldg(map + d);
+      if (CHECK) {
+        const int jn = d + 1 < D ? __ldg(map + d + 1) : (int)nd;
+        if (jn == j) j = -1;
+      }
+      mcache[h] = ((unsigned long long)(unsigned)j << 32) | d;
+    }
+    if (CHECK && j < 0) {
+      mybad |= kBadMiss;
+      continue;
+    }
+    vals[(int64_t)rk * nd + j] = __ldg(v + k);
+  }
+  if (CHECK) {
+    mybad = __reduce_or_sync(0xffffffffu, mybad);
+    if ((threadIdx.x & 31) == 0 && mybad) atomicOr(bad, mybad);
+  }
+}
+
+// the sampled census of a COO source: block b marks the diagonals of the
+// entries in chunk b * step (the last block: the last chunk)
+__global__ void coo_census_sample(int64_t nnz, int nrows, int ncols, int64_t chunk, int64_t step,
+                                  const int* __restrict__ r, const int* __restrict__ c,
+                                  unsigned char* flags) {
+  const int64_t nchunks = (nnz + chunk - 1) / chunk;
+  const int64_t ci = blockIdx.x + 1 == gridDim.x ? nchunks - 1 : (int64_t)blockIdx.x * step;
+  const int64_t k1 = min64((ci + 1) * chunk, nnz);
+  for (int64_t k = ci * chunk + threadIdx.x; k < k1; k += blockDim.x) {
+    const int rk = __ldg(r + k), ck = __ldg(c + k);
+    if ((unsigned)rk < (unsigned)nrows && (unsigned)ck < (unsigned)ncols) {
+      const unsigned d = (unsigned)ck - (unsigned)rk + (unsigned)(nrows - 1);
+      unsigned short f;
+      asm volatile("ld.global.ca.u8 %0, [%1];" : "=h"(f) : "l"(flags + d));
+      if (f == 0) flags[d] = 1;
+    }
   }
 }
 
@@ -2029,6 +2093,58 @@ extern "C" int ds_convert_begin_csr_dia_spec(int64_t nrows, int64_t ncols, int64
   return DS_OK;
 }
 
+
+// The same speculation for a COO source: the census of 256 evenly spaced
+// 4096-entry chunks and the last one; finish_dia clears the slab and runs
+// the checked scatter (dia_scatter<true>).
+extern "C" int ds_convert_begin_coo_dia_spec(int64_t nrows, int64_t ncols, int64_t nnz,
+                                             const int32_t* rows, const int32_t* cols,
+                                             const double* values, int64_t fill_limit,
+                                             void* stream, ds_convert_job** job,
+                                             int64_t* out_ndiags) {
+  *job = nullptr;
+  *out_ndiags = 0;
+  if (fill_limit == kDefaultFillLimit) fill_limit = 10 * std::max(nnz, nrows);   // datamove.py:55-57
+  if (!dims_ok(nrows, ncols, nnz)) return DS_ERR_NOT_SUPPORTED;
+  if (nnz <= 0 || nrows <= 0) return DS_ERR_RETRY;
+  ds_convert_job* j = new_job(nrows, ncols, DS_FMT_DIA, stream);
+  cudaStream_t st = j->st;
+  const int64_t flag_bytes = (nrows + ncols - 1 + 3) & ~int64_t(3);
+  int rc = DS_OK;
+  do {
+    if (cudaMallocAsync(reinterpret_cast<void**>(&j->flags), flag_bytes, st) != cudaSuccess ||
+        cudaMemsetAsync(j->flags, 0, flag_bytes, st) != cudaSuccess) {
+      rc = cuda_fail(cudaGetLastError(), "speculative census flags");
+      break;
+    }
+    const int64_t chunk = 4096, nchunks = ceil_div(nnz, chunk);
+    const int64_t S = std::min<int64_t>(nchunks, 256), step = std::max<int64_t>(1, nchunks / S);
+    coo_census_sample<<<(unsigned)S + 1, 256, 0, st>>>(nnz, (int)nrows, (int)ncols, chunk, step,
+                                                      rows, cols, j->flags);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      rc = cuda_fail(e, "coo_census_sample");
+      break;
+    }
+    j->nnz = nnz;
+    j->r = const_cast<int*>(rows);
+    j->c = const_cast<int*>(cols);
+    j->v = const_cast<double*>(values);
+    j->spec = true;
+    int64_t nnz_out = 0;
+    rc = size_target(j, fill_limit, &nnz_out, out_ndiags);
+    if (rc == DS_ERR_DIA_FILL_OVERFLOW) rc = DS_ERR_RETRY;
+    if (rc == DS_OK && *out_ndiags < 1) rc = DS_ERR_RETRY;
+  } while (false);
+  if (rc) {
+    free_job(j);
+    *out_ndiags = 0;
+    return rc;
+  }
+  *job = j;
+  return DS_OK;
+}
+
 // ---------------------------------------- one-pass canonical conversions --
 // A canonical COO / CSR source to a COO / CSR target: the order / range
 // check and the target writes in one pass over the source (the begin /
@@ -2299,6 +2415,25 @@ static int finish_dia_impl(ds_convert_job* job, int32_t* offsets, double* values
     DS_CUDA(cudaMemcpyAsync(offsets, job->dia_off, nd * sizeof(int), cudaMemcpyDeviceToDevice,
                             st));
     const int64_t slots = nd * job->nrows;
+    if (job->spec && !job->csr_off) {   // COO: zero + checked scatter; a miss -> DS_ERR_RETRY
+      DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&job->scratch), 4, st));
+      DS_CUDA(cudaMemsetAsync(job->scratch, 0, 4, st));
+      int* bad = reinterpret_cast<int*>(job->scratch);
+      DS_CUDA(cudaMemsetAsync(values, 0, slots * sizeof(double), st));   // +0.0
+      dia_scatter<true><<<grid1d(job->nnz), 256, 0, st>>>(job->nnz, (int)job->nrows, nd, job->r,
+                                                          job->c, job->v, job->diag_map, values,
+                                                          (int)job->ncols, bad);
+      DS_LAUNCH_CHECK("dia_scatter(check)");
+      int bad_h = 1;
+      DS_CUDA(cudaMemcpyAsync(&bad_h, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+      DS_CUDA(cudaStreamSynchronize(st));
+      if (bad_h & kBadIndex) return index_error(job->nrows, job->ncols);
+      if (bad_h) {
+        set_error("speculative COO -> DIA: diagonal set or order differs; use the census path");
+        return DS_ERR_RETRY;
+      }
+      return DS_OK;
+    }
     if (job->spec) {   // one pass: order check + fill; a miss -> DS_ERR_RETRY
       const int R = kCsrWalkRows * 8;   // 8 warps
       const size_t smem = (size_t)R * nd * 8;
@@ -2375,7 +2510,7 @@ static int finish_dia_impl(ds_convert_job* job, int32_t* offsets, double* values
       DS_LAUNCH_CHECK("csr_expand_rows");
     }
     zero_f64<<<grid1d(slots), 256, 0, st>>>(slots, values);
-    dia_scatter<<<grid1d(job->nnz), 256, 0, st>>>(job->nnz, (int)job->nrows, nd, job->r, job->c,
+    dia_scatter<false><<<grid1d(job->nnz), 256, 0, st>>>(job->nnz, (int)job->nrows, nd, job->r, job->c,
                                                   job->v, job->diag_map, values);
     DS_LAUNCH_CHECK("dia_scatter");
   }

@@ -468,3 +468,59 @@ def test_csr_to_dia_speculative_hit_and_miss():
     src3 = ds.CsrMatrix(nrows, ncols, offs, cols3, vals, ds.MemorySpace.DEVICE, DEV)
     with pytest.raises(ds.IndexOutOfRange):
         ds.convert(src3, ds.FormatId.DIA)
+
+
+def test_coo_to_dia_speculative_hit_and_miss():
+    """The speculative COO -> DIA (diagonal set from 256 sampled 4096-entry
+    chunks, then a checked scatter): a hit is bitwise the oracle's; an extra
+    diagonal only inside an unsampled chunk is a miss (DS_ERR_RETRY from
+    finish) and the public convert falls back to the census path; an
+    unsorted pair in an unsampled chunk likewise."""
+    import ctypes
+    from paper_2209_06478_b200 import _device, _native
+    rng = np.random.default_rng(78)
+    nrows = ncols = 512_000                  # 2.56 M entries: 625 chunks, every 2nd sampled
+    band = np.array([-700, -1, 0, 1, 700])
+    rows = np.repeat(np.arange(nrows), band.size)
+    cols = rows + np.tile(band, nrows)
+    keep = (cols >= 0) & (cols < ncols)
+    rows, cols = rows[keep], cols[keep]
+    vals = rng.standard_normal(rows.size)
+    vals[rng.random(rows.size) < 0.05] = -0.0
+
+    def spec(r, c, v):
+        lib = _native.load()
+        p = _device.ptr
+        rt, ct, vt = (torch.from_numpy(np.asarray(a, dt)).to(DEV)
+                      for a, dt in ((r, np.int32), (c, np.int32), (v, np.float64)))
+        job, nd = ctypes.c_void_p(), ctypes.c_int64()
+        rc = lib.ds_convert_begin_coo_dia_spec(nrows, ncols, r.size, p(rt), p(ct), p(vt),
+                                               -(2 ** 63), _device.stream(DEV), ctypes.byref(job),
+                                               ctypes.byref(nd))
+        assert rc == 0
+        o = torch.empty(nd.value, dtype=torch.int32, device=DEV)
+        d = torch.empty((nrows, nd.value), dtype=torch.float64, device=DEV)
+        return nd.value, lib.ds_convert_finish_dia(job, p(o), p(d))
+
+    assert spec(rows, cols, vals) == (5, 0)
+    src = ds.CooMatrix(nrows, ncols, rows, cols, vals, ds.MemorySpace.DEVICE, DEV)
+    assert_same(ds.convert(src, ds.FormatId.DIA),
+                O.convert(O.coo(nrows, ncols, rows, cols, vals), O.DIA), "hit")
+    k = 3 * 4096 + 100                        # chunk 3: not sampled
+    r = int(rows[k])
+    ins = int(np.searchsorted(rows, r, side="right"))   # append to row r (col r + 900)
+    rows2 = np.insert(rows, ins, r)
+    cols2 = np.insert(cols, ins, r + 900)
+    vals2 = np.insert(vals, ins, 2.5)
+    assert spec(rows2, cols2, vals2) == (5, 8)
+    src2 = ds.CooMatrix(nrows, ncols, rows2, cols2, vals2, ds.MemorySpace.DEVICE, DEV)
+    want2 = O.convert(O.coo(nrows, ncols, rows2, cols2, vals2), O.DIA)
+    assert want2.offsets.size == 6
+    assert_same(ds.convert(src2, ds.FormatId.DIA), want2, "miss")
+    cols3 = cols.copy()
+    cols3[k], cols3[k + 1] = cols3[k + 1], cols3[k]
+    if rows[k] == rows[k + 1]:
+        assert spec(rows, cols3, vals)[1] == 8
+        src3 = ds.CooMatrix(nrows, ncols, rows, cols3, vals, ds.MemorySpace.DEVICE, DEV)
+        assert_same(ds.convert(src3, ds.FormatId.DIA),
+                    O.convert(O.coo(nrows, ncols, rows, cols3, vals), O.DIA), "unsorted")
