@@ -629,6 +629,22 @@ constexpr int kBadOrder = 1, kBadIndex = 2, kBadRowOrder = 4;   // 4: rows decre
 constexpr int kBadMiss = 8;   // a diagonal outside the speculative set (dia_fill_csr<true>)
 
 
+// diag_map cache of the DIA fills: the target's nd diagonals (dia_off) are
+// entered by one thread before the walk ((j << 32) | d words, a later
+// diagonal taking a colliding slot), so the walk only reads it; a miss reads
+// diag_map itself.  Returns after the block barrier.
+__device__ __forceinline__ void preload_map_cache(unsigned long long* mc, const int* dia_off,
+                                                  int nd, int nrows) {
+  for (int i = threadIdx.x; i < (1 << kFlagTagBits); i += blockDim.x) mc[i] = ~0ull;
+  __syncthreads();
+  if (threadIdx.x == 0 && nd <= 256)   // wider sets: every lookup reads diag_map
+    for (int j = 0; j < nd; ++j) {
+      const unsigned d = (unsigned)__ldg(dia_off + j) + (unsigned)(nrows - 1);
+      mc[(d * 0x9E3779B1u) >> (32 - kFlagTagBits)] = ((unsigned long long)(unsigned)j << 32) | d;
+    }
+  __syncthreads();
+}
+
 // CHECK (the speculative CSR -> DIA, ds_convert_begin_csr_dia_spec): the
 // walk also checks the order ((row, col) strictly increasing in every row),
 // the column range and that every entry's diagonal is in `map` (the
@@ -637,13 +653,11 @@ constexpr int kBadMiss = 8;   // a diagonal outside the speculative set (dia_fil
 template <bool CHECK>
 __global__ void dia_fill_csr(int nrows, int nd, int R, const int* __restrict__ off,
                              const int* __restrict__ c, const double* __restrict__ v,
-                             const int* __restrict__ map, double* vals, int ncols = 0,
-                             int* bad = nullptr) {
+                             const int* __restrict__ map, const int* __restrict__ dia_off,
+                             double* vals, int ncols = 0, int* bad = nullptr) {
   extern __shared__ double slab[];   // R * nd, R = kCsrWalkRows * warps per block
-  // recently used diag_map entries, (j << 32 | d) in one 64-bit word so a
-  // racing writer can never pair one diagonal's key with another's column
   __shared__ unsigned long long mcache[1 << kFlagTagBits];
-  for (int i = threadIdx.x; i < (1 << kFlagTagBits); i += blockDim.x) mcache[i] = ~0ull;
+  preload_map_cache(mcache, dia_off, nd, nrows);
   const int warp = threadIdx.x >> 5;
   const unsigned D = (unsigned)nrows + (unsigned)ncols - 1u;
   int mybad = 0;
@@ -677,7 +691,12 @@ __global__ void dia_fill_csr(int nrows, int nd, int R, const int* __restrict__ o
                              carry = __shfl_sync(0xffffffffu, e[u].c, 31);
                              carry_row = __shfl_sync(0xffffffffu, rr[u], 31);
                              if (ok[u]) {
-                               if (prev_row == rr[u] && prev >= e[u].c) mybad |= kBadOrder;
+                               // an entry out of order is not stored (its
+                               // duplicate's slot stays single-writer)
+                               if (prev_row == rr[u] && prev >= e[u].c) {
+                                 mybad |= kBadOrder;
+                                 ok[u] = false;
+                               }
                                if ((unsigned)e[u].c >= (unsigned)ncols) {
                                  mybad |= kBadIndex;
                                  ok[u] = false;
@@ -696,7 +715,6 @@ __global__ void dia_fill_csr(int nrows, int nd, int R, const int* __restrict__ o
                                  const int jn = d + 1 < D ? __ldg(map + d + 1) : nd;
                                  if (jn == j[u]) j[u] = -1;
                                }
-                               mcache[h] = ((unsigned long long)(unsigned)j[u] << 32) | d;
                              }
                              if (CHECK && j[u] < 0) {
                                mybad |= kBadMiss;
@@ -786,18 +804,18 @@ struct QuadIds {
 
 
 // flag test of one entry: a per-CTA shared-memory tag table of recently set
-// diagonals first (the stencil's 27 diagonals stay resident: one shared load
-// per entry), then the L1-cached global test-before-set, predicated (no
-// branch) on `ok` (the column in range).  A tag is written only after its
+// diagonals first (the stencil's 27 diagonals stay resident: one shared
+// atomic per entry -- atomics, so the racing tag updates are not data races),
+// then the L1-cached global test-before-set.  A tag is written only after its
 // flag was tested / set, so a tag hit always means the flag is set.
 __device__ __forceinline__ void census_flag(unsigned char* flags, unsigned d, bool ok,
                                             unsigned* tags) {
   const unsigned h = (d * 0x9E3779B1u) >> (32 - kFlagTagBits);
-  if (ok && tags[h] != d) {
+  if (ok && atomicOr(&tags[h], 0u) != d) {
     unsigned short f;
     asm volatile("ld.global.ca.u8 %0, [%1];" : "=h"(f) : "l"(flags + d));
     if (f == 0) flags[d] = 1;
-    tags[h] = d;
+    atomicExch(&tags[h], d);
   }
 }
 
@@ -1128,11 +1146,10 @@ __global__ void zero_f64(int64_t n, double* p) {
 template <bool CHECK>
 __global__ void dia_scatter(int64_t nnz, int nrows, int64_t nd, const int* __restrict__ r,
                             const int* __restrict__ c, const double* __restrict__ v,
-                            const int* __restrict__ map, double* vals, int ncols = 0,
-                            int* bad = nullptr) {
+                            const int* __restrict__ map, const int* __restrict__ dia_off,
+                            double* vals, int ncols = 0, int* bad = nullptr) {
   __shared__ unsigned long long mcache[1 << kFlagTagBits];
-  for (int i = threadIdx.x; i < (1 << kFlagTagBits); i += blockDim.x) mcache[i] = ~0ull;
-  __syncthreads();
+  preload_map_cache(mcache, dia_off, (int)nd, nrows);
   const unsigned D = (unsigned)nrows + (unsigned)ncols - 1u;
   int mybad = 0;
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz;
@@ -1141,7 +1158,10 @@ __global__ void dia_scatter(int64_t nnz, int nrows, int64_t nd, const int* __res
     if (CHECK) {
       if (k > 0) {
         const int rp = __ldg(r + k - 1), cp = __ldg(c + k - 1);
-        if (rk < rp || (rk == rp && ck <= cp)) mybad |= kBadOrder;
+        if (rk < rp || (rk == rp && ck <= cp)) {
+          mybad |= kBadOrder;
+          continue;   // not stored: a duplicate's slot stays single-writer
+        }
       }
       if ((unsigned)rk >= (unsigned)nrows || (unsigned)ck >= (unsigned)ncols) {
         mybad |= kBadIndex;
@@ -1160,7 +1180,6 @@ __global__ void dia_scatter(int64_t nnz, int nrows, int64_t nd, const int* __res
         const int jn = d + 1 < D ? __ldg(map + d + 1) : (int)nd;
         if (jn == j) j = -1;
       }
-      mcache[h] = ((unsigned long long)(unsigned)j << 32) | d;
     }
     if (CHECK && j < 0) {
       mybad |= kBadMiss;
@@ -2421,8 +2440,9 @@ static int finish_dia_impl(ds_convert_job* job, int32_t* offsets, double* values
       int* bad = reinterpret_cast<int*>(job->scratch);
       DS_CUDA(cudaMemsetAsync(values, 0, slots * sizeof(double), st));   // +0.0
       dia_scatter<true><<<grid1d(job->nnz), 256, 0, st>>>(job->nnz, (int)job->nrows, nd, job->r,
-                                                          job->c, job->v, job->diag_map, values,
-                                                          (int)job->ncols, bad);
+                                                          job->c, job->v, job->diag_map,
+                                                          job->dia_off, values, (int)job->ncols,
+                                                          bad);
       DS_LAUNCH_CHECK("dia_scatter(check)");
       int bad_h = 1;
       DS_CUDA(cudaMemcpyAsync(&bad_h, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -2443,8 +2463,8 @@ static int finish_dia_impl(ds_convert_job* job, int32_t* offsets, double* values
       DS_CUDA(cudaMemsetAsync(job->scratch, 0, 4, st));
       int* bad = reinterpret_cast<int*>(job->scratch);
       dia_fill_csr<true><<<csr_walk_grid(job->nrows), 256, smem, st>>>(
-          (int)job->nrows, (int)nd, R, job->csr_off, job->c, job->v, job->diag_map, values,
-          (int)job->ncols, bad);
+          (int)job->nrows, (int)nd, R, job->csr_off, job->c, job->v, job->diag_map, job->dia_off,
+          values, (int)job->ncols, bad);
       DS_LAUNCH_CHECK("dia_fill_csr(check)");
       int bad_h = 1;
       DS_CUDA(cudaMemcpyAsync(&bad_h, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -2498,7 +2518,8 @@ static int finish_dia_impl(ds_convert_job* job, int32_t* offsets, double* values
         if (rc) return rc;
       }
       dia_fill_csr<false><<<csr_walk_grid(job->nrows), 256, (size_t)R * nd * 8, st>>>(
-          (int)job->nrows, (int)nd, R, job->csr_off, job->c, job->v, job->diag_map, values);
+          (int)job->nrows, (int)nd, R, job->csr_off, job->c, job->v, job->diag_map, job->dia_off,
+          values);
       DS_LAUNCH_CHECK("dia_fill_csr");
       return DS_OK;
     }
@@ -2510,8 +2531,9 @@ static int finish_dia_impl(ds_convert_job* job, int32_t* offsets, double* values
       DS_LAUNCH_CHECK("csr_expand_rows");
     }
     zero_f64<<<grid1d(slots), 256, 0, st>>>(slots, values);
-    dia_scatter<false><<<grid1d(job->nnz), 256, 0, st>>>(job->nnz, (int)job->nrows, nd, job->r, job->c,
-                                                  job->v, job->diag_map, values);
+    dia_scatter<false><<<grid1d(job->nnz), 256, 0, st>>>(job->nnz, (int)job->nrows, nd, job->r,
+                                                         job->c, job->v, job->diag_map,
+                                                         job->dia_off, values);
     DS_LAUNCH_CHECK("dia_scatter");
   }
   return DS_OK;
