@@ -22,6 +22,17 @@ if [ -n "${NCU:-}" ]; then
     timeout 600 ncu --set full --clock-control none --import-source on -k regex:$1 -s $2 -c 1 \
         -o $O/prof_$1 -f python tools/profile_kernels.py > $O/prof_$1.log 2>&1
   done
+  NX=192 timeout 300 python tools/time_convert.py > $O/convert_192.json 2>&1
+  NX=104 timeout 300 python tools/time_convert.py > $O/convert_104.json 2>&1
+  for p in "csr dia" "dia csr" "coo csr" "csr coo" "coo dia" "dia dia"; do
+    set -- $p
+    SRC=$1 DST=$2 NX=192 timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
+        --clock-control none --csv --log-file $O/conv_launch_$1_$2.csv python tools/one_convert.py > /dev/null 2>&1
+  done
+  SRC=csr DST=dia NX=192 timeout 600 ncu --set full --clock-control none --import-source on \
+      -k regex:"dia_fill_csr" -c 1 -o $O/prof_conv_fill -f python tools/one_convert.py > /dev/null 2>&1
+  SRC=dia DST=csr NX=192 timeout 600 ncu --set full --clock-control none --import-source on \
+      -k regex:"dia_group" -c 2 -o $O/prof_conv_dia -f python tools/one_convert.py > /dev/null 2>&1
   PROFILE=1 FMTS=csr,coo timeout 600 ncu --set full --clock-control none --import-source on -k regex:"csr_tile_kernel|coo_warp_segments" -s 2 -c 2 \
       -o $O/prof_powerlaw -f python tools/powerlaw_kernels.py > $O/prof_powerlaw.log 2>&1
 fi
