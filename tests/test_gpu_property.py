@@ -208,3 +208,53 @@ def test_irregular_csr_tiles_match_oracle(nrows, ncols, seed, longest):
             yd = ds.DenseVector(torch.from_numpy(y0.copy()).to(DEV))
             (ds.spmv_add if acc else ds.spmv)(ds.SERIAL, m, xt, yd)
             assert yd.data.cpu().numpy().tobytes() == yw.tobytes(), (type(m).__name__, acc)
+
+
+@settings(max_examples=15, deadline=None, suppress_health_check=[HealthCheck.too_slow])
+@given(st.integers(33_000, 90_000), st.integers(1, 9), st.integers(0, 3), st.integers(0, 2**31 - 1),
+       st.sampled_from(["none", "dup", "swap"]))
+def test_speculative_and_direct_paths_match_oracle(nrows, nd, extra, seed, damage):
+    """Banded matrices large enough that the speculative DIA conversions
+    sample (> 256 row tiles / 4096-entry chunks), plus `extra` entries on new
+    diagonals in random rows (usually unsampled: a miss -> the census path)
+    and optionally a duplicate or an unsorted pair (not canonical): CSR and
+    COO sources to every target, bitwise against the oracle."""
+    rng = np.random.default_rng(seed)
+    ncols = nrows + int(rng.integers(-50, 50))
+    band = np.sort(rng.choice(np.arange(-60, 61), size=nd, replace=False))
+    rows = np.repeat(np.arange(nrows), nd)
+    cols = rows + np.tile(band, nrows)
+    for _ in range(extra):
+        r = int(rng.integers(0, nrows))
+        rows = np.append(rows, r)
+        cols = np.append(cols, min(ncols - 1, r + int(rng.integers(100, 4000))))
+    keep = (cols >= 0) & (cols < ncols)
+    rows, cols = rows[keep], cols[keep]
+    order = np.lexsort((cols, rows))
+    rows, cols = rows[order], cols[order]
+    uniq = np.ones(rows.size, bool)
+    uniq[1:] = (rows[1:] != rows[:-1]) | (cols[1:] != cols[:-1])
+    rows, cols = rows[uniq], cols[uniq]
+    vals = rng.standard_normal(rows.size)
+    vals[rng.random(rows.size) < 0.05] = -0.0
+    if damage != "none" and rows.size > 2:
+        k = int(rng.integers(1, rows.size))
+        while k < rows.size and rows[k] != rows[k - 1]:
+            k += 1
+        if k < rows.size:
+            if damage == "dup":
+                cols[k] = cols[k - 1]
+            else:
+                cols[k - 1], cols[k] = cols[k], cols[k - 1]
+    offs = np.zeros(nrows + 1, np.int64)
+    np.add.at(offs, rows + 1, 1)
+    offs = np.cumsum(offs)
+    srcs = ((ds.CsrMatrix(nrows, ncols, offs, cols, vals, ds.MemorySpace.DEVICE, DEV),
+             O.csr(nrows, ncols, offs, cols, vals)),
+            (ds.CooMatrix(nrows, ncols, rows, cols, vals, ds.MemorySpace.DEVICE, DEV),
+             O.coo(nrows, ncols, rows, cols, vals)))
+    for src, osrc in srcs:
+        for target in (ds.FormatId.COO, ds.FormatId.CSR, ds.FormatId.DIA):
+            want = O.convert(osrc, FMT[target])
+            assert _same(_host(ds.convert(src, target)), want), (type(src).__name__, target,
+                                                                   damage, extra)
