@@ -33,6 +33,7 @@ for _ in range(10):
     st = _device.stream(dev)
     eng.setup(st)
     t = mark("setup", t)
+    eng._persist_on(st)   # as CgEngine.run does before a cached-graph launch
     _native.check(eng.lib.ds_graph_exec_launch(eng._while[1], st))
     t = mark("while_loop", t)
     eng.release_l2(st)
