@@ -1148,7 +1148,9 @@ __global__ void zero_f64(int64_t n, double* p) {
 // index range and that the entry's diagonal is in `map` (the exclusive scan
 // of the sampled presence: d present iff map[d+1] > map[d]), setting
 // kBadOrder / kBadIndex / kBadMiss in *bad instead of storing.  The map
-// lookups go through a shared-memory cache of (j << 32 | d) words.
+// lookups go through the preloaded shared-memory cache (preload_map_cache).
+// (Round 2: 4 warp-uniform groups of 32 entries in flight per thread with the
+// previous entry from a shuffle ran 192^3 COO->DIA 1.62 -> 2.19 ms.)
 template <bool CHECK>
 __global__ void dia_scatter(int64_t nnz, int nrows, int64_t nd, const int* __restrict__ r,
                             const int* __restrict__ c, const double* __restrict__ v,
