@@ -208,8 +208,10 @@ int ds_convert_direct(int src_format, int target, int64_t nrows, int64_t ncols, 
                       const int32_t* src_idx, const int32_t* cols, const double* values,
                       int32_t* out_idx, int32_t* out_cols, double* out_values, void* stream,
                       int* done);
-/* Speculative CSR -> DIA: the diagonal set is taken from a sample of row
- * tiles (every ntiles/256-th 128-row tile and the last) and finish_dia
+/* Speculative CSR -> DIA (convert's DIA branch, datamove.py:238-258, whose
+ * diagonal set is the COO proxy's, formats.py:439-479): the diagonal set is
+ * taken from a sample of row tiles (every ntiles/256-th 128-row tile and the
+ * last) and finish_dia
  * fills the slab in ONE pass that also checks the order, the index range and
  * that no entry lies outside the sampled set (the sample is a subset of the
  * true set, so no miss means equal).  DS_ERR_RETRY from begin (empty source,
