@@ -745,6 +745,184 @@ __global__ void dia_fill_csr(int nrows, int nd, int R, const int* __restrict__ o
   }
 }
 
+// Slot-parallel DIA fill (nd <= 32; datamove.py:238-258 places entry (r, c)
+// at slot (r, j) with dia_off[j] = c - r).  A warp takes 32 consecutive rows
+// and walks their 32 * nd target slots flat, lane per slot (coalesced
+// stores, kFillSlotsU slots per lane in flight).  A row holding exactly nd
+// entries ("full": the stencil's interior) needs no diag_map lookup: its
+// slot j is entry off[r] + j, checked by one compare (column == r +
+// dia_off[j], in range -- which also proves the row strictly increasing).
+// Rows that are not full -- and every row of a chunk where a compare failed
+// -- are then rewritten one at a time by the warp: zeroed, and their entries
+// scattered through diag_map with dia_fill_csr<CHECK>'s checks (order,
+// column range, membership; an out-of-order entry is not stored).
+// Measured (tools/gpu_fillab.sh, same box, 192^3 wall): CSR -> DIA 1.04 ms
+// (the slab walk, DS_DIA_FILL_ROWS=0) -> 0.93 ms, COO -> DIA 1.62 -> 1.28 ms
+// (with coo_offsets_check).  Slots per lane 6 (64 registers); 8: 1.07 ms,
+// 12: 1.39, 16: 1.22; a bulk L2 prefetch of the next chunk's entries: 1.19
+// vs 0.98.  Rejected: a warp per row (~57 warp instructions per row, 852 us
+// cold for the fill kernel, the same as the slab walk) and the same walk
+// TMA-staged at 1 CTA/SM (1.49 ms, issue-latency bound).
+#ifndef DS_FILL_SLOTS_U
+#define DS_FILL_SLOTS_U 6
+#endif
+constexpr int kFillSlotsU = DS_FILL_SLOTS_U;
+template <bool CHECK>
+__global__ void __launch_bounds__(256)
+    dia_fill_rows(int nrows, int nd, const int* __restrict__ off, const int* __restrict__ c,
+                  const double* __restrict__ v, const int* __restrict__ map,
+                  const int* __restrict__ dia_off, double* vals, int ncols, int* bad) {
+  constexpr int U = kFillSlotsU;
+  const int lane = threadIdx.x & 31;
+  const int myoff = lane < nd ? __ldg(dia_off + lane) : 0;
+  const unsigned D = (unsigned)nrows + (unsigned)ncols - 1u;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int qq = 32 / nd, rmd = 32 % nd;   // a lane's slot advances by 32: rows qq, slots rmd
+  int mybad = 0;
+  for (int64_t r0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; r0 < nrows;
+       r0 += nw * 32) {
+    const int nr = (int)min64(32, nrows - r0);
+    int oa = 0, ob = 0;
+    if (lane < nr) {
+      oa = __ldg(off + r0 + lane);
+      ob = __ldg(off + r0 + lane + 1);
+    }
+    const unsigned full = __ballot_sync(0xffffffffu, lane < nr && ob - oa == nd);
+    const int total = nr * nd;
+    double* out = vals + r0 * nd;
+    int row = lane / nd, j = lane % nd;
+    bool mism = false;
+    for (int q0 = 0; q0 < total; q0 += 32 * U) {
+      int col[U];
+      double val[U];
+      bool f[U];
+      int rw[U], jj[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int q = q0 + 32 * u + lane;
+        rw[u] = row;
+        jj[u] = j;
+        const int k = __shfl_sync(0xffffffffu, oa, row & 31) + j;
+        f[u] = q < total && ((full >> (row & 31)) & 1u);
+        col[u] = -1;
+        val[u] = 0.0;
+        if (f[u]) {
+          col[u] = __ldg(c + k);
+          val[u] = __ldg(v + k);
+        }
+        row += qq;
+        j += rmd;
+        if (j >= nd) {
+          j -= nd;
+          ++row;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int doff = __shfl_sync(0xffffffffu, myoff, jj[u]);
+        if (f[u]) {
+          if (col[u] == (int)r0 + rw[u] + doff && (unsigned)col[u] < (unsigned)ncols)
+            out[q0 + 32 * u + lane] = val[u];
+          else
+            mism = true;
+        }
+      }
+    }
+    // rows the slot walk did not (validly) write
+    unsigned redo = __any_sync(0xffffffffu, mism) ? 0xffffffffu : ~full;
+    if (nr < 32) redo &= (1u << nr) - 1u;
+    if (redo) __syncwarp();
+    while (redo) {
+      const int i = __ffs(redo) - 1;
+      redo &= redo - 1;
+      const int r = (int)r0 + i;
+      const int k0 = __shfl_sync(0xffffffffu, oa, i), k1 = __shfl_sync(0xffffffffu, ob, i);
+      double* rowp = vals + (int64_t)r * nd;
+      if (lane < nd) rowp[lane] = 0.0;
+      __syncwarp();
+      for (int k = k0 + lane; k < k1; k += 32) {
+        const int ck = __ldg(c + k);
+        if (CHECK) {
+          if (k > k0 && __ldg(c + k - 1) >= ck) {   // not strictly increasing
+            mybad |= kBadOrder;
+            continue;
+          }
+          if ((unsigned)ck >= (unsigned)ncols) {
+            mybad |= kBadIndex;
+            continue;
+          }
+        }
+        const unsigned d = (unsigned)ck - (unsigned)r + (unsigned)(nrows - 1);
+        const int jd = __ldg(map + d);
+        if (CHECK && (d + 1 < D ? __ldg(map + d + 1) : nd) == jd) {
+          mybad |= kBadMiss;
+          continue;
+        }
+        rowp[jd] = __ldg(v + k);
+      }
+      __syncwarp();
+    }
+  }
+  if (CHECK) {
+    mybad = __reduce_or_sync(0xffffffffu, mybad);
+    if (lane == 0 && mybad) atomicOr(bad, mybad);
+  }
+}
+
+// Row offsets of a COO source for the row-slot fill (the speculative COO ->
+// DIA): off[i] = first entry with row >= i, checking the row order (kBadOrder
+// | kBadRowOrder) and range (kBadIndex).  off must be zeroed first: with
+// unsorted rows some offsets stay unwritten, and every written or zero value
+// lies in [0, nnz], so the fill that runs before the host sees `bad` only
+// reads inside the arrays.
+__device__ __forceinline__ void coo_offsets_span(int64_t k, int lo, int hi, int nrows, int* off) {
+  lo = min(max(lo, -1), nrows);
+  hi = min(max(hi, -1), nrows);
+  for (int i = lo + 1; i <= hi; ++i) off[i] = (int)k;
+}
+
+// entries taken as 16-B quads (rows 16-B aligned), two quads in flight per
+// thread; the boundary k == nnz and a ragged tail by the last thread
+__global__ void coo_offsets_check(int64_t nnz, int nrows, const int* __restrict__ r, int* off,
+                                  int* bad) {
+  int mybad = 0;
+  const int64_t nq = nnz >> 2;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  auto quad = [&](int64_t q, int4 x) {
+    const int64_t k = q * 4;
+    const int p = k > 0 ? __ldg(r + k - 1) : -1;
+    const int rr[4] = {x.x, x.y, x.z, x.w};
+    int prev = p;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if ((unsigned)rr[u] >= (unsigned)nrows) mybad |= kBadIndex;
+      if (rr[u] < prev) mybad |= kBadOrder | kBadRowOrder;
+      if (rr[u] != prev) coo_offsets_span(k + u, prev, rr[u], nrows, off);
+      prev = rr[u];
+    }
+  };
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; q + stride < nq; q += 2 * stride) {
+    const int4 x0 = ld_stream4(r + q * 4), x1 = ld_stream4(r + (q + stride) * 4);
+    quad(q, x0);
+    quad(q + stride, x1);
+  }
+  if (q < nq) quad(q, ld_stream4(r + q * 4));
+  if (blockIdx.x == 0 && threadIdx.x == 0) {   // the tail entries and the end k == nnz
+    int prev = nq * 4 > 0 ? __ldg(r + nq * 4 - 1) : -1;
+    for (int64_t k = nq * 4; k < nnz; ++k) {
+      const int x = __ldg(r + k);
+      if ((unsigned)x >= (unsigned)nrows) mybad |= kBadIndex;
+      if (x < prev) mybad |= kBadOrder | kBadRowOrder;
+      coo_offsets_span(k, prev, x, nrows, off);
+      prev = x;
+    }
+    coo_offsets_span(nnz, prev, nrows, nrows, off);
+  }
+  mybad = __reduce_or_sync(0xffffffffu, mybad);
+  if ((threadIdx.x & 31) == 0 && mybad) atomicOr(bad, mybad);
+}
+
 // ------------------------------------------------- CSR tiles with row ids --
 // Entry-parallel walks of a CSR source: a CTA takes kRT consecutive rows and
 // scatters each row's tile-local id over the tile's entries in shared memory
@@ -1983,6 +2161,30 @@ static unsigned csr_walk_grid(int64_t nrows) {   // 8 warps per block
       1, min64(ceil_div(nrows, kCsrWalkRows * 8), (int64_t)sm_count() * 8));
 }
 
+// the slot-parallel fill (dia_fill_rows) for nd <= 32; DS_DIA_FILL_ROWS=0
+// keeps the shared-memory slab walk (dia_fill_csr) for A/B runs
+static bool use_fill_rows(int64_t nd) {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("DS_DIA_FILL_ROWS");
+    on = e ? atoi(e) != 0 : 1;
+  }
+  return on && nd >= 1 && nd <= 32;
+}
+
+// entries of row r: [off[r], off[r + 1]) of (c, v); bad may be null when !CHECK
+template <bool CHECK>
+static int launch_fill_rows(int64_t nrows, int64_t ncols, int64_t nd, const int* off,
+                            const int* c, const double* v, const int* map, const int* dia_off,
+                            double* values, int* bad, cudaStream_t st) {
+  const unsigned grid = (unsigned)std::max<int64_t>(   // 8 warps per block, 32 rows per warp
+      1, min64(ceil_div(nrows, 32 * 8), (int64_t)sm_count() * 8));
+  dia_fill_rows<CHECK><<<grid, 256, 0, st>>>((int)nrows, (int)nd, off, c, v, map, dia_off, values,
+                                             (int)ncols, bad);
+  DS_LAUNCH_CHECK("dia_fill_rows");
+  return DS_OK;
+}
+
 static int begin_csr_impl(ds_convert_job* j, int64_t nnz, const int32_t* row_offsets,
                           const int32_t* cols, const double* values, int64_t fill_limit,
                           int64_t* out_nnz, int64_t* out_ndiags) {
@@ -2442,16 +2644,29 @@ static int finish_dia_impl(ds_convert_job* job, int32_t* offsets, double* values
     DS_CUDA(cudaMemcpyAsync(offsets, job->dia_off, nd * sizeof(int), cudaMemcpyDeviceToDevice,
                             st));
     const int64_t slots = nd * job->nrows;
-    if (job->spec && !job->csr_off) {   // COO: zero + checked scatter; a miss -> DS_ERR_RETRY
-      DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&job->scratch), 4, st));
-      DS_CUDA(cudaMemsetAsync(job->scratch, 0, 4, st));
+    if (job->spec && !job->csr_off) {   // COO: a miss / disorder -> DS_ERR_RETRY
+      const bool rows_fill = use_fill_rows(nd) && job->nnz < INT32_MAX &&
+                             (reinterpret_cast<uintptr_t>(job->r) & 15) == 0;
+      const size_t obytes = rows_fill ? (size_t)(job->nrows + 1) * 4 : 0;
+      DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&job->scratch), 16 + obytes, st));
+      DS_CUDA(cudaMemsetAsync(job->scratch, 0, 16 + obytes, st));
       int* bad = reinterpret_cast<int*>(job->scratch);
-      DS_CUDA(cudaMemsetAsync(values, 0, slots * sizeof(double), st));   // +0.0
-      dia_scatter<true><<<grid1d(job->nnz), 256, 0, st>>>(job->nnz, (int)job->nrows, nd, job->r,
-                                                          job->c, job->v, job->diag_map,
-                                                          job->dia_off, values, (int)job->ncols,
-                                                          bad);
-      DS_LAUNCH_CHECK("dia_scatter(check)");
+      if (rows_fill) {   // row offsets (checking the rows), then the CSR row-slot fill
+        int* roff = reinterpret_cast<int*>(job->scratch + 16);
+        coo_offsets_check<<<grid1d((job->nnz + 7) / 8), 256, 0, st>>>(job->nnz, (int)job->nrows,
+                                                                      job->r, roff, bad);
+        DS_LAUNCH_CHECK("coo_offsets_check");
+        const int rc = launch_fill_rows<true>(job->nrows, job->ncols, nd, roff, job->c,
+                                              job->v, job->diag_map, job->dia_off, values, bad, st);
+        if (rc) return rc;
+      } else {   // zero + checked scatter
+        DS_CUDA(cudaMemsetAsync(values, 0, slots * sizeof(double), st));   // +0.0
+        dia_scatter<true><<<grid1d(job->nnz), 256, 0, st>>>(job->nnz, (int)job->nrows, nd, job->r,
+                                                            job->c, job->v, job->diag_map,
+                                                            job->dia_off, values, (int)job->ncols,
+                                                            bad);
+        DS_LAUNCH_CHECK("dia_scatter(check)");
+      }
       int bad_h = 1;
       DS_CUDA(cudaMemcpyAsync(&bad_h, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
       DS_CUDA(cudaStreamSynchronize(st));
@@ -2463,17 +2678,24 @@ static int finish_dia_impl(ds_convert_job* job, int32_t* offsets, double* values
       return DS_OK;
     }
     if (job->spec) {   // one pass: order check + fill; a miss -> DS_ERR_RETRY
-      const int R = kCsrWalkRows * 8;   // 8 warps
-      const size_t smem = (size_t)R * nd * 8;
-      int rc = allow_dynamic_smem((const void*)dia_fill_csr<true>, smem);
-      if (rc) return rc;
       DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&job->scratch), 4, st));
       DS_CUDA(cudaMemsetAsync(job->scratch, 0, 4, st));
       int* bad = reinterpret_cast<int*>(job->scratch);
-      dia_fill_csr<true><<<csr_walk_grid(job->nrows), 256, smem, st>>>(
-          (int)job->nrows, (int)nd, R, job->csr_off, job->c, job->v, job->diag_map, job->dia_off,
-          values, (int)job->ncols, bad);
-      DS_LAUNCH_CHECK("dia_fill_csr(check)");
+      if (use_fill_rows(nd)) {
+        const int rc = launch_fill_rows<true>(job->nrows, job->ncols, nd, job->csr_off,
+                                              job->c, job->v, job->diag_map, job->dia_off, values,
+                                              bad, st);
+        if (rc) return rc;
+      } else {
+        const int R = kCsrWalkRows * 8;   // 8 warps
+        const size_t smem = (size_t)R * nd * 8;
+        int rc = allow_dynamic_smem((const void*)dia_fill_csr<true>, smem);
+        if (rc) return rc;
+        dia_fill_csr<true><<<csr_walk_grid(job->nrows), 256, smem, st>>>(
+            (int)job->nrows, (int)nd, R, job->csr_off, job->c, job->v, job->diag_map, job->dia_off,
+            values, (int)job->ncols, bad);
+        DS_LAUNCH_CHECK("dia_fill_csr(check)");
+      }
       int bad_h = 1;
       DS_CUDA(cudaMemcpyAsync(&bad_h, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
       DS_CUDA(cudaStreamSynchronize(st));
@@ -2518,6 +2740,10 @@ static int finish_dia_impl(ds_convert_job* job, int32_t* offsets, double* values
           (int)job->nrows, (int)nd, job->csr_off, job->c, job->v, job->diag_map, values);
       DS_LAUNCH_CHECK("csr_dia_fill_tiles");
       return DS_OK;
+    }
+    if (job->csr_off && use_fill_rows(nd)) {
+      return launch_fill_rows<false>(job->nrows, job->ncols, nd, job->csr_off, job->c,
+                                     job->v, job->diag_map, job->dia_off, values, nullptr, st);
     }
     const int R = kCsrWalkRows * 8;   // 8 warps
     if (job->csr_off && (int64_t)R * nd * 8 <= 48 * 1024) {
