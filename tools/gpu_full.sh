@@ -30,7 +30,7 @@ if [ -n "${NCU:-}" ]; then
         --clock-control none --csv --log-file $O/conv_launch_$1_$2.csv python tools/one_convert.py > /dev/null 2>&1
   done
   SRC=csr DST=dia NX=192 timeout 600 ncu --set full --clock-control none --import-source on \
-      -k regex:"dia_fill_csr" -c 1 -o $O/prof_conv_fill -f python tools/one_convert.py > /dev/null 2>&1
+      -k regex:"dia_fill_(rows|csr)" -c 1 -o $O/prof_conv_fill -f python tools/one_convert.py > /dev/null 2>&1
   SRC=dia DST=csr NX=192 timeout 600 ncu --set full --clock-control none --import-source on \
       -k regex:"dia_group" -c 2 -o $O/prof_conv_dia -f python tools/one_convert.py > /dev/null 2>&1
   PROFILE=1 FMTS=csr,coo timeout 600 ncu --set full --clock-control none --import-source on -k regex:"csr_tile_kernel|coo_warp_segments" -s 2 -c 2 \
