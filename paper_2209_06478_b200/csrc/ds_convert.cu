@@ -840,25 +840,44 @@ __global__ void __launch_bounds__(256)
       double* rowp = vals + (int64_t)r * nd;
       if (lane < nd) rowp[lane] = 0.0;
       __syncwarp();
-      for (int k = k0 + lane; k < k1; k += 32) {
-        const int ck = __ldg(c + k);
-        if (CHECK) {
+      for (int kb = k0; kb < k1; kb += 32) {   // warp-uniform trips: the search shuffles
+        const int k = kb + lane;
+        bool ok = k < k1;
+        const int ck = ok ? __ldg(c + k) : 0;
+        if (CHECK && ok) {
           if (k > k0 && __ldg(c + k - 1) >= ck) {   // not strictly increasing
             mybad |= kBadOrder;
-            continue;
-          }
-          if ((unsigned)ck >= (unsigned)ncols) {
+            ok = false;
+          } else if ((unsigned)ck >= (unsigned)ncols) {
             mybad |= kBadIndex;
-            continue;
+            ok = false;
           }
         }
-        const unsigned d = (unsigned)ck - (unsigned)r + (unsigned)(nrows - 1);
-        const int jd = __ldg(map + d);
-        if (CHECK && (d + 1 < D ? __ldg(map + d + 1) : nd) == jd) {
-          mybad |= kBadMiss;
-          continue;
+        int jd = 0;
+        if (map) {
+          if (ok) {
+            const unsigned d = (unsigned)ck - (unsigned)r + (unsigned)(nrows - 1);
+            jd = __ldg(map + d);
+            if (CHECK && (d + 1 < D ? __ldg(map + d + 1) : nd) == jd) {
+              mybad |= kBadMiss;
+              ok = false;
+            }
+          }
+        } else {   // no diag_map (the small speculative set): search the lanes' offsets
+          const int o = ck - r;
+#pragma unroll
+          for (int step = 16; step > 0; step >>= 1) {
+            const int idx = jd + step;
+            const int val = __shfl_sync(0xffffffffu, myoff, idx & 31);
+            if (idx < nd && val <= o) jd = idx;
+          }
+          const int hit = __shfl_sync(0xffffffffu, myoff, jd);
+          if (ok && hit != o) {
+            mybad |= kBadMiss;
+            ok = false;
+          }
         }
-        rowp[jd] = __ldg(v + k);
+        if (ok) rowp[jd] = __ldg(v + k);
       }
       __syncwarp();
     }
@@ -867,6 +886,44 @@ __global__ void __launch_bounds__(256)
     mybad = __reduce_or_sync(0xffffffffu, mybad);
     if (lane == 0 && mybad) atomicOr(bad, mybad);
   }
+}
+
+// The sampled census's diagonals when there are at most kSmallDiags (the
+// slot fill's case, which then needs no D-long diag_map): flag bytes read
+// 16 at a time, set ones appended to a short list; one warp sorts it.
+constexpr int kSmallDiags = 32;
+__global__ void flags_collect(int64_t D, const unsigned char* __restrict__ flags, int* list,
+                              int* count) {
+  const int64_t n16 = D >> 4;
+  const uint4* w16 = reinterpret_cast<const uint4*>(flags);
+  auto put = [&](int64_t d) {
+    const int k = atomicAdd(count, 1);
+    if (k < kSmallDiags) list[k] = (int)d;
+  };
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 w = __ldg(w16 + i);
+    if (w.x | w.y | w.z | w.w) {
+      const unsigned q[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int b = 0; b < 16; ++b)
+        if ((q[b >> 2] >> (8 * (b & 3))) & 0xffu) put(i * 16 + b);
+    }
+  }
+  if (blockIdx.x == 0)
+    for (int64_t d = n16 * 16 + threadIdx.x; d < D; d += blockDim.x)
+      if (flags[d]) put(d);
+}
+
+// one warp: offsets[rank of list[l]] = list[l] - (nrows - 1), n <= 32 distinct
+__global__ void small_diags_sort(int nrows, const int* __restrict__ list,
+                                 const int* __restrict__ count, int* offsets) {
+  const int lane = threadIdx.x;
+  const int n = min(*count, kSmallDiags);
+  const int mine = lane < n ? list[lane] : INT_MAX;
+  int rank = 0;
+  for (int l = 0; l < n; ++l) rank += __shfl_sync(0xffffffffu, mine, l) < mine;
+  if (lane < n) offsets[rank] = mine - (nrows - 1);
 }
 
 // Row offsets of a COO source for the row-slot fill (the speculative COO ->
@@ -1544,6 +1601,48 @@ static void free_job(ds_convert_job* job) {
 }
 
 // size the target; DIA: presence flags -> ndiags -> fill check before alloc
+// size_target for a speculative DIA target whose sampled set is small: the
+// offsets straight from the flags (no D-long scan / diag_map; the slot fill
+// then searches the offsets).  *small = false (flags kept) when the set has
+// more than kSmallDiags diagonals: the caller runs size_target.
+static int size_target_small(ds_convert_job* job, int64_t fill_limit, int64_t* out_ndiags,
+                             bool* small) {
+  cudaStream_t st = job->st;
+  *small = false;
+  *out_ndiags = 0;
+  const int64_t D = job->nrows + job->ncols - 1;
+  if (D <= 0 || job->nnz <= 0 || !job->flags) return DS_OK;
+  int* tmp = nullptr;   // list[kSmallDiags] | count
+  DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tmp), (kSmallDiags + 1) * sizeof(int), st));
+  DS_CUDA(cudaMemsetAsync(tmp + kSmallDiags, 0, sizeof(int), st));
+  flags_collect<<<grid1d(ceil_div(D, 16)), 256, 0, st>>>(D, job->flags, tmp, tmp + kSmallDiags);
+  DS_LAUNCH_CHECK("flags_collect");
+  int n = 0;
+  DS_CUDA(cudaMemcpyAsync(&n, tmp + kSmallDiags, sizeof(int), cudaMemcpyDeviceToHost, st));
+  DS_CUDA(cudaStreamSynchronize(st));
+  if (n < 1 || n > kSmallDiags) {
+    DS_CUDA(cudaFreeAsync(tmp, st));
+    return DS_OK;
+  }
+  DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&job->dia_off), n * sizeof(int), st));
+  small_diags_sort<<<1, 32, 0, st>>>((int)job->nrows, tmp, tmp + kSmallDiags, job->dia_off);
+  DS_LAUNCH_CHECK("small_diags_sort");
+  DS_CUDA(cudaFreeAsync(tmp, st));
+  DS_CUDA(cudaFreeAsync(job->flags, st));
+  job->flags = nullptr;
+  *small = true;
+  job->ndiags = n;
+  *out_ndiags = n;
+  const __int128 slots = (__int128)n * (__int128)job->nrows;
+  if (slots > (__int128)fill_limit) {
+    set_error("%lld diagonals x %lld rows = %lld value slots exceed the fill limit of %lld",
+              (long long)n, (long long)job->nrows, (long long)(n * job->nrows),
+              (long long)fill_limit);
+    return DS_ERR_DIA_FILL_OVERFLOW;
+  }
+  return DS_OK;
+}
+
 static int size_target(ds_convert_job* job, int64_t fill_limit, int64_t* out_nnz,
                        int64_t* out_ndiags) {
   cudaStream_t st = job->st;
@@ -2307,7 +2406,9 @@ extern "C" int ds_convert_begin_csr_dia_spec(int64_t nrows, int64_t ncols, int64
     j->v = const_cast<double*>(values);
     j->spec = true;
     int64_t nnz_out = 0;
-    rc = size_target(j, fill_limit, &nnz_out, out_ndiags);
+    bool small = false;   // the slot fill's case: no diag_map (finish_dia_impl)
+    if (use_fill_rows(kSmallDiags)) rc = size_target_small(j, fill_limit, out_ndiags, &small);
+    if (rc == DS_OK && !small) rc = size_target(j, fill_limit, &nnz_out, out_ndiags);
     if (rc == DS_ERR_DIA_FILL_OVERFLOW) rc = DS_ERR_RETRY;
     // the fill keeps a 128-row slab in shared memory
     if (rc == DS_OK && (*out_ndiags < 1 || *out_ndiags * kCsrWalkRows * 8 * 8 > 160 * 1024))
@@ -2361,7 +2462,10 @@ extern "C" int ds_convert_begin_coo_dia_spec(int64_t nrows, int64_t ncols, int64
     j->v = const_cast<double*>(values);
     j->spec = true;
     int64_t nnz_out = 0;
-    rc = size_target(j, fill_limit, &nnz_out, out_ndiags);
+    bool small = false;   // the slot fill's case: no diag_map (finish_dia_impl)
+    if (use_fill_rows(kSmallDiags) && nnz < INT32_MAX && (reinterpret_cast<uintptr_t>(rows) & 15) == 0)
+      rc = size_target_small(j, fill_limit, out_ndiags, &small);
+    if (rc == DS_OK && !small) rc = size_target(j, fill_limit, &nnz_out, out_ndiags);
     if (rc == DS_ERR_DIA_FILL_OVERFLOW) rc = DS_ERR_RETRY;
     if (rc == DS_OK && *out_ndiags < 1) rc = DS_ERR_RETRY;
   } while (false);
