@@ -446,14 +446,40 @@ struct ArrayAt {
 // group of them counts the nonzero values of its contiguous slot range with
 // 16-B loads and no per-slot offset lookup (the caller passes an empty range
 // when the values are not 16-B aligned or `present` is wanted).
-template <bool INTERIOR>
+// SELECT (DIA -> DIA, nd <= 32): the census as one global bit mask and the
+// nonzero count as one global sum (separate 128-B lines), and every warp
+// stops once the answer is settled -- every diagonal present and at least
+// `need` nonzeros counted (the default fill limit's test; 0 with an
+// explicit limit).  The stencil settles after ~10% of the slab; a matrix
+// with an empty diagonal is read to the end, as before.
+struct DiaSelect {
+  unsigned* mask;
+  unsigned long long* count;
+  unsigned long long need;
+  unsigned full;
+};
+
+template <bool INTERIOR, bool SELECT = false>
 __global__ void dia_group_counts(int64_t nrows, int ncols, int nd, const int* __restrict__ off,
                                  const double* __restrict__ vals, int64_t ngroups, int* gcount,
-                                 unsigned char* present, int64_t in_lo, int64_t in_hi) {
+                                 unsigned char* present, int64_t in_lo, int64_t in_hi,
+                                 DiaSelect sel = DiaSelect{}) {
   const DiaSlots s(ncols, nd, off, vals);
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < ngroups; g += nwarps) {
+  int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  unsigned seen = 0;   // SELECT, lane 0: the global mask as last read
+  for (; g < ngroups; g += nwarps) {
+    if (SELECT) {   // the warps advance together, so the static order is ~ascending
+      int stop = 0;
+      if (lane == 0) {
+        unsigned long long n;
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(sel.mask) : "memory");
+        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(n) : "l"(sel.count) : "memory");
+        stop = seen == sel.full && n >= sel.need;
+      }
+      if (__shfl_sync(0xffffffffu, stop, 0)) break;
+    }
     const int64_t r0 = g * kDiaGroupRows;
     const int64_t r1 = r0 + kDiaGroupRows < nrows ? r0 + kDiaGroupRows : nrows;
     if (INTERIOR && r0 >= in_lo && r1 <= in_hi) {
@@ -464,8 +490,8 @@ __global__ void dia_group_counts(int64_t nrows, int ncols, int nd, const int* __
       // present (DIA target, nd <= 32): lane bit j = a nonzero on diagonal j;
       // a lane's slots advance by 64 per step, so its diagonal advances by 64 % nd
       unsigned mask = 0;
-      int j0 = present ? (2 * lane) % nd : 0;
-      const int rm = present ? 64 % nd : 0;
+      int j0 = (SELECT || present) ? (2 * lane) % nd : 0;
+      const int rm = (SELECT || present) ? 64 % nd : 0;
       for (int t0 = 0; t0 < n2; t0 += 32 * kDiaChunks) {
         double2 x[kDiaChunks];
 #pragma unroll
@@ -476,7 +502,7 @@ __global__ void dia_group_counts(int64_t nrows, int ncols, int nd, const int* __
 #pragma unroll
         for (int u = 0; u < kDiaChunks; ++u) {
           cnt += (x[u].x != 0.0) + (x[u].y != 0.0);
-          if (present) {
+          if (SELECT || present) {
             const int j1 = j0 + 1 == nd ? 0 : j0 + 1;
             mask |= ((unsigned)(x[u].x != 0.0) << j0) | ((unsigned)(x[u].y != 0.0) << j1);
             j0 += rm;
@@ -490,6 +516,14 @@ __global__ void dia_group_counts(int64_t nrows, int ncols, int nd, const int* __
         mask |= (unsigned)nz << (nd - 1);
       }
       cnt = __reduce_add_sync(0xffffffffu, cnt);
+      if (SELECT) {
+        mask = __reduce_or_sync(0xffffffffu, mask);
+        if (lane == 0) {
+          atomicAdd(sel.count, (unsigned long long)cnt);
+          if ((mask | seen) != seen) atomicOr(sel.mask, mask);
+        }
+        continue;
+      }
       if (lane == 0) gcount[g] = cnt;
       if (present) {
         mask = __reduce_or_sync(0xffffffffu, mask);
@@ -502,14 +536,27 @@ __global__ void dia_group_counts(int64_t nrows, int ncols, int nd, const int* __
       continue;
     }
     int cnt = 0;
+    unsigned smask = 0;
     s.walk(r0, r0 * nd, r1 * nd, [&](bool valid, bool, int64_t, int j, int, double) {
       cnt += __popc(__ballot_sync(0xffffffffu, valid));
+      if (SELECT) {
+        if (valid) smask |= 1u << j;
+        return;
+      }
       if (present && valid) {
         unsigned short f;
         asm volatile("ld.global.ca.u8 %0, [%1];" : "=h"(f) : "l"(present + j));
         if (f == 0) present[j] = 1;
       }
     });
+    if (SELECT) {
+      smask = __reduce_or_sync(0xffffffffu, smask);
+      if (lane == 0) {
+        atomicAdd(sel.count, (unsigned long long)cnt);
+        if ((smask | seen) != seen) atomicOr(sel.mask, smask);
+      }
+      continue;
+    }
     if ((threadIdx.x & 31) == 0) gcount[g] = cnt;
   }
 }
@@ -2571,7 +2618,7 @@ static int begin_dia_impl(ds_convert_job* j, int32_t ndiags, const int32_t* offs
     bool ascending = true;
     for (int q = 1; q < ndiags; ++q) ascending = ascending && h_off[q - 1] < h_off[q];
     const bool select = target == DS_FMT_DIA && ascending;   // DIA -> DIA: a column selection
-    if (select) {   // census of the source diagonals holding an entry
+    if (select && ndiags > 32) {   // census of the source diagonals holding an entry
       DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&j->scratch), ndiags, st));
       DS_CUDA(cudaMemsetAsync(j->scratch, 0, ndiags, st));
     }
@@ -2583,15 +2630,47 @@ static int begin_dia_impl(ds_convert_job* j, int32_t ndiags, const int32_t* offs
       in_lo = std::max<int64_t>(0, -omin);
       in_hi = std::min<int64_t>(nrows, ncols - omax);
     }
-    if (in_hi > in_lo)
-      dia_group_counts<true><<<dia_walk_grid(ngroups), 256, 0, st>>>(
-          nrows, (int)ncols, ndiags, offsets, values, ngroups, j->gtmp, j->scratch, in_lo, in_hi);
-    else
-      dia_group_counts<false><<<dia_walk_grid(ngroups), 256, 0, st>>>(
-          nrows, (int)ncols, ndiags, offsets, values, ngroups, j->gtmp, j->scratch, 0, 0);
-    DS_LAUNCH_CHECK("dia_group_counts");
-    int rc = exclusive_scan(ngroups, ArrayAt{j->gtmp}, j->dsrc_start, &nc, st);
-    if (rc) return rc;
+    // DIA -> DIA with <= 32 diagonals: the census alone, stopping once settled
+    const bool settle = select && ndiags <= 32;
+    std::vector<unsigned char> h_present(ndiags);
+    if (settle) {
+      unsigned char* sc = nullptr;   // mask | count, a 128-B line each
+      DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&sc), 256, st));
+      DS_CUDA(cudaMemsetAsync(sc, 0, 256, st));
+      DiaSelect sel;
+      sel.mask = reinterpret_cast<unsigned*>(sc);
+      sel.count = reinterpret_cast<unsigned long long*>(sc + 128);
+      sel.full = ndiags == 32 ? ~0u : (1u << ndiags) - 1u;
+      // the default limit passes once 10 * nnz >= ndiags * nrows (all present)
+      sel.need = (fill_limit == kDefaultFillLimit && ndiags > 10)
+                     ? (unsigned long long)ceil_div((int64_t)ndiags * nrows, 10)
+                     : 0ull;
+      if (in_hi > in_lo)
+        dia_group_counts<true, true><<<dia_walk_grid(ngroups), 256, 0, st>>>(
+            nrows, (int)ncols, ndiags, offsets, values, ngroups, nullptr, nullptr, in_lo, in_hi,
+            sel);
+      else
+        dia_group_counts<false, true><<<dia_walk_grid(ngroups), 256, 0, st>>>(
+            nrows, (int)ncols, ndiags, offsets, values, ngroups, nullptr, nullptr, 0, 0, sel);
+      DS_LAUNCH_CHECK("dia_group_counts(select)");
+      unsigned long long h[32] = {};
+      DS_CUDA(cudaMemcpyAsync(h, sc, 256, cudaMemcpyDeviceToHost, st));
+      DS_CUDA(cudaStreamSynchronize(st));
+      DS_CUDA(cudaFreeAsync(sc, st));
+      const unsigned m = (unsigned)h[0];
+      for (int q = 0; q < ndiags; ++q) h_present[q] = (m >> q) & 1u;
+      nc = (int64_t)h[16];   // exact unless the walk stopped early (then >= need)
+    } else {
+      if (in_hi > in_lo)
+        dia_group_counts<true><<<dia_walk_grid(ngroups), 256, 0, st>>>(
+            nrows, (int)ncols, ndiags, offsets, values, ngroups, j->gtmp, j->scratch, in_lo, in_hi);
+      else
+        dia_group_counts<false><<<dia_walk_grid(ngroups), 256, 0, st>>>(
+            nrows, (int)ncols, ndiags, offsets, values, ngroups, j->gtmp, j->scratch, 0, 0);
+      DS_LAUNCH_CHECK("dia_group_counts");
+      int rc = exclusive_scan(ngroups, ArrayAt{j->gtmp}, j->dsrc_start, &nc, st);
+      if (rc) return rc;
+    }
     DS_CUDA(cudaFreeAsync(j->gtmp, st));
     j->gtmp = nullptr;
     j->dsrc_off = offsets;
@@ -2599,11 +2678,13 @@ static int begin_dia_impl(ds_convert_job* j, int32_t ndiags, const int32_t* offs
     j->dsrc_nd = ndiags;
     j->dsrc_in_lo = in_lo;
     j->dsrc_in_hi = in_hi;
+    int rc = DS_OK;
     if (select) {
-      std::vector<unsigned char> h_present(ndiags);
-      DS_CUDA(cudaMemcpyAsync(h_present.data(), j->scratch, ndiags, cudaMemcpyDeviceToHost, st));
-      DS_CUDA(cudaStreamSynchronize(st));
-      DS_CUDA(cudaFreeAsync(j->scratch, st));
+      if (!settle) {
+        DS_CUDA(cudaMemcpyAsync(h_present.data(), j->scratch, ndiags, cudaMemcpyDeviceToHost, st));
+        DS_CUDA(cudaStreamSynchronize(st));
+      }
+      if (j->scratch) DS_CUDA(cudaFreeAsync(j->scratch, st));
       j->scratch = nullptr;
       DS_CUDA(cudaFreeAsync(j->dsrc_start, st));
       j->dsrc_start = nullptr;
