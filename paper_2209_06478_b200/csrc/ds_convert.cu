@@ -801,8 +801,9 @@ __global__ void dia_fill_csr(int nrows, int nd, int R, const int* __restrict__ o
 // dia_off[j], in range -- which also proves the row strictly increasing).
 // Rows that are not full -- and every row of a chunk where a compare failed
 // -- are then rewritten one at a time by the warp: zeroed, and their entries
-// scattered through diag_map with dia_fill_csr<CHECK>'s checks (order,
-// column range, membership; an out-of-order entry is not stored).
+// scattered through diag_map (or, without one, a 5-step shuffle search of
+// the lanes' offsets) with dia_fill_csr<CHECK>'s checks (order, column
+// range, membership; an out-of-order entry is not stored).
 // Measured (tools/gpu_fillab.sh, same box, 192^3 wall): CSR -> DIA 1.04 ms
 // (the slab walk, DS_DIA_FILL_ROWS=0) -> 0.93 ms, COO -> DIA 1.62 -> 1.28 ms
 // (with coo_offsets_check).  Slots per lane 6 (64 registers); 8: 1.07 ms,
