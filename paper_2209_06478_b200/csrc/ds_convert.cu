@@ -988,6 +988,10 @@ __device__ __forceinline__ void coo_offsets_span(int64_t k, int lo, int hi, int 
 
 // entries taken as 16-B quads (rows 16-B aligned), two quads in flight per
 // thread; the boundary k == nnz and a ragged tail by the last thread
+// (Rejected, 192^3: 4 quads per thread with the previous row from a shuffle,
+// 360 us; the same plus a compare-only path for quads without a row change,
+// 366 us -- against this kernel's 343 us; ncu: 884 MB read for 757 MB, L2
+// hit rate 26%, sm__throughput 76%.)
 __global__ void coo_offsets_check(int64_t nnz, int nrows, const int* __restrict__ r, int* off,
                                   int* bad) {
   int mybad = 0;
