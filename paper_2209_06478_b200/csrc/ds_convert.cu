@@ -808,7 +808,8 @@ __global__ void dia_fill_csr(int nrows, int nd, int R, const int* __restrict__ o
 // (the slab walk, DS_DIA_FILL_ROWS=0) -> 0.93 ms, COO -> DIA 1.62 -> 1.28 ms
 // (with coo_offsets_check).  Slots per lane 6 (64 registers); 8: 1.07 ms,
 // 12: 1.39, 16: 1.22; a bulk L2 prefetch of the next chunk's entries: 1.19
-// vs 0.98.  Rejected: a warp per row (~57 warp instructions per row, 852 us
+// vs 0.98; the slot state recomputed in the store loop instead of kept per
+// slot (6 / 8 / 10 slots): 0.98 / 1.04 / 0.95.  Rejected: a warp per row (~57 warp instructions per row, 852 us
 // cold for the fill kernel, the same as the slab walk) and the same walk
 // TMA-staged at 1 CTA/SM (1.49 ms, issue-latency bound).
 #ifndef DS_FILL_SLOTS_U
