@@ -1665,8 +1665,9 @@ static int size_target_small(ds_convert_job* job, int64_t fill_limit, int64_t* o
   *out_ndiags = 0;
   const int64_t D = job->nrows + job->ncols - 1;
   if (D <= 0 || job->nnz <= 0 || !job->flags) return DS_OK;
-  int* tmp = nullptr;   // list[kSmallDiags] | count
+  int* tmp = nullptr;   // list[kSmallDiags] | count; on the job until freed (free_job on errors)
   DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tmp), (kSmallDiags + 1) * sizeof(int), st));
+  job->scratch = reinterpret_cast<unsigned char*>(tmp);
   DS_CUDA(cudaMemsetAsync(tmp + kSmallDiags, 0, sizeof(int), st));
   flags_collect<<<grid1d(ceil_div(D, 16)), 256, 0, st>>>(D, job->flags, tmp, tmp + kSmallDiags);
   DS_LAUNCH_CHECK("flags_collect");
@@ -1674,12 +1675,14 @@ static int size_target_small(ds_convert_job* job, int64_t fill_limit, int64_t* o
   DS_CUDA(cudaMemcpyAsync(&n, tmp + kSmallDiags, sizeof(int), cudaMemcpyDeviceToHost, st));
   DS_CUDA(cudaStreamSynchronize(st));
   if (n < 1 || n > kSmallDiags) {
+    job->scratch = nullptr;
     DS_CUDA(cudaFreeAsync(tmp, st));
     return DS_OK;
   }
   DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&job->dia_off), n * sizeof(int), st));
   small_diags_sort<<<1, 32, 0, st>>>((int)job->nrows, tmp, tmp + kSmallDiags, job->dia_off);
   DS_LAUNCH_CHECK("small_diags_sort");
+  job->scratch = nullptr;
   DS_CUDA(cudaFreeAsync(tmp, st));
   DS_CUDA(cudaFreeAsync(job->flags, st));
   job->flags = nullptr;
@@ -2640,8 +2643,9 @@ static int begin_dia_impl(ds_convert_job* j, int32_t ndiags, const int32_t* offs
     const bool settle = select && ndiags <= 32;
     std::vector<unsigned char> h_present(ndiags);
     if (settle) {
-      unsigned char* sc = nullptr;   // mask | count, a 128-B line each
+      unsigned char* sc = nullptr;   // mask | count, a 128-B line each (freed with the job)
       DS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&sc), 256, st));
+      j->scratch = sc;
       DS_CUDA(cudaMemsetAsync(sc, 0, 256, st));
       DiaSelect sel;
       sel.mask = reinterpret_cast<unsigned*>(sc);
@@ -2662,7 +2666,6 @@ static int begin_dia_impl(ds_convert_job* j, int32_t ndiags, const int32_t* offs
       unsigned long long h[32] = {};
       DS_CUDA(cudaMemcpyAsync(h, sc, 256, cudaMemcpyDeviceToHost, st));
       DS_CUDA(cudaStreamSynchronize(st));
-      DS_CUDA(cudaFreeAsync(sc, st));
       const unsigned m = (unsigned)h[0];
       for (int q = 0; q < ndiags; ++q) h_present[q] = (m >> q) & 1u;
       nc = (int64_t)h[16];   // exact unless the walk stopped early (then >= need)
